@@ -1,0 +1,395 @@
+"""Pins of the fp64 oracle against things other than itself (SURVEY §8(c).4, C1–C13).
+
+Independent references used here:
+  * HuggingFace ``transformers`` LlamaForCausalLM in float64 (a library implementation of
+    the Llama decoder: RMSNorm, rotate-half RoPE, GQA, SwiGLU, causal softmax attention)
+    loaded with the oracle's weights — pins the decoder, full prefill, and (through its
+    KV-cache API) the Naive construction C6;
+  * scipy.special.softmax brute force per query (C1);
+  * complex-number RoPE (C7, C12);
+  * torch's bfloat16 conversion (generator rounding), published SplitMix64 outputs;
+  * closed-form plan arithmetic printed in SPEC/SURVEY (C10) and causality identities
+    (C3, C4, C8, C9, C11).
+"""
+import numpy as np
+import pytest
+import scipy.special
+
+import seedgen as sg
+from oracle import model as M
+from oracle import pic as P
+
+
+def rel(a, b):
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+# ----------------------------------------------------------------------------
+# generator pins
+# ----------------------------------------------------------------------------
+def test_splitmix64_published_vectors():
+    # SplitMix64 seeded with 0 (Steele/Lea/Flood; Vigna's reference C): the first outputs.
+    outs, state = [], 0
+    for _ in range(3):
+        outs.append(sg.sm64_int(state))
+        state = (state + sg.GOLDEN) & sg.M64
+    assert outs == [0xE220A8397B1DCDAF, 0x6E789E6AA1B965F4, 0x06C45D188009454F]
+    # the numpy path agrees with the integer path
+    x = np.arange(1000, dtype=np.uint64) * np.uint64(0x123456789)
+    assert all(int(a) == sg.sm64_int(int(b)) for a, b in zip(sg._sm64_np(x), x))
+
+
+def test_bf16_rounding_matches_torch():
+    torch = pytest.importorskip("torch")
+    rng = np.random.default_rng(0)
+    x = np.concatenate([rng.standard_normal(100000).astype(np.float32),
+                        sg.uniform_pm1(sg.U(1, 2, np.arange(100000, dtype=np.uint64)))])
+    ref = torch.from_numpy(x).to(torch.bfloat16).to(torch.float32).numpy()
+    assert np.array_equal(sg.bf16_rne(x), ref)
+
+
+def test_uniform_exact_and_range():
+    u = sg.U(7, 3, np.arange(1 << 16, dtype=np.uint64))
+    f = sg.uniform_pm1(u)
+    assert f.min() >= -1.0 and f.max() < 1.0
+    # exactness: float64 evaluation gives the same numbers
+    f64 = (u >> np.uint64(40)).astype(np.float64) * 2.0 ** -23 - 1.0
+    assert np.array_equal(f.astype(np.float64), f64)
+    w = sg.matrix(5, 9, 64, 4096)
+    assert np.array_equal(w, sg.bf16_rne(w))                      # bf16-exact
+    assert abs(np.var(w) * 4096 - 1.0) < 0.5                      # variance ≈ 1/fan_in
+
+
+# ----------------------------------------------------------------------------
+# decoder pinned against HuggingFace Llama (float64)
+# ----------------------------------------------------------------------------
+HF_TOL = 2e-6   # float32 internals of HF's RMSNorm / softmax (see hf_model)
+
+
+def test_rms_norm_matches_torch_and_silu():
+    torch = pytest.importorskip("torch")
+    rng = np.random.default_rng(9)
+    x = rng.standard_normal((7, 64)) * 3
+    g = rng.standard_normal(64)
+    ref = torch.nn.functional.rms_norm(torch.from_numpy(x), (64,), torch.from_numpy(g), eps=1e-5).numpy()
+    assert np.abs(M.rms_norm(x, g, 1e-5) - ref).max() < 1e-14
+    ref = torch.nn.functional.silu(torch.from_numpy(x)).numpy()
+    assert np.abs(M.silu(x) - ref).max() < 1e-14
+
+
+def hf_model(cfg: sg.ModelConfig, Wt: M.Weights):
+    torch = pytest.importorskip("torch")
+    tf = pytest.importorskip("transformers")
+    c = tf.LlamaConfig(vocab_size=cfg.vocab, hidden_size=cfg.d_model, intermediate_size=cfg.ffn_dim,
+                       num_hidden_layers=cfg.n_layers, num_attention_heads=cfg.n_heads,
+                       num_key_value_heads=cfg.n_kv_heads, head_dim=cfg.head_dim, rms_norm_eps=cfg.rms_eps,
+                       rope_theta=cfg.rope_theta, tie_word_embeddings=False, attention_bias=False,
+                       mlp_bias=False, max_position_embeddings=cfg.max_pos)
+    c._attn_implementation = "eager"
+    m = tf.LlamaForCausalLM(c).double().eval()
+    # HF evaluates RoPE angles, RMSNorm and the softmax in float32 even for a float64
+    # model.  The angles are re-evaluated in float64 here (θ^(−2j/D)·p, pinned again by
+    # the complex-rotation test); the float32 norm/softmax bound the comparison to
+    # HF_TOL.  RMSNorm and softmax are pinned separately at 1e-14 against
+    # torch.nn.functional.rms_norm and scipy.
+    rot = m.model.rotary_emb
+
+    def rot_forward(x, position_ids):
+        j = torch.arange(0, cfg.head_dim, 2, dtype=torch.float64)
+        inv = cfg.rope_theta ** (-j / cfg.head_dim)
+        fr = position_ids.to(torch.float64)[..., None] * inv
+        emb = torch.cat([fr, fr], dim=-1)
+        return emb.cos().to(x.dtype), emb.sin().to(x.dtype)
+
+    rot.forward = rot_forward
+    T = lambda a: torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64))
+    with torch.no_grad():
+        m.model.embed_tokens.weight.copy_(T(Wt.embed))
+        m.lm_head.weight.copy_(T(Wt.lm_head))
+        m.model.norm.weight.copy_(T(Wt.g_final))
+        for l, layer in enumerate(m.model.layers):
+            W = Wt.layer(l)
+            layer.self_attn.q_proj.weight.copy_(T(W["q"]))
+            layer.self_attn.k_proj.weight.copy_(T(W["k"]))
+            layer.self_attn.v_proj.weight.copy_(T(W["v"]))
+            layer.self_attn.o_proj.weight.copy_(T(W["o"]))
+            layer.mlp.gate_proj.weight.copy_(T(W["gate"]))
+            layer.mlp.up_proj.weight.copy_(T(W["up"]))
+            layer.mlp.down_proj.weight.copy_(T(W["down"]))
+            layer.input_layernorm.weight.copy_(T(W["g1"]))
+            layer.post_attention_layernorm.weight.copy_(T(W["g2"]))
+    return m
+
+
+@pytest.mark.parametrize("cfg", [sg.TINY, sg.TINY_GQA, sg.TINY_D128], ids=lambda c: c.name)
+def test_full_prefill_matches_hf_llama(cfg):
+    torch = pytest.importorskip("torch")
+    Wt = M.Weights(cfg)
+    w = sg.cfg1(model=cfg)
+    tok = np.concatenate([w.chunks[0], w.requests[0][-1].tokens])
+    logits, K, V, _ = M.full_prefill(Wt, tok)
+    m = hf_model(cfg, Wt)
+    with torch.no_grad():
+        out = m(torch.from_numpy(tok.astype(np.int64))[None], use_cache=True)
+    assert rel(logits, out.logits[0, -1].numpy()) < HF_TOL
+    # cached keys/values of HF are post-RoPE [B, H_kv, T, D]
+    kv = out.past_key_values
+    for l in range(cfg.n_layers):
+        k_hf = kv.layers[l].keys[0].numpy().transpose(1, 0, 2)
+        v_hf = kv.layers[l].values[0].numpy().transpose(1, 0, 2)
+        assert rel(K[l], k_hf) < HF_TOL
+        assert rel(V[l], v_hf) < HF_TOL
+
+
+# ----------------------------------------------------------------------------
+# C1 / C2: attention
+# ----------------------------------------------------------------------------
+def test_C1_attention_brute_force():
+    rng = np.random.default_rng(1)
+    n, Hq, Hkv, D = 9, 4, 2, 8
+    q = rng.standard_normal((n, Hq, D))
+    k = rng.standard_normal((n, Hkv, D))
+    v = rng.standard_normal((n, Hkv, D))
+    pos = np.arange(n)
+    out = M.causal_attention(q, k, v, pos)
+    for h in range(Hq):
+        g = h // (Hq // Hkv)
+        for i in range(n):
+            s = np.array([q[i, h] @ k[j, g] / np.sqrt(D) for j in range(i + 1)])
+            p = scipy.special.softmax(s)
+            ref = sum(p[j] * v[j, g] for j in range(i + 1))
+            assert np.allclose(out[i, h], ref, atol=1e-12, rtol=0)
+        A = M.attention_matrix_dense(q[:, h], k[:, g])
+        assert np.allclose(A.sum(1), 1.0, atol=1e-12)
+        assert np.all(A[np.triu_indices(n, 1)] == 0.0)
+    # closed forms: zero query → uniform average of visible values; first row → v[0]
+    out0 = M.causal_attention(np.zeros_like(q), k, v, pos)
+    for i in range(n):
+        assert np.allclose(out0[i, 0], v[: i + 1, 0].mean(0), atol=1e-12)
+    assert np.allclose(out[0, :, :], v[0, np.arange(Hq) // 2], atol=1e-12)
+
+
+def test_C2_sparse_query_rows_equal_dense_rows():
+    rng = np.random.default_rng(2)
+    n, H, D = 40, 2, 8
+    q = rng.standard_normal((n, H, D))
+    k = rng.standard_normal((n, H, D))
+    v = rng.standard_normal((n, H, D))
+    dense = M.causal_attention(q, k, v, np.arange(n))
+    sel = np.array([3, 7, 8, 20, 39])
+    sparse = M.causal_attention(q[sel], k, v, sel)
+    assert np.abs(sparse - dense[sel]).max() <= 1e-12
+
+
+# ----------------------------------------------------------------------------
+# RoPE pins (C7, C12)
+# ----------------------------------------------------------------------------
+def complex_rope(x, pos, theta):
+    D = x.shape[-1]
+    h = D // 2
+    z = x[..., :h] + 1j * x[..., h:]
+    ang = np.outer(pos, theta ** (-np.arange(h) * 2.0 / D))
+    z = z * np.exp(1j * ang)[:, None, :]
+    return np.concatenate([z.real, z.imag], axis=-1)
+
+
+def test_rope_matches_complex_rotation_and_preserves_norm():
+    rng = np.random.default_rng(3)
+    x = rng.standard_normal((50, 3, 128))
+    pos = rng.integers(0, 32832, 50)
+    y = M.rope(x, pos, 5e5)
+    assert np.abs(y - complex_rope(x, pos, 5e5)).max() < 1e-12
+    n1 = x[..., :64] ** 2 + x[..., 64:] ** 2
+    n2 = y[..., :64] ** 2 + y[..., 64:] ** 2
+    assert np.abs(n1 - n2).max() < 1e-12                         # C12 pair norms
+
+
+def test_C7_rebase_identity():
+    rng = np.random.default_rng(4)
+    k = rng.standard_normal((16, 2, 128))
+    p = np.arange(16)
+    for delta in (0, 1, 512, 31232):
+        lhs = P.rebase(M.rope(k, p, 1e4), delta, 128, 1e4)
+        rhs = M.rope(k, p + delta, 1e4)
+        assert np.abs(lhs - rhs).max() < 1e-10
+    assert np.array_equal(P.rebase(k, 0, 128, 1e4), k)            # Δ = 0 is exact
+
+
+# ----------------------------------------------------------------------------
+# link pins on cfg1
+# ----------------------------------------------------------------------------
+@pytest.fixture(scope="module", params=[sg.TINY, sg.TINY_GQA], ids=lambda c: c.name)
+def tiny(request):
+    cfg = request.param
+    w = sg.cfg1(model=cfg)
+    Wt = M.Weights(cfg)
+    store = P.Store(Wt)
+    ids = store.compile(w.chunks)
+    segs = [("cached", ids[0]), ("cached", ids[1]), ("cached", ids[2]), ("tokens", w.requests[0][-1].tokens)]
+    tok = np.concatenate(w.chunks + [w.requests[0][-1].tokens])
+    ref = M.full_prefill(Wt, tok)
+    return cfg, w, Wt, store, ids, segs, tok, ref
+
+
+def test_C3_fr_equals_full_prefill(tiny):
+    cfg, w, Wt, store, ids, segs, tok, (logits, K, V, _) = tiny
+    r = P.link(store, segs, "fr")
+    assert rel(r.logits, logits) < 1e-12
+    assert rel(r.K, K) < 1e-12 and rel(r.V, V) < 1e-12
+    assert len(r.plan.sel) == 112
+
+
+def test_C4_saturated_legolink_equals_fr(tiny):
+    cfg, w, Wt, store, ids, segs, tok, (logits, K, V, _) = tiny
+    r = P.link(store, segs, "legolink:32")
+    assert len(r.plan.sel) == 112 - 32                           # index-0 chunk exempt
+    assert rel(r.logits, logits) < 1e-12
+    assert rel(r.K, K) < 1e-12 and rel(r.V, V) < 1e-12
+    r2 = P.link(store, segs, "legolink:1000")
+    assert rel(r2.logits, logits) < 1e-12
+
+
+def test_C5_legolink0_equals_naive(tiny):
+    cfg, w, Wt, store, ids, segs, *_ = tiny
+    a = P.link(store, segs, "legolink:0")
+    b = P.link(store, segs, "naive")
+    assert np.array_equal(a.plan.sel, b.plan.sel)
+    assert np.array_equal(a.logits, b.logits)
+
+
+def test_C6_naive_equals_hf_prefill_over_rebased_prefix(tiny):
+    """Independent construction: HF Llama's KV cache filled with the re-based chunk KV
+    (the 'prefix'), then an ordinary HF forward of only the dynamic tokens."""
+    torch = pytest.importorskip("torch")
+    tf = pytest.importorskip("transformers")
+    cfg, w, Wt, store, ids, segs, tok, _ = tiny
+    r = P.link(store, segs, "naive")
+    m = hf_model(cfg, Wt)
+    cache = tf.DynamicCache(config=m.config)
+    n_pre = 96
+    for l in range(cfg.n_layers):
+        ks, vs = [], []
+        for c, cid in enumerate(ids):
+            ch = store.chunks[cid]
+            ks.append(P.rebase(ch.K[l], 32 * c, cfg.head_dim, cfg.rope_theta))
+            vs.append(ch.V[l])
+        k = torch.from_numpy(np.concatenate(ks).transpose(1, 0, 2)[None].copy())
+        v = torch.from_numpy(np.concatenate(vs).transpose(1, 0, 2)[None].copy())
+        cache.update(k, v, l)
+    q = w.requests[0][-1].tokens.astype(np.int64)
+    with torch.no_grad():
+        out = m(torch.from_numpy(q)[None], past_key_values=cache, use_cache=True,
+                position_ids=torch.arange(n_pre, n_pre + len(q))[None])
+    assert rel(r.logits, out.logits[0, -1].numpy()) < HF_TOL
+    for l in range(cfg.n_layers):
+        k_hf = out.past_key_values.layers[l].keys[0].numpy().transpose(1, 0, 2)
+        assert rel(r.K[l], k_hf) < HF_TOL
+
+
+def test_C8_layer0_kv_equals_prefill_for_every_algorithm(tiny):
+    cfg, w, Wt, store, ids, segs, tok, (logits, K, V, _) = tiny
+    for alg in ("naive", "legolink:4", "cacheblend:15", "fr"):
+        r = P.link(store, segs, alg)
+        assert rel(r.K[0], K[0]) < 1e-12, alg
+        assert rel(r.V[0], V[0]) < 1e-12, alg
+
+
+def test_C9_prefix_equivalence(tiny):
+    cfg, w, Wt, store, ids, segs, tok, _ = tiny
+    q = w.requests[0][-1].tokens
+    logits, K, V, _ = M.full_prefill(Wt, np.concatenate([w.chunks[1], q]))
+    for alg in ("naive", "legolink:4", "cacheblend:15", "fr"):
+        r = P.link(store, [("cached", ids[1]), ("tokens", q)], alg)
+        assert rel(r.logits, logits) < 1e-12, alg
+        assert rel(r.K, K) < 1e-12, alg
+
+
+def test_C10_plan_arithmetic():
+    cfg = sg.TINY
+    Wt = M.Weights(cfg)
+    store = P.Store(Wt)
+    w = sg.cfg1()
+    # planning needs only the store's token lists: use zero KV placeholders
+    ids = store.compile(w.chunks, compiled_override=[(None, None)] * 3)
+    q = w.requests[0][-1].tokens
+    segs = [("cached", i) for i in ids] + [("tokens", q)]
+    pl = P.plan(store, segs, "legolink:4")
+    assert pl.sel.tolist() == list(range(32, 36)) + list(range(64, 68)) + list(range(96, 112))
+    assert len(P.plan(store, segs, "fr").sel) == 112
+    assert P.plan(store, segs, "naive").sel.tolist() == list(range(96, 112))
+    # SPEC S:326 example: 3 chunks × 48 + 16-token query, LegoLink-16
+    ids48 = store.compile([np.arange(48, dtype=np.int32) + 2] * 3, compiled_override=[(None, None)] * 3)
+    segs48 = [("cached", i) for i in ids48] + [("tokens", np.arange(16, dtype=np.int32) + 5)]
+    pl = P.plan(store, segs48, "legolink:16")
+    assert pl.sel.tolist() == list(range(48, 64)) + list(range(96, 112)) + list(range(144, 160))
+    # CacheBlend-15 on that layout: 160 rows at layer 0, then 16 + ⌈0.15·144⌉ = 38
+    cb = P.plan(store, segs48, "cacheblend:15")
+    assert P.cacheblend_count(cb) == 22
+    dev = np.arange(160, dtype=np.float64)
+    sel = P.cacheblend_select(cb, dev)
+    assert len(sel) == 38 and sel[-1] == 159
+    # cfg1 CB-15: 112 → 15 + 16 = 31; cfg3 CB-15 (no dynamic): 5120 → 768 + forced last = 769
+    cb1 = P.plan(store, segs, "cacheblend:15")
+    assert len(P.cacheblend_select(cb1, np.zeros(112))) == 31
+    # dynamic-first order: no chunk is exempt
+    pl = P.plan(store, [("tokens", q)] + [("cached", i) for i in ids], "legolink:4")
+    assert pl.sel.tolist() == list(range(16)) + [16, 17, 18, 19, 48, 49, 50, 51, 80, 81, 82, 83] + [111]
+    # chunk deltas
+    assert [c[3] for c in pl.chunks] == [16, 48, 80]
+    # ties → lower index
+    dev = np.zeros(160)
+    assert P.cacheblend_select(cb, dev)[:22].tolist() == list(range(22))
+
+
+def test_C11_cacheblend_index0_deviation_zero_and_count(tiny):
+    cfg, w, Wt, store, ids, segs, *_ = tiny
+    r = P.link(store, segs, "cacheblend:15")
+    assert r.dev is not None
+    assert np.abs(r.dev[:32]).max() <= 1e-20 * max(1.0, np.abs(r.dev).max())
+    assert r.dev[32:96].min() > 0
+    assert len(r.sel_per_layer[0]) == 112 and len(r.sel_per_layer[1]) == 31
+    # selection override reproduces the oracle's own selection
+    r2 = P.link(store, segs, "cacheblend:15", sel_override=r.sel_per_layer[1])
+    assert np.array_equal(r2.logits, r.logits)
+
+
+def test_C12_unselected_cached_v_rows_bit_equal(tiny):
+    cfg, w, Wt, store, ids, segs, *_ = tiny
+    r = P.link(store, segs, "legolink:4")
+    sel = set(r.plan.sel.tolist())
+    for c, cid in enumerate(ids):
+        for j in range(32):
+            i = 32 * c + j
+            if i in sel:
+                continue
+            assert np.array_equal(r.V[:, i], store.chunks[cid].V[:, j])
+            if c == 0:
+                assert np.array_equal(r.K[:, i], store.chunks[cid].K[:, j])   # Δ = 0 exact
+
+
+def test_C13_algorithms_distinguishable(tiny):
+    cfg, w, Wt, store, ids, segs, tok, (logits, *_ ) = tiny
+    naive = P.link(store, segs, "naive").logits
+    lego = P.link(store, segs, "legolink:4").logits
+    assert rel(naive, logits) > 5 * 2e-2
+    assert rel(lego, logits) > 2e-2
+    assert rel(naive, lego) > 2e-2
+
+
+def test_rebase_off_reading_differs(tiny):
+    cfg, w, Wt, store, ids, segs, tok, (logits, K, V, _) = tiny
+    r = P.link(store, segs, "naive", rebase_keys=False)
+    assert rel(r.K[0], K[0]) > 0.1          # SPEC's no-rebase reading is a different method
+
+
+def test_allocator_and_slot_map():
+    a = P.BlockAllocator(10)
+    assert a.alloc(3) == [0, 1, 2]
+    assert a.alloc(2) == [3, 4]
+    a.release([1, 3])
+    assert a.alloc(3) == [1, 3, 5]
+    with pytest.raises(MemoryError):
+        a.alloc(10)
+    assert P.slot_map([7, 2], [0, 15, 16, 31]).tolist() == [112, 127, 32, 47]
