@@ -1,0 +1,203 @@
+/*
+ * pic.h — C ABI of the B200-native KVLink / LegoLink linked-prefill library (libpic.so).
+ *
+ * Paper: "Epic: Efficient Position-Independent Caching for Serving LLMs", arXiv 2410.15332
+ * (cited P:<line> = /root/reference/PAPER.md line; S:<line> = SPEC.md line).
+ *
+ * The API follows the paper's problem statement:
+ *   generate_context_cache(static_token_chunks[]) -> cache_ids        -> pic_generate_context_cache
+ *   chat_completion(message_list of cache ids and new tokens, "in any order"), narrowed by
+ *   the north star to link(message_list, algorithm, k) -> linked KV + first-token logits
+ *                                                                      -> pic_link / pic_link_batch
+ *   expire_cache(cache_id)                              -> pic_expire_cache
+ * with the explicit-ID caching paradigm of P:188 (ids are handed out, never deduplicated).
+ *
+ * Conventions for every entry point:
+ *   - All calls return pic_status; PIC_OK (0) on success.  On error nothing observable
+ *     changed (no ids handed out, no blocks leaked, no handle created) and
+ *     pic_last_error() returns a thread-local, NUL-terminated message.
+ *   - Input arrays are BORROWED for the duration of the call (the library copies what it
+ *     keeps, including chunk token ids).  Output arrays are CALLER-OWNED, sized as stated.
+ *   - "stream" is a cudaStream_t passed as void* (e.g. torch.cuda.current_stream().cuda_stream);
+ *     all device work of a call is ordered on it.  Calls on one engine must use one stream
+ *     (or the caller orders them): blocks freed by one call are reused by the next.
+ *   - Host-only engines (device = -1) run the planner, allocator and store bookkeeping only:
+ *     pic_generate_context_cache assigns ids and blocks without computing any KV, and every
+ *     call that needs device data (link, exports, weights) returns PIC_E_NO_DEVICE.  There is
+ *     no CPU fallback of any compute step.
+ *   - Not thread-safe per engine: one engine = one caller thread.
+ */
+#ifndef PIC_H
+#define PIC_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  PIC_OK = 0,
+  PIC_E_INVALID_ARG = 1,     /* NULL pointer, negative size, unknown algorithm, k < 0, R not in [0,100] */
+  PIC_E_CONFIG = 2,          /* inconsistent model shape: H_q % H_kv, D odd or % 16, d % 64 ... */
+  PIC_E_EMPTY_INPUT = 3,     /* empty chunk, empty message list, empty literal segment */
+  PIC_E_CAPACITY = 4,        /* N > max_pos, rows > max_rows, pool out of blocks */
+  PIC_E_MISSING_CACHE = 5,   /* unknown or expired cache id */
+  PIC_E_LAYOUT = 6,          /* bad buffer size / alignment (arena too small) */
+  PIC_E_VARIANT = 7,         /* algorithm/params not supported on this call */
+  PIC_E_OOM = 8,             /* host allocation failed */
+  PIC_E_CUDA = 9,            /* a CUDA runtime/driver call failed (message has the CUDA error) */
+  PIC_E_NO_DEVICE = 10,      /* compute call on a host-only engine */
+  PIC_E_TOKEN = 11           /* token id outside [0, vocab) */
+} pic_status;
+
+/* Model shape (Llama-family decoder; reading R4 in DESIGN.md).  Weights are not
+ * loaded: they are random-init from the counter-based generator of SURVEY §8(c).6 with
+ * `seed`, exactly reproducible by seedgen/ (bit-exact bf16). */
+typedef struct {
+  int32_t n_layers, d_model, n_heads, n_kv_heads, head_dim, ffn_dim, vocab, max_pos, bos_id;
+  double rope_theta;   /* RoPE base θ (reading R2) */
+  double rms_eps;      /* RMSNorm ε (reading R4) */
+  uint64_t seed;       /* weight generator seed */
+} pic_model_config;
+
+/* Capacities of the engine's device arena. */
+typedef struct {
+  int64_t num_blocks;  /* paged KV pool size in 16-token blocks; one id spans all layers' K and V */
+  int32_t max_rows;    /* max rows recomputed in one forward (k' summed over a batch; N for CacheBlend) */
+  int32_t max_tokens;  /* max linked prompt length N of one request (<= max_pos) */
+  int32_t max_requests;/* max requests per pic_link_batch call */
+} pic_engine_limits;
+
+typedef uint64_t pic_cache_id;   /* monotone from 1, never reused */
+
+typedef enum { PIC_SEG_CACHED = 0, PIC_SEG_TOKENS = 1 } pic_seg_kind;
+
+/* One message-list entry: a cached chunk id, or literal (dynamic) tokens.  Any order. */
+typedef struct {
+  int32_t kind;              /* pic_seg_kind */
+  int32_t n_tokens;          /* TOKENS: number of tokens (> 0); CACHED: ignored */
+  pic_cache_id id;           /* CACHED: cache id */
+  const int32_t* tokens;     /* TOKENS: host array [n_tokens]; CACHED: ignored */
+} pic_segment;
+
+/* Link algorithms of P:166-170 and P:211-217 (SPEC grammar naive|fr|cacheblend:R|legolink:K). */
+typedef enum { PIC_NAIVE = 0, PIC_FULL = 1, PIC_LEGOLINK = 2, PIC_CACHEBLEND = 3 } pic_algorithm;
+
+typedef struct {
+  int32_t alg;               /* pic_algorithm */
+  int32_t k;                 /* LegoLink: first k tokens of every chunk except an index-0 chunk (R6/R7) */
+  int32_t r_percent;         /* CacheBlend: recompute ⌈R·N_cached/100⌉ cached tokens (R11) */
+  int32_t check_layer;       /* CacheBlend: layer whose K/V deviation selects tokens (R9; default 1) */
+  int32_t rebase;            /* 1 = RoPE re-base cached keys to their new positions (R1; default 1) */
+  int32_t use_graph;         /* 1 = replay a CUDA graph per plan shape (default 1) */
+  const int32_t* sel_override; /* CacheBlend test hook: sorted linked indices to keep after the check (nullable) */
+  int32_t n_sel_override;
+  float* debug_hidden;       /* test hook (nullable, host): [n_layers][N][d_model] fp32; row r of layer l = residual of
+                                the r-th selected row after layer l (rows beyond that layer's k' untouched).
+                                Single-request pic_link only; disables graphs. */
+} pic_link_params;
+
+/* Per-request result of a link. */
+typedef struct {
+  float* logits;             /* caller-owned host buffer [vocab] fp32 (nullable); first-token logits */
+  float* logits_dev;         /* caller-owned device buffer [vocab] fp32 (nullable); filled on `stream` */
+  int32_t first_token;       /* argmax of the logits (ties -> lowest id, R20); -1 if no host output was requested */
+  int32_t n_tokens;          /* N: linked prompt length */
+  int32_t n_selected;        /* k': rows recomputed in the last layer */
+  int32_t n_selected_layer0; /* rows recomputed in layer 0 (N for CacheBlend) */
+  int32_t* selected;         /* caller-owned host buffer [N] (nullable): linked indices recomputed in the last
+                                layer (CacheBlend: the device-side selection); forces a stream sync */
+} pic_link_result;
+
+typedef struct pic_engine pic_engine;
+typedef struct pic_linked pic_linked;
+
+/* Host-only: bytes of device arena pic_engine_create needs for (cfg, limits). */
+pic_status pic_arena_bytes(const pic_model_config* cfg, const pic_engine_limits* limits, size_t* out_bytes);
+
+/* Create an engine on CUDA `device` (or -1 = host-only planner engine; arena must then be NULL).
+ * `arena` is a caller-owned device buffer of >= pic_arena_bytes() bytes, 256-B aligned, kept alive
+ * until pic_engine_destroy (PyTorch owns the memory; the engine carves weights, KV pools and
+ * workspaces from it).  Weights are generated on `stream`; the call returns after they are ready. */
+pic_status pic_engine_create(const pic_model_config* cfg, const pic_engine_limits* limits, int32_t device,
+                             void* arena, size_t arena_bytes, void* stream, pic_engine** out);
+void pic_engine_destroy(pic_engine* eng);
+
+/* Compile step ("each chunk is encoded with position IDs starting from zero, and the LLM
+ * performs only the prefill stage"; P:185 KVCompile).  chunks[i] is a host array of lens[i]
+ * tokens.  All-or-nothing: on error no id is assigned and *err_index (nullable) names the failing
+ * chunk.  out_ids: caller array [n].  Returns after the device work completed. */
+pic_status pic_generate_context_cache(pic_engine* eng, const int32_t* const* chunks, const int32_t* lens,
+                                      int32_t n, void* stream, pic_cache_id* out_ids, int32_t* err_index);
+
+/* Link step (P:162, P:185 KVLink, P:211-217 LegoLink; variants P:166-170).  Assembles the message
+ * list, re-bases and gathers cached KV into fresh linked blocks, recomputes the selected rows layer
+ * by layer (Eq. 1) and produces first-token logits.  out_linked (nullable): receives a handle
+ * to the linked KV (caller releases it); NULL frees the linked blocks when the call's stream work is
+ * done.  If result->logits is set the call synchronises `stream` before returning. */
+pic_status pic_link(pic_engine* eng, const pic_segment* segs, int32_t n_segs, const pic_link_params* params,
+                    void* stream, pic_linked** out_linked, pic_link_result* result);
+
+/* Batched link of n_req independent requests in one forward (the data-parallel unit of cfg4:
+ * rows of all requests are concatenated; weights are read once).  segs[r] / n_segs[r] per request;
+ * out_linked (nullable) is an array [n_req]; results is an array [n_req].  CacheBlend and
+ * debug hooks are single-request only (PIC_E_VARIANT). */
+pic_status pic_link_batch(pic_engine* eng, int32_t n_req, const pic_segment* const* segs, const int32_t* n_segs,
+                          const pic_link_params* params, void* stream, pic_linked** out_linked,
+                          pic_link_result* results);
+
+/* Host-only planner (step a1; P:211/P:213 selection).  Caller-allocated arrays,
+ * each NULL or at least the stated size (cap = pic_plan_out.capacity >= N):
+ *   sel[cap] sorted selected linked indices (pre-CacheBlend set; CacheBlend: dynamic ∪ {N-1});
+ *   tok[cap] token ids; src[2*cap] (cache id low 31 bits, row) or (-1,-1) for dynamic rows;
+ *   chunks[3*cap] (start, len, delta) per cached segment; block_table[cap] linked block ids that
+ *   pic_link would allocate now (lowest-free-first); slot[cap] slot of each selected row
+ *   (block_table[i/16]*16 + i%16). */
+typedef struct {
+  int32_t capacity;
+  int32_t n_tokens, n_sel, n_chunks, n_blocks;
+  int32_t *sel, *tok, *src, *chunks, *block_table, *slot;
+} pic_plan_out;
+pic_status pic_plan(pic_engine* eng, const pic_segment* segs, int32_t n_segs, const pic_link_params* params,
+                    pic_plan_out* out);
+
+/* Copy layer `layer` of a linked KV cache to host: k_host, v_host are [N][H_kv][D] bf16 (uint16). */
+pic_status pic_linked_export(pic_engine* eng, const pic_linked* linked, int32_t layer, void* k_host, void* v_host);
+/* Number of tokens N and the block table (int32[ceil(N/16)], nullable) of a linked cache. */
+pic_status pic_linked_info(pic_engine* eng, const pic_linked* linked, int32_t* n_tokens, int32_t* block_table);
+pic_status pic_linked_release(pic_engine* eng, pic_linked* linked);
+
+/* Copy layer `layer` of a compiled chunk to host: [n][H_kv][D] bf16 each (post-RoPE K at positions 0..n-1). */
+pic_status pic_cache_export(pic_engine* eng, pic_cache_id id, int32_t layer, void* k_host, void* v_host);
+/* Length and block list (int32[ceil(n/16)], nullable) of a compiled chunk. */
+pic_status pic_cache_info(pic_engine* eng, pic_cache_id id, int32_t* n_tokens, int32_t* blocks);
+
+/* Free a chunk's KV.  Idempotent: *was_present (nullable) says whether it existed
+ * (S:203-211).  Live linked caches are unaffected (they own copies). */
+pic_status pic_expire_cache(pic_engine* eng, pic_cache_id id, int32_t* was_present);
+
+/* Test hook: copy generated bf16 weights to host (uint16 bf16 bits).  which: 0=q 1=k 2=v 3=o 4=gate
+ * 5=up 6=down (rows of the logical [out][in] matrix row0..row0+nrows-1), 7=embed, 8=lm_head;
+ * gains: 9=g1 10=g2 11=g_final as fp32 (nrows ignored, d_model floats). */
+pic_status pic_read_weights(pic_engine* eng, int32_t which, int32_t layer, int64_t row0, int64_t nrows, void* host_out);
+
+/* Free blocks in the KV pool and counters for tests/bench. */
+typedef struct {
+  int64_t free_blocks, total_blocks;
+  int64_t n_cached_chunks;
+  int64_t kernels_last_call;   /* kernels launched by the last link/compile call (incl. graph nodes) */
+  int64_t graphs_cached;
+  int64_t h2d_bytes_last_call; /* plan bytes copied host->device by the last compile/link forward */
+  int64_t d2h_bytes_last_call; /* result bytes copied device->host by the last link */
+} pic_stats;
+pic_status pic_get_stats(pic_engine* eng, pic_stats* out);
+
+const char* pic_last_error(void);
+const char* pic_status_string(pic_status s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PIC_H */

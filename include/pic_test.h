@@ -1,0 +1,38 @@
+/*
+ * pic_test.h — kernel-level test entry points of libpic.so (tests only; not part of the
+ * product API).  Each runs ONE hot-path kernel on host-provided inputs through the same launcher
+ * the engine uses, so GPU tests can localise a parity failure to a kernel.  All buffers are
+ * host arrays; bf16 values are passed as uint16 bit patterns.  Device memory is cudaMalloc'ed and
+ * freed inside the call.  Return pic_status as in pic.h.
+ */
+#ifndef PIC_TEST_H
+#define PIC_TEST_H
+#include "pic.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* tcgen05 GEMM (a5/a7/a8/a10): out[m][n] = Σ_k A[m][k]·B[n][k] (fp32, summed over `splits` split-K
+ * partials), A [M][K], B [N][K] bf16; bn ∈ {64,128,256}; K % 64 == 0, N % 32 == 0. */
+pic_status pic_test_gemm(const uint16_t* A, const uint16_t* B, int32_t M, int32_t N, int32_t K, int32_t bn,
+                         int32_t splits, float* out);
+
+/* a6 sparse-query causal attention (tcgen05, D = 128) + split-KV combine over a PAGED copy of K/V:
+ * K, V [n_keys][Hkv][128] bf16 are scattered into 16-token blocks in the order `block_perm`
+ * (int32[ceil(n_keys/16)], a permutation of block ids < num_blocks), queries Q [M][Hq][128] at
+ * positions pos[M] (sorted ascending, < n_keys), tiles of 128/G consecutive rows.  O [M][Hq][128] bf16. */
+pic_status pic_test_attention(const uint16_t* Q, const uint16_t* K, const uint16_t* V, const int32_t* pos,
+                              int32_t M, int32_t n_keys, int32_t Hq, int32_t Hkv, const int32_t* block_perm,
+                              int32_t num_blocks, int32_t n_splits, uint16_t* O);
+
+/* a2 KV link on a raw pool: pool K/V [n_layers][num_blocks][Hkv][16][D] bf16 (in/out), rows
+ * (src_slot -> dst_slot, delta) for layers layer0..n_layers-1, RoPE table for positions < max_pos. */
+pic_status pic_test_kv_link(uint16_t* Kpool, uint16_t* Vpool, int32_t n_layers, int32_t num_blocks, int32_t Hkv,
+                            int32_t D, const int32_t* src_slot, const int32_t* dst_slot, const int32_t* delta,
+                            int32_t n_rows, int32_t layer0, int32_t rebase, double theta, int32_t max_pos);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

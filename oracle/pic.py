@@ -254,6 +254,9 @@ class BlockAllocator:
     def __init__(self, num_blocks: int):
         self.free = set(range(num_blocks))
 
+    def peek(self, n: int) -> List[int]:
+        return sorted(self.free)[:n]
+
     def alloc(self, n: int) -> List[int]:
         if n > len(self.free):
             raise MemoryError("pool full")

@@ -1,0 +1,1277 @@
+// engine.cpp — the C ABI of libpic.so (include/pic.h): engine/arena setup, weight generation,
+// chunk store + block allocator, the link planner (step a1), and the per-layer launch sequence
+// of the linked-prefill forward (steps a2-a10), replayed through per-shape CUDA graphs.
+#include "engine.h"
+
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <cstdlib>
+#include <unistd.h>
+
+using namespace pic;
+
+// ============================================================================ errors
+static thread_local std::string g_err;
+
+static pic_status fail(pic_status s, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return s;
+}
+
+#define CK(expr)                                                                                                  \
+  do {                                                                                                            \
+    cudaError_t e_ = (expr);                                                                                      \
+    if (e_ != cudaSuccess) return fail(PIC_E_CUDA, "%s failed: %s (%s:%d)", #expr, cudaGetErrorString(e_), __FILE__, \
+                                       __LINE__);                                                                 \
+  } while (0)
+
+// PIC_DEBUG_SYNC=1: synchronise after every launch with a 20 s deadline and name a hung or
+// faulting kernel on stderr (debugging aid; graphs are disabled in this mode).
+static bool debug_sync() {
+  static int v = -1;
+  if (v < 0) v = getenv("PIC_DEBUG_SYNC") ? 1 : 0;
+  return v == 1;
+}
+
+static void dbg_sync(const char* what, cudaStream_t st) {
+  if (!debug_sync()) return;
+  char name[64];
+  snprintf(name, sizeof name, "%s", what);
+  if (char* p = strchr(name, '(')) *p = 0;
+  for (int i = 0; i < 20000; ++i) {
+    cudaError_t e = cudaStreamQuery(st);
+    if (e == cudaSuccess) {
+      fprintf(stderr, "[pic] ok   %s\n", name);
+      return;
+    }
+    if (e != cudaErrorNotReady) {
+      fprintf(stderr, "[pic] FAIL %s: %s\n", name, cudaGetErrorString(e));
+      fflush(stderr);
+      _exit(4);
+    }
+    usleep(1000);
+  }
+  fprintf(stderr, "[pic] HANG %s\n", name);
+  fflush(stderr);
+  _exit(3);
+}
+
+#define CKL(expr)            \
+  do {                       \
+    CK(expr);                \
+    dbg_sync(#expr, st);     \
+  } while (0)
+
+#define TRY(expr)                    \
+  do {                               \
+    pic_status s_ = (expr);          \
+    if (s_ != PIC_OK) return s_;     \
+  } while (0)
+
+extern "C" const char* pic_last_error(void) { return g_err.c_str(); }
+
+extern "C" const char* pic_status_string(pic_status s) {
+  switch (s) {
+    case PIC_OK: return "PIC_OK";
+    case PIC_E_INVALID_ARG: return "PIC_E_INVALID_ARG";
+    case PIC_E_CONFIG: return "PIC_E_CONFIG";
+    case PIC_E_EMPTY_INPUT: return "PIC_E_EMPTY_INPUT";
+    case PIC_E_CAPACITY: return "PIC_E_CAPACITY";
+    case PIC_E_MISSING_CACHE: return "PIC_E_MISSING_CACHE";
+    case PIC_E_LAYOUT: return "PIC_E_LAYOUT";
+    case PIC_E_VARIANT: return "PIC_E_VARIANT";
+    case PIC_E_OOM: return "PIC_E_OOM";
+    case PIC_E_CUDA: return "PIC_E_CUDA";
+    case PIC_E_NO_DEVICE: return "PIC_E_NO_DEVICE";
+    case PIC_E_TOKEN: return "PIC_E_TOKEN";
+  }
+  return "PIC_E_?";
+}
+
+// ============================================================================ config / arena
+static const int kBN[3] = {64, 128, 256};
+
+static pic_status validate_cfg(const pic_model_config* c, const pic_engine_limits* l) {
+  if (!c || !l) return fail(PIC_E_INVALID_ARG, "NULL config or limits");
+  if (c->n_layers <= 0 || c->d_model <= 0 || c->n_heads <= 0 || c->n_kv_heads <= 0 || c->head_dim <= 0 ||
+      c->ffn_dim <= 0 || c->vocab <= 0 || c->max_pos <= 0)
+    return fail(PIC_E_CONFIG, "non-positive model dimension");
+  if (c->n_heads % c->n_kv_heads) return fail(PIC_E_CONFIG, "n_heads %% n_kv_heads != 0");
+  const int G = c->n_heads / c->n_kv_heads;
+  if (128 % G) return fail(PIC_E_CONFIG, "GQA group %d must divide 128", G);
+  if (c->head_dim != 16 && c->head_dim != 32 && c->head_dim != 64 && c->head_dim != 128)
+    return fail(PIC_E_CONFIG, "head_dim must be 16/32/64/128");
+  if (c->d_model % 64 || c->ffn_dim % 64 || (c->n_heads * c->head_dim) % 64)
+    return fail(PIC_E_CONFIG, "d_model, ffn_dim, n_heads*head_dim must be multiples of 64");
+  if (c->vocab % 32) return fail(PIC_E_CONFIG, "vocab must be a multiple of 32");
+  if (c->bos_id < 0 || c->bos_id >= c->vocab) return fail(PIC_E_CONFIG, "bos_id out of range");
+  if (!(c->rope_theta > 1.0) || !(c->rms_eps > 0.0)) return fail(PIC_E_CONFIG, "bad rope_theta / rms_eps");
+  if (l->num_blocks <= 0 || l->max_rows <= 0 || l->max_tokens <= 0 || l->max_requests <= 0)
+    return fail(PIC_E_INVALID_ARG, "non-positive limits");
+  if (l->max_tokens > c->max_pos) return fail(PIC_E_CONFIG, "max_tokens > max_pos");
+  if (l->num_blocks >= (1ll << 27)) return fail(PIC_E_CONFIG, "num_blocks too large for int32 slots");
+  return PIC_OK;
+}
+
+struct Layout {
+  size_t total = 0;
+  std::vector<std::pair<void**, size_t>> items;
+  size_t add(size_t bytes) {
+    size_t off = (total + 1023) & ~size_t(1023);
+    total = off + bytes;
+    return off;
+  }
+};
+
+struct ArenaPlan {
+  size_t w_qkv, w_o, w_gu, w_down, w_g;  // per layer sizes
+  size_t off_layers, layer_bytes;
+  size_t off_E, off_lm, off_gf, off_cos, off_sin, off_K, off_V;
+  size_t off_h, off_h2, off_ws, off_x, off_O, off_u, off_Q, off_xlast, off_opart, off_ml, off_logits, off_amax,
+      off_cbdev, off_plan;
+  size_t ws_floats;
+  int attn_rows_cap, max_seqs, max_tiles, max_bt, max_k2;
+  size_t plan_ints;
+  size_t total;
+};
+
+static ArenaPlan plan_arena(const pic_model_config& c, const pic_engine_limits& l) {
+  ArenaPlan a{};
+  const size_t d = c.d_model, D = c.head_dim, Hq = c.n_heads, Hkv = c.n_kv_heads, F = c.ffn_dim, V = c.vocab;
+  const size_t qkv = (Hq + 2 * Hkv) * D;
+  Layout L;
+  a.w_qkv = qkv * d * 2;
+  a.w_o = d * Hq * D * 2;
+  a.w_gu = 2 * F * d * 2;
+  a.w_down = d * F * 2;
+  a.w_g = d * 4;
+  auto al = [](size_t x) { return (x + 1023) & ~size_t(1023); };
+  a.layer_bytes = al(a.w_qkv) + al(a.w_o) + al(a.w_gu) + al(a.w_down) + 2 * al(a.w_g);
+  a.off_layers = L.add(a.layer_bytes * c.n_layers);
+  a.off_E = L.add(V * d * 2);
+  a.off_lm = L.add(V * d * 2);
+  a.off_gf = L.add(d * 4);
+  a.off_cos = L.add((size_t)c.max_pos * (D / 2) * 4);
+  a.off_sin = L.add((size_t)c.max_pos * (D / 2) * 4);
+  const size_t pool = (size_t)c.n_layers * l.num_blocks * Hkv * 16 * D * 2;
+  a.off_K = L.add(pool);
+  a.off_V = L.add(pool);
+  const size_t M = l.max_rows;
+  a.off_h = L.add(M * d * 4);
+  a.off_h2 = L.add(M * d * 4);
+  size_t wsf = std::max({M * qkv, M * 2 * F, M * d, (size_t)l.max_requests * V});
+  wsf = std::max(wsf, (size_t)148 * 128 * 256 * 2);
+  a.ws_floats = wsf;
+  a.off_ws = L.add(wsf * 4);
+  a.off_x = L.add(M * std::max(d, Hq * D) * 2);
+  a.off_O = L.add(M * Hq * D * 2);
+  a.off_u = L.add(M * F * 2);
+  a.off_Q = L.add(M * Hq * D * 2);
+  a.off_xlast = L.add((size_t)l.max_requests * d * 2);
+  a.attn_rows_cap = (int)std::max<size_t>(4 * M, 2048);
+  a.off_opart = L.add((size_t)a.attn_rows_cap * Hq * 128 * 4);
+  a.off_ml = L.add((size_t)a.attn_rows_cap * Hq * 2 * 4);
+  a.off_logits = L.add((size_t)l.max_requests * V * 4);
+  a.off_amax = L.add((size_t)l.max_requests * 4);
+  a.off_cbdev = L.add((size_t)l.max_tokens * 4);
+  a.max_seqs = std::max(l.max_requests, 256);
+  a.max_tiles = l.max_rows + a.max_seqs;
+  a.max_bt = (int)((size_t)l.max_requests * ((l.max_tokens + 15) / 16) + l.max_rows / 16 + a.max_seqs + 16);
+  a.max_k2 = (int)std::min<size_t>((size_t)l.max_requests * l.max_tokens, (size_t)1 << 30);
+  // per-row arrays (tok,pos,slot,seq,head) + tiles + seq offsets + bt + k2 (3) + CB (cand,forced,sel2,pos2,slot2,
+  // keep,count) + tiles2 + head2
+  a.plan_ints = 5 * M + 3 * (size_t)a.max_tiles + a.max_seqs + a.max_bt + 3 * (size_t)a.max_k2 +
+                7 * (size_t)l.max_tokens + 3 * (size_t)a.max_tiles + M + 4096;
+  a.off_plan = L.add(a.plan_ints * 4);
+  a.total = L.total + 1024;
+  return a;
+}
+
+extern "C" pic_status pic_arena_bytes(const pic_model_config* cfg, const pic_engine_limits* limits, size_t* out) {
+  TRY(validate_cfg(cfg, limits));
+  if (!out) return fail(PIC_E_INVALID_ARG, "NULL out_bytes");
+  *out = plan_arena(*cfg, *limits).total;
+  return PIC_OK;
+}
+
+// ============================================================================ tensor maps
+static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+
+static pic_status get_encoder() {
+  if (g_encode) return PIC_OK;
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+  if (!fn || q != cudaDriverEntryPointSuccess) return fail(PIC_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+  g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  return PIC_OK;
+}
+
+// bf16 tensor map, SWIZZLE_128B, dims[0] innermost; strides in bytes for dims 1..rank-1
+static pic_status make_tmap(CUtensorMap* m, void* base, int rank, const uint64_t* dims, const uint64_t* strides,
+                            const uint32_t* box) {
+  uint32_t es[5] = {1, 1, 1, 1, 1};
+  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, base, dims, strides, box, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(PIC_E_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return PIC_OK;
+}
+
+// row-major [rows][cols] bf16 matrix, box = 64 cols x box_rows rows
+static pic_status make_tmap_2d(CUtensorMap* m, void* base, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+  uint64_t dims[2] = {cols, rows};
+  uint64_t strides[1] = {cols * 2};
+  uint32_t box[2] = {64, box_rows};
+  return make_tmap(m, base, 2, dims, strides, box);
+}
+
+static pic_status make_tmaps_bn(CUtensorMap* m3, void* base, uint64_t rows, uint64_t cols) {
+  for (int i = 0; i < 3; ++i) TRY(make_tmap_2d(&m3[i], base, rows, cols, kBN[i]));
+  return PIC_OK;
+}
+
+static int bn_index(int bn) { return bn == 64 ? 0 : (bn == 128 ? 1 : 2); }
+
+// ============================================================================ engine create
+static int weight_exponent(int64_t fan_in) { return (int)std::nearbyint(std::log2(std::sqrt(3.0 / (double)fan_in))); }
+
+static pic_status init_device(pic_engine* e, void* arena, size_t bytes, cudaStream_t st) {
+  const pic_model_config& c = e->cfg;
+  const ArenaPlan a = plan_arena(c, e->lim);
+  if (!arena) return fail(PIC_E_INVALID_ARG, "NULL arena for a device engine");
+  if (bytes < a.total) return fail(PIC_E_LAYOUT, "arena too small: %zu < %zu bytes", bytes, a.total);
+  if (reinterpret_cast<uintptr_t>(arena) & 255) return fail(PIC_E_LAYOUT, "arena not 256-byte aligned");
+  TRY(get_encoder());
+  char* b = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(arena) + 1023) & ~uintptr_t(1023));
+  e->arena = b;
+  e->arena_bytes = bytes;
+  e->max_seqs = a.max_seqs;
+  e->max_tiles = a.max_tiles;
+  e->max_bt = a.max_bt;
+  e->max_k2 = a.max_k2;
+  const int64_t d = c.d_model, D = c.head_dim, Hq = c.n_heads, Hkv = c.n_kv_heads, F = c.ffn_dim, V = c.vocab;
+  const int64_t qkv = (Hq + 2 * Hkv) * D;
+  const uint64_t s = c.seed;
+  auto al = [](size_t x) { return (x + 1023) & ~size_t(1023); };
+  e->layers.resize(c.n_layers);
+  for (int l = 0; l < c.n_layers; ++l) {
+    LayerW& w = e->layers[l];
+    char* p = b + a.off_layers + (size_t)l * a.layer_bytes;
+    w.qkv = p;
+    p += al(a.w_qkv);
+    w.o = p;
+    p += al(a.w_o);
+    w.gu = p;
+    p += al(a.w_gu);
+    w.down = p;
+    p += al(a.w_down);
+    w.g1 = reinterpret_cast<float*>(p);
+    p += al(a.w_g);
+    w.g2 = reinterpret_cast<float*>(p);
+    const uint64_t T = (uint64_t)l * 16;
+    char* q = reinterpret_cast<char*>(w.qkv);
+    CK(launch_gen_matrix(q, Hq * D, d, s, T + 0, weight_exponent(d), 0, st));
+    CK(launch_gen_matrix(q + Hq * D * d * 2, Hkv * D, d, s, T + 1, weight_exponent(d), 0, st));
+    CK(launch_gen_matrix(q + (Hq + Hkv) * D * d * 2, Hkv * D, d, s, T + 2, weight_exponent(d), 0, st));
+    CK(launch_gen_matrix(w.o, d, Hq * D, s, T + 3, weight_exponent(Hq * D), 0, st));
+    char* gu = reinterpret_cast<char*>(w.gu);
+    CK(launch_gen_matrix(gu, F, d, s, T + 4, weight_exponent(d), 0, st));
+    CK(launch_gen_matrix(gu + F * d * 2, F, d, s, T + 5, weight_exponent(d), 0, st));
+    CK(launch_gen_matrix(w.down, d, F, s, T + 6, weight_exponent(F), 0, st));
+    CK(launch_gen_gains(w.g1, d, s, T + 7, st));
+    CK(launch_gen_gains(w.g2, d, s, T + 8, st));
+    TRY(make_tmaps_bn(w.tm_qkv, w.qkv, qkv, d));
+    TRY(make_tmaps_bn(w.tm_o, w.o, d, Hq * D));
+    TRY(make_tmaps_bn(w.tm_gu, w.gu, 2 * F, d));
+    TRY(make_tmaps_bn(w.tm_down, w.down, d, F));
+  }
+  e->E = b + a.off_E;
+  e->Wlm = b + a.off_lm;
+  e->gf = reinterpret_cast<float*>(b + a.off_gf);
+  CK(launch_gen_matrix(e->E, V, d, s, 0xE0000001ull, 0, 0, st));
+  CK(launch_gen_matrix(e->Wlm, V, d, s, 0xE0000002ull, weight_exponent(d), 0, st));
+  CK(launch_gen_gains(e->gf, d, s, 0xE0000003ull, st));
+  TRY(make_tmaps_bn(e->tm_lm, e->Wlm, V, d));
+
+  // RoPE table: angle = p · θ^(−2j/D) in fp64, stored fp32 (reading R2)
+  e->cos_t = reinterpret_cast<float*>(b + a.off_cos);
+  e->sin_t = reinterpret_cast<float*>(b + a.off_sin);
+  {
+    const int64_t half = D / 2, n = (int64_t)c.max_pos * half;
+    std::vector<float> cs(n), sn(n);
+    std::vector<double> inv(half);
+    for (int64_t j = 0; j < half; ++j) inv[j] = std::pow(c.rope_theta, -2.0 * (double)j / (double)D);
+    for (int64_t p = 0; p < c.max_pos; ++p)
+      for (int64_t j = 0; j < half; ++j) {
+        const double ang = (double)p * inv[j];
+        cs[p * half + j] = (float)std::cos(ang);
+        sn[p * half + j] = (float)std::sin(ang);
+      }
+    CK(cudaMemcpyAsync(e->cos_t, cs.data(), n * 4, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(e->sin_t, sn.data(), n * 4, cudaMemcpyHostToDevice, st));
+    CK(cudaStreamSynchronize(st));
+  }
+
+  // paged pools, zeroed so never-written slots are finite (masked keys multiply P = 0)
+  e->Kpool = b + a.off_K;
+  e->Vpool = b + a.off_V;
+  e->layer_stride = e->lim.num_blocks * Hkv * 16 * D;
+  const size_t pool = (size_t)c.n_layers * e->layer_stride * 2;
+  CK(cudaMemsetAsync(e->Kpool, 0, pool, st));
+  CK(cudaMemsetAsync(e->Vpool, 0, pool, st));
+  if (D >= 64) {
+    uint64_t dims[4] = {(uint64_t)D, 16, (uint64_t)Hkv, (uint64_t)c.n_layers * e->lim.num_blocks};
+    uint64_t strides[3] = {(uint64_t)D * 2, (uint64_t)16 * D * 2, (uint64_t)Hkv * 16 * D * 2};
+    uint32_t box[4] = {64, 16, 1, 1};
+    TRY(make_tmap(&e->tm_K, e->Kpool, 4, dims, strides, box));
+    TRY(make_tmap(&e->tm_V, e->Vpool, 4, dims, strides, box));
+  }
+  const int64_t M = e->lim.max_rows;
+  e->h = reinterpret_cast<float*>(b + a.off_h);
+  e->h2 = reinterpret_cast<float*>(b + a.off_h2);
+  e->ws = reinterpret_cast<float*>(b + a.off_ws);
+  e->ws_floats = a.ws_floats;
+  e->x = b + a.off_x;
+  e->Obuf = b + a.off_O;
+  e->u = b + a.off_u;
+  e->Q = b + a.off_Q;
+  e->x_last = b + a.off_xlast;
+  e->o_part = reinterpret_cast<float*>(b + a.off_opart);
+  e->ml_part = reinterpret_cast<float*>(b + a.off_ml);
+  e->attn_rows_cap = a.attn_rows_cap;
+  e->logits = reinterpret_cast<float*>(b + a.off_logits);
+  e->amax = reinterpret_cast<int32_t*>(b + a.off_amax);
+  e->cb_dev = reinterpret_cast<float*>(b + a.off_cbdev);
+  e->plan_dev = reinterpret_cast<int32_t*>(b + a.off_plan);
+  e->plan_cap_ints = a.plan_ints;
+  // A operands: the GEMM always stages 128-row A tiles
+  TRY(make_tmap_2d(&e->tm_x, e->x, M, d, 128));
+  TRY(make_tmap_2d(&e->tm_O, e->Obuf, M, Hq * D, 128));
+  TRY(make_tmap_2d(&e->tm_u, e->u, M, F, 128));
+  TRY(make_tmap_2d(&e->tm_xlast, e->x_last, e->lim.max_requests, d, 128));
+  if (D == 128) {
+    const int G = (int)(Hq / Hkv);
+    uint64_t dims[3] = {(uint64_t)D, (uint64_t)Hq, (uint64_t)M};
+    uint64_t strides[2] = {(uint64_t)D * 2, (uint64_t)Hq * D * 2};
+    uint32_t box[3] = {64, (uint32_t)G, (uint32_t)(128 / G)};
+    TRY(make_tmap(&e->tm_Q, e->Q, 3, dims, strides, box));
+  }
+  CK(cudaMallocHost(&e->plan_host, a.plan_ints * 4));
+  CK(cudaMallocHost(&e->host_logits, (size_t)e->lim.max_requests * V * 4));
+  CK(cudaMallocHost(&e->host_amax, (size_t)e->lim.max_requests * 4));
+  CK(cudaEventCreateWithFlags(&e->plan_ev, cudaEventDisableTiming));
+  CK(cudaEventRecord(e->plan_ev, st));
+  CK(cudaEventCreate(&e->ev0));
+  CK(cudaEventCreate(&e->ev1));
+  CK(cudaStreamCreateWithFlags(&e->cap_stream, cudaStreamNonBlocking));
+  CK(prepare_kernels());
+  CK(cudaStreamSynchronize(st));
+  return PIC_OK;
+}
+
+extern "C" pic_status pic_engine_create(const pic_model_config* cfg, const pic_engine_limits* limits, int32_t device,
+                                        void* arena, size_t arena_bytes, void* stream, pic_engine** out) {
+  TRY(validate_cfg(cfg, limits));
+  if (!out) return fail(PIC_E_INVALID_ARG, "NULL out");
+  *out = nullptr;
+  pic_engine* e = new (std::nothrow) pic_engine();
+  if (!e) return fail(PIC_E_OOM, "engine allocation failed");
+  e->cfg = *cfg;
+  e->lim = *limits;
+  e->device = device;
+  e->host_only = device < 0;
+  e->alloc.reset(limits->num_blocks);
+  if (!e->host_only) {
+    cudaError_t err = cudaSetDevice(device);
+    if (err != cudaSuccess) {
+      delete e;
+      return fail(PIC_E_CUDA, "cudaSetDevice(%d): %s", device, cudaGetErrorString(err));
+    }
+    pic_status s = init_device(e, arena, arena_bytes, reinterpret_cast<cudaStream_t>(stream));
+    if (s != PIC_OK) {
+      std::string msg = g_err;
+      pic_engine_destroy(e);
+      g_err = msg;
+      return s;
+    }
+  } else if (arena) {
+    delete e;
+    return fail(PIC_E_INVALID_ARG, "host-only engine takes no arena");
+  } else {
+    const ArenaPlan a = plan_arena(*cfg, *limits);
+    e->max_seqs = a.max_seqs;
+    e->max_tiles = a.max_tiles;
+    e->max_bt = a.max_bt;
+    e->max_k2 = a.max_k2;
+  }
+  *out = e;
+  return PIC_OK;
+}
+
+extern "C" void pic_engine_destroy(pic_engine* e) {
+  if (!e) return;
+  if (!e->host_only) {
+    for (auto& kv : e->graphs) cudaGraphExecDestroy(kv.second);
+    if (e->plan_host) cudaFreeHost(e->plan_host);
+    if (e->host_logits) cudaFreeHost(e->host_logits);
+    if (e->host_amax) cudaFreeHost(e->host_amax);
+    if (e->plan_ev) cudaEventDestroy(e->plan_ev);
+    if (e->ev0) cudaEventDestroy(e->ev0);
+    if (e->ev1) cudaEventDestroy(e->ev1);
+    if (e->cap_stream) cudaStreamDestroy(e->cap_stream);
+  }
+  delete e;
+}
+
+// ============================================================================ planner (a1)
+static pic_status assemble(pic_engine* e, const pic_segment* segs, int32_t n_segs, LinkPlanHost& p) {
+  if (!segs && n_segs) return fail(PIC_E_INVALID_ARG, "NULL segments");
+  if (n_segs <= 0) return fail(PIC_E_EMPTY_INPUT, "empty message list");
+  int64_t N = 0;
+  for (int i = 0; i < n_segs; ++i) {
+    const pic_segment& s = segs[i];
+    if (s.kind == PIC_SEG_CACHED) {
+      auto it = e->store.find(s.id);
+      if (it == e->store.end()) return fail(PIC_E_MISSING_CACHE, "segment %d: unknown or expired cache id %llu", i,
+                                            (unsigned long long)s.id);
+      N += (int64_t)it->second.tokens.size();
+    } else if (s.kind == PIC_SEG_TOKENS) {
+      if (s.n_tokens <= 0) return fail(PIC_E_EMPTY_INPUT, "segment %d: empty literal segment", i);
+      if (!s.tokens) return fail(PIC_E_INVALID_ARG, "segment %d: NULL tokens", i);
+      N += s.n_tokens;
+    } else {
+      return fail(PIC_E_INVALID_ARG, "segment %d: bad kind %d", i, s.kind);
+    }
+  }
+  if (N > e->lim.max_tokens || N > e->cfg.max_pos)
+    return fail(PIC_E_CAPACITY, "linked prompt of %lld tokens exceeds max_tokens %d / max_pos %d", (long long)N,
+                e->lim.max_tokens, e->cfg.max_pos);
+  p = LinkPlanHost();
+  p.N = (int)N;
+  p.tok.reserve(N);
+  p.src_cid.reserve(N);
+  p.src_row.reserve(N);
+  p.dynamic.assign(N, 0);
+  int32_t pos = 0;
+  for (int i = 0; i < n_segs; ++i) {
+    const pic_segment& s = segs[i];
+    if (s.kind == PIC_SEG_CACHED) {
+      const ChunkRec& c = e->store.at(s.id);
+      const int n = (int)c.tokens.size();
+      p.chunk_id.push_back(s.id);
+      p.chunk_start.push_back(pos);
+      p.chunk_len.push_back(n);
+      p.chunk_delta.push_back(pos - c.c0);  // Δ_c = s_c − c0 (reading R1)
+      for (int j = 0; j < n; ++j) {
+        p.tok.push_back(c.tokens[j]);
+        p.src_cid.push_back((int32_t)(s.id & 0x7FFFFFFF));
+        p.src_row.push_back(j);
+      }
+      pos += n;
+    } else {
+      for (int j = 0; j < s.n_tokens; ++j) {
+        const int32_t t = s.tokens[j];
+        if (t < 0 || t >= e->cfg.vocab) return fail(PIC_E_TOKEN, "segment %d token %d = %d out of range", i, j, t);
+        p.tok.push_back(t);
+        p.src_cid.push_back(-1);
+        p.src_row.push_back(-1);
+        p.dynamic[pos + j] = 1;
+      }
+      pos += s.n_tokens;
+    }
+  }
+  return PIC_OK;
+}
+
+static pic_status check_params(const pic_link_params* pr) {
+  if (!pr) return fail(PIC_E_INVALID_ARG, "NULL params");
+  if (pr->alg < PIC_NAIVE || pr->alg > PIC_CACHEBLEND) return fail(PIC_E_INVALID_ARG, "unknown algorithm %d", pr->alg);
+  if (pr->alg == PIC_LEGOLINK && pr->k < 0) return fail(PIC_E_INVALID_ARG, "LegoLink k < 0");
+  if (pr->alg == PIC_CACHEBLEND && (pr->r_percent < 0 || pr->r_percent > 100))
+    return fail(PIC_E_INVALID_ARG, "CacheBlend R outside [0,100]");
+  if (pr->alg == PIC_CACHEBLEND && pr->check_layer < 0) return fail(PIC_E_INVALID_ARG, "check_layer < 0");
+  return PIC_OK;
+}
+
+// Selected set: Naive = dynamic; FR = all; LegoLink(k) = dynamic ∪ first
+// min(k, n_c) rows of every chunk not starting at index 0 (R6, R7); CacheBlend = dynamic
+// (its cached rows are chosen at the check layer).  Then ∪ {N−1} (R8).
+static void select_rows(const pic_link_params* pr, LinkPlanHost& p) {
+  std::vector<uint8_t> s(p.N, 0);
+  for (int i = 0; i < p.N; ++i) s[i] = p.dynamic[i];
+  if (pr->alg == PIC_FULL) std::fill(s.begin(), s.end(), 1);
+  if (pr->alg == PIC_LEGOLINK)
+    for (size_t c = 0; c < p.chunk_start.size(); ++c) {
+      if (p.chunk_start[c] == 0) continue;
+      const int k = std::min(pr->k, p.chunk_len[c]);
+      for (int j = 0; j < k; ++j) s[p.chunk_start[c] + j] = 1;
+    }
+  s[p.N - 1] = 1;
+  p.sel.clear();
+  for (int i = 0; i < p.N; ++i)
+    if (s[i]) p.sel.push_back(i);
+}
+
+static int32_t slot_of(const std::vector<int32_t>& bt, int32_t i) { return bt[i / 16] * 16 + i % 16; }
+
+extern "C" pic_status pic_plan(pic_engine* e, const pic_segment* segs, int32_t n_segs, const pic_link_params* pr,
+                               pic_plan_out* out) {
+  if (!e || !out) return fail(PIC_E_INVALID_ARG, "NULL engine/out");
+  TRY(check_params(pr));
+  LinkPlanHost p;
+  TRY(assemble(e, segs, n_segs, p));
+  select_rows(pr, p);
+  const int nb = (p.N + 15) / 16;
+  if (out->capacity < p.N) return fail(PIC_E_LAYOUT, "plan capacity %d < N %d", out->capacity, p.N);
+  out->n_tokens = p.N;
+  out->n_sel = (int)p.sel.size();
+  out->n_chunks = (int)p.chunk_start.size();
+  out->n_blocks = nb;
+  std::vector<int32_t> bt = e->alloc.peek(nb);
+  if ((int)bt.size() < nb) return fail(PIC_E_CAPACITY, "pool has %zu free blocks, need %d", bt.size(), nb);
+  if (out->sel) std::copy(p.sel.begin(), p.sel.end(), out->sel);
+  if (out->tok) std::copy(p.tok.begin(), p.tok.end(), out->tok);
+  if (out->src)
+    for (int i = 0; i < p.N; ++i) {
+      out->src[2 * i] = p.src_cid[i];
+      out->src[2 * i + 1] = p.src_row[i];
+    }
+  if (out->chunks)
+    for (size_t c = 0; c < p.chunk_start.size(); ++c) {
+      out->chunks[3 * c] = p.chunk_start[c];
+      out->chunks[3 * c + 1] = p.chunk_len[c];
+      out->chunks[3 * c + 2] = p.chunk_delta[c];
+    }
+  if (out->block_table) std::copy(bt.begin(), bt.end(), out->block_table);
+  if (out->slot)
+    for (size_t r = 0; r < p.sel.size(); ++r) out->slot[r] = slot_of(bt, p.sel[r]);
+  return PIC_OK;
+}
+
+// ============================================================================ forward (a2..a10)
+struct PlanPack {  // dynamic packing of the plan arrays into one H2D copy
+  std::vector<int32_t>* host = nullptr;
+  size_t n = 0;
+  int32_t* base_dev = nullptr;
+  int32_t* put(const std::vector<int32_t>& v, size_t reserve = 0) {
+    const size_t off = n;
+    const size_t len = std::max(v.size(), reserve);
+    n += (len + 31) & ~size_t(31);
+    host->resize(n, 0);
+    std::copy(v.begin(), v.end(), host->begin() + off);
+    return base_dev + off;
+  }
+};
+
+static int choose_attn_splits(int n_tiles, int Hkv, int max_kv_tiles, int M, int cap_rows) {
+  const int ctas = n_tiles * Hkv;
+  int s = std::max(1, std::min({(2 * 148 + ctas - 1) / ctas, std::max(1, max_kv_tiles / 2), 16}));
+  while (s > 1 && (int64_t)s * M > cap_rows) --s;
+  return s;
+}
+
+struct GemmChoice {
+  int bn, splits;
+};
+
+static GemmChoice choose_gemm(const pic_engine* e, int M, int N, int K) {
+  const int kblk = K / 64;
+  GemmChoice best{128, 1};
+  double best_eff = -1;
+  for (int bi = 2; bi >= 0; --bi) {
+    const int bn = kBN[bi];
+    const int tiles = ((M + 127) / 128) * ((N + bn - 1) / bn);
+    int s = std::max(1, std::min(148 / std::max(tiles, 1), std::max(1, kblk / 2)));
+    while (s > 1 && (size_t)s * M * N > e->ws_floats) --s;
+    const int ctas = tiles * s;
+    const double eff = (double)ctas / (148.0 * ((ctas + 147) / 148));
+    if (eff > best_eff + 1e-9) {
+      best_eff = eff;
+      best = {bn, s};
+    }
+  }
+  return best;
+}
+
+struct Runner {
+  pic_engine* e;
+  cudaStream_t st;
+  int64_t launches = 0;
+  pic_status gemm(const CUtensorMap& A, const CUtensorMap* B3, int M, int N, int K, int* splits_out) {
+    GemmChoice g = choose_gemm(e, M, N, K);
+    *splits_out = g.splits;
+    if (debug_sync()) fprintf(stderr, "[pic] gemm M=%d N=%d K=%d bn=%d splits=%d\n", M, N, K, g.bn, g.splits);
+    ++launches;
+    CKL(launch_gemm_partial(A, B3[bn_index(g.bn)], e->ws, M, N, K, g.splits, g.bn, st));
+    return PIC_OK;
+  }
+};
+
+// Enqueue the whole forward on `st`.  Plan arrays are already on the device at the given pointers.
+struct DevPlan {
+  int32_t *tok, *pos, *slot, *seq, *tiles, *seq_bt_off, *bt, *k2_src, *k2_dst, *k2_delta, *head_map;
+  int32_t *cb_cand, *cb_forced, *cb_sel2, *cb_pos2, *cb_slot2, *cb_keep, *cb_count, *tiles2, *head_map2;
+  int n_tiles, n_tiles2;
+};
+
+static pic_status enqueue_forward(pic_engine* e, const Fwd& f, const DevPlan& dp, cudaStream_t st, float* debug_hidden,
+                                  int64_t* n_launch) {
+  const pic_model_config& c = e->cfg;
+  const int L = c.n_layers, d = c.d_model, D = c.head_dim, Hq = c.n_heads, Hkv = c.n_kv_heads, F = c.ffn_dim;
+  const int qkv = (Hq + 2 * Hkv) * D;
+  const float eps = (float)c.rms_eps;
+  Runner R{e, st};
+  char* Kp = reinterpret_cast<char*>(e->Kpool);
+  char* Vp = reinterpret_cast<char*>(e->Vpool);
+  const size_t lbytes = (size_t)e->layer_stride * 2;
+
+  if (!f.k2_src.empty() && f.k2_layer0 < L) {
+    ++R.launches;
+    CKL(launch_kv_link(e->Kpool, e->Vpool, dp.k2_src, dp.k2_dst, dp.k2_delta, (int)f.k2_src.size(), f.k2_layer0,
+                      L - f.k2_layer0, e->layer_stride, Hkv, D, e->cos_t, e->sin_t, f.rebase, st));
+  }
+  ++R.launches;
+  CKL(launch_embed(e->E, dp.tok, e->h, f.M, d, st));
+  int M = f.M;
+  float* hc = e->h;
+  const int32_t *pos = dp.pos, *slot = dp.slot, *tiles = dp.tiles;
+  int n_tiles = dp.n_tiles;
+  const int32_t* head_map = dp.head_map;
+  float* prevP = nullptr;
+  int prev_s = 0;
+  auto capture = [&](int layer) -> pic_status {
+    if (!debug_hidden) return PIC_OK;
+    CK(cudaMemcpyAsync(debug_hidden + (size_t)layer * f.debug_rows * d, hc, (size_t)M * d * 4, cudaMemcpyDeviceToHost,
+                       st));
+    return PIC_OK;
+  };
+  for (int l = 0; l < L; ++l) {
+    const LayerW& w = e->layers[l];
+    char* Kl = Kp + l * lbytes;
+    char* Vl = Vp + l * lbytes;
+    int s = 0;
+    ++R.launches;
+    CKL(launch_residual_rmsnorm(hc, prevP, prev_s, w.g1, e->x, nullptr, M, d, eps, st));
+    if (l > 0) TRY(capture(l - 1));
+    TRY(R.gemm(e->tm_x, w.tm_qkv, M, qkv, d, &s));
+    if (f.cb && l == f.cb_layer) {
+      // a9: CacheBlend selection at the check layer (P:170 steps 3-4)
+      if (!f.cb_override) {
+        R.launches += 3;
+        CKL(launch_cb_deviation(e->ws, s, dp.cb_cand, dp.slot, e->cos_t, e->sin_t, Kl, Vl, e->cb_dev, M, Hq, Hkv, D,
+                               st));
+        CKL(launch_cb_rank(e->cb_dev, dp.cb_keep, M, f.cb_T, st));
+        CKL(launch_cb_compact(dp.cb_keep, dp.cb_forced, dp.bt, dp.cb_sel2, dp.cb_pos2, dp.cb_slot2, dp.cb_count, M,
+                             st));
+      }
+      ++R.launches;
+      CKL(launch_gather_rows(hc, dp.cb_sel2, e->h2, f.M2, d, st));
+      hc = e->h2;
+      ++R.launches;
+      CKL(launch_qkv_rope_scatter(e->ws, s, M, dp.cb_sel2, dp.cb_pos2, dp.cb_slot2, e->cos_t, e->sin_t, e->Q, Kl, Vl,
+                                 f.M2, Hq, Hkv, D, st));
+      M = f.M2;
+      pos = dp.cb_pos2;
+      slot = dp.cb_slot2;
+      tiles = dp.tiles2;
+      n_tiles = dp.n_tiles2;
+      head_map = dp.head_map2;
+    } else {
+      ++R.launches;
+      CKL(launch_qkv_rope_scatter(e->ws, s, M, nullptr, pos, slot, e->cos_t, e->sin_t, e->Q, Kl, Vl, M, Hq, Hkv, D,
+                                 st));
+    }
+    if (f.compile && l == L - 1) break;  // compile needs only the last layer's K/V
+    // a6 attention
+    if (D == 128) {
+      AttnArgs a{};
+      a.tiles = tiles;
+      a.seq_bt_off = dp.seq_bt_off;
+      a.bt = dp.bt;
+      a.row_pos = pos;
+      a.n_tiles = n_tiles;
+      a.M = M;
+      a.Hq = Hq;
+      a.Hkv = Hkv;
+      a.layer = l;
+      a.num_blocks = (int)e->lim.num_blocks;
+      int max_len = 0;
+      for (size_t q = 0; q < f.seq_bt_off.size(); ++q) {
+        const int end = (q + 1 < f.seq_bt_off.size()) ? f.seq_bt_off[q + 1] : (int)f.bt.size();
+        max_len = std::max(max_len, (end - f.seq_bt_off[q]) * 16);
+      }
+      a.n_splits = choose_attn_splits(n_tiles, Hkv, (max_len + 127) / 128, M, e->attn_rows_cap);
+      a.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)D));
+      a.o_part = e->o_part;
+      a.ml_part = e->ml_part;
+      R.launches += 2;
+      CKL(launch_attention_tc(e->tm_Q, e->tm_K, e->tm_V, a, st));
+      CKL(launch_attn_combine(e->o_part, e->ml_part, e->Obuf, M, Hq, D, a.n_splits, st));
+    } else {
+      if (f.cb && l >= f.cb_layer) return fail(PIC_E_VARIANT, "CacheBlend needs head_dim 128 on the GPU path");
+      ++R.launches;
+      CKL(launch_attention_simt(e->Q, Kl, Vl, dp.seq, dp.seq_bt_off, dp.bt, pos, e->Obuf, M, Hq, Hkv, D,
+                               (float)(1.0 / std::sqrt((double)D)), st));
+    }
+    // a7 O projection, residual + a8 MLP
+    TRY(R.gemm(e->tm_O, w.tm_o, M, d, Hq * D, &s));
+    ++R.launches;
+    CKL(launch_residual_rmsnorm(hc, e->ws, s, w.g2, e->x, nullptr, M, d, eps, st));
+    TRY(R.gemm(e->tm_x, w.tm_gu, M, 2 * F, d, &s));
+    ++R.launches;
+    CKL(launch_swiglu(e->ws, s, e->u, M, F, st));
+    TRY(R.gemm(e->tm_u, w.tm_down, M, d, F, &s));
+    prevP = e->ws;
+    prev_s = s;
+  }
+  if (!f.compile) {
+    // a10: final norm of the last rows, LM head, argmax
+    ++R.launches;
+    CKL(launch_residual_rmsnorm(hc, prevP, prev_s, e->gf, e->x_last, head_map, M, d, eps, st));
+    TRY(capture(L - 1));
+    int s = 0;
+    TRY(R.gemm(e->tm_xlast, e->tm_lm, f.n_head, c.vocab, d, &s));
+    ++R.launches;
+    CKL(launch_logits_argmax(e->ws, s, e->logits, e->amax, f.n_head, c.vocab, st));
+  }
+  *n_launch = R.launches;
+  return PIC_OK;
+}
+
+static void add_sig(std::vector<int64_t>& sig, const Fwd& f, const DevPlan& dp) {
+  sig = {f.M,  dp.n_tiles, (int64_t)f.seq_bt_off.size(), (int64_t)f.bt.size(), (int64_t)f.k2_src.size(), f.k2_layer0,
+         f.n_head, f.compile, f.rebase, f.cb, f.cb_layer, f.cb_T, f.M2, f.cb_override, dp.n_tiles2};
+  // attention split choice depends on the per-sequence block-table lengths
+  for (size_t q = 0; q < f.seq_bt_off.size(); ++q) sig.push_back(f.seq_bt_off[q]);
+}
+
+static pic_status run_forward(pic_engine* e, const Fwd& f, cudaStream_t st, bool use_graph, float* debug_hidden) {
+  const int Mcap = e->lim.max_rows;
+  if (f.M > Mcap) return fail(PIC_E_CAPACITY, "%d rows exceed max_rows %d", f.M, Mcap);
+  if ((int)f.tiles.size() / 3 > e->max_tiles || (int)f.seq_bt_off.size() > e->max_seqs ||
+      (int)f.bt.size() > e->max_bt || (int)f.k2_src.size() > e->max_k2)
+    return fail(PIC_E_CAPACITY, "plan exceeds engine capacities");
+  // pack plan arrays
+  std::vector<int32_t> host;
+  host.reserve(4096);
+  PlanPack pk{&host, 0, e->plan_dev};
+  DevPlan dp{};
+  dp.tok = pk.put(f.tok);
+  dp.pos = pk.put(f.pos);
+  dp.slot = pk.put(f.slot);
+  dp.seq = pk.put(f.seq);
+  dp.tiles = pk.put(f.tiles);
+  dp.seq_bt_off = pk.put(f.seq_bt_off);
+  dp.bt = pk.put(f.bt);
+  dp.k2_src = pk.put(f.k2_src);
+  dp.k2_dst = pk.put(f.k2_dst);
+  dp.k2_delta = pk.put(f.k2_delta);
+  dp.head_map = pk.put(f.head_map);
+  dp.n_tiles = (int)f.tiles.size() / 3;
+  if (f.cb) {
+    dp.cb_cand = pk.put(f.cb_cand);
+    dp.cb_forced = pk.put(f.cb_forced);
+    dp.cb_sel2 = pk.put(f.cb_sel2, f.M);
+    dp.cb_pos2 = pk.put(f.cb_pos2, f.M);
+    dp.cb_slot2 = pk.put(f.cb_slot2, f.M);
+    dp.cb_keep = pk.put({}, f.M);
+    dp.cb_count = pk.put({}, 1);
+    dp.tiles2 = pk.put(f.tiles2);
+    dp.head_map2 = pk.put(f.head_map2);
+    dp.n_tiles2 = (int)f.tiles2.size() / 3;
+    e->last_cb_sel2 = dp.cb_sel2;
+  }
+  if (pk.n > e->plan_cap_ints) return fail(PIC_E_CAPACITY, "plan of %zu ints exceeds %zu", pk.n, e->plan_cap_ints);
+  // the previous call's H2D copy must have consumed the pinned staging buffer
+  CK(cudaEventSynchronize(e->plan_ev));
+  std::memcpy(e->plan_host, host.data(), pk.n * 4);
+  CK(cudaMemcpyAsync(e->plan_dev, e->plan_host, pk.n * 4, cudaMemcpyHostToDevice, st));
+  CK(cudaEventRecord(e->plan_ev, st));
+  e->h2d_last = (int64_t)pk.n * 4;
+
+  int64_t nl = 0;
+  if (!use_graph || debug_hidden || debug_sync()) {
+    TRY(enqueue_forward(e, f, dp, st, debug_hidden, &nl));
+    e->kernels_last = nl;
+    return PIC_OK;
+  }
+  std::vector<int64_t> sig;
+  add_sig(sig, f, dp);
+  auto it = e->graphs.find(sig);
+  if (it == e->graphs.end()) {
+    // capture on the engine's own stream (the caller's may be the legacy default stream, which
+    // cannot be captured); the instantiated graph is then launched on the caller's stream
+    cudaGraph_t g = nullptr;
+    CK(cudaStreamBeginCapture(e->cap_stream, cudaStreamCaptureModeThreadLocal));
+    pic_status s = enqueue_forward(e, f, dp, e->cap_stream, nullptr, &nl);
+    cudaError_t ce = cudaStreamEndCapture(e->cap_stream, &g);
+    if (s != PIC_OK) {
+      if (g) cudaGraphDestroy(g);
+      return s;
+    }
+    if (ce != cudaSuccess) return fail(PIC_E_CUDA, "graph capture: %s", cudaGetErrorString(ce));
+    cudaGraphExec_t ex = nullptr;
+    ce = cudaGraphInstantiate(&ex, g, 0);
+    cudaGraphDestroy(g);
+    if (ce != cudaSuccess) return fail(PIC_E_CUDA, "graph instantiate: %s", cudaGetErrorString(ce));
+    if (e->graphs.size() > 64) {
+      cudaGraphExecDestroy(e->graphs.begin()->second);
+      e->graphs.erase(e->graphs.begin());
+    }
+    it = e->graphs.emplace(sig, ex).first;
+    e->kernels_last = nl;
+  }
+  CK(cudaGraphLaunch(it->second, st));
+  return PIC_OK;
+}
+
+// Build the tiles of `rows` rows of sequence `seq` starting at row index r0 of the forward.
+static void add_tiles(std::vector<int32_t>& tiles, int seq, int r0, int rows, int qpt) {
+  for (int a = 0; a < rows; a += qpt) {
+    tiles.push_back(seq);
+    tiles.push_back(r0 + a);
+    tiles.push_back(std::min(qpt, rows - a));
+  }
+}
+
+static int qpt_of(const pic_model_config& c) { return 128 / (c.n_heads / c.n_kv_heads); }
+
+// ============================================================================ compile (a0)
+extern "C" pic_status pic_generate_context_cache(pic_engine* e, const int32_t* const* chunks, const int32_t* lens,
+                                                 int32_t n, void* stream, pic_cache_id* out_ids, int32_t* err_index) {
+  if (err_index) *err_index = -1;
+  if (!e || !out_ids || (n > 0 && (!chunks || !lens))) return fail(PIC_E_INVALID_ARG, "NULL argument");
+  if (n <= 0) return fail(PIC_E_EMPTY_INPUT, "no chunks");
+  int64_t need = 0;
+  for (int i = 0; i < n; ++i) {
+    if (lens[i] <= 0) {
+      if (err_index) *err_index = i;
+      return fail(PIC_E_EMPTY_INPUT, "chunk %d is empty", i);
+    }
+    if (!chunks[i]) {
+      if (err_index) *err_index = i;
+      return fail(PIC_E_INVALID_ARG, "chunk %d is NULL", i);
+    }
+    if (lens[i] > e->cfg.max_pos || lens[i] > e->lim.max_tokens) {
+      if (err_index) *err_index = i;
+      return fail(PIC_E_CAPACITY, "chunk %d of %d tokens exceeds max_tokens/max_pos", i, lens[i]);
+    }
+    for (int j = 0; j < lens[i]; ++j)
+      if (chunks[i][j] < 0 || chunks[i][j] >= e->cfg.vocab) {
+        if (err_index) *err_index = i;
+        return fail(PIC_E_TOKEN, "chunk %d token %d = %d out of range", i, j, chunks[i][j]);
+      }
+    need += (lens[i] + 15) / 16;
+  }
+  if (!e->alloc.can(need)) return fail(PIC_E_CAPACITY, "pool has %zu free blocks, compile needs %lld",
+                                       e->alloc.free_ids.size(), (long long)need);
+  // allocate blocks lowest-free-first in chunk order
+  std::vector<std::vector<int32_t>> blocks(n);
+  for (int i = 0; i < n; ++i) blocks[i] = e->alloc.alloc((lens[i] + 15) / 16);
+  auto rollback = [&]() {
+    for (auto& b : blocks) e->alloc.release(b);
+  };
+  if (!e->host_only) {
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    // pack (chunk, row range) pieces into forwards of <= max_rows rows / max_seqs sequences
+    const int qpt = qpt_of(e->cfg);
+    Fwd f;
+    f.compile = true;
+    auto flush = [&]() -> pic_status {
+      if (f.M == 0) return PIC_OK;
+      pic_status s = run_forward(e, f, st, false, nullptr);
+      f = Fwd();
+      f.compile = true;
+      return s;
+    };
+    for (int i = 0; i < n; ++i) {
+      for (int a = 0; a < lens[i];) {
+        const int room = e->lim.max_rows - f.M;
+        if (room <= 0 || (int)f.seq_bt_off.size() >= e->max_seqs ||
+            (int)f.bt.size() + (int)blocks[i].size() > e->max_bt) {
+          pic_status s = flush();
+          if (s != PIC_OK) {
+            rollback();
+            return s;
+          }
+          continue;
+        }
+        const int take = std::min(room, lens[i] - a);
+        const int seq = (int)f.seq_bt_off.size();
+        f.seq_bt_off.push_back((int)f.bt.size());
+        f.bt.insert(f.bt.end(), blocks[i].begin(), blocks[i].end());
+        add_tiles(f.tiles, seq, f.M, take, qpt);
+        for (int j = a; j < a + take; ++j) {
+          f.tok.push_back(chunks[i][j]);
+          f.pos.push_back(j);                          // positions from zero
+          f.slot.push_back(slot_of(blocks[i], j));
+          f.seq.push_back(seq);
+        }
+        f.M += take;
+        a += take;
+      }
+    }
+    pic_status s = flush();
+    if (s != PIC_OK) {
+      rollback();
+      return s;
+    }
+    cudaError_t ce = cudaStreamSynchronize(st);
+    if (ce != cudaSuccess) {
+      rollback();
+      return fail(PIC_E_CUDA, "compile: %s", cudaGetErrorString(ce));
+    }
+  }
+  for (int i = 0; i < n; ++i) {
+    ChunkRec rec;
+    rec.tokens.assign(chunks[i], chunks[i] + lens[i]);
+    rec.blocks = blocks[i];
+    const pic_cache_id id = e->next_id++;
+    e->store.emplace(id, std::move(rec));
+    out_ids[i] = id;
+  }
+  return PIC_OK;
+}
+
+// ============================================================================ link
+struct ReqBuild {
+  LinkPlanHost p;
+  std::vector<int32_t> bt;
+};
+
+// Append one request's rows / tiles / K2 work to a forward.
+static void append_request(pic_engine* e, const pic_link_params* pr, ReqBuild& rb, int req, Fwd& f) {
+  const LinkPlanHost& p = rb.p;
+  const int qpt = qpt_of(e->cfg);
+  const int seq = (int)f.seq_bt_off.size();
+  f.seq_bt_off.push_back((int)f.bt.size());
+  f.bt.insert(f.bt.end(), rb.bt.begin(), rb.bt.end());
+  const bool cb = pr->alg == PIC_CACHEBLEND;
+  const std::vector<int32_t>* rows = &p.sel;
+  std::vector<int32_t> all;
+  if (cb) {
+    all.resize(p.N);
+    for (int i = 0; i < p.N; ++i) all[i] = i;
+    rows = &all;
+  }
+  const int r0 = f.M;
+  add_tiles(f.tiles, seq, r0, (int)rows->size(), qpt);
+  for (int32_t i : *rows) {
+    f.tok.push_back(p.tok[i]);
+    f.pos.push_back(i);  // p_i = i (R18)
+    f.slot.push_back(slot_of(rb.bt, i));
+    f.seq.push_back(seq);
+    f.head_map.push_back(-1);
+  }
+  f.M += (int)rows->size();
+  f.head_map[f.M - 1] = req;  // last row N−1 (always selected, R8)
+  // a2 work list: cached rows not recomputed (CacheBlend: all cached rows, from the check layer on)
+  std::vector<uint8_t> in_sel(p.N, 0);
+  if (!cb)
+    for (int32_t i : p.sel) in_sel[i] = 1;
+  for (size_t c = 0; c < p.chunk_start.size(); ++c) {
+    const ChunkRec& ch = e->store.at(p.chunk_id[c]);
+    for (int j = 0; j < p.chunk_len[c]; ++j) {
+      const int i = p.chunk_start[c] + j;
+      if (in_sel[i]) continue;
+      f.k2_src.push_back(slot_of(ch.blocks, j));
+      f.k2_dst.push_back(slot_of(rb.bt, i));
+      f.k2_delta.push_back(p.chunk_delta[c]);
+    }
+  }
+}
+
+static pic_status link_impl(pic_engine* e, int32_t n_req, const pic_segment* const* segs, const int32_t* n_segs,
+                            const pic_link_params* pr, void* stream, pic_linked** out_linked,
+                            pic_link_result* results) {
+  if (!e || !segs || !n_segs || !results) return fail(PIC_E_INVALID_ARG, "NULL argument");
+  if (n_req <= 0) return fail(PIC_E_EMPTY_INPUT, "no requests");
+  if (n_req > e->lim.max_requests) return fail(PIC_E_CAPACITY, "%d requests exceed max_requests", n_req);
+  TRY(check_params(pr));
+  const bool cb = pr->alg == PIC_CACHEBLEND;
+  if ((cb || pr->debug_hidden) && n_req != 1) return fail(PIC_E_VARIANT, "CacheBlend/debug hooks are single-request");
+  if (pr->sel_override && !cb) return fail(PIC_E_VARIANT, "sel_override is a CacheBlend hook");
+  if (e->host_only) return fail(PIC_E_NO_DEVICE, "host-only engine cannot link");
+  std::vector<ReqBuild> reqs(n_req);
+  int64_t need = 0;
+  for (int r = 0; r < n_req; ++r) {
+    TRY(assemble(e, segs[r], n_segs[r], reqs[r].p));
+    select_rows(pr, reqs[r].p);
+    need += (reqs[r].p.N + 15) / 16;
+  }
+  if (!e->alloc.can(need)) return fail(PIC_E_CAPACITY, "pool has %zu free blocks, link needs %lld",
+                                       e->alloc.free_ids.size(), (long long)need);
+  Fwd f;
+  f.rebase = pr->rebase;
+  f.n_head = n_req;
+  f.debug_rows = reqs[0].p.N;
+  for (int r = 0; r < n_req; ++r) reqs[r].bt = e->alloc.alloc((reqs[r].p.N + 15) / 16);
+  auto rollback = [&]() {
+    for (auto& rb : reqs) e->alloc.release(rb.bt);
+  };
+  for (int r = 0; r < n_req; ++r) append_request(e, pr, reqs[r], r, f);
+  if (cb) {
+    const LinkPlanHost& p = reqs[0].p;
+    const int N = p.N;
+    f.cb = pr->check_layer < e->cfg.n_layers;
+    f.cb_layer = pr->check_layer;
+    f.k2_layer0 = std::min(pr->check_layer, e->cfg.n_layers);
+    int n_cached = 0;
+    f.cb_cand.assign(N, 0);
+    f.cb_forced.assign(N, 0);
+    for (int i = 0; i < N; ++i) {
+      if (!p.dynamic[i]) ++n_cached;
+      f.cb_cand[i] = (!p.dynamic[i] && i != N - 1) ? 1 : 0;
+      f.cb_forced[i] = (p.dynamic[i] || i == N - 1) ? 1 : 0;
+    }
+    int n_cand = 0;
+    for (int i = 0; i < N; ++i) n_cand += f.cb_cand[i];
+    f.cb_T = std::min(n_cand, (int)(((int64_t)pr->r_percent * n_cached + 99) / 100));  // ⌈R·N_cached/100⌉ (R11)
+    if (!f.cb) {
+      // check layer beyond the model: every layer recomputes all rows (≡ FR)
+    } else if (pr->sel_override) {
+      if (pr->n_sel_override <= 0 || pr->n_sel_override > N) {
+        rollback();
+        return fail(PIC_E_INVALID_ARG, "bad n_sel_override");
+      }
+      f.cb_override = true;
+      for (int r = 0; r < pr->n_sel_override; ++r) {
+        const int i = pr->sel_override[r];
+        if (i < 0 || i >= N || (r && i <= pr->sel_override[r - 1])) {
+          rollback();
+          return fail(PIC_E_INVALID_ARG, "sel_override must be sorted distinct indices in [0,N)");
+        }
+        f.cb_sel2.push_back(i);
+        f.cb_pos2.push_back(i);
+        f.cb_slot2.push_back(slot_of(reqs[0].bt, i));
+      }
+      if (f.cb_sel2.back() != N - 1) {
+        rollback();
+        return fail(PIC_E_INVALID_ARG, "sel_override must contain the last row N-1");
+      }
+      f.M2 = pr->n_sel_override;
+    } else {
+      int n_forced = 0;
+      for (int i = 0; i < N; ++i) n_forced += f.cb_forced[i];
+      f.M2 = f.cb_T + n_forced;
+    }
+    if (f.cb) {
+      add_tiles(f.tiles2, 0, 0, f.M2, qpt_of(e->cfg));
+      f.head_map2.assign(f.M2, -1);
+      f.head_map2[f.M2 - 1] = 0;
+    }
+  }
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const bool use_graph = pr->use_graph != 0;
+  pic_status s = run_forward(e, f, st, use_graph, pr->debug_hidden);
+  if (s != PIC_OK) {
+    rollback();
+    return s;
+  }
+  const int V = e->cfg.vocab;
+  bool want_host = false;
+  for (int r = 0; r < n_req; ++r) {
+    if (results[r].logits_dev) {
+      cudaError_t ce = cudaMemcpyAsync(results[r].logits_dev, e->logits + (size_t)r * V, (size_t)V * 4,
+                                       cudaMemcpyDeviceToDevice, st);
+      if (ce != cudaSuccess) {
+        rollback();
+        return fail(PIC_E_CUDA, "logits copy: %s", cudaGetErrorString(ce));
+      }
+    }
+    if (results[r].logits || !results[r].logits_dev) want_host = true;
+  }
+  e->d2h_last = 0;
+  if (pr->debug_hidden) want_host = true;
+  for (int r = 0; r < n_req; ++r) want_host |= results[r].selected != nullptr;
+  std::vector<int32_t> cb_sel_host;
+  if (f.cb && results[0].selected) {
+    cb_sel_host.resize(f.M2);
+    cudaError_t ce = cudaMemcpyAsync(cb_sel_host.data(), e->last_cb_sel2, (size_t)f.M2 * 4,
+                                     cudaMemcpyDeviceToHost, st);
+    if (ce != cudaSuccess) {
+      rollback();
+      return fail(PIC_E_CUDA, "selection copy: %s", cudaGetErrorString(ce));
+    }
+  }
+  if (want_host) {
+    bool any_logits = false;
+    for (int r = 0; r < n_req; ++r) any_logits |= results[r].logits != nullptr;
+    cudaError_t ce = cudaSuccess;
+    if (any_logits) {
+      ce = cudaMemcpyAsync(e->host_logits, e->logits, (size_t)n_req * V * 4, cudaMemcpyDeviceToHost, st);
+      e->d2h_last += (int64_t)n_req * V * 4;
+    }
+    if (ce == cudaSuccess) ce = cudaMemcpyAsync(e->host_amax, e->amax, (size_t)n_req * 4, cudaMemcpyDeviceToHost, st);
+    e->d2h_last += (int64_t)n_req * 4;
+    if (ce == cudaSuccess) ce = cudaStreamSynchronize(st);
+    if (ce != cudaSuccess) {
+      rollback();
+      return fail(PIC_E_CUDA, "link: %s", cudaGetErrorString(ce));
+    }
+  }
+  for (int r = 0; r < n_req; ++r) {
+    pic_link_result& res = results[r];
+    res.n_tokens = reqs[r].p.N;
+    res.n_selected_layer0 = cb ? reqs[r].p.N : (int)reqs[r].p.sel.size();
+    res.n_selected = cb ? (f.cb ? f.M2 : reqs[r].p.N) : (int)reqs[r].p.sel.size();
+    res.first_token = want_host ? e->host_amax[r] : -1;
+    if (res.logits) std::memcpy(res.logits, e->host_logits + (size_t)r * V, (size_t)V * 4);
+    if (res.selected) {
+      if (f.cb)
+        std::copy(cb_sel_host.begin(), cb_sel_host.end(), res.selected);
+      else if (cb)
+        for (int i = 0; i < reqs[r].p.N; ++i) res.selected[i] = i;
+      else
+        std::copy(reqs[r].p.sel.begin(), reqs[r].p.sel.end(), res.selected);
+    }
+    if (out_linked) {
+      pic_linked* h = new (std::nothrow) pic_linked();
+      if (!h) {
+        rollback();
+        return fail(PIC_E_OOM, "linked handle");
+      }
+      h->n_tokens = reqs[r].p.N;
+      h->blocks = reqs[r].bt;
+      out_linked[r] = h;
+    } else {
+      e->alloc.release(reqs[r].bt);  // stream-ordered reuse on the same stream
+    }
+  }
+  return PIC_OK;
+}
+
+extern "C" pic_status pic_link(pic_engine* e, const pic_segment* segs, int32_t n_segs, const pic_link_params* params,
+                               void* stream, pic_linked** out_linked, pic_link_result* result) {
+  return link_impl(e, 1, &segs, &n_segs, params, stream, out_linked, result);
+}
+
+extern "C" pic_status pic_link_batch(pic_engine* e, int32_t n_req, const pic_segment* const* segs,
+                                     const int32_t* n_segs, const pic_link_params* params, void* stream,
+                                     pic_linked** out_linked, pic_link_result* results) {
+  return link_impl(e, n_req, segs, n_segs, params, stream, out_linked, results);
+}
+
+// ============================================================================ exports / lifecycle
+static pic_status export_rows(pic_engine* e, const std::vector<int32_t>& blocks, int n, int layer, void* k_host,
+                              void* v_host) {
+  if (e->host_only) return fail(PIC_E_NO_DEVICE, "host-only engine");
+  if (layer < 0 || layer >= e->cfg.n_layers) return fail(PIC_E_INVALID_ARG, "layer out of range");
+  const int Hkv = e->cfg.n_kv_heads, D = e->cfg.head_dim;
+  const size_t row = (size_t)D * 2;
+  std::vector<uint16_t> kb((size_t)n * Hkv * D), vb((size_t)n * Hkv * D);
+  CK(cudaDeviceSynchronize());
+  for (int i = 0; i < n; ++i)
+    for (int g = 0; g < Hkv; ++g) {
+      const size_t src = (size_t)layer * e->layer_stride + (((size_t)blocks[i / 16] * Hkv + g) * 16 + i % 16) * D;
+      if (k_host)
+        CK(cudaMemcpy(reinterpret_cast<char*>(k_host) + ((size_t)i * Hkv + g) * row,
+                      reinterpret_cast<char*>(e->Kpool) + src * 2, row, cudaMemcpyDeviceToHost));
+      if (v_host)
+        CK(cudaMemcpy(reinterpret_cast<char*>(v_host) + ((size_t)i * Hkv + g) * row,
+                      reinterpret_cast<char*>(e->Vpool) + src * 2, row, cudaMemcpyDeviceToHost));
+    }
+  return PIC_OK;
+}
+
+extern "C" pic_status pic_linked_export(pic_engine* e, const pic_linked* h, int32_t layer, void* k_host, void* v_host) {
+  if (!e || !h) return fail(PIC_E_INVALID_ARG, "NULL argument");
+  return export_rows(e, h->blocks, h->n_tokens, layer, k_host, v_host);
+}
+
+extern "C" pic_status pic_linked_info(pic_engine* e, const pic_linked* h, int32_t* n_tokens, int32_t* block_table) {
+  if (!e || !h) return fail(PIC_E_INVALID_ARG, "NULL argument");
+  if (n_tokens) *n_tokens = h->n_tokens;
+  if (block_table) std::copy(h->blocks.begin(), h->blocks.end(), block_table);
+  return PIC_OK;
+}
+
+extern "C" pic_status pic_linked_release(pic_engine* e, pic_linked* h) {
+  if (!e || !h) return fail(PIC_E_INVALID_ARG, "NULL argument");
+  e->alloc.release(h->blocks);
+  delete h;
+  return PIC_OK;
+}
+
+extern "C" pic_status pic_cache_export(pic_engine* e, pic_cache_id id, int32_t layer, void* k_host, void* v_host) {
+  if (!e) return fail(PIC_E_INVALID_ARG, "NULL engine");
+  auto it = e->store.find(id);
+  if (it == e->store.end()) return fail(PIC_E_MISSING_CACHE, "unknown cache id %llu", (unsigned long long)id);
+  return export_rows(e, it->second.blocks, (int)it->second.tokens.size(), layer, k_host, v_host);
+}
+
+extern "C" pic_status pic_cache_info(pic_engine* e, pic_cache_id id, int32_t* n_tokens, int32_t* blocks) {
+  if (!e) return fail(PIC_E_INVALID_ARG, "NULL engine");
+  auto it = e->store.find(id);
+  if (it == e->store.end()) return fail(PIC_E_MISSING_CACHE, "unknown cache id %llu", (unsigned long long)id);
+  if (n_tokens) *n_tokens = (int32_t)it->second.tokens.size();
+  if (blocks) std::copy(it->second.blocks.begin(), it->second.blocks.end(), blocks);
+  return PIC_OK;
+}
+
+extern "C" pic_status pic_expire_cache(pic_engine* e, pic_cache_id id, int32_t* was_present) {
+  if (!e) return fail(PIC_E_INVALID_ARG, "NULL engine");
+  auto it = e->store.find(id);
+  if (was_present) *was_present = it != e->store.end();
+  if (it != e->store.end()) {
+    e->alloc.release(it->second.blocks);
+    e->store.erase(it);
+  }
+  return PIC_OK;
+}
+
+extern "C" pic_status pic_read_weights(pic_engine* e, int32_t which, int32_t layer, int64_t row0, int64_t nrows,
+                                       void* host_out) {
+  if (!e || !host_out) return fail(PIC_E_INVALID_ARG, "NULL argument");
+  if (e->host_only) return fail(PIC_E_NO_DEVICE, "host-only engine");
+  const pic_model_config& c = e->cfg;
+  const int64_t d = c.d_model, D = c.head_dim, Hq = c.n_heads, Hkv = c.n_kv_heads, F = c.ffn_dim;
+  if (which <= 6 && (layer < 0 || layer >= c.n_layers)) return fail(PIC_E_INVALID_ARG, "layer out of range");
+  const char* base = nullptr;
+  int64_t rows = 0, cols = 0;
+  const LayerW* w = which <= 6 || which == 9 || which == 10 ? &e->layers[std::max(0, std::min(layer, c.n_layers - 1))]
+                                                            : nullptr;
+  switch (which) {
+    case 0: base = (const char*)w->qkv; rows = Hq * D; cols = d; break;
+    case 1: base = (const char*)w->qkv + Hq * D * d * 2; rows = Hkv * D; cols = d; break;
+    case 2: base = (const char*)w->qkv + (Hq + Hkv) * D * d * 2; rows = Hkv * D; cols = d; break;
+    case 3: base = (const char*)w->o; rows = d; cols = Hq * D; break;
+    case 4: base = (const char*)w->gu; rows = F; cols = d; break;
+    case 5: base = (const char*)w->gu + F * d * 2; rows = F; cols = d; break;
+    case 6: base = (const char*)w->down; rows = d; cols = F; break;
+    case 7: base = (const char*)e->E; rows = c.vocab; cols = d; break;
+    case 8: base = (const char*)e->Wlm; rows = c.vocab; cols = d; break;
+    case 9: CK(cudaMemcpy(host_out, w->g1, d * 4, cudaMemcpyDeviceToHost)); return PIC_OK;
+    case 10: CK(cudaMemcpy(host_out, w->g2, d * 4, cudaMemcpyDeviceToHost)); return PIC_OK;
+    case 11: CK(cudaMemcpy(host_out, e->gf, d * 4, cudaMemcpyDeviceToHost)); return PIC_OK;
+    default: return fail(PIC_E_INVALID_ARG, "bad weight id %d", which);
+  }
+  if (row0 < 0 || nrows < 0 || row0 + nrows > rows) return fail(PIC_E_INVALID_ARG, "row range out of bounds");
+  CK(cudaDeviceSynchronize());
+  CK(cudaMemcpy(host_out, base + row0 * cols * 2, nrows * cols * 2, cudaMemcpyDeviceToHost));
+  return PIC_OK;
+}
+
+extern "C" pic_status pic_get_stats(pic_engine* e, pic_stats* out) {
+  if (!e || !out) return fail(PIC_E_INVALID_ARG, "NULL argument");
+  out->free_blocks = (int64_t)e->alloc.free_ids.size();
+  out->total_blocks = e->lim.num_blocks;
+  out->n_cached_chunks = (int64_t)e->store.size();
+  out->kernels_last_call = e->kernels_last;
+  out->graphs_cached = (int64_t)e->graphs.size();
+  out->h2d_bytes_last_call = e->h2d_last;
+  out->d2h_bytes_last_call = e->d2h_last;
+  return PIC_OK;
+}

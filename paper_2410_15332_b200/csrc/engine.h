@@ -1,0 +1,136 @@
+// engine.h — internal state of a pic_engine (libpic.so).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <map>
+#include <set>
+#include <string>
+#include <vector>
+
+#include "../../include/pic.h"
+#include "kernels/kernels.h"
+
+namespace pic {
+
+// Deterministic paged-block allocator: lowest free ids first (D3; modelled by oracle.pic.BlockAllocator).
+struct BlockAllocator {
+  std::set<int32_t> free_ids;
+  void reset(int64_t n) {
+    free_ids.clear();
+    for (int64_t i = 0; i < n; ++i) free_ids.insert(free_ids.end(), (int32_t)i);
+  }
+  bool can(int64_t n) const { return (int64_t)free_ids.size() >= n; }
+  std::vector<int32_t> peek(int64_t n) const {
+    std::vector<int32_t> v;
+    for (auto it = free_ids.begin(); it != free_ids.end() && (int64_t)v.size() < n; ++it) v.push_back(*it);
+    return v;
+  }
+  std::vector<int32_t> alloc(int64_t n) {
+    std::vector<int32_t> v = peek(n);
+    for (int32_t b : v) free_ids.erase(b);
+    return v;
+  }
+  void release(const std::vector<int32_t>& v) {
+    for (int32_t b : v) free_ids.insert(b);
+  }
+};
+
+struct ChunkRec {
+  std::vector<int32_t> tokens;
+  std::vector<int32_t> blocks;
+  int32_t c0 = 0;  // compile position of row 0 (0; LegoLink-0 would use the dummy-prefix length)
+};
+
+struct LayerW {
+  void *qkv, *o, *gu, *down;  // bf16 [out][in]
+  float *g1, *g2;
+  CUtensorMap tm_qkv[3], tm_o[3], tm_gu[3], tm_down[3];  // per GEMM N-tile (64/128/256)
+};
+
+// One forward over a set of rows (a compile batch, one link or a batched link).
+struct Fwd {
+  int M = 0;                                  // rows recomputed at layer 0
+  std::vector<int32_t> tok, pos, slot, seq;   // per row
+  std::vector<int32_t> tiles;                 // attention q-tiles: (seq, row_start, row_count)
+  std::vector<int32_t> seq_bt_off, bt;        // block tables (concatenated)
+  std::vector<int32_t> k2_src, k2_dst, k2_delta;  // a2 work: cached rows gathered into linked blocks
+  int k2_layer0 = 0;
+  std::vector<int32_t> head_map;              // per final row: request index or -1
+  int n_head = 0;                             // requests producing logits (0 = compile)
+  bool compile = false;
+  int rebase = 1;
+  int debug_rows = 0;                         // row stride of the debug_hidden capture (N)
+  // CacheBlend (single request)
+  bool cb = false;
+  int cb_layer = 1, cb_T = 0, M2 = 0;
+  bool cb_override = false;
+  std::vector<int32_t> cb_cand, cb_forced, cb_sel2, cb_pos2, cb_slot2, tiles2, head_map2;
+};
+
+// Per-request link bookkeeping produced by the planner.
+struct LinkPlanHost {
+  int N = 0;
+  std::vector<int32_t> tok;
+  std::vector<int32_t> src_cid, src_row;       // -1 for dynamic rows
+  std::vector<int32_t> chunk_start, chunk_len, chunk_delta;
+  std::vector<uint64_t> chunk_id;
+  std::vector<uint8_t> dynamic;
+  std::vector<int32_t> sel;                    // sorted selected rows (pre-CacheBlend: dynamic ∪ {N-1})
+};
+
+}  // namespace pic
+
+struct pic_linked {
+  int32_t n_tokens = 0;
+  std::vector<int32_t> blocks;
+};
+
+struct pic_engine {
+  pic_model_config cfg{};
+  pic_engine_limits lim{};
+  int device = -1;
+  bool host_only = true;
+  int max_seqs = 0, max_tiles = 0, max_bt = 0, max_k2 = 0;
+  // arena
+  char* arena = nullptr;
+  size_t arena_bytes = 0;
+  // weights
+  std::vector<pic::LayerW> layers;
+  void *E = nullptr, *Wlm = nullptr;
+  float* gf = nullptr;
+  CUtensorMap tm_lm[3];
+  float *cos_t = nullptr, *sin_t = nullptr;
+  // paged KV pools [L][NB][Hkv][16][D] bf16
+  void *Kpool = nullptr, *Vpool = nullptr;
+  int64_t layer_stride = 0;  // elements per layer per pool
+  CUtensorMap tm_K, tm_V;
+  // activations / workspaces
+  float *h = nullptr, *h2 = nullptr, *ws = nullptr;
+  size_t ws_floats = 0;
+  void *x = nullptr, *Obuf = nullptr, *u = nullptr, *Q = nullptr, *x_last = nullptr;
+  float *o_part = nullptr, *ml_part = nullptr;
+  int attn_rows_cap = 0;  // max splits*M of the attention partials
+  float* logits = nullptr;
+  int32_t* amax = nullptr;
+  float* cb_dev = nullptr;
+  CUtensorMap tm_x, tm_O, tm_u, tm_xlast, tm_Q;  // A operands (128-row boxes), Q (attention)
+  // plan buffers
+  int32_t* plan_dev = nullptr;
+  int32_t* plan_host = nullptr;  // pinned staging
+  size_t plan_cap_ints = 0;
+  cudaEvent_t plan_ev = nullptr;
+  float* host_logits = nullptr;  // pinned
+  int32_t* host_amax = nullptr;  // pinned
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaStream_t cap_stream = nullptr;
+  int32_t* last_cb_sel2 = nullptr;  // device: CacheBlend selection of the last forward
+  // store
+  std::map<pic_cache_id, pic::ChunkRec> store;
+  uint64_t next_id = 1;
+  pic::BlockAllocator alloc;
+  // graphs
+  std::map<std::vector<int64_t>, cudaGraphExec_t> graphs;
+  // stats
+  int64_t kernels_last = 0, h2d_last = 0, d2h_last = 0;
+};

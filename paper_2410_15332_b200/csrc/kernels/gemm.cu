@@ -1,0 +1,158 @@
+// gemm.cu — tcgen05 / TMEM / TMA GEMM for the projections of the recomputed rows.
+//
+//   P[split][m][n] = Σ_{k in split} A[m][k] · B[n][k]        (A = activations, B = weights [out][in])
+//
+// Used for a5 (x·W_qkvᵀ, "Q = EW_Q, K = EW_K, V = EW_V"), a7 (O·W_oᵀ, "O = A V_exp W_O"),
+// a8 (gate/up and down projections) and a10 (LM head).  Only the k' recomputed rows enter
+// (recomputation is O(k'), not O(N)).
+//
+// Warp roles (one CTA per SM, 192 threads):
+//   warp 0      TMA producer: A tile [128 x 64] and B tile [BN x 64] per stage, SWIZZLE_128B
+//   warp 1      MMA issuer:   4 x tcgen05.mma (M=128, N=BN, K=16) per stage, fp32 accumulator in TMEM
+//   warps 2..5  epilogue:     tcgen05.ld 32x32b rows -> fp32 partial sums in HBM
+// Split-K across blockIdx.z fills all 148 SMs when M is skinny (cfg2: M = k' = 128); the partials
+// are summed by the fused epilogue kernels (RMSNorm / RoPE+scatter / SwiGLU / argmax), so the
+// reduction order is fixed and the result deterministic.
+#include <cuda.h>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace pic {
+
+template <int BN, int STAGES>
+struct GemmSmem {
+  static constexpr int kA = 128 * 64 * 2;  // 16 KB
+  static constexpr int kB = BN * 64 * 2;
+  static constexpr int kStage = kA + kB;
+  static constexpr int kBars = 2 * STAGES + 1;
+  static constexpr int kBytes = STAGES * kStage + kBars * 8 + 16 + 1024;  // + alignment slack
+};
+
+template <int BN, int STAGES>
+__global__ void __launch_bounds__(192, 1)
+    gemm_bf16_partial_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                             float* __restrict__ out, int M, int N, int kblk_total, int kblk_per_split) {
+  using S = GemmSmem<BN, STAGES>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * S::kA;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * S::kStage);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + S::kBars);
+  const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + STAGES), accf = smem_u32(bars + 2 * STAGES);
+
+  const int warp = warp_id(), lane = lane_id();
+  const int n0 = blockIdx.x * BN, m0 = blockIdx.y * 128;
+  const int kb0 = blockIdx.z * kblk_per_split;
+  const int nkb = min(kblk_per_split, kblk_total - kb0);
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(full0 + 8 * s, 1);
+      mbar_init(empty0 + 8 * s, 1);
+    }
+    mbar_init(accf, 1);
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc(smem_u32(tmem_slot), BN);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0 && nkb > 0) {
+      tma_prefetch(&tmA);
+      tma_prefetch(&tmB);
+      for (int i = 0; i < nkb; ++i) {
+        const int s = i % STAGES;
+        const uint32_t ph = (i / STAGES) & 1;
+        mbar_wait(empty0 + 8 * s, ph ^ 1);
+        mbar_expect_tx(full0 + 8 * s, S::kStage);
+        const int kc = (kb0 + i) * 64;
+        tma_load_2d(smem_u32(sA + s * S::kA), &tmA, full0 + 8 * s, kc, m0);
+        tma_load_2d(smem_u32(sB + s * S::kB), &tmB, full0 + 8 * s, kc, n0);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && nkb > 0) {
+      constexpr uint32_t idesc = idesc_bf16(128, BN, 0, 0);
+      for (int i = 0; i < nkb; ++i) {
+        const int s = i % STAGES;
+        const uint32_t ph = (i / STAGES) & 1;
+        mbar_wait(full0 + 8 * s, ph);
+        tc_fence_after();
+        const uint32_t a = smem_u32(sA + s * S::kA), b = smem_u32(sB + s * S::kB);
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          umma_bf16(tmem, sdesc_sw128(a + kk * 32, 16, 1024), sdesc_sw128(b + kk * 32, 16, 1024), idesc,
+                    (i | kk) != 0);
+        umma_commit(empty0 + 8 * s);
+      }
+      umma_commit(accf);
+    }
+  } else {
+    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    const int row = m0 + q * 32 + lane;
+    float* orow = out + (size_t)blockIdx.z * M * N + (size_t)row * N;
+    if (nkb > 0) {
+      mbar_wait(accf, 0);
+      tc_fence_after();
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        float v[32];
+        tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + c * 32, v);
+        const int col = n0 + c * 32;
+        if (row < M && col < N) {
+          float4* dst = reinterpret_cast<float4*>(orow + col);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) dst[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+        }
+      }
+    } else if (row < M) {
+      for (int col = n0; col < min(N, n0 + BN); col += 4)
+        *reinterpret_cast<float4*>(orow + col) = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem, BN);
+  }
+}
+
+template <int BN, int STAGES>
+static cudaError_t launch_gemm_t(const CUtensorMap& A, const CUtensorMap& B, float* out, int M, int N, int K,
+                                 int splits, cudaStream_t st) {
+  using S = GemmSmem<BN, STAGES>;
+  auto kern = gemm_bf16_partial_kernel<BN, STAGES>;
+  const int kblk = K / 64;
+  const int per = (kblk + splits - 1) / splits;
+  dim3 grid((N + BN - 1) / BN, (M + 127) / 128, splits);
+  kern<<<grid, 192, S::kBytes, st>>>(A, B, out, M, N, kblk, per);
+  return cudaGetLastError();
+}
+
+template <int BN, int STAGES>
+static cudaError_t prep_t() {
+  return cudaFuncSetAttribute(gemm_bf16_partial_kernel<BN, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              GemmSmem<BN, STAGES>::kBytes);
+}
+
+cudaError_t prepare_gemm() {
+  cudaError_t e = prep_t<256, 4>();
+  if (e == cudaSuccess) e = prep_t<128, 6>();
+  if (e == cudaSuccess) e = prep_t<64, 8>();
+  return e;
+}
+
+cudaError_t launch_gemm_partial(const CUtensorMap& A, const CUtensorMap& B, float* out, int M, int N, int K,
+                                int splits, int bn, cudaStream_t st) {
+  if (bn == 256) return launch_gemm_t<256, 4>(A, B, out, M, N, K, splits, st);
+  if (bn == 64) return launch_gemm_t<64, 8>(A, B, out, M, N, K, splits, st);
+  return launch_gemm_t<128, 6>(A, B, out, M, N, K, splits, st);
+}
+
+}  // namespace pic

@@ -1,0 +1,82 @@
+// kernels.h — host launchers of the sm_100a kernels (internal to libpic.so, C++ linkage).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace pic {
+
+// Set dynamic-smem attributes of every kernel instance (call once, outside graph capture).
+cudaError_t prepare_kernels();
+
+// ---- K15 weight generator, bit-exact with seedgen/ -------------------------
+// dst[r][c] = bf16( bf16_rne(f(U(seed, tag, (row0 + r) * cols + c))) * 2^exp2 ), r < rows.
+cudaError_t launch_gen_matrix(void* dst_bf16, int64_t rows, int64_t cols, uint64_t seed, uint64_t tag, int exp2,
+                              int64_t row0, cudaStream_t st);
+// dst[i] = 1 + ((U(seed, tag, i) >> 61) - 4) / 32   (fp32)
+cudaError_t launch_gen_gains(float* dst, int64_t n, uint64_t seed, uint64_t tag, cudaStream_t st);
+
+// ---- a3: embed gather ----------------------------------------------------------------------
+cudaError_t launch_embed(const void* E, const int32_t* tok, float* h, int M, int d, cudaStream_t st);
+
+// ---- a4: residual add of split-K partials + RMSNorm ----------------------------------------
+// h[r] += Σ_s P[s][r] (P nullable); if x: x[out_map ? out_map[r] : r] = bf16(rms(h[r]) ⊙ g) for out_map[r] >= 0
+cudaError_t launch_residual_rmsnorm(float* h, const float* P, int splits, const float* g, void* x,
+                                    const int32_t* out_map, int M, int d, float eps, cudaStream_t st);
+
+// ---- a5 epilogue: Σ partials, RoPE at row positions, Q dense, K/V scattered to the paged pool
+cudaError_t launch_qkv_rope_scatter(const float* P, int splits, int P_rows, const int32_t* src_row,
+                                    const int32_t* pos, const int32_t* slot, const float* cos_t, const float* sin_t,
+                                    void* Q, void* Kpool_l, void* Vpool_l, int M, int Hq, int Hkv, int D,
+                                    cudaStream_t st);
+
+// ---- a8 epilogue: u = bf16(silu(Σ gate) ⊙ Σ up) ----------------------------------------------
+cudaError_t launch_swiglu(const float* P, int splits, void* u, int M, int F, cudaStream_t st);
+
+// ---- a2: KV link — gather cached rows into the linked blocks, RoPE re-base K by Δ -----------
+cudaError_t launch_kv_link(void* Kpool, void* Vpool, const int32_t* src_slot, const int32_t* dst_slot,
+                           const int32_t* delta, int n_rows, int layer0, int n_layers, int64_t layer_stride_elems,
+                           int Hkv, int D, const float* cos_t, const float* sin_t, int rebase, cudaStream_t st);
+
+// ---- GEMM (tcgen05): P[split][M][N] = A[M][K] · B[N][K]^T --------------------------------------
+cudaError_t launch_gemm_partial(const CUtensorMap& A, const CUtensorMap& B, float* out, int M, int N, int K,
+                                int splits, int bn, cudaStream_t st);
+
+// ---- a6: sparse-query causal attention (tcgen05, D = 128) + split-KV combine ----------------
+struct AttnArgs {
+  const int32_t* tiles;      // [n_tiles][3] (seq, row_start, row_count)
+  const int32_t* seq_bt_off; // per sequence: offset into bt
+  const int32_t* bt;         // block tables
+  const int32_t* row_pos;    // [M] absolute position of every query row
+  int n_tiles, M, Hq, Hkv, layer, num_blocks, n_splits;
+  float scale_log2;
+  float* o_part;             // [n_splits][M][Hq][128]
+  float* ml_part;            // [n_splits][M][Hq][2]
+};
+cudaError_t launch_attention_tc(const CUtensorMap& tmQ, const CUtensorMap& tmK, const CUtensorMap& tmV,
+                                const AttnArgs& a, cudaStream_t st);
+cudaError_t launch_attn_combine(const float* o_part, const float* ml_part, void* O, int M, int Hq, int D,
+                                int n_splits, cudaStream_t st);
+// generic-D SIMT attention (tiny shapes, D in {16,32,64}); writes O bf16 directly
+cudaError_t launch_attention_simt(const void* Q, const void* Kpool_l, const void* Vpool_l, const int32_t* row_seq,
+                                  const int32_t* seq_bt_off, const int32_t* bt, const int32_t* row_pos, void* O,
+                                  int M, int Hq, int Hkv, int D, float scale, cudaStream_t st);
+
+// ---- a10: Σ LM-head partials, fp32 logits, argmax (ties -> lowest id) -----------------------
+cudaError_t launch_logits_argmax(const float* P, int splits, float* logits, int32_t* argmax, int n_req, int V,
+                                 cudaStream_t st);
+
+// ---- a9: CacheBlend (check layer) -------------------------------------------------------------
+// dev[i] = ||RoPE(Σk)_i − K_lnk[i]||² + ||Σv_i − V_lnk[i]||² for candidate rows (cand[i] != 0), else −1
+cudaError_t launch_cb_deviation(const float* P, int splits, const int32_t* cand, const int32_t* slot,
+                                const float* cos_t, const float* sin_t, const void* Kpool_l, const void* Vpool_l,
+                                float* dev, int N, int Hq, int Hkv, int D, cudaStream_t st);
+// keep[i] = cand[i] && rank_i < T, rank by (dev desc, index asc)
+cudaError_t launch_cb_rank(const float* dev, int32_t* keep, int N, int T, cudaStream_t st);
+// sel = sorted {i : keep[i] || forced[i]}; pos = sel; slot = bt[sel/16]*16 + sel%16; writes count
+cudaError_t launch_cb_compact(const int32_t* keep, const int32_t* forced, const int32_t* bt, int32_t* sel,
+                              int32_t* pos, int32_t* slot, int32_t* count, int N, cudaStream_t st);
+// dst[r] = src[idx[r]] rows of d floats
+cudaError_t launch_gather_rows(const float* src, const int32_t* idx, float* dst, int M, int d, cudaStream_t st);
+
+}  // namespace pic

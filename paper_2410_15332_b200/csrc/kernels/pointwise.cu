@@ -1,0 +1,502 @@
+// pointwise.cu — HBM-bound kernels of the linked-prefill path: weight generator, embed gather,
+// residual+RMSNorm, QKV RoPE/scatter epilogue, SwiGLU epilogue, KV link (gather + RoPE re-base),
+// LM-head argmax and the CacheBlend selection kernels.  All use 16-byte vector accesses on the
+// contiguous dimension and are launched with grids sized from the row counts.
+#include <algorithm>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace pic {
+
+cudaError_t prepare_gemm();
+cudaError_t prepare_attention();
+cudaError_t prepare_kernels() {
+  cudaError_t e = prepare_gemm();
+  return e == cudaSuccess ? prepare_attention() : e;
+}
+
+// ================================================================================ generator
+PIC_DEV uint64_t sm64(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  uint64_t z = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+static uint64_t sm64_host(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  uint64_t z = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+static uint64_t stream_key(uint64_t seed, uint64_t tag) { return sm64_host(seed ^ (tag * 0xD1B54A32D192ED03ull)); }
+
+// bf16 bits of  bf16_rne((U>>40)·2^-23 − 1) · 2^e   (exact: the power-of-two scale keeps bf16 values)
+PIC_DEV uint16_t gen_weight_bits(uint64_t key, uint64_t idx, float scale) {
+  const uint64_t u = sm64(key + idx);
+  const float f = (float)(uint32_t)(u >> 40) * (1.0f / 8388608.0f) - 1.0f;
+  uint32_t b = __float_as_uint(f);
+  b = (b + 0x7FFFu + ((b >> 16) & 1u)) & 0xFFFF0000u;
+  const float w = __uint_as_float(b) * scale;
+  return (uint16_t)(__float_as_uint(w) >> 16);
+}
+
+__global__ void gen_matrix_kernel(uint16_t* __restrict__ dst, int64_t n8, int64_t base, uint64_t key, float scale) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n8; i += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t w[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const uint64_t c = (uint64_t)(base + 8 * i + 2 * j);
+      w[j] = (uint32_t)gen_weight_bits(key, c, scale) | ((uint32_t)gen_weight_bits(key, c + 1, scale) << 16);
+    }
+    reinterpret_cast<uint4*>(dst)[i] = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+}
+
+cudaError_t launch_gen_matrix(void* dst, int64_t rows, int64_t cols, uint64_t seed, uint64_t tag, int exp2,
+                              int64_t row0, cudaStream_t st) {
+  const int64_t n = rows * cols;
+  if (n % 8) return cudaErrorInvalidValue;
+  const float scale = ldexpf(1.0f, exp2);
+  gen_matrix_kernel<<<148 * 8, 256, 0, st>>>(reinterpret_cast<uint16_t*>(dst), n / 8, row0 * cols,
+                                             stream_key(seed, tag), scale);
+  return cudaGetLastError();
+}
+
+__global__ void gen_gains_kernel(float* dst, int64_t n, uint64_t key) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t u = sm64(key + (uint64_t)i);
+    dst[i] = 1.0f + ((float)(int)(u >> 61) - 4.0f) / 32.0f;
+  }
+}
+
+cudaError_t launch_gen_gains(float* dst, int64_t n, uint64_t seed, uint64_t tag, cudaStream_t st) {
+  gen_gains_kernel<<<64, 256, 0, st>>>(dst, n, stream_key(seed, tag));
+  return cudaGetLastError();
+}
+
+// ================================================================================ a3 embed
+// h[r] = fp32(E[tok[r]])  (P:213 step 1: "the embedding matrix E (with shape (k', d))")
+__global__ void embed_kernel(const uint16_t* __restrict__ E, const int32_t* __restrict__ tok, float* __restrict__ h,
+                             int d) {
+  const int r = blockIdx.x;
+  const uint4* src = reinterpret_cast<const uint4*>(E + (size_t)tok[r] * d);
+  float4* dst = reinterpret_cast<float4*>(h + (size_t)r * d);
+  for (int i = threadIdx.x; i < d / 8; i += blockDim.x) {
+    const uint4 v = src[i];
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+    dst[2 * i] = make_float4(__uint_as_float(w[0] << 16), __uint_as_float(w[0] & 0xFFFF0000u),
+                             __uint_as_float(w[1] << 16), __uint_as_float(w[1] & 0xFFFF0000u));
+    dst[2 * i + 1] = make_float4(__uint_as_float(w[2] << 16), __uint_as_float(w[2] & 0xFFFF0000u),
+                                 __uint_as_float(w[3] << 16), __uint_as_float(w[3] & 0xFFFF0000u));
+  }
+}
+
+cudaError_t launch_embed(const void* E, const int32_t* tok, float* h, int M, int d, cudaStream_t st) {
+  if (M == 0) return cudaSuccess;
+  embed_kernel<<<M, 128, 0, st>>>(reinterpret_cast<const uint16_t*>(E), tok, h, d);
+  return cudaGetLastError();
+}
+
+// ================================================================================ a4 RMSNorm
+template <int NT>
+PIC_DEV float block_sum(float v, float* red) {
+  v = warp_sum(v);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  float t = 0.f;
+#pragma unroll
+  for (int i = 0; i < NT / 32; ++i) t += red[i];
+  __syncthreads();
+  return t;
+}
+
+// h[r] += Σ_s P[s][r];  x[out] = bf16(h · rsqrt(mean h² + ε) · g)   (reading R4, fp32 residual R15)
+__global__ void __launch_bounds__(256) residual_rmsnorm_kernel(float* __restrict__ h, const float* __restrict__ P,
+                                                                int splits, const float* __restrict__ g,
+                                                                uint16_t* __restrict__ x,
+                                                                const int32_t* __restrict__ out_map, int M, int d,
+                                                                float eps) {
+  __shared__ float red[8];
+  const int r = blockIdx.x;
+  float4* hr = reinterpret_cast<float4*>(h + (size_t)r * d);
+  const int n4 = d / 4;
+  float ss = 0.f;
+  for (int i = threadIdx.x; i < n4; i += 256) {
+    float4 v = hr[i];
+    for (int s = 0; s < splits; ++s) {
+      const float4 p = reinterpret_cast<const float4*>(P + ((size_t)s * M + r) * d)[i];
+      v.x += p.x;
+      v.y += p.y;
+      v.z += p.z;
+      v.w += p.w;
+    }
+    if (splits) hr[i] = v;
+    ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+  }
+  if (!x) return;
+  const int orow = out_map ? out_map[r] : r;
+  ss = block_sum<256>(ss, red);
+  if (orow < 0) return;
+  const float inv = rsqrtf(ss / d + eps);
+  uint2* xr = reinterpret_cast<uint2*>(x + (size_t)orow * d);
+  const float4* g4 = reinterpret_cast<const float4*>(g);
+  for (int i = threadIdx.x; i < n4; i += 256) {
+    const float4 v = hr[i], w = g4[i];
+    xr[i] = make_uint2(pack_bf16(v.x * inv * w.x, v.y * inv * w.y), pack_bf16(v.z * inv * w.z, v.w * inv * w.w));
+  }
+}
+
+cudaError_t launch_residual_rmsnorm(float* h, const float* P, int splits, const float* g, void* x,
+                                    const int32_t* out_map, int M, int d, float eps, cudaStream_t st) {
+  if (M == 0) return cudaSuccess;
+  residual_rmsnorm_kernel<<<M, 256, 0, st>>>(h, P, P ? splits : 0, g, reinterpret_cast<uint16_t*>(x), out_map, M, d,
+                                             eps);
+  return cudaGetLastError();
+}
+
+// ================================================================================ a5 epilogue
+PIC_DEV float sum_partials(const float* P, int splits, size_t split_stride, size_t off) {
+  float a = 0.f;
+  for (int s = 0; s < splits; ++s) a += P[s * split_stride + off];
+  return a;
+}
+
+// Q = RoPE(Σ q, p), K = RoPE(Σ k, p) -> pool slot, V = Σ v -> pool slot  (P:213 steps 2-3; written
+// BEFORE attention so the selected rows also see each other)
+__global__ void qkv_rope_scatter_kernel(const float* __restrict__ P, int splits, int P_rows,
+                                        const int32_t* __restrict__ src_row, const int32_t* __restrict__ pos,
+                                        const int32_t* __restrict__ slot, const float* __restrict__ cos_t,
+                                        const float* __restrict__ sin_t, __nv_bfloat16* __restrict__ Q,
+                                        __nv_bfloat16* __restrict__ Kp, __nv_bfloat16* __restrict__ Vp, int Hq,
+                                        int Hkv, int D) {
+  const int r = blockIdx.x;
+  const int srow = src_row ? src_row[r] : r;
+  const int p = pos[r];
+  const int sl = slot[r];
+  const int half = D / 2;
+  const int ncol = (Hq + 2 * Hkv) * D;
+  const size_t sstride = (size_t)P_rows * ncol;
+  const float* prow = P + (size_t)srow * ncol;
+  const float* cs = cos_t + (size_t)p * half;
+  const float* sn = sin_t + (size_t)p * half;
+  const int qpairs = Hq * half, kpairs = Hkv * half;
+  const size_t kv_base = ((size_t)(sl / 16) * Hkv) * 16 * D + (size_t)(sl % 16) * D;  // + g*16*D + d
+  for (int t = threadIdx.x; t < qpairs + kpairs; t += blockDim.x) {
+    const bool isq = t < qpairs;
+    const int u = isq ? t : t - qpairs;
+    const int hd = u / half, j = u % half;
+    const int col = (isq ? 0 : Hq * D) + hd * D + j;
+    const float a = sum_partials(prow, splits, sstride, col);
+    const float b = sum_partials(prow, splits, sstride, col + half);
+    const float c = cs[j], s = sn[j];
+    const __nv_bfloat16 o1 = __float2bfloat16(a * c - b * s), o2 = __float2bfloat16(b * c + a * s);
+    if (isq) {
+      Q[((size_t)r * Hq + hd) * D + j] = o1;
+      Q[((size_t)r * Hq + hd) * D + j + half] = o2;
+    } else {
+      const size_t o = kv_base + (size_t)hd * 16 * D + j;
+      Kp[o] = o1;
+      Kp[o + half] = o2;
+    }
+  }
+  for (int t = threadIdx.x; t < Hkv * D; t += blockDim.x) {
+    const int hd = t / D, j = t % D;
+    const float v = sum_partials(prow, splits, sstride, (Hq + Hkv) * D + t);
+    Vp[kv_base + (size_t)hd * 16 * D + j] = __float2bfloat16(v);
+  }
+}
+
+cudaError_t launch_qkv_rope_scatter(const float* P, int splits, int P_rows, const int32_t* src_row, const int32_t* pos,
+                                    const int32_t* slot, const float* cos_t, const float* sin_t, void* Q,
+                                    void* Kpool_l, void* Vpool_l, int M, int Hq, int Hkv, int D, cudaStream_t st) {
+  if (M == 0) return cudaSuccess;
+  qkv_rope_scatter_kernel<<<M, 256, 0, st>>>(P, splits, P_rows, src_row, pos, slot, cos_t, sin_t,
+                                             reinterpret_cast<__nv_bfloat16*>(Q),
+                                             reinterpret_cast<__nv_bfloat16*>(Kpool_l),
+                                             reinterpret_cast<__nv_bfloat16*>(Vpool_l), Hq, Hkv, D);
+  return cudaGetLastError();
+}
+
+// ================================================================================ a8 SwiGLU
+__global__ void swiglu_kernel(const float* __restrict__ P, int splits, uint32_t* __restrict__ u, int M, int F) {
+  const size_t n2 = (size_t)M * F / 2;
+  const size_t sstride = (size_t)M * 2 * F;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n2; i += (size_t)gridDim.x * blockDim.x) {
+    const size_t r = (2 * i) / F, f = (2 * i) % F;
+    float2 g = make_float2(0.f, 0.f), up = make_float2(0.f, 0.f);
+    for (int s = 0; s < splits; ++s) {
+      const float* row = P + s * sstride + r * 2 * F;
+      const float2 a = *reinterpret_cast<const float2*>(row + f);
+      const float2 b = *reinterpret_cast<const float2*>(row + F + f);
+      g.x += a.x;
+      g.y += a.y;
+      up.x += b.x;
+      up.y += b.y;
+    }
+    const float s0 = g.x / (1.f + __expf(-g.x)), s1 = g.y / (1.f + __expf(-g.y));
+    u[i] = pack_bf16(s0 * up.x, s1 * up.y);
+  }
+}
+
+cudaError_t launch_swiglu(const float* P, int splits, void* u, int M, int F, cudaStream_t st) {
+  if (M == 0) return cudaSuccess;
+  const size_t n2 = (size_t)M * F / 2;
+  const int blocks = (int)std::min<size_t>((n2 + 255) / 256, (size_t)148 * 16);
+  swiglu_kernel<<<blocks, 256, 0, st>>>(P, splits, reinterpret_cast<uint32_t*>(u), M, F);
+  return cudaGetLastError();
+}
+
+// ================================================================================ a2 KV link
+// For every cached, unselected row w and layer l >= layer0:
+//   K_lnk = R(Δ_w) · K_store   (bf16 -> fp32 rotate -> bf16; reading R1, Δ = s_c − c0)
+//   V_lnk = V_store            (bit copy)
+// (P:213 step 3: "incorporating the cached KV vectors of the N − k' unselected tokens at correct
+// positions").  One thread = one 16-byte chunk of the first half of a K head-row plus its RoPE
+// partner chunk D/2 further (NeoX pairs), or one 16-byte chunk of a V head-row.
+__global__ void kv_link_kernel(uint4* __restrict__ Kpool, uint4* __restrict__ Vpool, const int32_t* __restrict__ src_slot,
+                               const int32_t* __restrict__ dst_slot, const int32_t* __restrict__ delta, int n_rows,
+                               int layer0, int n_layers, int64_t layer_stride16, int Hkv, int D,
+                               const float* __restrict__ cos_t, const float* __restrict__ sin_t, int rebase) {
+  const int cK = D / 16, cV = D / 8;  // 16-byte chunks per half row (K) / per row (V)
+  const int64_t nK = (int64_t)n_layers * n_rows * Hkv * cK;
+  const int64_t nV = (int64_t)n_layers * n_rows * Hkv * cV;
+  const int rowq = D / 8;             // 16-byte chunks per head-row
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nK + nV; t += (int64_t)gridDim.x * blockDim.x) {
+    const bool isK = t < nK;
+    int64_t u = isK ? t : t - nK;
+    const int per = isK ? cK : cV;
+    const int c = (int)(u % per);
+    u /= per;
+    const int g = (int)(u % Hkv);
+    u /= Hkv;
+    const int w = (int)(u % n_rows);
+    const int l = layer0 + (int)(u / n_rows);
+    const int ss = src_slot[w], ds = dst_slot[w];
+    const int64_t lo = (int64_t)l * layer_stride16;
+    const int64_t so = lo + ((int64_t)(ss / 16) * Hkv + g) * 16 * rowq + (int64_t)(ss % 16) * rowq;
+    const int64_t dof = lo + ((int64_t)(ds / 16) * Hkv + g) * 16 * rowq + (int64_t)(ds % 16) * rowq;
+    if (!isK) {
+      Vpool[dof + c] = Vpool[so + c];
+      continue;
+    }
+    const uint4 xa = Kpool[so + c], xb = Kpool[so + c + cK];
+    const int dl = delta[w];
+    if (!rebase || dl == 0) {
+      Kpool[dof + c] = xa;
+      Kpool[dof + c + cK] = xb;
+      continue;
+    }
+    const int ad = dl < 0 ? -dl : dl;
+    const float sg = dl < 0 ? -1.f : 1.f;
+    const float* cs = cos_t + (size_t)ad * (D / 2) + c * 8;
+    const float* sn = sin_t + (size_t)ad * (D / 2) + c * 8;
+    const uint32_t a4[4] = {xa.x, xa.y, xa.z, xa.w}, b4[4] = {xb.x, xb.y, xb.z, xb.w};
+    uint32_t oa[4], ob[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float a0 = __uint_as_float(a4[k] << 16), a1 = __uint_as_float(a4[k] & 0xFFFF0000u);
+      const float b0 = __uint_as_float(b4[k] << 16), b1 = __uint_as_float(b4[k] & 0xFFFF0000u);
+      const float c0 = cs[2 * k], c1 = cs[2 * k + 1], s0 = sg * sn[2 * k], s1 = sg * sn[2 * k + 1];
+      oa[k] = pack_bf16(a0 * c0 - b0 * s0, a1 * c1 - b1 * s1);
+      ob[k] = pack_bf16(b0 * c0 + a0 * s0, b1 * c1 + a1 * s1);
+    }
+    Kpool[dof + c] = make_uint4(oa[0], oa[1], oa[2], oa[3]);
+    Kpool[dof + c + cK] = make_uint4(ob[0], ob[1], ob[2], ob[3]);
+  }
+}
+
+cudaError_t launch_kv_link(void* Kpool, void* Vpool, const int32_t* src_slot, const int32_t* dst_slot,
+                           const int32_t* delta, int n_rows, int layer0, int n_layers, int64_t layer_stride_elems,
+                           int Hkv, int D, const float* cos_t, const float* sin_t, int rebase, cudaStream_t st) {
+  if (n_rows == 0 || n_layers == 0) return cudaSuccess;
+  const int64_t total = (int64_t)n_layers * n_rows * Hkv * (D / 16 + D / 8);
+  const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
+  kv_link_kernel<<<blocks, 256, 0, st>>>(reinterpret_cast<uint4*>(Kpool), reinterpret_cast<uint4*>(Vpool), src_slot,
+                                         dst_slot, delta, n_rows, layer0, n_layers, layer_stride_elems / 8, Hkv, D,
+                                         cos_t, sin_t, rebase);
+  return cudaGetLastError();
+}
+
+// ================================================================================ a10 argmax
+__global__ void __launch_bounds__(1024) logits_argmax_kernel(const float* __restrict__ P, int splits,
+                                                             float* __restrict__ logits, int32_t* __restrict__ amax,
+                                                             int n_req, int V) {
+  __shared__ float bv[32];
+  __shared__ int bi[32];
+  const int r = blockIdx.x;
+  float best = -INFINITY;
+  int bidx = 0x7FFFFFFF;
+  for (int v = threadIdx.x; v < V; v += blockDim.x) {
+    float s = 0.f;
+    for (int k = 0; k < splits; ++k) s += P[((size_t)k * n_req + r) * V + v];
+    logits[(size_t)r * V + v] = s;
+    if (s > best || (s == best && v < bidx)) {
+      best = s;
+      bidx = v;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float ov = __shfl_xor_sync(0xffffffffu, best, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, bidx, o);
+    if (ov > best || (ov == best && oi < bidx)) {
+      best = ov;
+      bidx = oi;
+    }
+  }
+  if ((threadIdx.x & 31) == 0) {
+    bv[threadIdx.x >> 5] = best;
+    bi[threadIdx.x >> 5] = bidx;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w)
+      if (bv[w] > best || (bv[w] == best && bi[w] < bidx)) {
+        best = bv[w];
+        bidx = bi[w];
+      }
+    amax[r] = bidx;
+  }
+}
+
+cudaError_t launch_logits_argmax(const float* P, int splits, float* logits, int32_t* argmax, int n_req, int V,
+                                 cudaStream_t st) {
+  if (n_req == 0) return cudaSuccess;
+  logits_argmax_kernel<<<n_req, 1024, 0, st>>>(P, splits, logits, argmax, n_req, V);
+  return cudaGetLastError();
+}
+
+// ================================================================================ a9 CacheBlend
+// Deviation of the check layer's fresh K (roped at p_i = i) and V from the linked (re-based) K/V
+// (P:170 step 3; readings R9/R10).  Non-candidates (dynamic rows and the forced last row) get −1.
+__global__ void cb_deviation_kernel(const float* __restrict__ P, int splits, const int32_t* __restrict__ cand,
+                                    const int32_t* __restrict__ slot, const float* __restrict__ cos_t,
+                                    const float* __restrict__ sin_t, const __nv_bfloat16* __restrict__ Kp,
+                                    const __nv_bfloat16* __restrict__ Vp, float* __restrict__ dev, int N, int Hq,
+                                    int Hkv, int D) {
+  __shared__ float red[8];
+  const int i = blockIdx.x;
+  if (!cand[i]) {
+    if (threadIdx.x == 0) dev[i] = -1.f;
+    return;
+  }
+  const int half = D / 2, ncol = (Hq + 2 * Hkv) * D;
+  const size_t sstride = (size_t)N * ncol;
+  const float* prow = P + (size_t)i * ncol;
+  const int sl = slot[i];
+  const size_t kv_base = ((size_t)(sl / 16) * Hkv) * 16 * D + (size_t)(sl % 16) * D;
+  float acc = 0.f;
+  for (int t = threadIdx.x; t < Hkv * half; t += blockDim.x) {
+    const int hd = t / half, j = t % half;
+    const int col = Hq * D + hd * D + j;
+    const float a = sum_partials(prow, splits, sstride, col), b = sum_partials(prow, splits, sstride, col + half);
+    const float c = cos_t[(size_t)i * half + j], s = sin_t[(size_t)i * half + j];
+    const size_t o = kv_base + (size_t)hd * 16 * D + j;
+    const float d1 = a * c - b * s - __bfloat162float(Kp[o]);
+    const float d2 = b * c + a * s - __bfloat162float(Kp[o + half]);
+    acc += d1 * d1 + d2 * d2;
+  }
+  for (int t = threadIdx.x; t < Hkv * D; t += blockDim.x) {
+    const int hd = t / D, j = t % D;
+    const float v = sum_partials(prow, splits, sstride, (Hq + Hkv) * D + t);
+    const float dd = v - __bfloat162float(Vp[kv_base + (size_t)hd * 16 * D + j]);
+    acc += dd * dd;
+  }
+  acc = block_sum<256>(acc, red);
+  if (threadIdx.x == 0) dev[i] = acc;
+}
+
+cudaError_t launch_cb_deviation(const float* P, int splits, const int32_t* cand, const int32_t* slot,
+                                const float* cos_t, const float* sin_t, const void* Kpool_l, const void* Vpool_l,
+                                float* dev, int N, int Hq, int Hkv, int D, cudaStream_t st) {
+  cb_deviation_kernel<<<N, 256, 0, st>>>(P, splits, cand, slot, cos_t, sin_t,
+                                         reinterpret_cast<const __nv_bfloat16*>(Kpool_l),
+                                         reinterpret_cast<const __nv_bfloat16*>(Vpool_l), dev, N, Hq, Hkv, D);
+  return cudaGetLastError();
+}
+
+// rank_i = #{j : dev_j > dev_i or (dev_j == dev_i and j < i)}; keep the T best candidates (R13)
+__global__ void cb_rank_kernel(const float* __restrict__ dev, int32_t* __restrict__ keep, int N, int T) {
+  __shared__ float tile[256];
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const float di = i < N ? dev[i] : -1.f;
+  int rank = 0;
+  for (int j0 = 0; j0 < N; j0 += 256) {
+    const int j = j0 + threadIdx.x;
+    tile[threadIdx.x] = j < N ? dev[j] : -2.f;
+    __syncthreads();
+    const int lim = min(256, N - j0);
+    for (int k = 0; k < lim; ++k) {
+      const float dj = tile[k];
+      rank += (dj > di) || (dj == di && j0 + k < i);
+    }
+    __syncthreads();
+  }
+  if (i < N) keep[i] = (di >= 0.f && rank < T) ? 1 : 0;
+}
+
+cudaError_t launch_cb_rank(const float* dev, int32_t* keep, int N, int T, cudaStream_t st) {
+  cb_rank_kernel<<<(N + 255) / 256, 256, 0, st>>>(dev, keep, N, T);
+  return cudaGetLastError();
+}
+
+// single-CTA ordered compaction (exclusive scan in 1024-wide chunks)
+__global__ void __launch_bounds__(1024) cb_compact_kernel(const int32_t* __restrict__ keep, const int32_t* __restrict__ forced,
+                                                          const int32_t* __restrict__ bt, int32_t* __restrict__ sel,
+                                                          int32_t* __restrict__ pos, int32_t* __restrict__ slot,
+                                                          int32_t* __restrict__ count, int N) {
+  __shared__ int wsum[32];
+  __shared__ int base;
+  if (threadIdx.x == 0) base = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int c0 = 0; c0 < N; c0 += 1024) {
+    const int i = c0 + threadIdx.x;
+    const int f = (i < N) && (keep[i] || forced[i]);
+    const unsigned bal = __ballot_sync(0xffffffffu, f);
+    const int pre = __popc(bal & ((1u << lane) - 1));
+    if (lane == 0) wsum[w] = __popc(bal);
+    __syncthreads();
+    int off = base;
+    for (int k = 0; k < w; ++k) off += wsum[k];
+    if (f) {
+      const int o = off + pre;
+      sel[o] = i;
+      pos[o] = i;
+      slot[o] = bt[i / 16] * 16 + i % 16;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int t = 0;
+      for (int k = 0; k < 32; ++k) t += wsum[k];
+      base += t;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *count = base;
+}
+
+cudaError_t launch_cb_compact(const int32_t* keep, const int32_t* forced, const int32_t* bt, int32_t* sel, int32_t* pos,
+                              int32_t* slot, int32_t* count, int N, cudaStream_t st) {
+  cb_compact_kernel<<<1, 1024, 0, st>>>(keep, forced, bt, sel, pos, slot, count, N);
+  return cudaGetLastError();
+}
+
+__global__ void gather_rows_kernel(const float4* __restrict__ src, const int32_t* __restrict__ idx,
+                                   float4* __restrict__ dst, int d4) {
+  const int r = blockIdx.x;
+  const float4* s = src + (size_t)idx[r] * d4;
+  float4* o = dst + (size_t)r * d4;
+  for (int i = threadIdx.x; i < d4; i += blockDim.x) o[i] = s[i];
+}
+
+cudaError_t launch_gather_rows(const float* src, const int32_t* idx, float* dst, int M, int d, cudaStream_t st) {
+  if (M == 0) return cudaSuccess;
+  gather_rows_kernel<<<M, 256, 0, st>>>(reinterpret_cast<const float4*>(src), idx, reinterpret_cast<float4*>(dst), d / 4);
+  return cudaGetLastError();
+}
+
+}  // namespace pic

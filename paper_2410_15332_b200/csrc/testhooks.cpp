@@ -1,0 +1,188 @@
+// testhooks.cpp — kernel-level test entry points (include/pic_test.h).  Tests only.
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/pic_test.h"
+#include "kernels/kernels.h"
+
+using namespace pic;
+
+namespace {
+struct DevBuf {
+  void* p = nullptr;
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+};
+PFN_cuTensorMapEncodeTiled_v12000 encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }
+  return fn;
+}
+bool tmap(CUtensorMap* m, void* base, int rank, const uint64_t* dims, const uint64_t* strides, const uint32_t* box) {
+  uint32_t es[5] = {1, 1, 1, 1, 1};
+  auto fn = encoder();
+  return fn && fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+}  // namespace
+
+#define TCK(x)                                   \
+  do {                                           \
+    if ((x) != cudaSuccess) return PIC_E_CUDA;   \
+  } while (0)
+
+extern "C" pic_status pic_test_gemm(const uint16_t* A, const uint16_t* B, int32_t M, int32_t N, int32_t K, int32_t bn,
+                                    int32_t splits, float* out) {
+  if (!A || !B || !out || M <= 0 || N <= 0 || K <= 0 || K % 64 || N % 32 || splits <= 0) return PIC_E_INVALID_ARG;
+  if (bn != 64 && bn != 128 && bn != 256) return PIC_E_INVALID_ARG;
+  TCK(prepare_kernels());
+  DevBuf a, b, p;
+  TCK(cudaMalloc(&a.p, (size_t)M * K * 2));
+  TCK(cudaMalloc(&b.p, (size_t)N * K * 2));
+  TCK(cudaMalloc(&p.p, (size_t)splits * M * N * 4));
+  TCK(cudaMemcpy(a.p, A, (size_t)M * K * 2, cudaMemcpyHostToDevice));
+  TCK(cudaMemcpy(b.p, B, (size_t)N * K * 2, cudaMemcpyHostToDevice));
+  CUtensorMap ta, tb;
+  uint64_t da[2] = {(uint64_t)K, (uint64_t)M}, db[2] = {(uint64_t)K, (uint64_t)N}, st[1] = {(uint64_t)K * 2};
+  uint32_t ba[2] = {64, 128}, bb[2] = {64, (uint32_t)bn};
+  if (!tmap(&ta, a.p, 2, da, st, ba) || !tmap(&tb, b.p, 2, db, st, bb)) return PIC_E_CUDA;
+  TCK(launch_gemm_partial(ta, tb, reinterpret_cast<float*>(p.p), M, N, K, splits, bn, 0));
+  TCK(cudaDeviceSynchronize());
+  std::vector<float> part((size_t)splits * M * N);
+  TCK(cudaMemcpy(part.data(), p.p, part.size() * 4, cudaMemcpyDeviceToHost));
+  for (size_t i = 0; i < (size_t)M * N; ++i) {
+    float s = 0.f;
+    for (int k = 0; k < splits; ++k) s += part[(size_t)k * M * N + i];
+    out[i] = s;
+  }
+  return PIC_OK;
+}
+
+extern "C" pic_status pic_test_attention(const uint16_t* Q, const uint16_t* K, const uint16_t* V, const int32_t* pos,
+                                         int32_t M, int32_t n_keys, int32_t Hq, int32_t Hkv,
+                                         const int32_t* block_perm, int32_t num_blocks, int32_t n_splits,
+                                         uint16_t* O) {
+  const int D = 128;
+  if (!Q || !K || !V || !pos || !block_perm || !O || M <= 0 || n_keys <= 0 || Hq % Hkv || 128 % (Hq / Hkv))
+    return PIC_E_INVALID_ARG;
+  const int nb = (n_keys + 15) / 16;
+  TCK(prepare_kernels());
+  // paged pools [num_blocks][Hkv][16][D]
+  const size_t pool = (size_t)num_blocks * Hkv * 16 * D;
+  std::vector<uint16_t> kp(pool, 0), vp(pool, 0);
+  for (int t = 0; t < n_keys; ++t)
+    for (int g = 0; g < Hkv; ++g) {
+      const size_t dst = (((size_t)block_perm[t / 16] * Hkv + g) * 16 + t % 16) * D;
+      std::memcpy(&kp[dst], K + ((size_t)t * Hkv + g) * D, D * 2);
+      std::memcpy(&vp[dst], V + ((size_t)t * Hkv + g) * D, D * 2);
+    }
+  const int G = Hq / Hkv, qpt = 128 / G;
+  std::vector<int32_t> tiles;
+  for (int a = 0; a < M; a += qpt) {
+    tiles.push_back(0);
+    tiles.push_back(a);
+    tiles.push_back(std::min(qpt, M - a));
+  }
+  const int n_tiles = (int)tiles.size() / 3;
+  DevBuf dq, dk, dv, dpos, dt, dbt, doff, dop, dml, dout;
+  TCK(cudaMalloc(&dq.p, (size_t)M * Hq * D * 2));
+  TCK(cudaMalloc(&dk.p, pool * 2));
+  TCK(cudaMalloc(&dv.p, pool * 2));
+  TCK(cudaMalloc(&dpos.p, M * 4));
+  TCK(cudaMalloc(&dt.p, tiles.size() * 4));
+  TCK(cudaMalloc(&dbt.p, nb * 4));
+  TCK(cudaMalloc(&doff.p, 4));
+  TCK(cudaMalloc(&dop.p, (size_t)n_splits * M * Hq * D * 4));
+  TCK(cudaMalloc(&dml.p, (size_t)n_splits * M * Hq * 2 * 4));
+  TCK(cudaMalloc(&dout.p, (size_t)M * Hq * D * 2));
+  TCK(cudaMemcpy(dq.p, Q, (size_t)M * Hq * D * 2, cudaMemcpyHostToDevice));
+  TCK(cudaMemcpy(dk.p, kp.data(), pool * 2, cudaMemcpyHostToDevice));
+  TCK(cudaMemcpy(dv.p, vp.data(), pool * 2, cudaMemcpyHostToDevice));
+  TCK(cudaMemcpy(dpos.p, pos, M * 4, cudaMemcpyHostToDevice));
+  TCK(cudaMemcpy(dt.p, tiles.data(), tiles.size() * 4, cudaMemcpyHostToDevice));
+  TCK(cudaMemcpy(dbt.p, block_perm, nb * 4, cudaMemcpyHostToDevice));
+  TCK(cudaMemset(doff.p, 0, 4));
+  CUtensorMap tq, tk, tv;
+  {
+    uint64_t dims[3] = {(uint64_t)D, (uint64_t)Hq, (uint64_t)M};
+    uint64_t strides[2] = {(uint64_t)D * 2, (uint64_t)Hq * D * 2};
+    uint32_t box[3] = {64, (uint32_t)G, (uint32_t)qpt};
+    if (!tmap(&tq, dq.p, 3, dims, strides, box)) return PIC_E_CUDA;
+  }
+  {
+    uint64_t dims[4] = {(uint64_t)D, 16, (uint64_t)Hkv, (uint64_t)num_blocks};
+    uint64_t strides[3] = {(uint64_t)D * 2, (uint64_t)16 * D * 2, (uint64_t)Hkv * 16 * D * 2};
+    uint32_t box[4] = {64, 16, 1, 1};
+    if (!tmap(&tk, dk.p, 4, dims, strides, box) || !tmap(&tv, dv.p, 4, dims, strides, box)) return PIC_E_CUDA;
+  }
+  AttnArgs a{};
+  a.tiles = reinterpret_cast<int32_t*>(dt.p);
+  a.seq_bt_off = reinterpret_cast<int32_t*>(doff.p);
+  a.bt = reinterpret_cast<int32_t*>(dbt.p);
+  a.row_pos = reinterpret_cast<int32_t*>(dpos.p);
+  a.n_tiles = n_tiles;
+  a.M = M;
+  a.Hq = Hq;
+  a.Hkv = Hkv;
+  a.layer = 0;
+  a.num_blocks = num_blocks;
+  a.n_splits = n_splits;
+  a.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)D));
+  a.o_part = reinterpret_cast<float*>(dop.p);
+  a.ml_part = reinterpret_cast<float*>(dml.p);
+  TCK(launch_attention_tc(tq, tk, tv, a, 0));
+  TCK(launch_attn_combine(a.o_part, a.ml_part, dout.p, M, Hq, D, n_splits, 0));
+  TCK(cudaDeviceSynchronize());
+  TCK(cudaMemcpy(O, dout.p, (size_t)M * Hq * D * 2, cudaMemcpyDeviceToHost));
+  return PIC_OK;
+}
+
+extern "C" pic_status pic_test_kv_link(uint16_t* Kpool, uint16_t* Vpool, int32_t n_layers, int32_t num_blocks,
+                                       int32_t Hkv, int32_t D, const int32_t* src_slot, const int32_t* dst_slot,
+                                       const int32_t* delta, int32_t n_rows, int32_t layer0, int32_t rebase,
+                                       double theta, int32_t max_pos) {
+  if (!Kpool || !Vpool || n_rows < 0 || D % 16) return PIC_E_INVALID_ARG;
+  const size_t stride = (size_t)num_blocks * Hkv * 16 * D;
+  const size_t pool = (size_t)n_layers * stride;
+  const int half = D / 2;
+  std::vector<float> cs((size_t)max_pos * half), sn((size_t)max_pos * half);
+  for (int p = 0; p < max_pos; ++p)
+    for (int j = 0; j < half; ++j) {
+      const double ang = (double)p * std::pow(theta, -2.0 * j / (double)D);
+      cs[(size_t)p * half + j] = (float)std::cos(ang);
+      sn[(size_t)p * half + j] = (float)std::sin(ang);
+    }
+  DevBuf dk, dv, ds, dd, de, dc, dsn;
+  TCK(cudaMalloc(&dk.p, pool * 2));
+  TCK(cudaMalloc(&dv.p, pool * 2));
+  TCK(cudaMalloc(&ds.p, std::max(1, n_rows) * 4));
+  TCK(cudaMalloc(&dd.p, std::max(1, n_rows) * 4));
+  TCK(cudaMalloc(&de.p, std::max(1, n_rows) * 4));
+  TCK(cudaMalloc(&dc.p, cs.size() * 4));
+  TCK(cudaMalloc(&dsn.p, sn.size() * 4));
+  TCK(cudaMemcpy(dk.p, Kpool, pool * 2, cudaMemcpyHostToDevice));
+  TCK(cudaMemcpy(dv.p, Vpool, pool * 2, cudaMemcpyHostToDevice));
+  TCK(cudaMemcpy(ds.p, src_slot, n_rows * 4, cudaMemcpyHostToDevice));
+  TCK(cudaMemcpy(dd.p, dst_slot, n_rows * 4, cudaMemcpyHostToDevice));
+  TCK(cudaMemcpy(de.p, delta, n_rows * 4, cudaMemcpyHostToDevice));
+  TCK(cudaMemcpy(dc.p, cs.data(), cs.size() * 4, cudaMemcpyHostToDevice));
+  TCK(cudaMemcpy(dsn.p, sn.data(), sn.size() * 4, cudaMemcpyHostToDevice));
+  TCK(launch_kv_link(dk.p, dv.p, (int32_t*)ds.p, (int32_t*)dd.p, (int32_t*)de.p, n_rows, layer0, n_layers - layer0,
+                     stride, Hkv, D, (float*)dc.p, (float*)dsn.p, rebase, 0));
+  TCK(cudaDeviceSynchronize());
+  TCK(cudaMemcpy(Kpool, dk.p, pool * 2, cudaMemcpyDeviceToHost));
+  TCK(cudaMemcpy(Vpool, dv.p, pool * 2, cudaMemcpyDeviceToHost));
+  return PIC_OK;
+}

@@ -1,0 +1,413 @@
+"""ctypes binding of libpic.so (include/pic.h).  Argument marshalling only: every step of the
+linked-prefill path runs in the library's CUDA kernels.  PyTorch provides the device arena and
+the stream.  There is no fallback: if libpic.so is missing or the GPU is absent, calls fail."""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+from typing import List, Optional, Sequence, Tuple
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libpic.so")
+
+PIC_SEG_CACHED, PIC_SEG_TOKENS = 0, 1
+PIC_NAIVE, PIC_FULL, PIC_LEGOLINK, PIC_CACHEBLEND = 0, 1, 2, 3
+STATUS = ["PIC_OK", "PIC_E_INVALID_ARG", "PIC_E_CONFIG", "PIC_E_EMPTY_INPUT", "PIC_E_CAPACITY",
+          "PIC_E_MISSING_CACHE", "PIC_E_LAYOUT", "PIC_E_VARIANT", "PIC_E_OOM", "PIC_E_CUDA",
+          "PIC_E_NO_DEVICE", "PIC_E_TOKEN"]
+
+
+class PicError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS[status] if 0 <= status < len(STATUS) else status}: {msg}")
+        self.status = status
+        self.name = STATUS[status] if 0 <= status < len(STATUS) else str(status)
+
+
+class ModelConfigC(C.Structure):
+    _fields_ = [("n_layers", C.c_int32), ("d_model", C.c_int32), ("n_heads", C.c_int32),
+                ("n_kv_heads", C.c_int32), ("head_dim", C.c_int32), ("ffn_dim", C.c_int32),
+                ("vocab", C.c_int32), ("max_pos", C.c_int32), ("bos_id", C.c_int32),
+                ("rope_theta", C.c_double), ("rms_eps", C.c_double), ("seed", C.c_uint64)]
+
+
+class LimitsC(C.Structure):
+    _fields_ = [("num_blocks", C.c_int64), ("max_rows", C.c_int32), ("max_tokens", C.c_int32),
+                ("max_requests", C.c_int32)]
+
+
+class SegmentC(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("n_tokens", C.c_int32), ("id", C.c_uint64),
+                ("tokens", C.POINTER(C.c_int32))]
+
+
+class LinkParamsC(C.Structure):
+    _fields_ = [("alg", C.c_int32), ("k", C.c_int32), ("r_percent", C.c_int32), ("check_layer", C.c_int32),
+                ("rebase", C.c_int32), ("use_graph", C.c_int32), ("sel_override", C.POINTER(C.c_int32)),
+                ("n_sel_override", C.c_int32), ("debug_hidden", C.POINTER(C.c_float))]
+
+
+class LinkResultC(C.Structure):
+    _fields_ = [("logits", C.POINTER(C.c_float)), ("logits_dev", C.c_void_p), ("first_token", C.c_int32),
+                ("n_tokens", C.c_int32), ("n_selected", C.c_int32), ("n_selected_layer0", C.c_int32),
+                ("selected", C.POINTER(C.c_int32))]
+
+
+class PlanOutC(C.Structure):
+    _fields_ = [("capacity", C.c_int32), ("n_tokens", C.c_int32), ("n_sel", C.c_int32), ("n_chunks", C.c_int32),
+                ("n_blocks", C.c_int32), ("sel", C.POINTER(C.c_int32)), ("tok", C.POINTER(C.c_int32)),
+                ("src", C.POINTER(C.c_int32)), ("chunks", C.POINTER(C.c_int32)),
+                ("block_table", C.POINTER(C.c_int32)), ("slot", C.POINTER(C.c_int32))]
+
+
+class StatsC(C.Structure):
+    _fields_ = [("free_blocks", C.c_int64), ("total_blocks", C.c_int64), ("n_cached_chunks", C.c_int64),
+                ("kernels_last_call", C.c_int64), ("graphs_cached", C.c_int64),
+                ("h2d_bytes_last_call", C.c_int64), ("d2h_bytes_last_call", C.c_int64)]
+
+
+# every symbol include/pic.h and include/pic_test.h declare
+EXPORTS = ["pic_arena_bytes", "pic_engine_create", "pic_engine_destroy", "pic_generate_context_cache", "pic_link",
+           "pic_link_batch", "pic_plan", "pic_linked_export", "pic_linked_info", "pic_linked_release",
+           "pic_cache_export", "pic_cache_info", "pic_expire_cache", "pic_read_weights", "pic_get_stats",
+           "pic_last_error", "pic_status_string", "pic_test_gemm", "pic_test_attention", "pic_test_kv_link"]
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_2410_15332_b200.build` "
+                              "(there is no fallback path)")
+        L = C.CDLL(LIB_PATH)
+        P = C.POINTER
+        L.pic_last_error.restype = C.c_char_p
+        L.pic_status_string.restype = C.c_char_p
+        L.pic_arena_bytes.argtypes = [P(ModelConfigC), P(LimitsC), P(C.c_size_t)]
+        L.pic_engine_create.argtypes = [P(ModelConfigC), P(LimitsC), C.c_int32, C.c_void_p, C.c_size_t, C.c_void_p,
+                                        P(C.c_void_p)]
+        L.pic_engine_destroy.argtypes = [C.c_void_p]
+        L.pic_engine_destroy.restype = None
+        L.pic_generate_context_cache.argtypes = [C.c_void_p, P(P(C.c_int32)), P(C.c_int32), C.c_int32, C.c_void_p,
+                                                 P(C.c_uint64), P(C.c_int32)]
+        L.pic_link.argtypes = [C.c_void_p, P(SegmentC), C.c_int32, P(LinkParamsC), C.c_void_p, P(C.c_void_p),
+                               P(LinkResultC)]
+        L.pic_link_batch.argtypes = [C.c_void_p, C.c_int32, P(P(SegmentC)), P(C.c_int32), P(LinkParamsC), C.c_void_p,
+                                     P(C.c_void_p), P(LinkResultC)]
+        L.pic_plan.argtypes = [C.c_void_p, P(SegmentC), C.c_int32, P(LinkParamsC), P(PlanOutC)]
+        L.pic_linked_export.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p]
+        L.pic_linked_info.argtypes = [C.c_void_p, C.c_void_p, P(C.c_int32), P(C.c_int32)]
+        L.pic_linked_release.argtypes = [C.c_void_p, C.c_void_p]
+        L.pic_cache_export.argtypes = [C.c_void_p, C.c_uint64, C.c_int32, C.c_void_p, C.c_void_p]
+        L.pic_cache_info.argtypes = [C.c_void_p, C.c_uint64, P(C.c_int32), P(C.c_int32)]
+        L.pic_expire_cache.argtypes = [C.c_void_p, C.c_uint64, P(C.c_int32)]
+        L.pic_read_weights.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_int64, C.c_int64, C.c_void_p]
+        L.pic_get_stats.argtypes = [C.c_void_p, P(StatsC)]
+        L.pic_test_gemm.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+                                    C.c_void_p]
+        L.pic_test_attention.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32,
+                                         C.c_int32, C.c_int32, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p]
+        L.pic_test_kv_link.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p,
+                                       C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_double, C.c_int32]
+        for name in EXPORTS:
+            getattr(L, name)  # AttributeError if the library lacks a declared entry point
+        _lib = L
+    return _lib
+
+
+def check(status: int) -> None:
+    if status != 0:
+        raise PicError(status, lib().pic_last_error().decode(errors="replace"))
+
+
+def _ptr(a: Optional[np.ndarray], ctype=C.c_int32):
+    return None if a is None else a.ctypes.data_as(C.POINTER(ctype))
+
+
+def config_struct(cfg) -> ModelConfigC:
+    return ModelConfigC(cfg.n_layers, cfg.d_model, cfg.n_heads, cfg.n_kv_heads, cfg.head_dim, cfg.ffn_dim,
+                        cfg.vocab, cfg.max_pos, cfg.bos_id, float(cfg.rope_theta), float(cfg.rms_eps),
+                        int(cfg.seed))
+
+
+ALGS = {"naive": PIC_NAIVE, "fr": PIC_FULL, "legolink": PIC_LEGOLINK, "cacheblend": PIC_CACHEBLEND}
+
+
+def parse_alg(alg: str) -> Tuple[int, int, int]:
+    """SPEC grammar -> (pic_algorithm, k, r_percent)."""
+    if alg == "naive":
+        return PIC_NAIVE, 0, 0
+    if alg == "fr":
+        return PIC_FULL, 0, 0
+    name, _, val = alg.partition(":")
+    if name == "legolink":
+        return PIC_LEGOLINK, int(val), 0
+    if name == "cacheblend":
+        return PIC_CACHEBLEND, 0, int(val)
+    raise ValueError(f"unknown algorithm {alg!r}")
+
+
+class _Segs:
+    """Keeps the ctypes segment array and its token buffers alive for one call."""
+
+    def __init__(self, segments):
+        self.keep = []
+        self.arr = (SegmentC * max(1, len(segments)))()
+        self.n = len(segments)
+        for i, (kind, val) in enumerate(segments):
+            if kind == "cached":
+                self.arr[i] = SegmentC(PIC_SEG_CACHED, 0, int(val), None)
+            elif kind == "tokens":
+                t = np.ascontiguousarray(val, dtype=np.int32)
+                self.keep.append(t)
+                self.arr[i] = SegmentC(PIC_SEG_TOKENS, len(t), 0, _ptr(t))
+            else:
+                raise ValueError(kind)
+
+
+@dataclass
+class LinkOutput:
+    logits: Optional[np.ndarray]
+    first_token: int
+    n_tokens: int
+    n_selected: int
+    n_selected_layer0: int
+    linked: Optional[int] = None          # opaque pic_linked* (release with Engine.release)
+    selected: Optional[np.ndarray] = None # linked indices recomputed in the last layer
+    hidden: Optional[np.ndarray] = None   # debug hidden [L][N][d]
+
+
+def bf16_bits_to_f32(b: np.ndarray) -> np.ndarray:
+    return (b.astype(np.uint32) << np.uint32(16)).view(np.float32)
+
+
+class Engine:
+    """One engine = one model replica on one GPU (or a host-only planner when device=None)."""
+
+    def __init__(self, cfg, num_blocks: int, max_rows: int, max_tokens: int, max_requests: int = 1,
+                 device: Optional[int] = 0, stream=None):
+        L = lib()
+        self.cfg = cfg
+        self._cfg = config_struct(cfg)
+        self._lim = LimitsC(num_blocks, max_rows, max_tokens, max_requests)
+        self.max_tokens = max_tokens
+        self._h = C.c_void_p()
+        self.arena = None
+        self.device = device
+        if device is None:
+            check(L.pic_engine_create(C.byref(self._cfg), C.byref(self._lim), -1, None, 0, None, C.byref(self._h)))
+            self.stream = None
+            return
+        import torch
+        nbytes = C.c_size_t()
+        check(L.pic_arena_bytes(C.byref(self._cfg), C.byref(self._lim), C.byref(nbytes)))
+        torch.cuda.set_device(device)
+        self.arena = torch.empty(nbytes.value, dtype=torch.uint8, device=f"cuda:{device}")
+        self.stream = stream if stream is not None else torch.cuda.current_stream(device)
+        check(L.pic_engine_create(C.byref(self._cfg), C.byref(self._lim), device, C.c_void_p(self.arena.data_ptr()),
+                                  nbytes.value, C.c_void_p(self.stream.cuda_stream), C.byref(self._h)))
+
+    @property
+    def _stream(self):
+        return None if self.stream is None else C.c_void_p(self.stream.cuda_stream)
+
+    def close(self):
+        if self._h:
+            lib().pic_engine_destroy(self._h)
+            self._h = C.c_void_p()
+        self.arena = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ------------------------------------------------------------------ compile
+    def generate_context_cache(self, chunks: Sequence[np.ndarray]) -> List[int]:
+        arrs = [np.ascontiguousarray(c, dtype=np.int32) for c in chunks]
+        n = len(arrs)
+        ptrs = (C.POINTER(C.c_int32) * max(1, n))(*[_ptr(a) for a in arrs])
+        lens = (C.c_int32 * max(1, n))(*[len(a) for a in arrs])
+        ids = (C.c_uint64 * max(1, n))()
+        err = C.c_int32(-1)
+        st = lib().pic_generate_context_cache(self._h, ptrs, lens, n, self._stream, ids, C.byref(err))
+        if st != 0:
+            e = PicError(st, lib().pic_last_error().decode())
+            e.err_index = err.value
+            raise e
+        return [int(ids[i]) for i in range(n)]
+
+    # ------------------------------------------------------------------ link
+    def _params(self, alg, check_layer=1, rebase=True, use_graph=True, sel_override=None, debug_hidden=None):
+        a, k, r = parse_alg(alg)
+        p = LinkParamsC(a, k, r, check_layer, int(rebase), int(use_graph), None, 0, None)
+        keep = []
+        if sel_override is not None:
+            so = np.ascontiguousarray(sel_override, dtype=np.int32)
+            keep.append(so)
+            p.sel_override = _ptr(so)
+            p.n_sel_override = len(so)
+        if debug_hidden is not None:
+            p.debug_hidden = debug_hidden.ctypes.data_as(C.POINTER(C.c_float))
+        return p, keep
+
+    def link(self, segments, alg: str, *, check_layer: int = 1, rebase: bool = True, use_graph: bool = True,
+             want_logits: bool = True, logits_dev=None, keep_linked: bool = False, sel_override=None,
+             debug_hidden: bool = False, want_selected: bool = False) -> LinkOutput:
+        segs = _Segs(segments)
+        hid = None
+        N = self.plan(segments, alg)["n_tokens"] if (debug_hidden or want_selected) else 0
+        if debug_hidden:
+            hid = np.full((self.cfg.n_layers, N, self.cfg.d_model), np.nan, dtype=np.float32)
+        p, keep = self._params(alg, check_layer, rebase, use_graph, sel_override, hid)
+        res = LinkResultC()
+        logits = None
+        if want_logits:
+            logits = np.empty(self.cfg.vocab, dtype=np.float32)
+            res.logits = _ptr(logits, C.c_float)
+        if logits_dev is not None:
+            res.logits_dev = C.c_void_p(logits_dev.data_ptr())
+        sel = None
+        if want_selected:
+            sel = np.full(N, -1, dtype=np.int32)
+            res.selected = _ptr(sel)
+        linked = C.c_void_p()
+        check(lib().pic_link(self._h, segs.arr, segs.n, C.byref(p), self._stream,
+                             C.byref(linked) if keep_linked else None, C.byref(res)))
+        return LinkOutput(logits, res.first_token, res.n_tokens, res.n_selected, res.n_selected_layer0,
+                          linked.value if keep_linked else None, sel[:res.n_selected] if sel is not None else None,
+                          hid)
+
+    def link_batch(self, requests, alg: str, *, use_graph: bool = True, want_logits: bool = True,
+                   keep_linked: bool = False) -> List[LinkOutput]:
+        n = len(requests)
+        segs = [_Segs(r) for r in requests]
+        arrp = (C.POINTER(SegmentC) * n)(*[C.cast(s.arr, C.POINTER(SegmentC)) for s in segs])
+        ns = (C.c_int32 * n)(*[s.n for s in segs])
+        p, keep = self._params(alg, use_graph=use_graph)
+        res = (LinkResultC * n)()
+        logits = None
+        if want_logits:
+            logits = np.empty((n, self.cfg.vocab), dtype=np.float32)
+            for i in range(n):
+                res[i].logits = logits[i].ctypes.data_as(C.POINTER(C.c_float))
+        linked = (C.c_void_p * n)()
+        check(lib().pic_link_batch(self._h, n, arrp, ns, C.byref(p), self._stream, linked if keep_linked else None,
+                                   res))
+        return [LinkOutput(None if logits is None else logits[i], res[i].first_token, res[i].n_tokens,
+                           res[i].n_selected, res[i].n_selected_layer0, linked[i] if keep_linked else None)
+                for i in range(n)]
+
+    def plan(self, segments, alg: str) -> dict:
+        segs = _Segs(segments)
+        p, _ = self._params(alg)
+        cap = self.max_tokens
+        bufs = {k: np.zeros(n * cap, dtype=np.int32) for k, n in
+                (("sel", 1), ("tok", 1), ("src", 2), ("chunks", 3), ("block_table", 1), ("slot", 1))}
+        out = PlanOutC(cap, 0, 0, 0, 0, *[_ptr(bufs[k]) for k in
+                                          ("sel", "tok", "src", "chunks", "block_table", "slot")])
+        check(lib().pic_plan(self._h, segs.arr, segs.n, C.byref(p), C.byref(out)))
+        N, ns, nc, nb = out.n_tokens, out.n_sel, out.n_chunks, out.n_blocks
+        return {"n_tokens": N, "sel": bufs["sel"][:ns].copy(), "tok": bufs["tok"][:N].copy(),
+                "src": bufs["src"][:2 * N].reshape(N, 2).copy(), "chunks": bufs["chunks"][:3 * nc].reshape(nc, 3).copy(),
+                "block_table": bufs["block_table"][:nb].copy(), "slot": bufs["slot"][:ns].copy()}
+
+    # ------------------------------------------------------------------ exports / lifecycle
+    def linked_export(self, linked: int, layer: int) -> Tuple[np.ndarray, np.ndarray]:
+        n = C.c_int32()
+        check(lib().pic_linked_info(self._h, C.c_void_p(linked), C.byref(n), None))
+        shape = (n.value, self.cfg.n_kv_heads, self.cfg.head_dim)
+        k = np.empty(shape, dtype=np.uint16)
+        v = np.empty(shape, dtype=np.uint16)
+        check(lib().pic_linked_export(self._h, C.c_void_p(linked), layer, k.ctypes.data, v.ctypes.data))
+        return k, v
+
+    def linked_blocks(self, linked: int) -> np.ndarray:
+        n = C.c_int32()
+        check(lib().pic_linked_info(self._h, C.c_void_p(linked), C.byref(n), None))
+        bt = np.zeros((n.value + 15) // 16, dtype=np.int32)
+        check(lib().pic_linked_info(self._h, C.c_void_p(linked), C.byref(n), _ptr(bt)))
+        return bt
+
+    def release(self, linked: int) -> None:
+        check(lib().pic_linked_release(self._h, C.c_void_p(linked)))
+
+    def cache_export(self, cid: int, layer: int) -> Tuple[np.ndarray, np.ndarray]:
+        n = C.c_int32()
+        check(lib().pic_cache_info(self._h, cid, C.byref(n), None))
+        shape = (n.value, self.cfg.n_kv_heads, self.cfg.head_dim)
+        k = np.empty(shape, dtype=np.uint16)
+        v = np.empty(shape, dtype=np.uint16)
+        check(lib().pic_cache_export(self._h, cid, layer, k.ctypes.data, v.ctypes.data))
+        return k, v
+
+    def cache_blocks(self, cid: int) -> np.ndarray:
+        n = C.c_int32()
+        check(lib().pic_cache_info(self._h, cid, C.byref(n), None))
+        b = np.zeros((n.value + 15) // 16, dtype=np.int32)
+        check(lib().pic_cache_info(self._h, cid, C.byref(n), _ptr(b)))
+        return b
+
+    def expire(self, cid: int) -> bool:
+        w = C.c_int32()
+        check(lib().pic_expire_cache(self._h, cid, C.byref(w)))
+        return bool(w.value)
+
+    def read_weights(self, which: int, layer: int = 0, row0: int = 0, nrows: int = 1) -> np.ndarray:
+        c = self.cfg
+        if which >= 9:
+            out = np.empty(c.d_model, dtype=np.float32)
+        else:
+            cols = {0: c.d_model, 1: c.d_model, 2: c.d_model, 3: c.n_heads * c.head_dim, 4: c.d_model,
+                    5: c.d_model, 6: c.ffn_dim, 7: c.d_model, 8: c.d_model}[which]
+            out = np.empty((nrows, cols), dtype=np.uint16)
+        check(lib().pic_read_weights(self._h, which, layer, row0, nrows, out.ctypes.data))
+        return out
+
+    def stats(self) -> dict:
+        s = StatsC()
+        check(lib().pic_get_stats(self._h, C.byref(s)))
+        return {k: getattr(s, k) for k, _ in StatsC._fields_}
+
+
+# ---------------------------------------------------------------------------- kernel test hooks
+def test_gemm(A: np.ndarray, B: np.ndarray, bn: int = 128, splits: int = 1) -> np.ndarray:
+    A = np.ascontiguousarray(A, dtype=np.uint16)
+    B = np.ascontiguousarray(B, dtype=np.uint16)
+    M, K = A.shape
+    N = B.shape[0]
+    out = np.empty((M, N), dtype=np.float32)
+    check(lib().pic_test_gemm(A.ctypes.data, B.ctypes.data, M, N, K, bn, splits, out.ctypes.data))
+    return out
+
+
+def test_attention(Q, K, V, pos, block_perm, num_blocks, n_splits=1) -> np.ndarray:
+    Q = np.ascontiguousarray(Q, dtype=np.uint16)
+    K = np.ascontiguousarray(K, dtype=np.uint16)
+    V = np.ascontiguousarray(V, dtype=np.uint16)
+    pos = np.ascontiguousarray(pos, dtype=np.int32)
+    bp = np.ascontiguousarray(block_perm, dtype=np.int32)
+    M, Hq, D = Q.shape
+    n, Hkv, _ = K.shape
+    O = np.empty((M, Hq, D), dtype=np.uint16)
+    check(lib().pic_test_attention(Q.ctypes.data, K.ctypes.data, V.ctypes.data, pos.ctypes.data, M, n, Hq, Hkv,
+                                   bp.ctypes.data, num_blocks, n_splits, O.ctypes.data))
+    return O
+
+
+def test_kv_link(Kpool, Vpool, src, dst, delta, layer0=0, rebase=True, theta=1e4, max_pos=4096):
+    Kpool = np.ascontiguousarray(Kpool, dtype=np.uint16)
+    Vpool = np.ascontiguousarray(Vpool, dtype=np.uint16)
+    L, NB, Hkv, _, D = Kpool.shape
+    src = np.ascontiguousarray(src, dtype=np.int32)
+    dst = np.ascontiguousarray(dst, dtype=np.int32)
+    delta = np.ascontiguousarray(delta, dtype=np.int32)
+    check(lib().pic_test_kv_link(Kpool.ctypes.data, Vpool.ctypes.data, L, NB, Hkv, D, src.ctypes.data,
+                                 dst.ctypes.data, delta.ctypes.data, len(src), layer0, int(rebase), theta, max_pos))
+    return Kpool, Vpool
