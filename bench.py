@@ -1,0 +1,327 @@
+#!/usr/bin/env python
+"""Linked-prefill benchmark (BASELINE.json metric: linked-prefill TTFT and linked tokens/s,
+with % of HBM / tensor roofline).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg2|cfg3|cfg4] [--alg ALG]
+                    [--impl ours|reference]
+
+A step = one linked prefill (pic_link, all rows of SURVEY §8(a)) of the workload's request(s)
+on synthetic random-init weights of the named shape.  Multi-GPU (torchrun): one process per
+GPU, each links its own independent requests (data parallel by request, no collective on the
+path; "scaling": "weak"); timing is the max over ranks of CUDA-event time.
+
+--impl reference times the fp64 CPU oracle (oracle/) on a bounded sample of the same workload
+(there is no reference implementation to install: the paper ships no code)."""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import seedgen as sg  # noqa: E402
+
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+
+
+def peaks():
+    try:
+        with open(PEAKS_PATH) as f:
+            p = json.load(f)
+        return p, "measured"
+    except Exception:
+        return FALLBACK, "fallback"
+
+
+def workload(name: str, alg: str | None):
+    if name == "cfg2":
+        w = sg.cfg2(alg or "legolink:16")
+    elif name == "cfg3":
+        w = sg.cfg3(alg or "legolink:32")
+    elif name == "cfg4":
+        w = sg.cfg4(n_requests=32, alg=alg or "legolink:16")
+    else:
+        raise SystemExit(f"unknown config {name}")
+    return w
+
+
+def describe(w) -> dict:
+    m = w.model
+    n_chunks = len(w.requests[0]) - (0 if w.requests[0][-1].cached else 1)
+    q = 0 if w.requests[0][-1].cached else len(w.requests[0][-1].tokens)
+    return {"workload": f"{w.name}: {m.name}-shaped random-init bf16, {n_chunks} chunks x {len(w.chunks[0])} tokens"
+                        f" + {q}-token query, {w.alg}, {len(w.requests)} request(s) per GPU",
+            "model": m.name, "n_layers": m.n_layers, "d_model": m.d_model, "vocab": m.vocab,
+            "chunk_len": len(w.chunks[0]), "n_chunks": n_chunks, "query_len": q, "alg": w.alg,
+            "requests_per_gpu_step": len(w.requests),
+            "l2": "inputs larger than L2 (weights 14+ GB re-read every step), no flush"}
+
+
+# ------------------------------------------------------------------------------------- clocks
+class ClockSampler:
+    def __init__(self, gpu: int):
+        self.gpu, self.samples, self.proc = gpu, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.samples.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 3 + i and s[3 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------------------------- CPU oracle
+def oracle_sample(w, reps: int = 1):
+    """Time the fp64 oracle's link on a bounded sample: layer 0 of the request (all its work:
+    re-base of every cached row, the layer on the k' rows) plus the LM head, then extrapolate to
+    all L layers.  Returns (tokens/s, seconds per full request (extrapolated), sample text)."""
+    from oracle import model as M
+    from oracle import pic as P
+    cfg = w.model
+    Wt = M.Weights(sg.truncated(cfg, 1))
+    Wt.layer(0)
+    Wt.lm_head
+    store = P.Store(Wt)
+    L1 = 1
+    over = [(np.zeros((L1, len(c), cfg.n_kv_heads, cfg.head_dim)), np.zeros((L1, len(c), cfg.n_kv_heads, cfg.head_dim)))
+            for c in w.chunks]
+    oids = store.compile(w.chunks, compiled_override=over)
+    segs = [("cached", oids[s.chunk]) if s.cached else ("tokens", s.tokens) for s in w.requests[0]]
+    N = sum(len(w.chunks[s.chunk]) if s.cached else len(s.tokens) for s in w.requests[0])
+    t_link, t_head = [], []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        r = P.link(store, segs, w.alg, layers=1)
+        t_link.append(time.perf_counter() - t0)
+        h = r.hidden[-1][-1]
+        t0 = time.perf_counter()
+        M.logits_of(Wt, h)
+        t_head.append(time.perf_counter() - t0)
+    tl, th = min(t_link), min(t_head)
+    per_req = cfg.n_layers * (tl - th) + th
+    return N / per_req, per_req, (f"oracle fp64 link of 1 request, layer 0 of {cfg.n_layers} + LM head timed "
+                                  f"({tl:.2f}s), extrapolated x{cfg.n_layers} layers; N={N}")
+
+
+def cores_used():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count()
+
+
+# ------------------------------------------------------------------------------------- main
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="cfg2")
+    ap.add_argument("--alg", default=None)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile-steps", type=int, default=3)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    w = workload(args.config, args.alg)
+    cfgd = describe(w)
+    N_tok = [sum(len(w.chunks[s.chunk]) if s.cached else len(s.tokens) for s in r) for r in w.requests]
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        vals = []
+        for i in range(args.warmup + args.steps):
+            v, per_req, sample = oracle_sample(w)
+            if i >= args.warmup:
+                vals.append((v, per_req))
+        v = float(np.median([x[0] for x in vals]))
+        ms = float(np.median([x[1] for x in vals])) * 1e3 * len(w.requests)
+        line = {"impl": "reference", "metric": "linked_prefill_tokens_per_s", "value": v, "unit": "tokens/s",
+                "n_gpus": 0, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic", "config": cfgd,
+                "cpu_baseline": {"kind": "oracle", "value": v, "unit": "tokens/s", "cores": cores_used(),
+                                 "sample": sample},
+                "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line))
+        return
+
+    import torch
+    import torch.distributed as dist
+    from paper_2410_15332_b200 import pic as B
+
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    dev = local
+    torch.cuda.set_device(dev)
+    stream = torch.cuda.Stream(dev)
+    m = w.model
+    total_tokens = sum(len(c) for c in w.chunks)
+    max_N = max(N_tok)
+    rows_link = sum(N_tok) if w.alg.startswith("cacheblend") else None
+    with torch.cuda.stream(stream):
+        eng = B.Engine(m, num_blocks=(total_tokens + sum(N_tok)) // 16 + 2 * len(w.chunks) + 64 * len(w.requests),
+                       max_rows=max(4096, rows_link or 0), max_tokens=max(max_N, 512) + 16,
+                       max_requests=len(w.requests), device=dev, stream=stream)
+        ids = eng.generate_context_cache(w.chunks)
+        reqs = [[("cached", ids[s.chunk]) if s.cached else ("tokens", s.tokens) for s in r] for r in w.requests]
+        logits_dev = torch.empty((len(reqs), m.vocab), dtype=torch.float32, device=f"cuda:{dev}")
+
+        def step():
+            if len(reqs) == 1:
+                return [eng.link(reqs[0], w.alg, want_logits=False, logits_dev=logits_dev[0])]
+            return eng.link_batch(reqs, w.alg, want_logits=False)
+
+        for _ in range(args.warmup):
+            step()
+        stream.synchronize()
+        kernels_per_step = eng.stats()["kernels_last_call"]
+
+        def barrier():
+            if world > 1:
+                dist.barrier()
+
+        # ---------------- timed region: device-resident inputs, CUDA events on our stream
+        barrier()
+        torch.cuda.synchronize(dev)
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with ClockSampler(dev) as clk:
+            ev0.record(stream)
+            for _ in range(args.steps):
+                outs = step()
+            ev1.record(stream)
+            ev1.synchronize()
+        torch.cuda.synchronize(dev)
+        barrier()
+        ms = ev0.elapsed_time(ev1)
+        t = torch.tensor([ms], dtype=torch.float64, device=f"cuda:{dev}")
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_max = float(t.item())
+        ms_per_step = ms_max / args.steps
+        tokens_all = sum(N_tok) * args.steps * world
+        value = tokens_all / (ms_max / 1e3)
+
+        # ---------------- e2e: the public call with host buffers (plan H2D + logits D2H per step)
+        barrier()
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0 = time.perf_counter()
+        e0.record(stream)
+        for _ in range(args.steps):
+            if len(reqs) == 1:
+                o = eng.link(reqs[0], w.alg, want_logits=True)
+            else:
+                o = eng.link_batch(reqs, w.alg, want_logits=True)[0]
+        e1.record(stream)
+        e1.synchronize()
+        wall = time.perf_counter() - t0
+        st = eng.stats()
+        te = torch.tensor([wall], dtype=torch.float64, device=f"cuda:{dev}")
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        wall_max = float(te.item())
+        e2e_value = tokens_all / wall_max
+
+        # ---------------- per-kernel CUDA-event profile (separate pass, same stream)
+        eng.set_profiling(True)
+        eng.profile(reset=True)
+        for _ in range(args.profile_steps):
+            step()
+        prof = eng.profile(reset=True)
+        eng.set_profiling(False)
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    P, src = peaks()
+    tot = sum(v["ms"] for v in prof.values())
+    dom_name, dom = max(prof.items(), key=lambda kv: kv[1]["ms"])
+    intensity = dom["flops"] / max(dom["bytes"], 1)
+    ridge = P["bf16_tflops"] * 1e12 / (P["hbm_gbs"] * 1e9)
+    if intensity < ridge:
+        achieved = dom["bytes"] / (dom["ms"] / 1e3) / 1e9
+        roof = {"bound": "hbm", "achieved": achieved, "peak": P["hbm_gbs"], "unit": "GB/s"}
+    else:
+        achieved = dom["flops"] / (dom["ms"] / 1e3) / 1e12
+        roof = {"bound": "tensor", "achieved": achieved, "peak": P["bf16_tflops"], "unit": "TFLOP/s"}
+    roof["frac"] = roof["achieved"] / roof["peak"]
+    roof["traffic"] = None
+    roof["kernel"] = dom_name
+    roof["share_of_step"] = dom["ms"] / tot
+    roof["peak_source"] = f"{src} (MEASURED_PEAKS.json burst)" if src == "measured" else "fallback (B200_PROFILING.md)"
+    roof["launches_per_step"] = dom["launches"] / args.profile_steps
+    roof["how"] = (f"algorithmic bytes/FLOPs per launch (SURVEY §8(d)) over CUDA-event durations of every launch, "
+                   f"{args.profile_steps} profiled steps on the bench stream (graphs off)")
+    breakdown = {k: {"ms_per_step": v["ms"] / args.profile_steps, "launches_per_step": v["launches"] / args.profile_steps,
+                     "GB/s": v["bytes"] / max(v["ms"], 1e-9) / 1e6, "TFLOP/s": v["flops"] / max(v["ms"], 1e-9) / 1e9}
+                 for k, v in sorted(prof.items(), key=lambda kv: -kv[1]["ms"])}
+    line = {"metric": "linked_prefill_tokens_per_s", "value": value, "unit": "tokens/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "ttft_ms_device": ms_per_step if len(reqs) == 1 else None,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic", "config": dict(cfgd, parallelism=f"dp{world} (independent requests)"),
+            "clocks": clk.summary(), "gpu_launches": int(kernels_per_step * args.steps),
+            "e2e": {"value": e2e_value, "unit": "tokens/s", "ttft_ms_host": wall_max / args.steps * 1e3,
+                    "h2d_bytes_per_step": int(st["h2d_bytes_last_call"]),
+                    "d2h_bytes_per_step": int(st["d2h_bytes_last_call"])},
+            "roofline": roof, "kernel_breakdown": breakdown,
+            "context": "paper (A100-80GB, vLLM 0.4.1): LegoLink-16 up to 8x lower TTFT and 7x throughput vs "
+                       "CacheBlend-15 under load (P:303-305); not comparable hardware/workload"}
+    if world == 1 and not args.no_cpu_baseline:
+        v, per_req, sample = oracle_sample(w)
+        line["cpu_baseline"] = {"value": v, "unit": "tokens/s", "cores": cores_used(), "kind": "oracle",
+                                "sample": sample}
+    print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -194,6 +194,17 @@ typedef struct {
 } pic_stats;
 pic_status pic_get_stats(pic_engine* eng, pic_stats* out);
 
+/* Kernel profiling (bench/tests): when on, forwards run without graphs and every launch is bracketed
+ * by CUDA events on its stream.  pic_get_profile synchronises those events and returns per-class
+ * totals (launches, device ms, algorithmic bytes and FLOPs per SURVEY §8(d)); reset != 0 clears. */
+typedef struct {
+  char name[32];
+  int64_t launches;
+  double ms, bytes, flops;
+} pic_kernel_stat;
+pic_status pic_set_profiling(pic_engine* eng, int32_t on);
+pic_status pic_get_profile(pic_engine* eng, pic_kernel_stat* out, int32_t cap, int32_t* n, int32_t reset);
+
 const char* pic_last_error(void);
 const char* pic_status_string(pic_status s);
 

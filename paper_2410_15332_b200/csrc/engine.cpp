@@ -73,6 +73,17 @@ static void dbg_sync(const char* what, cudaStream_t st) {
     dbg_sync(#expr, st);     \
   } while (0)
 
+// Profiling (pic_set_profiling): CUDA events around every launch on the launching stream, tagged
+// with the kernel class and its algorithmic bytes / FLOPs (SURVEY §8(d) formulas).
+static pic_status prof_push(pic_engine* e, cudaStream_t st, const char* name, double bytes, double flops, bool begin);
+
+#define PROF(name, bytes, flops, expr)                                      \
+  do {                                                                      \
+    if (e->profiling) TRY(prof_push(e, st, name, bytes, flops, true));      \
+    CKL(expr);                                                              \
+    if (e->profiling) TRY(prof_push(e, st, name, 0, 0, false));             \
+  } while (0)
+
 #define TRY(expr)                    \
   do {                               \
     pic_status s_ = (expr);          \
@@ -431,6 +442,7 @@ extern "C" void pic_engine_destroy(pic_engine* e) {
     if (e->ev0) cudaEventDestroy(e->ev0);
     if (e->ev1) cudaEventDestroy(e->ev1);
     if (e->cap_stream) cudaStreamDestroy(e->cap_stream);
+    for (cudaEvent_t ev : e->ev_pool) cudaEventDestroy(ev);
   }
   delete e;
 }
@@ -614,7 +626,7 @@ struct Runner {
     *splits_out = g.splits;
     if (debug_sync()) fprintf(stderr, "[pic] gemm M=%d N=%d K=%d bn=%d splits=%d\n", M, N, K, g.bn, g.splits);
     ++launches;
-    CKL(launch_gemm_partial(A, B3[bn_index(g.bn)], e->ws, M, N, K, g.splits, g.bn, st));
+    PROF("gemm", (double)N * K * 2 + (double)M * K * 2 + (double)M * N * 4, 2.0 * M * N * K, launch_gemm_partial(A, B3[bn_index(g.bn)], e->ws, M, N, K, g.splits, g.bn, st));
     return PIC_OK;
   }
 };
@@ -639,11 +651,11 @@ static pic_status enqueue_forward(pic_engine* e, const Fwd& f, const DevPlan& dp
 
   if (!f.k2_src.empty() && f.k2_layer0 < L) {
     ++R.launches;
-    CKL(launch_kv_link(e->Kpool, e->Vpool, dp.k2_src, dp.k2_dst, dp.k2_delta, (int)f.k2_src.size(), f.k2_layer0,
+    PROF("kv_link", 8.0 * D * Hkv * (double)f.k2_src.size() * (L - f.k2_layer0), 0, launch_kv_link(e->Kpool, e->Vpool, dp.k2_src, dp.k2_dst, dp.k2_delta, (int)f.k2_src.size(), f.k2_layer0,
                       L - f.k2_layer0, e->layer_stride, Hkv, D, e->cos_t, e->sin_t, f.rebase, st));
   }
   ++R.launches;
-  CKL(launch_embed(e->E, dp.tok, e->h, f.M, d, st));
+  PROF("embed", 6.0 * f.M * d, 0, launch_embed(e->E, dp.tok, e->h, f.M, d, st));
   int M = f.M;
   float* hc = e->h;
   const int32_t *pos = dp.pos, *slot = dp.slot, *tiles = dp.tiles;
@@ -663,24 +675,24 @@ static pic_status enqueue_forward(pic_engine* e, const Fwd& f, const DevPlan& dp
     char* Vl = Vp + l * lbytes;
     int s = 0;
     ++R.launches;
-    CKL(launch_residual_rmsnorm(hc, prevP, prev_s, w.g1, e->x, nullptr, M, d, eps, st));
+    PROF("rmsnorm", (double)M * d * (8 + 4 * prev_s + 2), 0, launch_residual_rmsnorm(hc, prevP, prev_s, w.g1, e->x, nullptr, M, d, eps, st));
     if (l > 0) TRY(capture(l - 1));
     TRY(R.gemm(e->tm_x, w.tm_qkv, M, qkv, d, &s));
     if (f.cb && l == f.cb_layer) {
       // a9: CacheBlend selection at the check layer (P:170 steps 3-4)
       if (!f.cb_override) {
         R.launches += 3;
-        CKL(launch_cb_deviation(e->ws, s, dp.cb_cand, dp.slot, e->cos_t, e->sin_t, Kl, Vl, e->cb_dev, M, Hq, Hkv, D,
+        PROF("cb_select", (double)M * qkv * 4 * s, 0, launch_cb_deviation(e->ws, s, dp.cb_cand, dp.slot, e->cos_t, e->sin_t, Kl, Vl, e->cb_dev, M, Hq, Hkv, D,
                                st));
-        CKL(launch_cb_rank(e->cb_dev, dp.cb_keep, M, f.cb_T, st));
-        CKL(launch_cb_compact(dp.cb_keep, dp.cb_forced, dp.bt, dp.cb_sel2, dp.cb_pos2, dp.cb_slot2, dp.cb_count, M,
+        PROF("cb_select", 4.0 * M, 0, launch_cb_rank(e->cb_dev, dp.cb_keep, M, f.cb_T, st));
+        PROF("cb_select", 16.0 * M, 0, launch_cb_compact(dp.cb_keep, dp.cb_forced, dp.bt, dp.cb_sel2, dp.cb_pos2, dp.cb_slot2, dp.cb_count, M,
                              st));
       }
       ++R.launches;
-      CKL(launch_gather_rows(hc, dp.cb_sel2, e->h2, f.M2, d, st));
+      PROF("cb_select", 8.0 * f.M2 * d, 0, launch_gather_rows(hc, dp.cb_sel2, e->h2, f.M2, d, st));
       hc = e->h2;
       ++R.launches;
-      CKL(launch_qkv_rope_scatter(e->ws, s, M, dp.cb_sel2, dp.cb_pos2, dp.cb_slot2, e->cos_t, e->sin_t, e->Q, Kl, Vl,
+      PROF("qkv_rope_scatter", (double)f.M2 * qkv * 4 * s + (double)f.M2 * qkv * 2, 0, launch_qkv_rope_scatter(e->ws, s, M, dp.cb_sel2, dp.cb_pos2, dp.cb_slot2, e->cos_t, e->sin_t, e->Q, Kl, Vl,
                                  f.M2, Hq, Hkv, D, st));
       M = f.M2;
       pos = dp.cb_pos2;
@@ -690,11 +702,28 @@ static pic_status enqueue_forward(pic_engine* e, const Fwd& f, const DevPlan& dp
       head_map = dp.head_map2;
     } else {
       ++R.launches;
-      CKL(launch_qkv_rope_scatter(e->ws, s, M, nullptr, pos, slot, e->cos_t, e->sin_t, e->Q, Kl, Vl, M, Hq, Hkv, D,
+      PROF("qkv_rope_scatter", (double)M * qkv * 4 * s + (double)M * qkv * 2, 0, launch_qkv_rope_scatter(e->ws, s, M, nullptr, pos, slot, e->cos_t, e->sin_t, e->Q, Kl, Vl, M, Hq, Hkv, D,
                                  st));
     }
     if (f.compile && l == L - 1) break;  // compile needs only the last layer's K/V
-    // a6 attention
+    // a6 attention — algorithmic work: 4·H_q·D·Σ(p_i+1) FLOPs, K/V of keys 0..max p read once
+    double attn_flops = 0, attn_bytes = 0;
+    if (e->profiling) {
+      const std::vector<int32_t>& pv = (M == f.M) ? f.pos : f.cb_pos2;
+      double sp = 0;
+      if ((int)pv.size() == M)
+        for (int32_t p : pv) sp += p + 1.0;
+      else
+        sp = (double)M * (f.M / 2.0);  // CacheBlend device-side selection: positions not on the host
+      attn_flops = 4.0 * Hq * D * sp;
+      for (size_t q = 0; q < f.seq_bt_off.size(); ++q) {
+        int mx = 0;
+        for (int r = 0; r < (int)f.pos.size(); ++r)
+          if (f.seq[r] == (int)q) mx = std::max(mx, f.pos[r] + 1);
+        attn_bytes += 2.0 * Hkv * D * 2 * mx;
+      }
+      attn_bytes += (double)M * Hq * D * 2 * 2;
+    }
     if (D == 128) {
       AttnArgs a{};
       a.tiles = tiles;
@@ -717,21 +746,21 @@ static pic_status enqueue_forward(pic_engine* e, const Fwd& f, const DevPlan& dp
       a.o_part = e->o_part;
       a.ml_part = e->ml_part;
       R.launches += 2;
-      CKL(launch_attention_tc(e->tm_Q, e->tm_K, e->tm_V, a, st));
-      CKL(launch_attn_combine(e->o_part, e->ml_part, e->Obuf, M, Hq, D, a.n_splits, st));
+      PROF("attention", attn_bytes, attn_flops, launch_attention_tc(e->tm_Q, e->tm_K, e->tm_V, a, st));
+      PROF("attn_combine", (double)a.n_splits * M * Hq * D * 4 + (double)M * Hq * D * 2, 0, launch_attn_combine(e->o_part, e->ml_part, e->Obuf, M, Hq, D, a.n_splits, st));
     } else {
       if (f.cb && l >= f.cb_layer) return fail(PIC_E_VARIANT, "CacheBlend needs head_dim 128 on the GPU path");
       ++R.launches;
-      CKL(launch_attention_simt(e->Q, Kl, Vl, dp.seq, dp.seq_bt_off, dp.bt, pos, e->Obuf, M, Hq, Hkv, D,
+      PROF("attention", attn_bytes, attn_flops, launch_attention_simt(e->Q, Kl, Vl, dp.seq, dp.seq_bt_off, dp.bt, pos, e->Obuf, M, Hq, Hkv, D,
                                (float)(1.0 / std::sqrt((double)D)), st));
     }
     // a7 O projection, residual + a8 MLP
     TRY(R.gemm(e->tm_O, w.tm_o, M, d, Hq * D, &s));
     ++R.launches;
-    CKL(launch_residual_rmsnorm(hc, e->ws, s, w.g2, e->x, nullptr, M, d, eps, st));
+    PROF("rmsnorm", (double)M * d * (8 + 4 * s + 2), 0, launch_residual_rmsnorm(hc, e->ws, s, w.g2, e->x, nullptr, M, d, eps, st));
     TRY(R.gemm(e->tm_x, w.tm_gu, M, 2 * F, d, &s));
     ++R.launches;
-    CKL(launch_swiglu(e->ws, s, e->u, M, F, st));
+    PROF("swiglu", (double)M * 2 * F * 4 * s + (double)M * F * 2, 0, launch_swiglu(e->ws, s, e->u, M, F, st));
     TRY(R.gemm(e->tm_u, w.tm_down, M, d, F, &s));
     prevP = e->ws;
     prev_s = s;
@@ -739,12 +768,12 @@ static pic_status enqueue_forward(pic_engine* e, const Fwd& f, const DevPlan& dp
   if (!f.compile) {
     // a10: final norm of the last rows, LM head, argmax
     ++R.launches;
-    CKL(launch_residual_rmsnorm(hc, prevP, prev_s, e->gf, e->x_last, head_map, M, d, eps, st));
+    PROF("rmsnorm", (double)M * d * (8 + 4 * prev_s) + (double)f.n_head * d * 2, 0, launch_residual_rmsnorm(hc, prevP, prev_s, e->gf, e->x_last, head_map, M, d, eps, st));
     TRY(capture(L - 1));
     int s = 0;
     TRY(R.gemm(e->tm_xlast, e->tm_lm, f.n_head, c.vocab, d, &s));
     ++R.launches;
-    CKL(launch_logits_argmax(e->ws, s, e->logits, e->amax, f.n_head, c.vocab, st));
+    PROF("logits_argmax", (double)f.n_head * c.vocab * 4 * (s + 1), 0, launch_logits_argmax(e->ws, s, e->logits, e->amax, f.n_head, c.vocab, st));
   }
   *n_launch = R.launches;
   return PIC_OK;
@@ -802,7 +831,7 @@ static pic_status run_forward(pic_engine* e, const Fwd& f, cudaStream_t st, bool
   e->h2d_last = (int64_t)pk.n * 4;
 
   int64_t nl = 0;
-  if (!use_graph || debug_hidden || debug_sync()) {
+  if (!use_graph || debug_hidden || debug_sync() || e->profiling) {
     TRY(enqueue_forward(e, f, dp, st, debug_hidden, &nl));
     e->kernels_last = nl;
     return PIC_OK;
@@ -1261,6 +1290,63 @@ extern "C" pic_status pic_read_weights(pic_engine* e, int32_t which, int32_t lay
   if (row0 < 0 || nrows < 0 || row0 + nrows > rows) return fail(PIC_E_INVALID_ARG, "row range out of bounds");
   CK(cudaDeviceSynchronize());
   CK(cudaMemcpy(host_out, base + row0 * cols * 2, nrows * cols * 2, cudaMemcpyDeviceToHost));
+  return PIC_OK;
+}
+
+static pic_status prof_push(pic_engine* e, cudaStream_t st, const char* name, double bytes, double flops,
+                            bool begin) {
+  cudaEvent_t ev;
+  if (e->ev_pool_next < e->ev_pool.size()) {
+    ev = e->ev_pool[e->ev_pool_next];
+  } else {
+    CK(cudaEventCreate(&ev));
+    e->ev_pool.push_back(ev);
+  }
+  ++e->ev_pool_next;
+  CK(cudaEventRecord(ev, st));
+  if (begin) {
+    e->prof_pending.push_back({name, ev, nullptr, bytes, flops});
+  } else {
+    e->prof_pending.back().end = ev;
+  }
+  return PIC_OK;
+}
+
+extern "C" pic_status pic_set_profiling(pic_engine* e, int32_t on) {
+  if (!e) return fail(PIC_E_INVALID_ARG, "NULL engine");
+  e->profiling = on != 0;
+  return PIC_OK;
+}
+
+extern "C" pic_status pic_get_profile(pic_engine* e, pic_kernel_stat* out, int32_t cap, int32_t* n, int32_t reset) {
+  if (!e || !n) return fail(PIC_E_INVALID_ARG, "NULL argument");
+  for (auto& r : e->prof_pending) {
+    if (!r.end) continue;
+    CK(cudaEventSynchronize(r.end));
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, r.begin, r.end));
+    ProfAgg& a = e->prof_agg[r.name];
+    a.launches += 1;
+    a.ms += ms;
+    a.bytes += r.bytes;
+    a.flops += r.flops;
+  }
+  e->prof_pending.clear();
+  e->ev_pool_next = 0;
+  int i = 0;
+  for (auto& kv : e->prof_agg) {
+    if (out && i < cap) {
+      std::memset(&out[i], 0, sizeof(pic_kernel_stat));
+      std::snprintf(out[i].name, sizeof out[i].name, "%s", kv.first.c_str());
+      out[i].launches = kv.second.launches;
+      out[i].ms = kv.second.ms;
+      out[i].bytes = kv.second.bytes;
+      out[i].flops = kv.second.flops;
+    }
+    ++i;
+  }
+  *n = i;
+  if (reset) e->prof_agg.clear();
   return PIC_OK;
 }
 

@@ -69,6 +69,16 @@ struct Fwd {
 };
 
 // Per-request link bookkeeping produced by the planner.
+struct ProfRec {
+  std::string name;
+  cudaEvent_t begin, end;
+  double bytes, flops;
+};
+struct ProfAgg {
+  int64_t launches = 0;
+  double ms = 0, bytes = 0, flops = 0;
+};
+
 struct LinkPlanHost {
   int N = 0;
   std::vector<int32_t> tok;
@@ -125,6 +135,12 @@ struct pic_engine {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   cudaStream_t cap_stream = nullptr;
   int32_t* last_cb_sel2 = nullptr;  // device: CacheBlend selection of the last forward
+  // profiling
+  bool profiling = false;
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_pool_next = 0;
+  std::vector<pic::ProfRec> prof_pending;
+  std::map<std::string, pic::ProfAgg> prof_agg;
   // store
   std::map<pic_cache_id, pic::ChunkRec> store;
   uint64_t next_id = 1;

@@ -69,11 +69,16 @@ class StatsC(C.Structure):
                 ("h2d_bytes_last_call", C.c_int64), ("d2h_bytes_last_call", C.c_int64)]
 
 
+class KernelStatC(C.Structure):
+    _fields_ = [("name", C.c_char * 32), ("launches", C.c_int64), ("ms", C.c_double), ("bytes", C.c_double),
+                ("flops", C.c_double)]
+
+
 # every symbol include/pic.h and include/pic_test.h declare
 EXPORTS = ["pic_arena_bytes", "pic_engine_create", "pic_engine_destroy", "pic_generate_context_cache", "pic_link",
            "pic_link_batch", "pic_plan", "pic_linked_export", "pic_linked_info", "pic_linked_release",
            "pic_cache_export", "pic_cache_info", "pic_expire_cache", "pic_read_weights", "pic_get_stats",
-           "pic_last_error", "pic_status_string", "pic_test_gemm", "pic_test_attention", "pic_test_kv_link"]
+           "pic_last_error", "pic_status_string", "pic_set_profiling", "pic_get_profile", "pic_test_gemm", "pic_test_attention", "pic_test_kv_link"]
 
 _lib = None
 
@@ -108,6 +113,8 @@ def lib() -> C.CDLL:
         L.pic_expire_cache.argtypes = [C.c_void_p, C.c_uint64, P(C.c_int32)]
         L.pic_read_weights.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_int64, C.c_int64, C.c_void_p]
         L.pic_get_stats.argtypes = [C.c_void_p, P(StatsC)]
+        L.pic_set_profiling.argtypes = [C.c_void_p, C.c_int32]
+        L.pic_get_profile.argtypes = [C.c_void_p, P(KernelStatC), C.c_int32, P(C.c_int32), C.c_int32]
         L.pic_test_gemm.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
                                     C.c_void_p]
         L.pic_test_attention.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32,
@@ -369,6 +376,16 @@ class Engine:
             out = np.empty((nrows, cols), dtype=np.uint16)
         check(lib().pic_read_weights(self._h, which, layer, row0, nrows, out.ctypes.data))
         return out
+
+    def set_profiling(self, on: bool) -> None:
+        check(lib().pic_set_profiling(self._h, int(on)))
+
+    def profile(self, reset: bool = True) -> dict:
+        arr = (KernelStatC * 64)()
+        n = C.c_int32()
+        check(lib().pic_get_profile(self._h, arr, 64, C.byref(n), int(reset)))
+        return {arr[i].name.decode(): {"launches": arr[i].launches, "ms": arr[i].ms, "bytes": arr[i].bytes,
+                                       "flops": arr[i].flops} for i in range(n.value)}
 
     def stats(self) -> dict:
         s = StatsC()
