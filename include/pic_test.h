@@ -32,6 +32,11 @@ pic_status pic_test_kv_link(uint16_t* Kpool, uint16_t* Vpool, int32_t n_layers, 
                             int32_t D, const int32_t* src_slot, const int32_t* dst_slot, const int32_t* delta,
                             int32_t n_rows, int32_t layer0, int32_t rebase, double theta, int32_t max_pos);
 
+/* GEMM timing: average device µs per launch of the tcgen05 GEMM over `iters` back-to-back launches
+ * (weights cycled through > 512 MB of copies so each launch streams from HBM). */
+pic_status pic_bench_gemm(int32_t M, int32_t N, int32_t K, int32_t bn, int32_t splits, int32_t iters,
+                          float* us_per_launch);
+
 #ifdef __cplusplus
 }
 #endif

@@ -587,34 +587,20 @@ struct PlanPack {  // dynamic packing of the plan arrays into one H2D copy
   }
 };
 
-static int choose_attn_splits(int n_tiles, int Hkv, int max_kv_tiles, int M, int cap_rows) {
-  const int ctas = n_tiles * Hkv;
-  int s = std::max(1, std::min({(2 * 148 + ctas - 1) / ctas, std::max(1, max_kv_tiles / 2), 16}));
-  while (s > 1 && (int64_t)s * M > cap_rows) --s;
-  return s;
-}
-
 struct GemmChoice {
   int bn, splits;
 };
 
+// Tile / split-K choice (measured, scripts/gemm_sweep.py): a CTA streams ~40 GB/s of weights, so a
+// GEMM wants every SM busy in ONE wave.  bn=128 with split-K when its tiles fit in a wave (skinny M:
+// QKV 48x3, O and down 32x4 CTAs), otherwise bn=256 (fewer A re-reads, full-rate UMMA N=256).
 static GemmChoice choose_gemm(const pic_engine* e, int M, int N, int K) {
-  const int kblk = K / 64;
-  GemmChoice best{128, 1};
-  double best_eff = -1;
-  for (int bi = 2; bi >= 0; --bi) {
-    const int bn = kBN[bi];
-    const int tiles = ((M + 127) / 128) * ((N + bn - 1) / bn);
-    int s = std::max(1, std::min(148 / std::max(tiles, 1), std::max(1, kblk / 2)));
-    while (s > 1 && (size_t)s * M * N > e->ws_floats) --s;
-    const int ctas = tiles * s;
-    const double eff = (double)ctas / (148.0 * ((ctas + 147) / 148));
-    if (eff > best_eff + 1e-9) {
-      best_eff = eff;
-      best = {bn, s};
-    }
-  }
-  return best;
+  const int kblk = K / 64, mt = (M + 127) / 128;
+  const int t128 = mt * ((N + 127) / 128), t256 = mt * ((N + 255) / 256);
+  GemmChoice g = t128 <= 148 ? GemmChoice{128, 148 / t128} : GemmChoice{256, std::max(1, 148 / t256)};
+  g.splits = std::max(1, std::min(g.splits, kblk / 4));
+  while (g.splits > 1 && (size_t)g.splits * M * N > e->ws_floats) --g.splits;
+  return g;
 }
 
 struct Runner {
@@ -636,6 +622,7 @@ struct DevPlan {
   int32_t *tok, *pos, *slot, *seq, *tiles, *seq_bt_off, *bt, *k2_src, *k2_dst, *k2_delta, *head_map;
   int32_t *cb_cand, *cb_forced, *cb_sel2, *cb_pos2, *cb_slot2, *cb_keep, *cb_count, *tiles2, *head_map2;
   int n_tiles, n_tiles2;
+  int32_t *attn_work, *attn_nsplit, *attn_work2, *attn_nsplit2;
 };
 
 static pic_status enqueue_forward(pic_engine* e, const Fwd& f, const DevPlan& dp, cudaStream_t st, float* debug_hidden,
@@ -726,28 +713,27 @@ static pic_status enqueue_forward(pic_engine* e, const Fwd& f, const DevPlan& dp
     }
     if (D == 128) {
       AttnArgs a{};
+      a.work = (tiles == dp.tiles) ? dp.attn_work : dp.attn_work2;
+      a.n_work = (tiles == dp.tiles) ? f.attn_n_work : f.attn_n_work2;
       a.tiles = tiles;
       a.seq_bt_off = dp.seq_bt_off;
       a.bt = dp.bt;
       a.row_pos = pos;
-      a.n_tiles = n_tiles;
       a.M = M;
       a.Hq = Hq;
       a.Hkv = Hkv;
       a.layer = l;
       a.num_blocks = (int)e->lim.num_blocks;
-      int max_len = 0;
-      for (size_t q = 0; q < f.seq_bt_off.size(); ++q) {
-        const int end = (q + 1 < f.seq_bt_off.size()) ? f.seq_bt_off[q + 1] : (int)f.bt.size();
-        max_len = std::max(max_len, (end - f.seq_bt_off[q]) * 16);
-      }
-      a.n_splits = choose_attn_splits(n_tiles, Hkv, (max_len + 127) / 128, M, e->attn_rows_cap);
       a.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)D));
       a.o_part = e->o_part;
       a.ml_part = e->ml_part;
       R.launches += 2;
       PROF("attention", attn_bytes, attn_flops, launch_attention_tc(e->tm_Q, e->tm_K, e->tm_V, a, st));
-      PROF("attn_combine", (double)a.n_splits * M * Hq * D * 4 + (double)M * Hq * D * 2, 0, launch_attn_combine(e->o_part, e->ml_part, e->Obuf, M, Hq, D, a.n_splits, st));
+      PROF("attn_combine", (double)((tiles == dp.tiles) ? f.attn_max_split : f.attn_max_split2) * M * Hq * D * 4 +
+                                 (double)M * Hq * D * 2,
+           0,
+           launch_attn_combine(e->o_part, e->ml_part, (tiles == dp.tiles) ? dp.attn_nsplit : dp.attn_nsplit2, e->Obuf,
+                               M, Hq, D, st));
     } else {
       if (f.cb && l >= f.cb_layer) return fail(PIC_E_VARIANT, "CacheBlend needs head_dim 128 on the GPU path");
       ++R.launches;
@@ -781,9 +767,41 @@ static pic_status enqueue_forward(pic_engine* e, const Fwd& f, const DevPlan& dp
 
 static void add_sig(std::vector<int64_t>& sig, const Fwd& f, const DevPlan& dp) {
   sig = {f.M,  dp.n_tiles, (int64_t)f.seq_bt_off.size(), (int64_t)f.bt.size(), (int64_t)f.k2_src.size(), f.k2_layer0,
-         f.n_head, f.compile, f.rebase, f.cb, f.cb_layer, f.cb_T, f.M2, f.cb_override, dp.n_tiles2};
+         f.n_head, f.compile, f.rebase, f.cb, f.cb_layer, f.cb_T, f.M2, f.cb_override, dp.n_tiles2, f.attn_n_work,
+         f.attn_n_work2};
   // attention split choice depends on the per-sequence block-table lengths
   for (size_t q = 0; q < f.seq_bt_off.size(); ++q) sig.push_back(f.seq_bt_off[q]);
+}
+
+// Balanced split-KV schedules for the attention of this forward (host-known positions; CacheBlend's
+// post-check rows use the request length as the causal extent and the kernel clamps).
+static void schedule_attention(pic_engine* e, Fwd& f) {
+  const int Hkv = e->cfg.n_kv_heads;
+  auto build = [&](const std::vector<int32_t>& tiles, const std::vector<int32_t>* pos, int M, int fallback_len,
+                   std::vector<int32_t>& work, std::vector<int32_t>& nsplit, int& n_work, int& max_split) {
+    const int nt = (int)tiles.size() / 3;
+    std::vector<int> n_kv(nt);
+    for (int t = 0; t < nt; ++t) {
+      int mx = fallback_len - 1;
+      if (pos) {
+        mx = 0;
+        for (int r = 0; r < tiles[3 * t + 2]; ++r) mx = std::max(mx, (*pos)[tiles[3 * t + 1] + r]);
+      }
+      n_kv[t] = mx / 128 + 1;
+    }
+    const int cap = std::max(1, std::min(32, e->attn_rows_cap / std::max(M, 1)));
+    long total = 0;
+    for (int v : n_kv) total += v;
+    work.assign(4 * (size_t)(total + nt), 0);
+    nsplit.assign(M, 1);
+    max_split = attn_schedule(tiles.data(), nt, n_kv.data(), Hkv, 148, cap, work.data(), &n_work, nsplit.data());
+    work.resize(4 * (size_t)n_work);
+  };
+  build(f.tiles, &f.pos, f.M, 0, f.attn_work, f.attn_nsplit, f.attn_n_work, f.attn_max_split);
+  if (f.cb) {
+    const int N = f.M;  // single request, all rows at layer 0
+    build(f.tiles2, nullptr, f.M2, N, f.attn_work2, f.attn_nsplit2, f.attn_n_work2, f.attn_max_split2);
+  }
 }
 
 static pic_status run_forward(pic_engine* e, const Fwd& f, cudaStream_t st, bool use_graph, float* debug_hidden) {
@@ -808,6 +826,8 @@ static pic_status run_forward(pic_engine* e, const Fwd& f, cudaStream_t st, bool
   dp.k2_dst = pk.put(f.k2_dst);
   dp.k2_delta = pk.put(f.k2_delta);
   dp.head_map = pk.put(f.head_map);
+  dp.attn_work = pk.put(f.attn_work);
+  dp.attn_nsplit = pk.put(f.attn_nsplit);
   dp.n_tiles = (int)f.tiles.size() / 3;
   if (f.cb) {
     dp.cb_cand = pk.put(f.cb_cand);
@@ -820,6 +840,8 @@ static pic_status run_forward(pic_engine* e, const Fwd& f, cudaStream_t st, bool
     dp.tiles2 = pk.put(f.tiles2);
     dp.head_map2 = pk.put(f.head_map2);
     dp.n_tiles2 = (int)f.tiles2.size() / 3;
+    dp.attn_work2 = pk.put(f.attn_work2);
+    dp.attn_nsplit2 = pk.put(f.attn_nsplit2);
     e->last_cb_sel2 = dp.cb_sel2;
   }
   if (pk.n > e->plan_cap_ints) return fail(PIC_E_CAPACITY, "plan of %zu ints exceeds %zu", pk.n, e->plan_cap_ints);
@@ -920,6 +942,7 @@ extern "C" pic_status pic_generate_context_cache(pic_engine* e, const int32_t* c
     f.compile = true;
     auto flush = [&]() -> pic_status {
       if (f.M == 0) return PIC_OK;
+      schedule_attention(e, f);
       pic_status s = run_forward(e, f, st, false, nullptr);
       f = Fwd();
       f.compile = true;
@@ -1104,6 +1127,7 @@ static pic_status link_impl(pic_engine* e, int32_t n_req, const pic_segment* con
   }
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const bool use_graph = pr->use_graph != 0;
+  schedule_attention(e, f);
   pic_status s = run_forward(e, f, st, use_graph, pr->debug_hidden);
   if (s != PIC_OK) {
     rollback();

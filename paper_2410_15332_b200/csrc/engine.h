@@ -66,6 +66,9 @@ struct Fwd {
   int cb_layer = 1, cb_T = 0, M2 = 0;
   bool cb_override = false;
   std::vector<int32_t> cb_cand, cb_forced, cb_sel2, cb_pos2, cb_slot2, tiles2, head_map2;
+  // attention split-KV schedules (main rows, and CacheBlend rows after the check)
+  std::vector<int32_t> attn_work, attn_nsplit, attn_work2, attn_nsplit2;
+  int attn_n_work = 0, attn_n_work2 = 0, attn_max_split = 1, attn_max_split2 = 1;
 };
 
 // Per-request link bookkeeping produced by the planner.

@@ -20,8 +20,16 @@
 //     cross-split max/sum is a warp-shuffle reduction.
 #include <cuda.h>
 
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.h"
+
+#define CUDA_TRY_LAUNCH(x)              \
+  do {                                 \
+    cudaError_t e__ = (x);             \
+    if (e__ != cudaSuccess) return e__; \
+  } while (0)
 
 namespace pic {
 
@@ -40,6 +48,7 @@ template <int G>
 __global__ void __launch_bounds__(192, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                    const __grid_constant__ CUtensorMap tmV, const AttnArgs a) {
+  griddep_launch();
   using namespace attn;
   constexpr int QPT = 128 / G;  // queries per tile
   extern __shared__ uint8_t smem_raw[];
@@ -53,7 +62,10 @@ __global__ void __launch_bounds__(192, 1)
   const uint32_t s_full = smem_u32(bars + 9), p_full = smem_u32(bars + 11), o_full = smem_u32(bars + 13);
 
   const int warp = warp_id(), lane = lane_id();
-  const int tile = blockIdx.x, g = blockIdx.y, split = blockIdx.z;
+  // work item (host-balanced split-KV schedule): q-tile, KV-tile range [j0, j1), split slot
+  const int* wk = a.work + 4 * blockIdx.x;
+  const int tile = wk[0], split = wk[3], g = blockIdx.y;
+  griddep_wait();  // Q, row positions and the linked K/V come from upstream kernels
   const int seq = a.tiles[3 * tile], row_start = a.tiles[3 * tile + 1], row_count = a.tiles[3 * tile + 2];
 
   // causal extent of this tile: keys 0..max_p (rows are sorted, but take the max anyway)
@@ -62,8 +74,7 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) max_p = max(max_p, __shfl_xor_sync(0xffffffffu, max_p, o));
   const int n_kv = max_p / 128 + 1;
-  const int chunk = (n_kv + a.n_splits - 1) / a.n_splits;
-  const int j0 = split * chunk, j1 = min(n_kv, j0 + chunk);
+  const int j0 = wk[1], j1 = min(n_kv, wk[2]);  // positions may be device-side (CacheBlend): clamp
   const int n = max(0, j1 - j0);
   const int* bt = a.bt + a.seq_bt_off[seq];
   const int last_blk = max_p / 16;
@@ -132,7 +143,8 @@ __global__ void __launch_bounds__(192, 1)
         for (int kk = 0; kk < 8; ++kk) {
           const uint32_t pa = base + kP + (2 * pb + (kk >> 2)) * kTile + (kk & 3) * 32;
           const uint32_t vb = base + kV + (2 * pb) * kTile + kk * 2048;  // 16 keys x 128 B
-          umma_bf16(tmem + 256 + pb * 128, sdesc_sw128(pa, 16, 1024), sdesc_sw128(vb, kTile, 1024), idO, kk > 0);
+          // O accumulates in TMEM across KV tiles (rescaled by the softmax warps when needed)
+          umma_bf16(tmem + 256, sdesc_sw128(pa, 16, 1024), sdesc_sw128(vb, kTile, 1024), idO, (u | kk) != 0);
         }
         umma_commit(o_full + 8 * pb);
         umma_commit(v_empty + 8 * pb);
@@ -164,10 +176,11 @@ __global__ void __launch_bounds__(192, 1)
     const int head = g * G + hh;
     const int pos = valid ? a.row_pos[row] : max_p;
     const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
-    float o[128];
-#pragma unroll
-    for (int i = 0; i < 128; ++i) o[i] = 0.f;
-    float m = -INFINITY, l = 0.f;
+    const uint32_t oAddr = tmem + lane_addr + 256;
+    // m_ref: the max the current O / l are scaled to.  It is raised only when a row's max grows by
+    // more than 2^8 (then O in TMEM and l are rescaled), so exp2 arguments stay <= 8 and the common
+    // case never touches O (FA4-style lazy rescale; exact because the final normalisation uses m_ref).
+    float m_ref = -INFINITY, l = 0.f;
     for (int t = 0; t < n; ++t) {
       const int sb = t & 1;
       const uint32_t ph = (t >> 1) & 1;
@@ -175,80 +188,76 @@ __global__ void __launch_bounds__(192, 1)
       mbar_wait(s_full + 8 * sb, ph);
       tc_fence_after();
       const uint32_t sAddr = tmem + lane_addr + sb * 128;
+      float sv[128];
+      tmem_ld128(sAddr, sv);
       float mx = -INFINITY;
-#pragma unroll 1
-      for (int c = 0; c < 4; ++c) {
-        float v[32];
-        tmem_ld32(sAddr + c * 32, v);
 #pragma unroll
-        for (int i = 0; i < 32; ++i)
-          if (key0 + c * 32 + i <= pos) mx = fmaxf(mx, v[i] * a.scale_log2);
+      for (int i = 0; i < 128; ++i) {
+        sv[i] = (key0 + i <= pos) ? sv[i] * a.scale_log2 : -INFINITY;
+        mx = fmaxf(mx, sv[i]);
       }
-      const float m_new = fmaxf(m, mx);
-      const float m_use = (m_new == -INFINITY) ? 0.f : m_new;
-      const float alpha = exp2f(m - m_use);
+      // tcgen05.ld/st are warp-collective: the rescale runs for the whole warp if any row needs it
+      const bool grow = mx > m_ref + 8.f;
+      const bool need = grow && m_ref != -INFINITY;
+      if (__any_sync(0xffffffffu, need)) {
+        // rescale O (all PV up to tile t-1 must have landed) and l to the new reference
+        mbar_wait(o_full + 8 * ((t - 1) & 1), ((t - 1) >> 1) & 1);
+        tc_fence_after();
+        const float alpha = need ? exp2f(m_ref - mx) : 1.f;
+#pragma unroll 1
+        for (int c = 0; c < 4; ++c) {
+          float ov[32];
+          tmem_ld32(oAddr + c * 32, ov);
+#pragma unroll
+          for (int i = 0; i < 32; ++i) ov[i] *= alpha;
+          tmem_st32(oAddr + c * 32, ov);
+        }
+        tmem_wait_st();
+        l *= alpha;
+      }
+      if (grow) m_ref = mx;
+      // P buffer sb was read by PV_{t-2}: it must have completed
+      if (t >= 2) mbar_wait(o_full + 8 * (t & 1), ((t - 2) >> 1) & 1);
       float sum = 0.f;
       uint8_t* pbuf = smem + kP + (2 * sb) * kTile + r * 128;
-#pragma unroll 1
-      for (int c = 0; c < 4; ++c) {
-        float v[32];
-        tmem_ld32(sAddr + c * 32, v);
-        uint32_t pk[16];
+      const float mu = (m_ref == -INFINITY) ? 0.f : m_ref;
 #pragma unroll
-        for (int i = 0; i < 32; i += 2) {
-          const int k = key0 + c * 32 + i;
-          const float p0 = (k <= pos) ? exp2f(v[i] * a.scale_log2 - m_use) : 0.f;
-          const float p1 = (k + 1 <= pos) ? exp2f(v[i + 1] * a.scale_log2 - m_use) : 0.f;
+      for (int c = 0; c < 16; ++c) {  // 16 chunks of 8 keys = 16 bytes of bf16 P
+        uint32_t pk[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float p0 = exp2f(sv[8 * c + 2 * e] - mu), p1 = exp2f(sv[8 * c + 2 * e + 1] - mu);
           sum += p0 + p1;
-          pk[i / 2] = pack_bf16(p0, p1);
+          pk[e] = pack_bf16(p0, p1);
         }
-        // 32 keys = 4 16-byte chunks; chunk index within the 64-key half, swizzled by row
-        const int half = c >> 1;
-#pragma unroll
-        for (int cc = 0; cc < 4; ++cc) {
-          const int chunk16 = (c & 1) * 4 + cc;
-          uint4* dst = reinterpret_cast<uint4*>(pbuf + half * kTile + ((chunk16 ^ (r & 7)) << 4));
-          *dst = make_uint4(pk[4 * cc], pk[4 * cc + 1], pk[4 * cc + 2], pk[4 * cc + 3]);
-        }
+        const int half = c >> 3, chunk16 = c & 7;
+        *reinterpret_cast<uint4*>(pbuf + half * kTile + ((chunk16 ^ (r & 7)) << 4)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
       }
-      l = l * alpha + sum;
-      m = m_new;
+      l += sum;
       fence_async_smem();
       tc_fence_before();
       mbar_arrive(p_full + 8 * sb);
-      if (t >= 1) {
-        const int ob = (t - 1) & 1;
-        mbar_wait(o_full + 8 * ob, ((t - 1) >> 1) & 1);
-        tc_fence_after();
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          float v[32];
-          tmem_ld32(tmem + lane_addr + 256 + ob * 128 + c * 32, v);
-#pragma unroll
-          for (int i = 0; i < 32; ++i) o[c * 32 + i] += v[i];
-        }
-      }
-#pragma unroll
-      for (int i = 0; i < 128; ++i) o[i] *= alpha;
     }
     if (n > 0) {
-      const int ob = (n - 1) & 1;
-      mbar_wait(o_full + 8 * ob, ((n - 1) >> 1) & 1);
+      mbar_wait(o_full + 8 * ((n - 1) & 1), ((n - 1) >> 1) & 1);
       tc_fence_after();
-#pragma unroll
+    }
+    const size_t idx = ((size_t)split * a.M + row) * a.Hq + head;
+    float4* dst = reinterpret_cast<float4*>(a.o_part + idx * 128);
+    if (n > 0) {
+#pragma unroll 1
       for (int c = 0; c < 4; ++c) {
-        float v[32];
-        tmem_ld32(tmem + lane_addr + 256 + ob * 128 + c * 32, v);
+        float ov[32];
+        tmem_ld32(oAddr + c * 32, ov);  // warp-collective: all lanes load, valid rows store
+        if (valid)
 #pragma unroll
-        for (int i = 0; i < 32; ++i) o[c * 32 + i] += v[i];
+          for (int i = 0; i < 8; ++i) dst[c * 8 + i] = make_float4(ov[4 * i], ov[4 * i + 1], ov[4 * i + 2], ov[4 * i + 3]);
       }
+    } else if (valid) {
+      for (int i = 0; i < 32; ++i) dst[i] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
     if (valid) {
-      const size_t idx = ((size_t)split * a.M + row) * a.Hq + head;
-      float4* dst = reinterpret_cast<float4*>(a.o_part + idx * 128);
-#pragma unroll
-      for (int i = 0; i < 32; ++i) dst[i] = make_float4(o[4 * i], o[4 * i + 1], o[4 * i + 2], o[4 * i + 3]);
-      a.ml_part[2 * idx] = m;
+      a.ml_part[2 * idx] = m_ref;
       a.ml_part[2 * idx + 1] = l;
     }
   }
@@ -260,11 +269,42 @@ __global__ void __launch_bounds__(192, 1)
   }
 }
 
+int attn_schedule(const int32_t* tiles, int n_tiles, const int* n_kv, int Hkv, int target_ctas, int max_split,
+                  int32_t* work, int* n_work, int32_t* row_nsplit) {
+  long total = 0;
+  for (int t = 0; t < n_tiles; ++t) total += n_kv[t];
+  total *= Hkv;
+  long budget = std::max(1L, (total + target_ctas - 1) / target_ctas);
+  // grow the per-CTA budget until the work list fits in one wave of target_ctas CTAs
+  for (;; ++budget) {
+    long ctas = 0;
+    for (int t = 0; t < n_tiles; ++t) ctas += std::min<long>(max_split, (n_kv[t] + budget - 1) / budget);
+    if (ctas * Hkv <= target_ctas || budget >= 1 << 20) break;
+  }
+  int w = 0, mx = 1;
+  for (int t = 0; t < n_tiles; ++t) {
+    int pieces = (int)std::min<long>(max_split, std::max(1L, (n_kv[t] + budget - 1) / budget));
+    const int chunk = (n_kv[t] + pieces - 1) / pieces;
+    pieces = (n_kv[t] + chunk - 1) / chunk;
+    for (int p = 0; p < pieces; ++p) {
+      work[4 * w] = t;
+      work[4 * w + 1] = p * chunk;
+      work[4 * w + 2] = std::min(n_kv[t], (p + 1) * chunk);
+      work[4 * w + 3] = p;
+      ++w;
+    }
+    for (int r = 0; r < tiles[3 * t + 2]; ++r) row_nsplit[tiles[3 * t + 1] + r] = pieces;
+    mx = std::max(mx, pieces);
+  }
+  *n_work = w;
+  return mx;
+}
+
 template <int G>
 static cudaError_t launch_attn_g(const CUtensorMap& tmQ, const CUtensorMap& tmK, const CUtensorMap& tmV,
                                  const AttnArgs& a, cudaStream_t st) {
-  dim3 grid(a.n_tiles, a.Hkv, a.n_splits);
-  attn_tc_kernel<G><<<grid, 192, attn::kSmem, st>>>(tmQ, tmK, tmV, a);
+  dim3 grid(a.n_work, a.Hkv);
+  CUDA_TRY_LAUNCH(launch_k(attn_tc_kernel<G>, dim3(grid), dim3(192), attn::kSmem, st, tmQ, tmK, tmV, a));
   return cudaGetLastError();
 }
 
@@ -291,10 +331,13 @@ cudaError_t launch_attention_tc(const CUtensorMap& tmQ, const CUtensorMap& tmK, 
 // split-KV combine: one warp per (row, head); lane s holds split s's (m, l); cross-split max and
 // sum are warp-shuffle reductions; each lane then merges 4 of the 128 output columns.
 __global__ void attn_combine_kernel(const float* __restrict__ o_part, const float* __restrict__ ml_part,
-                                    __nv_bfloat16* __restrict__ O, int M, int Hq, int n_splits) {
+                                    const int32_t* __restrict__ row_nsplit, __nv_bfloat16* __restrict__ O, int M,
+                                    int Hq) {
+  PIC_PDL_ENTRY();
   const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (wid >= M * Hq) return;
+  const int n_splits = row_nsplit[wid / Hq];
   const size_t stride = (size_t)M * Hq;
   float ms = -INFINITY, ls = 0.f;
   if (lane < n_splits) {
@@ -305,6 +348,7 @@ __global__ void attn_combine_kernel(const float* __restrict__ o_part, const floa
   const float w = (lane < n_splits && ms != -INFINITY) ? exp2f(ms - mmax) : 0.f;
   const float L = warp_sum(w * ls);
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 4
   for (int s = 0; s < n_splits; ++s) {
     const float ws = __shfl_sync(0xffffffffu, w, s);
     if (ws == 0.f) continue;
@@ -319,12 +363,12 @@ __global__ void attn_combine_kernel(const float* __restrict__ o_part, const floa
   reinterpret_cast<uint2*>(O + (size_t)wid * 128)[lane] = pk;
 }
 
-cudaError_t launch_attn_combine(const float* o_part, const float* ml_part, void* O, int M, int Hq, int D,
-                                int n_splits, cudaStream_t st) {
-  if (D != 128 || n_splits > 32) return cudaErrorInvalidValue;
+cudaError_t launch_attn_combine(const float* o_part, const float* ml_part, const int32_t* row_nsplit, void* O, int M,
+                                int Hq, int D, cudaStream_t st) {
+  if (D != 128) return cudaErrorInvalidValue;
   const int warps = M * Hq;
-  attn_combine_kernel<<<(warps + 7) / 8, 256, 0, st>>>(o_part, ml_part, reinterpret_cast<__nv_bfloat16*>(O), M, Hq,
-                                                       n_splits);
+  CUDA_TRY_LAUNCH(launch_k(attn_combine_kernel, dim3((warps + 7) / 8), dim3(256), 0, st, o_part, ml_part, row_nsplit,
+                           reinterpret_cast<__nv_bfloat16*>(O), M, Hq));
   return cudaGetLastError();
 }
 
@@ -337,6 +381,7 @@ __global__ void attn_simt_kernel(const __nv_bfloat16* __restrict__ Q, const __nv
                                  const int32_t* __restrict__ seq_bt_off, const int32_t* __restrict__ bt,
                                  const int32_t* __restrict__ row_pos, __nv_bfloat16* __restrict__ O, int M, int Hq,
                                  int Hkv, float scale) {
+  PIC_PDL_ENTRY();
   const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (wid >= M * Hq) return;
@@ -392,9 +437,9 @@ cudaError_t launch_attention_simt(const void* Q, const void* Kpool_l, const void
   auto v = reinterpret_cast<const __nv_bfloat16*>(Vpool_l);
   auto o = reinterpret_cast<__nv_bfloat16*>(O);
   switch (D) {
-    case 16: attn_simt_kernel<16><<<grid, block, 0, st>>>(q, k, v, row_seq, seq_bt_off, bt, row_pos, o, M, Hq, Hkv, scale); break;
-    case 32: attn_simt_kernel<32><<<grid, block, 0, st>>>(q, k, v, row_seq, seq_bt_off, bt, row_pos, o, M, Hq, Hkv, scale); break;
-    case 64: attn_simt_kernel<64><<<grid, block, 0, st>>>(q, k, v, row_seq, seq_bt_off, bt, row_pos, o, M, Hq, Hkv, scale); break;
+    case 16: CUDA_TRY_LAUNCH(launch_k(attn_simt_kernel<16>, dim3(grid), dim3(block), 0, st, q, k, v, row_seq, seq_bt_off, bt, row_pos, o, M, Hq, Hkv, scale)); break;
+    case 32: CUDA_TRY_LAUNCH(launch_k(attn_simt_kernel<32>, dim3(grid), dim3(block), 0, st, q, k, v, row_seq, seq_bt_off, bt, row_pos, o, M, Hq, Hkv, scale)); break;
+    case 64: CUDA_TRY_LAUNCH(launch_k(attn_simt_kernel<64>, dim3(grid), dim3(block), 0, st, q, k, v, row_seq, seq_bt_off, bt, row_pos, o, M, Hq, Hkv, scale)); break;
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();

@@ -18,6 +18,12 @@
 #include "common.cuh"
 #include "kernels.h"
 
+#define CUDA_TRY_LAUNCH(x)              \
+  do {                                 \
+    cudaError_t e__ = (x);             \
+    if (e__ != cudaSuccess) return e__; \
+  } while (0)
+
 namespace pic {
 
 template <int BN, int STAGES>
@@ -46,6 +52,7 @@ __global__ void __launch_bounds__(192, 1)
   const int n0 = blockIdx.x * BN, m0 = blockIdx.y * 128;
   const int kb0 = blockIdx.z * kblk_per_split;
   const int nkb = min(kblk_per_split, kblk_total - kb0);
+  griddep_launch();
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -65,7 +72,16 @@ __global__ void __launch_bounds__(192, 1)
     if (lane == 0 && nkb > 0) {
       tma_prefetch(&tmA);
       tma_prefetch(&tmB);
-      for (int i = 0; i < nkb; ++i) {
+      // Weights do not depend on the previous kernel: stream the first stages of B while it
+      // drains (PDL), then wait for it before loading the activations A.
+      const int pre = min(nkb, STAGES);
+      for (int i = 0; i < pre; ++i) {
+        mbar_expect_tx(full0 + 8 * i, S::kStage);
+        tma_load_2d(smem_u32(sB + i * S::kB), &tmB, full0 + 8 * i, (kb0 + i) * 64, n0);
+      }
+      griddep_wait();
+      for (int i = 0; i < pre; ++i) tma_load_2d(smem_u32(sA + i * S::kA), &tmA, full0 + 8 * i, (kb0 + i) * 64, m0);
+      for (int i = pre; i < nkb; ++i) {
         const int s = i % STAGES;
         const uint32_t ph = (i / STAGES) & 1;
         mbar_wait(empty0 + 8 * s, ph ^ 1);
@@ -93,6 +109,7 @@ __global__ void __launch_bounds__(192, 1)
       umma_commit(accf);
     }
   } else {
+    griddep_wait();  // `out` may still be read by the previous kernel
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     const int row = m0 + q * 32 + lane;
     float* orow = out + (size_t)blockIdx.z * M * N + (size_t)row * N;
@@ -131,7 +148,7 @@ static cudaError_t launch_gemm_t(const CUtensorMap& A, const CUtensorMap& B, flo
   const int kblk = K / 64;
   const int per = (kblk + splits - 1) / splits;
   dim3 grid((N + BN - 1) / BN, (M + 127) / 128, splits);
-  kern<<<grid, 192, S::kBytes, st>>>(A, B, out, M, N, kblk, per);
+  CUDA_TRY_LAUNCH(launch_k(kern, dim3(grid), dim3(192), S::kBytes, st, A, B, out, M, N, kblk, per));
   return cudaGetLastError();
 }
 

@@ -4,7 +4,28 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <utility>
+
 namespace pic {
+
+// PDL on by default; PIC_NO_PDL=1 disables (debugging).
+bool pdl_enabled();
+
+// Launch with the programmatic-stream-serialization attribute (works inside graph capture).
+template <typename... KArgs, typename... Args>
+cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 // Set dynamic-smem attributes of every kernel instance (call once, outside graph capture).
 cudaError_t prepare_kernels();
@@ -44,19 +65,25 @@ cudaError_t launch_gemm_partial(const CUtensorMap& A, const CUtensorMap& B, floa
 
 // ---- a6: sparse-query causal attention (tcgen05, D = 128) + split-KV combine ----------------
 struct AttnArgs {
+  const int32_t* work;       // [n_work][4] (q-tile, kv-tile begin, kv-tile end, split slot): balanced split-KV
   const int32_t* tiles;      // [n_tiles][3] (seq, row_start, row_count)
   const int32_t* seq_bt_off; // per sequence: offset into bt
   const int32_t* bt;         // block tables
   const int32_t* row_pos;    // [M] absolute position of every query row
-  int n_tiles, M, Hq, Hkv, layer, num_blocks, n_splits;
+  int n_work, M, Hq, Hkv, layer, num_blocks;
   float scale_log2;
-  float* o_part;             // [n_splits][M][Hq][128]
-  float* ml_part;            // [n_splits][M][Hq][2]
+  float* o_part;             // [max splits][M][Hq][128]
+  float* ml_part;            // [max splits][M][Hq][2]
 };
+// Balanced split-KV schedule: each q-tile t (KV extent n_kv[t] 128-key tiles) gets
+// ceil(n_kv[t] / budget) splits, budget = ceil(Σ n_kv · Hkv / target_ctas); splits <= 32.
+// Writes work items (tile, j0, j1, slot) and the per-row split count; returns the max splits.
+int attn_schedule(const int32_t* tiles, int n_tiles, const int* n_kv, int Hkv, int target_ctas, int max_split,
+                  int32_t* work_out /*[4 * cap]*/, int* n_work, int32_t* row_nsplit /*[M]*/);
 cudaError_t launch_attention_tc(const CUtensorMap& tmQ, const CUtensorMap& tmK, const CUtensorMap& tmV,
                                 const AttnArgs& a, cudaStream_t st);
-cudaError_t launch_attn_combine(const float* o_part, const float* ml_part, void* O, int M, int Hq, int D,
-                                int n_splits, cudaStream_t st);
+cudaError_t launch_attn_combine(const float* o_part, const float* ml_part, const int32_t* row_nsplit, void* O, int M,
+                                int Hq, int D, cudaStream_t st);
 // generic-D SIMT attention (tiny shapes, D in {16,32,64}); writes O bf16 directly
 cudaError_t launch_attention_simt(const void* Q, const void* Kpool_l, const void* Vpool_l, const int32_t* row_seq,
                                   const int32_t* seq_bt_off, const int32_t* bt, const int32_t* row_pos, void* O,

@@ -3,14 +3,27 @@
 // LM-head argmax and the CacheBlend selection kernels.  All use 16-byte vector accesses on the
 // contiguous dimension and are launched with grids sized from the row counts.
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.h"
+
+#define CUDA_TRY_LAUNCH(x)              \
+  do {                                 \
+    cudaError_t e__ = (x);             \
+    if (e__ != cudaSuccess) return e__; \
+  } while (0)
 
 namespace pic {
 
 cudaError_t prepare_gemm();
 cudaError_t prepare_attention();
+bool pdl_enabled() {
+  static int v = -1;
+  if (v < 0) v = getenv("PIC_NO_PDL") ? 0 : 1;
+  return v == 1;
+}
+
 cudaError_t prepare_kernels() {
   cudaError_t e = prepare_gemm();
   return e == cudaSuccess ? prepare_attention() : e;
@@ -44,6 +57,7 @@ PIC_DEV uint16_t gen_weight_bits(uint64_t key, uint64_t idx, float scale) {
 }
 
 __global__ void gen_matrix_kernel(uint16_t* __restrict__ dst, int64_t n8, int64_t base, uint64_t key, float scale) {
+  PIC_PDL_ENTRY();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n8; i += (int64_t)gridDim.x * blockDim.x) {
     uint32_t w[4];
 #pragma unroll
@@ -60,12 +74,13 @@ cudaError_t launch_gen_matrix(void* dst, int64_t rows, int64_t cols, uint64_t se
   const int64_t n = rows * cols;
   if (n % 8) return cudaErrorInvalidValue;
   const float scale = ldexpf(1.0f, exp2);
-  gen_matrix_kernel<<<148 * 8, 256, 0, st>>>(reinterpret_cast<uint16_t*>(dst), n / 8, row0 * cols,
-                                             stream_key(seed, tag), scale);
+  CUDA_TRY_LAUNCH(launch_k(gen_matrix_kernel, dim3(148 * 8), dim3(256), 0, st, reinterpret_cast<uint16_t*>(dst), n / 8, row0 * cols,
+                                             stream_key(seed, tag), scale));
   return cudaGetLastError();
 }
 
 __global__ void gen_gains_kernel(float* dst, int64_t n, uint64_t key) {
+  PIC_PDL_ENTRY();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const uint64_t u = sm64(key + (uint64_t)i);
     dst[i] = 1.0f + ((float)(int)(u >> 61) - 4.0f) / 32.0f;
@@ -73,7 +88,7 @@ __global__ void gen_gains_kernel(float* dst, int64_t n, uint64_t key) {
 }
 
 cudaError_t launch_gen_gains(float* dst, int64_t n, uint64_t seed, uint64_t tag, cudaStream_t st) {
-  gen_gains_kernel<<<64, 256, 0, st>>>(dst, n, stream_key(seed, tag));
+  CUDA_TRY_LAUNCH(launch_k(gen_gains_kernel, dim3(64), dim3(256), 0, st, dst, n, stream_key(seed, tag)));
   return cudaGetLastError();
 }
 
@@ -81,6 +96,7 @@ cudaError_t launch_gen_gains(float* dst, int64_t n, uint64_t seed, uint64_t tag,
 // h[r] = fp32(E[tok[r]])  (P:213 step 1: "the embedding matrix E (with shape (k', d))")
 __global__ void embed_kernel(const uint16_t* __restrict__ E, const int32_t* __restrict__ tok, float* __restrict__ h,
                              int d) {
+  PIC_PDL_ENTRY();
   const int r = blockIdx.x;
   const uint4* src = reinterpret_cast<const uint4*>(E + (size_t)tok[r] * d);
   float4* dst = reinterpret_cast<float4*>(h + (size_t)r * d);
@@ -96,7 +112,7 @@ __global__ void embed_kernel(const uint16_t* __restrict__ E, const int32_t* __re
 
 cudaError_t launch_embed(const void* E, const int32_t* tok, float* h, int M, int d, cudaStream_t st) {
   if (M == 0) return cudaSuccess;
-  embed_kernel<<<M, 128, 0, st>>>(reinterpret_cast<const uint16_t*>(E), tok, h, d);
+  CUDA_TRY_LAUNCH(launch_k(embed_kernel, dim3(M), dim3(128), 0, st, reinterpret_cast<const uint16_t*>(E), tok, h, d));
   return cudaGetLastError();
 }
 
@@ -113,37 +129,62 @@ PIC_DEV float block_sum(float v, float* red) {
   return t;
 }
 
+PIC_DEV float block_sum_dyn(float v, float* red) {
+  v = warp_sum(v);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  float t = 0.f;
+  for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += red[i];
+  __syncthreads();
+  return t;
+}
+
+PIC_DEV void add4(float4& a, const float4& b) {
+  a.x += b.x;
+  a.y += b.y;
+  a.z += b.z;
+  a.w += b.w;
+}
+
+// Σ_s P4[s·stride4 + off4]: the split loads are independent (unrolled) so they overlap in flight
+PIC_DEV float4 sum_splits4(const float4* __restrict__ P4, int splits, size_t stride4, size_t off4) {
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 8
+  for (int s = 0; s < splits; ++s) add4(acc, __ldg(P4 + s * stride4 + off4));
+  return acc;
+}
+
 // h[r] += Σ_s P[s][r];  x[out] = bf16(h · rsqrt(mean h² + ε) · g)   (reading R4, fp32 residual R15)
-__global__ void __launch_bounds__(256) residual_rmsnorm_kernel(float* __restrict__ h, const float* __restrict__ P,
-                                                                int splits, const float* __restrict__ g,
-                                                                uint16_t* __restrict__ x,
-                                                                const int32_t* __restrict__ out_map, int M, int d,
-                                                                float eps) {
-  __shared__ float red[8];
+// One CTA per row, one float4 of the row per thread (d/4 threads, <= 1024).
+__global__ void __launch_bounds__(1024) residual_rmsnorm_kernel(float* __restrict__ h, const float* __restrict__ P,
+                                                                 int splits, const float* __restrict__ g,
+                                                                 uint16_t* __restrict__ x,
+                                                                 const int32_t* __restrict__ out_map, int M, int d,
+                                                                 float eps) {
+  PIC_PDL_ENTRY();
+  __shared__ float red[32];
   const int r = blockIdx.x;
-  float4* hr = reinterpret_cast<float4*>(h + (size_t)r * d);
   const int n4 = d / 4;
+  float4* hr = reinterpret_cast<float4*>(h + (size_t)r * d);
+  const float4* P4 = reinterpret_cast<const float4*>(P) + (size_t)r * n4;
+  const size_t stride4 = (size_t)M * n4;
   float ss = 0.f;
-  for (int i = threadIdx.x; i < n4; i += 256) {
+  for (int i = threadIdx.x; i < n4; i += blockDim.x) {
     float4 v = hr[i];
-    for (int s = 0; s < splits; ++s) {
-      const float4 p = reinterpret_cast<const float4*>(P + ((size_t)s * M + r) * d)[i];
-      v.x += p.x;
-      v.y += p.y;
-      v.z += p.z;
-      v.w += p.w;
+    if (splits) {
+      add4(v, sum_splits4(P4, splits, stride4, i));
+      hr[i] = v;
     }
-    if (splits) hr[i] = v;
     ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
   }
   if (!x) return;
   const int orow = out_map ? out_map[r] : r;
-  ss = block_sum<256>(ss, red);
+  ss = block_sum_dyn(ss, red);
   if (orow < 0) return;
   const float inv = rsqrtf(ss / d + eps);
   uint2* xr = reinterpret_cast<uint2*>(x + (size_t)orow * d);
   const float4* g4 = reinterpret_cast<const float4*>(g);
-  for (int i = threadIdx.x; i < n4; i += 256) {
+  for (int i = threadIdx.x; i < n4; i += blockDim.x) {
     const float4 v = hr[i], w = g4[i];
     xr[i] = make_uint2(pack_bf16(v.x * inv * w.x, v.y * inv * w.y), pack_bf16(v.z * inv * w.z, v.w * inv * w.w));
   }
@@ -152,8 +193,9 @@ __global__ void __launch_bounds__(256) residual_rmsnorm_kernel(float* __restrict
 cudaError_t launch_residual_rmsnorm(float* h, const float* P, int splits, const float* g, void* x,
                                     const int32_t* out_map, int M, int d, float eps, cudaStream_t st) {
   if (M == 0) return cudaSuccess;
-  residual_rmsnorm_kernel<<<M, 256, 0, st>>>(h, P, P ? splits : 0, g, reinterpret_cast<uint16_t*>(x), out_map, M, d,
-                                             eps);
+  const int nt = std::max(32, std::min(1024, d / 4));
+  CUDA_TRY_LAUNCH(launch_k(residual_rmsnorm_kernel, dim3(M), dim3(nt), 0, st, h, P, P ? splits : 0, g, reinterpret_cast<uint16_t*>(x), out_map, M, d,
+                                            eps));
   return cudaGetLastError();
 }
 
@@ -164,48 +206,51 @@ PIC_DEV float sum_partials(const float* P, int splits, size_t split_stride, size
   return a;
 }
 
+PIC_DEV uint2 pack4(float a, float b, float c, float d) { return make_uint2(pack_bf16(a, b), pack_bf16(c, d)); }
+
 // Q = RoPE(Σ q, p), K = RoPE(Σ k, p) -> pool slot, V = Σ v -> pool slot  (P:213 steps 2-3; written
-// BEFORE attention so the selected rows also see each other)
-__global__ void qkv_rope_scatter_kernel(const float* __restrict__ P, int splits, int P_rows,
-                                        const int32_t* __restrict__ src_row, const int32_t* __restrict__ pos,
-                                        const int32_t* __restrict__ slot, const float* __restrict__ cos_t,
-                                        const float* __restrict__ sin_t, __nv_bfloat16* __restrict__ Q,
-                                        __nv_bfloat16* __restrict__ Kp, __nv_bfloat16* __restrict__ Vp, int Hq,
-                                        int Hkv, int D) {
+// BEFORE attention so the selected rows also see each other).  Grid (rows, column groups); a RoPE
+// thread owns 4 NeoX pairs (j..j+3, j+D/2..j+D/2+3) of one q/k head, a V thread 4 values.
+__global__ void __launch_bounds__(128) qkv_rope_scatter_kernel(
+    const float* __restrict__ P, int splits, int P_rows, const int32_t* __restrict__ src_row,
+    const int32_t* __restrict__ pos, const int32_t* __restrict__ slot, const float* __restrict__ cos_t,
+    const float* __restrict__ sin_t, __nv_bfloat16* __restrict__ Q, __nv_bfloat16* __restrict__ Kp,
+    __nv_bfloat16* __restrict__ Vp, int Hq, int Hkv, int D) {
+  PIC_PDL_ENTRY();
   const int r = blockIdx.x;
+  const int t = blockIdx.y * blockDim.x + threadIdx.x;
+  const int half = D / 2, q8 = D / 8;
+  const int n_rope = (Hq + Hkv) * q8, n_v = Hkv * (D / 4);
+  if (t >= n_rope + n_v) return;
   const int srow = src_row ? src_row[r] : r;
-  const int p = pos[r];
+  const int ncol4 = (Hq + 2 * Hkv) * D / 4;
+  const size_t stride4 = (size_t)P_rows * ncol4;
+  const float4* P4 = reinterpret_cast<const float4*>(P) + (size_t)srow * ncol4;
   const int sl = slot[r];
-  const int half = D / 2;
-  const int ncol = (Hq + 2 * Hkv) * D;
-  const size_t sstride = (size_t)P_rows * ncol;
-  const float* prow = P + (size_t)srow * ncol;
-  const float* cs = cos_t + (size_t)p * half;
-  const float* sn = sin_t + (size_t)p * half;
-  const int qpairs = Hq * half, kpairs = Hkv * half;
   const size_t kv_base = ((size_t)(sl / 16) * Hkv) * 16 * D + (size_t)(sl % 16) * D;  // + g*16*D + d
-  for (int t = threadIdx.x; t < qpairs + kpairs; t += blockDim.x) {
-    const bool isq = t < qpairs;
-    const int u = isq ? t : t - qpairs;
-    const int hd = u / half, j = u % half;
-    const int col = (isq ? 0 : Hq * D) + hd * D + j;
-    const float a = sum_partials(prow, splits, sstride, col);
-    const float b = sum_partials(prow, splits, sstride, col + half);
-    const float c = cs[j], s = sn[j];
-    const __nv_bfloat16 o1 = __float2bfloat16(a * c - b * s), o2 = __float2bfloat16(b * c + a * s);
-    if (isq) {
-      Q[((size_t)r * Hq + hd) * D + j] = o1;
-      Q[((size_t)r * Hq + hd) * D + j + half] = o2;
+  if (t < n_rope) {
+    const int hd = t / q8, j = (t % q8) * 4;
+    const int col4 = (hd * D + j) / 4;
+    const float4 a = sum_splits4(P4, splits, stride4, col4);
+    const float4 b = sum_splits4(P4, splits, stride4, col4 + half / 4);
+    const int p = pos[r];
+    const float4 c = *reinterpret_cast<const float4*>(cos_t + (size_t)p * half + j);
+    const float4 s = *reinterpret_cast<const float4*>(sin_t + (size_t)p * half + j);
+    const uint2 o1 = pack4(a.x * c.x - b.x * s.x, a.y * c.y - b.y * s.y, a.z * c.z - b.z * s.z, a.w * c.w - b.w * s.w);
+    const uint2 o2 = pack4(b.x * c.x + a.x * s.x, b.y * c.y + a.y * s.y, b.z * c.z + a.z * s.z, b.w * c.w + a.w * s.w);
+    __nv_bfloat16* dst;
+    if (hd < Hq) {
+      dst = Q + ((size_t)r * Hq + hd) * D;
     } else {
-      const size_t o = kv_base + (size_t)hd * 16 * D + j;
-      Kp[o] = o1;
-      Kp[o + half] = o2;
+      dst = Kp + kv_base + (size_t)(hd - Hq) * 16 * D;
     }
-  }
-  for (int t = threadIdx.x; t < Hkv * D; t += blockDim.x) {
-    const int hd = t / D, j = t % D;
-    const float v = sum_partials(prow, splits, sstride, (Hq + Hkv) * D + t);
-    Vp[kv_base + (size_t)hd * 16 * D + j] = __float2bfloat16(v);
+    *reinterpret_cast<uint2*>(dst + j) = o1;
+    *reinterpret_cast<uint2*>(dst + j + half) = o2;
+  } else {
+    const int u = t - n_rope;
+    const int hd = u / (D / 4), j = (u % (D / 4)) * 4;
+    const float4 v = sum_splits4(P4, splits, stride4, ((Hq + Hkv) * D + hd * D + j) / 4);
+    *reinterpret_cast<uint2*>(Vp + kv_base + (size_t)hd * 16 * D + j) = pack4(v.x, v.y, v.z, v.w);
   }
 }
 
@@ -213,39 +258,37 @@ cudaError_t launch_qkv_rope_scatter(const float* P, int splits, int P_rows, cons
                                     const int32_t* slot, const float* cos_t, const float* sin_t, void* Q,
                                     void* Kpool_l, void* Vpool_l, int M, int Hq, int Hkv, int D, cudaStream_t st) {
   if (M == 0) return cudaSuccess;
-  qkv_rope_scatter_kernel<<<M, 256, 0, st>>>(P, splits, P_rows, src_row, pos, slot, cos_t, sin_t,
-                                             reinterpret_cast<__nv_bfloat16*>(Q),
-                                             reinterpret_cast<__nv_bfloat16*>(Kpool_l),
-                                             reinterpret_cast<__nv_bfloat16*>(Vpool_l), Hq, Hkv, D);
+  const int threads = (Hq + Hkv) * (D / 8) + Hkv * (D / 4);
+  dim3 grid(M, (threads + 127) / 128);
+  CUDA_TRY_LAUNCH(launch_k(qkv_rope_scatter_kernel, dim3(grid), dim3(128), 0, st, P, splits, P_rows, src_row, pos, slot, cos_t, sin_t,
+                                                reinterpret_cast<__nv_bfloat16*>(Q),
+                                                reinterpret_cast<__nv_bfloat16*>(Kpool_l),
+                                                reinterpret_cast<__nv_bfloat16*>(Vpool_l), Hq, Hkv, D));
   return cudaGetLastError();
 }
 
 // ================================================================================ a8 SwiGLU
-__global__ void swiglu_kernel(const float* __restrict__ P, int splits, uint32_t* __restrict__ u, int M, int F) {
-  const size_t n2 = (size_t)M * F / 2;
-  const size_t sstride = (size_t)M * 2 * F;
-  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n2; i += (size_t)gridDim.x * blockDim.x) {
-    const size_t r = (2 * i) / F, f = (2 * i) % F;
-    float2 g = make_float2(0.f, 0.f), up = make_float2(0.f, 0.f);
-    for (int s = 0; s < splits; ++s) {
-      const float* row = P + s * sstride + r * 2 * F;
-      const float2 a = *reinterpret_cast<const float2*>(row + f);
-      const float2 b = *reinterpret_cast<const float2*>(row + F + f);
-      g.x += a.x;
-      g.y += a.y;
-      up.x += b.x;
-      up.y += b.y;
-    }
-    const float s0 = g.x / (1.f + __expf(-g.x)), s1 = g.y / (1.f + __expf(-g.y));
-    u[i] = pack_bf16(s0 * up.x, s1 * up.y);
+// u = bf16(silu(Σ gate) ⊙ Σ up), 4 columns per thread
+__global__ void swiglu_kernel(const float* __restrict__ P, int splits, uint2* __restrict__ u, int M, int F) {
+  PIC_PDL_ENTRY();
+  const size_t n4 = (size_t)M * F / 4;
+  const size_t F4 = F / 4;
+  const size_t stride4 = (size_t)M * 2 * F4;
+  const float4* P4 = reinterpret_cast<const float4*>(P);
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n4; i += (size_t)gridDim.x * blockDim.x) {
+    const size_t r = i / F4, f = i % F4;
+    const float4 g = sum_splits4(P4, splits, stride4, r * 2 * F4 + f);
+    const float4 up = sum_splits4(P4, splits, stride4, r * 2 * F4 + F4 + f);
+    u[i] = pack4(g.x / (1.f + __expf(-g.x)) * up.x, g.y / (1.f + __expf(-g.y)) * up.y,
+                 g.z / (1.f + __expf(-g.z)) * up.z, g.w / (1.f + __expf(-g.w)) * up.w);
   }
 }
 
 cudaError_t launch_swiglu(const float* P, int splits, void* u, int M, int F, cudaStream_t st) {
   if (M == 0) return cudaSuccess;
-  const size_t n2 = (size_t)M * F / 2;
-  const int blocks = (int)std::min<size_t>((n2 + 255) / 256, (size_t)148 * 16);
-  swiglu_kernel<<<blocks, 256, 0, st>>>(P, splits, reinterpret_cast<uint32_t*>(u), M, F);
+  const size_t n4 = (size_t)M * F / 4;
+  const int blocks = (int)std::min<size_t>((n4 + 255) / 256, (size_t)148 * 16);
+  CUDA_TRY_LAUNCH(launch_k(swiglu_kernel, dim3(blocks), dim3(256), 0, st, P, splits, reinterpret_cast<uint2*>(u), M, F));
   return cudaGetLastError();
 }
 
@@ -260,6 +303,7 @@ __global__ void kv_link_kernel(uint4* __restrict__ Kpool, uint4* __restrict__ Vp
                                const int32_t* __restrict__ dst_slot, const int32_t* __restrict__ delta, int n_rows,
                                int layer0, int n_layers, int64_t layer_stride16, int Hkv, int D,
                                const float* __restrict__ cos_t, const float* __restrict__ sin_t, int rebase) {
+  PIC_PDL_ENTRY();
   const int cK = D / 16, cV = D / 8;  // 16-byte chunks per half row (K) / per row (V)
   const int64_t nK = (int64_t)n_layers * n_rows * Hkv * cK;
   const int64_t nV = (int64_t)n_layers * n_rows * Hkv * cV;
@@ -314,9 +358,9 @@ cudaError_t launch_kv_link(void* Kpool, void* Vpool, const int32_t* src_slot, co
   if (n_rows == 0 || n_layers == 0) return cudaSuccess;
   const int64_t total = (int64_t)n_layers * n_rows * Hkv * (D / 16 + D / 8);
   const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
-  kv_link_kernel<<<blocks, 256, 0, st>>>(reinterpret_cast<uint4*>(Kpool), reinterpret_cast<uint4*>(Vpool), src_slot,
+  CUDA_TRY_LAUNCH(launch_k(kv_link_kernel, dim3(blocks), dim3(256), 0, st, reinterpret_cast<uint4*>(Kpool), reinterpret_cast<uint4*>(Vpool), src_slot,
                                          dst_slot, delta, n_rows, layer0, n_layers, layer_stride_elems / 8, Hkv, D,
-                                         cos_t, sin_t, rebase);
+                                         cos_t, sin_t, rebase));
   return cudaGetLastError();
 }
 
@@ -324,6 +368,7 @@ cudaError_t launch_kv_link(void* Kpool, void* Vpool, const int32_t* src_slot, co
 __global__ void __launch_bounds__(1024) logits_argmax_kernel(const float* __restrict__ P, int splits,
                                                              float* __restrict__ logits, int32_t* __restrict__ amax,
                                                              int n_req, int V) {
+  PIC_PDL_ENTRY();
   __shared__ float bv[32];
   __shared__ int bi[32];
   const int r = blockIdx.x;
@@ -365,7 +410,7 @@ __global__ void __launch_bounds__(1024) logits_argmax_kernel(const float* __rest
 cudaError_t launch_logits_argmax(const float* P, int splits, float* logits, int32_t* argmax, int n_req, int V,
                                  cudaStream_t st) {
   if (n_req == 0) return cudaSuccess;
-  logits_argmax_kernel<<<n_req, 1024, 0, st>>>(P, splits, logits, argmax, n_req, V);
+  CUDA_TRY_LAUNCH(launch_k(logits_argmax_kernel, dim3(n_req), dim3(1024), 0, st, P, splits, logits, argmax, n_req, V));
   return cudaGetLastError();
 }
 
@@ -377,6 +422,7 @@ __global__ void cb_deviation_kernel(const float* __restrict__ P, int splits, con
                                     const float* __restrict__ sin_t, const __nv_bfloat16* __restrict__ Kp,
                                     const __nv_bfloat16* __restrict__ Vp, float* __restrict__ dev, int N, int Hq,
                                     int Hkv, int D) {
+  PIC_PDL_ENTRY();
   __shared__ float red[8];
   const int i = blockIdx.x;
   if (!cand[i]) {
@@ -412,14 +458,15 @@ __global__ void cb_deviation_kernel(const float* __restrict__ P, int splits, con
 cudaError_t launch_cb_deviation(const float* P, int splits, const int32_t* cand, const int32_t* slot,
                                 const float* cos_t, const float* sin_t, const void* Kpool_l, const void* Vpool_l,
                                 float* dev, int N, int Hq, int Hkv, int D, cudaStream_t st) {
-  cb_deviation_kernel<<<N, 256, 0, st>>>(P, splits, cand, slot, cos_t, sin_t,
+  CUDA_TRY_LAUNCH(launch_k(cb_deviation_kernel, dim3(N), dim3(256), 0, st, P, splits, cand, slot, cos_t, sin_t,
                                          reinterpret_cast<const __nv_bfloat16*>(Kpool_l),
-                                         reinterpret_cast<const __nv_bfloat16*>(Vpool_l), dev, N, Hq, Hkv, D);
+                                         reinterpret_cast<const __nv_bfloat16*>(Vpool_l), dev, N, Hq, Hkv, D));
   return cudaGetLastError();
 }
 
 // rank_i = #{j : dev_j > dev_i or (dev_j == dev_i and j < i)}; keep the T best candidates (R13)
 __global__ void cb_rank_kernel(const float* __restrict__ dev, int32_t* __restrict__ keep, int N, int T) {
+  PIC_PDL_ENTRY();
   __shared__ float tile[256];
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const float di = i < N ? dev[i] : -1.f;
@@ -439,7 +486,7 @@ __global__ void cb_rank_kernel(const float* __restrict__ dev, int32_t* __restric
 }
 
 cudaError_t launch_cb_rank(const float* dev, int32_t* keep, int N, int T, cudaStream_t st) {
-  cb_rank_kernel<<<(N + 255) / 256, 256, 0, st>>>(dev, keep, N, T);
+  CUDA_TRY_LAUNCH(launch_k(cb_rank_kernel, dim3((N + 255) / 256), dim3(256), 0, st, dev, keep, N, T));
   return cudaGetLastError();
 }
 
@@ -448,6 +495,7 @@ __global__ void __launch_bounds__(1024) cb_compact_kernel(const int32_t* __restr
                                                           const int32_t* __restrict__ bt, int32_t* __restrict__ sel,
                                                           int32_t* __restrict__ pos, int32_t* __restrict__ slot,
                                                           int32_t* __restrict__ count, int N) {
+  PIC_PDL_ENTRY();
   __shared__ int wsum[32];
   __shared__ int base;
   if (threadIdx.x == 0) base = 0;
@@ -481,12 +529,13 @@ __global__ void __launch_bounds__(1024) cb_compact_kernel(const int32_t* __restr
 
 cudaError_t launch_cb_compact(const int32_t* keep, const int32_t* forced, const int32_t* bt, int32_t* sel, int32_t* pos,
                               int32_t* slot, int32_t* count, int N, cudaStream_t st) {
-  cb_compact_kernel<<<1, 1024, 0, st>>>(keep, forced, bt, sel, pos, slot, count, N);
+  CUDA_TRY_LAUNCH(launch_k(cb_compact_kernel, dim3(1), dim3(1024), 0, st, keep, forced, bt, sel, pos, slot, count, N));
   return cudaGetLastError();
 }
 
 __global__ void gather_rows_kernel(const float4* __restrict__ src, const int32_t* __restrict__ idx,
                                    float4* __restrict__ dst, int d4) {
+  PIC_PDL_ENTRY();
   const int r = blockIdx.x;
   const float4* s = src + (size_t)idx[r] * d4;
   float4* o = dst + (size_t)r * d4;
@@ -495,7 +544,7 @@ __global__ void gather_rows_kernel(const float4* __restrict__ src, const int32_t
 
 cudaError_t launch_gather_rows(const float* src, const int32_t* idx, float* dst, int M, int d, cudaStream_t st) {
   if (M == 0) return cudaSuccess;
-  gather_rows_kernel<<<M, 256, 0, st>>>(reinterpret_cast<const float4*>(src), idx, reinterpret_cast<float4*>(dst), d / 4);
+  CUDA_TRY_LAUNCH(launch_k(gather_rows_kernel, dim3(M), dim3(256), 0, st, reinterpret_cast<const float4*>(src), idx, reinterpret_cast<float4*>(dst), d / 4));
   return cudaGetLastError();
 }
 

@@ -96,6 +96,18 @@ extern "C" pic_status pic_test_attention(const uint16_t* Q, const uint16_t* K, c
     tiles.push_back(std::min(qpt, M - a));
   }
   const int n_tiles = (int)tiles.size() / 3;
+  std::vector<int> n_kv(n_tiles);
+  for (int t = 0; t < n_tiles; ++t) n_kv[t] = pos[tiles[3 * t + 1] + tiles[3 * t + 2] - 1] / 128 + 1;
+  std::vector<int32_t> work(4 * (n_kv.size() + 64 * n_tiles)), nsplit(M, 1);
+  int n_work = 0;
+  // the test forces up to n_splits pieces per tile by asking for n_splits x more CTAs than tiles
+  attn_schedule(tiles.data(), n_tiles, n_kv.data(), Hkv, n_tiles * Hkv * n_splits, n_splits, work.data(), &n_work,
+                nsplit.data());
+  DevBuf dw, dns;
+  TCK(cudaMalloc(&dw.p, 4 * n_work * 4));
+  TCK(cudaMalloc(&dns.p, M * 4));
+  TCK(cudaMemcpy(dw.p, work.data(), 4 * n_work * 4, cudaMemcpyHostToDevice));
+  TCK(cudaMemcpy(dns.p, nsplit.data(), M * 4, cudaMemcpyHostToDevice));
   DevBuf dq, dk, dv, dpos, dt, dbt, doff, dop, dml, dout;
   TCK(cudaMalloc(&dq.p, (size_t)M * Hq * D * 2));
   TCK(cudaMalloc(&dk.p, pool * 2));
@@ -132,18 +144,18 @@ extern "C" pic_status pic_test_attention(const uint16_t* Q, const uint16_t* K, c
   a.seq_bt_off = reinterpret_cast<int32_t*>(doff.p);
   a.bt = reinterpret_cast<int32_t*>(dbt.p);
   a.row_pos = reinterpret_cast<int32_t*>(dpos.p);
-  a.n_tiles = n_tiles;
+  a.work = reinterpret_cast<int32_t*>(dw.p);
+  a.n_work = n_work;
   a.M = M;
   a.Hq = Hq;
   a.Hkv = Hkv;
   a.layer = 0;
   a.num_blocks = num_blocks;
-  a.n_splits = n_splits;
   a.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)D));
   a.o_part = reinterpret_cast<float*>(dop.p);
   a.ml_part = reinterpret_cast<float*>(dml.p);
   TCK(launch_attention_tc(tq, tk, tv, a, 0));
-  TCK(launch_attn_combine(a.o_part, a.ml_part, dout.p, M, Hq, D, n_splits, 0));
+  TCK(launch_attn_combine(a.o_part, a.ml_part, reinterpret_cast<int32_t*>(dns.p), dout.p, M, Hq, D, 0));
   TCK(cudaDeviceSynchronize());
   TCK(cudaMemcpy(O, dout.p, (size_t)M * Hq * D * 2, cudaMemcpyDeviceToHost));
   return PIC_OK;
@@ -184,5 +196,45 @@ extern "C" pic_status pic_test_kv_link(uint16_t* Kpool, uint16_t* Vpool, int32_t
   TCK(cudaDeviceSynchronize());
   TCK(cudaMemcpy(Kpool, dk.p, pool * 2, cudaMemcpyDeviceToHost));
   TCK(cudaMemcpy(Vpool, dv.p, pool * 2, cudaMemcpyDeviceToHost));
+  return PIC_OK;
+}
+
+extern "C" pic_status pic_bench_gemm(int32_t M, int32_t N, int32_t K, int32_t bn, int32_t splits, int32_t iters,
+                                     float* us_per_launch) {
+  if (M <= 0 || N <= 0 || K % 64 || N % 32 || splits <= 0 || iters <= 0 || !us_per_launch) return PIC_E_INVALID_ARG;
+  TCK(prepare_kernels());
+  const size_t wbytes = (size_t)N * K * 2;
+  const int copies = (int)std::max<size_t>(2, (size_t)(512u << 20) / wbytes + 1);  // > L2 in total
+  DevBuf a, b, p;
+  TCK(cudaMalloc(&a.p, (size_t)M * K * 2));
+  TCK(cudaMalloc(&b.p, wbytes * copies));
+  TCK(cudaMalloc(&p.p, (size_t)splits * M * N * 4));
+  TCK(cudaMemset(a.p, 0, (size_t)M * K * 2));
+  TCK(cudaMemset(b.p, 0, wbytes * copies));
+  CUtensorMap ta;
+  std::vector<CUtensorMap> tb(copies);
+  uint64_t da[2] = {(uint64_t)K, (uint64_t)M}, db[2] = {(uint64_t)K, (uint64_t)N}, st[1] = {(uint64_t)K * 2};
+  uint32_t ba[2] = {64, 128}, bb[2] = {64, (uint32_t)bn};
+  if (!tmap(&ta, a.p, 2, da, st, ba)) return PIC_E_CUDA;
+  for (int c = 0; c < copies; ++c)
+    if (!tmap(&tb[c], (char*)b.p + wbytes * c, 2, db, st, bb)) return PIC_E_CUDA;
+  cudaStream_t s;
+  TCK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  cudaEvent_t e0, e1;
+  TCK(cudaEventCreate(&e0));
+  TCK(cudaEventCreate(&e1));
+  for (int i = 0; i < 3; ++i)
+    TCK(launch_gemm_partial(ta, tb[i % copies], reinterpret_cast<float*>(p.p), M, N, K, splits, bn, s));
+  TCK(cudaEventRecord(e0, s));
+  for (int i = 0; i < iters; ++i)
+    TCK(launch_gemm_partial(ta, tb[i % copies], reinterpret_cast<float*>(p.p), M, N, K, splits, bn, s));
+  TCK(cudaEventRecord(e1, s));
+  TCK(cudaEventSynchronize(e1));
+  float ms = 0;
+  TCK(cudaEventElapsedTime(&ms, e0, e1));
+  *us_per_launch = ms * 1000.f / iters;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaStreamDestroy(s);
   return PIC_OK;
 }

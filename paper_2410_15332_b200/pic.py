@@ -78,7 +78,7 @@ class KernelStatC(C.Structure):
 EXPORTS = ["pic_arena_bytes", "pic_engine_create", "pic_engine_destroy", "pic_generate_context_cache", "pic_link",
            "pic_link_batch", "pic_plan", "pic_linked_export", "pic_linked_info", "pic_linked_release",
            "pic_cache_export", "pic_cache_info", "pic_expire_cache", "pic_read_weights", "pic_get_stats",
-           "pic_last_error", "pic_status_string", "pic_set_profiling", "pic_get_profile", "pic_test_gemm", "pic_test_attention", "pic_test_kv_link"]
+           "pic_last_error", "pic_status_string", "pic_set_profiling", "pic_get_profile", "pic_test_gemm", "pic_test_attention", "pic_test_kv_link", "pic_bench_gemm"]
 
 _lib = None
 
@@ -121,6 +121,7 @@ def lib() -> C.CDLL:
                                          C.c_int32, C.c_int32, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p]
         L.pic_test_kv_link.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p,
                                        C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_double, C.c_int32]
+        L.pic_bench_gemm.argtypes = [C.c_int32] * 6 + [P(C.c_float)]
         for name in EXPORTS:
             getattr(L, name)  # AttributeError if the library lacks a declared entry point
         _lib = L
@@ -428,3 +429,9 @@ def test_kv_link(Kpool, Vpool, src, dst, delta, layer0=0, rebase=True, theta=1e4
     check(lib().pic_test_kv_link(Kpool.ctypes.data, Vpool.ctypes.data, L, NB, Hkv, D, src.ctypes.data,
                                  dst.ctypes.data, delta.ctypes.data, len(src), layer0, int(rebase), theta, max_pos))
     return Kpool, Vpool
+
+
+def bench_gemm(M, N, K, bn, splits, iters=50) -> float:
+    us = C.c_float()
+    check(lib().pic_bench_gemm(M, N, K, bn, splits, iters, C.byref(us)))
+    return us.value
