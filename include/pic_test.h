@@ -37,6 +37,12 @@ pic_status pic_test_kv_link(uint16_t* Kpool, uint16_t* Vpool, int32_t n_layers, 
 pic_status pic_bench_gemm(int32_t M, int32_t N, int32_t K, int32_t bn, int32_t splits, int32_t iters,
                           float* us_per_launch);
 
+/* Attention timing: as pic_test_attention, then `iters` back-to-back launches of the attention
+ * kernel alone; *us = average device µs per launch. */
+pic_status pic_bench_attention(const uint16_t* Q, const uint16_t* K, const uint16_t* V, const int32_t* pos,
+                               int32_t M, int32_t n_keys, int32_t Hq, int32_t Hkv, const int32_t* block_perm,
+                               int32_t num_blocks, int32_t n_splits, int32_t iters, float* us);
+
 #ifdef __cplusplus
 }
 #endif

@@ -348,6 +348,9 @@ static pic_status init_device(pic_engine* e, void* arena, size_t bytes, cudaStre
     uint32_t box[4] = {64, 16, 1, 1};
     TRY(make_tmap(&e->tm_K, e->Kpool, 4, dims, strides, box));
     TRY(make_tmap(&e->tm_V, e->Vpool, 4, dims, strides, box));
+    uint32_t box8[4] = {64, 16, 1, 8};
+    TRY(make_tmap(&e->tm_K8, e->Kpool, 4, dims, strides, box8));
+    TRY(make_tmap(&e->tm_V8, e->Vpool, 4, dims, strides, box8));
   }
   const int64_t M = e->lim.max_rows;
   e->h = reinterpret_cast<float*>(b + a.off_h);
@@ -728,7 +731,7 @@ static pic_status enqueue_forward(pic_engine* e, const Fwd& f, const DevPlan& dp
       a.o_part = e->o_part;
       a.ml_part = e->ml_part;
       R.launches += 2;
-      PROF("attention", attn_bytes, attn_flops, launch_attention_tc(e->tm_Q, e->tm_K, e->tm_V, a, st));
+      PROF("attention", attn_bytes, attn_flops, launch_attention_tc(e->tm_Q, e->tm_K, e->tm_V, e->tm_K8, e->tm_V8, a, st));
       PROF("attn_combine", (double)((tiles == dp.tiles) ? f.attn_max_split : f.attn_max_split2) * M * Hq * D * 4 +
                                  (double)M * Hq * D * 2,
            0,

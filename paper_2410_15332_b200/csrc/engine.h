@@ -117,7 +117,7 @@ struct pic_engine {
   // paged KV pools [L][NB][Hkv][16][D] bf16
   void *Kpool = nullptr, *Vpool = nullptr;
   int64_t layer_stride = 0;  // elements per layer per pool
-  CUtensorMap tm_K, tm_V;
+  CUtensorMap tm_K, tm_V, tm_K8, tm_V8;  // one-block and eight-block boxes
   // activations / workspaces
   float *h = nullptr, *h2 = nullptr, *ws = nullptr;
   size_t ws_floats = 0;

@@ -39,20 +39,24 @@ constexpr int kQ = 0;                        // Q: 2 halves
 constexpr int kK = kQ + 2 * kTile;           // K stages: 2 x 2 halves
 constexpr int kV = kK + 4 * kTile;           // V stages
 constexpr int kP = kV + 4 * kTile;           // P buffers: 2 x 2 halves
-constexpr int kBar = kP + 4 * kTile;         // barriers
+constexpr int kX = kP + 4 * kTile;           // softmax pair exchange: [2 parity][2 halves][128] fp32
+constexpr int kBar = kX + 2 * 2 * 128 * 4;   // barriers
 constexpr int kNumBars = 1 + 2 * 2 + 2 * 2 + 2 + 2 + 2;
-constexpr int kSmem = kBar + kNumBars * 8 + 16 + 1024;
+constexpr int kSmem = kBar + kNumBars * 8 + 16;
+static_assert(kSmem <= 232448, "attention smem over the 227 KB limit");
 }  // namespace attn
 
 template <int G>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(320, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-                   const __grid_constant__ CUtensorMap tmV, const AttnArgs a) {
+                   const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmK8,
+                   const __grid_constant__ CUtensorMap tmV8, const AttnArgs a) {
   griddep_launch();
   using namespace attn;
   constexpr int QPT = 128 / G;  // queries per tile
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw;
+  if (threadIdx.x == 0 && (smem_u32(smem) & 1023)) __trap();  // SWIZZLE_128B tiles need 1 KB alignment
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kBar);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + kNumBars);
   const uint32_t base = smem_u32(smem);
@@ -87,7 +91,7 @@ __global__ void __launch_bounds__(192, 1)
       mbar_init(v_full + 8 * s, 1);
       mbar_init(v_empty + 8 * s, 1);
       mbar_init(s_full + 8 * s, 1);
-      mbar_init(p_full + 8 * s, 128);
+      mbar_init(p_full + 8 * s, 256);
       mbar_init(o_full + 8 * s, 1);
     }
     fence_mbar_init();
@@ -100,31 +104,56 @@ __global__ void __launch_bounds__(192, 1)
 
   if (warp == 0) {
     // ------------------------------------------------------------------ TMA producer
-    if (lane == 0 && n > 0) {
-      tma_prefetch(&tmQ);
-      tma_prefetch(&tmK);
-      tma_prefetch(&tmV);
-      mbar_expect_tx(q_full, 2 * kTile);
-      for (int h = 0; h < 2; ++h) tma_load_3d(base + kQ + h * kTile, &tmQ, q_full, h * 64, g * G, row_start);
+    if (n > 0) {
+      if (lane == 0) {
+        tma_prefetch(&tmQ);
+        tma_prefetch(&tmK);
+        tma_prefetch(&tmV);
+        tma_prefetch(&tmK8);
+        tma_prefetch(&tmV8);
+        mbar_expect_tx(q_full, 2 * kTile);
+        for (int h = 0; h < 2; ++h) tma_load_3d(base + kQ + h * kTile, &tmQ, q_full, h * 64, g * G, row_start);
+      }
       const int kv_base = a.layer * a.num_blocks;
+      // the 8 paged-block ids of a 128-key tile: one coalesced load by lanes 0-7, one tile ahead
+      int blk_next = lane < 8 ? bt[min(j0 * 8 + lane, last_blk)] : 0;
       for (int t = 0; t < n; ++t) {
         const int s = t & 1;
         const uint32_t ph = (t >> 1) & 1;
-        const int j = j0 + t;
-        mbar_wait(k_empty + 8 * s, ph ^ 1);
-        mbar_expect_tx(k_full + 8 * s, 2 * kTile);
-        for (int b = 0; b < 8; ++b) {
-          const int blk = bt[min(j * 8 + b, last_blk)];
-          for (int h = 0; h < 2; ++h)
-            tma_load_4d(base + kK + (2 * s + h) * kTile + b * 2048, &tmK, k_full + 8 * s, h * 64, 0, g, kv_base + blk);
+        const int blk_mine = blk_next;
+        if (t + 1 < n && lane < 8) blk_next = bt[min((j0 + t + 1) * 8 + lane, last_blk)];
+        int blk[8];
+#pragma unroll
+        for (int b = 0; b < 8; ++b) blk[b] = __shfl_sync(0xffffffffu, blk_mine, b);
+        // 8 consecutive block ids: one 8-block box per half instead of 8 one-block boxes
+        const bool contig = __all_sync(0xffffffffu, lane >= 8 || blk_mine == blk[0] + lane);
+        if (lane == 0) {
+          mbar_wait(k_empty + 8 * s, ph ^ 1);
+          mbar_expect_tx(k_full + 8 * s, 2 * kTile);
+          if (contig) {
+            for (int h = 0; h < 2; ++h)
+              tma_load_4d(base + kK + (2 * s + h) * kTile, &tmK8, k_full + 8 * s, h * 64, 0, g, kv_base + blk[0]);
+          } else {
+#pragma unroll
+            for (int b = 0; b < 8; ++b)
+              for (int h = 0; h < 2; ++h)
+                tma_load_4d(base + kK + (2 * s + h) * kTile + b * 2048, &tmK, k_full + 8 * s, h * 64, 0, g,
+                            kv_base + blk[b]);
+          }
+          mbar_wait(v_empty + 8 * s, ph ^ 1);
+          mbar_expect_tx(v_full + 8 * s, 2 * kTile);
+          if (contig) {
+            for (int h = 0; h < 2; ++h)
+              tma_load_4d(base + kV + (2 * s + h) * kTile, &tmV8, v_full + 8 * s, h * 64, 0, g, kv_base + blk[0]);
+          } else {
+#pragma unroll
+            for (int b = 0; b < 8; ++b)
+              for (int h = 0; h < 2; ++h)
+                tma_load_4d(base + kV + (2 * s + h) * kTile + b * 2048, &tmV, v_full + 8 * s, h * 64, 0, g,
+                            kv_base + blk[b]);
+          }
         }
-        mbar_wait(v_empty + 8 * s, ph ^ 1);
-        mbar_expect_tx(v_full + 8 * s, 2 * kTile);
-        for (int b = 0; b < 8; ++b) {
-          const int blk = bt[min(j * 8 + b, last_blk)];
-          for (int h = 0; h < 2; ++h)
-            tma_load_4d(base + kV + (2 * s + h) * kTile + b * 2048, &tmV, v_full + 8 * s, h * 64, 0, g, kv_base + blk);
-        }
+        __syncwarp();
       }
     }
   } else if (warp == 1) {
@@ -168,7 +197,11 @@ __global__ void __launch_bounds__(192, 1)
     }
   } else {
     // ------------------------------------------------------------------ softmax warps
+    // 8 warps: warps w and w+4 share TMEM lane quarter q = w % 4 (rows 32q..32q+31); warp half hc
+    // owns keys [64hc, 64hc+64) of every S tile (= P half hc) and O columns [64hc, 64hc+64).
+    // The pair exchanges its partial row max through double-buffered smem (named barrier 1+q).
     const int q = warp & 3;
+    const int hc = (warp - 2) >> 2;
     const int r = q * 32 + lane;              // MMA row = TMEM lane
     const int qi = r / G, hh = r % G;
     const bool valid = qi < row_count;
@@ -176,7 +209,8 @@ __global__ void __launch_bounds__(192, 1)
     const int head = g * G + hh;
     const int pos = valid ? a.row_pos[row] : max_p;
     const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
-    const uint32_t oAddr = tmem + lane_addr + 256;
+    const uint32_t oAddr = tmem + lane_addr + 256 + hc * 64;
+    float* xmax = reinterpret_cast<float*>(smem + kX);   // [2 parity][2 halves][128 rows]
     // m_ref: the max the current O / l are scaled to.  It is raised only when a row's max grows by
     // more than 2^8 (then O in TMEM and l are rescaled), so exp2 arguments stay <= 8 and the common
     // case never touches O (FA4-style lazy rescale; exact because the final normalisation uses m_ref).
@@ -184,19 +218,22 @@ __global__ void __launch_bounds__(192, 1)
     for (int t = 0; t < n; ++t) {
       const int sb = t & 1;
       const uint32_t ph = (t >> 1) & 1;
-      const int key0 = (j0 + t) * 128;
+      const int key0 = (j0 + t) * 128 + hc * 64;
       mbar_wait(s_full + 8 * sb, ph);
       tc_fence_after();
-      const uint32_t sAddr = tmem + lane_addr + sb * 128;
-      float sv[128];
-      tmem_ld128(sAddr, sv);
+      float sv[64];
+      tmem_ld64(tmem + lane_addr + sb * 128 + hc * 64, sv);
       float mx = -INFINITY;
 #pragma unroll
-      for (int i = 0; i < 128; ++i) {
+      for (int i = 0; i < 64; ++i) {
         sv[i] = (key0 + i <= pos) ? sv[i] * a.scale_log2 : -INFINITY;
         mx = fmaxf(mx, sv[i]);
       }
+      xmax[(sb * 2 + hc) * 128 + r] = mx;
+      named_bar_sync(1 + q, 64);
+      mx = fmaxf(mx, xmax[(sb * 2 + (hc ^ 1)) * 128 + r]);
       // tcgen05.ld/st are warp-collective: the rescale runs for the whole warp if any row needs it
+      // (both warps of a pair see identical maxima, so they take identical decisions)
       const bool grow = mx > m_ref + 8.f;
       const bool need = grow && m_ref != -INFINITY;
       if (__any_sync(0xffffffffu, need)) {
@@ -205,7 +242,7 @@ __global__ void __launch_bounds__(192, 1)
         tc_fence_after();
         const float alpha = need ? exp2f(m_ref - mx) : 1.f;
 #pragma unroll 1
-        for (int c = 0; c < 4; ++c) {
+        for (int c = 0; c < 2; ++c) {
           float ov[32];
           tmem_ld32(oAddr + c * 32, ov);
 #pragma unroll
@@ -218,22 +255,23 @@ __global__ void __launch_bounds__(192, 1)
       if (grow) m_ref = mx;
       // P buffer sb was read by PV_{t-2}: it must have completed
       if (t >= 2) mbar_wait(o_full + 8 * (t & 1), ((t - 2) >> 1) & 1);
-      float sum = 0.f;
-      uint8_t* pbuf = smem + kP + (2 * sb) * kTile + r * 128;
+      float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+      uint8_t* pbuf = smem + kP + (2 * sb + hc) * kTile + r * 128;
       const float mu = (m_ref == -INFINITY) ? 0.f : m_ref;
 #pragma unroll
-      for (int c = 0; c < 16; ++c) {  // 16 chunks of 8 keys = 16 bytes of bf16 P
-        uint32_t pk[4];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const float p0 = exp2f(sv[8 * c + 2 * e] - mu), p1 = exp2f(sv[8 * c + 2 * e + 1] - mu);
-          sum += p0 + p1;
-          pk[e] = pack_bf16(p0, p1);
-        }
-        const int half = c >> 3, chunk16 = c & 7;
-        *reinterpret_cast<uint4*>(pbuf + half * kTile + ((chunk16 ^ (r & 7)) << 4)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+      for (int c = 0; c < 8; ++c) {  // 8 chunks of 8 keys = 16 bytes of bf16 P
+        const float p0 = exp2f(sv[8 * c] - mu), p1 = exp2f(sv[8 * c + 1] - mu);
+        const float p2 = exp2f(sv[8 * c + 2] - mu), p3 = exp2f(sv[8 * c + 3] - mu);
+        const float p4 = exp2f(sv[8 * c + 4] - mu), p5 = exp2f(sv[8 * c + 5] - mu);
+        const float p6 = exp2f(sv[8 * c + 6] - mu), p7 = exp2f(sv[8 * c + 7] - mu);
+        s0 += p0 + p1;
+        s1 += p2 + p3;
+        s2 += p4 + p5;
+        s3 += p6 + p7;
+        *reinterpret_cast<uint4*>(pbuf + ((c ^ (r & 7)) << 4)) =
+            make_uint4(pack_bf16(p0, p1), pack_bf16(p2, p3), pack_bf16(p4, p5), pack_bf16(p6, p7));
       }
-      l += sum;
+      l += (s0 + s1) + (s2 + s3);
       fence_async_smem();
       tc_fence_before();
       mbar_arrive(p_full + 8 * sb);
@@ -243,10 +281,10 @@ __global__ void __launch_bounds__(192, 1)
       tc_fence_after();
     }
     const size_t idx = ((size_t)split * a.M + row) * a.Hq + head;
-    float4* dst = reinterpret_cast<float4*>(a.o_part + idx * 128);
+    float4* dst = reinterpret_cast<float4*>(a.o_part + idx * 128 + hc * 64);
     if (n > 0) {
 #pragma unroll 1
-      for (int c = 0; c < 4; ++c) {
+      for (int c = 0; c < 2; ++c) {
         float ov[32];
         tmem_ld32(oAddr + c * 32, ov);  // warp-collective: all lanes load, valid rows store
         if (valid)
@@ -254,11 +292,14 @@ __global__ void __launch_bounds__(192, 1)
           for (int i = 0; i < 8; ++i) dst[c * 8 + i] = make_float4(ov[4 * i], ov[4 * i + 1], ov[4 * i + 2], ov[4 * i + 3]);
       }
     } else if (valid) {
-      for (int i = 0; i < 32; ++i) dst[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int i = 0; i < 16; ++i) dst[i] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
-    if (valid) {
+    // row sum = both halves' partial sums (parity slot n&1 was last read at tile n-2)
+    xmax[((n & 1) * 2 + hc) * 128 + r] = l;
+    named_bar_sync(1 + q, 64);
+    if (valid && hc == 0) {
       a.ml_part[2 * idx] = m_ref;
-      a.ml_part[2 * idx + 1] = l;
+      a.ml_part[2 * idx + 1] = l + xmax[((n & 1) * 2 + 1) * 128 + r];
     }
   }
   tc_fence_before();
@@ -302,9 +343,9 @@ int attn_schedule(const int32_t* tiles, int n_tiles, const int* n_kv, int Hkv, i
 
 template <int G>
 static cudaError_t launch_attn_g(const CUtensorMap& tmQ, const CUtensorMap& tmK, const CUtensorMap& tmV,
-                                 const AttnArgs& a, cudaStream_t st) {
+                                 const CUtensorMap& tmK8, const CUtensorMap& tmV8, const AttnArgs& a, cudaStream_t st) {
   dim3 grid(a.n_work, a.Hkv);
-  CUDA_TRY_LAUNCH(launch_k(attn_tc_kernel<G>, dim3(grid), dim3(192), attn::kSmem, st, tmQ, tmK, tmV, a));
+  CUDA_TRY_LAUNCH(launch_k(attn_tc_kernel<G>, dim3(grid), dim3(320), attn::kSmem, st, tmQ, tmK, tmV, tmK8, tmV8, a));
   return cudaGetLastError();
 }
 
@@ -317,12 +358,12 @@ cudaError_t prepare_attention() {
 }
 
 cudaError_t launch_attention_tc(const CUtensorMap& tmQ, const CUtensorMap& tmK, const CUtensorMap& tmV,
-                                const AttnArgs& a, cudaStream_t st) {
+                                const CUtensorMap& tmK8, const CUtensorMap& tmV8, const AttnArgs& a, cudaStream_t st) {
   switch (a.Hq / a.Hkv) {
-    case 1: return launch_attn_g<1>(tmQ, tmK, tmV, a, st);
-    case 2: return launch_attn_g<2>(tmQ, tmK, tmV, a, st);
-    case 4: return launch_attn_g<4>(tmQ, tmK, tmV, a, st);
-    case 8: return launch_attn_g<8>(tmQ, tmK, tmV, a, st);
+    case 1: return launch_attn_g<1>(tmQ, tmK, tmV, tmK8, tmV8, a, st);
+    case 2: return launch_attn_g<2>(tmQ, tmK, tmV, tmK8, tmV8, a, st);
+    case 4: return launch_attn_g<4>(tmQ, tmK, tmV, tmK8, tmV8, a, st);
+    case 8: return launch_attn_g<8>(tmQ, tmK, tmV, tmK8, tmV8, a, st);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -32,7 +32,7 @@ struct GemmSmem {
   static constexpr int kB = BN * 64 * 2;
   static constexpr int kStage = kA + kB;
   static constexpr int kBars = 2 * STAGES + 1;
-  static constexpr int kBytes = STAGES * kStage + kBars * 8 + 16 + 1024;  // + alignment slack
+  static constexpr int kBytes = STAGES * kStage + kBars * 8 + 16;
 };
 
 template <int BN, int STAGES>
@@ -40,8 +40,9 @@ __global__ void __launch_bounds__(192, 1)
     gemm_bf16_partial_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                              float* __restrict__ out, int M, int N, int kblk_total, int kblk_per_split) {
   using S = GemmSmem<BN, STAGES>;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw;
+  if (threadIdx.x == 0 && (smem_u32(smem) & 1023)) __trap();  // SWIZZLE_128B tiles need 1 KB alignment
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * S::kA;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * S::kStage);

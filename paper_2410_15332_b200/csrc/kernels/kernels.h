@@ -80,8 +80,9 @@ struct AttnArgs {
 // Writes work items (tile, j0, j1, slot) and the per-row split count; returns the max splits.
 int attn_schedule(const int32_t* tiles, int n_tiles, const int* n_kv, int Hkv, int target_ctas, int max_split,
                   int32_t* work_out /*[4 * cap]*/, int* n_work, int32_t* row_nsplit /*[M]*/);
+// tmK/tmV: pool maps with a one-block box (64, 16, 1, 1); tmK8/tmV8: eight-block box (64, 16, 1, 8)
 cudaError_t launch_attention_tc(const CUtensorMap& tmQ, const CUtensorMap& tmK, const CUtensorMap& tmV,
-                                const AttnArgs& a, cudaStream_t st);
+                                const CUtensorMap& tmK8, const CUtensorMap& tmV8, const AttnArgs& a, cudaStream_t st);
 cudaError_t launch_attn_combine(const float* o_part, const float* ml_part, const int32_t* row_nsplit, void* O, int M,
                                 int Hq, int D, cudaStream_t st);
 // generic-D SIMT attention (tiny shapes, D in {16,32,64}); writes O bf16 directly

@@ -38,6 +38,9 @@ bool tmap(CUtensorMap* m, void* base, int rank, const uint64_t* dims, const uint
 }
 }  // namespace
 
+static int g_attn_iters = 0;
+static float g_attn_us = 0.f;
+
 #define TCK(x)                                   \
   do {                                           \
     if ((x) != cudaSuccess) return PIC_E_CUDA;   \
@@ -126,7 +129,7 @@ extern "C" pic_status pic_test_attention(const uint16_t* Q, const uint16_t* K, c
   TCK(cudaMemcpy(dt.p, tiles.data(), tiles.size() * 4, cudaMemcpyHostToDevice));
   TCK(cudaMemcpy(dbt.p, block_perm, nb * 4, cudaMemcpyHostToDevice));
   TCK(cudaMemset(doff.p, 0, 4));
-  CUtensorMap tq, tk, tv;
+  CUtensorMap tq, tk, tv, tk8, tv8;
   {
     uint64_t dims[3] = {(uint64_t)D, (uint64_t)Hq, (uint64_t)M};
     uint64_t strides[2] = {(uint64_t)D * 2, (uint64_t)Hq * D * 2};
@@ -136,8 +139,9 @@ extern "C" pic_status pic_test_attention(const uint16_t* Q, const uint16_t* K, c
   {
     uint64_t dims[4] = {(uint64_t)D, 16, (uint64_t)Hkv, (uint64_t)num_blocks};
     uint64_t strides[3] = {(uint64_t)D * 2, (uint64_t)16 * D * 2, (uint64_t)Hkv * 16 * D * 2};
-    uint32_t box[4] = {64, 16, 1, 1};
+    uint32_t box[4] = {64, 16, 1, 1}, box8[4] = {64, 16, 1, 8};
     if (!tmap(&tk, dk.p, 4, dims, strides, box) || !tmap(&tv, dv.p, 4, dims, strides, box)) return PIC_E_CUDA;
+    if (!tmap(&tk8, dk.p, 4, dims, strides, box8) || !tmap(&tv8, dv.p, 4, dims, strides, box8)) return PIC_E_CUDA;
   }
   AttnArgs a{};
   a.tiles = reinterpret_cast<int32_t*>(dt.p);
@@ -154,9 +158,23 @@ extern "C" pic_status pic_test_attention(const uint16_t* Q, const uint16_t* K, c
   a.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)D));
   a.o_part = reinterpret_cast<float*>(dop.p);
   a.ml_part = reinterpret_cast<float*>(dml.p);
-  TCK(launch_attention_tc(tq, tk, tv, a, 0));
+  TCK(launch_attention_tc(tq, tk, tv, tk8, tv8, a, 0));
   TCK(launch_attn_combine(a.o_part, a.ml_part, reinterpret_cast<int32_t*>(dns.p), dout.p, M, Hq, D, 0));
   TCK(cudaDeviceSynchronize());
+  if (g_attn_iters > 0) {
+    cudaEvent_t e0, e1;
+    TCK(cudaEventCreate(&e0));
+    TCK(cudaEventCreate(&e1));
+    TCK(cudaEventRecord(e0, 0));
+    for (int i = 0; i < g_attn_iters; ++i) TCK(launch_attention_tc(tq, tk, tv, tk8, tv8, a, 0));
+    TCK(cudaEventRecord(e1, 0));
+    TCK(cudaEventSynchronize(e1));
+    float ms = 0;
+    TCK(cudaEventElapsedTime(&ms, e0, e1));
+    g_attn_us = ms * 1000.f / g_attn_iters;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+  }
   TCK(cudaMemcpy(O, dout.p, (size_t)M * Hq * D * 2, cudaMemcpyDeviceToHost));
   return PIC_OK;
 }
@@ -237,4 +255,16 @@ extern "C" pic_status pic_bench_gemm(int32_t M, int32_t N, int32_t K, int32_t bn
   cudaEventDestroy(e1);
   cudaStreamDestroy(s);
   return PIC_OK;
+}
+
+extern "C" pic_status pic_bench_attention(const uint16_t* Q, const uint16_t* K, const uint16_t* V, const int32_t* pos,
+                                          int32_t M, int32_t n_keys, int32_t Hq, int32_t Hkv,
+                                          const int32_t* block_perm, int32_t num_blocks, int32_t n_splits,
+                                          int32_t iters, float* us) {
+  std::vector<uint16_t> O((size_t)M * Hq * 128);
+  g_attn_iters = iters;
+  pic_status s = pic_test_attention(Q, K, V, pos, M, n_keys, Hq, Hkv, block_perm, num_blocks, n_splits, O.data());
+  g_attn_iters = 0;
+  if (us) *us = g_attn_us;
+  return s;
 }

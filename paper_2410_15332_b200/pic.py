@@ -78,7 +78,7 @@ class KernelStatC(C.Structure):
 EXPORTS = ["pic_arena_bytes", "pic_engine_create", "pic_engine_destroy", "pic_generate_context_cache", "pic_link",
            "pic_link_batch", "pic_plan", "pic_linked_export", "pic_linked_info", "pic_linked_release",
            "pic_cache_export", "pic_cache_info", "pic_expire_cache", "pic_read_weights", "pic_get_stats",
-           "pic_last_error", "pic_status_string", "pic_set_profiling", "pic_get_profile", "pic_test_gemm", "pic_test_attention", "pic_test_kv_link", "pic_bench_gemm"]
+           "pic_last_error", "pic_status_string", "pic_set_profiling", "pic_get_profile", "pic_test_gemm", "pic_test_attention", "pic_test_kv_link", "pic_bench_gemm", "pic_bench_attention"]
 
 _lib = None
 
@@ -122,6 +122,7 @@ def lib() -> C.CDLL:
         L.pic_test_kv_link.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p,
                                        C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_double, C.c_int32]
         L.pic_bench_gemm.argtypes = [C.c_int32] * 6 + [P(C.c_float)]
+        L.pic_bench_attention.argtypes = [C.c_void_p] * 4 + [C.c_int32] * 4 + [C.c_void_p] + [C.c_int32] * 3 + [P(C.c_float)]
         for name in EXPORTS:
             getattr(L, name)  # AttributeError if the library lacks a declared entry point
         _lib = L
@@ -434,4 +435,18 @@ def test_kv_link(Kpool, Vpool, src, dst, delta, layer0=0, rebase=True, theta=1e4
 def bench_gemm(M, N, K, bn, splits, iters=50) -> float:
     us = C.c_float()
     check(lib().pic_bench_gemm(M, N, K, bn, splits, iters, C.byref(us)))
+    return us.value
+
+
+def bench_attention(Q, K, V, pos, block_perm, num_blocks, n_splits=1, iters=20) -> float:
+    Q = np.ascontiguousarray(Q, dtype=np.uint16)
+    K = np.ascontiguousarray(K, dtype=np.uint16)
+    V = np.ascontiguousarray(V, dtype=np.uint16)
+    pos = np.ascontiguousarray(pos, dtype=np.int32)
+    bp = np.ascontiguousarray(block_perm, dtype=np.int32)
+    M, Hq, D = Q.shape
+    n, Hkv, _ = K.shape
+    us = C.c_float()
+    check(lib().pic_bench_attention(Q.ctypes.data, K.ctypes.data, V.ctypes.data, pos.ctypes.data, M, n, Hq, Hkv,
+                                    bp.ctypes.data, num_blocks, n_splits, iters, C.byref(us)))
     return us.value
