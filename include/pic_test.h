@@ -18,6 +18,11 @@ extern "C" {
 pic_status pic_test_gemm(const uint16_t* A, const uint16_t* B, int32_t M, int32_t N, int32_t K, int32_t bn,
                          int32_t splits, float* out);
 
+/* tcgen05 GEMM with the fused SwiGLU epilogue (a8): B [N2][K] holds W_gate / W_up interleaved in groups of
+ * bn/2 rows; u [M][N2/2] bf16 = silu(A·W_gᵀ) ⊙ (A·W_uᵀ). */
+pic_status pic_test_gemm_swiglu(const uint16_t* A, const uint16_t* B, int32_t M, int32_t N2, int32_t K, int32_t bn,
+                                uint16_t* u);
+
 /* a6 sparse-query causal attention (tcgen05, D = 128) + split-KV combine over a PAGED copy of K/V:
  * K, V [n_keys][Hkv][128] bf16 are scattered into 16-token blocks in the order `block_perm`
  * (int32[ceil(n_keys/16)], a permutation of block ids < num_blocks), queries Q [M][Hq][128] at

@@ -276,6 +276,21 @@ static pic_status init_device(pic_engine* e, void* arena, size_t bytes, cudaStre
   const int64_t qkv = (Hq + 2 * Hkv) * D;
   const uint64_t s = c.seed;
   auto al = [](size_t x) { return (x + 1023) & ~size_t(1023); };
+  // gate/up interleave group for the fused SwiGLU epilogue: the g dividing F whose F/g tiles best fill
+  // one wave of 148 CTAs at skinny M (Mistral/Llama F = 14336: g = 112 -> 128 tiles of N = 224)
+  e->gu_group = 0;
+  if (!getenv("PIC_NO_FUSED_SWIGLU")) {
+    double best = -1;
+    for (int g : {112, 128, 64, 32, 16}) {
+      if (F % g || !gemm_bn_supported(2 * g, true)) continue;
+      const int tiles = (int)(F / g);
+      const double eff = (double)tiles / (148.0 * ((tiles + 147) / 148));
+      if (eff > best + 1e-9) {
+        best = eff;
+        e->gu_group = g;
+      }
+    }
+  }
   e->layers.resize(c.n_layers);
   for (int l = 0; l < c.n_layers; ++l) {
     LayerW& w = e->layers[l];
@@ -297,14 +312,21 @@ static pic_status init_device(pic_engine* e, void* arena, size_t bytes, cudaStre
     CK(launch_gen_matrix(q + Hq * D * d * 2, Hkv * D, d, s, T + 1, weight_exponent(d), 0, st));
     CK(launch_gen_matrix(q + (Hq + Hkv) * D * d * 2, Hkv * D, d, s, T + 2, weight_exponent(d), 0, st));
     CK(launch_gen_matrix(w.o, d, Hq * D, s, T + 3, weight_exponent(Hq * D), 0, st));
-    char* gu = reinterpret_cast<char*>(w.gu);
-    CK(launch_gen_matrix(gu, F, d, s, T + 4, weight_exponent(d), 0, st));
-    CK(launch_gen_matrix(gu + F * d * 2, F, d, s, T + 5, weight_exponent(d), 0, st));
+    if (e->gu_group > 0) {
+      // gate/up interleaved in groups of g rows for the fused SwiGLU GEMM epilogue
+      CK(launch_gen_gateup(w.gu, F, d, s, T + 4, T + 5, weight_exponent(d), e->gu_group, st));
+    } else {
+      char* gu = reinterpret_cast<char*>(w.gu);
+      CK(launch_gen_matrix(gu, F, d, s, T + 4, weight_exponent(d), 0, st));
+      CK(launch_gen_matrix(gu + F * d * 2, F, d, s, T + 5, weight_exponent(d), 0, st));
+    }
     CK(launch_gen_matrix(w.down, d, F, s, T + 6, weight_exponent(F), 0, st));
     CK(launch_gen_gains(w.g1, d, s, T + 7, st));
     CK(launch_gen_gains(w.g2, d, s, T + 8, st));
     TRY(make_tmaps_bn(w.tm_qkv, w.qkv, qkv, d));
     TRY(make_tmaps_bn(w.tm_o, w.o, d, Hq * D));
+    if (e->gu_group > 0)
+      TRY(make_tmap_2d(&w.tm_gu_fused, w.gu, 2 * F, d, 2 * e->gu_group));
     TRY(make_tmaps_bn(w.tm_gu, w.gu, 2 * F, d));
     TRY(make_tmaps_bn(w.tm_down, w.down, d, F));
   }
@@ -747,9 +769,15 @@ static pic_status enqueue_forward(pic_engine* e, const Fwd& f, const DevPlan& dp
     TRY(R.gemm(e->tm_O, w.tm_o, M, d, Hq * D, &s));
     ++R.launches;
     PROF("rmsnorm", (double)M * d * (8 + 4 * s + 2), 0, launch_residual_rmsnorm(hc, e->ws, s, w.g2, e->x, nullptr, M, d, eps, st));
-    TRY(R.gemm(e->tm_x, w.tm_gu, M, 2 * F, d, &s));
-    ++R.launches;
-    PROF("swiglu", (double)M * 2 * F * 4 * s + (double)M * F * 2, 0, launch_swiglu(e->ws, s, e->u, M, F, st));
+    if (e->gu_group > 0) {
+      ++R.launches;
+      PROF("gemm", (double)2 * F * d * 2 + (double)M * d * 2 + (double)M * F * 2, 2.0 * M * 2 * F * d,
+           launch_gemm_swiglu(e->tm_x, w.tm_gu_fused, e->u, M, 2 * F, d, 2 * e->gu_group, st));
+    } else {
+      TRY(R.gemm(e->tm_x, w.tm_gu, M, 2 * F, d, &s));
+      ++R.launches;
+      PROF("swiglu", (double)M * 2 * F * 4 * s + (double)M * F * 2, 0, launch_swiglu(e->ws, s, e->u, M, F, st));
+    }
     TRY(R.gemm(e->tm_u, w.tm_down, M, d, F, &s));
     prevP = e->ws;
     prev_s = s;
@@ -1316,6 +1344,16 @@ extern "C" pic_status pic_read_weights(pic_engine* e, int32_t which, int32_t lay
   }
   if (row0 < 0 || nrows < 0 || row0 + nrows > rows) return fail(PIC_E_INVALID_ARG, "row range out of bounds");
   CK(cudaDeviceSynchronize());
+  if ((which == 4 || which == 5) && e->gu_group > 0) {
+    const int64_t g = e->gu_group;
+    for (int64_t r = 0; r < nrows; ++r) {
+      const int64_t f = row0 + r;
+      const int64_t p = (f / g) * 2 * g + f % g + (which == 5 ? g : 0);
+      CK(cudaMemcpy(reinterpret_cast<char*>(host_out) + r * cols * 2, (const char*)w->gu + p * cols * 2, cols * 2,
+                    cudaMemcpyDeviceToHost));
+    }
+    return PIC_OK;
+  }
   CK(cudaMemcpy(host_out, base + row0 * cols * 2, nrows * cols * 2, cudaMemcpyDeviceToHost));
   return PIC_OK;
 }

@@ -46,6 +46,7 @@ struct LayerW {
   void *qkv, *o, *gu, *down;  // bf16 [out][in]
   float *g1, *g2;
   CUtensorMap tm_qkv[3], tm_o[3], tm_gu[3], tm_down[3];  // per GEMM N-tile (64/128/256)
+  CUtensorMap tm_gu_fused;                                 // interleaved gate/up, box 2g rows (fused SwiGLU)
 };
 
 // One forward over a set of rows (a compile batch, one link or a batched link).
@@ -105,6 +106,7 @@ struct pic_engine {
   int device = -1;
   bool host_only = true;
   int max_seqs = 0, max_tiles = 0, max_bt = 0, max_k2 = 0;
+  int gu_group = 0;  // gate/up interleave group g (fused SwiGLU GEMM, N-tile 2g); 0 = separate SwiGLU kernel
   // arena
   char* arena = nullptr;
   size_t arena_bytes = 0;

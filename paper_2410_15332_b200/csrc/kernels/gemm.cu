@@ -26,6 +26,8 @@
 
 namespace pic {
 
+enum { EPI_PARTIAL = 0, EPI_SWIGLU = 1 };
+
 template <int BN, int STAGES>
 struct GemmSmem {
   static constexpr int kA = 128 * 64 * 2;  // 16 KB
@@ -33,12 +35,21 @@ struct GemmSmem {
   static constexpr int kStage = kA + kB;
   static constexpr int kBars = 2 * STAGES + 1;
   static constexpr int kBytes = STAGES * kStage + kBars * 8 + 16;
+  static constexpr int kTmemCols = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
+  static_assert(BN % 16 == 0 && BN <= 256, "UMMA N (M=128): multiple of 16, <= 256");
+  static_assert(kBytes <= 232448, "GEMM smem over the 227 KB limit");
 };
 
-template <int BN, int STAGES>
+constexpr int gemm_stages(int bn) { return (225 * 1024) / (16384 + bn * 128) > 8 ? 8 : (225 * 1024) / (16384 + bn * 128); }
+
+// EPI_PARTIAL: out = fp32 P[split][M][N] (summed by the consumer kernel).
+// EPI_SWIGLU (split-K = 1): B rows are W_gate/W_up interleaved in groups of BN/2 (tile n = gate rows
+//   [n·BN/2, (n+1)·BN/2) then the matching up rows), out = bf16 u[M][N/2] = silu(gate) ⊙ up
+//   (the a8 SwiGLU fused into the GEMM epilogue; P:241 Llama-family MLP, reading R4).
+template <int BN, int STAGES, int EPI>
 __global__ void __launch_bounds__(192, 1)
-    gemm_bf16_partial_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                             float* __restrict__ out, int M, int N, int kblk_total, int kblk_per_split) {
+    gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                     void* __restrict__ out_, int M, int N, int kblk_total, int kblk_per_split) {
   using S = GemmSmem<BN, STAGES>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw;
@@ -63,7 +74,7 @@ __global__ void __launch_bounds__(192, 1)
     mbar_init(accf, 1);
     fence_mbar_init();
   }
-  if (warp == 2) tmem_alloc(smem_u32(tmem_slot), BN);
+  if (warp == 2) tmem_alloc(smem_u32(tmem_slot), S::kTmemCols);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -113,39 +124,66 @@ __global__ void __launch_bounds__(192, 1)
     griddep_wait();  // `out` may still be read by the previous kernel
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     const int row = m0 + q * 32 + lane;
-    float* orow = out + (size_t)blockIdx.z * M * N + (size_t)row * N;
-    if (nkb > 0) {
+    const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16);
+    if constexpr (EPI == EPI_PARTIAL) {
+      float* orow = reinterpret_cast<float*>(out_) + (size_t)blockIdx.z * M * N + (size_t)row * N;
+      const int ncol = min(BN, N - n0);  // multiple of 16
+      if (nkb > 0) {
+        mbar_wait(accf, 0);
+        tc_fence_after();
+#pragma unroll 1
+        for (int c = 0; c < BN; c += 32) {
+          float v[32];
+          tmem_ld32(tl + c, v);  // columns beyond BN are allocated (power-of-2 TMEM) and ignored
+          if (row < M)
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              if (c + 4 * j < ncol)
+                reinterpret_cast<float4*>(orow + n0 + c)[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+        }
+      } else if (row < M) {
+        for (int col = n0; col < n0 + ncol; col += 4)
+          *reinterpret_cast<float4*>(orow + col) = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    } else {
+      constexpr int G = BN / 2;
+      const int F = N / 2;
+      uint16_t* urow = reinterpret_cast<uint16_t*>(out_) + (size_t)row * F + (size_t)blockIdx.x * G;
       mbar_wait(accf, 0);
       tc_fence_after();
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
-        float v[32];
-        tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + c * 32, v);
-        const int col = n0 + c * 32;
-        if (row < M && col < N) {
-          float4* dst = reinterpret_cast<float4*>(orow + col);
+      for (int c = 0; c < G; c += 16) {
+        float gv[16], uv[16];
+        tmem_ld16(tl + c, gv);
+        tmem_ld16(tl + G + c, uv);
+        uint32_t pk[8];
 #pragma unroll
-          for (int j = 0; j < 8; ++j) dst[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+        for (int j = 0; j < 8; ++j) {
+          const float g0 = gv[2 * j], g1 = gv[2 * j + 1];
+          pk[j] = pack_bf16(g0 / (1.f + __expf(-g0)) * uv[2 * j], g1 / (1.f + __expf(-g1)) * uv[2 * j + 1]);
+        }
+        if (row < M && blockIdx.x * G + c < F) {
+          uint4* dst = reinterpret_cast<uint4*>(urow + c);
+          dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+          dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
         }
       }
-    } else if (row < M) {
-      for (int col = n0; col < min(N, n0 + BN); col += 4)
-        *reinterpret_cast<float4*>(orow + col) = make_float4(0.f, 0.f, 0.f, 0.f);
     }
   }
   tc_fence_before();
   __syncthreads();
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc(tmem, BN);
+    tmem_dealloc(tmem, S::kTmemCols);
   }
 }
 
-template <int BN, int STAGES>
-static cudaError_t launch_gemm_t(const CUtensorMap& A, const CUtensorMap& B, float* out, int M, int N, int K,
-                                 int splits, cudaStream_t st) {
-  using S = GemmSmem<BN, STAGES>;
-  auto kern = gemm_bf16_partial_kernel<BN, STAGES>;
+template <int BN, int EPI>
+static cudaError_t launch_gemm_t(const CUtensorMap& A, const CUtensorMap& B, void* out, int M, int N, int K, int splits,
+                                 cudaStream_t st) {
+  constexpr int ST = gemm_stages(BN);
+  using S = GemmSmem<BN, ST>;
+  auto kern = gemm_bf16_kernel<BN, ST, EPI>;
   const int kblk = K / 64;
   const int per = (kblk + splits - 1) / splits;
   dim3 grid((N + BN - 1) / BN, (M + 127) / 128, splits);
@@ -153,24 +191,57 @@ static cudaError_t launch_gemm_t(const CUtensorMap& A, const CUtensorMap& B, flo
   return cudaGetLastError();
 }
 
-template <int BN, int STAGES>
+template <int BN, int EPI>
 static cudaError_t prep_t() {
-  return cudaFuncSetAttribute(gemm_bf16_partial_kernel<BN, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              GemmSmem<BN, STAGES>::kBytes);
+  constexpr int ST = gemm_stages(BN);
+  return cudaFuncSetAttribute(gemm_bf16_kernel<BN, ST, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              GemmSmem<BN, ST>::kBytes);
 }
 
+#define PIC_GEMM_BNS(X) X(64) X(128) X(208) X(256)
+#define PIC_SWIGLU_BNS(X) X(32) X(64) X(128) X(224) X(256)
+
 cudaError_t prepare_gemm() {
-  cudaError_t e = prep_t<256, 4>();
-  if (e == cudaSuccess) e = prep_t<128, 6>();
-  if (e == cudaSuccess) e = prep_t<64, 8>();
+  cudaError_t e = cudaSuccess;
+#define P1(bn) \
+  if (e == cudaSuccess) e = prep_t<bn, EPI_PARTIAL>();
+#define P2(bn) \
+  if (e == cudaSuccess) e = prep_t<bn, EPI_SWIGLU>();
+  PIC_GEMM_BNS(P1)
+  PIC_SWIGLU_BNS(P2)
+#undef P1
+#undef P2
   return e;
+}
+
+bool gemm_bn_supported(int bn, bool swiglu) {
+#define C1(b) || bn == b
+  return swiglu ? (false PIC_SWIGLU_BNS(C1)) : (false PIC_GEMM_BNS(C1));
+#undef C1
 }
 
 cudaError_t launch_gemm_partial(const CUtensorMap& A, const CUtensorMap& B, float* out, int M, int N, int K,
                                 int splits, int bn, cudaStream_t st) {
-  if (bn == 256) return launch_gemm_t<256, 4>(A, B, out, M, N, K, splits, st);
-  if (bn == 64) return launch_gemm_t<64, 8>(A, B, out, M, N, K, splits, st);
-  return launch_gemm_t<128, 6>(A, B, out, M, N, K, splits, st);
+  switch (bn) {
+#define L1(b) \
+  case b:     \
+    return launch_gemm_t<b, EPI_PARTIAL>(A, B, out, M, N, K, splits, st);
+    PIC_GEMM_BNS(L1)
+#undef L1
+  }
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_gemm_swiglu(const CUtensorMap& A, const CUtensorMap& B, void* u, int M, int N2, int K, int bn,
+                               cudaStream_t st) {
+  switch (bn) {
+#define L2(b) \
+  case b:     \
+    return launch_gemm_t<b, EPI_SWIGLU>(A, B, u, M, N2, K, 1, st);
+    PIC_SWIGLU_BNS(L2)
+#undef L2
+  }
+  return cudaErrorInvalidValue;
 }
 
 }  // namespace pic

@@ -62,6 +62,15 @@ cudaError_t launch_kv_link(void* Kpool, void* Vpool, const int32_t* src_slot, co
 // ---- GEMM (tcgen05): P[split][M][N] = A[M][K] · B[N][K]^T --------------------------------------
 cudaError_t launch_gemm_partial(const CUtensorMap& A, const CUtensorMap& B, float* out, int M, int N, int K,
                                 int splits, int bn, cudaStream_t st);
+// Gate/up GEMM with the SwiGLU epilogue fused: B = interleaved [gate|up] groups of bn/2 rows (N2 = 2F rows),
+// u[M][F] bf16 = silu(x·W_gᵀ) ⊙ (x·W_uᵀ).  Split-K 1.
+cudaError_t launch_gemm_swiglu(const CUtensorMap& A, const CUtensorMap& B, void* u, int M, int N2, int K, int bn,
+                               cudaStream_t st);
+bool gemm_bn_supported(int bn, bool swiglu);
+// Interleaved gate/up generator: physical row p = n·2g + j holds gate row n·g + j (j < g) or up row
+// n·g + j − g (j >= g) of the logical [F][d] matrices (tags tag_gate / tag_up, same exponent).
+cudaError_t launch_gen_gateup(void* dst_bf16, int64_t F, int64_t d, uint64_t seed, uint64_t tag_gate,
+                              uint64_t tag_up, int exp2, int g, cudaStream_t st);
 
 // ---- a6: sparse-query causal attention (tcgen05, D = 128) + split-KV combine ----------------
 struct AttnArgs {

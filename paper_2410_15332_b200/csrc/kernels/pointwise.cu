@@ -79,6 +79,34 @@ cudaError_t launch_gen_matrix(void* dst, int64_t rows, int64_t cols, uint64_t se
   return cudaGetLastError();
 }
 
+__global__ void gen_gateup_kernel(uint16_t* __restrict__ dst, int64_t F, int64_t d, uint64_t key_g, uint64_t key_u,
+                                  float scale, int g) {
+  PIC_PDL_ENTRY();
+  const int64_t n8 = 2 * F * d / 8;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n8; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = (8 * i) / d, c = (8 * i) % d;  // physical row, column
+    const int64_t n = p / (2 * g), j = p % (2 * g);
+    const bool up = j >= g;
+    const int64_t f = n * g + (up ? j - g : j);
+    const uint64_t key = up ? key_u : key_g;
+    uint32_t w[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint64_t idx = (uint64_t)(f * d + c + 2 * k);
+      w[k] = (uint32_t)gen_weight_bits(key, idx, scale) | ((uint32_t)gen_weight_bits(key, idx + 1, scale) << 16);
+    }
+    reinterpret_cast<uint4*>(dst)[i] = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+}
+
+cudaError_t launch_gen_gateup(void* dst, int64_t F, int64_t d, uint64_t seed, uint64_t tag_gate, uint64_t tag_up,
+                              int exp2, int g, cudaStream_t st) {
+  if (d % 8 || F % g) return cudaErrorInvalidValue;
+  CUDA_TRY_LAUNCH(launch_k(gen_gateup_kernel, dim3(148 * 8), dim3(256), 0, st, reinterpret_cast<uint16_t*>(dst), F, d,
+                           stream_key(seed, tag_gate), stream_key(seed, tag_up), ldexpf(1.0f, exp2), g));
+  return cudaGetLastError();
+}
+
 __global__ void gen_gains_kernel(float* dst, int64_t n, uint64_t key) {
   PIC_PDL_ENTRY();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {

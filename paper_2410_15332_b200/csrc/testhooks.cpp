@@ -268,3 +268,23 @@ extern "C" pic_status pic_bench_attention(const uint16_t* Q, const uint16_t* K, 
   if (us) *us = g_attn_us;
   return s;
 }
+
+extern "C" pic_status pic_test_gemm_swiglu(const uint16_t* A, const uint16_t* B, int32_t M, int32_t N2, int32_t K,
+                                           int32_t bn, uint16_t* u) {
+  if (!A || !B || !u || M <= 0 || N2 <= 0 || K % 64 || N2 % bn || !gemm_bn_supported(bn, true)) return PIC_E_INVALID_ARG;
+  TCK(prepare_kernels());
+  DevBuf a, b, p;
+  TCK(cudaMalloc(&a.p, (size_t)M * K * 2));
+  TCK(cudaMalloc(&b.p, (size_t)N2 * K * 2));
+  TCK(cudaMalloc(&p.p, (size_t)M * (N2 / 2) * 2));
+  TCK(cudaMemcpy(a.p, A, (size_t)M * K * 2, cudaMemcpyHostToDevice));
+  TCK(cudaMemcpy(b.p, B, (size_t)N2 * K * 2, cudaMemcpyHostToDevice));
+  CUtensorMap ta, tb;
+  uint64_t da[2] = {(uint64_t)K, (uint64_t)M}, db[2] = {(uint64_t)K, (uint64_t)N2}, st[1] = {(uint64_t)K * 2};
+  uint32_t ba[2] = {64, 128}, bb[2] = {64, (uint32_t)bn};
+  if (!tmap(&ta, a.p, 2, da, st, ba) || !tmap(&tb, b.p, 2, db, st, bb)) return PIC_E_CUDA;
+  TCK(launch_gemm_swiglu(ta, tb, p.p, M, N2, K, bn, 0));
+  TCK(cudaDeviceSynchronize());
+  TCK(cudaMemcpy(u, p.p, (size_t)M * (N2 / 2) * 2, cudaMemcpyDeviceToHost));
+  return PIC_OK;
+}

@@ -78,7 +78,7 @@ class KernelStatC(C.Structure):
 EXPORTS = ["pic_arena_bytes", "pic_engine_create", "pic_engine_destroy", "pic_generate_context_cache", "pic_link",
            "pic_link_batch", "pic_plan", "pic_linked_export", "pic_linked_info", "pic_linked_release",
            "pic_cache_export", "pic_cache_info", "pic_expire_cache", "pic_read_weights", "pic_get_stats",
-           "pic_last_error", "pic_status_string", "pic_set_profiling", "pic_get_profile", "pic_test_gemm", "pic_test_attention", "pic_test_kv_link", "pic_bench_gemm", "pic_bench_attention"]
+           "pic_last_error", "pic_status_string", "pic_set_profiling", "pic_get_profile", "pic_test_gemm", "pic_test_attention", "pic_test_kv_link", "pic_bench_gemm", "pic_bench_attention", "pic_test_gemm_swiglu"]
 
 _lib = None
 
@@ -122,6 +122,7 @@ def lib() -> C.CDLL:
         L.pic_test_kv_link.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p,
                                        C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_double, C.c_int32]
         L.pic_bench_gemm.argtypes = [C.c_int32] * 6 + [P(C.c_float)]
+        L.pic_test_gemm_swiglu.argtypes = [C.c_void_p, C.c_void_p] + [C.c_int32] * 4 + [C.c_void_p]
         L.pic_bench_attention.argtypes = [C.c_void_p] * 4 + [C.c_int32] * 4 + [C.c_void_p] + [C.c_int32] * 3 + [P(C.c_float)]
         for name in EXPORTS:
             getattr(L, name)  # AttributeError if the library lacks a declared entry point
@@ -404,6 +405,16 @@ def test_gemm(A: np.ndarray, B: np.ndarray, bn: int = 128, splits: int = 1) -> n
     out = np.empty((M, N), dtype=np.float32)
     check(lib().pic_test_gemm(A.ctypes.data, B.ctypes.data, M, N, K, bn, splits, out.ctypes.data))
     return out
+
+
+def test_gemm_swiglu(A: np.ndarray, B: np.ndarray, bn: int) -> np.ndarray:
+    A = np.ascontiguousarray(A, dtype=np.uint16)
+    B = np.ascontiguousarray(B, dtype=np.uint16)
+    M, K = A.shape
+    N2 = B.shape[0]
+    u = np.empty((M, N2 // 2), dtype=np.uint16)
+    check(lib().pic_test_gemm_swiglu(A.ctypes.data, B.ctypes.data, M, N2, K, bn, u.ctypes.data))
+    return u
 
 
 def test_attention(Q, K, V, pos, block_perm, num_blocks, n_splits=1) -> np.ndarray:

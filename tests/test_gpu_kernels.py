@@ -72,6 +72,21 @@ def test_gemm_vs_fp64(M_, N_, K_, bn, splits):
     assert rel(got, ref) < 1e-5, rel(got, ref)
 
 
+@pytest.mark.parametrize("M_,F,K_,bn", [(128, 14336 // 8, 512, 224), (37, 256, 128, 64), (300, 512, 256, 256),
+                                       (5, 64, 64, 32)])
+def test_gemm_swiglu_vs_fp64(M_, F, K_, bn):
+    g = bn // 2
+    A = rand_bf16(M_ + K_, (M_, K_))
+    Wg = rand_bf16(F + 1, (F, K_), 0.05)
+    Wu = rand_bf16(F + 2, (F, K_), 0.05)
+    Bi = np.concatenate([np.concatenate([Wg[n * g:(n + 1) * g], Wu[n * g:(n + 1) * g]]) for n in range(F // g)])
+    got = f32(B.test_gemm_swiglu(A, Bi, bn))
+    a = f32(A)
+    gate, up = a @ f32(Wg).T, a @ f32(Wu).T
+    ref = gate / (1 + np.exp(-gate)) * up
+    assert rel(got, ref) < 1e-2, rel(got, ref)
+
+
 # ------------------------------------------------------------------ attention
 @pytest.mark.parametrize("Hq,Hkv,n_keys,M_,splits", [
     (4, 4, 300, 40, 1), (8, 2, 257, 70, 2), (32, 8, 700, 128, 3), (64, 8, 1000, 33, 4), (8, 1, 130, 130, 1),
