@@ -42,13 +42,14 @@ def peaks():
         return FALLBACK, "fallback"
 
 
-def workload(name: str, alg: str | None):
+def workload(name: str, alg: str | None, world: int = 1, per_gpu: int = 32):
     if name == "cfg2":
         w = sg.cfg2(alg or "legolink:16")
     elif name == "cfg3":
         w = sg.cfg3(alg or "legolink:32")
     elif name == "cfg4":
-        w = sg.cfg4(n_requests=32, alg=alg or "legolink:16")
+        # weak scaling: `per_gpu` independent requests per GPU, request r -> rank r mod world
+        w = sg.cfg4(n_requests=per_gpu * world, alg=alg or "legolink:16")
     else:
         raise SystemExit(f"unknown config {name}")
     return w
@@ -110,36 +111,41 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------------------------- CPU oracle
-def oracle_sample(w, reps: int = 1):
-    """Time the fp64 oracle's link on a bounded sample: layer 0 of the request (all its work:
-    re-base of every cached row, the layer on the k' rows) plus the LM head, then extrapolate to
-    all L layers.  Returns (tokens/s, seconds per full request (extrapolated), sample text)."""
-    from oracle import model as M
-    from oracle import pic as P
-    cfg = w.model
-    Wt = M.Weights(sg.truncated(cfg, 1))
-    Wt.layer(0)
-    Wt.lm_head
-    store = P.Store(Wt)
-    L1 = 1
-    over = [(np.zeros((L1, len(c), cfg.n_kv_heads, cfg.head_dim)), np.zeros((L1, len(c), cfg.n_kv_heads, cfg.head_dim)))
-            for c in w.chunks]
-    oids = store.compile(w.chunks, compiled_override=over)
-    segs = [("cached", oids[s.chunk]) if s.cached else ("tokens", s.tokens) for s in w.requests[0]]
-    N = sum(len(w.chunks[s.chunk]) if s.cached else len(s.tokens) for s in w.requests[0])
-    t_link, t_head = [], []
-    for _ in range(reps):
+class OracleSample:
+    """The fp64 oracle's link on a bounded sample: layer 0 of one request (all its work: re-base of
+    every cached row of that layer, the layer on the k' rows) plus the LM head, extrapolated to all
+    L layers.  Weights are generated once (not timed); each run() is one timed sample."""
+
+    def __init__(self, w):
+        from oracle import model as M
+        from oracle import pic as P
+        self.M, self.P, self.w = M, P, w
+        cfg = w.model
+        self.Wt = M.Weights(sg.truncated(cfg, 1))
+        self.Wt.layer(0)
+        self.Wt.lm_head
+        self.store = P.Store(self.Wt)
+        over = [(np.zeros((1, len(c), cfg.n_kv_heads, cfg.head_dim)), np.zeros((1, len(c), cfg.n_kv_heads, cfg.head_dim)))
+                for c in w.chunks]
+        oids = self.store.compile(w.chunks, compiled_override=over)
+        self.segs = [("cached", oids[s.chunk]) if s.cached else ("tokens", s.tokens) for s in w.requests[0]]
+        self.N = sum(len(w.chunks[s.chunk]) if s.cached else len(s.tokens) for s in w.requests[0])
+
+    def run(self):
+        cfg = self.w.model
         t0 = time.perf_counter()
-        r = P.link(store, segs, w.alg, layers=1)
-        t_link.append(time.perf_counter() - t0)
-        h = r.hidden[-1][-1]
+        r = self.P.link(self.store, self.segs, self.w.alg, layers=1)
+        tl = time.perf_counter() - t0
         t0 = time.perf_counter()
-        M.logits_of(Wt, h)
-        t_head.append(time.perf_counter() - t0)
-    tl, th = min(t_link), min(t_head)
-    per_req = cfg.n_layers * (tl - th) + th
-    return N / per_req, per_req, (f"oracle fp64 link of 1 request, layer 0 of {cfg.n_layers} + LM head timed "
-                                  f"({tl:.2f}s), extrapolated x{cfg.n_layers} layers; N={N}")
+        self.M.logits_of(self.Wt, r.hidden[-1][-1])
+        th = time.perf_counter() - t0
+        per_req = cfg.n_layers * (tl - th) + th
+        return self.N / per_req, per_req, (f"oracle fp64 link of 1 request (N={self.N}): layer 0 of {cfg.n_layers} "
+                                           f"+ LM head timed ({tl:.2f} s), extrapolated x{cfg.n_layers} layers")
+
+
+def oracle_sample(w):
+    return OracleSample(w).run()
 
 
 def cores_used():
@@ -163,10 +169,12 @@ def main():
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    w = workload(args.config, args.alg)
+    from paper_2410_15332_b200 import dist as D
+    rank, world, local = D.env_rank()
+    w = workload(args.config, args.alg, world)
+    if len(w.requests) == 1:
+        w.requests = w.requests * world                # single-request configs: one copy per GPU
+    w.requests = D.shard(w.requests, rank, world)       # data parallel by independent request
     cfgd = describe(w)
     N_tok = [sum(len(w.chunks[s.chunk]) if s.cached else len(s.tokens) for s in r) for r in w.requests]
 
@@ -174,8 +182,9 @@ def main():
         if rank != 0:
             return
         vals = []
+        osamp = OracleSample(w)
         for i in range(args.warmup + args.steps):
-            v, per_req, sample = oracle_sample(w)
+            v, per_req, sample = osamp.run()
             if i >= args.warmup:
                 vals.append((v, per_req))
         v = float(np.median([x[0] for x in vals]))
@@ -191,12 +200,11 @@ def main():
         return
 
     import torch
-    import torch.distributed as dist
     from paper_2410_15332_b200 import pic as B
 
     if world > 1:
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        D.init("nccl", device_id=torch.device(f"cuda:{local}"))
     dev = local
     torch.cuda.set_device(dev)
     stream = torch.cuda.Stream(dev)
@@ -222,9 +230,7 @@ def main():
         stream.synchronize()
         kernels_per_step = eng.stats()["kernels_last_call"]
 
-        def barrier():
-            if world > 1:
-                dist.barrier()
+        barrier = D.barrier
 
         # ---------------- timed region: device-resident inputs, CUDA events on our stream
         barrier()
@@ -238,13 +244,9 @@ def main():
             ev1.synchronize()
         torch.cuda.synchronize(dev)
         barrier()
-        ms = ev0.elapsed_time(ev1)
-        t = torch.tensor([ms], dtype=torch.float64, device=f"cuda:{dev}")
-        if world > 1:
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_max = float(t.item())
+        ms_max = D.max_over_ranks(ev0.elapsed_time(ev1), device=f"cuda:{dev}")
         ms_per_step = ms_max / args.steps
-        tokens_all = sum(N_tok) * args.steps * world
+        tokens_all = D.sum_over_ranks(sum(N_tok), device=f"cuda:{dev}") * args.steps
         value = tokens_all / (ms_max / 1e3)
 
         # ---------------- e2e: the public call with host buffers (plan H2D + logits D2H per step)
@@ -262,10 +264,7 @@ def main():
         e1.synchronize()
         wall = time.perf_counter() - t0
         st = eng.stats()
-        te = torch.tensor([wall], dtype=torch.float64, device=f"cuda:{dev}")
-        if world > 1:
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        wall_max = float(te.item())
+        wall_max = D.max_over_ranks(wall, device=f"cuda:{dev}")
         e2e_value = tokens_all / wall_max
 
         # ---------------- per-kernel CUDA-event profile (separate pass, same stream)
@@ -278,6 +277,7 @@ def main():
 
     if rank != 0:
         if world > 1:
+            import torch.distributed as dist
             dist.destroy_process_group()
         return
     P, src = peaks()
@@ -320,6 +320,7 @@ def main():
                                 "sample": sample}
     print(json.dumps(line))
     if world > 1:
+        import torch.distributed as dist
         dist.destroy_process_group()
 
 
