@@ -211,10 +211,17 @@ def main():
     m = w.model
     total_tokens = sum(len(c) for c in w.chunks)
     max_N = max(N_tok)
-    rows_link = sum(N_tok) if w.alg.startswith("cacheblend") else None
+    # rows recomputed per forward: Σ k' of the batch (host-only planner), N for CacheBlend
+    planner = B.Engine(m, num_blocks=(total_tokens + max_N) // 16 + 2 * len(w.chunks) + 64, max_rows=64,
+                       max_tokens=max(max_N, 512) + 16, max_requests=1, device=None)
+    pids = planner.generate_context_cache(w.chunks)
+    rows_link = sum(N_tok) if w.alg.startswith("cacheblend") else sum(
+        len(planner.plan([("cached", pids[s.chunk]) if s.cached else ("tokens", s.tokens) for s in r], w.alg)["sel"])
+        for r in w.requests)
+    planner.close()
     with torch.cuda.stream(stream):
         eng = B.Engine(m, num_blocks=(total_tokens + sum(N_tok)) // 16 + 2 * len(w.chunks) + 64 * len(w.requests),
-                       max_rows=max(4096, rows_link or 0), max_tokens=max(max_N, 512) + 16,
+                       max_rows=max(4096, rows_link), max_tokens=max(max_N, 512) + 16,
                        max_requests=len(w.requests), device=dev, stream=stream)
         ids = eng.generate_context_cache(w.chunks)
         reqs = [[("cached", ids[s.chunk]) if s.cached else ("tokens", s.tokens) for s in r] for r in w.requests]

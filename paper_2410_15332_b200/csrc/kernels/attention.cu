@@ -316,11 +316,14 @@ int attn_schedule(const int32_t* tiles, int n_tiles, const int* n_kv, int Hkv, i
   for (int t = 0; t < n_tiles; ++t) total += n_kv[t];
   total *= Hkv;
   long budget = std::max(1L, (total + target_ctas - 1) / target_ctas);
-  // grow the per-CTA budget until the work list fits in one wave of target_ctas CTAs
-  for (;; ++budget) {
+  // grow the per-CTA budget until the work list fits in one wave of target_ctas CTAs (at most up
+  // to the longest tile: beyond that every tile is a single piece and nothing changes)
+  long max_kv = 1;
+  for (int t = 0; t < n_tiles; ++t) max_kv = std::max<long>(max_kv, n_kv[t]);
+  for (; budget < max_kv; ++budget) {
     long ctas = 0;
     for (int t = 0; t < n_tiles; ++t) ctas += std::min<long>(max_split, (n_kv[t] + budget - 1) / budget);
-    if (ctas * Hkv <= target_ctas || budget >= 1 << 20) break;
+    if (ctas * Hkv <= target_ctas) break;
   }
   int w = 0, mx = 1;
   for (int t = 0; t < n_tiles; ++t) {
