@@ -33,23 +33,27 @@ struct GemmSmem {
   static constexpr int kA = 128 * 64 * 2;  // 16 KB
   static constexpr int kB = BN * 64 * 2;
   static constexpr int kStage = kA + kB;
-  static constexpr int kBars = 2 * STAGES + 1;
+  static constexpr int kBars = 2 * STAGES + 4;
   static constexpr int kBytes = STAGES * kStage + kBars * 8 + 16;
-  static constexpr int kTmemCols = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
+  static constexpr int kAcc = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;  // TMEM cols per accumulator
+  static constexpr int kTmemCols = 2 * kAcc;                                              // double buffered
   static_assert(BN % 16 == 0 && BN <= 256, "UMMA N (M=128): multiple of 16, <= 256");
   static_assert(kBytes <= 232448, "GEMM smem over the 227 KB limit");
 };
 
 constexpr int gemm_stages(int bn) { return (225 * 1024) / (16384 + bn * 128) > 8 ? 8 : (225 * 1024) / (16384 + bn * 128); }
 
-// EPI_PARTIAL: out = fp32 P[split][M][N] (summed by the consumer kernel).
-// EPI_SWIGLU (split-K = 1): B rows are W_gate/W_up interleaved in groups of BN/2 (tile n = gate rows
-//   [n·BN/2, (n+1)·BN/2) then the matching up rows), out = bf16 u[M][N/2] = silu(gate) ⊙ up
-//   (the a8 SwiGLU fused into the GEMM epilogue; P:241 Llama-family MLP, reading R4).
+// Persistent tcgen05 GEMM.  Work units (m-tile, n-tile, k-split) are dealt round-robin to
+// min(units, 148) CTAs; the smem ring runs continuously across units and the fp32 accumulator is
+// double-buffered in TMEM, so the epilogue of unit i overlaps the MMAs of unit i+1.
+//   EPI_PARTIAL: out = fp32 P[split][M][N] (summed by the consumer kernel in a fixed order).
+//   EPI_SWIGLU (split-K = 1): B rows are W_gate/W_up interleaved in groups of BN/2 (n-tile = gate rows
+//     [n·BN/2, (n+1)·BN/2) then the matching up rows); out = bf16 u[M][N/2] = silu(gate) ⊙ up
+//     (the a8 SwiGLU fused into the GEMM epilogue; P:241 Llama-family MLP, reading R4).
 template <int BN, int STAGES, int EPI>
 __global__ void __launch_bounds__(192, 1)
     gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                     void* __restrict__ out_, int M, int N, int kblk_total, int kblk_per_split) {
+                     void* __restrict__ out_, int M, int N, int kblk_total, int kblk_per_split, int splits) {
   using S = GemmSmem<BN, STAGES>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw;
@@ -58,12 +62,12 @@ __global__ void __launch_bounds__(192, 1)
   uint8_t* sB = smem + STAGES * S::kA;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * S::kStage);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + S::kBars);
-  const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + STAGES), accf = smem_u32(bars + 2 * STAGES);
+  const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + STAGES);
+  const uint32_t tfull0 = smem_u32(bars + 2 * STAGES), tempty0 = smem_u32(bars + 2 * STAGES + 2);
 
   const int warp = warp_id(), lane = lane_id();
-  const int n0 = blockIdx.x * BN, m0 = blockIdx.y * 128;
-  const int kb0 = blockIdx.z * kblk_per_split;
-  const int nkb = min(kblk_per_split, kblk_total - kb0);
+  const int mt = (M + 127) / 128, nt = (N + BN - 1) / BN;
+  const int units = mt * nt * splits;
   griddep_launch();
 
   if (threadIdx.x == 0) {
@@ -71,7 +75,10 @@ __global__ void __launch_bounds__(192, 1)
       mbar_init(full0 + 8 * s, 1);
       mbar_init(empty0 + 8 * s, 1);
     }
-    mbar_init(accf, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(tfull0 + 8 * b, 1);
+      mbar_init(tempty0 + 8 * b, 128);
+    }
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc(smem_u32(tmem_slot), S::kTmemCols);
@@ -80,94 +87,135 @@ __global__ void __launch_bounds__(192, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
+  // unit u -> (m fastest, then split, then n): concurrently running CTAs share weight tiles in L2
+  auto decode = [&](int u, int& m0, int& n_idx, int& kb0, int& nkb) {
+    const int m = u % mt;
+    const int r = u / mt;
+    const int sp = r % splits;
+    n_idx = r / splits;
+    m0 = m * 128;
+    kb0 = sp * kblk_per_split;
+    nkb = max(0, min(kblk_per_split, kblk_total - kb0));
+  };
+
   if (warp == 0) {
-    if (lane == 0 && nkb > 0) {
+    if (lane == 0) {
       tma_prefetch(&tmA);
       tma_prefetch(&tmB);
-      // Weights do not depend on the previous kernel: stream the first stages of B while it
-      // drains (PDL), then wait for it before loading the activations A.
-      const int pre = min(nkb, STAGES);
-      for (int i = 0; i < pre; ++i) {
-        mbar_expect_tx(full0 + 8 * i, S::kStage);
-        tma_load_2d(smem_u32(sB + i * S::kB), &tmB, full0 + 8 * i, (kb0 + i) * 64, n0);
+      int it = 0;
+      bool waited = false;
+      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        int m0, n_idx, kb0, nkb;
+        decode(u, m0, n_idx, kb0, nkb);
+        const int n0 = n_idx * BN;
+        int kk = 0;
+        if (!waited) {
+          // Weights do not depend on the previous kernel: stream the first stages of B while it
+          // drains (PDL), then wait for it before loading the activations A.
+          const int pre = min(nkb, STAGES);
+          for (int i = 0; i < pre; ++i) {
+            mbar_expect_tx(full0 + 8 * i, S::kStage);
+            tma_load_2d(smem_u32(sB + i * S::kB), &tmB, full0 + 8 * i, (kb0 + i) * 64, n0);
+          }
+          griddep_wait();
+          waited = true;
+          for (int i = 0; i < pre; ++i) tma_load_2d(smem_u32(sA + i * S::kA), &tmA, full0 + 8 * i, (kb0 + i) * 64, m0);
+          kk = pre;
+          it = pre;
+        }
+        for (; kk < nkb; ++kk, ++it) {
+          const int s = it % STAGES;
+          mbar_wait(empty0 + 8 * s, ((it / STAGES) & 1) ^ 1);
+          mbar_expect_tx(full0 + 8 * s, S::kStage);
+          const int kc = (kb0 + kk) * 64;
+          tma_load_2d(smem_u32(sA + s * S::kA), &tmA, full0 + 8 * s, kc, m0);
+          tma_load_2d(smem_u32(sB + s * S::kB), &tmB, full0 + 8 * s, kc, n0);
+        }
       }
-      griddep_wait();
-      for (int i = 0; i < pre; ++i) tma_load_2d(smem_u32(sA + i * S::kA), &tmA, full0 + 8 * i, (kb0 + i) * 64, m0);
-      for (int i = pre; i < nkb; ++i) {
-        const int s = i % STAGES;
-        const uint32_t ph = (i / STAGES) & 1;
-        mbar_wait(empty0 + 8 * s, ph ^ 1);
-        mbar_expect_tx(full0 + 8 * s, S::kStage);
-        const int kc = (kb0 + i) * 64;
-        tma_load_2d(smem_u32(sA + s * S::kA), &tmA, full0 + 8 * s, kc, m0);
-        tma_load_2d(smem_u32(sB + s * S::kB), &tmB, full0 + 8 * s, kc, n0);
-      }
+      if (!waited) griddep_wait();
     }
   } else if (warp == 1) {
-    if (lane == 0 && nkb > 0) {
+    if (lane == 0) {
       constexpr uint32_t idesc = idesc_bf16(128, BN, 0, 0);
-      for (int i = 0; i < nkb; ++i) {
-        const int s = i % STAGES;
-        const uint32_t ph = (i / STAGES) & 1;
-        mbar_wait(full0 + 8 * s, ph);
+      int it = 0, i = 0;
+      for (int u = blockIdx.x; u < units; u += gridDim.x, ++i) {
+        int m0, n_idx, kb0, nkb;
+        decode(u, m0, n_idx, kb0, nkb);
+        const int ab = i & 1;
+        mbar_wait(tempty0 + 8 * ab, ((i >> 1) & 1) ^ 1);  // epilogue has drained this accumulator
         tc_fence_after();
-        const uint32_t a = smem_u32(sA + s * S::kA), b = smem_u32(sB + s * S::kB);
+        const uint32_t d = tmem + ab * S::kAcc;
+        for (int kk = 0; kk < nkb; ++kk, ++it) {
+          const int s = it % STAGES;
+          mbar_wait(full0 + 8 * s, (it / STAGES) & 1);
+          tc_fence_after();
+          const uint32_t a = smem_u32(sA + s * S::kA), b = smem_u32(sB + s * S::kB);
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk)
-          umma_bf16(tmem, sdesc_sw128(a + kk * 32, 16, 1024), sdesc_sw128(b + kk * 32, 16, 1024), idesc,
-                    (i | kk) != 0);
-        umma_commit(empty0 + 8 * s);
+          for (int k4 = 0; k4 < 4; ++k4)
+            umma_bf16(d, sdesc_sw128(a + k4 * 32, 16, 1024), sdesc_sw128(b + k4 * 32, 16, 1024), idesc,
+                      (kk | k4) != 0);
+          umma_commit(empty0 + 8 * s);
+        }
+        umma_commit(tfull0 + 8 * ab);
       }
-      umma_commit(accf);
     }
   } else {
     griddep_wait();  // `out` may still be read by the previous kernel
     const int q = warp & 3;  // TMEM lane quarter this warp may access
-    const int row = m0 + q * 32 + lane;
-    const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16);
-    if constexpr (EPI == EPI_PARTIAL) {
-      float* orow = reinterpret_cast<float*>(out_) + (size_t)blockIdx.z * M * N + (size_t)row * N;
-      const int ncol = min(BN, N - n0);  // multiple of 16
-      if (nkb > 0) {
-        mbar_wait(accf, 0);
-        tc_fence_after();
-#pragma unroll 1
-        for (int c = 0; c < BN; c += 32) {
-          float v[32];
-          tmem_ld32(tl + c, v);  // columns beyond BN are allocated (power-of-2 TMEM) and ignored
-          if (row < M)
-#pragma unroll
-            for (int j = 0; j < 8; ++j)
-              if (c + 4 * j < ncol)
-                reinterpret_cast<float4*>(orow + n0 + c)[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
-        }
-      } else if (row < M) {
-        for (int col = n0; col < n0 + ncol; col += 4)
-          *reinterpret_cast<float4*>(orow + col) = make_float4(0.f, 0.f, 0.f, 0.f);
-      }
-    } else {
-      constexpr int G = BN / 2;
-      const int F = N / 2;
-      uint16_t* urow = reinterpret_cast<uint16_t*>(out_) + (size_t)row * F + (size_t)blockIdx.x * G;
-      mbar_wait(accf, 0);
+    int i = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x, ++i) {
+      int m0, n_idx, kb0, nkb;
+      decode(u, m0, n_idx, kb0, nkb);
+      const int ab = i & 1;
+      const int row = m0 + q * 32 + lane;
+      const uint32_t tl = tmem + ab * S::kAcc + ((uint32_t)(q * 32) << 16);
+      const int n0 = n_idx * BN;
+      mbar_wait(tfull0 + 8 * ab, (i >> 1) & 1);
       tc_fence_after();
+      if constexpr (EPI == EPI_PARTIAL) {
+        const int sp = (u / mt) % splits;
+        float* orow = reinterpret_cast<float*>(out_) + (size_t)sp * M * N + (size_t)row * N;
+        const int ncol = min(BN, N - n0);  // multiple of 16
+        if (nkb > 0) {
 #pragma unroll 1
-      for (int c = 0; c < G; c += 16) {
-        float gv[16], uv[16];
-        tmem_ld16(tl + c, gv);
-        tmem_ld16(tl + G + c, uv);
-        uint32_t pk[8];
+          for (int c = 0; c < BN; c += 32) {
+            float v[32];
+            tmem_ld32(tl + c, v);  // columns beyond BN are allocated (power-of-2 TMEM) and ignored
+            if (row < M)
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const float g0 = gv[2 * j], g1 = gv[2 * j + 1];
-          pk[j] = pack_bf16(g0 / (1.f + __expf(-g0)) * uv[2 * j], g1 / (1.f + __expf(-g1)) * uv[2 * j + 1]);
+              for (int j = 0; j < 8; ++j)
+                if (c + 4 * j < ncol)
+                  reinterpret_cast<float4*>(orow + n0 + c)[j] =
+                      make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+          }
+        } else if (row < M) {
+          for (int col = n0; col < n0 + ncol; col += 4)
+            *reinterpret_cast<float4*>(orow + col) = make_float4(0.f, 0.f, 0.f, 0.f);
         }
-        if (row < M && blockIdx.x * G + c < F) {
-          uint4* dst = reinterpret_cast<uint4*>(urow + c);
-          dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-          dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+      } else {
+        constexpr int G = BN / 2;
+        const int F = N / 2;
+        uint16_t* urow = reinterpret_cast<uint16_t*>(out_) + (size_t)row * F + (size_t)n_idx * G;
+#pragma unroll 1
+        for (int c = 0; c < G; c += 16) {
+          float gv[16], uv[16];
+          tmem_ld16(tl + c, gv);
+          tmem_ld16(tl + G + c, uv);
+          uint32_t pk[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const float g0 = gv[2 * j], g1 = gv[2 * j + 1];
+            pk[j] = pack_bf16(g0 / (1.f + __expf(-g0)) * uv[2 * j], g1 / (1.f + __expf(-g1)) * uv[2 * j + 1]);
+          }
+          if (row < M && n_idx * G + c < F) {
+            uint4* dst = reinterpret_cast<uint4*>(urow + c);
+            dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+            dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+          }
         }
       }
+      tc_fence_before();
+      mbar_arrive(tempty0 + 8 * ab);
     }
   }
   tc_fence_before();
@@ -186,8 +234,9 @@ static cudaError_t launch_gemm_t(const CUtensorMap& A, const CUtensorMap& B, voi
   auto kern = gemm_bf16_kernel<BN, ST, EPI>;
   const int kblk = K / 64;
   const int per = (kblk + splits - 1) / splits;
-  dim3 grid((N + BN - 1) / BN, (M + 127) / 128, splits);
-  CUDA_TRY_LAUNCH(launch_k(kern, dim3(grid), dim3(192), S::kBytes, st, A, B, out, M, N, kblk, per));
+  const int units = ((N + BN - 1) / BN) * ((M + 127) / 128) * splits;
+  const int grid = units < 148 ? units : 148;  // persistent: one CTA per SM
+  CUDA_TRY_LAUNCH(launch_k(kern, dim3(grid), dim3(192), S::kBytes, st, A, B, out, M, N, kblk, per, splits));
   return cudaGetLastError();
 }
 
