@@ -47,6 +47,8 @@ def workload(name: str, alg: str | None, world: int = 1, per_gpu: int = 32):
         w = sg.cfg2(alg or "legolink:16")
     elif name == "cfg3":
         w = sg.cfg3(alg or "legolink:32")
+    elif name == "cfg5":
+        w = sg.cfg5(alg or "legolink:16")             # 70B shape, 32K context: fits one B200 (141 GB bf16)
     elif name == "cfg4":
         # weak scaling: `per_gpu` independent requests per GPU, request r -> rank r mod world
         w = sg.cfg4(n_requests=per_gpu * world, alg=alg or "legolink:16")
@@ -161,7 +163,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="cfg2")
+    ap.add_argument("--config", default="cfg2", choices=["cfg2", "cfg3", "cfg4", "cfg5"])
     ap.add_argument("--alg", default=None)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -53,7 +53,8 @@ constexpr int gemm_stages(int bn) { return (225 * 1024) / (16384 + bn * 128) > 8
 template <int BN, int STAGES, int EPI>
 __global__ void __launch_bounds__(192, 1)
     gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                     void* __restrict__ out_, int M, int N, int kblk_total, int kblk_per_split, int splits) {
+                     void* __restrict__ out_, int M, int N, int kblk_total, int kblk_per_split, int splits,
+                     int pack) {
   using S = GemmSmem<BN, STAGES>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw;
@@ -98,6 +99,20 @@ __global__ void __launch_bounds__(192, 1)
     nkb = max(0, min(kblk_per_split, kblk_total - kb0));
   };
 
+  // B tile of k-block kb: row-major weights -> one [BN x 64] box; packed weights (pack rows per
+  // sub-tile, stored [N/pack][K/64][pack][64]) -> BN/pack contiguous boxes of pack x 128 B.
+  auto load_b = [&](uint32_t dst, uint32_t bar, int kb, int n_idx) {
+    if (pack == 0) {
+      tma_load_2d(dst, &tmB, bar, kb * 64, n_idx * BN);
+    } else {
+      const int per = BN / pack;
+      for (int j = 0; j < per; ++j) {
+        const int t = n_idx * per + j;
+        tma_load_2d(dst + j * pack * 128, &tmB, bar, 0, (t * kblk_total + kb) * pack);
+      }
+    }
+  };
+
   if (warp == 0) {
     if (lane == 0) {
       tma_prefetch(&tmA);
@@ -115,7 +130,7 @@ __global__ void __launch_bounds__(192, 1)
           const int pre = min(nkb, STAGES);
           for (int i = 0; i < pre; ++i) {
             mbar_expect_tx(full0 + 8 * i, S::kStage);
-            tma_load_2d(smem_u32(sB + i * S::kB), &tmB, full0 + 8 * i, (kb0 + i) * 64, n0);
+            load_b(smem_u32(sB + i * S::kB), full0 + 8 * i, kb0 + i, n_idx);
           }
           griddep_wait();
           waited = true;
@@ -129,7 +144,7 @@ __global__ void __launch_bounds__(192, 1)
           mbar_expect_tx(full0 + 8 * s, S::kStage);
           const int kc = (kb0 + kk) * 64;
           tma_load_2d(smem_u32(sA + s * S::kA), &tmA, full0 + 8 * s, kc, m0);
-          tma_load_2d(smem_u32(sB + s * S::kB), &tmB, full0 + 8 * s, kc, n0);
+          load_b(smem_u32(sB + s * S::kB), full0 + 8 * s, kb0 + kk, n_idx);
         }
       }
       if (!waited) griddep_wait();
@@ -228,7 +243,7 @@ __global__ void __launch_bounds__(192, 1)
 
 template <int BN, int EPI>
 static cudaError_t launch_gemm_t(const CUtensorMap& A, const CUtensorMap& B, void* out, int M, int N, int K, int splits,
-                                 cudaStream_t st) {
+                                 int pack, cudaStream_t st) {
   constexpr int ST = gemm_stages(BN);
   using S = GemmSmem<BN, ST>;
   auto kern = gemm_bf16_kernel<BN, ST, EPI>;
@@ -236,7 +251,7 @@ static cudaError_t launch_gemm_t(const CUtensorMap& A, const CUtensorMap& B, voi
   const int per = (kblk + splits - 1) / splits;
   const int units = ((N + BN - 1) / BN) * ((M + 127) / 128) * splits;
   const int grid = units < 148 ? units : 148;  // persistent: one CTA per SM
-  CUDA_TRY_LAUNCH(launch_k(kern, dim3(grid), dim3(192), S::kBytes, st, A, B, out, M, N, kblk, per, splits));
+  CUDA_TRY_LAUNCH(launch_k(kern, dim3(grid), dim3(192), S::kBytes, st, A, B, out, M, N, kblk, per, splits, pack));
   return cudaGetLastError();
 }
 
@@ -270,11 +285,11 @@ bool gemm_bn_supported(int bn, bool swiglu) {
 }
 
 cudaError_t launch_gemm_partial(const CUtensorMap& A, const CUtensorMap& B, float* out, int M, int N, int K,
-                                int splits, int bn, cudaStream_t st) {
+                                int splits, int bn, cudaStream_t st, int pack) {
   switch (bn) {
 #define L1(b) \
   case b:     \
-    return launch_gemm_t<b, EPI_PARTIAL>(A, B, out, M, N, K, splits, st);
+    return launch_gemm_t<b, EPI_PARTIAL>(A, B, out, M, N, K, splits, pack, st);
     PIC_GEMM_BNS(L1)
 #undef L1
   }
@@ -282,11 +297,11 @@ cudaError_t launch_gemm_partial(const CUtensorMap& A, const CUtensorMap& B, floa
 }
 
 cudaError_t launch_gemm_swiglu(const CUtensorMap& A, const CUtensorMap& B, void* u, int M, int N2, int K, int bn,
-                               cudaStream_t st) {
+                               cudaStream_t st, int pack) {
   switch (bn) {
 #define L2(b) \
   case b:     \
-    return launch_gemm_t<b, EPI_SWIGLU>(A, B, u, M, N2, K, 1, st);
+    return launch_gemm_t<b, EPI_SWIGLU>(A, B, u, M, N2, K, 1, pack, st);
     PIC_SWIGLU_BNS(L2)
 #undef L2
   }

@@ -60,12 +60,14 @@ cudaError_t launch_kv_link(void* Kpool, void* Vpool, const int32_t* src_slot, co
                            int Hkv, int D, const float* cos_t, const float* sin_t, int rebase, cudaStream_t st);
 
 // ---- GEMM (tcgen05): P[split][M][N] = A[M][K] · B[N][K]^T --------------------------------------
+// pack > 0: B is stored pre-tiled [N/pack][K/64][pack][64] (every TMA box contiguous); the tensor map
+// is then the 2-D view [rows][64] with a (64, pack) box.  pack = 0: row-major [N][K], box (64, bn).
 cudaError_t launch_gemm_partial(const CUtensorMap& A, const CUtensorMap& B, float* out, int M, int N, int K,
-                                int splits, int bn, cudaStream_t st);
+                                int splits, int bn, cudaStream_t st, int pack = 0);
 // Gate/up GEMM with the SwiGLU epilogue fused: B = interleaved [gate|up] groups of bn/2 rows (N2 = 2F rows),
 // u[M][F] bf16 = silu(x·W_gᵀ) ⊙ (x·W_uᵀ).  Split-K 1.
 cudaError_t launch_gemm_swiglu(const CUtensorMap& A, const CUtensorMap& B, void* u, int M, int N2, int K, int bn,
-                               cudaStream_t st);
+                               cudaStream_t st, int pack = 0);
 bool gemm_bn_supported(int bn, bool swiglu);
 // Interleaved gate/up generator: physical row p = n·2g + j holds gate row n·g + j (j < g) or up row
 // n·g + j − g (j >= g) of the logical [F][d] matrices (tags tag_gate / tag_up, same exponent).

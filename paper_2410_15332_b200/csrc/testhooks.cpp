@@ -3,6 +3,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -231,9 +232,17 @@ extern "C" pic_status pic_bench_gemm(int32_t M, int32_t N, int32_t K, int32_t bn
   TCK(cudaMemset(b.p, 0, wbytes * copies));
   CUtensorMap ta;
   std::vector<CUtensorMap> tb(copies);
+  const int pack = getenv("PIC_BENCH_PACK") ? atoi(getenv("PIC_BENCH_PACK")) : 0;
   uint64_t da[2] = {(uint64_t)K, (uint64_t)M}, db[2] = {(uint64_t)K, (uint64_t)N}, st[1] = {(uint64_t)K * 2};
   uint32_t ba[2] = {64, 128}, bb[2] = {64, (uint32_t)bn};
-  if (!tmap(&ta, a.p, 2, da, st, ba)) return PIC_E_CUDA;
+  if (pack) {  // packed view: rows of 64 elements
+    db[0] = 64;
+    db[1] = (uint64_t)N * K / 64;
+    st[0] = 128;
+    bb[1] = (uint32_t)pack;
+  }
+  uint64_t sta[1] = {(uint64_t)K * 2};
+  if (!tmap(&ta, a.p, 2, da, sta, ba)) return PIC_E_CUDA;
   for (int c = 0; c < copies; ++c)
     if (!tmap(&tb[c], (char*)b.p + wbytes * c, 2, db, st, bb)) return PIC_E_CUDA;
   cudaStream_t s;
@@ -242,10 +251,10 @@ extern "C" pic_status pic_bench_gemm(int32_t M, int32_t N, int32_t K, int32_t bn
   TCK(cudaEventCreate(&e0));
   TCK(cudaEventCreate(&e1));
   for (int i = 0; i < 3; ++i)
-    TCK(launch_gemm_partial(ta, tb[i % copies], reinterpret_cast<float*>(p.p), M, N, K, splits, bn, s));
+    TCK(launch_gemm_partial(ta, tb[i % copies], reinterpret_cast<float*>(p.p), M, N, K, splits, bn, s, pack));
   TCK(cudaEventRecord(e0, s));
   for (int i = 0; i < iters; ++i)
-    TCK(launch_gemm_partial(ta, tb[i % copies], reinterpret_cast<float*>(p.p), M, N, K, splits, bn, s));
+    TCK(launch_gemm_partial(ta, tb[i % copies], reinterpret_cast<float*>(p.p), M, N, K, splits, bn, s, pack));
   TCK(cudaEventRecord(e1, s));
   TCK(cudaEventSynchronize(e1));
   float ms = 0;
