@@ -125,6 +125,23 @@ pic_status pic_engine_create(const pic_model_config* cfg, const pic_engine_limit
                              void* arena, size_t arena_bytes, void* stream, pic_engine** out);
 void pic_engine_destroy(pic_engine* eng);
 
+/* Tensor parallelism (the Llama-3-70B shape): rank tp_rank of tp_size (1..8) owns q heads
+ * [r·H_q/tp, ...), kv heads [r·H_kv/tp, ...) and MLP columns [r·F/tp, ...) of the GLOBAL model `cfg`
+ * (weights are exact slices of the global generator); d_model, vocab, embeddings, norms and the LM head are
+ * replicated.  After the O and down projections the ranks' partial sums are all-reduced by the residual
+ * kernel itself, reading every rank's reduced partial directly from peer memory (CUDA IPC / NVLink) after
+ * an epoch barrier — no separate collective call.  Every rank must issue the same sequence of compile /
+ * link calls.  CacheBlend is single-rank only (PIC_E_VARIANT). */
+pic_status pic_arena_bytes_tp(const pic_model_config* cfg, const pic_engine_limits* limits, int32_t tp_size,
+                              size_t* out_bytes);
+pic_status pic_engine_create_tp(const pic_model_config* cfg, const pic_engine_limits* limits, int32_t device,
+                                void* arena, size_t arena_bytes, void* stream, int32_t tp_rank, int32_t tp_size,
+                                pic_engine** out);
+/* 64-byte CUDA IPC handle of this rank's arena (+ the arena's offset in that allocation). */
+pic_status pic_tp_ipc_handle(pic_engine* eng, void* handle64, uint64_t* offset);
+/* handles: tp_size x 64 bytes, offsets: tp_size (rank order, own entry ignored).  Must precede any compute. */
+pic_status pic_tp_connect(pic_engine* eng, const void* handles, const uint64_t* offsets);
+
 /* Compile step ("each chunk is encoded with position IDs starting from zero, and the LLM
  * performs only the prefill stage"; P:185 KVCompile).  chunks[i] is a host array of lens[i]
  * tokens.  All-or-nothing: on error no id is assigned and *err_index (nullable) names the failing

@@ -151,6 +151,7 @@ struct ArenaPlan {
   size_t off_E, off_lm, off_gf, off_cos, off_sin, off_K, off_V;
   size_t off_h, off_h2, off_ws, off_x, off_O, off_u, off_Q, off_xlast, off_opart, off_ml, off_logits, off_amax,
       off_cbdev, off_plan;
+  size_t off_ar, off_tpflags;
   size_t ws_floats;
   int attn_rows_cap, max_seqs, max_tiles, max_bt, max_k2;
   size_t plan_ints;
@@ -205,14 +206,45 @@ static ArenaPlan plan_arena(const pic_model_config& c, const pic_engine_limits& 
   a.plan_ints = 5 * M + 3 * (size_t)a.max_tiles + a.max_seqs + a.max_bt + 3 * (size_t)a.max_k2 +
                 7 * (size_t)l.max_tokens + 3 * (size_t)a.max_tiles + M + 4096;
   a.off_plan = L.add(a.plan_ints * 4);
+  // tensor parallel: two reduced-partial buffers (alternating per all-reduce), flags, epoch counter
+  a.off_ar = L.add(2 * M * d * 4);
+  a.off_tpflags = L.add(8 * 8 + 8);
   a.total = L.total + 1024;
   return a;
+}
+
+// Per-rank model: heads and MLP columns sharded over tp ranks; d_model, vocab replicated.
+static pic_model_config local_cfg(const pic_model_config& g, int tp) {
+  pic_model_config c = g;
+  c.n_heads /= tp;
+  c.n_kv_heads /= tp;
+  c.ffn_dim /= tp;
+  return c;
+}
+
+static pic_status validate_tp(const pic_model_config* c, int tp_rank, int tp_size) {
+  if (tp_size < 1 || tp_size > 8 || tp_rank < 0 || tp_rank >= tp_size)
+    return fail(PIC_E_INVALID_ARG, "bad tensor-parallel rank %d / size %d (size 1..8)", tp_rank, tp_size);
+  if (c->n_heads % tp_size || c->n_kv_heads % tp_size || c->ffn_dim % tp_size || (c->ffn_dim / tp_size) % 64)
+    return fail(PIC_E_CONFIG, "heads / kv-heads / ffn_dim not divisible by tp %d (ffn_dim/tp %% 64)", tp_size);
+  return PIC_OK;
 }
 
 extern "C" pic_status pic_arena_bytes(const pic_model_config* cfg, const pic_engine_limits* limits, size_t* out) {
   TRY(validate_cfg(cfg, limits));
   if (!out) return fail(PIC_E_INVALID_ARG, "NULL out_bytes");
   *out = plan_arena(*cfg, *limits).total;
+  return PIC_OK;
+}
+
+extern "C" pic_status pic_arena_bytes_tp(const pic_model_config* cfg, const pic_engine_limits* limits, int32_t tp_size,
+                                         size_t* out) {
+  TRY(validate_cfg(cfg, limits));
+  TRY(validate_tp(cfg, 0, tp_size));
+  if (!out) return fail(PIC_E_INVALID_ARG, "NULL out_bytes");
+  const pic_model_config lc = local_cfg(*cfg, tp_size);
+  TRY(validate_cfg(&lc, limits));
+  *out = plan_arena(lc, *limits).total;
   return PIC_OK;
 }
 
@@ -276,6 +308,10 @@ static pic_status init_device(pic_engine* e, void* arena, size_t bytes, cudaStre
   const int64_t qkv = (Hq + 2 * Hkv) * D;
   const uint64_t s = c.seed;
   auto al = [](size_t x) { return (x + 1023) & ~size_t(1023); };
+  // tensor-parallel shard of the global weights: rank r owns q heads [r·Hq, (r+1)·Hq), kv heads
+  // [r·Hkv, ...), MLP columns [r·F, (r+1)·F) (local sizes); exponents use the GLOBAL fan-in.
+  const int64_t tr = e->tp_rank, tp = e->tp_size;
+  const int64_t gHqD = Hq * D * tp, gF = F * tp;
   // gate/up interleave group for the fused SwiGLU epilogue: the g dividing F whose F/g tiles best fill
   // one wave of 148 CTAs at skinny M (Mistral/Llama F = 14336: g = 112 -> 128 tiles of N = 224)
   e->gu_group = 0;
@@ -308,19 +344,19 @@ static pic_status init_device(pic_engine* e, void* arena, size_t bytes, cudaStre
     w.g2 = reinterpret_cast<float*>(p);
     const uint64_t T = (uint64_t)l * 16;
     char* q = reinterpret_cast<char*>(w.qkv);
-    CK(launch_gen_matrix(q, Hq * D, d, s, T + 0, weight_exponent(d), 0, st));
-    CK(launch_gen_matrix(q + Hq * D * d * 2, Hkv * D, d, s, T + 1, weight_exponent(d), 0, st));
-    CK(launch_gen_matrix(q + (Hq + Hkv) * D * d * 2, Hkv * D, d, s, T + 2, weight_exponent(d), 0, st));
-    CK(launch_gen_matrix(w.o, d, Hq * D, s, T + 3, weight_exponent(Hq * D), 0, st));
+    CK(launch_gen_matrix(q, Hq * D, d, s, T + 0, weight_exponent(d), tr * Hq * D, st));
+    CK(launch_gen_matrix(q + Hq * D * d * 2, Hkv * D, d, s, T + 1, weight_exponent(d), tr * Hkv * D, st));
+    CK(launch_gen_matrix(q + (Hq + Hkv) * D * d * 2, Hkv * D, d, s, T + 2, weight_exponent(d), tr * Hkv * D, st));
+    CK(launch_gen_matrix(w.o, d, Hq * D, s, T + 3, weight_exponent(gHqD), 0, st, gHqD, tr * Hq * D));
     if (e->gu_group > 0) {
       // gate/up interleaved in groups of g rows for the fused SwiGLU GEMM epilogue
-      CK(launch_gen_gateup(w.gu, F, d, s, T + 4, T + 5, weight_exponent(d), e->gu_group, st));
+      CK(launch_gen_gateup(w.gu, F, d, s, T + 4, T + 5, weight_exponent(d), e->gu_group, st, tr * F));
     } else {
       char* gu = reinterpret_cast<char*>(w.gu);
-      CK(launch_gen_matrix(gu, F, d, s, T + 4, weight_exponent(d), 0, st));
-      CK(launch_gen_matrix(gu + F * d * 2, F, d, s, T + 5, weight_exponent(d), 0, st));
+      CK(launch_gen_matrix(gu, F, d, s, T + 4, weight_exponent(d), tr * F, st));
+      CK(launch_gen_matrix(gu + F * d * 2, F, d, s, T + 5, weight_exponent(d), tr * F, st));
     }
-    CK(launch_gen_matrix(w.down, d, F, s, T + 6, weight_exponent(F), 0, st));
+    CK(launch_gen_matrix(w.down, d, F, s, T + 6, weight_exponent(gF), 0, st, gF, tr * F));
     CK(launch_gen_gains(w.g1, d, s, T + 7, st));
     CK(launch_gen_gains(w.g2, d, s, T + 8, st));
     TRY(make_tmaps_bn(w.tm_qkv, w.qkv, qkv, d));
@@ -404,6 +440,18 @@ static pic_status init_device(pic_engine* e, void* arena, size_t bytes, cudaStre
     uint32_t box[3] = {64, (uint32_t)G, (uint32_t)(128 / G)};
     TRY(make_tmap(&e->tm_Q, e->Q, 3, dims, strides, box));
   }
+  e->ar_buf[0] = reinterpret_cast<float*>(b + a.off_ar);
+  e->ar_buf[1] = e->ar_buf[0] + (size_t)M * d;
+  e->tp_flags = reinterpret_cast<long long*>(b + a.off_tpflags);
+  e->tp_counter = e->tp_flags + 8;
+  CK(cudaMemsetAsync(e->tp_flags, 0, 9 * 8, st));
+  for (int r = 0; r < 8; ++r) {
+    e->peer_flags.p[r] = nullptr;
+    e->peer_ar[0][r] = e->peer_ar[1][r] = nullptr;
+  }
+  e->peer_flags.p[e->tp_rank] = e->tp_flags;
+  e->peer_ar[0][e->tp_rank] = e->ar_buf[0];
+  e->peer_ar[1][e->tp_rank] = e->ar_buf[1];
   CK(cudaMallocHost(&e->plan_host, a.plan_ints * 4));
   CK(cudaMallocHost(&e->host_logits, (size_t)e->lim.max_requests * V * 4));
   CK(cudaMallocHost(&e->host_amax, (size_t)e->lim.max_requests * 4));
@@ -417,13 +465,21 @@ static pic_status init_device(pic_engine* e, void* arena, size_t bytes, cudaStre
   return PIC_OK;
 }
 
-extern "C" pic_status pic_engine_create(const pic_model_config* cfg, const pic_engine_limits* limits, int32_t device,
-                                        void* arena, size_t arena_bytes, void* stream, pic_engine** out) {
+extern "C" pic_status pic_engine_create_tp(const pic_model_config* gcfg, const pic_engine_limits* limits,
+                                           int32_t device, void* arena, size_t arena_bytes, void* stream,
+                                           int32_t tp_rank, int32_t tp_size, pic_engine** out) {
+  TRY(validate_cfg(gcfg, limits));
+  TRY(validate_tp(gcfg, tp_rank, tp_size));
+  const pic_model_config lc = local_cfg(*gcfg, tp_size);
+  const pic_model_config* cfg = &lc;
   TRY(validate_cfg(cfg, limits));
   if (!out) return fail(PIC_E_INVALID_ARG, "NULL out");
   *out = nullptr;
   pic_engine* e = new (std::nothrow) pic_engine();
   if (!e) return fail(PIC_E_OOM, "engine allocation failed");
+  e->tp_rank = tp_rank;
+  e->tp_size = tp_size;
+  e->gcfg = *gcfg;
   e->cfg = *cfg;
   e->lim = *limits;
   e->device = device;
@@ -456,6 +512,56 @@ extern "C" pic_status pic_engine_create(const pic_model_config* cfg, const pic_e
   return PIC_OK;
 }
 
+extern "C" pic_status pic_engine_create(const pic_model_config* cfg, const pic_engine_limits* limits, int32_t device,
+                                        void* arena, size_t arena_bytes, void* stream, pic_engine** out) {
+  return pic_engine_create_tp(cfg, limits, device, arena, arena_bytes, stream, 0, 1, out);
+}
+
+// CUDA IPC handle of this engine's arena (exchanged by the caller, e.g. torch.distributed all_gather).
+extern "C" pic_status pic_tp_ipc_handle(pic_engine* e, void* handle64, uint64_t* offset) {
+  if (!e || !handle64 || !offset) return fail(PIC_E_INVALID_ARG, "NULL argument");
+  if (e->host_only) return fail(PIC_E_NO_DEVICE, "host-only engine");
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  typedef CUresult (*GetRange)(CUdeviceptr*, size_t*, CUdeviceptr);
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  CK(cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q));
+  if (!fn || reinterpret_cast<GetRange>(fn)(&base, &size, (CUdeviceptr)e->arena) != CUDA_SUCCESS)
+    return fail(PIC_E_CUDA, "cuMemGetAddressRange failed");
+  cudaIpcMemHandle_t h;
+  CK(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)));
+  std::memcpy(handle64, &h, sizeof h);
+  *offset = (uint64_t)((CUdeviceptr)e->arena - base);
+  return PIC_OK;
+}
+
+// Open every peer rank's arena (handles[r], offsets[r] from pic_tp_ipc_handle of rank r) and wire the
+// peer pointers of the fused all-reduce.  Same layout on every rank (same config and limits).
+extern "C" pic_status pic_tp_connect(pic_engine* e, const void* handles, const uint64_t* offsets) {
+  if (!e || !handles || !offsets) return fail(PIC_E_INVALID_ARG, "NULL argument");
+  if (e->host_only) return fail(PIC_E_NO_DEVICE, "host-only engine");
+  for (int r = 0; r < e->tp_size; ++r) {
+    if (r == e->tp_rank) continue;
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, reinterpret_cast<const char*>(handles) + 64 * r, sizeof h);
+    void* base = nullptr;
+    CK(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
+    e->ipc_opened.push_back(base);
+    char* peer = reinterpret_cast<char*>(base) + offsets[r];
+    const ptrdiff_t d_ar0 = reinterpret_cast<char*>(e->ar_buf[0]) - e->arena;
+    const ptrdiff_t d_ar1 = reinterpret_cast<char*>(e->ar_buf[1]) - e->arena;
+    const ptrdiff_t d_fl = reinterpret_cast<char*>(e->tp_flags) - e->arena;
+    // the arena base is aligned up to 1 KB inside the caller's buffer: same rule on every rank
+    char* pb = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(peer) + 1023) & ~uintptr_t(1023));
+    e->peer_ar[0][r] = reinterpret_cast<float*>(pb + d_ar0);
+    e->peer_ar[1][r] = reinterpret_cast<float*>(pb + d_ar1);
+    e->peer_flags.p[r] = pb + d_fl;
+  }
+  e->tp_connected = true;
+  return PIC_OK;
+}
+
 extern "C" void pic_engine_destroy(pic_engine* e) {
   if (!e) return;
   if (!e->host_only) {
@@ -467,6 +573,7 @@ extern "C" void pic_engine_destroy(pic_engine* e) {
     if (e->ev0) cudaEventDestroy(e->ev0);
     if (e->ev1) cudaEventDestroy(e->ev1);
     if (e->cap_stream) cudaStreamDestroy(e->cap_stream);
+    for (void* p : e->ipc_opened) cudaIpcCloseMemHandle(p);
     for (cudaEvent_t ev : e->ev_pool) cudaEventDestroy(ev);
   }
   delete e;
@@ -675,6 +782,27 @@ static pic_status enqueue_forward(pic_engine* e, const Fwd& f, const DevPlan& dp
   const int32_t* head_map = dp.head_map;
   float* prevP = nullptr;
   int prev_s = 0;
+  int ar_parity = 0;  // alternates per all-reduce; 2L (link) or 2L-2 (compile) per forward: even
+  // residual add (+ RMSNorm): h += Σ partials; under tensor parallelism the partials of every rank are
+  // summed straight from peer memory (this rank's splits reduced first, then an epoch barrier)
+  auto add_norm = [&](float* Pp, int sp, const float* gain, void* xout, const int32_t* map, int rows,
+                      double extra_bytes) -> pic_status {
+    if (e->tp_size == 1 || !Pp) {
+      PROF("rmsnorm", (double)rows * d * (8 + 4 * (Pp ? sp : 0)) + extra_bytes, 0,
+           launch_residual_rmsnorm(hc, Pp, sp, gain, xout, map, rows, d, eps, st));
+      return PIC_OK;
+    }
+    float* mine = e->ar_buf[ar_parity];
+    PROF("tp_allreduce", (double)rows * d * 4 * (sp + 1), 0, launch_tp_reduce_local(Pp, sp, rows, d, mine, st));
+    PROF("tp_allreduce", 0, 0, launch_tp_barrier(e->tp_counter, e->peer_flags, e->tp_rank, e->tp_size, st));
+    Srcs srcs{};
+    srcs.n = e->tp_size;
+    for (int r = 0; r < e->tp_size; ++r) srcs.p[r] = e->peer_ar[ar_parity][r];
+    PROF("rmsnorm", (double)rows * d * (8 + 4 * e->tp_size) + extra_bytes, 0,
+         launch_residual_rmsnorm_srcs(hc, srcs, gain, xout, map, rows, d, eps, st));
+    ar_parity ^= 1;
+    return PIC_OK;
+  };
   auto capture = [&](int layer) -> pic_status {
     if (!debug_hidden) return PIC_OK;
     CK(cudaMemcpyAsync(debug_hidden + (size_t)layer * f.debug_rows * d, hc, (size_t)M * d * 4, cudaMemcpyDeviceToHost,
@@ -687,7 +815,7 @@ static pic_status enqueue_forward(pic_engine* e, const Fwd& f, const DevPlan& dp
     char* Vl = Vp + l * lbytes;
     int s = 0;
     ++R.launches;
-    PROF("rmsnorm", (double)M * d * (8 + 4 * prev_s + 2), 0, launch_residual_rmsnorm(hc, prevP, prev_s, w.g1, e->x, nullptr, M, d, eps, st));
+    TRY(add_norm(prevP, prev_s, w.g1, e->x, nullptr, M, (double)M * d * 2));
     if (l > 0) TRY(capture(l - 1));
     TRY(R.gemm(e->tm_x, w.tm_qkv, M, qkv, d, &s));
     if (f.cb && l == f.cb_layer) {
@@ -768,7 +896,7 @@ static pic_status enqueue_forward(pic_engine* e, const Fwd& f, const DevPlan& dp
     // a7 O projection, residual + a8 MLP
     TRY(R.gemm(e->tm_O, w.tm_o, M, d, Hq * D, &s));
     ++R.launches;
-    PROF("rmsnorm", (double)M * d * (8 + 4 * s + 2), 0, launch_residual_rmsnorm(hc, e->ws, s, w.g2, e->x, nullptr, M, d, eps, st));
+    TRY(add_norm(e->ws, s, w.g2, e->x, nullptr, M, (double)M * d * 2));
     if (e->gu_group > 0) {
       ++R.launches;
       PROF("gemm", (double)2 * F * d * 2 + (double)M * d * 2 + (double)M * F * 2, 2.0 * M * 2 * F * d,
@@ -785,7 +913,7 @@ static pic_status enqueue_forward(pic_engine* e, const Fwd& f, const DevPlan& dp
   if (!f.compile) {
     // a10: final norm of the last rows, LM head, argmax
     ++R.launches;
-    PROF("rmsnorm", (double)M * d * (8 + 4 * prev_s) + (double)f.n_head * d * 2, 0, launch_residual_rmsnorm(hc, prevP, prev_s, e->gf, e->x_last, head_map, M, d, eps, st));
+    TRY(add_norm(prevP, prev_s, e->gf, e->x_last, head_map, M, (double)f.n_head * d * 2));
     TRY(capture(L - 1));
     int s = 0;
     TRY(R.gemm(e->tm_xlast, e->tm_lm, f.n_head, c.vocab, d, &s));
@@ -965,6 +1093,10 @@ extern "C" pic_status pic_generate_context_cache(pic_engine* e, const int32_t* c
   auto rollback = [&]() {
     for (auto& b : blocks) e->alloc.release(b);
   };
+  if (!e->host_only && e->tp_size > 1 && !e->tp_connected) {
+    rollback();
+    return fail(PIC_E_INVALID_ARG, "tensor-parallel engine: call pic_tp_connect first");
+  }
   if (!e->host_only) {
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     // pack (chunk, row range) pieces into forwards of <= max_rows rows / max_seqs sequences
@@ -1087,6 +1219,8 @@ static pic_status link_impl(pic_engine* e, int32_t n_req, const pic_segment* con
   if ((cb || pr->debug_hidden) && n_req != 1) return fail(PIC_E_VARIANT, "CacheBlend/debug hooks are single-request");
   if (pr->sel_override && !cb) return fail(PIC_E_VARIANT, "sel_override is a CacheBlend hook");
   if (e->host_only) return fail(PIC_E_NO_DEVICE, "host-only engine cannot link");
+  if (e->tp_size > 1 && !e->tp_connected) return fail(PIC_E_INVALID_ARG, "tensor-parallel engine: call pic_tp_connect first");
+  if (e->tp_size > 1 && cb) return fail(PIC_E_VARIANT, "CacheBlend is not supported with tensor parallelism");
   std::vector<ReqBuild> reqs(n_req);
   int64_t need = 0;
   for (int r = 0; r < n_req; ++r) {

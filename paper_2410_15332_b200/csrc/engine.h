@@ -101,7 +101,16 @@ struct pic_linked {
 };
 
 struct pic_engine {
-  pic_model_config cfg{};
+  pic_model_config cfg{};   // this rank's (local) model: heads / ffn_dim divided by tp_size
+  pic_model_config gcfg{};  // global model
+  int tp_rank = 0, tp_size = 1;
+  bool tp_connected = false;
+  float* ar_buf[2] = {nullptr, nullptr};       // reduced partials exchanged across ranks (alternating)
+  long long *tp_flags = nullptr, *tp_counter = nullptr;
+  float* peer_ar[2][8];                        // every rank's ar_buf (peer memory), own included
+  pic::Peers peer_flags{};
+  std::vector<void*> ipc_opened;
+  int ar_parity = 0;
   pic_engine_limits lim{};
   int device = -1;
   bool host_only = true;

@@ -31,9 +31,10 @@ cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
 cudaError_t prepare_kernels();
 
 // ---- K15 weight generator, bit-exact with seedgen/ -------------------------
-// dst[r][c] = bf16( bf16_rne(f(U(seed, tag, (row0 + r) * cols + c))) * 2^exp2 ), r < rows.
+// dst[r][c] = bf16( bf16_rne(f(U(seed, tag, (row0 + r) * logical_cols + col0 + c))) * 2^exp2 ), r < rows,
+// c < cols (logical_cols = 0 -> cols): row/column slices of the logical matrix (tensor-parallel shards).
 cudaError_t launch_gen_matrix(void* dst_bf16, int64_t rows, int64_t cols, uint64_t seed, uint64_t tag, int exp2,
-                              int64_t row0, cudaStream_t st);
+                              int64_t row0, cudaStream_t st, int64_t logical_cols = 0, int64_t col0 = 0);
 // dst[i] = 1 + ((U(seed, tag, i) >> 61) - 4) / 32   (fp32)
 cudaError_t launch_gen_gains(float* dst, int64_t n, uint64_t seed, uint64_t tag, cudaStream_t st);
 
@@ -41,6 +42,19 @@ cudaError_t launch_gen_gains(float* dst, int64_t n, uint64_t seed, uint64_t tag,
 cudaError_t launch_embed(const void* E, const int32_t* tok, float* h, int M, int d, cudaStream_t st);
 
 // ---- a4: residual add of split-K partials + RMSNorm ----------------------------------------
+constexpr int kMaxSrcs = 16;
+struct Srcs {  // fp32 [M][d] arrays summed into the residual (split-K partials or peer ranks' sums)
+  const float* p[kMaxSrcs];
+  int n;
+};
+struct Peers {  // per-rank device pointers (peer memory through CUDA IPC / NVLink)
+  void* p[8];
+};
+cudaError_t launch_residual_rmsnorm_srcs(float* h, const Srcs& srcs, const float* g, void* x, const int32_t* out_map,
+                                         int M, int d, float eps, cudaStream_t st);
+// tensor parallel: reduce this rank's split-K partials; cross-rank epoch barrier over peer memory
+cudaError_t launch_tp_reduce_local(const float* P, int splits, int M, int d, float* out, cudaStream_t st);
+cudaError_t launch_tp_barrier(long long* counter, const Peers& flags, int rank, int tp, cudaStream_t st);
 // h[r] += Σ_s P[s][r] (P nullable); if x: x[out_map ? out_map[r] : r] = bf16(rms(h[r]) ⊙ g) for out_map[r] >= 0
 cudaError_t launch_residual_rmsnorm(float* h, const float* P, int splits, const float* g, void* x,
                                     const int32_t* out_map, int M, int d, float eps, cudaStream_t st);
@@ -72,7 +86,7 @@ bool gemm_bn_supported(int bn, bool swiglu);
 // Interleaved gate/up generator: physical row p = n·2g + j holds gate row n·g + j (j < g) or up row
 // n·g + j − g (j >= g) of the logical [F][d] matrices (tags tag_gate / tag_up, same exponent).
 cudaError_t launch_gen_gateup(void* dst_bf16, int64_t F, int64_t d, uint64_t seed, uint64_t tag_gate,
-                              uint64_t tag_up, int exp2, int g, cudaStream_t st);
+                              uint64_t tag_up, int exp2, int g, cudaStream_t st, int64_t f0 = 0);
 
 // ---- a6: sparse-query causal attention (tcgen05, D = 128) + split-KV combine ----------------
 struct AttnArgs {

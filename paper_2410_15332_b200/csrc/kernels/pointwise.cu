@@ -56,38 +56,43 @@ PIC_DEV uint16_t gen_weight_bits(uint64_t key, uint64_t idx, float scale) {
   return (uint16_t)(__float_as_uint(w) >> 16);
 }
 
-__global__ void gen_matrix_kernel(uint16_t* __restrict__ dst, int64_t n8, int64_t base, uint64_t key, float scale) {
+// dst[r][c] (r < rows, c < cols) = weight at logical index (row0 + r) * logical_cols + col0 + c:
+// a row slice (row0) and/or column slice (col0, logical_cols) of the logical [out][in] matrix, so a
+// tensor-parallel shard gets exactly the global weights (SURVEY §8(c).6 "TP shards take slices").
+__global__ void gen_matrix_kernel(uint16_t* __restrict__ dst, int64_t n8, int64_t cols, int64_t row0,
+                                  int64_t logical_cols, int64_t col0, uint64_t key, float scale) {
   PIC_PDL_ENTRY();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n8; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = (8 * i) / cols, c = (8 * i) % cols;
+    const uint64_t base = (uint64_t)((row0 + r) * logical_cols + col0 + c);
     uint32_t w[4];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const uint64_t c = (uint64_t)(base + 8 * i + 2 * j);
-      w[j] = (uint32_t)gen_weight_bits(key, c, scale) | ((uint32_t)gen_weight_bits(key, c + 1, scale) << 16);
-    }
+    for (int j = 0; j < 4; ++j)
+      w[j] = (uint32_t)gen_weight_bits(key, base + 2 * j, scale) | ((uint32_t)gen_weight_bits(key, base + 2 * j + 1, scale) << 16);
     reinterpret_cast<uint4*>(dst)[i] = make_uint4(w[0], w[1], w[2], w[3]);
   }
 }
 
 cudaError_t launch_gen_matrix(void* dst, int64_t rows, int64_t cols, uint64_t seed, uint64_t tag, int exp2,
-                              int64_t row0, cudaStream_t st) {
+                              int64_t row0, cudaStream_t st, int64_t logical_cols, int64_t col0) {
   const int64_t n = rows * cols;
-  if (n % 8) return cudaErrorInvalidValue;
+  if (n % 8 || cols % 8) return cudaErrorInvalidValue;
+  if (logical_cols <= 0) logical_cols = cols;
   const float scale = ldexpf(1.0f, exp2);
-  CUDA_TRY_LAUNCH(launch_k(gen_matrix_kernel, dim3(148 * 8), dim3(256), 0, st, reinterpret_cast<uint16_t*>(dst), n / 8, row0 * cols,
-                                             stream_key(seed, tag), scale));
+  CUDA_TRY_LAUNCH(launch_k(gen_matrix_kernel, dim3(148 * 8), dim3(256), 0, st, reinterpret_cast<uint16_t*>(dst), n / 8,
+                           cols, row0, logical_cols, col0, stream_key(seed, tag), scale));
   return cudaGetLastError();
 }
 
 __global__ void gen_gateup_kernel(uint16_t* __restrict__ dst, int64_t F, int64_t d, uint64_t key_g, uint64_t key_u,
-                                  float scale, int g) {
+                                  float scale, int g, int64_t f0) {
   PIC_PDL_ENTRY();
   const int64_t n8 = 2 * F * d / 8;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n8; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t p = (8 * i) / d, c = (8 * i) % d;  // physical row, column
     const int64_t n = p / (2 * g), j = p % (2 * g);
     const bool up = j >= g;
-    const int64_t f = n * g + (up ? j - g : j);
+    const int64_t f = f0 + n * g + (up ? j - g : j);
     const uint64_t key = up ? key_u : key_g;
     uint32_t w[4];
 #pragma unroll
@@ -100,10 +105,10 @@ __global__ void gen_gateup_kernel(uint16_t* __restrict__ dst, int64_t F, int64_t
 }
 
 cudaError_t launch_gen_gateup(void* dst, int64_t F, int64_t d, uint64_t seed, uint64_t tag_gate, uint64_t tag_up,
-                              int exp2, int g, cudaStream_t st) {
+                              int exp2, int g, cudaStream_t st, int64_t f0) {
   if (d % 8 || F % g) return cudaErrorInvalidValue;
   CUDA_TRY_LAUNCH(launch_k(gen_gateup_kernel, dim3(148 * 8), dim3(256), 0, st, reinterpret_cast<uint16_t*>(dst), F, d,
-                           stream_key(seed, tag_gate), stream_key(seed, tag_up), ldexpf(1.0f, exp2), g));
+                           stream_key(seed, tag_gate), stream_key(seed, tag_up), ldexpf(1.0f, exp2), g, f0));
   return cudaGetLastError();
 }
 
@@ -182,10 +187,12 @@ PIC_DEV float4 sum_splits4(const float4* __restrict__ P4, int splits, size_t str
   return acc;
 }
 
-// h[r] += Σ_s P[s][r];  x[out] = bf16(h · rsqrt(mean h² + ε) · g)   (reading R4, fp32 residual R15)
-// One CTA per row, one float4 of the row per thread (d/4 threads, <= 1024).
-__global__ void __launch_bounds__(1024) residual_rmsnorm_kernel(float* __restrict__ h, const float* __restrict__ P,
-                                                                 int splits, const float* __restrict__ g,
+// h[r] += Σ_k src_k[r];  x[out] = bf16(h · rsqrt(mean h² + ε) · g)   (reading R4, fp32 residual R15)
+// The sources are the split-K partials of the producing GEMM, or — under tensor parallelism — every
+// rank's reduced partial read directly from peer memory in rank order (the all-reduce fused into the
+// consumer; deterministic and identical on all ranks).  One CTA per row, one float4 per thread.
+__global__ void __launch_bounds__(1024) residual_rmsnorm_kernel(float* __restrict__ h, Srcs srcs,
+                                                                 const float* __restrict__ g,
                                                                  uint16_t* __restrict__ x,
                                                                  const int32_t* __restrict__ out_map, int M, int d,
                                                                  float eps) {
@@ -194,13 +201,15 @@ __global__ void __launch_bounds__(1024) residual_rmsnorm_kernel(float* __restric
   const int r = blockIdx.x;
   const int n4 = d / 4;
   float4* hr = reinterpret_cast<float4*>(h + (size_t)r * d);
-  const float4* P4 = reinterpret_cast<const float4*>(P) + (size_t)r * n4;
-  const size_t stride4 = (size_t)M * n4;
   float ss = 0.f;
   for (int i = threadIdx.x; i < n4; i += blockDim.x) {
     float4 v = hr[i];
-    if (splits) {
-      add4(v, sum_splits4(P4, splits, stride4, i));
+    if (srcs.n) {
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 8
+      for (int k = 0; k < srcs.n; ++k)
+        add4(acc, __ldcg(reinterpret_cast<const float4*>(srcs.p[k]) + (size_t)r * n4 + i));
+      add4(v, acc);
       hr[i] = v;
     }
     ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
@@ -218,12 +227,68 @@ __global__ void __launch_bounds__(1024) residual_rmsnorm_kernel(float* __restric
   }
 }
 
-cudaError_t launch_residual_rmsnorm(float* h, const float* P, int splits, const float* g, void* x,
-                                    const int32_t* out_map, int M, int d, float eps, cudaStream_t st) {
+cudaError_t launch_residual_rmsnorm_srcs(float* h, const Srcs& srcs, const float* g, void* x, const int32_t* out_map,
+                                         int M, int d, float eps, cudaStream_t st) {
   if (M == 0) return cudaSuccess;
   const int nt = std::max(32, std::min(1024, d / 4));
-  CUDA_TRY_LAUNCH(launch_k(residual_rmsnorm_kernel, dim3(M), dim3(nt), 0, st, h, P, P ? splits : 0, g, reinterpret_cast<uint16_t*>(x), out_map, M, d,
-                                            eps));
+  CUDA_TRY_LAUNCH(launch_k(residual_rmsnorm_kernel, dim3(M), dim3(nt), 0, st, h, srcs, g, reinterpret_cast<uint16_t*>(x),
+                           out_map, M, d, eps));
+  return cudaGetLastError();
+}
+
+cudaError_t launch_residual_rmsnorm(float* h, const float* P, int splits, const float* g, void* x,
+                                    const int32_t* out_map, int M, int d, float eps, cudaStream_t st) {
+  Srcs s{};
+  s.n = P ? splits : 0;
+  if (s.n > kMaxSrcs) return cudaErrorInvalidValue;
+  for (int k = 0; k < s.n; ++k) s.p[k] = P + (size_t)k * M * d;
+  return launch_residual_rmsnorm_srcs(h, s, g, x, out_map, M, d, eps, st);
+}
+
+// ================================================================================ tensor parallel
+// out[r] = Σ_s P[s][r]  (this rank's split-K partials reduced before the cross-rank exchange)
+__global__ void tp_reduce_local_kernel(const float4* __restrict__ P, int splits, size_t n4, float4* __restrict__ out) {
+  PIC_PDL_ENTRY();
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n4; i += (size_t)gridDim.x * blockDim.x) {
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 8
+    for (int s = 0; s < splits; ++s) add4(acc, P[s * n4 + i]);
+    out[i] = acc;
+  }
+}
+
+cudaError_t launch_tp_reduce_local(const float* P, int splits, int M, int d, float* out, cudaStream_t st) {
+  const size_t n4 = (size_t)M * d / 4;
+  const int blocks = (int)std::min<size_t>((n4 + 255) / 256, (size_t)148 * 8);
+  CUDA_TRY_LAUNCH(launch_k(tp_reduce_local_kernel, dim3(blocks), dim3(256), 0, st, reinterpret_cast<const float4*>(P),
+                           splits, n4, reinterpret_cast<float4*>(out)));
+  return cudaGetLastError();
+}
+
+// Cross-rank epoch barrier over peer memory: every rank writes the new epoch into slot [rank] of every
+// rank's flag array (system-scope release), then waits until all slots of its own array reach it
+// (acquire).  The epoch counter lives in device memory, so CUDA-graph replays stay in lockstep.
+__global__ void tp_barrier_kernel(long long* counter, Peers flags, int rank, int tp) {
+  PIC_PDL_ENTRY();
+  if (threadIdx.x != 0) return;
+  const long long epoch = *counter + 1;
+  *counter = epoch;
+  __threadfence_system();
+  for (int p = 0; p < tp; ++p) {
+    long long* slot = reinterpret_cast<long long*>(flags.p[p]) + rank;
+    asm volatile("st.release.sys.global.b64 [%0], %1;" ::"l"(slot), "l"(epoch) : "memory");
+  }
+  const long long* mine = reinterpret_cast<const long long*>(flags.p[rank]);
+  for (int p = 0; p < tp; ++p) {
+    long long v;
+    do {
+      asm volatile("ld.acquire.sys.global.b64 %0, [%1];" : "=l"(v) : "l"(mine + p) : "memory");
+    } while (v < epoch);
+  }
+}
+
+cudaError_t launch_tp_barrier(long long* counter, const Peers& flags, int rank, int tp, cudaStream_t st) {
+  CUDA_TRY_LAUNCH(launch_k(tp_barrier_kernel, dim3(1), dim3(32), 0, st, counter, flags, rank, tp));
   return cudaGetLastError();
 }
 

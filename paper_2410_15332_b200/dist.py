@@ -55,3 +55,13 @@ def sum_over_ranks(value: float, device=None) -> float:
     t = torch.tensor([float(value)], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.SUM)
     return float(t.item())
+
+
+def tp_connect(engine, group=None) -> None:
+    """Exchange the engines' CUDA IPC arena handles across the tensor-parallel group and wire the peer
+    pointers of the fused all-reduce (every rank of `group` calls this once, in rank order)."""
+    import torch.distributed as dist
+    mine = engine.ipc_handle()
+    allh = [None] * dist.get_world_size(group)
+    dist.all_gather_object(allh, mine, group=group)
+    engine.tp_connect(allh)

@@ -78,7 +78,8 @@ class KernelStatC(C.Structure):
 EXPORTS = ["pic_arena_bytes", "pic_engine_create", "pic_engine_destroy", "pic_generate_context_cache", "pic_link",
            "pic_link_batch", "pic_plan", "pic_linked_export", "pic_linked_info", "pic_linked_release",
            "pic_cache_export", "pic_cache_info", "pic_expire_cache", "pic_read_weights", "pic_get_stats",
-           "pic_last_error", "pic_status_string", "pic_set_profiling", "pic_get_profile", "pic_test_gemm", "pic_test_attention", "pic_test_kv_link", "pic_bench_gemm", "pic_bench_attention", "pic_test_gemm_swiglu"]
+           "pic_last_error", "pic_status_string", "pic_arena_bytes_tp", "pic_engine_create_tp", "pic_tp_ipc_handle",
+           "pic_tp_connect", "pic_set_profiling", "pic_get_profile", "pic_test_gemm", "pic_test_attention", "pic_test_kv_link", "pic_bench_gemm", "pic_bench_attention", "pic_test_gemm_swiglu"]
 
 _lib = None
 
@@ -96,6 +97,11 @@ def lib() -> C.CDLL:
         L.pic_arena_bytes.argtypes = [P(ModelConfigC), P(LimitsC), P(C.c_size_t)]
         L.pic_engine_create.argtypes = [P(ModelConfigC), P(LimitsC), C.c_int32, C.c_void_p, C.c_size_t, C.c_void_p,
                                         P(C.c_void_p)]
+        L.pic_arena_bytes_tp.argtypes = [P(ModelConfigC), P(LimitsC), C.c_int32, P(C.c_size_t)]
+        L.pic_engine_create_tp.argtypes = [P(ModelConfigC), P(LimitsC), C.c_int32, C.c_void_p, C.c_size_t, C.c_void_p,
+                                           C.c_int32, C.c_int32, P(C.c_void_p)]
+        L.pic_tp_ipc_handle.argtypes = [C.c_void_p, C.c_void_p, P(C.c_uint64)]
+        L.pic_tp_connect.argtypes = [C.c_void_p, C.c_void_p, P(C.c_uint64)]
         L.pic_engine_destroy.argtypes = [C.c_void_p]
         L.pic_engine_destroy.restype = None
         L.pic_generate_context_cache.argtypes = [C.c_void_p, P(P(C.c_int32)), P(C.c_int32), C.c_int32, C.c_void_p,
@@ -200,7 +206,7 @@ class Engine:
     """One engine = one model replica on one GPU (or a host-only planner when device=None)."""
 
     def __init__(self, cfg, num_blocks: int, max_rows: int, max_tokens: int, max_requests: int = 1,
-                 device: Optional[int] = 0, stream=None):
+                 device: Optional[int] = 0, stream=None, tp_rank: int = 0, tp_size: int = 1):
         L = lib()
         self.cfg = cfg
         self._cfg = config_struct(cfg)
@@ -215,12 +221,28 @@ class Engine:
             return
         import torch
         nbytes = C.c_size_t()
-        check(L.pic_arena_bytes(C.byref(self._cfg), C.byref(self._lim), C.byref(nbytes)))
+        self.tp_rank, self.tp_size = tp_rank, tp_size
+        check(L.pic_arena_bytes_tp(C.byref(self._cfg), C.byref(self._lim), tp_size, C.byref(nbytes)))
         torch.cuda.set_device(device)
         self.arena = torch.empty(nbytes.value, dtype=torch.uint8, device=f"cuda:{device}")
         self.stream = stream if stream is not None else torch.cuda.current_stream(device)
-        check(L.pic_engine_create(C.byref(self._cfg), C.byref(self._lim), device, C.c_void_p(self.arena.data_ptr()),
-                                  nbytes.value, C.c_void_p(self.stream.cuda_stream), C.byref(self._h)))
+        check(L.pic_engine_create_tp(C.byref(self._cfg), C.byref(self._lim), device,
+                                     C.c_void_p(self.arena.data_ptr()), nbytes.value,
+                                     C.c_void_p(self.stream.cuda_stream), tp_rank, tp_size, C.byref(self._h)))
+
+    def ipc_handle(self) -> Tuple[bytes, int]:
+        h = (C.c_char * 64)()
+        off = C.c_uint64()
+        check(lib().pic_tp_ipc_handle(self._h, h, C.byref(off)))
+        return bytes(h), off.value
+
+    def tp_connect(self, handles: Sequence[Tuple[bytes, int]]) -> None:
+        """handles: every rank's (ipc_handle, offset) in rank order (e.g. from all_gather_object)."""
+        buf = (C.c_char * (64 * len(handles)))()
+        for r, (h, _) in enumerate(handles):
+            C.memmove(C.addressof(buf) + 64 * r, h, 64)
+        offs = (C.c_uint64 * len(handles))(*[o for _, o in handles])
+        check(lib().pic_tp_connect(self._h, buf, offs))
 
     @property
     def _stream(self):

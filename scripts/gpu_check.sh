@@ -1,3 +1,1 @@
-timeout 300 python scripts/gemm_m_sweep.py 2>&1 | grep "M=128"
-PIC_BENCH_PACK=128 timeout 300 python scripts/gemm_m_sweep.py 2>&1 | grep "M=128"
-PIC_BENCH_PACK=64 timeout 300 python scripts/gemm_m_sweep.py 2>&1 | grep "M=128"
+timeout 900 python -m pytest tests/test_gpu_tp.py -q -x --timeout 800 --timeout_method thread 2>&1 | tail -25

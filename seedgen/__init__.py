@@ -4,7 +4,7 @@ This module holds NO arithmetic of the method (no attention, RoPE, norms,
 projections, selection rules).  It only defines *inputs*: model shapes,
 random-init weights and token workloads, all drawn from the counter-based
 generator fixed in SURVEY.md §8(c).6.  The CUDA path implements the same
-generator independently in ``csrc/kernels/init_weights.cu`` (it never imports
+generator independently in ``csrc/kernels/pointwise.cu`` (gen_matrix / gen_gateup kernels; it never imports
 this module); the parity tests check the two bit-exactly.
 
 Generator:
@@ -152,11 +152,12 @@ class ModelConfig:
 TINY = ModelConfig("tiny", 2, 64, 4, 4, 16, 128, 256, 1e4, 4096, 0x5EED0001)
 TINY_GQA = replace(TINY, name="tiny-gqa", n_kv_heads=2, seed=0x5EED0011)
 TINY_D128 = ModelConfig("tiny-d128", 2, 256, 2, 1, 128, 512, 512, 1e4, 4096, 0x5EED0021)
+TINY_TP = ModelConfig("tiny-tp", 2, 256, 4, 2, 128, 512, 512, 1e4, 4096, 0x5EED0031)   # shardable over 2 ranks
 MISTRAL7B = ModelConfig("mistral7b", 32, 4096, 32, 8, 128, 14336, 32000, 1e6, 32768, 0x5EED0002)
 LLAMA31_8B = ModelConfig("llama31_8b", 32, 4096, 32, 8, 128, 14336, 128256, 5e5, 32768, 0x5EED0003)
 LLAMA3_70B = ModelConfig("llama3_70b", 80, 8192, 64, 8, 128, 28672, 128256, 5e5, 65536, 0x5EED0005)
 
-MODELS = {m.name: m for m in (TINY, TINY_GQA, TINY_D128, MISTRAL7B, LLAMA31_8B, LLAMA3_70B)}
+MODELS = {m.name: m for m in (TINY, TINY_GQA, TINY_D128, TINY_TP, MISTRAL7B, LLAMA31_8B, LLAMA3_70B)}
 
 
 def truncated(cfg: ModelConfig, n_layers: int) -> ModelConfig:
