@@ -168,15 +168,22 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-steps", type=int, default=3)
+    ap.add_argument("--tp", action="store_true",
+                    help="tensor parallel over all ranks (heads/MLP columns sharded, fused peer-memory all-reduce); "
+                         "strong scaling of one request instead of data parallel requests")
+    ap.add_argument("--layers", type=int, default=None, help="truncate depth (functional runs only; marked in config)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
     from paper_2410_15332_b200 import dist as D
     rank, world, local = D.env_rank()
-    w = workload(args.config, args.alg, world)
-    if len(w.requests) == 1:
-        w.requests = w.requests * world                # single-request configs: one copy per GPU
-    w.requests = D.shard(w.requests, rank, world)       # data parallel by independent request
+    w = workload(args.config, args.alg, 1 if args.tp else world)
+    if args.layers:
+        w.model = sg.truncated(w.model, args.layers)
+    if not args.tp:
+        if len(w.requests) == 1:
+            w.requests = w.requests * world            # single-request configs: one copy per GPU
+        w.requests = D.shard(w.requests, rank, world)   # data parallel by independent request
     cfgd = describe(w)
     N_tok = [sum(len(w.chunks[s.chunk]) if s.cached else len(s.tokens) for s in r) for r in w.requests]
 
@@ -204,11 +211,15 @@ def main():
     import torch
     from paper_2410_15332_b200 import pic as B
 
-    if world > 1:
-        torch.cuda.set_device(local)
-        D.init("nccl", device_id=torch.device(f"cuda:{local}"))
-    dev = local
+    dev = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(dev)
+    red_dev = f"cuda:{dev}"
+    if world > 1:
+        if args.tp:
+            D.init("gloo")        # TP data moves through peer memory; the group only exchanges handles/timings
+            red_dev = None
+        else:
+            D.init("nccl", device_id=torch.device(f"cuda:{dev}"))
     stream = torch.cuda.Stream(dev)
     m = w.model
     total_tokens = sum(len(c) for c in w.chunks)
@@ -222,9 +233,12 @@ def main():
         for r in w.requests)
     planner.close()
     with torch.cuda.stream(stream):
+        tp_kw = dict(tp_rank=rank, tp_size=world) if args.tp else {}
         eng = B.Engine(m, num_blocks=(total_tokens + sum(N_tok)) // 16 + 2 * len(w.chunks) + 64 * len(w.requests),
                        max_rows=max(4096, rows_link), max_tokens=max(max_N, 512) + 16,
-                       max_requests=len(w.requests), device=dev, stream=stream)
+                       max_requests=len(w.requests), device=dev, stream=stream, **tp_kw)
+        if args.tp and world > 1:
+            D.tp_connect(eng)
         ids = eng.generate_context_cache(w.chunks)
         reqs = [[("cached", ids[s.chunk]) if s.cached else ("tokens", s.tokens) for s in r] for r in w.requests]
         logits_dev = torch.empty((len(reqs), m.vocab), dtype=torch.float32, device=f"cuda:{dev}")
@@ -253,9 +267,9 @@ def main():
             ev1.synchronize()
         torch.cuda.synchronize(dev)
         barrier()
-        ms_max = D.max_over_ranks(ev0.elapsed_time(ev1), device=f"cuda:{dev}")
+        ms_max = D.max_over_ranks(ev0.elapsed_time(ev1), device=red_dev)
         ms_per_step = ms_max / args.steps
-        tokens_all = D.sum_over_ranks(sum(N_tok), device=f"cuda:{dev}") * args.steps
+        tokens_all = (sum(N_tok) if args.tp else D.sum_over_ranks(sum(N_tok), device=red_dev)) * args.steps
         value = tokens_all / (ms_max / 1e3)
 
         # ---------------- e2e: the public call with host buffers (plan H2D + logits D2H per step)
@@ -273,7 +287,7 @@ def main():
         e1.synchronize()
         wall = time.perf_counter() - t0
         st = eng.stats()
-        wall_max = D.max_over_ranks(wall, device=f"cuda:{dev}")
+        wall_max = D.max_over_ranks(wall, device=red_dev)
         e2e_value = tokens_all / wall_max
 
         # ---------------- per-kernel CUDA-event profile (separate pass, same stream)
@@ -314,8 +328,11 @@ def main():
     line = {"metric": "linked_prefill_tokens_per_s", "value": value, "unit": "tokens/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
             "ttft_ms_device": ms_per_step if len(reqs) == 1 else None,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
-            "data": "synthetic", "config": dict(cfgd, parallelism=f"dp{world} (independent requests)"),
+            "higher_is_better": True, "scaling": "strong" if args.tp else "weak", "vs_baseline": None,
+            "dtype": "bf16", "data": "synthetic",
+            "config": dict(cfgd, parallelism=(f"tp{world} (heads/MLP sharded, fused peer-memory all-reduce)" if args.tp
+                                              else f"dp{world} (independent requests)"),
+                           **({"truncated_layers": args.layers} if args.layers else {})),
             "clocks": clk.summary(), "gpu_launches": int(kernels_per_step * args.steps),
             "e2e": {"value": e2e_value, "unit": "tokens/s", "ttft_ms_host": wall_max / args.steps * 1e3,
                     "h2d_bytes_per_step": int(st["h2d_bytes_last_call"]),
