@@ -60,7 +60,11 @@ typedef struct {
   double rope_theta;   /* RoPE base θ (reading R2) */
   double rms_eps;      /* RMSNorm ε (reading R4) */
   uint64_t seed;       /* weight generator seed */
+  int32_t dtype;       /* PIC_DTYPE_BF16 (0, the product) or PIC_DTYPE_FP32_DEBUG (1): activations, Q/K/V, the KV
+                          pools and P/O kept in fp32 and projections on CUDA cores (weights stay bf16, which is exact:
+                          they are bf16-representable by construction) — the <= 1e-4 parity build (north star) */
 } pic_model_config;
+enum { PIC_DTYPE_BF16 = 0, PIC_DTYPE_FP32_DEBUG = 1 };
 
 /* Capacities of the engine's device arena. */
 typedef struct {
@@ -180,7 +184,8 @@ typedef struct {
 pic_status pic_plan(pic_engine* eng, const pic_segment* segs, int32_t n_segs, const pic_link_params* params,
                     pic_plan_out* out);
 
-/* Copy layer `layer` of a linked KV cache to host: k_host, v_host are [N][H_kv][D] bf16 (uint16). */
+/* Copy layer `layer` of a linked KV cache to host: k_host, v_host are [N][H_kv][D] bf16 (uint16), or fp32 for a
+ * PIC_DTYPE_FP32_DEBUG engine. */
 pic_status pic_linked_export(pic_engine* eng, const pic_linked* linked, int32_t layer, void* k_host, void* v_host);
 /* Number of tokens N and the block table (int32[ceil(N/16)], nullable) of a linked cache. */
 pic_status pic_linked_info(pic_engine* eng, const pic_linked* linked, int32_t* n_tokens, int32_t* block_table);

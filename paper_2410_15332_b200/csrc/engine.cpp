@@ -126,6 +126,7 @@ static pic_status validate_cfg(const pic_model_config* c, const pic_engine_limit
   if (c->d_model % 64 || c->ffn_dim % 64 || (c->n_heads * c->head_dim) % 64)
     return fail(PIC_E_CONFIG, "d_model, ffn_dim, n_heads*head_dim must be multiples of 64");
   if (c->vocab % 32) return fail(PIC_E_CONFIG, "vocab must be a multiple of 32");
+  if (c->dtype != 0 && c->dtype != 1) return fail(PIC_E_CONFIG, "dtype must be 0 (bf16) or 1 (fp32 debug)");
   if (c->bos_id < 0 || c->bos_id >= c->vocab) return fail(PIC_E_CONFIG, "bos_id out of range");
   if (!(c->rope_theta > 1.0) || !(c->rms_eps > 0.0)) return fail(PIC_E_CONFIG, "bad rope_theta / rms_eps");
   if (l->num_blocks <= 0 || l->max_rows <= 0 || l->max_tokens <= 0 || l->max_requests <= 0)
@@ -176,7 +177,8 @@ static ArenaPlan plan_arena(const pic_model_config& c, const pic_engine_limits& 
   a.off_gf = L.add(d * 4);
   a.off_cos = L.add((size_t)c.max_pos * (D / 2) * 4);
   a.off_sin = L.add((size_t)c.max_pos * (D / 2) * 4);
-  const size_t pool = (size_t)c.n_layers * l.num_blocks * Hkv * 16 * D * 2;
+  const size_t es = c.dtype == 1 ? 4 : 2;  // activation / KV element size (fp32 debug build: 4)
+  const size_t pool = (size_t)c.n_layers * l.num_blocks * Hkv * 16 * D * es;
   a.off_K = L.add(pool);
   a.off_V = L.add(pool);
   const size_t M = l.max_rows;
@@ -186,11 +188,11 @@ static ArenaPlan plan_arena(const pic_model_config& c, const pic_engine_limits& 
   wsf = std::max(wsf, (size_t)148 * 128 * 256 * 2);
   a.ws_floats = wsf;
   a.off_ws = L.add(wsf * 4);
-  a.off_x = L.add(M * std::max(d, Hq * D) * 2);
-  a.off_O = L.add(M * Hq * D * 2);
-  a.off_u = L.add(M * F * 2);
-  a.off_Q = L.add(M * Hq * D * 2);
-  a.off_xlast = L.add((size_t)l.max_requests * d * 2);
+  a.off_x = L.add(M * std::max(d, Hq * D) * es);
+  a.off_O = L.add(M * Hq * D * es);
+  a.off_u = L.add(M * F * es);
+  a.off_Q = L.add(M * Hq * D * es);
+  a.off_xlast = L.add((size_t)l.max_requests * d * es);
   a.attn_rows_cap = (int)std::max<size_t>(4 * M, 2048);
   a.off_opart = L.add((size_t)a.attn_rows_cap * Hq * 128 * 4);
   a.off_ml = L.add((size_t)a.attn_rows_cap * Hq * 2 * 4);
@@ -314,8 +316,9 @@ static pic_status init_device(pic_engine* e, void* arena, size_t bytes, cudaStre
   const int64_t gHqD = Hq * D * tp, gF = F * tp;
   // gate/up interleave group for the fused SwiGLU epilogue: the g dividing F whose F/g tiles best fill
   // one wave of 148 CTAs at skinny M (Mistral/Llama F = 14336: g = 112 -> 128 tiles of N = 224)
+  e->f32 = c.dtype == 1;
   e->gu_group = 0;
-  if (!getenv("PIC_NO_FUSED_SWIGLU")) {
+  if (!getenv("PIC_NO_FUSED_SWIGLU") && !e->f32) {
     double best = -1;
     for (int g : {112, 128, 64, 32, 16}) {
       if (F % g || !gemm_bn_supported(2 * g, true)) continue;
@@ -397,10 +400,10 @@ static pic_status init_device(pic_engine* e, void* arena, size_t bytes, cudaStre
   e->Kpool = b + a.off_K;
   e->Vpool = b + a.off_V;
   e->layer_stride = e->lim.num_blocks * Hkv * 16 * D;
-  const size_t pool = (size_t)c.n_layers * e->layer_stride * 2;
+  const size_t pool = (size_t)c.n_layers * e->layer_stride * (e->f32 ? 4 : 2);
   CK(cudaMemsetAsync(e->Kpool, 0, pool, st));
   CK(cudaMemsetAsync(e->Vpool, 0, pool, st));
-  if (D >= 64) {
+  if (D >= 64 && !e->f32) {
     uint64_t dims[4] = {(uint64_t)D, 16, (uint64_t)Hkv, (uint64_t)c.n_layers * e->lim.num_blocks};
     uint64_t strides[3] = {(uint64_t)D * 2, (uint64_t)16 * D * 2, (uint64_t)Hkv * 16 * D * 2};
     uint32_t box[4] = {64, 16, 1, 1};
@@ -433,7 +436,7 @@ static pic_status init_device(pic_engine* e, void* arena, size_t bytes, cudaStre
   TRY(make_tmap_2d(&e->tm_O, e->Obuf, M, Hq * D, 128));
   TRY(make_tmap_2d(&e->tm_u, e->u, M, F, 128));
   TRY(make_tmap_2d(&e->tm_xlast, e->x_last, e->lim.max_requests, d, 128));
-  if (D == 128) {
+  if (D == 128 && !e->f32) {
     const int G = (int)(Hq / Hkv);
     uint64_t dims[3] = {(uint64_t)D, (uint64_t)Hq, (uint64_t)M};
     uint64_t strides[2] = {(uint64_t)D * 2, (uint64_t)Hq * D * 2};
@@ -739,7 +742,15 @@ struct Runner {
   pic_engine* e;
   cudaStream_t st;
   int64_t launches = 0;
-  pic_status gemm(const CUtensorMap& A, const CUtensorMap* B3, int M, int N, int K, int* splits_out) {
+  pic_status gemm(const CUtensorMap& A, const CUtensorMap* B3, int M, int N, int K, int* splits_out,
+                  const void* A_ptr = nullptr, const void* B_ptr = nullptr) {
+    if (e->f32) {  // fp32 debug build: CUDA-core GEMM, exact bf16 weight products, fp32 activations
+      *splits_out = 1;
+      ++launches;
+      PROF("gemm", (double)N * K * 2 + (double)M * K * 4 + (double)M * N * 4, 2.0 * M * N * K,
+           launch_gemm_simt_f32(reinterpret_cast<const float*>(A_ptr), B_ptr, e->ws, M, N, K, st));
+      return PIC_OK;
+    }
     GemmChoice g = choose_gemm(e, M, N, K);
     *splits_out = g.splits;
     if (debug_sync()) fprintf(stderr, "[pic] gemm M=%d N=%d K=%d bn=%d splits=%d\n", M, N, K, g.bn, g.splits);
@@ -766,12 +777,12 @@ static pic_status enqueue_forward(pic_engine* e, const Fwd& f, const DevPlan& dp
   Runner R{e, st};
   char* Kp = reinterpret_cast<char*>(e->Kpool);
   char* Vp = reinterpret_cast<char*>(e->Vpool);
-  const size_t lbytes = (size_t)e->layer_stride * 2;
+  const size_t lbytes = (size_t)e->layer_stride * (e->f32 ? 4 : 2);
 
   if (!f.k2_src.empty() && f.k2_layer0 < L) {
     ++R.launches;
     PROF("kv_link", 8.0 * D * Hkv * (double)f.k2_src.size() * (L - f.k2_layer0), 0, launch_kv_link(e->Kpool, e->Vpool, dp.k2_src, dp.k2_dst, dp.k2_delta, (int)f.k2_src.size(), f.k2_layer0,
-                      L - f.k2_layer0, e->layer_stride, Hkv, D, e->cos_t, e->sin_t, f.rebase, st));
+                      L - f.k2_layer0, e->layer_stride, Hkv, D, e->cos_t, e->sin_t, f.rebase, st, e->f32));
   }
   ++R.launches;
   PROF("embed", 6.0 * f.M * d, 0, launch_embed(e->E, dp.tok, e->h, f.M, d, st));
@@ -789,7 +800,7 @@ static pic_status enqueue_forward(pic_engine* e, const Fwd& f, const DevPlan& dp
                       double extra_bytes) -> pic_status {
     if (e->tp_size == 1 || !Pp) {
       PROF("rmsnorm", (double)rows * d * (8 + 4 * (Pp ? sp : 0)) + extra_bytes, 0,
-           launch_residual_rmsnorm(hc, Pp, sp, gain, xout, map, rows, d, eps, st));
+           launch_residual_rmsnorm(hc, Pp, sp, gain, xout, map, rows, d, eps, st, e->f32));
       return PIC_OK;
     }
     float* mine = e->ar_buf[ar_parity];
@@ -799,7 +810,7 @@ static pic_status enqueue_forward(pic_engine* e, const Fwd& f, const DevPlan& dp
     srcs.n = e->tp_size;
     for (int r = 0; r < e->tp_size; ++r) srcs.p[r] = e->peer_ar[ar_parity][r];
     PROF("rmsnorm", (double)rows * d * (8 + 4 * e->tp_size) + extra_bytes, 0,
-         launch_residual_rmsnorm_srcs(hc, srcs, gain, xout, map, rows, d, eps, st));
+         launch_residual_rmsnorm_srcs(hc, srcs, gain, xout, map, rows, d, eps, st, e->f32));
     ar_parity ^= 1;
     return PIC_OK;
   };
@@ -817,13 +828,13 @@ static pic_status enqueue_forward(pic_engine* e, const Fwd& f, const DevPlan& dp
     ++R.launches;
     TRY(add_norm(prevP, prev_s, w.g1, e->x, nullptr, M, (double)M * d * 2));
     if (l > 0) TRY(capture(l - 1));
-    TRY(R.gemm(e->tm_x, w.tm_qkv, M, qkv, d, &s));
+    TRY(R.gemm(e->tm_x, w.tm_qkv, M, qkv, d, &s, e->x, w.qkv));
     if (f.cb && l == f.cb_layer) {
       // a9: CacheBlend selection at the check layer (P:170 steps 3-4)
       if (!f.cb_override) {
         R.launches += 3;
         PROF("cb_select", (double)M * qkv * 4 * s, 0, launch_cb_deviation(e->ws, s, dp.cb_cand, dp.slot, e->cos_t, e->sin_t, Kl, Vl, e->cb_dev, M, Hq, Hkv, D,
-                               st));
+                               st, e->f32));
         PROF("cb_select", 4.0 * M, 0, launch_cb_rank(e->cb_dev, dp.cb_keep, M, f.cb_T, st));
         PROF("cb_select", 16.0 * M, 0, launch_cb_compact(dp.cb_keep, dp.cb_forced, dp.bt, dp.cb_sel2, dp.cb_pos2, dp.cb_slot2, dp.cb_count, M,
                              st));
@@ -833,7 +844,7 @@ static pic_status enqueue_forward(pic_engine* e, const Fwd& f, const DevPlan& dp
       hc = e->h2;
       ++R.launches;
       PROF("qkv_rope_scatter", (double)f.M2 * qkv * 4 * s + (double)f.M2 * qkv * 2, 0, launch_qkv_rope_scatter(e->ws, s, M, dp.cb_sel2, dp.cb_pos2, dp.cb_slot2, e->cos_t, e->sin_t, e->Q, Kl, Vl,
-                                 f.M2, Hq, Hkv, D, st));
+                                 f.M2, Hq, Hkv, D, st, e->f32));
       M = f.M2;
       pos = dp.cb_pos2;
       slot = dp.cb_slot2;
@@ -843,7 +854,7 @@ static pic_status enqueue_forward(pic_engine* e, const Fwd& f, const DevPlan& dp
     } else {
       ++R.launches;
       PROF("qkv_rope_scatter", (double)M * qkv * 4 * s + (double)M * qkv * 2, 0, launch_qkv_rope_scatter(e->ws, s, M, nullptr, pos, slot, e->cos_t, e->sin_t, e->Q, Kl, Vl, M, Hq, Hkv, D,
-                                 st));
+                                 st, e->f32));
     }
     if (f.compile && l == L - 1) break;  // compile needs only the last layer's K/V
     // a6 attention — algorithmic work: 4·H_q·D·Σ(p_i+1) FLOPs, K/V of keys 0..max p read once
@@ -864,7 +875,7 @@ static pic_status enqueue_forward(pic_engine* e, const Fwd& f, const DevPlan& dp
       }
       attn_bytes += (double)M * Hq * D * 2 * 2;
     }
-    if (D == 128) {
+    if (D == 128 && !e->f32) {
       AttnArgs a{};
       a.work = (tiles == dp.tiles) ? dp.attn_work : dp.attn_work2;
       a.n_work = (tiles == dp.tiles) ? f.attn_n_work : f.attn_n_work2;
@@ -888,13 +899,12 @@ static pic_status enqueue_forward(pic_engine* e, const Fwd& f, const DevPlan& dp
            launch_attn_combine(e->o_part, e->ml_part, (tiles == dp.tiles) ? dp.attn_nsplit : dp.attn_nsplit2, e->Obuf,
                                M, Hq, D, st));
     } else {
-      if (f.cb && l >= f.cb_layer) return fail(PIC_E_VARIANT, "CacheBlend needs head_dim 128 on the GPU path");
       ++R.launches;
       PROF("attention", attn_bytes, attn_flops, launch_attention_simt(e->Q, Kl, Vl, dp.seq, dp.seq_bt_off, dp.bt, pos, e->Obuf, M, Hq, Hkv, D,
-                               (float)(1.0 / std::sqrt((double)D)), st));
+                               (float)(1.0 / std::sqrt((double)D)), st, e->f32));
     }
     // a7 O projection, residual + a8 MLP
-    TRY(R.gemm(e->tm_O, w.tm_o, M, d, Hq * D, &s));
+    TRY(R.gemm(e->tm_O, w.tm_o, M, d, Hq * D, &s, e->Obuf, w.o));
     ++R.launches;
     TRY(add_norm(e->ws, s, w.g2, e->x, nullptr, M, (double)M * d * 2));
     if (e->gu_group > 0) {
@@ -902,11 +912,11 @@ static pic_status enqueue_forward(pic_engine* e, const Fwd& f, const DevPlan& dp
       PROF("gemm", (double)2 * F * d * 2 + (double)M * d * 2 + (double)M * F * 2, 2.0 * M * 2 * F * d,
            launch_gemm_swiglu(e->tm_x, w.tm_gu_fused, e->u, M, 2 * F, d, 2 * e->gu_group, st));
     } else {
-      TRY(R.gemm(e->tm_x, w.tm_gu, M, 2 * F, d, &s));
+      TRY(R.gemm(e->tm_x, w.tm_gu, M, 2 * F, d, &s, e->x, w.gu));
       ++R.launches;
-      PROF("swiglu", (double)M * 2 * F * 4 * s + (double)M * F * 2, 0, launch_swiglu(e->ws, s, e->u, M, F, st));
+      PROF("swiglu", (double)M * 2 * F * 4 * s + (double)M * F * 2, 0, launch_swiglu(e->ws, s, e->u, M, F, st, e->f32));
     }
-    TRY(R.gemm(e->tm_u, w.tm_down, M, d, F, &s));
+    TRY(R.gemm(e->tm_u, w.tm_down, M, d, F, &s, e->u, w.down));
     prevP = e->ws;
     prev_s = s;
   }
@@ -916,7 +926,7 @@ static pic_status enqueue_forward(pic_engine* e, const Fwd& f, const DevPlan& dp
     TRY(add_norm(prevP, prev_s, e->gf, e->x_last, head_map, M, (double)f.n_head * d * 2));
     TRY(capture(L - 1));
     int s = 0;
-    TRY(R.gemm(e->tm_xlast, e->tm_lm, f.n_head, c.vocab, d, &s));
+    TRY(R.gemm(e->tm_xlast, e->tm_lm, f.n_head, c.vocab, d, &s, e->x_last, e->Wlm));
     ++R.launches;
     PROF("logits_argmax", (double)f.n_head * c.vocab * 4 * (s + 1), 0, launch_logits_argmax(e->ws, s, e->logits, e->amax, f.n_head, c.vocab, st));
   }
@@ -1388,7 +1398,8 @@ static pic_status export_rows(pic_engine* e, const std::vector<int32_t>& blocks,
   if (e->host_only) return fail(PIC_E_NO_DEVICE, "host-only engine");
   if (layer < 0 || layer >= e->cfg.n_layers) return fail(PIC_E_INVALID_ARG, "layer out of range");
   const int Hkv = e->cfg.n_kv_heads, D = e->cfg.head_dim;
-  const size_t row = (size_t)D * 2;
+  const size_t es = e->f32 ? 4 : 2;
+  const size_t row = (size_t)D * es;
   std::vector<uint16_t> kb((size_t)n * Hkv * D), vb((size_t)n * Hkv * D);
   CK(cudaDeviceSynchronize());
   for (int i = 0; i < n; ++i)
@@ -1396,10 +1407,10 @@ static pic_status export_rows(pic_engine* e, const std::vector<int32_t>& blocks,
       const size_t src = (size_t)layer * e->layer_stride + (((size_t)blocks[i / 16] * Hkv + g) * 16 + i % 16) * D;
       if (k_host)
         CK(cudaMemcpy(reinterpret_cast<char*>(k_host) + ((size_t)i * Hkv + g) * row,
-                      reinterpret_cast<char*>(e->Kpool) + src * 2, row, cudaMemcpyDeviceToHost));
+                      reinterpret_cast<char*>(e->Kpool) + src * es, row, cudaMemcpyDeviceToHost));
       if (v_host)
         CK(cudaMemcpy(reinterpret_cast<char*>(v_host) + ((size_t)i * Hkv + g) * row,
-                      reinterpret_cast<char*>(e->Vpool) + src * 2, row, cudaMemcpyDeviceToHost));
+                      reinterpret_cast<char*>(e->Vpool) + src * es, row, cudaMemcpyDeviceToHost));
     }
   return PIC_OK;
 }

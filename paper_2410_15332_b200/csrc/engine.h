@@ -104,6 +104,7 @@ struct pic_engine {
   pic_model_config cfg{};   // this rank's (local) model: heads / ffn_dim divided by tp_size
   pic_model_config gcfg{};  // global model
   int tp_rank = 0, tp_size = 1;
+  bool f32 = false;         // fp32 debug build (dtype 1): fp32 activations / KV, CUDA-core GEMM + attention
   bool tp_connected = false;
   float* ar_buf[2] = {nullptr, nullptr};       // reduced partials exchanged across ranks (alternating)
   long long *tp_flags = nullptr, *tp_counter = nullptr;

@@ -417,14 +417,22 @@ cudaError_t launch_attn_combine(const float* o_part, const float* ml_part, const
 }
 
 // ------------------------------------------------------------------------------------------------
-// Generic-D SIMT attention for the tiny configs (D = 16/32/64, no TMA box fits): one warp per
-// (row, head); lanes stride over keys; two passes (max, then exp/sum/PV) in fp32.
-template <int D>
-__global__ void attn_simt_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* __restrict__ Kp,
-                                 const __nv_bfloat16* __restrict__ Vp, const int32_t* __restrict__ row_seq,
-                                 const int32_t* __restrict__ seq_bt_off, const int32_t* __restrict__ bt,
-                                 const int32_t* __restrict__ row_pos, __nv_bfloat16* __restrict__ O, int M, int Hq,
-                                 int Hkv, float scale) {
+// Generic-D SIMT attention for the tiny configs (D = 16/32/64, no TMA box fits) and for the fp32
+// debug build (any D <= 128, fp32 Q/K/V/O): one warp per (row, head); lanes stride over keys; two
+// passes (max, then exp/sum/PV) in fp32.
+template <bool F32>
+PIC_DEV float ldx(const void* p, size_t i) {
+  if constexpr (F32)
+    return reinterpret_cast<const float*>(p)[i];
+  else
+    return __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(p)[i]);
+}
+
+template <int D, bool F32>
+__global__ void attn_simt_kernel(const void* __restrict__ Q, const void* __restrict__ Kp, const void* __restrict__ Vp,
+                                 const int32_t* __restrict__ row_seq, const int32_t* __restrict__ seq_bt_off,
+                                 const int32_t* __restrict__ bt, const int32_t* __restrict__ row_pos,
+                                 void* __restrict__ O, int M, int Hq, int Hkv, float scale) {
   PIC_PDL_ENTRY();
   const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
@@ -435,17 +443,17 @@ __global__ void attn_simt_kernel(const __nv_bfloat16* __restrict__ Q, const __nv
   const int* tb = bt + seq_bt_off[row_seq[row]];
   float q[D];
 #pragma unroll
-  for (int i = 0; i < D; ++i) q[i] = __bfloat162float(Q[((size_t)row * Hq + head) * D + i]);
+  for (int i = 0; i < D; ++i) q[i] = ldx<F32>(Q, ((size_t)row * Hq + head) * D + i);
   auto kv_off = [&](int key) -> size_t {
     const int blk = tb[key / 16];
     return (((size_t)blk * Hkv + g) * 16 + (key % 16)) * D;
   };
   float mx = -INFINITY;
   for (int key = lane; key <= pos; key += 32) {
-    const __nv_bfloat16* kr = Kp + kv_off(key);
+    const size_t off = kv_off(key);
     float s = 0.f;
 #pragma unroll
-    for (int i = 0; i < D; ++i) s += q[i] * __bfloat162float(kr[i]);
+    for (int i = 0; i < D; ++i) s += q[i] * ldx<F32>(Kp, off + i);
     mx = fmaxf(mx, s * scale);
   }
   mx = warp_max(mx);
@@ -456,36 +464,52 @@ __global__ void attn_simt_kernel(const __nv_bfloat16* __restrict__ Q, const __nv
     const size_t off = kv_off(key);
     float s = 0.f;
 #pragma unroll
-    for (int i = 0; i < D; ++i) s += q[i] * __bfloat162float(Kp[off + i]);
-    const float p = __expf(s * scale - mx);
+    for (int i = 0; i < D; ++i) s += q[i] * ldx<F32>(Kp, off + i);
+    const float p = expf(s * scale - mx);
     l += p;
 #pragma unroll
-    for (int i = 0; i < D; ++i) o[i] += p * __bfloat162float(Vp[off + i]);
+    for (int i = 0; i < D; ++i) o[i] += p * ldx<F32>(Vp, off + i);
   }
   l = warp_sum(l);
 #pragma unroll
   for (int i = 0; i < D; ++i) o[i] = warp_sum(o[i]);
   if (lane == 0) {
 #pragma unroll
-    for (int i = 0; i < D; ++i) O[((size_t)row * Hq + head) * D + i] = __float2bfloat16(o[i] / l);
+    for (int i = 0; i < D; ++i) {
+      const size_t oi = ((size_t)row * Hq + head) * D + i;
+      if constexpr (F32)
+        reinterpret_cast<float*>(O)[oi] = o[i] / l;
+      else
+        reinterpret_cast<__nv_bfloat16*>(O)[oi] = __float2bfloat16(o[i] / l);
+    }
   }
 }
 
 cudaError_t launch_attention_simt(const void* Q, const void* Kpool_l, const void* Vpool_l, const int32_t* row_seq,
                                   const int32_t* seq_bt_off, const int32_t* bt, const int32_t* row_pos, void* O,
-                                  int M, int Hq, int Hkv, int D, float scale, cudaStream_t st) {
+                                  int M, int Hq, int Hkv, int D, float scale, cudaStream_t st, int f32) {
   const int warps = M * Hq;
   dim3 grid((warps + 3) / 4), block(128);
-  auto q = reinterpret_cast<const __nv_bfloat16*>(Q);
-  auto k = reinterpret_cast<const __nv_bfloat16*>(Kpool_l);
-  auto v = reinterpret_cast<const __nv_bfloat16*>(Vpool_l);
-  auto o = reinterpret_cast<__nv_bfloat16*>(O);
-  switch (D) {
-    case 16: CUDA_TRY_LAUNCH(launch_k(attn_simt_kernel<16>, dim3(grid), dim3(block), 0, st, q, k, v, row_seq, seq_bt_off, bt, row_pos, o, M, Hq, Hkv, scale)); break;
-    case 32: CUDA_TRY_LAUNCH(launch_k(attn_simt_kernel<32>, dim3(grid), dim3(block), 0, st, q, k, v, row_seq, seq_bt_off, bt, row_pos, o, M, Hq, Hkv, scale)); break;
-    case 64: CUDA_TRY_LAUNCH(launch_k(attn_simt_kernel<64>, dim3(grid), dim3(block), 0, st, q, k, v, row_seq, seq_bt_off, bt, row_pos, o, M, Hq, Hkv, scale)); break;
-    default: return cudaErrorInvalidValue;
+#define SIMT_L(DD, FF)                                                                                              \
+  CUDA_TRY_LAUNCH(launch_k(attn_simt_kernel<DD, FF>, dim3(grid), dim3(block), 0, st, Q, Kpool_l, Vpool_l, row_seq,  \
+                           seq_bt_off, bt, row_pos, O, M, Hq, Hkv, scale))
+  if (f32) {
+    switch (D) {
+      case 16: SIMT_L(16, true); break;
+      case 32: SIMT_L(32, true); break;
+      case 64: SIMT_L(64, true); break;
+      case 128: SIMT_L(128, true); break;
+      default: return cudaErrorInvalidValue;
+    }
+  } else {
+    switch (D) {
+      case 16: SIMT_L(16, false); break;
+      case 32: SIMT_L(32, false); break;
+      case 64: SIMT_L(64, false); break;
+      default: return cudaErrorInvalidValue;
+    }
   }
+#undef SIMT_L
   return cudaGetLastError();
 }
 

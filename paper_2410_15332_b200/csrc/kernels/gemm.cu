@@ -308,4 +308,46 @@ cudaError_t launch_gemm_swiglu(const CUtensorMap& A, const CUtensorMap& B, void*
   return cudaErrorInvalidValue;
 }
 
+// ------------------------------------------------------------------------------------------------
+// fp32 debug build GEMM on CUDA cores: out[M][N] = A[M][K] (fp32) · B[N][K]^T (bf16 weights, exact in
+// fp32), accumulated in fp32 in ascending k.  64 x 64 output tile per CTA, 4 x 4 per thread.
+__global__ void __launch_bounds__(256) gemm_simt_f32_kernel(const float* __restrict__ A, const uint16_t* __restrict__ B,
+                                                            float* __restrict__ out, int M, int N, int K) {
+  griddep_launch();
+  griddep_wait();
+  __shared__ float As[16][65], Bs[16][65];
+  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+  const int m0 = blockIdx.y * 64, n0 = blockIdx.x * 64;
+  float acc[4][4] = {};
+  for (int k0 = 0; k0 < K; k0 += 16) {
+    for (int i = threadIdx.x; i < 64 * 16; i += 256) {
+      const int r = i / 16, k = i % 16;
+      As[k][r] = (m0 + r < M && k0 + k < K) ? A[(size_t)(m0 + r) * K + k0 + k] : 0.f;
+      Bs[k][r] = (n0 + r < N && k0 + k < K) ? __uint_as_float((uint32_t)B[(size_t)(n0 + r) * K + k0 + k] << 16) : 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 16; ++k)
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(As[k][ty * 4 + i], Bs[k][tx * 4 + j], acc[i][j]);
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int m = m0 + ty * 4 + i, n = n0 + tx * 4 + j;
+      if (m < M && n < N) out[(size_t)m * N + n] = acc[i][j];
+    }
+}
+
+cudaError_t launch_gemm_simt_f32(const float* A, const void* B, float* out, int M, int N, int K, cudaStream_t st) {
+  dim3 grid((N + 63) / 64, (M + 63) / 64);
+  CUDA_TRY_LAUNCH(launch_k(gemm_simt_f32_kernel, dim3(grid), dim3(256), 0, st, A, reinterpret_cast<const uint16_t*>(B),
+                           out, M, N, K));
+  return cudaGetLastError();
+}
+
 }  // namespace pic

@@ -51,27 +51,29 @@ struct Peers {  // per-rank device pointers (peer memory through CUDA IPC / NVLi
   void* p[8];
 };
 cudaError_t launch_residual_rmsnorm_srcs(float* h, const Srcs& srcs, const float* g, void* x, const int32_t* out_map,
-                                         int M, int d, float eps, cudaStream_t st);
+                                         int M, int d, float eps, cudaStream_t st, int f32 = 0);
 // tensor parallel: reduce this rank's split-K partials; cross-rank epoch barrier over peer memory
 cudaError_t launch_tp_reduce_local(const float* P, int splits, int M, int d, float* out, cudaStream_t st);
 cudaError_t launch_tp_barrier(long long* counter, const Peers& flags, int rank, int tp, cudaStream_t st);
 // h[r] += Σ_s P[s][r] (P nullable); if x: x[out_map ? out_map[r] : r] = bf16(rms(h[r]) ⊙ g) for out_map[r] >= 0
+// f32 != 0: fp32 debug build (activations / KV stored fp32 instead of bf16)
 cudaError_t launch_residual_rmsnorm(float* h, const float* P, int splits, const float* g, void* x,
-                                    const int32_t* out_map, int M, int d, float eps, cudaStream_t st);
+                                    const int32_t* out_map, int M, int d, float eps, cudaStream_t st, int f32 = 0);
 
 // ---- a5 epilogue: Σ partials, RoPE at row positions, Q dense, K/V scattered to the paged pool
 cudaError_t launch_qkv_rope_scatter(const float* P, int splits, int P_rows, const int32_t* src_row,
                                     const int32_t* pos, const int32_t* slot, const float* cos_t, const float* sin_t,
                                     void* Q, void* Kpool_l, void* Vpool_l, int M, int Hq, int Hkv, int D,
-                                    cudaStream_t st);
+                                    cudaStream_t st, int f32 = 0);
 
 // ---- a8 epilogue: u = bf16(silu(Σ gate) ⊙ Σ up) ----------------------------------------------
-cudaError_t launch_swiglu(const float* P, int splits, void* u, int M, int F, cudaStream_t st);
+cudaError_t launch_swiglu(const float* P, int splits, void* u, int M, int F, cudaStream_t st, int f32 = 0);
 
 // ---- a2: KV link — gather cached rows into the linked blocks, RoPE re-base K by Δ -----------
 cudaError_t launch_kv_link(void* Kpool, void* Vpool, const int32_t* src_slot, const int32_t* dst_slot,
                            const int32_t* delta, int n_rows, int layer0, int n_layers, int64_t layer_stride_elems,
-                           int Hkv, int D, const float* cos_t, const float* sin_t, int rebase, cudaStream_t st);
+                           int Hkv, int D, const float* cos_t, const float* sin_t, int rebase, cudaStream_t st,
+                           int f32 = 0);
 
 // ---- GEMM (tcgen05): P[split][M][N] = A[M][K] · B[N][K]^T --------------------------------------
 // pack > 0: B is stored pre-tiled [N/pack][K/64][pack][64] (every TMA box contiguous); the tensor map
@@ -110,10 +112,12 @@ cudaError_t launch_attention_tc(const CUtensorMap& tmQ, const CUtensorMap& tmK, 
                                 const CUtensorMap& tmK8, const CUtensorMap& tmV8, const AttnArgs& a, cudaStream_t st);
 cudaError_t launch_attn_combine(const float* o_part, const float* ml_part, const int32_t* row_nsplit, void* O, int M,
                                 int Hq, int D, cudaStream_t st);
-// generic-D SIMT attention (tiny shapes, D in {16,32,64}); writes O bf16 directly
+// generic-D SIMT attention (tiny shapes D in {16,32,64}; any D <= 128 in the fp32 debug build); writes O directly
 cudaError_t launch_attention_simt(const void* Q, const void* Kpool_l, const void* Vpool_l, const int32_t* row_seq,
                                   const int32_t* seq_bt_off, const int32_t* bt, const int32_t* row_pos, void* O,
-                                  int M, int Hq, int Hkv, int D, float scale, cudaStream_t st);
+                                  int M, int Hq, int Hkv, int D, float scale, cudaStream_t st, int f32 = 0);
+// fp32 debug build GEMM (CUDA cores, exact products): P[M][N] = A[M][K] (fp32) · B[N][K]^T (bf16 weights)
+cudaError_t launch_gemm_simt_f32(const float* A, const void* B, float* out, int M, int N, int K, cudaStream_t st);
 
 // ---- a10: Σ LM-head partials, fp32 logits, argmax (ties -> lowest id) -----------------------
 cudaError_t launch_logits_argmax(const float* P, int splits, float* logits, int32_t* argmax, int n_req, int V,
@@ -123,7 +127,7 @@ cudaError_t launch_logits_argmax(const float* P, int splits, float* logits, int3
 // dev[i] = ||RoPE(Σk)_i − K_lnk[i]||² + ||Σv_i − V_lnk[i]||² for candidate rows (cand[i] != 0), else −1
 cudaError_t launch_cb_deviation(const float* P, int splits, const int32_t* cand, const int32_t* slot,
                                 const float* cos_t, const float* sin_t, const void* Kpool_l, const void* Vpool_l,
-                                float* dev, int N, int Hq, int Hkv, int D, cudaStream_t st);
+                                float* dev, int N, int Hq, int Hkv, int D, cudaStream_t st, int f32 = 0);
 // keep[i] = cand[i] && rank_i < T, rank by (dev desc, index asc)
 cudaError_t launch_cb_rank(const float* dev, int32_t* keep, int N, int T, cudaStream_t st);
 // sel = sorted {i : keep[i] || forced[i]}; pos = sel; slot = bt[sel/16]*16 + sel%16; writes count

@@ -149,6 +149,23 @@ cudaError_t launch_embed(const void* E, const int32_t* tok, float* h, int M, int
   return cudaGetLastError();
 }
 
+// Element storage of activations / KV: bf16 (product) or fp32 (the fp32 debug build, dtype = 1).
+PIC_DEV uint2 pack4(float a, float b, float c, float d) { return make_uint2(pack_bf16(a, b), pack_bf16(c, d)); }
+template <bool F32>
+PIC_DEV void store4(void* base, size_t idx, float a, float b, float c, float d) {
+  if constexpr (F32)
+    *reinterpret_cast<float4*>(reinterpret_cast<float*>(base) + idx) = make_float4(a, b, c, d);
+  else
+    *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(base) + idx) = pack4(a, b, c, d);
+}
+template <bool F32>
+PIC_DEV float load1(const void* base, size_t idx) {
+  if constexpr (F32)
+    return reinterpret_cast<const float*>(base)[idx];
+  else
+    return __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(base)[idx]);
+}
+
 // ================================================================================ a4 RMSNorm
 template <int NT>
 PIC_DEV float block_sum(float v, float* red) {
@@ -191,9 +208,10 @@ PIC_DEV float4 sum_splits4(const float4* __restrict__ P4, int splits, size_t str
 // The sources are the split-K partials of the producing GEMM, or — under tensor parallelism — every
 // rank's reduced partial read directly from peer memory in rank order (the all-reduce fused into the
 // consumer; deterministic and identical on all ranks).  One CTA per row, one float4 per thread.
+template <bool F32>
 __global__ void __launch_bounds__(1024) residual_rmsnorm_kernel(float* __restrict__ h, Srcs srcs,
                                                                  const float* __restrict__ g,
-                                                                 uint16_t* __restrict__ x,
+                                                                 void* __restrict__ x,
                                                                  const int32_t* __restrict__ out_map, int M, int d,
                                                                  float eps) {
   PIC_PDL_ENTRY();
@@ -219,30 +237,31 @@ __global__ void __launch_bounds__(1024) residual_rmsnorm_kernel(float* __restric
   ss = block_sum_dyn(ss, red);
   if (orow < 0) return;
   const float inv = rsqrtf(ss / d + eps);
-  uint2* xr = reinterpret_cast<uint2*>(x + (size_t)orow * d);
   const float4* g4 = reinterpret_cast<const float4*>(g);
   for (int i = threadIdx.x; i < n4; i += blockDim.x) {
     const float4 v = hr[i], w = g4[i];
-    xr[i] = make_uint2(pack_bf16(v.x * inv * w.x, v.y * inv * w.y), pack_bf16(v.z * inv * w.z, v.w * inv * w.w));
+    store4<F32>(x, (size_t)orow * d + 4 * i, v.x * inv * w.x, v.y * inv * w.y, v.z * inv * w.z, v.w * inv * w.w);
   }
 }
 
 cudaError_t launch_residual_rmsnorm_srcs(float* h, const Srcs& srcs, const float* g, void* x, const int32_t* out_map,
-                                         int M, int d, float eps, cudaStream_t st) {
+                                         int M, int d, float eps, cudaStream_t st, int f32) {
   if (M == 0) return cudaSuccess;
   const int nt = std::max(32, std::min(1024, d / 4));
-  CUDA_TRY_LAUNCH(launch_k(residual_rmsnorm_kernel, dim3(M), dim3(nt), 0, st, h, srcs, g, reinterpret_cast<uint16_t*>(x),
-                           out_map, M, d, eps));
+  if (f32)
+    CUDA_TRY_LAUNCH(launch_k(residual_rmsnorm_kernel<true>, dim3(M), dim3(nt), 0, st, h, srcs, g, x, out_map, M, d, eps));
+  else
+    CUDA_TRY_LAUNCH(launch_k(residual_rmsnorm_kernel<false>, dim3(M), dim3(nt), 0, st, h, srcs, g, x, out_map, M, d, eps));
   return cudaGetLastError();
 }
 
 cudaError_t launch_residual_rmsnorm(float* h, const float* P, int splits, const float* g, void* x,
-                                    const int32_t* out_map, int M, int d, float eps, cudaStream_t st) {
+                                    const int32_t* out_map, int M, int d, float eps, cudaStream_t st, int f32) {
   Srcs s{};
   s.n = P ? splits : 0;
   if (s.n > kMaxSrcs) return cudaErrorInvalidValue;
   for (int k = 0; k < s.n; ++k) s.p[k] = P + (size_t)k * M * d;
-  return launch_residual_rmsnorm_srcs(h, s, g, x, out_map, M, d, eps, st);
+  return launch_residual_rmsnorm_srcs(h, s, g, x, out_map, M, d, eps, st, f32);
 }
 
 // ================================================================================ tensor parallel
@@ -299,16 +318,16 @@ PIC_DEV float sum_partials(const float* P, int splits, size_t split_stride, size
   return a;
 }
 
-PIC_DEV uint2 pack4(float a, float b, float c, float d) { return make_uint2(pack_bf16(a, b), pack_bf16(c, d)); }
 
 // Q = RoPE(Σ q, p), K = RoPE(Σ k, p) -> pool slot, V = Σ v -> pool slot  (P:213 steps 2-3; written
 // BEFORE attention so the selected rows also see each other).  Grid (rows, column groups); a RoPE
 // thread owns 4 NeoX pairs (j..j+3, j+D/2..j+D/2+3) of one q/k head, a V thread 4 values.
+template <bool F32>
 __global__ void __launch_bounds__(128) qkv_rope_scatter_kernel(
     const float* __restrict__ P, int splits, int P_rows, const int32_t* __restrict__ src_row,
     const int32_t* __restrict__ pos, const int32_t* __restrict__ slot, const float* __restrict__ cos_t,
-    const float* __restrict__ sin_t, __nv_bfloat16* __restrict__ Q, __nv_bfloat16* __restrict__ Kp,
-    __nv_bfloat16* __restrict__ Vp, int Hq, int Hkv, int D) {
+    const float* __restrict__ sin_t, void* __restrict__ Q, void* __restrict__ Kp, void* __restrict__ Vp, int Hq,
+    int Hkv, int D) {
   PIC_PDL_ENTRY();
   const int r = blockIdx.x;
   const int t = blockIdx.y * blockDim.x + threadIdx.x;
@@ -329,40 +348,39 @@ __global__ void __launch_bounds__(128) qkv_rope_scatter_kernel(
     const int p = pos[r];
     const float4 c = *reinterpret_cast<const float4*>(cos_t + (size_t)p * half + j);
     const float4 s = *reinterpret_cast<const float4*>(sin_t + (size_t)p * half + j);
-    const uint2 o1 = pack4(a.x * c.x - b.x * s.x, a.y * c.y - b.y * s.y, a.z * c.z - b.z * s.z, a.w * c.w - b.w * s.w);
-    const uint2 o2 = pack4(b.x * c.x + a.x * s.x, b.y * c.y + a.y * s.y, b.z * c.z + a.z * s.z, b.w * c.w + a.w * s.w);
-    __nv_bfloat16* dst;
-    if (hd < Hq) {
-      dst = Q + ((size_t)r * Hq + hd) * D;
-    } else {
-      dst = Kp + kv_base + (size_t)(hd - Hq) * 16 * D;
-    }
-    *reinterpret_cast<uint2*>(dst + j) = o1;
-    *reinterpret_cast<uint2*>(dst + j + half) = o2;
+    void* dst = hd < Hq ? Q : Kp;
+    const size_t o = hd < Hq ? ((size_t)r * Hq + hd) * D : kv_base + (size_t)(hd - Hq) * 16 * D;
+    store4<F32>(dst, o + j, a.x * c.x - b.x * s.x, a.y * c.y - b.y * s.y, a.z * c.z - b.z * s.z, a.w * c.w - b.w * s.w);
+    store4<F32>(dst, o + j + half, b.x * c.x + a.x * s.x, b.y * c.y + a.y * s.y, b.z * c.z + a.z * s.z,
+                b.w * c.w + a.w * s.w);
   } else {
     const int u = t - n_rope;
     const int hd = u / (D / 4), j = (u % (D / 4)) * 4;
     const float4 v = sum_splits4(P4, splits, stride4, ((Hq + Hkv) * D + hd * D + j) / 4);
-    *reinterpret_cast<uint2*>(Vp + kv_base + (size_t)hd * 16 * D + j) = pack4(v.x, v.y, v.z, v.w);
+    store4<F32>(Vp, kv_base + (size_t)hd * 16 * D + j, v.x, v.y, v.z, v.w);
   }
 }
 
 cudaError_t launch_qkv_rope_scatter(const float* P, int splits, int P_rows, const int32_t* src_row, const int32_t* pos,
                                     const int32_t* slot, const float* cos_t, const float* sin_t, void* Q,
-                                    void* Kpool_l, void* Vpool_l, int M, int Hq, int Hkv, int D, cudaStream_t st) {
+                                    void* Kpool_l, void* Vpool_l, int M, int Hq, int Hkv, int D, cudaStream_t st,
+                                    int f32) {
   if (M == 0) return cudaSuccess;
   const int threads = (Hq + Hkv) * (D / 8) + Hkv * (D / 4);
   dim3 grid(M, (threads + 127) / 128);
-  CUDA_TRY_LAUNCH(launch_k(qkv_rope_scatter_kernel, dim3(grid), dim3(128), 0, st, P, splits, P_rows, src_row, pos, slot, cos_t, sin_t,
-                                                reinterpret_cast<__nv_bfloat16*>(Q),
-                                                reinterpret_cast<__nv_bfloat16*>(Kpool_l),
-                                                reinterpret_cast<__nv_bfloat16*>(Vpool_l), Hq, Hkv, D));
+  if (f32)
+    CUDA_TRY_LAUNCH(launch_k(qkv_rope_scatter_kernel<true>, dim3(grid), dim3(128), 0, st, P, splits, P_rows, src_row,
+                             pos, slot, cos_t, sin_t, Q, Kpool_l, Vpool_l, Hq, Hkv, D));
+  else
+    CUDA_TRY_LAUNCH(launch_k(qkv_rope_scatter_kernel<false>, dim3(grid), dim3(128), 0, st, P, splits, P_rows, src_row,
+                             pos, slot, cos_t, sin_t, Q, Kpool_l, Vpool_l, Hq, Hkv, D));
   return cudaGetLastError();
 }
 
 // ================================================================================ a8 SwiGLU
 // u = bf16(silu(Σ gate) ⊙ Σ up), 4 columns per thread
-__global__ void swiglu_kernel(const float* __restrict__ P, int splits, uint2* __restrict__ u, int M, int F) {
+template <bool F32>
+__global__ void swiglu_kernel(const float* __restrict__ P, int splits, void* __restrict__ u, int M, int F) {
   PIC_PDL_ENTRY();
   const size_t n4 = (size_t)M * F / 4;
   const size_t F4 = F / 4;
@@ -372,16 +390,19 @@ __global__ void swiglu_kernel(const float* __restrict__ P, int splits, uint2* __
     const size_t r = i / F4, f = i % F4;
     const float4 g = sum_splits4(P4, splits, stride4, r * 2 * F4 + f);
     const float4 up = sum_splits4(P4, splits, stride4, r * 2 * F4 + F4 + f);
-    u[i] = pack4(g.x / (1.f + __expf(-g.x)) * up.x, g.y / (1.f + __expf(-g.y)) * up.y,
-                 g.z / (1.f + __expf(-g.z)) * up.z, g.w / (1.f + __expf(-g.w)) * up.w);
+    store4<F32>(u, 4 * i, g.x / (1.f + expf(-g.x)) * up.x, g.y / (1.f + expf(-g.y)) * up.y,
+                g.z / (1.f + expf(-g.z)) * up.z, g.w / (1.f + expf(-g.w)) * up.w);
   }
 }
 
-cudaError_t launch_swiglu(const float* P, int splits, void* u, int M, int F, cudaStream_t st) {
+cudaError_t launch_swiglu(const float* P, int splits, void* u, int M, int F, cudaStream_t st, int f32) {
   if (M == 0) return cudaSuccess;
   const size_t n4 = (size_t)M * F / 4;
   const int blocks = (int)std::min<size_t>((n4 + 255) / 256, (size_t)148 * 16);
-  CUDA_TRY_LAUNCH(launch_k(swiglu_kernel, dim3(blocks), dim3(256), 0, st, P, splits, reinterpret_cast<uint2*>(u), M, F));
+  if (f32)
+    CUDA_TRY_LAUNCH(launch_k(swiglu_kernel<true>, dim3(blocks), dim3(256), 0, st, P, splits, u, M, F));
+  else
+    CUDA_TRY_LAUNCH(launch_k(swiglu_kernel<false>, dim3(blocks), dim3(256), 0, st, P, splits, u, M, F));
   return cudaGetLastError();
 }
 
@@ -445,10 +466,51 @@ __global__ void kv_link_kernel(uint4* __restrict__ Kpool, uint4* __restrict__ Vp
   }
 }
 
+// fp32 debug build: same gather + re-base on fp32 pools, one thread per NeoX pair (K) or element (V)
+__global__ void kv_link_f32_kernel(float* __restrict__ Kpool, float* __restrict__ Vpool, const int32_t* __restrict__ src_slot,
+                                   const int32_t* __restrict__ dst_slot, const int32_t* __restrict__ delta, int n_rows,
+                                   int layer0, int n_layers, int64_t layer_stride, int Hkv, int D,
+                                   const float* __restrict__ cos_t, const float* __restrict__ sin_t, int rebase) {
+  PIC_PDL_ENTRY();
+  const int half = D / 2;
+  const int64_t per_row = (int64_t)Hkv * (half + D);
+  const int64_t total = (int64_t)n_layers * n_rows * per_row;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t u = t;
+    const int e = (int)(u % per_row);
+    u /= per_row;
+    const int w = (int)(u % n_rows);
+    const int l = layer0 + (int)(u / n_rows);
+    const int ss = src_slot[w], ds = dst_slot[w];
+    const bool isK = e < Hkv * half;
+    const int g = isK ? e / half : (e - Hkv * half) / D;
+    const int j = isK ? e % half : (e - Hkv * half) % D;
+    const int64_t so = (int64_t)l * layer_stride + ((int64_t)(ss / 16) * Hkv + g) * 16 * D + (int64_t)(ss % 16) * D;
+    const int64_t dof = (int64_t)l * layer_stride + ((int64_t)(ds / 16) * Hkv + g) * 16 * D + (int64_t)(ds % 16) * D;
+    if (!isK) {
+      Vpool[dof + j] = Vpool[so + j];
+      continue;
+    }
+    const float a = Kpool[so + j], b = Kpool[so + j + half];
+    const int dl = rebase ? delta[w] : 0;
+    const int ad = dl < 0 ? -dl : dl;
+    const float c = cos_t[(size_t)ad * half + j], sn = (dl < 0 ? -1.f : 1.f) * sin_t[(size_t)ad * half + j];
+    Kpool[dof + j] = dl ? a * c - b * sn : a;
+    Kpool[dof + j + half] = dl ? b * c + a * sn : b;
+  }
+}
+
 cudaError_t launch_kv_link(void* Kpool, void* Vpool, const int32_t* src_slot, const int32_t* dst_slot,
                            const int32_t* delta, int n_rows, int layer0, int n_layers, int64_t layer_stride_elems,
-                           int Hkv, int D, const float* cos_t, const float* sin_t, int rebase, cudaStream_t st) {
+                           int Hkv, int D, const float* cos_t, const float* sin_t, int rebase, cudaStream_t st,
+                           int f32) {
   if (n_rows == 0 || n_layers == 0) return cudaSuccess;
+  if (f32) {
+    CUDA_TRY_LAUNCH(launch_k(kv_link_f32_kernel, dim3(148 * 8), dim3(256), 0, st, reinterpret_cast<float*>(Kpool),
+                             reinterpret_cast<float*>(Vpool), src_slot, dst_slot, delta, n_rows, layer0, n_layers,
+                             layer_stride_elems, Hkv, D, cos_t, sin_t, rebase));
+    return cudaGetLastError();
+  }
   const int64_t total = (int64_t)n_layers * n_rows * Hkv * (D / 16 + D / 8);
   const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
   CUDA_TRY_LAUNCH(launch_k(kv_link_kernel, dim3(blocks), dim3(256), 0, st, reinterpret_cast<uint4*>(Kpool), reinterpret_cast<uint4*>(Vpool), src_slot,
@@ -510,10 +572,11 @@ cudaError_t launch_logits_argmax(const float* P, int splits, float* logits, int3
 // ================================================================================ a9 CacheBlend
 // Deviation of the check layer's fresh K (roped at p_i = i) and V from the linked (re-based) K/V
 // (P:170 step 3; readings R9/R10).  Non-candidates (dynamic rows and the forced last row) get −1.
+template <bool F32>
 __global__ void cb_deviation_kernel(const float* __restrict__ P, int splits, const int32_t* __restrict__ cand,
                                     const int32_t* __restrict__ slot, const float* __restrict__ cos_t,
-                                    const float* __restrict__ sin_t, const __nv_bfloat16* __restrict__ Kp,
-                                    const __nv_bfloat16* __restrict__ Vp, float* __restrict__ dev, int N, int Hq,
+                                    const float* __restrict__ sin_t, const void* __restrict__ Kp,
+                                    const void* __restrict__ Vp, float* __restrict__ dev, int N, int Hq,
                                     int Hkv, int D) {
   PIC_PDL_ENTRY();
   __shared__ float red[8];
@@ -534,14 +597,14 @@ __global__ void cb_deviation_kernel(const float* __restrict__ P, int splits, con
     const float a = sum_partials(prow, splits, sstride, col), b = sum_partials(prow, splits, sstride, col + half);
     const float c = cos_t[(size_t)i * half + j], s = sin_t[(size_t)i * half + j];
     const size_t o = kv_base + (size_t)hd * 16 * D + j;
-    const float d1 = a * c - b * s - __bfloat162float(Kp[o]);
-    const float d2 = b * c + a * s - __bfloat162float(Kp[o + half]);
+    const float d1 = a * c - b * s - load1<F32>(Kp, o);
+    const float d2 = b * c + a * s - load1<F32>(Kp, o + half);
     acc += d1 * d1 + d2 * d2;
   }
   for (int t = threadIdx.x; t < Hkv * D; t += blockDim.x) {
     const int hd = t / D, j = t % D;
     const float v = sum_partials(prow, splits, sstride, (Hq + Hkv) * D + t);
-    const float dd = v - __bfloat162float(Vp[kv_base + (size_t)hd * 16 * D + j]);
+    const float dd = v - load1<F32>(Vp, kv_base + (size_t)hd * 16 * D + j);
     acc += dd * dd;
   }
   acc = block_sum<256>(acc, red);
@@ -550,10 +613,13 @@ __global__ void cb_deviation_kernel(const float* __restrict__ P, int splits, con
 
 cudaError_t launch_cb_deviation(const float* P, int splits, const int32_t* cand, const int32_t* slot,
                                 const float* cos_t, const float* sin_t, const void* Kpool_l, const void* Vpool_l,
-                                float* dev, int N, int Hq, int Hkv, int D, cudaStream_t st) {
-  CUDA_TRY_LAUNCH(launch_k(cb_deviation_kernel, dim3(N), dim3(256), 0, st, P, splits, cand, slot, cos_t, sin_t,
-                                         reinterpret_cast<const __nv_bfloat16*>(Kpool_l),
-                                         reinterpret_cast<const __nv_bfloat16*>(Vpool_l), dev, N, Hq, Hkv, D));
+                                float* dev, int N, int Hq, int Hkv, int D, cudaStream_t st, int f32) {
+  if (f32)
+    CUDA_TRY_LAUNCH(launch_k(cb_deviation_kernel<true>, dim3(N), dim3(256), 0, st, P, splits, cand, slot, cos_t, sin_t,
+                             Kpool_l, Vpool_l, dev, N, Hq, Hkv, D));
+  else
+    CUDA_TRY_LAUNCH(launch_k(cb_deviation_kernel<false>, dim3(N), dim3(256), 0, st, P, splits, cand, slot, cos_t,
+                             sin_t, Kpool_l, Vpool_l, dev, N, Hq, Hkv, D));
   return cudaGetLastError();
 }
 

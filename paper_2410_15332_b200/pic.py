@@ -31,7 +31,7 @@ class ModelConfigC(C.Structure):
     _fields_ = [("n_layers", C.c_int32), ("d_model", C.c_int32), ("n_heads", C.c_int32),
                 ("n_kv_heads", C.c_int32), ("head_dim", C.c_int32), ("ffn_dim", C.c_int32),
                 ("vocab", C.c_int32), ("max_pos", C.c_int32), ("bos_id", C.c_int32),
-                ("rope_theta", C.c_double), ("rms_eps", C.c_double), ("seed", C.c_uint64)]
+                ("rope_theta", C.c_double), ("rms_eps", C.c_double), ("seed", C.c_uint64), ("dtype", C.c_int32)]
 
 
 class LimitsC(C.Structure):
@@ -148,7 +148,7 @@ def _ptr(a: Optional[np.ndarray], ctype=C.c_int32):
 def config_struct(cfg) -> ModelConfigC:
     return ModelConfigC(cfg.n_layers, cfg.d_model, cfg.n_heads, cfg.n_kv_heads, cfg.head_dim, cfg.ffn_dim,
                         cfg.vocab, cfg.max_pos, cfg.bos_id, float(cfg.rope_theta), float(cfg.rms_eps),
-                        int(cfg.seed))
+                        int(cfg.seed), int(getattr(cfg, "dtype", 0)))
 
 
 ALGS = {"naive": PIC_NAIVE, "fr": PIC_FULL, "legolink": PIC_LEGOLINK, "cacheblend": PIC_CACHEBLEND}
@@ -199,6 +199,9 @@ class LinkOutput:
 
 
 def bf16_bits_to_f32(b: np.ndarray) -> np.ndarray:
+    """bf16 bit patterns (uint16) -> float32; float32 arrays (fp32 debug build) pass through."""
+    if b.dtype == np.float32:
+        return b
     return (b.astype(np.uint32) << np.uint32(16)).view(np.float32)
 
 
@@ -351,12 +354,21 @@ class Engine:
                 "block_table": bufs["block_table"][:nb].copy(), "slot": bufs["slot"][:ns].copy()}
 
     # ------------------------------------------------------------------ exports / lifecycle
+    @property
+    def kv_dtype(self):
+        """uint16 (bf16 bits) for the product, float32 for the fp32 debug build."""
+        return np.float32 if int(getattr(self.cfg, "dtype", 0)) == 1 else np.uint16
+
+    @property
+    def local_kv_heads(self) -> int:
+        return self.cfg.n_kv_heads // getattr(self, "tp_size", 1)
+
     def linked_export(self, linked: int, layer: int) -> Tuple[np.ndarray, np.ndarray]:
         n = C.c_int32()
         check(lib().pic_linked_info(self._h, C.c_void_p(linked), C.byref(n), None))
-        shape = (n.value, self.cfg.n_kv_heads, self.cfg.head_dim)
-        k = np.empty(shape, dtype=np.uint16)
-        v = np.empty(shape, dtype=np.uint16)
+        shape = (n.value, self.local_kv_heads, self.cfg.head_dim)
+        k = np.empty(shape, dtype=self.kv_dtype)
+        v = np.empty(shape, dtype=self.kv_dtype)
         check(lib().pic_linked_export(self._h, C.c_void_p(linked), layer, k.ctypes.data, v.ctypes.data))
         return k, v
 
@@ -373,9 +385,9 @@ class Engine:
     def cache_export(self, cid: int, layer: int) -> Tuple[np.ndarray, np.ndarray]:
         n = C.c_int32()
         check(lib().pic_cache_info(self._h, cid, C.byref(n), None))
-        shape = (n.value, self.cfg.n_kv_heads, self.cfg.head_dim)
-        k = np.empty(shape, dtype=np.uint16)
-        v = np.empty(shape, dtype=np.uint16)
+        shape = (n.value, self.local_kv_heads, self.cfg.head_dim)
+        k = np.empty(shape, dtype=self.kv_dtype)
+        v = np.empty(shape, dtype=self.kv_dtype)
         check(lib().pic_cache_export(self._h, cid, layer, k.ctypes.data, v.ctypes.data))
         return k, v
 

@@ -1,1 +1,2 @@
-timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29511 bench.py --config cfg5 --tp --layers 4 --steps 3 --warmup 3 --no-cpu-baseline 2>&1 | grep -v Warning | tail -3 | cut -c1-900
+timeout 900 python -m pytest tests/test_gpu_fp32debug.py -q -x --timeout 600 --timeout_method thread 2>&1 | tail -20
+timeout 900 python -m pytest tests/ -m gpu -q -x --timeout 600 --timeout_method thread -k "not fullsize" 2>&1 | tail -3

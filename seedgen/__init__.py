@@ -139,6 +139,7 @@ class ModelConfig:
     seed: int
     rms_eps: float = 1e-5
     bos_id: int = 1
+    dtype: int = 0      # engine numeric mode under test: 0 bf16 product, 1 fp32 debug build (not model data)
 
     @property
     def qkv_dim(self) -> int:
