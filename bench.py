@@ -158,6 +158,32 @@ def cores_used():
 
 
 # ------------------------------------------------------------------------------------- main
+def roofline(prof, P, src, nsteps):
+    """Dominant kernel class of the profiled steps against its roofline."""
+    tot = sum(v["ms"] for v in prof.values())
+    dom_name, dom = max(prof.items(), key=lambda kv: kv[1]["ms"])
+    intensity = dom["flops"] / max(dom["bytes"], 1)
+    ridge = P["bf16_tflops"] * 1e12 / (P["hbm_gbs"] * 1e9)
+    if intensity < ridge:
+        achieved = dom["bytes"] / (dom["ms"] / 1e3) / 1e9
+        roof = {"bound": "hbm", "achieved": achieved, "peak": P["hbm_gbs"], "unit": "GB/s"}
+    else:
+        achieved = dom["flops"] / (dom["ms"] / 1e3) / 1e12
+        roof = {"bound": "tensor", "achieved": achieved, "peak": P["bf16_tflops"], "unit": "TFLOP/s"}
+    roof["frac"] = roof["achieved"] / roof["peak"]
+    roof["traffic"] = None
+    roof["kernel"] = dom_name
+    roof["share_of_step"] = dom["ms"] / tot
+    roof["peak_source"] = f"{src} (MEASURED_PEAKS.json burst)" if src == "measured" else "fallback (B200_PROFILING.md)"
+    roof["launches_per_step"] = dom["launches"] / nsteps
+    roof["how"] = (f"algorithmic bytes/FLOPs per launch (SURVEY §8(d)) over CUDA-event durations of every launch, "
+                   f"{nsteps} profiled steps on the bench stream (graphs off)")
+    breakdown = {k: {"ms_per_step": v["ms"] / nsteps, "launches_per_step": v["launches"] / nsteps,
+                     "GB/s": v["bytes"] / max(v["ms"], 1e-9) / 1e6, "TFLOP/s": v["flops"] / max(v["ms"], 1e-9) / 1e9}
+                 for k, v in sorted(prof.items(), key=lambda kv: -kv[1]["ms"])}
+    return roof, breakdown
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -304,27 +330,7 @@ def main():
             dist.destroy_process_group()
         return
     P, src = peaks()
-    tot = sum(v["ms"] for v in prof.values())
-    dom_name, dom = max(prof.items(), key=lambda kv: kv[1]["ms"])
-    intensity = dom["flops"] / max(dom["bytes"], 1)
-    ridge = P["bf16_tflops"] * 1e12 / (P["hbm_gbs"] * 1e9)
-    if intensity < ridge:
-        achieved = dom["bytes"] / (dom["ms"] / 1e3) / 1e9
-        roof = {"bound": "hbm", "achieved": achieved, "peak": P["hbm_gbs"], "unit": "GB/s"}
-    else:
-        achieved = dom["flops"] / (dom["ms"] / 1e3) / 1e12
-        roof = {"bound": "tensor", "achieved": achieved, "peak": P["bf16_tflops"], "unit": "TFLOP/s"}
-    roof["frac"] = roof["achieved"] / roof["peak"]
-    roof["traffic"] = None
-    roof["kernel"] = dom_name
-    roof["share_of_step"] = dom["ms"] / tot
-    roof["peak_source"] = f"{src} (MEASURED_PEAKS.json burst)" if src == "measured" else "fallback (B200_PROFILING.md)"
-    roof["launches_per_step"] = dom["launches"] / args.profile_steps
-    roof["how"] = (f"algorithmic bytes/FLOPs per launch (SURVEY §8(d)) over CUDA-event durations of every launch, "
-                   f"{args.profile_steps} profiled steps on the bench stream (graphs off)")
-    breakdown = {k: {"ms_per_step": v["ms"] / args.profile_steps, "launches_per_step": v["launches"] / args.profile_steps,
-                     "GB/s": v["bytes"] / max(v["ms"], 1e-9) / 1e6, "TFLOP/s": v["flops"] / max(v["ms"], 1e-9) / 1e9}
-                 for k, v in sorted(prof.items(), key=lambda kv: -kv[1]["ms"])}
+    roof, breakdown = roofline(prof, P, src, args.profile_steps) if prof else (None, {})
     line = {"metric": "linked_prefill_tokens_per_s", "value": value, "unit": "tokens/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
             "ttft_ms_device": ms_per_step if len(reqs) == 1 else None,

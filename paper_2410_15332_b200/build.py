@@ -15,8 +15,8 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
-OBJ = os.path.join(ROOT, "build", "obj")
-LIB = os.path.join(PKG, "libpic.so")
+OBJ = os.path.join(ROOT, "build", os.environ.get("PIC_OBJ_DIR", "obj"))
+LIB = os.path.join(PKG, os.environ.get("PIC_LIB_NAME", "libpic.so"))  # name override: experiment builds only
 INCLUDE = os.path.join(ROOT, "include")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -52,7 +52,7 @@ def _obj(src: str) -> str:
 
 def _compile(src: str, verbose: bool) -> str:
     o = _obj(src)
-    cmd = [nvcc(), *ARCH, *FLAGS, "-c", src, "-o", o]
+    cmd = [nvcc(), *ARCH, *FLAGS, *os.environ.get("PIC_NVCC_EXTRA", "").split(), "-c", src, "-o", o]
     if verbose:
         cmd += ["-Xptxas", "-v"]
     r = subprocess.run(cmd, capture_output=True, text=True)

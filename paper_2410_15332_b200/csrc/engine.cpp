@@ -77,10 +77,66 @@ static void dbg_sync(const char* what, cudaStream_t st) {
 // with the kernel class and its algorithmic bytes / FLOPs (SURVEY §8(d) formulas).
 static pic_status prof_push(pic_engine* e, cudaStream_t st, const char* name, double bytes, double flops, bool begin);
 
+// Bench-only timing ablation (PIC_ABLATE bit mask; results are wrong when set): skip every launch of
+// a kernel class to measure its in-graph cost.  Never set by the engine, tests or bench.py.
+// Bench-only attention timeline (PIC_ATTN_TRACE=1): every attention launch writes per-CTA timestamps
+// into one static buffer (the last layer's launch wins); pic_link prints a summary after the call.
+static int g_attn_trace_ctas = 0;
+static unsigned long long* attn_trace_buffer() {
+  static unsigned long long* buf = nullptr;
+  static const bool on = getenv("PIC_ATTN_TRACE") != nullptr;
+  if (on && !buf && cudaMalloc(&buf, 16 * 8192 * sizeof(unsigned long long)) != cudaSuccess) buf = nullptr;
+  return on ? buf : nullptr;
+}
+static void attn_trace_print(int n_cta) {
+  unsigned long long* buf = attn_trace_buffer();
+  if (!buf || n_cta <= 0) return;
+  std::vector<unsigned long long> t((size_t)16 * n_cta);
+  if (cudaMemcpy(t.data(), buf, t.size() * 8, cudaMemcpyDeviceToHost) != cudaSuccess) return;
+  unsigned long long t0 = ~0ull;
+  for (int c = 0; c < n_cta; ++c) t0 = std::min(t0, t[16 * c]);
+  static const char* nm[8] = {"entry", "wait_done", "q_full", "first_S", "last_P", "last_O", "epi_done", "exit"};
+  {
+    std::vector<int> nt;
+    for (int c = 0; c < n_cta; ++c) nt.push_back((int)t[16 * c + 7]);
+    std::sort(nt.begin(), nt.end());
+    fprintf(stderr, "  attn kv tiles per CTA: min %d med %d max %d\n", nt[0], nt[nt.size() / 2], nt.back());
+  }
+  {
+    static const char* an[6] = {"wait S", "max+xchg", "exp+P", "mma wK", "mma wP", "mma wV"};
+    for (int k = 0; k < 6; ++k) {
+      std::vector<double> v;
+      for (int c = 0; c < n_cta; ++c)
+        if (t[16 * c + 7] > 0) v.push_back((double)t[16 * c + 8 + k] / 1e3 / (double)t[16 * c + 7]);
+      if (v.empty()) continue;
+      std::sort(v.begin(), v.end());
+      fprintf(stderr, "  attn per-tile %-9s min %6.3f med %6.3f max %6.3f us\n", an[k], v[0], v[v.size() / 2], v.back());
+    }
+  }
+  for (int k = 0; k < 7; ++k) {
+    std::vector<double> v;
+    for (int c = 0; c < n_cta; ++c)
+      if (t[16 * c + k] >= t0) v.push_back((double)(t[16 * c + k] - t0) / 1e3);
+    if (v.empty()) continue;
+    std::sort(v.begin(), v.end());
+    fprintf(stderr, "  attn %-9s min %7.2f  med %7.2f  max %7.2f us (n=%zu)\n", nm[k], v[0], v[v.size() / 2], v.back(),
+            v.size());
+  }
+}
+
+static bool ablated(const char* name) {
+  static const int mask = getenv("PIC_ABLATE") ? atoi(getenv("PIC_ABLATE")) : 0;
+  if (!mask) return false;
+  static const char* names[] = {"rmsnorm", "qkv_rope_scatter", "attention", "attn_combine", "gemm", "kv_link", "swiglu"};
+  for (int i = 0; i < 7; ++i)
+    if ((mask >> i & 1) && !strcmp(name, names[i])) return true;
+  return false;
+}
+
 #define PROF(name, bytes, flops, expr)                                      \
   do {                                                                      \
     if (e->profiling) TRY(prof_push(e, st, name, bytes, flops, true));      \
-    CKL(expr);                                                              \
+    if (!ablated(name)) CKL(expr);                                          \
     if (e->profiling) TRY(prof_push(e, st, name, 0, 0, false));             \
   } while (0)
 
@@ -889,6 +945,12 @@ static pic_status enqueue_forward(pic_engine* e, const Fwd& f, const DevPlan& dp
       a.layer = l;
       a.num_blocks = (int)e->lim.num_blocks;
       a.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)D));
+      a.trace = attn_trace_buffer();
+      a.static_plan = (tiles == dp.tiles) ? 1 : 0;  // CacheBlend's post-selection tiles/positions are device-side
+      a.kpool = nullptr;  // L2 prefetch of K/V pages: measured slower (TMA unit busy ahead of the real loads)
+      a.vpool = e->Vpool;
+      a.Q = e->Q;
+      g_attn_trace_ctas = a.n_work * Hkv;
       a.o_part = e->o_part;
       a.ml_part = e->ml_part;
       R.launches += 2;
@@ -1383,7 +1445,12 @@ static pic_status link_impl(pic_engine* e, int32_t n_req, const pic_segment* con
 
 extern "C" pic_status pic_link(pic_engine* e, const pic_segment* segs, int32_t n_segs, const pic_link_params* params,
                                void* stream, pic_linked** out_linked, pic_link_result* result) {
-  return link_impl(e, 1, &segs, &n_segs, params, stream, out_linked, result);
+  const pic_status st = link_impl(e, 1, &segs, &n_segs, params, stream, out_linked, result);
+  if (st == PIC_OK && attn_trace_buffer()) {
+    cudaStreamSynchronize(reinterpret_cast<cudaStream_t>(stream));
+    attn_trace_print(g_attn_trace_ctas);
+  }
+  return st;
 }
 
 extern "C" pic_status pic_link_batch(pic_engine* e, int32_t n_req, const pic_segment* const* segs,

@@ -34,26 +34,32 @@
 namespace pic {
 
 namespace attn {
-constexpr int kTile = 16384;                 // one [128 rows][64 cols] bf16 SW128 half tile
-constexpr int kQ = 0;                        // Q: 2 halves
-constexpr int kK = kQ + 2 * kTile;           // K stages: 2 x 2 halves
-constexpr int kV = kK + 4 * kTile;           // V stages
-constexpr int kP = kV + 4 * kTile;           // P buffers: 2 x 2 halves
-constexpr int kX = kP + 4 * kTile;           // softmax pair exchange: [2 parity][2 halves][128] fp32
-constexpr int kBar = kX + 2 * 2 * 128 * 4;   // barriers
-constexpr int kNumBars = 1 + 2 * 2 + 2 * 2 + 2 + 2 + 2;
+constexpr int kTile = 16384;                  // one [128 rows][64 cols] bf16 SW128 half tile
+constexpr int kStages = 3;                    // K and V ring depth
+constexpr int kK = 0;                         // K stages: kStages x 2 halves
+constexpr int kV = kK + kStages * 2 * kTile;  // V stages
+constexpr int kX = kV + kStages * 2 * kTile;  // softmax pair exchange: [2 parity][2 halves][128] fp32
+constexpr int kBar = kX + 2 * 2 * 128 * 4;    // barriers
+constexpr int kNumBars = 1 + 4 * kStages + 6;
 constexpr int kSmem = kBar + kNumBars * 8 + 16;
 static_assert(kSmem <= 232448, "attention smem over the 227 KB limit");
+// TMEM columns (512 allocated)
+constexpr uint32_t kTmS = 0;    // S double buffer [0, 256); P(t) (bf16 pairs) overwrites S(t): half hc at +64·hc
+constexpr uint32_t kTmO = 256;  // O accumulator [256, 384)
+constexpr uint32_t kTmQ = 384;  // Q (bf16 pairs) [384, 448)
 }  // namespace attn
 
+// Both MMAs take their A operand from TMEM (Q for S = Q·Kᵀ, P for O += P·V), so shared memory only
+// carries K and V: per 128-key tile the smem traffic is the two TMA writes and the two B-operand reads.
 template <int G>
 __global__ void __launch_bounds__(320, 1)
-    attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-                   const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmK8,
-                   const __grid_constant__ CUtensorMap tmV8, const AttnArgs a) {
+    attn_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
+                   const __grid_constant__ CUtensorMap tmK8, const __grid_constant__ CUtensorMap tmV8, const AttnArgs a) {
   griddep_launch();
   using namespace attn;
-  constexpr int QPT = 128 / G;  // queries per tile
+  constexpr int S = kStages;
+  unsigned long long* const tr = a.trace ? a.trace + 16 * (blockIdx.y * gridDim.x + blockIdx.x) : nullptr;
+  if (tr && threadIdx.x == 0) tr[0] = globaltimer();
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw;
   if (threadIdx.x == 0 && (smem_u32(smem) & 1023)) __trap();  // SWIZZLE_128B tiles need 1 KB alignment
@@ -61,15 +67,40 @@ __global__ void __launch_bounds__(320, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + kNumBars);
   const uint32_t base = smem_u32(smem);
   const uint32_t q_full = smem_u32(bars + 0);
-  const uint32_t k_full = smem_u32(bars + 1), k_empty = smem_u32(bars + 3);
-  const uint32_t v_full = smem_u32(bars + 5), v_empty = smem_u32(bars + 7);
-  const uint32_t s_full = smem_u32(bars + 9), p_full = smem_u32(bars + 11), o_full = smem_u32(bars + 13);
+  const uint32_t k_full = smem_u32(bars + 1), k_empty = smem_u32(bars + 1 + S);
+  const uint32_t v_full = smem_u32(bars + 1 + 2 * S), v_empty = smem_u32(bars + 1 + 3 * S);
+  const uint32_t s_full = smem_u32(bars + 1 + 4 * S), p_full = smem_u32(bars + 3 + 4 * S);
+  const uint32_t o_full = smem_u32(bars + 5 + 4 * S);
 
   const int warp = warp_id(), lane = lane_id();
+  // barriers and TMEM do not depend on upstream data: set them up while the previous kernel drains
+  if (threadIdx.x == 0) {
+    mbar_init(q_full, 256);
+    for (int s = 0; s < S; ++s) {
+      mbar_init(k_full + 8 * s, 1);
+      mbar_init(k_empty + 8 * s, 1);
+      mbar_init(v_full + 8 * s, 1);
+      mbar_init(v_empty + 8 * s, 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(s_full + 8 * b, 1);
+      mbar_init(p_full + 8 * b, 256);
+      mbar_init(o_full + 8 * b, 1);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc(smem_u32(tmem_slot), 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  // Host-uploaded plans (work list, tiles, positions, block tables) are complete before the graph
+  // starts; device-side ones (CacheBlend's re-selected rows) come from upstream kernels.
+  if (!a.static_plan) griddep_wait();
+  if (tr && threadIdx.x == 0 && !a.static_plan) tr[1] = globaltimer();
   // work item (host-balanced split-KV schedule): q-tile, KV-tile range [j0, j1), split slot
   const int* wk = a.work + 4 * blockIdx.x;
   const int tile = wk[0], split = wk[3], g = blockIdx.y;
-  griddep_wait();  // Q, row positions and the linked K/V come from upstream kernels
   const int seq = a.tiles[3 * tile], row_start = a.tiles[3 * tile + 1], row_count = a.tiles[3 * tile + 2];
 
   // causal extent of this tile: keys 0..max_p (rows are sorted, but take the max anyway)
@@ -82,44 +113,34 @@ __global__ void __launch_bounds__(320, 1)
   const int n = max(0, j1 - j0);
   const int* bt = a.bt + a.seq_bt_off[seq];
   const int last_blk = max_p / 16;
-
-  if (threadIdx.x == 0) {
-    mbar_init(q_full, 1);
-    for (int s = 0; s < 2; ++s) {
-      mbar_init(k_full + 8 * s, 1);
-      mbar_init(k_empty + 8 * s, 1);
-      mbar_init(v_full + 8 * s, 1);
-      mbar_init(v_empty + 8 * s, 1);
-      mbar_init(s_full + 8 * s, 1);
-      mbar_init(p_full + 8 * s, 256);
-      mbar_init(o_full + 8 * s, 1);
+  // L2 prefetch of this CTA's K/V pages (a hint, so it may run before the upstream kernel that
+  // writes the recomputed rows has finished: L2 is the coherence point)
+  if (warp == 0 && a.kpool) {  // one paged block per lane and round: the block-id loads run in parallel
+    for (int i = lane; i < n * 8; i += 32) {
+      const int blk = bt[min(j0 * 8 + i, last_blk)];
+      const size_t off = (((size_t)a.layer * a.num_blocks + blk) * a.Hkv + g) * (16 * 128 * 2);
+      bulk_prefetch_l2(reinterpret_cast<const uint8_t*>(a.kpool) + off, 16 * 128 * 2);
+      bulk_prefetch_l2(reinterpret_cast<const uint8_t*>(a.vpool) + off, 16 * 128 * 2);
     }
-    fence_mbar_init();
   }
-  if (warp == 2) tmem_alloc(smem_u32(tmem_slot), 512);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
+  if (a.static_plan) griddep_wait();  // Q and the recomputed rows' K/V come from the upstream kernel
+  if (tr && threadIdx.x == 0 && a.static_plan) tr[1] = globaltimer();
 
   if (warp == 0) {
-    // ------------------------------------------------------------------ TMA producer
+    // ------------------------------------------------------------------ TMA producer (K, V)
     if (n > 0) {
       if (lane == 0) {
-        tma_prefetch(&tmQ);
         tma_prefetch(&tmK);
         tma_prefetch(&tmV);
         tma_prefetch(&tmK8);
         tma_prefetch(&tmV8);
-        mbar_expect_tx(q_full, 2 * kTile);
-        for (int h = 0; h < 2; ++h) tma_load_3d(base + kQ + h * kTile, &tmQ, q_full, h * 64, g * G, row_start);
       }
       const int kv_base = a.layer * a.num_blocks;
       // the 8 paged-block ids of a 128-key tile: one coalesced load by lanes 0-7, one tile ahead
       int blk_next = lane < 8 ? bt[min(j0 * 8 + lane, last_blk)] : 0;
       for (int t = 0; t < n; ++t) {
-        const int s = t & 1;
-        const uint32_t ph = (t >> 1) & 1;
+        const int s = t % S;
+        const uint32_t ph = (t / S) & 1;
         const int blk_mine = blk_next;
         if (t + 1 < n && lane < 8) blk_next = bt[min((j0 + t + 1) * 8 + lane, last_blk)];
         int blk[8];
@@ -159,41 +180,57 @@ __global__ void __launch_bounds__(320, 1)
   } else if (warp == 1) {
     // ------------------------------------------------------------------ MMA issuer
     if (lane == 0 && n > 0) {
-      constexpr uint32_t idS = idesc_bf16(128, 128, 0, 0);  // Q (K-major) x K (K-major)
-      constexpr uint32_t idO = idesc_bf16(128, 128, 0, 1);  // P (K-major) x V (MN-major)
+      constexpr uint32_t idS = idesc_bf16(128, 128, 0, 0);  // Q (TMEM, K-major) x K (smem, K-major)
+      constexpr uint32_t idO = idesc_bf16(128, 128, 0, 1);  // P (TMEM, K-major) x V (smem, MN-major)
+      unsigned long long w_k = 0, w_p = 0, w_v = 0, q0 = 0;
       mbar_wait(q_full, 0);
+      tc_fence_after();
+      if (tr) tr[2] = globaltimer();
       auto issue_pv = [&](int u) {
-        const int pb = u & 1;
-        const uint32_t ph = (u >> 1) & 1;
-        mbar_wait(p_full + 8 * pb, ph);
-        mbar_wait(v_full + 8 * pb, ph);
+        const int pb = u & 1, vs = u % S;
+        if (tr) q0 = globaltimer();
+        mbar_wait(p_full + 8 * pb, (u >> 1) & 1);
+        if (tr) {
+          const unsigned long long q1 = globaltimer();
+          w_p += q1 - q0;
+          q0 = q1;
+        }
+        mbar_wait(v_full + 8 * vs, (u / S) & 1);
+        if (tr) w_v += globaltimer() - q0;
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
-          const uint32_t pa = base + kP + (2 * pb + (kk >> 2)) * kTile + (kk & 3) * 32;
-          const uint32_t vb = base + kV + (2 * pb) * kTile + kk * 2048;  // 16 keys x 128 B
+          // keys 16kk..16kk+15: P half kk/4 at S-buffer column 64·(kk/4), 8 columns per 16 keys
+          const uint32_t pa = tmem + kTmS + pb * 128 + (kk >> 2) * 64 + (kk & 3) * 8;
+          const uint32_t vb = base + kV + (2 * vs) * kTile + kk * 2048;  // 16 keys x 128 B
           // O accumulates in TMEM across KV tiles (rescaled by the softmax warps when needed)
-          umma_bf16(tmem + 256, sdesc_sw128(pa, 16, 1024), sdesc_sw128(vb, kTile, 1024), idO, (u | kk) != 0);
+          umma_bf16_ts(tmem + kTmO, pa, sdesc_sw128(vb, kTile, 1024), idO, (u | kk) != 0);
         }
         umma_commit(o_full + 8 * pb);
-        umma_commit(v_empty + 8 * pb);
+        umma_commit(v_empty + 8 * vs);
       };
       for (int t = 0; t < n; ++t) {
-        const int sb = t & 1;
-        const uint32_t ph = (t >> 1) & 1;
-        mbar_wait(k_full + 8 * sb, ph);
+        const int sb = t & 1, ks = t % S;
+        if (tr) q0 = globaltimer();
+        mbar_wait(k_full + 8 * ks, (t / S) & 1);
+        if (tr) w_k += globaltimer() - q0;
         tc_fence_after();
+        // S(t) overwrites the buffer holding P(t-2): PV(t-2) was issued before and MMAs run in order
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
-          const uint32_t qa = base + kQ + (kk >> 2) * kTile + (kk & 3) * 32;
-          const uint32_t kb = base + kK + (2 * sb + (kk >> 2)) * kTile + (kk & 3) * 32;
-          umma_bf16(tmem + sb * 128, sdesc_sw128(qa, 16, 1024), sdesc_sw128(kb, 16, 1024), idS, kk > 0);
+          const uint32_t kb = base + kK + (2 * ks + (kk >> 2)) * kTile + (kk & 3) * 32;
+          umma_bf16_ts(tmem + kTmS + sb * 128, tmem + kTmQ + kk * 8, sdesc_sw128(kb, 16, 1024), idS, kk > 0);
         }
         umma_commit(s_full + 8 * sb);
-        umma_commit(k_empty + 8 * sb);
+        umma_commit(k_empty + 8 * ks);
         if (t >= 1) issue_pv(t - 1);
       }
       issue_pv(n - 1);
+      if (tr) {
+        tr[11] = w_k;
+        tr[12] = w_p;
+        tr[13] = w_v;
+      }
     }
   } else {
     // ------------------------------------------------------------------ softmax warps
@@ -209,26 +246,66 @@ __global__ void __launch_bounds__(320, 1)
     const int head = g * G + hh;
     const int pos = valid ? a.row_pos[row] : max_p;
     const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
-    const uint32_t oAddr = tmem + lane_addr + 256 + hc * 64;
+    const uint32_t oAddr = tmem + lane_addr + kTmO + hc * 64;
+    // Q row -> TMEM: this thread's 64 dims as 32 bf16 pairs (the A operand of S = Q·Kᵀ)
+    {
+      uint32_t qv[32];
+      if (valid) {
+        const uint4* src = reinterpret_cast<const uint4*>(reinterpret_cast<const uint16_t*>(a.Q) +
+                                                          ((size_t)row * a.Hq + head) * 128 + hc * 64);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const uint4 x = src[i];
+          qv[4 * i] = x.x;
+          qv[4 * i + 1] = x.y;
+          qv[4 * i + 2] = x.z;
+          qv[4 * i + 3] = x.w;
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) qv[i] = 0u;
+      }
+      tmem_st32u(tmem + lane_addr + kTmQ + hc * 32, qv);
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(q_full);
+    }
     float* xmax = reinterpret_cast<float*>(smem + kX);   // [2 parity][2 halves][128 rows]
-    // m_ref: the max the current O / l are scaled to.  It is raised only when a row's max grows by
-    // more than 2^8 (then O in TMEM and l are rescaled), so exp2 arguments stay <= 8 and the common
-    // case never touches O (FA4-style lazy rescale; exact because the final normalisation uses m_ref).
+    const float sc = a.scale_log2;
+    // m_ref (log2 units): the max the current O / l are scaled to.  It is raised only when a row's
+    // max grows by more than 2^8 (then O in TMEM and l are rescaled), so exp2 arguments stay <= 8
+    // and the common case never touches O (FA4-style lazy rescale; exact because the final
+    // normalisation uses m_ref).
     float m_ref = -INFINITY, l = 0.f;
+    const bool trc = tr && threadIdx.x == 64;
+    unsigned long long acc_ws = 0, acc_mx = 0, acc_ex = 0, tt0 = 0, tt1 = 0;
     for (int t = 0; t < n; ++t) {
       const int sb = t & 1;
       const uint32_t ph = (t >> 1) & 1;
       const int key0 = (j0 + t) * 128 + hc * 64;
+      if (trc) tt0 = globaltimer();
       mbar_wait(s_full + 8 * sb, ph);
-      tc_fence_after();
-      float sv[64];
-      tmem_ld64(tmem + lane_addr + sb * 128 + hc * 64, sv);
-      float mx = -INFINITY;
-#pragma unroll
-      for (int i = 0; i < 64; ++i) {
-        sv[i] = (key0 + i <= pos) ? sv[i] * a.scale_log2 : -INFINITY;
-        mx = fmaxf(mx, sv[i]);
+      if (trc) {
+        tt1 = globaltimer();
+        acc_ws += tt1 - tt0;
       }
+      if (tr && t == 0 && threadIdx.x == 64) tr[3] = globaltimer();
+      tc_fence_after();
+      const uint32_t sAddr = tmem + lane_addr + kTmS + sb * 128 + hc * 64;
+      float sv[64];
+      tmem_ld64(sAddr, sv);
+      float mx = -INFINITY;
+      if (key0 + 63 <= pos) {  // the whole half is causal-visible: no mask
+#pragma unroll
+        for (int i = 0; i < 64; ++i) mx = fmaxf(mx, sv[i]);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 64; ++i) {
+          sv[i] = (key0 + i <= pos) ? sv[i] : -INFINITY;
+          mx = fmaxf(mx, sv[i]);
+        }
+      }
+      mx *= sc;  // log2 units (sc > 0)
       xmax[(sb * 2 + hc) * 128 + r] = mx;
       named_bar_sync(1 + q, 64);
       mx = fmaxf(mx, xmax[(sb * 2 + (hc ^ 1)) * 128 + r]);
@@ -253,45 +330,67 @@ __global__ void __launch_bounds__(320, 1)
         l *= alpha;
       }
       if (grow) m_ref = mx;
-      // P buffer sb was read by PV_{t-2}: it must have completed
-      if (t >= 2) mbar_wait(o_full + 8 * (t & 1), ((t - 2) >> 1) & 1);
+      if (trc) {
+        tt0 = globaltimer();
+        acc_mx += tt0 - tt1;
+      }
+      const float nmu = (m_ref == -INFINITY) ? 0.f : -m_ref;
       float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
-      uint8_t* pbuf = smem + kP + (2 * sb + hc) * kTile + r * 128;
-      const float mu = (m_ref == -INFINITY) ? 0.f : m_ref;
+      uint32_t pk[32];
 #pragma unroll
-      for (int c = 0; c < 8; ++c) {  // 8 chunks of 8 keys = 16 bytes of bf16 P
-        const float p0 = exp2f(sv[8 * c] - mu), p1 = exp2f(sv[8 * c + 1] - mu);
-        const float p2 = exp2f(sv[8 * c + 2] - mu), p3 = exp2f(sv[8 * c + 3] - mu);
-        const float p4 = exp2f(sv[8 * c + 4] - mu), p5 = exp2f(sv[8 * c + 5] - mu);
-        const float p6 = exp2f(sv[8 * c + 6] - mu), p7 = exp2f(sv[8 * c + 7] - mu);
-        s0 += p0 + p1;
-        s1 += p2 + p3;
-        s2 += p4 + p5;
-        s3 += p6 + p7;
-        *reinterpret_cast<uint4*>(pbuf + ((c ^ (r & 7)) << 4)) =
-            make_uint4(pack_bf16(p0, p1), pack_bf16(p2, p3), pack_bf16(p4, p5), pack_bf16(p6, p7));
+      for (int c = 0; c < 16; ++c) {  // p = 2^(s·scale − m_ref); masked keys are −inf → 0
+        const float p0 = ex2_approx(fmaf(sv[4 * c], sc, nmu)), p1 = ex2_approx(fmaf(sv[4 * c + 1], sc, nmu));
+        const float p2 = ex2_approx(fmaf(sv[4 * c + 2], sc, nmu)), p3 = ex2_approx(fmaf(sv[4 * c + 3], sc, nmu));
+        s0 += p0;
+        s1 += p1;
+        s2 += p2;
+        s3 += p3;
+        pk[2 * c] = pack_bf16(p0, p1);
+        pk[2 * c + 1] = pack_bf16(p2, p3);
       }
       l += (s0 + s1) + (s2 + s3);
-      fence_async_smem();
+      // P(t) overwrites this half's S(t) columns (already in registers); PV(t) reads it from TMEM
+      tmem_st32u(sAddr, pk);
+      tmem_wait_st();
       tc_fence_before();
       mbar_arrive(p_full + 8 * sb);
+      if (trc) acc_ex += globaltimer() - tt0;
+    }
+    if (trc) {
+      tr[4] = globaltimer();
+      tr[8] = acc_ws;
+      tr[9] = acc_mx;
+      tr[10] = acc_ex;
     }
     if (n > 0) {
       mbar_wait(o_full + 8 * ((n - 1) & 1), ((n - 1) >> 1) & 1);
       tc_fence_after();
     }
+    if (tr && threadIdx.x == 64) tr[5] = globaltimer();
     const size_t idx = ((size_t)split * a.M + row) * a.Hq + head;
-    float4* dst = reinterpret_cast<float4*>(a.o_part + idx * 128 + hc * 64);
     if (n > 0) {
+      // every MMA has completed, so the K ring is idle: stage this warp's [32 rows][64 cols] fp32
+      // O slice there (XOR-swizzled float4 slots) and store full 256-B row segments
+      float4* stg = reinterpret_cast<float4*>(smem + kK + (warp - 2) * 8192);
 #pragma unroll 1
       for (int c = 0; c < 2; ++c) {
         float ov[32];
-        tmem_ld32(oAddr + c * 32, ov);  // warp-collective: all lanes load, valid rows store
-        if (valid)
+        tmem_ld32(oAddr + c * 32, ov);  // warp-collective
 #pragma unroll
-          for (int i = 0; i < 8; ++i) dst[c * 8 + i] = make_float4(ov[4 * i], ov[4 * i + 1], ov[4 * i + 2], ov[4 * i + 3]);
+        for (int i = 0; i < 8; ++i)
+          stg[lane * 16 + ((c * 8 + i) ^ (lane & 7))] = make_float4(ov[4 * i], ov[4 * i + 1], ov[4 * i + 2], ov[4 * i + 3]);
+      }
+      __syncwarp();
+      const int jj = lane & 15;
+#pragma unroll 4
+      for (int i = 0; i < 16; ++i) {
+        const int rr = 2 * i + (lane >> 4), rm = q * 32 + rr, qi2 = rm / G;
+        if (qi2 < row_count)
+          reinterpret_cast<float4*>(a.o_part + (((size_t)split * a.M + row_start + qi2) * a.Hq + g * G + rm % G) * 128 +
+                                    hc * 64)[jj] = stg[rr * 16 + (jj ^ (rr & 7))];
       }
     } else if (valid) {
+      float4* dst = reinterpret_cast<float4*>(a.o_part + idx * 128 + hc * 64);
       for (int i = 0; i < 16; ++i) dst[i] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
     // row sum = both halves' partial sums (parity slot n&1 was last read at tile n-2)
@@ -301,7 +400,9 @@ __global__ void __launch_bounds__(320, 1)
       a.ml_part[2 * idx] = m_ref;
       a.ml_part[2 * idx + 1] = l + xmax[((n & 1) * 2 + 1) * 128 + r];
     }
+    if (tr && threadIdx.x == 64) tr[6] = globaltimer();
   }
+  if (tr && threadIdx.x == 0) tr[7] = (unsigned long long)n;
   tc_fence_before();
   __syncthreads();
   if (warp == 2) {
@@ -348,7 +449,8 @@ template <int G>
 static cudaError_t launch_attn_g(const CUtensorMap& tmQ, const CUtensorMap& tmK, const CUtensorMap& tmV,
                                  const CUtensorMap& tmK8, const CUtensorMap& tmV8, const AttnArgs& a, cudaStream_t st) {
   dim3 grid(a.n_work, a.Hkv);
-  CUDA_TRY_LAUNCH(launch_k(attn_tc_kernel<G>, dim3(grid), dim3(320), attn::kSmem, st, tmQ, tmK, tmV, tmK8, tmV8, a));
+  (void)tmQ;  // Q rows are loaded into TMEM by the softmax warps (AttnArgs::Q)
+  CUDA_TRY_LAUNCH(launch_k(attn_tc_kernel<G>, dim3(grid), dim3(320), attn::kSmem, st, tmK, tmV, tmK8, tmV8, a));
   return cudaGetLastError();
 }
 

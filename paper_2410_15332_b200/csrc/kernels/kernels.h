@@ -78,12 +78,20 @@ cudaError_t launch_kv_link(void* Kpool, void* Vpool, const int32_t* src_slot, co
 // ---- GEMM (tcgen05): P[split][M][N] = A[M][K] · B[N][K]^T --------------------------------------
 // pack > 0: B is stored pre-tiled [N/pack][K/64][pack][64] (every TMA box contiguous); the tensor map
 // is then the 2-D view [rows][64] with a (64, pack) box.  pack = 0: row-major [N][K], box (64, bn).
+extern unsigned long long* g_gemm_trace;  // bench-only GEMM timeline (gemm.cu)
+// The GEMM launched after this one (same stream): this GEMM's producer prefetches the first `pfk`
+// k-blocks of every unit of the next one into L2 once its own loads are issued.  pfk = 0: none.
+struct GemmNext {
+  const CUtensorMap* tm;
+  int units, mt, splits, kper, kblk_total, bn, pfk;
+};
+GemmNext gemm_next(const CUtensorMap* B, int M, int N, int K, int splits, int bn, int pfk);
 cudaError_t launch_gemm_partial(const CUtensorMap& A, const CUtensorMap& B, float* out, int M, int N, int K,
-                                int splits, int bn, cudaStream_t st, int pack = 0);
+                                int splits, int bn, cudaStream_t st, int pack = 0, const GemmNext& nx = GemmNext{});
 // Gate/up GEMM with the SwiGLU epilogue fused: B = interleaved [gate|up] groups of bn/2 rows (N2 = 2F rows),
 // u[M][F] bf16 = silu(x·W_gᵀ) ⊙ (x·W_uᵀ).  Split-K 1.
 cudaError_t launch_gemm_swiglu(const CUtensorMap& A, const CUtensorMap& B, void* u, int M, int N2, int K, int bn,
-                               cudaStream_t st, int pack = 0);
+                               cudaStream_t st, int pack = 0, const GemmNext& nx = GemmNext{});
 bool gemm_bn_supported(int bn, bool swiglu);
 // Interleaved gate/up generator: physical row p = n·2g + j holds gate row n·g + j (j < g) or up row
 // n·g + j − g (j >= g) of the logical [F][d] matrices (tags tag_gate / tag_up, same exponent).
@@ -101,6 +109,11 @@ struct AttnArgs {
   float scale_log2;
   float* o_part;             // [max splits][M][Hq][128]
   float* ml_part;            // [max splits][M][Hq][2]
+  unsigned long long* trace; // bench-only per-CTA timeline (globaltimer ns, 8 slots per CTA) or null
+  const void* Q;             // bf16 [M][Hq][128] queries
+  int static_plan;           // 1: work/tiles/row_pos/bt were uploaded before the launch (read before PDL wait)
+  const void* kpool;         // K/V pools (bf16 [L][NB][Hkv][16][128]) for the L2 prefetch; null: none
+  const void* vpool;
 };
 // Balanced split-KV schedule: each q-tile t (KV extent n_kv[t] 128-key tiles) gets
 // ceil(n_kv[t] / budget) splits, budget = ceil(Σ n_kv · Hkv / target_ctas); splits <= 32.

@@ -159,6 +159,7 @@ extern "C" pic_status pic_test_attention(const uint16_t* Q, const uint16_t* K, c
   a.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)D));
   a.o_part = reinterpret_cast<float*>(dop.p);
   a.ml_part = reinterpret_cast<float*>(dml.p);
+  a.Q = dq.p;
   TCK(launch_attention_tc(tq, tk, tv, tk8, tv8, a, 0));
   TCK(launch_attn_combine(a.o_part, a.ml_part, reinterpret_cast<int32_t*>(dns.p), dout.p, M, Hq, D, 0));
   TCK(cudaDeviceSynchronize());
@@ -252,14 +253,38 @@ extern "C" pic_status pic_bench_gemm(int32_t M, int32_t N, int32_t K, int32_t bn
   TCK(cudaEventCreate(&e1));
   for (int i = 0; i < 3; ++i)
     TCK(launch_gemm_partial(ta, tb[i % copies], reinterpret_cast<float*>(p.p), M, N, K, splits, bn, s, pack));
+  const int pfk = getenv("PIC_BENCH_PFK") ? atoi(getenv("PIC_BENCH_PFK")) : 0;  // next-GEMM L2 prefetch depth
   TCK(cudaEventRecord(e0, s));
   for (int i = 0; i < iters; ++i)
-    TCK(launch_gemm_partial(ta, tb[i % copies], reinterpret_cast<float*>(p.p), M, N, K, splits, bn, s, pack));
+    TCK(launch_gemm_partial(ta, tb[i % copies], reinterpret_cast<float*>(p.p), M, N, K, splits, bn, s, pack,
+                            gemm_next(pack ? nullptr : &tb[(i + 1) % copies], M, N, K, splits, bn, pfk)));
   TCK(cudaEventRecord(e1, s));
   TCK(cudaEventSynchronize(e1));
   float ms = 0;
   TCK(cudaEventElapsedTime(&ms, e0, e1));
   *us_per_launch = ms * 1000.f / iters;
+  if (getenv("PIC_GEMM_TRACE")) {  // one more pair of launches with the per-CTA timeline of the second
+    DevBuf tr;
+    TCK(cudaMalloc(&tr.p, 148 * 6 * 8));
+    TCK(cudaMemset(tr.p, 0, 148 * 6 * 8));
+    TCK(launch_gemm_partial(ta, tb[0], reinterpret_cast<float*>(p.p), M, N, K, splits, bn, s, pack));
+    g_gemm_trace = reinterpret_cast<unsigned long long*>(tr.p);
+    TCK(launch_gemm_partial(ta, tb[1 % copies], reinterpret_cast<float*>(p.p), M, N, K, splits, bn, s, pack));
+    g_gemm_trace = nullptr;
+    TCK(cudaStreamSynchronize(s));
+    std::vector<unsigned long long> t(148 * 6);
+    TCK(cudaMemcpy(t.data(), tr.p, t.size() * 8, cudaMemcpyDeviceToHost));
+    const int units = ((N + bn - 1) / bn) * ((M + 127) / 128) * splits, grid = std::min(units, 148);
+    unsigned long long t0 = ~0ull;
+    for (int b = 0; b < grid; ++b) t0 = std::min(t0, t[b * 6]);
+    const char* nm[5] = {"entry", "wait_done", "first_full", "last_mma", "epi_done"};
+    for (int k = 0; k < 5; ++k) {
+      std::vector<double> v;
+      for (int b = 0; b < grid; ++b) v.push_back((double)(t[b * 6 + k] - t0) / 1e3);
+      std::sort(v.begin(), v.end());
+      fprintf(stderr, "  %-10s min %7.2f  med %7.2f  max %7.2f us\n", nm[k], v[0], v[v.size() / 2], v.back());
+    }
+  }
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   cudaStreamDestroy(s);

@@ -11,7 +11,7 @@ from typing import List, Optional, Sequence, Tuple
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libpic.so")
+LIB_PATH = os.path.join(_HERE, os.environ.get("PIC_LIB_NAME", "libpic.so"))  # override: experiment builds only
 
 PIC_SEG_CACHED, PIC_SEG_TOKENS = 0, 1
 PIC_NAIVE, PIC_FULL, PIC_LEGOLINK, PIC_CACHEBLEND = 0, 1, 2, 3

@@ -1,0 +1,18 @@
+"""Per-CTA attention timeline of the last layer of one cfg2 link (PIC_ATTN_TRACE=1 must be set)."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import seedgen as sg
+from paper_2410_15332_b200 import pic as B
+
+w = sg.cfg2() if len(sys.argv) < 2 else getattr(sg, sys.argv[1])()
+N = sum(len(w.chunks[s.chunk]) if s.cached else len(s.tokens) for s in w.requests[0])
+eng = B.Engine(w.model, num_blocks=(sum(len(c) for c in w.chunks) + 3 * N) // 16 + 64, max_rows=4096, max_tokens=N + 16, device=0)
+ids = eng.generate_context_cache(w.chunks)
+segs = [("cached", ids[s.chunk]) if s.cached else ("tokens", s.tokens) for s in w.requests[0]]
+for i in range(3):
+    print(f"--- link {i} (graph)", file=sys.stderr, flush=True)
+    eng.link(segs, w.alg)
+print("--- eager", file=sys.stderr, flush=True)
+eng.link(segs, w.alg, use_graph=False)
