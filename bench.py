@@ -112,6 +112,12 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
+def dummy_prefix(alg):
+    """LegoLink-0 links chunks compiled behind 4 dummy BOS tokens; every other
+    algorithm uses the plain compile."""
+    return 4 if alg == "legolink0" else 0
+
+
 # ------------------------------------------------------------------------------------- CPU oracle
 class OracleSample:
     """The fp64 oracle's link on a bounded sample: layer 0 of one request (all its work: re-base of
@@ -129,7 +135,7 @@ class OracleSample:
         self.store = P.Store(self.Wt)
         over = [(np.zeros((1, len(c), cfg.n_kv_heads, cfg.head_dim)), np.zeros((1, len(c), cfg.n_kv_heads, cfg.head_dim)))
                 for c in w.chunks]
-        oids = self.store.compile(w.chunks, compiled_override=over)
+        oids = self.store.compile(w.chunks, compiled_override=over, dummy_prefix=dummy_prefix(w.alg))
         self.segs = [("cached", oids[s.chunk]) if s.cached else ("tokens", s.tokens) for s in w.requests[0]]
         self.N = sum(len(w.chunks[s.chunk]) if s.cached else len(s.tokens) for s in w.requests[0])
 
@@ -253,7 +259,7 @@ def main():
     # rows recomputed per forward: Σ k' of the batch (host-only planner), N for CacheBlend
     planner = B.Engine(m, num_blocks=(total_tokens + max_N) // 16 + 2 * len(w.chunks) + 64, max_rows=64,
                        max_tokens=max(max_N, 512) + 16, max_requests=1, device=None)
-    pids = planner.generate_context_cache(w.chunks)
+    pids = planner.generate_context_cache(w.chunks, dummy_prefix=dummy_prefix(w.alg))
     rows_link = sum(N_tok) if w.alg.startswith("cacheblend") else sum(
         len(planner.plan([("cached", pids[s.chunk]) if s.cached else ("tokens", s.tokens) for s in r], w.alg)["sel"])
         for r in w.requests)
@@ -265,7 +271,7 @@ def main():
                        max_requests=len(w.requests), device=dev, stream=stream, **tp_kw)
         if args.tp and world > 1:
             D.tp_connect(eng)
-        ids = eng.generate_context_cache(w.chunks)
+        ids = eng.generate_context_cache(w.chunks, dummy_prefix=dummy_prefix(w.alg))
         reqs = [[("cached", ids[s.chunk]) if s.cached else ("tokens", s.tokens) for s in r] for r in w.requests]
         logits_dev = torch.empty((len(reqs), m.vocab), dtype=torch.float32, device=f"cuda:{dev}")
 

@@ -86,8 +86,10 @@ typedef struct {
   const int32_t* tokens;     /* TOKENS: host array [n_tokens]; CACHED: ignored */
 } pic_segment;
 
-/* Link algorithms of P:166-170 and P:211-217 (SPEC grammar naive|fr|cacheblend:R|legolink:K). */
-typedef enum { PIC_NAIVE = 0, PIC_FULL = 1, PIC_LEGOLINK = 2, PIC_CACHEBLEND = 3 } pic_algorithm;
+/* Link algorithms of P:166-170 and P:211-217 (SPEC grammar naive|fr|cacheblend:R|legolink:K),
+ * plus LegoLink-0: Naive over chunks compiled with a dummy prefix (pic_compile_options);
+ * PIC_E_VARIANT if any linked chunk was compiled without one. */
+typedef enum { PIC_NAIVE = 0, PIC_FULL = 1, PIC_LEGOLINK = 2, PIC_CACHEBLEND = 3, PIC_LEGOLINK0 = 4 } pic_algorithm;
 
 typedef struct {
   int32_t alg;               /* pic_algorithm */
@@ -152,6 +154,20 @@ pic_status pic_tp_connect(pic_engine* eng, const void* handles, const uint64_t* 
  * chunk.  out_ids: caller array [n].  Returns after the device work completed. */
 pic_status pic_generate_context_cache(pic_engine* eng, const int32_t* const* chunks, const int32_t* lens,
                                       int32_t n, void* stream, pic_cache_id* out_ids, int32_t* err_index);
+
+/* Compile variants.  dummy_prefix = m > 0 is the LegoLink-0 compile ("prepends four dummy tokens
+ * (e.g., begin-of-sentence tokens) to each immutable chunk during compilation, then discards their
+ * corresponding KV vectors"): the chunk is prefilled as dummy^m ‖ chunk at positions 0..m+n−1 and
+ * only rows m..m+n−1 are stored (keys rotated at positions m.., so the chunk's compile base is c0 = m and
+ * a link re-bases it by Δ = s_c − m, negative for a chunk placed first; reading R21).  dummy_token < 0
+ * means cfg.bos_id.  m + n must fit max_pos and max_tokens. */
+typedef struct {
+  int32_t dummy_prefix;      /* m >= 0 (0 = the standard compile of pic_generate_context_cache) */
+  int32_t dummy_token;       /* token id of the dummies (< 0: bos_id) */
+} pic_compile_options;
+pic_status pic_generate_context_cache_ex(pic_engine* eng, const int32_t* const* chunks, const int32_t* lens,
+                                         int32_t n, const pic_compile_options* opts, void* stream,
+                                         pic_cache_id* out_ids, int32_t* err_index);
 
 /* Link step (P:162, P:185 KVLink, P:211-217 LegoLink; variants P:166-170).  Assembles the message
  * list, re-bases and gathers cached KV into fresh linked blocks, recomputes the selected rows layer

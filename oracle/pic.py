@@ -38,7 +38,7 @@ class Chunk:
     tokens: np.ndarray
     K: np.ndarray          # [L, n, H_kv, D] post-RoPE keys at positions c0..c0+n-1
     V: np.ndarray
-    c0: int = 0            # compile position of the chunk's first row (0; LegoLink-0 would use m)
+    c0: int = 0            # compile position of the chunk's first row (0; m for a LegoLink-0 compile)
 
 
 class Store:
@@ -51,22 +51,35 @@ class Store:
         self.next_id = 1
 
     def compile(self, chunk_tokens: Sequence[np.ndarray],
-                compiled_override: Optional[Sequence[Tuple[np.ndarray, np.ndarray]]] = None) -> List[int]:
+                compiled_override: Optional[Sequence[Tuple[np.ndarray, np.ndarray]]] = None,
+                dummy_prefix: int = 0) -> List[int]:
         """generate_context_cache(static_token_chunks[]) -> cache_ids (PAPER.md:391-393).
         Each chunk alone, positions 0..n−1, prefill only (no decode).  ``compiled_override``
-        supplies (K, V) computed elsewhere (the GPU) for full-depth large-shape tests."""
+        supplies (K, V) computed elsewhere (the GPU) for full-depth large-shape tests.
+
+        ``dummy_prefix`` = m > 0 is the LegoLink-0 compile ("prepends four dummy
+        tokens (e.g., begin-of-sentence tokens) to each immutable chunk during compilation, then
+        discards their corresponding KV vectors"): prefill BOS^m ‖ chunk at positions
+        0..m+n−1 and keep rows m..m+n−1, whose keys are rotated at positions m.. (c0 = m) [R21]."""
         ids = []
+        m = int(dummy_prefix)
+        if m < 0:
+            raise ValueError("negative dummy prefix")
         for i, t in enumerate(chunk_tokens):
             t = np.asarray(t, dtype=np.int32)
             if len(t) == 0:
                 raise ValueError("empty chunk")
             if compiled_override is not None:
                 K, V = compiled_override[i]
-            else:
+            elif m == 0:
                 _, K, V, _ = M.full_prefill(self.W, t)
+            else:
+                full = np.concatenate([np.full(m, self.W.cfg.bos_id, np.int32), t])
+                _, K, V, _ = M.full_prefill(self.W, full)
+                K, V = K[:, m:], V[:, m:]
             cid = self.next_id
             self.next_id += 1
-            self.chunks[cid] = Chunk(cid, t.copy(), K, V)
+            self.chunks[cid] = Chunk(cid, t.copy(), K, V, c0=m)
             ids.append(cid)
         return ids
 
@@ -137,6 +150,12 @@ def plan(store: Store, segments, alg: str) -> Plan:
         sel = set(range(N))
     elif name == "naive":
         pass                                            # PAPER.md:166 (≡ LegoLink k=0)
+    elif name == "legolink0":
+        # PAPER.md:286 "in the link step, LegoLink-0 skips recomputation entirely": Naive over
+        # chunks compiled with a dummy prefix (Δ = s_c − m, negative for a chunk placed at 0) [R21]
+        for cid, s, n, _ in chunks:
+            if store.chunks[cid].c0 <= 0:
+                raise ValueError(f"legolink0 needs chunks compiled with a dummy prefix (cache id {cid})")
     elif name == "legolink":
         k = param
         for cid, s, n, _ in chunks:

@@ -700,7 +700,7 @@ static pic_status assemble(pic_engine* e, const pic_segment* segs, int32_t n_seg
 
 static pic_status check_params(const pic_link_params* pr) {
   if (!pr) return fail(PIC_E_INVALID_ARG, "NULL params");
-  if (pr->alg < PIC_NAIVE || pr->alg > PIC_CACHEBLEND) return fail(PIC_E_INVALID_ARG, "unknown algorithm %d", pr->alg);
+  if (pr->alg < PIC_NAIVE || pr->alg > PIC_LEGOLINK0) return fail(PIC_E_INVALID_ARG, "unknown algorithm %d", pr->alg);
   if (pr->alg == PIC_LEGOLINK && pr->k < 0) return fail(PIC_E_INVALID_ARG, "LegoLink k < 0");
   if (pr->alg == PIC_CACHEBLEND && (pr->r_percent < 0 || pr->r_percent > 100))
     return fail(PIC_E_INVALID_ARG, "CacheBlend R outside [0,100]");
@@ -729,12 +729,24 @@ static void select_rows(const pic_link_params* pr, LinkPlanHost& p) {
 
 static int32_t slot_of(const std::vector<int32_t>& bt, int32_t i) { return bt[i / 16] * 16 + i % 16; }
 
+// LegoLink-0 links only chunks compiled with a dummy prefix (S:324 variant mismatch); its selection is
+// Naive's ("skips recomputation entirely").
+static pic_status check_variant(const pic_engine* e, const pic_link_params* pr, const LinkPlanHost& p) {
+  if (pr->alg != PIC_LEGOLINK0) return PIC_OK;
+  for (size_t c = 0; c < p.chunk_id.size(); ++c)
+    if (e->store.at(p.chunk_id[c]).c0 <= 0)
+      return fail(PIC_E_VARIANT, "legolink0: cache id %llu was compiled without a dummy prefix",
+                  (unsigned long long)p.chunk_id[c]);
+  return PIC_OK;
+}
+
 extern "C" pic_status pic_plan(pic_engine* e, const pic_segment* segs, int32_t n_segs, const pic_link_params* pr,
                                pic_plan_out* out) {
   if (!e || !out) return fail(PIC_E_INVALID_ARG, "NULL engine/out");
   TRY(check_params(pr));
   LinkPlanHost p;
   TRY(assemble(e, segs, n_segs, p));
+  TRY(check_variant(e, pr, p));
   select_rows(pr, p);
   const int nb = (p.N + 15) / 16;
   if (out->capacity < p.N) return fail(PIC_E_LAYOUT, "plan capacity %d < N %d", out->capacity, p.N);
@@ -1131,11 +1143,17 @@ static void add_tiles(std::vector<int32_t>& tiles, int seq, int r0, int rows, in
 static int qpt_of(const pic_model_config& c) { return 128 / (c.n_heads / c.n_kv_heads); }
 
 // ============================================================================ compile (a0)
-extern "C" pic_status pic_generate_context_cache(pic_engine* e, const int32_t* const* chunks, const int32_t* lens,
-                                                 int32_t n, void* stream, pic_cache_id* out_ids, int32_t* err_index) {
+// Compile (a0).  m > 0: LegoLink-0 compile (reading R21) — each chunk is prefilled as
+// dummy^m ‖ chunk in scratch blocks, then rows m..m+n−1 of every layer are copied into the chunk's
+// own blocks (the dummy rows are discarded) and the chunk records c0 = m.
+static pic_status compile_impl(pic_engine* e, const int32_t* const* chunks, const int32_t* lens, int32_t n, int32_t m,
+                               int32_t dummy_tok, void* stream, pic_cache_id* out_ids, int32_t* err_index) {
   if (err_index) *err_index = -1;
   if (!e || !out_ids || (n > 0 && (!chunks || !lens))) return fail(PIC_E_INVALID_ARG, "NULL argument");
   if (n <= 0) return fail(PIC_E_EMPTY_INPUT, "no chunks");
+  if (m < 0) return fail(PIC_E_INVALID_ARG, "negative dummy prefix");
+  if (dummy_tok < 0) dummy_tok = e->cfg.bos_id;
+  if (m > 0 && dummy_tok >= e->cfg.vocab) return fail(PIC_E_TOKEN, "dummy token %d out of range", dummy_tok);
   int64_t need = 0;
   for (int i = 0; i < n; ++i) {
     if (lens[i] <= 0) {
@@ -1146,24 +1164,30 @@ extern "C" pic_status pic_generate_context_cache(pic_engine* e, const int32_t* c
       if (err_index) *err_index = i;
       return fail(PIC_E_INVALID_ARG, "chunk %d is NULL", i);
     }
-    if (lens[i] > e->cfg.max_pos || lens[i] > e->lim.max_tokens) {
+    if (lens[i] + m > e->cfg.max_pos || lens[i] + m > e->lim.max_tokens) {
       if (err_index) *err_index = i;
-      return fail(PIC_E_CAPACITY, "chunk %d of %d tokens exceeds max_tokens/max_pos", i, lens[i]);
+      return fail(PIC_E_CAPACITY, "chunk %d of %d (+%d dummy) tokens exceeds max_tokens/max_pos", i, lens[i], m);
     }
     for (int j = 0; j < lens[i]; ++j)
       if (chunks[i][j] < 0 || chunks[i][j] >= e->cfg.vocab) {
         if (err_index) *err_index = i;
         return fail(PIC_E_TOKEN, "chunk %d token %d = %d out of range", i, j, chunks[i][j]);
       }
-    need += (lens[i] + 15) / 16;
+    need += (lens[i] + 15) / 16 + (m > 0 ? (lens[i] + m + 15) / 16 : 0);
   }
   if (!e->alloc.can(need)) return fail(PIC_E_CAPACITY, "pool has %zu free blocks, compile needs %lld",
                                        e->alloc.free_ids.size(), (long long)need);
-  // allocate blocks lowest-free-first in chunk order
-  std::vector<std::vector<int32_t>> blocks(n);
+  // allocate blocks lowest-free-first in chunk order (then the dummy-prefix scratch blocks)
+  std::vector<std::vector<int32_t>> blocks(n), scratch(n);
   for (int i = 0; i < n; ++i) blocks[i] = e->alloc.alloc((lens[i] + 15) / 16);
+  if (m > 0)
+    for (int i = 0; i < n; ++i) scratch[i] = e->alloc.alloc((lens[i] + m + 15) / 16);
+  auto release_scratch = [&]() {
+    for (auto& b : scratch) e->alloc.release(b);
+  };
   auto rollback = [&]() {
     for (auto& b : blocks) e->alloc.release(b);
+    release_scratch();
   };
   if (!e->host_only && e->tp_size > 1 && !e->tp_connected) {
     rollback();
@@ -1184,10 +1208,11 @@ extern "C" pic_status pic_generate_context_cache(pic_engine* e, const int32_t* c
       return s;
     };
     for (int i = 0; i < n; ++i) {
-      for (int a = 0; a < lens[i];) {
+      const std::vector<int32_t>& fb = m > 0 ? scratch[i] : blocks[i];
+      const int len = lens[i] + m;
+      for (int a = 0; a < len;) {
         const int room = e->lim.max_rows - f.M;
-        if (room <= 0 || (int)f.seq_bt_off.size() >= e->max_seqs ||
-            (int)f.bt.size() + (int)blocks[i].size() > e->max_bt) {
+        if (room <= 0 || (int)f.seq_bt_off.size() >= e->max_seqs || (int)f.bt.size() + (int)fb.size() > e->max_bt) {
           pic_status s = flush();
           if (s != PIC_OK) {
             rollback();
@@ -1195,15 +1220,15 @@ extern "C" pic_status pic_generate_context_cache(pic_engine* e, const int32_t* c
           }
           continue;
         }
-        const int take = std::min(room, lens[i] - a);
+        const int take = std::min(room, len - a);
         const int seq = (int)f.seq_bt_off.size();
         f.seq_bt_off.push_back((int)f.bt.size());
-        f.bt.insert(f.bt.end(), blocks[i].begin(), blocks[i].end());
+        f.bt.insert(f.bt.end(), fb.begin(), fb.end());
         add_tiles(f.tiles, seq, f.M, take, qpt);
         for (int j = a; j < a + take; ++j) {
-          f.tok.push_back(chunks[i][j]);
+          f.tok.push_back(j < m ? dummy_tok : chunks[i][j - m]);
           f.pos.push_back(j);                          // positions from zero
-          f.slot.push_back(slot_of(blocks[i], j));
+          f.slot.push_back(slot_of(fb, j));
           f.seq.push_back(seq);
         }
         f.M += take;
@@ -1211,6 +1236,35 @@ extern "C" pic_status pic_generate_context_cache(pic_engine* e, const int32_t* c
       }
     }
     pic_status s = flush();
+    if (s == PIC_OK && m > 0) {
+      // keep rows m..m+n−1 of every layer: the gather of a2 with Δ = 0 (no rotation)
+      std::vector<int32_t> src, dst, zero;
+      for (int i = 0; i < n; ++i)
+        for (int j = 0; j < lens[i]; ++j) {
+          src.push_back(slot_of(scratch[i], m + j));
+          dst.push_back(slot_of(blocks[i], j));
+        }
+      zero.assign(src.size(), 0);
+      std::vector<int32_t> host;
+      PlanPack pk{&host, 0, e->plan_dev};
+      const int32_t* d_src = pk.put(src);
+      const int32_t* d_dst = pk.put(dst);
+      const int32_t* d_zero = pk.put(zero);
+      if (pk.n > e->plan_cap_ints) {
+        s = fail(PIC_E_CAPACITY, "dummy-prefix copy list of %zu ints exceeds %zu", pk.n, e->plan_cap_ints);
+      } else {
+        cudaError_t ce = cudaEventSynchronize(e->plan_ev);
+        if (ce == cudaSuccess) {
+          std::memcpy(e->plan_host, host.data(), pk.n * 4);
+          ce = cudaMemcpyAsync(e->plan_dev, e->plan_host, pk.n * 4, cudaMemcpyHostToDevice, st);
+        }
+        if (ce == cudaSuccess) ce = cudaEventRecord(e->plan_ev, st);
+        if (ce == cudaSuccess)
+          ce = launch_kv_link(e->Kpool, e->Vpool, d_src, d_dst, d_zero, (int)src.size(), 0, e->cfg.n_layers,
+                              e->layer_stride, e->cfg.n_kv_heads, e->cfg.head_dim, e->cos_t, e->sin_t, 0, st, e->f32);
+        if (ce != cudaSuccess) s = fail(PIC_E_CUDA, "dummy-prefix copy: %s", cudaGetErrorString(ce));
+      }
+    }
     if (s != PIC_OK) {
       rollback();
       return s;
@@ -1221,15 +1275,29 @@ extern "C" pic_status pic_generate_context_cache(pic_engine* e, const int32_t* c
       return fail(PIC_E_CUDA, "compile: %s", cudaGetErrorString(ce));
     }
   }
+  release_scratch();
   for (int i = 0; i < n; ++i) {
     ChunkRec rec;
     rec.tokens.assign(chunks[i], chunks[i] + lens[i]);
     rec.blocks = blocks[i];
+    rec.c0 = m;
     const pic_cache_id id = e->next_id++;
     e->store.emplace(id, std::move(rec));
     out_ids[i] = id;
   }
   return PIC_OK;
+}
+
+extern "C" pic_status pic_generate_context_cache(pic_engine* e, const int32_t* const* chunks, const int32_t* lens,
+                                                 int32_t n, void* stream, pic_cache_id* out_ids, int32_t* err_index) {
+  return compile_impl(e, chunks, lens, n, 0, -1, stream, out_ids, err_index);
+}
+
+extern "C" pic_status pic_generate_context_cache_ex(pic_engine* e, const int32_t* const* chunks, const int32_t* lens,
+                                                    int32_t n, const pic_compile_options* opts, void* stream,
+                                                    pic_cache_id* out_ids, int32_t* err_index) {
+  return compile_impl(e, chunks, lens, n, opts ? opts->dummy_prefix : 0, opts ? opts->dummy_token : -1, stream,
+                      out_ids, err_index);
 }
 
 // ============================================================================ link
@@ -1297,6 +1365,7 @@ static pic_status link_impl(pic_engine* e, int32_t n_req, const pic_segment* con
   int64_t need = 0;
   for (int r = 0; r < n_req; ++r) {
     TRY(assemble(e, segs[r], n_segs[r], reqs[r].p));
+    TRY(check_variant(e, pr, reqs[r].p));
     select_rows(pr, reqs[r].p);
     need += (reqs[r].p.N + 15) / 16;
   }

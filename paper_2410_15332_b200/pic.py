@@ -14,7 +14,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, os.environ.get("PIC_LIB_NAME", "libpic.so"))  # override: experiment builds only
 
 PIC_SEG_CACHED, PIC_SEG_TOKENS = 0, 1
-PIC_NAIVE, PIC_FULL, PIC_LEGOLINK, PIC_CACHEBLEND = 0, 1, 2, 3
+PIC_NAIVE, PIC_FULL, PIC_LEGOLINK, PIC_CACHEBLEND, PIC_LEGOLINK0 = 0, 1, 2, 3, 4
 STATUS = ["PIC_OK", "PIC_E_INVALID_ARG", "PIC_E_CONFIG", "PIC_E_EMPTY_INPUT", "PIC_E_CAPACITY",
           "PIC_E_MISSING_CACHE", "PIC_E_LAYOUT", "PIC_E_VARIANT", "PIC_E_OOM", "PIC_E_CUDA",
           "PIC_E_NO_DEVICE", "PIC_E_TOKEN"]
@@ -42,6 +42,10 @@ class LimitsC(C.Structure):
 class SegmentC(C.Structure):
     _fields_ = [("kind", C.c_int32), ("n_tokens", C.c_int32), ("id", C.c_uint64),
                 ("tokens", C.POINTER(C.c_int32))]
+
+
+class CompileOptionsC(C.Structure):
+    _fields_ = [("dummy_prefix", C.c_int32), ("dummy_token", C.c_int32)]
 
 
 class LinkParamsC(C.Structure):
@@ -79,7 +83,7 @@ EXPORTS = ["pic_arena_bytes", "pic_engine_create", "pic_engine_destroy", "pic_ge
            "pic_link_batch", "pic_plan", "pic_linked_export", "pic_linked_info", "pic_linked_release",
            "pic_cache_export", "pic_cache_info", "pic_expire_cache", "pic_read_weights", "pic_get_stats",
            "pic_last_error", "pic_status_string", "pic_arena_bytes_tp", "pic_engine_create_tp", "pic_tp_ipc_handle",
-           "pic_tp_connect", "pic_set_profiling", "pic_get_profile", "pic_test_gemm", "pic_test_attention", "pic_test_kv_link", "pic_bench_gemm", "pic_bench_attention", "pic_test_gemm_swiglu"]
+           "pic_tp_connect", "pic_generate_context_cache_ex", "pic_set_profiling", "pic_get_profile", "pic_test_gemm", "pic_test_attention", "pic_test_kv_link", "pic_bench_gemm", "pic_bench_attention", "pic_test_gemm_swiglu"]
 
 _lib = None
 
@@ -106,6 +110,8 @@ def lib() -> C.CDLL:
         L.pic_engine_destroy.restype = None
         L.pic_generate_context_cache.argtypes = [C.c_void_p, P(P(C.c_int32)), P(C.c_int32), C.c_int32, C.c_void_p,
                                                  P(C.c_uint64), P(C.c_int32)]
+        L.pic_generate_context_cache_ex.argtypes = [C.c_void_p, P(P(C.c_int32)), P(C.c_int32), C.c_int32,
+                                                    P(CompileOptionsC), C.c_void_p, P(C.c_uint64), P(C.c_int32)]
         L.pic_link.argtypes = [C.c_void_p, P(SegmentC), C.c_int32, P(LinkParamsC), C.c_void_p, P(C.c_void_p),
                                P(LinkResultC)]
         L.pic_link_batch.argtypes = [C.c_void_p, C.c_int32, P(P(SegmentC)), P(C.c_int32), P(LinkParamsC), C.c_void_p,
@@ -151,7 +157,8 @@ def config_struct(cfg) -> ModelConfigC:
                         int(cfg.seed), int(getattr(cfg, "dtype", 0)))
 
 
-ALGS = {"naive": PIC_NAIVE, "fr": PIC_FULL, "legolink": PIC_LEGOLINK, "cacheblend": PIC_CACHEBLEND}
+ALGS = {"naive": PIC_NAIVE, "fr": PIC_FULL, "legolink": PIC_LEGOLINK, "cacheblend": PIC_CACHEBLEND,
+        "legolink0": PIC_LEGOLINK0}
 
 
 def parse_alg(alg: str) -> Tuple[int, int, int]:
@@ -160,6 +167,8 @@ def parse_alg(alg: str) -> Tuple[int, int, int]:
         return PIC_NAIVE, 0, 0
     if alg == "fr":
         return PIC_FULL, 0, 0
+    if alg == "legolink0":
+        return PIC_LEGOLINK0, 0, 0
     name, _, val = alg.partition(":")
     if name == "legolink":
         return PIC_LEGOLINK, int(val), 0
@@ -264,14 +273,21 @@ class Engine:
             pass
 
     # ------------------------------------------------------------------ compile
-    def generate_context_cache(self, chunks: Sequence[np.ndarray]) -> List[int]:
+    def generate_context_cache(self, chunks: Sequence[np.ndarray], dummy_prefix: int = 0,
+                               dummy_token: int = -1) -> List[int]:
+        """Compile (a0); dummy_prefix = m > 0 is the LegoLink-0 compile (pic_generate_context_cache_ex)."""
         arrs = [np.ascontiguousarray(c, dtype=np.int32) for c in chunks]
         n = len(arrs)
         ptrs = (C.POINTER(C.c_int32) * max(1, n))(*[_ptr(a) for a in arrs])
         lens = (C.c_int32 * max(1, n))(*[len(a) for a in arrs])
         ids = (C.c_uint64 * max(1, n))()
         err = C.c_int32(-1)
-        st = lib().pic_generate_context_cache(self._h, ptrs, lens, n, self._stream, ids, C.byref(err))
+        if dummy_prefix:
+            opts = CompileOptionsC(int(dummy_prefix), int(dummy_token))
+            st = lib().pic_generate_context_cache_ex(self._h, ptrs, lens, n, C.byref(opts), self._stream, ids,
+                                                     C.byref(err))
+        else:
+            st = lib().pic_generate_context_cache(self._h, ptrs, lens, n, self._stream, ids, C.byref(err))
         if st != 0:
             e = PicError(st, lib().pic_last_error().decode())
             e.err_index = err.value

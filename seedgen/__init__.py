@@ -283,9 +283,11 @@ def permuted_requests(w: Workload, n_perm: int, seed: int = 0xBADC0DE) -> List[L
 
 
 def parse_alg(alg: str) -> Tuple[str, int]:
-    """SPEC grammar: naive | fr | legolink:K | cacheblend:R  ->  (name, param)."""
+    """SPEC grammar: naive | fr | legolink:K | cacheblend:R | legolink0  ->  (name, param)."""
     if alg == "naive":
         return "naive", 0
+    if alg == "legolink0":
+        return "legolink0", 0
     if alg == "fr":
         return "fr", 0
     if alg.startswith("legolink:"):

@@ -162,3 +162,23 @@ def test_block_allocator_model_sequence():
             assert eng.expire(cid)
             alloc.release(live.pop(cid))
     assert eng.stats()["free_blocks"] == len(alloc.free)
+
+
+def test_legolink0_planner_and_variant_error():
+    """Dummy-prefix compile on a host-only engine: same blocks as a plain compile (the scratch blocks
+    are returned), Δ = s_c − m in the plan, and LegoLink-0 over a plain chunk is PIC_E_VARIANT."""
+    w = sg.cfg1()
+    eng = host_engine()
+    eids = eng.generate_context_cache(w.chunks, dummy_prefix=4)
+    st = P.Store(M.Weights(sg.TINY))
+    oids = st.compile(w.chunks, compiled_override=[(None, None)] * len(w.chunks), dummy_prefix=4)
+    assert eng.stats()["free_blocks"] == 256 - sum(P.n_blocks(len(c)) for c in w.chunks)
+    for segs in [w.requests[0]] + sg.permuted_requests(w, 20):
+        pe = eng.plan(to_engine_segs(segs, eids), "legolink0")
+        po = P.plan(st, to_engine_segs(segs, oids), "legolink0")
+        assert np.array_equal(pe["sel"], po.sel)
+        assert pe["chunks"].tolist() == [[s, n, dl] for _, s, n, dl in po.chunks]
+    plain = eng.generate_context_cache([w.chunks[0]])
+    with pytest.raises(B.PicError) as e:
+        eng.plan([("cached", plain[0]), ("cached", eids[1])], "legolink0")
+    assert e.value.name == "PIC_E_VARIANT"

@@ -393,3 +393,47 @@ def test_allocator_and_slot_map():
     with pytest.raises(MemoryError):
         a.alloc(10)
     assert P.slot_map([7, 2], [0, 15, 16, 31]).tolist() == [112, 127, 32, 47]
+
+
+def test_C14_legolink0_after_literal_dummies_equals_prefill(tiny):
+    """LegoLink-0: a chunk compiled behind m dummy tokens, linked right after m literal
+    dummies, lands at Δ = s_c − m = 0 and needs no recomputation — the result is exactly an ordinary
+    prefill of dummy^m ‖ chunk (the compile's own computation seen from the link side)."""
+    cfg, w, Wt, *_ = tiny
+    m = 4
+    store = P.Store(Wt)
+    chunk = w.chunks[1]
+    (cid,) = store.compile([chunk], dummy_prefix=m)
+    assert store.chunks[cid].c0 == m and store.chunks[cid].K.shape[1] == len(chunk)
+    bos = np.full(m, cfg.bos_id, np.int32)
+    r = P.link(store, [("tokens", bos), ("cached", cid)], "legolink0")
+    logits, K, V, _ = M.full_prefill(Wt, np.concatenate([bos, chunk]))
+    assert r.plan.chunks[0][3] == 0
+    assert r.plan.sel.tolist() == list(range(m)) + [m + len(chunk) - 1]
+    assert rel(r.logits, logits) < 1e-12
+    assert rel(r.K, K) < 1e-12 and rel(r.V, V) < 1e-12
+
+
+def test_C15_legolink0_variant_check_and_negative_delta(tiny):
+    """S:324 variant mismatch; Δ = s_c − m (negative for the chunk placed first, R21) is undone by R(+m)."""
+    cfg, w, Wt, *_ = tiny
+    m = 4
+    store = P.Store(Wt)
+    plain = store.compile([w.chunks[0]])
+    dummy = store.compile(w.chunks, dummy_prefix=m)
+    # the dummies change what the chunk's KV encodes (attention sink removed in advance, P:286)
+    assert rel(store.chunks[dummy[0]].K, store.chunks[plain[0]].K) > 1e-3
+    with pytest.raises(ValueError):
+        P.plan(store, [("cached", plain[0]), ("cached", dummy[1])], "legolink0")
+    segs = [("cached", c) for c in dummy] + [("tokens", w.requests[0][-1].tokens)]
+    r = P.link(store, segs, "legolink0")
+    nv = P.plan(store, segs, "naive")
+    assert np.array_equal(r.plan.sel, nv.sel)                          # "skips recomputation entirely"
+    assert [d for *_, d in r.plan.chunks] == [s - m for _, s, _, _ in r.plan.chunks]
+    assert r.plan.chunks[0][3] == -m
+    c = store.chunks[dummy[0]]
+    n = len(c.tokens)
+    for l in range(cfg.n_layers):
+        back = P.rebase(r.K[l, :n], m, cfg.head_dim, cfg.rope_theta)
+        assert rel(back, c.K[l]) < 1e-12
+        assert np.array_equal(r.V[l, :n], c.V[l])
