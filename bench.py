@@ -204,6 +204,8 @@ def main():
                     help="tensor parallel over all ranks (heads/MLP columns sharded, fused peer-memory all-reduce); "
                          "strong scaling of one request instead of data parallel requests")
     ap.add_argument("--layers", type=int, default=None, help="truncate depth (functional runs only; marked in config)")
+    ap.add_argument("--decode-steps", type=int, default=32,
+                    help="f1: decode steps over the linked caches after the link measurement (0 = skip)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -267,7 +269,7 @@ def main():
     with torch.cuda.stream(stream):
         tp_kw = dict(tp_rank=rank, tp_size=world) if args.tp else {}
         eng = B.Engine(m, num_blocks=(total_tokens + sum(N_tok)) // 16 + 2 * len(w.chunks) + 64 * len(w.requests),
-                       max_rows=max(4096, rows_link), max_tokens=max(max_N, 512) + 16,
+                       max_rows=max(4096, rows_link), max_tokens=max(max_N + 2 * args.decode_steps + 16, 512) + 16,
                        max_requests=len(w.requests), device=dev, stream=stream, **tp_kw)
         if args.tp and world > 1:
             D.tp_connect(eng)
@@ -322,6 +324,41 @@ def main():
         wall_max = D.max_over_ranks(wall, device=red_dev)
         e2e_value = tokens_all / wall_max
 
+        # ---------------- f1: decode over the linked caches (TPOT); batch = this rank's requests
+        dec = None
+        if args.decode_steps > 0 and not args.tp:
+            held = (eng.link_batch(reqs, w.alg, keep_linked=True) if len(reqs) > 1
+                    else [eng.link(reqs[0], w.alg, keep_linked=True)])
+            hs = [o.linked for o in held]
+            forced = [int(t) for t in sg.tokens(0xDEC0DE, 7, len(hs), m.vocab, None)]
+            dl = torch.empty((len(hs), m.vocab), dtype=torch.float32, device=f"cuda:{dev}")
+            for _ in range(3):
+                eng.decode(hs, forced, want_logits=False, logits_dev=dl.data_ptr())
+            dec_launches = eng.stats()["kernels_last_call"]
+            barrier()
+            torch.cuda.synchronize(dev)
+            d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            d0.record(stream)
+            for _ in range(args.decode_steps):                    # teacher-forced: no host round trip
+                eng.decode(hs, forced, want_logits=False, logits_dev=dl.data_ptr())
+            d1.record(stream)
+            d1.synchronize()
+            barrier()
+            tpot = D.max_over_ranks(d0.elapsed_time(d1), device=red_dev) / args.decode_steps
+            t0 = time.perf_counter()
+            toks = forced
+            for _ in range(args.decode_steps // 2):               # greedy through the public call
+                toks = [int(t) for t in eng.decode(hs, toks, want_logits=False).next_token]
+            tpot_host = (time.perf_counter() - t0) / max(1, args.decode_steps // 2) * 1e3
+            batch_all = D.sum_over_ranks(len(hs), device=red_dev)
+            dec = {"tpot_ms": tpot, "tokens_per_s": batch_all / (tpot / 1e3), "batch_per_gpu": len(hs),
+                   "context_tokens": int(max_N), "steps": args.decode_steps, "tpot_ms_host_greedy": tpot_host,
+                   "gpu_launches_per_step": int(dec_launches),
+                   "how": "pic_decode over the linked caches of this rank's requests (f1), one token per cache per "
+                          "step, CUDA events on the bench stream (teacher-forced), then a greedy host loop"}
+            for h in hs:
+                eng.release(h)
+
         # ---------------- per-kernel CUDA-event profile (separate pass, same stream)
         eng.set_profiling(True)
         eng.profile(reset=True)
@@ -349,7 +386,7 @@ def main():
             "e2e": {"value": e2e_value, "unit": "tokens/s", "ttft_ms_host": wall_max / args.steps * 1e3,
                     "h2d_bytes_per_step": int(st["h2d_bytes_last_call"]),
                     "d2h_bytes_per_step": int(st["d2h_bytes_last_call"])},
-            "roofline": roof, "kernel_breakdown": breakdown,
+            "roofline": roof, "kernel_breakdown": breakdown, "decode": dec,
             "context": "paper (A100-80GB, vLLM 0.4.1): LegoLink-16 up to 8x lower TTFT and 7x throughput vs "
                        "CacheBlend-15 under load (P:303-305); not comparable hardware/workload"}
     if world == 1 and not args.no_cpu_baseline:

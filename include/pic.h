@@ -207,7 +207,29 @@ pic_status pic_linked_export(pic_engine* eng, const pic_linked* linked, int32_t 
 pic_status pic_linked_info(pic_engine* eng, const pic_linked* linked, int32_t* n_tokens, int32_t* block_table);
 pic_status pic_linked_release(pic_engine* eng, pic_linked* linked);
 
-/* Copy layer `layer` of a compiled chunk to host: [n][H_kv][D] bf16 each (post-RoPE K at positions 0..n-1). */
+/* Decode over linked caches ("proceeds to the decode stage"): one step
+ * for a batch of n live linked caches (distinct handles from pic_link(_batch) with out_linked).  Cache b
+ * of current length N_b gets tokens[b] appended at position N_b: the model runs on that single row
+ * (the same projections, RMSNorm/SwiGLU and sparse-query attention kernels as the link, at M = n),
+ * attending to keys 0..N_b, its K/V is written into the cache (which grows to N_b + 1; a fresh block
+ * is taken from the pool when N_b is a multiple of 16) and its next-token logits are produced.
+ * Greedy decoding feeds results[b].next_token back as the next step's token.
+ *   results: caller array [n]; per entry logits (host [vocab], nullable), logits_dev (device [vocab],
+ *   nullable), next_token (argmax, ties -> lowest id; -1 unless a host output was requested or both
+ *   logits pointers are NULL), n_tokens (length after the step).
+ * Errors: PIC_E_CAPACITY (n > max_requests, N_b + 1 > max_pos / max_tokens, pool exhausted),
+ * PIC_E_TOKEN, PIC_E_INVALID_ARG (NULL / repeated handle).  On error no cache changed. */
+typedef struct {
+  float* logits;
+  float* logits_dev;
+  int32_t next_token;
+  int32_t n_tokens;
+} pic_decode_result;
+pic_status pic_decode(pic_engine* eng, pic_linked* const* linked, const int32_t* tokens, int32_t n, int32_t use_graph,
+                      void* stream, pic_decode_result* results);
+
+/* Copy layer `layer` of a compiled chunk to host: [n][H_kv][D] bf16 each (post-RoPE K at positions c0..c0+n-1;
+ * c0 = 0, or the dummy-prefix length of a LegoLink-0 compile). */
 pic_status pic_cache_export(pic_engine* eng, pic_cache_id id, int32_t layer, void* k_host, void* v_host);
 /* Length and block list (int32[ceil(n/16)], nullable) of a compiled chunk. */
 pic_status pic_cache_info(pic_engine* eng, pic_cache_id id, int32_t* n_tokens, int32_t* blocks);

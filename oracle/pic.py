@@ -296,3 +296,22 @@ def slot_map(block_table: Sequence[int], rows: Sequence[int]) -> np.ndarray:
     bt = np.asarray(block_table, dtype=np.int64)
     r = np.asarray(rows, dtype=np.int64)
     return (bt[r // BLOCK] * BLOCK + r % BLOCK).astype(np.int32)
+
+
+# ----------------------------------------------------------------------------
+# decode over the linked cache
+# ----------------------------------------------------------------------------
+def decode(W: M.Weights, K: np.ndarray, V: np.ndarray, token: int):
+    """One decode step (PAPER.md:141 "proceeds to the decode stage", :185): the new token at position
+    N = len(K[0]) attends to keys 0..N — the linked cache plus its own K/V, which are appended
+    (PAPER.md:217 causal mask).  K, V: [L, N, H_kv, D].  Returns (logits, K', V') with N + 1 rows."""
+    cfg = W.cfg
+    L, N = K.shape[0], K.shape[1]
+    pad = np.zeros((L, 1) + K.shape[2:])
+    K2 = np.concatenate([K, pad], axis=1)
+    V2 = np.concatenate([V, pad], axis=1)
+    h = W.embed_rows(np.asarray([token], dtype=np.int32))
+    row = np.asarray([N])
+    for l in range(L):
+        h = M.layer_rows(W.layer(l), cfg, h, row, row, K2[l], V2[l])
+    return M.logits_of(W, h[-1]), K2, V2

@@ -1512,6 +1512,97 @@ static pic_status link_impl(pic_engine* e, int32_t n_req, const pic_segment* con
   return PIC_OK;
 }
 
+// ============================================================================ decode (f1)
+extern "C" pic_status pic_decode(pic_engine* e, pic_linked* const* linked, const int32_t* tokens, int32_t n,
+                                 int32_t use_graph, void* stream, pic_decode_result* results) {
+  if (!e || !linked || !tokens || !results) return fail(PIC_E_INVALID_ARG, "NULL argument");
+  if (n <= 0) return fail(PIC_E_EMPTY_INPUT, "no sequences");
+  if (n > e->lim.max_requests) return fail(PIC_E_CAPACITY, "%d sequences exceed max_requests", n);
+  if (e->host_only) return fail(PIC_E_NO_DEVICE, "host-only engine cannot decode");
+  if (e->tp_size > 1 && !e->tp_connected) return fail(PIC_E_INVALID_ARG, "tensor-parallel engine: call pic_tp_connect first");
+  int64_t need = 0;
+  for (int b = 0; b < n; ++b) {
+    if (!linked[b]) return fail(PIC_E_INVALID_ARG, "linked[%d] is NULL", b);
+    for (int c = 0; c < b; ++c)
+      if (linked[c] == linked[b]) return fail(PIC_E_INVALID_ARG, "linked[%d] repeats linked[%d]", b, c);
+    if (tokens[b] < 0 || tokens[b] >= e->cfg.vocab) return fail(PIC_E_TOKEN, "token %d = %d out of range", b, tokens[b]);
+    const int N = linked[b]->n_tokens;
+    if (N + 1 > e->cfg.max_pos || N + 1 > e->lim.max_tokens)
+      return fail(PIC_E_CAPACITY, "sequence %d: %d + 1 tokens exceed max_pos / max_tokens", b, N);
+    if (N % 16 == 0) ++need;
+  }
+  if (!e->alloc.can(need)) return fail(PIC_E_CAPACITY, "pool has %zu free blocks, decode needs %lld",
+                                       e->alloc.free_ids.size(), (long long)need);
+  std::vector<int32_t> grown(n, -1);
+  for (int b = 0; b < n; ++b)
+    if (linked[b]->n_tokens % 16 == 0) {
+      grown[b] = e->alloc.alloc(1)[0];
+      linked[b]->blocks.push_back(grown[b]);
+    }
+  auto rollback = [&]() {
+    for (int b = 0; b < n; ++b)
+      if (grown[b] >= 0) {
+        linked[b]->blocks.pop_back();
+        e->alloc.release({grown[b]});
+      }
+  };
+  // one row per sequence: position N_b, K/V slot N_b of its own block table
+  Fwd f;
+  f.n_head = n;
+  const int qpt = qpt_of(e->cfg);
+  for (int b = 0; b < n; ++b) {
+    const pic_linked& h = *linked[b];
+    f.seq_bt_off.push_back((int)f.bt.size());
+    f.bt.insert(f.bt.end(), h.blocks.begin(), h.blocks.end());
+    add_tiles(f.tiles, b, b, 1, qpt);
+    f.tok.push_back(tokens[b]);
+    f.pos.push_back(h.n_tokens);
+    f.slot.push_back(slot_of(h.blocks, h.n_tokens));
+    f.seq.push_back(b);
+    f.head_map.push_back(b);
+  }
+  f.M = n;
+  f.debug_rows = 1;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  schedule_attention(e, f);
+  pic_status s = run_forward(e, f, st, use_graph != 0, nullptr);
+  if (s != PIC_OK) {
+    rollback();
+    return s;
+  }
+  const int V = e->cfg.vocab;
+  bool want_host = false;
+  cudaError_t ce = cudaSuccess;
+  for (int b = 0; b < n && ce == cudaSuccess; ++b) {
+    if (results[b].logits_dev)
+      ce = cudaMemcpyAsync(results[b].logits_dev, e->logits + (size_t)b * V, (size_t)V * 4, cudaMemcpyDeviceToDevice, st);
+    if (results[b].logits || !results[b].logits_dev) want_host = true;
+  }
+  e->d2h_last = 0;
+  if (ce == cudaSuccess && want_host) {
+    bool any_logits = false;
+    for (int b = 0; b < n; ++b) any_logits |= results[b].logits != nullptr;
+    if (any_logits) {
+      ce = cudaMemcpyAsync(e->host_logits, e->logits, (size_t)n * V * 4, cudaMemcpyDeviceToHost, st);
+      e->d2h_last += (int64_t)n * V * 4;
+    }
+    if (ce == cudaSuccess) ce = cudaMemcpyAsync(e->host_amax, e->amax, (size_t)n * 4, cudaMemcpyDeviceToHost, st);
+    e->d2h_last += (int64_t)n * 4;
+    if (ce == cudaSuccess) ce = cudaStreamSynchronize(st);
+  }
+  if (ce != cudaSuccess) {
+    rollback();
+    return fail(PIC_E_CUDA, "decode: %s", cudaGetErrorString(ce));
+  }
+  for (int b = 0; b < n; ++b) {
+    linked[b]->n_tokens += 1;
+    results[b].n_tokens = linked[b]->n_tokens;
+    results[b].next_token = want_host ? e->host_amax[b] : -1;
+    if (results[b].logits) std::memcpy(results[b].logits, e->host_logits + (size_t)b * V, (size_t)V * 4);
+  }
+  return PIC_OK;
+}
+
 extern "C" pic_status pic_link(pic_engine* e, const pic_segment* segs, int32_t n_segs, const pic_link_params* params,
                                void* stream, pic_linked** out_linked, pic_link_result* result) {
   const pic_status st = link_impl(e, 1, &segs, &n_segs, params, stream, out_linked, result);

@@ -67,6 +67,11 @@ class PlanOutC(C.Structure):
                 ("block_table", C.POINTER(C.c_int32)), ("slot", C.POINTER(C.c_int32))]
 
 
+class DecodeResultC(C.Structure):
+    _fields_ = [("logits", C.POINTER(C.c_float)), ("logits_dev", C.POINTER(C.c_float)), ("next_token", C.c_int32),
+                ("n_tokens", C.c_int32)]
+
+
 class StatsC(C.Structure):
     _fields_ = [("free_blocks", C.c_int64), ("total_blocks", C.c_int64), ("n_cached_chunks", C.c_int64),
                 ("kernels_last_call", C.c_int64), ("graphs_cached", C.c_int64),
@@ -83,7 +88,7 @@ EXPORTS = ["pic_arena_bytes", "pic_engine_create", "pic_engine_destroy", "pic_ge
            "pic_link_batch", "pic_plan", "pic_linked_export", "pic_linked_info", "pic_linked_release",
            "pic_cache_export", "pic_cache_info", "pic_expire_cache", "pic_read_weights", "pic_get_stats",
            "pic_last_error", "pic_status_string", "pic_arena_bytes_tp", "pic_engine_create_tp", "pic_tp_ipc_handle",
-           "pic_tp_connect", "pic_generate_context_cache_ex", "pic_set_profiling", "pic_get_profile", "pic_test_gemm", "pic_test_attention", "pic_test_kv_link", "pic_bench_gemm", "pic_bench_attention", "pic_test_gemm_swiglu"]
+           "pic_tp_connect", "pic_generate_context_cache_ex", "pic_decode", "pic_set_profiling", "pic_get_profile", "pic_test_gemm", "pic_test_attention", "pic_test_kv_link", "pic_bench_gemm", "pic_bench_attention", "pic_test_gemm_swiglu"]
 
 _lib = None
 
@@ -112,6 +117,8 @@ def lib() -> C.CDLL:
                                                  P(C.c_uint64), P(C.c_int32)]
         L.pic_generate_context_cache_ex.argtypes = [C.c_void_p, P(P(C.c_int32)), P(C.c_int32), C.c_int32,
                                                     P(CompileOptionsC), C.c_void_p, P(C.c_uint64), P(C.c_int32)]
+        L.pic_decode.argtypes = [C.c_void_p, C.c_void_p, P(C.c_int32), C.c_int32, C.c_int32, C.c_void_p,
+                                 P(DecodeResultC)]
         L.pic_link.argtypes = [C.c_void_p, P(SegmentC), C.c_int32, P(LinkParamsC), C.c_void_p, P(C.c_void_p),
                                P(LinkResultC)]
         L.pic_link_batch.argtypes = [C.c_void_p, C.c_int32, P(P(SegmentC)), P(C.c_int32), P(LinkParamsC), C.c_void_p,
@@ -205,6 +212,13 @@ class LinkOutput:
     linked: Optional[int] = None          # opaque pic_linked* (release with Engine.release)
     selected: Optional[np.ndarray] = None # linked indices recomputed in the last layer
     hidden: Optional[np.ndarray] = None   # debug hidden [L][N][d]
+
+
+@dataclass
+class DecodeOutput:
+    logits: Optional[np.ndarray]          # [n][vocab] fp32 (None unless requested)
+    next_token: np.ndarray                # argmax per sequence (-1 without host output)
+    n_tokens: np.ndarray                  # cache lengths after the step
 
 
 def bf16_bits_to_f32(b: np.ndarray) -> np.ndarray:
@@ -354,6 +368,26 @@ class Engine:
         return [LinkOutput(None if logits is None else logits[i], res[i].first_token, res[i].n_tokens,
                            res[i].n_selected, res[i].n_selected_layer0, linked[i] if keep_linked else None)
                 for i in range(n)]
+
+    def decode(self, linked: Sequence[int], tokens: Sequence[int], *, use_graph: bool = True,
+               want_logits: bool = True, logits_dev=None) -> "DecodeOutput":
+        """One decode step over live linked caches (pic_decode): tokens[b] is appended to linked[b].
+        logits_dev: optional device pointer (int) of an fp32 [n][vocab] buffer filled on the stream."""
+        n = len(linked)
+        hs = (C.c_void_p * n)(*[int(h) for h in linked])
+        toks = (C.c_int32 * n)(*[int(t) for t in tokens])
+        res = (DecodeResultC * n)()
+        logits = None
+        if want_logits:
+            logits = np.empty((n, self.cfg.vocab), dtype=np.float32)
+            for i in range(n):
+                res[i].logits = logits[i].ctypes.data_as(C.POINTER(C.c_float))
+        if logits_dev is not None:
+            for i in range(n):
+                res[i].logits_dev = C.cast(C.c_void_p(int(logits_dev) + 4 * i * self.cfg.vocab), C.POINTER(C.c_float))
+        check(lib().pic_decode(self._h, hs, toks, n, int(use_graph), self._stream, res))
+        return DecodeOutput(logits, np.array([res[i].next_token for i in range(n)], dtype=np.int64),
+                            np.array([res[i].n_tokens for i in range(n)], dtype=np.int64))
 
     def plan(self, segments, alg: str) -> dict:
         segs = _Segs(segments)

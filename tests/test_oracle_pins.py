@@ -437,3 +437,31 @@ def test_C15_legolink0_variant_check_and_negative_delta(tiny):
         back = P.rebase(r.K[l, :n], m, cfg.head_dim, cfg.rope_theta)
         assert rel(back, c.K[l]) < 1e-12
         assert np.array_equal(r.V[l, :n], c.V[l])
+
+
+def test_C16_decode_after_fr_equals_prefill_of_extended_prompt(tiny):
+    """Decode (f1): FR link of the prompt, then two decode steps, equals an ordinary prefill of
+    prompt ‖ t1 ‖ t2 (logits of the last row and every K/V row)."""
+    cfg, w, Wt, store, ids, segs, tok, _ = tiny
+    r = P.link(store, segs, "fr")
+    t1, t2 = 17, 201
+    lg1, K, V = P.decode(Wt, r.K, r.V, t1)
+    lg2, K, V = P.decode(Wt, K, V, t2)
+    ref1 = M.full_prefill(Wt, np.concatenate([tok, [t1]]))
+    ref2 = M.full_prefill(Wt, np.concatenate([tok, [t1, t2]]))
+    assert rel(lg1, ref1[0]) < 1e-12 and rel(lg2, ref2[0]) < 1e-12
+    assert rel(K, ref2[1]) < 1e-12 and rel(V, ref2[2]) < 1e-12
+
+
+def test_C17_decode_equals_link_with_the_token_as_literal(tiny):
+    """For Naive / LegoLink requests that end with literal tokens, decoding t after the link equals
+    linking the same message list with t appended as one more literal token (the new row is dynamic,
+    every earlier row is computed exactly as before)."""
+    cfg, w, Wt, store, ids, segs, tok, _ = tiny
+    for alg in ("naive", "legolink:4"):
+        r = P.link(store, segs, alg)
+        lg, K, V = P.decode(Wt, r.K, r.V, 99)
+        q = np.concatenate([segs[-1][1], [99]]).astype(np.int32)
+        r2 = P.link(store, segs[:-1] + [("tokens", q)], alg)
+        assert rel(lg, r2.logits) < 1e-12, alg
+        assert rel(K, r2.K) < 1e-12 and rel(V, r2.V) < 1e-12, alg
