@@ -124,6 +124,41 @@ static void attn_trace_print(int n_cta) {
   }
 }
 
+// Bench-only chain timeline (PIC_CHAIN_TRACE=1): per layer and CTA: entry, per phase boundary
+// (epilogue done, barrier passed), exit.  pic_link prints the middle layer.
+static unsigned long long* chain_trace_buffer() {
+  static unsigned long long* buf = nullptr;
+  static const bool on = getenv("PIC_CHAIN_TRACE") != nullptr;
+  if (on && !buf && cudaMalloc(&buf, (size_t)16 * 148 * 128 * sizeof(unsigned long long)) != cudaSuccess) buf = nullptr;
+  return on ? buf : nullptr;
+}
+static void chain_trace_dump(int layer) {
+  unsigned long long* buf = chain_trace_buffer();
+  if (!buf) return;
+  std::vector<unsigned long long> t(16 * 148);
+  if (cudaMemcpy(t.data(), buf + (size_t)layer * 16 * 148, t.size() * 8, cudaMemcpyDeviceToHost) != cudaSuccess) return;
+  unsigned long long t0 = ~0ull;
+  for (int c = 0; c < 148; ++c)
+    if (t[16 * c]) t0 = std::min(t0, t[16 * c]);
+  for (int k = 0; k < 16; ++k) {
+    std::vector<double> v;
+    for (int c = 0; c < 148; ++c)
+      if (t[16 * c + k] >= t0 && t[16 * c + k]) v.push_back((double)(t[16 * c + k] - t0) / 1e3);
+    if (v.empty()) continue;
+    std::sort(v.begin(), v.end());
+    fprintf(stderr, "  chain L%d slot %2d min %7.2f  med %7.2f  max %7.2f us (n=%zu)\n", layer, k, v[0], v[v.size() / 2],
+            v.back(), v.size());
+  }
+}
+
+// The persistent GEMM chain is opt-in (PIC_CHAIN=1): measured on cfg2 it streams each phase at the
+// same rate as the separate kernels, and its norm phases and grid barriers add ~18 µs per layer
+// (4.77 vs 4.28 ms per link), so the separate PDL-chained kernels remain the default.
+static bool chain_enabled() {
+  static const bool on = getenv("PIC_CHAIN") != nullptr;
+  return on;
+}
+
 static bool ablated(const char* name) {
   static const int mask = getenv("PIC_ABLATE") ? atoi(getenv("PIC_ABLATE")) : 0;
   if (!mask) return false;
@@ -266,7 +301,7 @@ static ArenaPlan plan_arena(const pic_model_config& c, const pic_engine_limits& 
   a.off_plan = L.add(a.plan_ints * 4);
   // tensor parallel: two reduced-partial buffers (alternating per all-reduce), flags, epoch counter
   a.off_ar = L.add(2 * M * d * 4);
-  a.off_tpflags = L.add(8 * 8 + 8);
+  a.off_tpflags = L.add(8 * 8 + 8 + 16);  // TP epoch flags + counter, then the GEMM-chain barrier counters
   a.total = L.total + 1024;
   return a;
 }
@@ -503,7 +538,8 @@ static pic_status init_device(pic_engine* e, void* arena, size_t bytes, cudaStre
   e->ar_buf[1] = e->ar_buf[0] + (size_t)M * d;
   e->tp_flags = reinterpret_cast<long long*>(b + a.off_tpflags);
   e->tp_counter = e->tp_flags + 8;
-  CK(cudaMemsetAsync(e->tp_flags, 0, 9 * 8, st));
+  e->chain_bar = reinterpret_cast<unsigned*>(e->tp_flags + 9);
+  CK(cudaMemsetAsync(e->tp_flags, 0, 9 * 8 + 16, st));
   for (int r = 0; r < 8; ++r) {
     e->peer_flags.p[r] = nullptr;
     e->peer_ar[0][r] = e->peer_ar[1][r] = nullptr;
@@ -888,15 +924,26 @@ static pic_status enqueue_forward(pic_engine* e, const Fwd& f, const DevPlan& dp
                        st));
     return PIC_OK;
   };
+  // Persistent GEMM chain (gemm_chain.cu) for the weight-streaming regime: one launch per layer runs
+  // O-proj, residual+RMSNorm, gate/up+SwiGLU, down, residual+RMSNorm and the next layer's QKV.
+  const bool use_chain = chain_enabled() && !e->f32 && e->tp_size == 1 && !f.cb && e->gu_group > 0 && f.M <= 128 &&
+                         f.M > 0;
+  bool qkv_done = false;  // this layer's QKV partials were produced by the previous layer's chain
+  int s_chain_qkv = 0;
   for (int l = 0; l < L; ++l) {
     const LayerW& w = e->layers[l];
     char* Kl = Kp + l * lbytes;
     char* Vl = Vp + l * lbytes;
     int s = 0;
-    ++R.launches;
-    TRY(add_norm(prevP, prev_s, w.g1, e->x, nullptr, M, (double)M * d * 2));
-    if (l > 0) TRY(capture(l - 1));
-    TRY(R.gemm(e->tm_x, w.tm_qkv, M, qkv, d, &s, e->x, w.qkv));
+    if (qkv_done) {
+      s = s_chain_qkv;
+      qkv_done = false;
+    } else {
+      ++R.launches;
+      TRY(add_norm(prevP, prev_s, w.g1, e->x, nullptr, M, (double)M * d * 2));
+      if (l > 0) TRY(capture(l - 1));
+      TRY(R.gemm(e->tm_x, w.tm_qkv, M, qkv, d, &s, e->x, w.qkv));
+    }
     if (f.cb && l == f.cb_layer) {
       // a9: CacheBlend selection at the check layer (P:170 steps 3-4)
       if (!f.cb_override) {
@@ -976,6 +1023,68 @@ static pic_status enqueue_forward(pic_engine* e, const Fwd& f, const DevPlan& dp
       ++R.launches;
       PROF("attention", attn_bytes, attn_flops, launch_attention_simt(e->Q, Kl, Vl, dp.seq, dp.seq_bt_off, dp.bt, pos, e->Obuf, M, Hq, Hkv, D,
                                (float)(1.0 / std::sqrt((double)D)), st, e->f32));
+    }
+    if (use_chain) {
+      ChainParams cp{};
+      const CUtensorMap* maps[kMaxChainMaps];
+      int nm = 0;
+      double bytes = 0, flops = 0;
+      auto gemm_phase = [&](int type, const CUtensorMap* A, const CUtensorMap* B, int N, int K, void* out) -> int {
+        ChainPhase& ph = cp.ph[cp.n_phases++];
+        ph.type = type;
+        ph.M = M;
+        ph.N = N;
+        ph.kblk = K / 64;
+        ph.bn = type == CHAIN_SWIGLU ? 2 * e->gu_group : 128;
+        const int tiles = (N + ph.bn - 1) / ph.bn;
+        ph.splits = type == CHAIN_SWIGLU ? 1 : std::max(1, std::min(148 / tiles, ph.kblk / 4));
+        while (ph.splits > 1 && (size_t)ph.splits * M * N > e->ws_floats) --ph.splits;
+        ph.kper = (ph.kblk + ph.splits - 1) / ph.splits;
+        ph.a = nm;
+        maps[nm++] = A;
+        ph.b = nm;
+        maps[nm++] = B;
+        ph.out = out;
+        bytes += (double)N * K * 2 + (double)M * K * 2 + (double)M * N * (type == CHAIN_SWIGLU ? 1 : 4 * ph.splits);
+        flops += 2.0 * M * N * K;
+        return ph.splits;
+      };
+      auto norm_phase = [&](int splits, const float* g) {
+        ChainPhase& ph = cp.ph[cp.n_phases++];
+        ph.type = CHAIN_NORM;
+        ph.M = M;
+        ph.N = d;
+        ph.bn = 128;
+        ph.splits = splits;
+        ph.P = e->ws;
+        ph.g = g;
+        ph.h = hc;
+        ph.out = e->x;
+        ph.eps = eps;
+        bytes += (double)M * d * (8 + 4 * splits + 2);
+      };
+      const int s_o = gemm_phase(CHAIN_GEMM, &e->tm_O, &w.tm_o[bn_index(128)], d, Hq * D, e->ws);
+      norm_phase(s_o, w.g2);
+      gemm_phase(CHAIN_SWIGLU, &e->tm_x, &w.tm_gu_fused, 2 * F, d, e->u);
+      const int s_dn = gemm_phase(CHAIN_GEMM, &e->tm_u, &w.tm_down[bn_index(128)], d, F, e->ws);
+      const bool next = l + 1 < L;
+      if (next) {
+        const LayerW& wn = e->layers[l + 1];
+        norm_phase(s_dn, wn.g1);
+        s_chain_qkv = gemm_phase(CHAIN_GEMM, &e->tm_x, &wn.tm_qkv[bn_index(128)], qkv, d, e->ws);
+        qkv_done = true;
+      }
+      cp.bar = e->chain_bar;
+      cp.trace = chain_trace_buffer() ? chain_trace_buffer() + (size_t)l * 16 * 148 : nullptr;
+      ++R.launches;
+      PROF("gemm", bytes, flops, launch_gemm_chain(maps, nm, cp, st));
+      if (next) {
+        TRY(capture(l));  // h after layer l (written by the chain's second norm phase)
+      } else {
+        prevP = e->ws;
+        prev_s = s_dn;
+      }
+      continue;
     }
     // a7 O projection, residual + a8 MLP
     TRY(R.gemm(e->tm_O, w.tm_o, M, d, Hq * D, &s, e->Obuf, w.o));
@@ -1101,6 +1210,8 @@ static pic_status run_forward(pic_engine* e, const Fwd& f, cudaStream_t st, bool
     e->kernels_last = nl;
     return PIC_OK;
   }
+  (void)chain_trace_buffer();  // bench-only trace buffers are allocated outside any capture
+  (void)attn_trace_buffer();
   std::vector<int64_t> sig;
   add_sig(sig, f, dp);
   auto it = e->graphs.find(sig);
@@ -1609,6 +1720,10 @@ extern "C" pic_status pic_link(pic_engine* e, const pic_segment* segs, int32_t n
   if (st == PIC_OK && attn_trace_buffer()) {
     cudaStreamSynchronize(reinterpret_cast<cudaStream_t>(stream));
     attn_trace_print(g_attn_trace_ctas);
+  }
+  if (st == PIC_OK && chain_trace_buffer()) {
+    cudaStreamSynchronize(reinterpret_cast<cudaStream_t>(stream));
+    chain_trace_dump(e->cfg.n_layers / 2);
   }
   return st;
 }

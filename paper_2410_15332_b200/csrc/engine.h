@@ -108,6 +108,7 @@ struct pic_engine {
   bool tp_connected = false;
   float* ar_buf[2] = {nullptr, nullptr};       // reduced partials exchanged across ranks (alternating)
   long long *tp_flags = nullptr, *tp_counter = nullptr;
+  unsigned* chain_bar = nullptr;  // 2 self-resetting counters of the persistent GEMM chain's grid barrier
   float* peer_ar[2][8];                        // every rank's ar_buf (peer memory), own included
   pic::Peers peer_flags{};
   std::vector<void*> ipc_opened;

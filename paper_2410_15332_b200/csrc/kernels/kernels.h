@@ -93,6 +93,31 @@ cudaError_t launch_gemm_partial(const CUtensorMap& A, const CUtensorMap& B, floa
 cudaError_t launch_gemm_swiglu(const CUtensorMap& A, const CUtensorMap& B, void* u, int M, int N2, int K, int bn,
                                cudaStream_t st, int pack = 0, const GemmNext& nx = GemmNext{});
 bool gemm_bn_supported(int bn, bool swiglu);
+
+// ---- persistent GEMM chain (gemm_chain.cu): O-proj -> residual+RMSNorm -> gate/up+SwiGLU -> down ->
+// residual+RMSNorm -> next QKV, phases separated by grid barriers, weights streamed across them.
+enum { CHAIN_GEMM = 0, CHAIN_SWIGLU = 1, CHAIN_NORM = 2 };
+constexpr int kMaxChainPhases = 6;
+constexpr int kMaxChainMaps = 8;
+struct ChainPhase {
+  int type;               // CHAIN_*
+  int bn, M, N, kblk, kper, splits;  // GEMM: tile N, rows, cols, K/64, k-blocks per split, splits. NORM: M rows, N = d,
+                                     //   splits = partial count
+  int a, b;               // GEMM: tensor-map indices of A [M][K] and B [N][K]
+  void* out;              // GEMM: fp32 partials [splits][M][N]; SWIGLU: bf16 u [M][N/2]; NORM: bf16 x [M][d]
+  const float* P;         // NORM: partials [splits][M][d] added to h
+  const float* g;         // NORM: gain [d]
+  float* h;               // NORM: fp32 residual [M][d]
+  float eps;
+};
+struct ChainParams {
+  int n_phases;
+  ChainPhase ph[kMaxChainPhases];
+  unsigned* bar;          // 2 zero-initialised counters (self-resetting)
+  unsigned long long* trace;  // bench-only: per CTA 16 globaltimer stamps, or null
+};
+cudaError_t launch_gemm_chain(const CUtensorMap* const* maps, int n_maps, const ChainParams& cp, cudaStream_t st);
+cudaError_t prepare_gemm_chain();
 // Interleaved gate/up generator: physical row p = n·2g + j holds gate row n·g + j (j < g) or up row
 // n·g + j − g (j >= g) of the logical [F][d] matrices (tags tag_gate / tag_up, same exponent).
 cudaError_t launch_gen_gateup(void* dst_bf16, int64_t F, int64_t d, uint64_t seed, uint64_t tag_gate,

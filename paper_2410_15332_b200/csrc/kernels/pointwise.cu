@@ -26,6 +26,7 @@ bool pdl_enabled() {
 
 cudaError_t prepare_kernels() {
   cudaError_t e = prepare_gemm();
+  if (e == cudaSuccess) e = prepare_gemm_chain();
   return e == cudaSuccess ? prepare_attention() : e;
 }
 
