@@ -255,6 +255,16 @@ def cfg5(alg: str = "legolink:16", n_layers: Optional[int] = None) -> Workload:
     return rag_workload("cfg5", m, 5, 64, 512, 64, alg)
 
 
+LLAMA31_8B_LONG = replace(LLAMA31_8B, name="llama31_8b_64k", max_pos=65536)   # long-context sweep (f3)
+
+
+def long_context(n_chunks: int, alg: str = "legolink:16", n_layers: Optional[int] = None) -> Workload:
+    """SURVEY §8(f) f3 / PAPER.md:307-316 (Fig. 8): n_chunks x 512-token chunks + a 64-token query,
+    Llama-3.1-8B shape with a 64K position table."""
+    m = LLAMA31_8B_LONG if n_layers is None else truncated(LLAMA31_8B_LONG, n_layers)
+    return rag_workload(f"long{n_chunks}", m, 6, n_chunks, 512, 64, alg)
+
+
 def permuted_requests(w: Workload, n_perm: int, seed: int = 0xBADC0DE) -> List[List[Segment]]:
     """Seeded permutations / interleavings of request 0's segments (cfg1 planner tests):
     includes dynamic-first orders, split queries and repeated cache ids."""

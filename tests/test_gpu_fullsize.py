@@ -129,3 +129,38 @@ def test_fullsize_cacheblend_selection_cfg3():
 
 def N_rows(w):
     return sum(len(w.chunks[s.chunk]) if s.cached else len(s.tokens) for s in w.requests[0])
+
+
+def test_long_context_16k_legolink_sampled_rows():
+    """f3 long-context point: N = 16448 (32 x 512 + 64), LegoLink-16 on the
+    Llama-3.1-8B shape.  Graph = eager bit-identically; layer 0 and L-1 recomputed by the oracle for
+    every 8th selected row from the GPU's inputs; unselected cached keys are R(Δ)·K_chunk."""
+    w = sg.long_context(32)
+    cfg = w.model
+    eng, ids, segs, N = build(w)
+    assert N == 16448
+    g = eng.link(segs, w.alg, keep_linked=True, want_selected=True)
+    d = eng.link(segs, w.alg, keep_linked=True, debug_hidden=True, use_graph=False, want_selected=True)
+    assert np.array_equal(g.logits, d.logits) and np.array_equal(g.selected, d.selected)
+    sel = g.selected
+    assert len(sel) == 31 * 16 + 64
+    Wt = M.Weights(cfg, cache_layers=1)
+    pl = eng.plan(segs, w.alg)
+    L = cfg.n_layers
+    sub = np.arange(0, len(sel), 8)
+    for l in (0, L - 1):
+        kg, vg = eng.linked_export(g.linked, l)
+        h_in = Wt.embed_rows(pl["tok"][sel[sub]]) if l == 0 else d.hidden[l - 1, sub].astype(np.float64)
+        K, V = f32(kg), f32(vg)
+        h_out = M.layer_rows(Wt.layer(l), cfg, h_in, sel[sub], sel[sub], K, V)
+        assert rel(d.hidden[l, sub], h_out) < LAYER_TOL, (l, rel(d.hidden[l, sub], h_out))
+        assert rel(f32(kg)[sel[sub]], K[sel[sub]]) < LAYER_TOL
+        (start, n, delta), cid = pl["chunks"][-1], ids[-1]
+        ck, cv = eng.cache_export(cid, l)
+        rows = np.arange(16, n)                                  # past the recomputed first 16
+        assert np.array_equal(vg[start + rows], cv[rows])
+        ref = P.rebase(f32(ck[rows]), int(delta), cfg.head_dim, cfg.rope_theta)
+        assert rel(f32(kg[start + rows]), ref) < 4e-3
+    eng.release(g.linked)
+    eng.release(d.linked)
+    eng.close()
