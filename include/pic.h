@@ -207,6 +207,40 @@ pic_status pic_linked_export(pic_engine* eng, const pic_linked* linked, int32_t 
 pic_status pic_linked_info(pic_engine* eng, const pic_linked* linked, int32_t* n_tokens, int32_t* block_table);
 pic_status pic_linked_release(pic_engine* eng, pic_linked* linked);
 
+/* Open-loop Poisson serving of link requests ("each user compiles all immutable
+ * chunks in the test case once and then repeatedly sends the same request ... at a constant rate";
+ * "we simulate request arrival times by sampling from a Poisson distribution").
+ * Users u = 0..n_users-1 each resend their own message list as a Poisson process of rate rate/n_users
+ * during [0, duration_s).  The server (this call, one host thread, wall clock) admits queued
+ * requests FIFO into pic_link_batch calls of up to max_batch requests whose linked blocks fit the
+ * free pool and whose recomputed rows fit max_rows (CacheBlend: one request per call, the engine's
+ * limit); TTFT = first token on the host − arrival.  The chunks must already be compiled; the
+ * context cache ratio (CCR) is reported as resident cache blocks / pool blocks at the start. */
+typedef struct {
+  int32_t n_users;
+  const pic_segment* const* user_segs; /* [n_users] message lists */
+  const int32_t* user_n_segs;          /* [n_users] */
+  double rate;                         /* total arrival rate (requests / s) */
+  double duration_s;                   /* arrival window */
+  uint64_t seed;                       /* arrival-time generator (SplitMix64 counter stream) */
+  int32_t max_batch;                   /* <= limits.max_requests */
+  pic_link_params params;
+} pic_serve_config;
+typedef struct {
+  int64_t n_requests, n_completed, n_batches;
+  double elapsed_s;                    /* first arrival -> last completion */
+  double throughput_rps;               /* n_completed / elapsed_s */
+  double ttft_mean_ms, ttft_p50_ms, ttft_p90_ms, ttft_p99_ms, ttft_max_ms;
+  double mean_batch;                   /* requests per link call */
+  double ccr;                          /* context cache ratio at the start */
+  double tokens_per_s;                 /* linked tokens completed / elapsed_s */
+} pic_serve_stats;
+pic_status pic_serve_poisson(pic_engine* eng, const pic_serve_config* cfg, void* stream, pic_serve_stats* out);
+/* The arrival schedule pic_serve_poisson uses (host only): times (s, ascending) and users of every
+ * request in [0, duration_s); *n_inout = capacity on input, count on output (PIC_E_CAPACITY if short). */
+pic_status pic_serve_arrivals(int32_t n_users, double rate, double duration_s, uint64_t seed, double* times,
+                              int32_t* users, int32_t* n_inout);
+
 /* Decode over linked caches ("proceeds to the decode stage"): one step
  * for a batch of n live linked caches (distinct handles from pic_link(_batch) with out_linked).  Cache b
  * of current length N_b gets tokens[b] appended at position N_b: the model runs on that single row

@@ -32,7 +32,7 @@ def nvcc() -> str:
 
 
 def sources():
-    out = [os.path.join(CSRC, "engine.cpp"), os.path.join(CSRC, "testhooks.cpp")]
+    out = [os.path.join(CSRC, "engine.cpp"), os.path.join(CSRC, "serve.cpp"), os.path.join(CSRC, "testhooks.cpp")]
     kd = os.path.join(CSRC, "kernels")
     out += sorted(os.path.join(kd, f) for f in os.listdir(kd) if f.endswith(".cu"))
     return out

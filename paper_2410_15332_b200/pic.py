@@ -72,6 +72,20 @@ class DecodeResultC(C.Structure):
                 ("n_tokens", C.c_int32)]
 
 
+class ServeConfigC(C.Structure):
+    _fields_ = [("n_users", C.c_int32), ("user_segs", C.c_void_p), ("user_n_segs", C.POINTER(C.c_int32)),
+                ("rate", C.c_double), ("duration_s", C.c_double), ("seed", C.c_uint64), ("max_batch", C.c_int32),
+                ("params", LinkParamsC)]
+
+
+class ServeStatsC(C.Structure):
+    _fields_ = [("n_requests", C.c_int64), ("n_completed", C.c_int64), ("n_batches", C.c_int64),
+                ("elapsed_s", C.c_double), ("throughput_rps", C.c_double), ("ttft_mean_ms", C.c_double),
+                ("ttft_p50_ms", C.c_double), ("ttft_p90_ms", C.c_double), ("ttft_p99_ms", C.c_double),
+                ("ttft_max_ms", C.c_double), ("mean_batch", C.c_double), ("ccr", C.c_double),
+                ("tokens_per_s", C.c_double)]
+
+
 class StatsC(C.Structure):
     _fields_ = [("free_blocks", C.c_int64), ("total_blocks", C.c_int64), ("n_cached_chunks", C.c_int64),
                 ("kernels_last_call", C.c_int64), ("graphs_cached", C.c_int64),
@@ -88,7 +102,7 @@ EXPORTS = ["pic_arena_bytes", "pic_engine_create", "pic_engine_destroy", "pic_ge
            "pic_link_batch", "pic_plan", "pic_linked_export", "pic_linked_info", "pic_linked_release",
            "pic_cache_export", "pic_cache_info", "pic_expire_cache", "pic_read_weights", "pic_get_stats",
            "pic_last_error", "pic_status_string", "pic_arena_bytes_tp", "pic_engine_create_tp", "pic_tp_ipc_handle",
-           "pic_tp_connect", "pic_generate_context_cache_ex", "pic_decode", "pic_set_profiling", "pic_get_profile", "pic_test_gemm", "pic_test_attention", "pic_test_kv_link", "pic_bench_gemm", "pic_bench_attention", "pic_test_gemm_swiglu"]
+           "pic_tp_connect", "pic_generate_context_cache_ex", "pic_decode", "pic_serve_poisson", "pic_serve_arrivals", "pic_set_profiling", "pic_get_profile", "pic_test_gemm", "pic_test_attention", "pic_test_kv_link", "pic_bench_gemm", "pic_bench_attention", "pic_test_gemm_swiglu"]
 
 _lib = None
 
@@ -117,6 +131,9 @@ def lib() -> C.CDLL:
                                                  P(C.c_uint64), P(C.c_int32)]
         L.pic_generate_context_cache_ex.argtypes = [C.c_void_p, P(P(C.c_int32)), P(C.c_int32), C.c_int32,
                                                     P(CompileOptionsC), C.c_void_p, P(C.c_uint64), P(C.c_int32)]
+        L.pic_serve_poisson.argtypes = [C.c_void_p, P(ServeConfigC), C.c_void_p, P(ServeStatsC)]
+        L.pic_serve_arrivals.argtypes = [C.c_int32, C.c_double, C.c_double, C.c_uint64, P(C.c_double), P(C.c_int32),
+                                         P(C.c_int32)]
         L.pic_decode.argtypes = [C.c_void_p, C.c_void_p, P(C.c_int32), C.c_int32, C.c_int32, C.c_void_p,
                                  P(DecodeResultC)]
         L.pic_link.argtypes = [C.c_void_p, P(SegmentC), C.c_int32, P(LinkParamsC), C.c_void_p, P(C.c_void_p),
@@ -212,6 +229,19 @@ class LinkOutput:
     linked: Optional[int] = None          # opaque pic_linked* (release with Engine.release)
     selected: Optional[np.ndarray] = None # linked indices recomputed in the last layer
     hidden: Optional[np.ndarray] = None   # debug hidden [L][N][d]
+
+
+def serve_arrivals(n_users: int, rate: float, duration_s: float, seed: int = 0x5E12E):
+    """The Poisson arrival schedule pic_serve_poisson uses: (times [s], users)."""
+    n = C.c_int32(0)
+    st = lib().pic_serve_arrivals(n_users, rate, duration_s, seed, None, None, C.byref(n))
+    if st not in (0, 4):
+        check(st)
+    t = np.zeros(max(1, n.value), dtype=np.float64)
+    u = np.zeros(max(1, n.value), dtype=np.int32)
+    check(lib().pic_serve_arrivals(n_users, rate, duration_s, seed, t.ctypes.data_as(C.POINTER(C.c_double)),
+                                   u.ctypes.data_as(C.POINTER(C.c_int32)), C.byref(n)))
+    return t[:n.value], u[:n.value]
 
 
 @dataclass
@@ -388,6 +418,21 @@ class Engine:
         check(lib().pic_decode(self._h, hs, toks, n, int(use_graph), self._stream, res))
         return DecodeOutput(logits, np.array([res[i].next_token for i in range(n)], dtype=np.int64),
                             np.array([res[i].n_tokens for i in range(n)], dtype=np.int64))
+
+    def serve_poisson(self, requests, alg: str, rate: float, duration_s: float, *, seed: int = 0x5E12E,
+                      max_batch: Optional[int] = None, check_layer: int = 1, use_graph: bool = False) -> dict:
+        """Open-loop Poisson serving (pic_serve_poisson, f4): user u resends requests[u] at rate/len(requests).
+        Eager launches by default: batch compositions vary, so per-shape graphs would be captured per call."""
+        n = len(requests)
+        segs = [_Segs(r) for r in requests]
+        arrp = (C.POINTER(SegmentC) * n)(*[C.cast(x.arr, C.POINTER(SegmentC)) for x in segs])
+        ns = (C.c_int32 * n)(*[x.n for x in segs])
+        p, keep = self._params(alg, check_layer=check_layer, use_graph=use_graph)
+        cfgc = ServeConfigC(n, C.cast(arrp, C.c_void_p), ns, float(rate), float(duration_s), int(seed),
+                            int(max_batch or self._lim.max_requests), p)
+        out = ServeStatsC()
+        check(lib().pic_serve_poisson(self._h, C.byref(cfgc), self._stream, C.byref(out)))
+        return {k: getattr(out, k) for k, _ in ServeStatsC._fields_}
 
     def plan(self, segments, alg: str) -> dict:
         segs = _Segs(segments)
