@@ -164,6 +164,17 @@ def cores_used():
 
 
 # ------------------------------------------------------------------------------------- main
+def ncu_traffic(kernel_class):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of this kernel class from the committed
+    ncu --set full capture (profiles/ncu_r1_traffic.json), or None."""
+    path = os.path.join(ROOT, "profiles", "ncu_r1_traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f).get(kernel_class, {}).get("dram_bytes_per_launch")
+    except (OSError, ValueError):
+        return None
+
+
 def roofline(prof, P, src, nsteps):
     """Dominant kernel class of the profiled steps against its roofline."""
     tot = sum(v["ms"] for v in prof.values())
@@ -177,7 +188,7 @@ def roofline(prof, P, src, nsteps):
         achieved = dom["flops"] / (dom["ms"] / 1e3) / 1e12
         roof = {"bound": "tensor", "achieved": achieved, "peak": P["bf16_tflops"], "unit": "TFLOP/s"}
     roof["frac"] = roof["achieved"] / roof["peak"]
-    roof["traffic"] = None
+    roof["traffic"] = ncu_traffic(dom_name)
     roof["kernel"] = dom_name
     roof["share_of_step"] = dom["ms"] / tot
     roof["peak_source"] = f"{src} (MEASURED_PEAKS.json burst)" if src == "measured" else "fallback (B200_PROFILING.md)"
