@@ -154,6 +154,12 @@ static void chain_trace_dump(int layer) {
 // The persistent GEMM chain is opt-in (PIC_CHAIN=1): measured on cfg2 it streams each phase at the
 // same rate as the separate kernels, and its norm phases and grid barriers add ~18 µs per layer
 // (4.77 vs 4.28 ms per link), so the separate PDL-chained kernels remain the default.
+// a2 on a side stream overlapping the first layers (PIC_NO_K2_OVERLAP=1: everything on the main stream)
+static bool k2_overlap() {
+  static const bool on = getenv("PIC_NO_K2_OVERLAP") == nullptr;
+  return on;
+}
+
 static bool chain_enabled() {
   static const bool on = getenv("PIC_CHAIN") != nullptr;
   return on;
@@ -555,6 +561,9 @@ static pic_status init_device(pic_engine* e, void* arena, size_t bytes, cudaStre
   CK(cudaEventCreate(&e->ev0));
   CK(cudaEventCreate(&e->ev1));
   CK(cudaStreamCreateWithFlags(&e->cap_stream, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&e->side_stream, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&e->k2_fork, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&e->k2_join, cudaEventDisableTiming));
   CK(prepare_kernels());
   CK(cudaStreamSynchronize(st));
   return PIC_OK;
@@ -668,6 +677,9 @@ extern "C" void pic_engine_destroy(pic_engine* e) {
     if (e->ev0) cudaEventDestroy(e->ev0);
     if (e->ev1) cudaEventDestroy(e->ev1);
     if (e->cap_stream) cudaStreamDestroy(e->cap_stream);
+    if (e->side_stream) cudaStreamDestroy(e->side_stream);
+    if (e->k2_fork) cudaEventDestroy(e->k2_fork);
+    if (e->k2_join) cudaEventDestroy(e->k2_join);
     for (void* p : e->ipc_opened) cudaIpcCloseMemHandle(p);
     for (cudaEvent_t ev : e->ev_pool) cudaEventDestroy(ev);
   }
@@ -883,10 +895,23 @@ static pic_status enqueue_forward(pic_engine* e, const Fwd& f, const DevPlan& dp
   char* Vp = reinterpret_cast<char*>(e->Vpool);
   const size_t lbytes = (size_t)e->layer_stride * (e->f32 ? 4 : 2);
 
+  // a2: the first K2 layer on the main stream; the other layers on a side stream, overlapping the
+  // first layers' weight streaming (layer l's attention waits for them; scatter writes disjoint slots)
+  const bool k2_side = !f.k2_src.empty() && f.k2_layer0 + 1 < L && !e->profiling && k2_overlap() && e->side_stream;
   if (!f.k2_src.empty() && f.k2_layer0 < L) {
+    const int n_first = k2_side ? 1 : L - f.k2_layer0;
     ++R.launches;
-    PROF("kv_link", 8.0 * D * Hkv * (double)f.k2_src.size() * (L - f.k2_layer0), 0, launch_kv_link(e->Kpool, e->Vpool, dp.k2_src, dp.k2_dst, dp.k2_delta, (int)f.k2_src.size(), f.k2_layer0,
-                      L - f.k2_layer0, e->layer_stride, Hkv, D, e->cos_t, e->sin_t, f.rebase, st, e->f32));
+    PROF("kv_link", 8.0 * D * Hkv * (double)f.k2_src.size() * n_first, 0, launch_kv_link(e->Kpool, e->Vpool, dp.k2_src, dp.k2_dst, dp.k2_delta, (int)f.k2_src.size(), f.k2_layer0,
+                      n_first, e->layer_stride, Hkv, D, e->cos_t, e->sin_t, f.rebase, st, e->f32));
+    if (k2_side) {
+      CK(cudaEventRecord(e->k2_fork, st));
+      CK(cudaStreamWaitEvent(e->side_stream, e->k2_fork, 0));
+      ++R.launches;
+      CKL(launch_kv_link(e->Kpool, e->Vpool, dp.k2_src, dp.k2_dst, dp.k2_delta, (int)f.k2_src.size(), f.k2_layer0 + 1,
+                         L - f.k2_layer0 - 1, e->layer_stride, Hkv, D, e->cos_t, e->sin_t, f.rebase, e->side_stream,
+                         e->f32));
+      CK(cudaEventRecord(e->k2_join, e->side_stream));
+    }
   }
   ++R.launches;
   PROF("embed", 6.0 * f.M * d, 0, launch_embed(e->E, dp.tok, e->h, f.M, d, st));
@@ -972,6 +997,7 @@ static pic_status enqueue_forward(pic_engine* e, const Fwd& f, const DevPlan& dp
                                  st, e->f32));
     }
     if (f.compile && l == L - 1) break;  // compile needs only the last layer's K/V
+    if (k2_side && l == f.k2_layer0 + 1) CK(cudaStreamWaitEvent(st, e->k2_join, 0));  // side-stream K2 landed
     // a6 attention — algorithmic work: 4·H_q·D·Σ(p_i+1) FLOPs, K/V of keys 0..max p read once
     double attn_flops = 0, attn_bytes = 0;
     if (e->profiling) {

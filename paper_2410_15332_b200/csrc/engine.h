@@ -150,6 +150,8 @@ struct pic_engine {
   int32_t* host_amax = nullptr;  // pinned
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   cudaStream_t cap_stream = nullptr;
+  cudaStream_t side_stream = nullptr;   // a2 layers >= 1 overlap the first layers (joined before their attention)
+  cudaEvent_t k2_fork = nullptr, k2_join = nullptr;
   int32_t* last_cb_sel2 = nullptr;  // device: CacheBlend selection of the last forward
   // profiling
   bool profiling = false;
