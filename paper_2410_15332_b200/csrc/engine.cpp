@@ -160,6 +160,12 @@ static bool k2_overlap() {
   return on;
 }
 
+// Wave-quantised N-tile choice for multi-m-tile GEMMs (PIC_NO_WAVE_FIT=1: the bn 128/256 rule only)
+static bool wave_fit() {
+  static const bool on = getenv("PIC_NO_WAVE_FIT") == nullptr;
+  return on;
+}
+
 static bool chain_enabled() {
   static const bool on = getenv("PIC_CHAIN") != nullptr;
   return on;
@@ -847,6 +853,28 @@ struct GemmChoice {
 // QKV 48x3, O and down 32x4 CTAs), otherwise bn=256 (fewer A re-reads, full-rate UMMA N=256).
 static GemmChoice choose_gemm(const pic_engine* e, int M, int N, int K) {
   const int kblk = K / 64, mt = (M + 127) / 128;
+  const int base_units = mt * ((N + 255) / 256);  // the bn-256 rule below at several m-tiles
+  if (mt >= 2 && wave_fit() && base_units <= 132) {
+    // (only when that rule would leave SMs idle in a single wave: at several waves bn 256's higher
+    // per-instruction efficiency won in measurement, cfg4 124 vs 137 ms)
+    // Several m-tiles: the GEMM is MMA-bound, so its time is waves x per-unit work.  Pick the N-tile
+    // (and split-K) that quantises best onto 148 SMs, e.g. cfg3's O/down (M = 608, N = 4096): bn 144 ->
+    // 145 units in one wave instead of bn 256 -> 80 units on 80 SMs.
+    GemmChoice best{256, 1};
+    double best_cost = 1e300;
+    for (int bn : {256, 224, 208, 192, 176, 160, 144, 128})
+      for (int sp = 1; sp <= 4; ++sp) {
+        if (sp > 1 && (sp > kblk / 4 || (size_t)sp * M * N > e->ws_floats)) continue;
+        const int units = mt * ((N + bn - 1) / bn) * sp;
+        const int waves = (units + 147) / 148, kper = (kblk + sp - 1) / sp;
+        const double cost = (double)waves * kper * (bn + 32) + (sp - 1) * 0.02 * kblk * bn;  // + partial traffic
+        if (cost < best_cost - 1e-9) {
+          best_cost = cost;
+          best = GemmChoice{bn, sp};
+        }
+      }
+    return best;
+  }
   const int t128 = mt * ((N + 127) / 128), t256 = mt * ((N + 255) / 256);
   GemmChoice g = t128 <= 148 ? GemmChoice{128, 148 / t128} : GemmChoice{256, std::max(1, 148 / t256)};
   g.splits = std::max(1, std::min(g.splits, kblk / 4));
@@ -871,7 +899,18 @@ struct Runner {
     *splits_out = g.splits;
     if (debug_sync()) fprintf(stderr, "[pic] gemm M=%d N=%d K=%d bn=%d splits=%d\n", M, N, K, g.bn, g.splits);
     ++launches;
-    PROF("gemm", (double)N * K * 2 + (double)M * K * 2 + (double)M * N * 4, 2.0 * M * N * K, launch_gemm_partial(A, B3[bn_index(g.bn)], e->ws, M, N, K, g.splits, g.bn, st));
+    const CUtensorMap* Bm = (g.bn == 64 || g.bn == 128 || g.bn == 256) ? &B3[bn_index(g.bn)] : nullptr;
+    if (!Bm) {  // other N-tiles: weight tensor maps built on first use and cached per (matrix, bn)
+      const auto key = std::make_pair(B_ptr, g.bn);
+      auto it = e->wmaps.find(key);
+      if (it == e->wmaps.end()) {
+        CUtensorMap m;
+        TRY(make_tmap_2d(&m, const_cast<void*>(B_ptr), (uint64_t)N, (uint64_t)K, (uint32_t)g.bn));
+        it = e->wmaps.emplace(key, m).first;
+      }
+      Bm = &it->second;
+    }
+    PROF("gemm", (double)N * K * 2 + (double)M * K * 2 + (double)M * N * 4, 2.0 * M * N * K, launch_gemm_partial(A, *Bm, e->ws, M, N, K, g.splits, g.bn, st));
     return PIC_OK;
   }
 };

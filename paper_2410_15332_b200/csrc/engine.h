@@ -165,6 +165,7 @@ struct pic_engine {
   pic::BlockAllocator alloc;
   // graphs
   std::map<std::vector<int64_t>, cudaGraphExec_t> graphs;
+  std::map<std::pair<const void*, int>, CUtensorMap> wmaps;  // weight tensor maps for N-tiles other than 64/128/256
   // stats
   int64_t kernels_last = 0, h2d_last = 0, d2h_last = 0;
 };

@@ -337,7 +337,7 @@ static cudaError_t prep_t() {
                               GemmSmem<BN, ST>::kBytes);
 }
 
-#define PIC_GEMM_BNS(X) X(64) X(128) X(208) X(256)
+#define PIC_GEMM_BNS(X) X(64) X(128) X(144) X(160) X(176) X(192) X(208) X(224) X(256)
 #define PIC_SWIGLU_BNS(X) X(32) X(64) X(128) X(224) X(256)
 
 cudaError_t prepare_gemm() {
