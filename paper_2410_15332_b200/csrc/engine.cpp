@@ -991,6 +991,7 @@ static pic_status enqueue_forward(pic_engine* e, const Fwd& f, const DevPlan& dp
   // Persistent GEMM chain (gemm_chain.cu) for the weight-streaming regime: one launch per layer runs
   // O-proj, residual+RMSNorm, gate/up+SwiGLU, down, residual+RMSNorm and the next layer's QKV.
   const bool use_chain = chain_enabled() && !e->f32 && e->tp_size == 1 && !f.cb && e->gu_group > 0 && f.M <= 128 &&
+                         c.d_model <= 4096 &&
                          f.M > 0;
   bool qkv_done = false;  // this layer's QKV partials were produced by the previous layer's chain
   int s_chain_qkv = 0;
@@ -1094,7 +1095,8 @@ static pic_status enqueue_forward(pic_engine* e, const Fwd& f, const DevPlan& dp
       const CUtensorMap* maps[kMaxChainMaps];
       int nm = 0;
       double bytes = 0, flops = 0;
-      auto gemm_phase = [&](int type, const CUtensorMap* A, const CUtensorMap* B, int N, int K, void* out) -> int {
+      auto gemm_phase = [&](int type, const CUtensorMap* A, const CUtensorMap* B, int N, int K, void* out,
+                            int max_splits = 4) -> int {
         ChainPhase& ph = cp.ph[cp.n_phases++];
         ph.type = type;
         ph.M = M;
@@ -1102,7 +1104,7 @@ static pic_status enqueue_forward(pic_engine* e, const Fwd& f, const DevPlan& dp
         ph.kblk = K / 64;
         ph.bn = type == CHAIN_SWIGLU ? 2 * e->gu_group : 128;
         const int tiles = (N + ph.bn - 1) / ph.bn;
-        ph.splits = type == CHAIN_SWIGLU ? 1 : std::max(1, std::min(148 / tiles, ph.kblk / 4));
+        ph.splits = type == CHAIN_SWIGLU ? 1 : std::max(1, std::min({148 / tiles, ph.kblk / 4, max_splits}));
         while (ph.splits > 1 && (size_t)ph.splits * M * N > e->ws_floats) --ph.splits;
         ph.kper = (ph.kblk + ph.splits - 1) / ph.splits;
         ph.a = nm;
@@ -1136,7 +1138,7 @@ static pic_status enqueue_forward(pic_engine* e, const Fwd& f, const DevPlan& dp
       if (next) {
         const LayerW& wn = e->layers[l + 1];
         norm_phase(s_dn, wn.g1);
-        s_chain_qkv = gemm_phase(CHAIN_GEMM, &e->tm_x, &wn.tm_qkv[bn_index(128)], qkv, d, e->ws);
+        s_chain_qkv = gemm_phase(CHAIN_GEMM, &e->tm_x, &wn.tm_qkv[bn_index(128)], qkv, d, e->ws, 32);
         qkv_done = true;
       }
       cp.bar = e->chain_bar;

@@ -35,7 +35,8 @@ constexpr int kBars = 2 * kSlots + 4 + kMaxChainPhases;
 constexpr int kSmem = kRing + kStg + kBars * 8 + 16;
 static_assert(kSmem <= 232448, "chain smem over the 227 KB limit");
 constexpr int kA = 128 * 64 * 2;
-constexpr int kNormVec = 16;  // norm phase: float4 per thread, d <= 8192
+constexpr int kNormVec = 8;     // norm phase: float4 per thread, d <= 4096
+constexpr int kNormSplits = 4;  // norm phase: partials summed (fixed order, zeros beyond `splits`)
 
 // Stages of one phase tile the ring uniformly from offset 0 (at most kSlots of them).
 __device__ __forceinline__ int ring_stages(int bn) {
@@ -107,6 +108,7 @@ __global__ void __launch_bounds__(192, 1)
     if (lane == 0) {
       for (int i = 0; i < kMaxChainMaps; ++i) tma_prefetch(&maps.m[i]);
       int it = 0;  // global stage counter (barrier slot it % kSlots)
+      const uint64_t wpol = l2_policy_evict_first();  // weights: streamed once
       // stages issued with B only while the phase's A operand is not ready yet (at most one ring fill)
       int pend_off[kSlots], pend_slot[kSlots], pend_kb[kSlots], pend_m0[kSlots];
       for (int p = 0; p < cp.n_phases; ++p) {
@@ -144,7 +146,7 @@ __global__ void __launch_bounds__(192, 1)
               mbar_wait(empty0 + 8 * ((it - nst) % kSlots), ((it - nst) / kSlots) & 1);
             }
             mbar_expect_tx(full0 + 8 * slot, sbytes);
-            tma_load_2d(smem_u32(ring + off + kA), tB, full0 + 8 * slot, (kb0 + kk) * 64, n_idx * ph.bn);
+            tma_load_2d_hint(smem_u32(ring + off + kA), tB, full0 + 8 * slot, (kb0 + kk) * 64, n_idx * ph.bn, wpol);
             if (ready) {
               tma_load_2d(smem_u32(ring + off), tA, full0 + 8 * slot, (kb0 + kk) * 64, m0);
             } else {
@@ -225,28 +227,32 @@ __global__ void __launch_bounds__(192, 1)
         const int d = ph.N, n4 = d / 4;  // d <= 128·4·kNormVec
         for (int r = blockIdx.x; r < ph.M; r += G) {
           float4* hr = reinterpret_cast<float4*>(ph.h + (size_t)r * d);
+          // every load of the row in flight at once: h and all split partials (unrolled, no dependences)
           float4 v[kNormVec];
+          float4 w[kNormSplits][kNormVec];
 #pragma unroll
           for (int j = 0; j < kNormVec; ++j) {
             const int c = et + 128 * j;
             v[j] = c < n4 ? __ldcg(hr + c) : make_float4(0.f, 0.f, 0.f, 0.f);
           }
-          for (int s2 = 0; s2 < ph.splits; ++s2) {
+#pragma unroll
+          for (int s2 = 0; s2 < kNormSplits; ++s2) {
             const float4* Ps = reinterpret_cast<const float4*>(ph.P + ((size_t)s2 * ph.M + r) * d);
-            float4 w[kNormVec];
 #pragma unroll
             for (int j = 0; j < kNormVec; ++j) {
               const int c = et + 128 * j;
-              w[j] = c < n4 ? __ldcg(Ps + c) : make_float4(0.f, 0.f, 0.f, 0.f);
-            }
-#pragma unroll
-            for (int j = 0; j < kNormVec; ++j) {
-              v[j].x += w[j].x;
-              v[j].y += w[j].y;
-              v[j].z += w[j].z;
-              v[j].w += w[j].w;
+              w[s2][j] = (s2 < ph.splits && c < n4) ? __ldcg(Ps + c) : make_float4(0.f, 0.f, 0.f, 0.f);
             }
           }
+#pragma unroll
+          for (int s2 = 0; s2 < kNormSplits; ++s2)
+#pragma unroll
+            for (int j = 0; j < kNormVec; ++j) {
+              v[j].x += w[s2][j].x;
+              v[j].y += w[s2][j].y;
+              v[j].z += w[s2][j].z;
+              v[j].w += w[s2][j].w;
+            }
           float ss = 0.f;
 #pragma unroll
           for (int j = 0; j < kNormVec; ++j) {
