@@ -43,6 +43,13 @@ def _rank(rank, world, port, q):
             g = eng.link(segs, alg, use_graph=True)      # graph replay path too
             out[alg] = (o.logits, g.logits, o.first_token)
         kq = eng.read_weights(0, 1, 0, 2 * 128)          # this rank's q-head rows of layer 1
+        # decode over the linked cache (f1) and LegoLink-0 (f2) under tensor parallelism
+        h = eng.link(segs, "legolink:4", keep_linked=True)
+        out["decode"] = [eng.decode([h.linked], [t]).logits[0] for t in (5, 77, 300, 2)]
+        eng.release(h.linked)
+        ids0 = eng.generate_context_cache(w.chunks, dummy_prefix=4)
+        segs0 = [("cached", i) for i in ids0] + [("tokens", w.requests[0][-1].tokens)]
+        out["legolink0"] = eng.link(segs0, "legolink0").logits
         q.put((rank, out, kq))
         eng.close()
         dist.destroy_process_group()
@@ -78,6 +85,19 @@ def test_tp2_matches_oracle_and_tp1():
         ref = P.link(store, segs, alg)
         err = np.linalg.norm(l0 - ref.logits) / np.linalg.norm(ref.logits)
         assert err < 2e-2, (alg, err)
+    # decode steps after a LegoLink-4 link (f1) and LegoLink-0 (f2), both sharded
+    r4 = P.link(store, segs, "legolink:4")
+    K, V = r4.K, r4.V
+    for i, t in enumerate((5, 77, 300, 2)):
+        lg, K, V = P.decode(Wt, K, V, t)
+        a, b = res[0][1]["decode"][i], res[1][1]["decode"][i]
+        assert np.array_equal(a, b)
+        assert np.linalg.norm(a - lg) / np.linalg.norm(lg) < 2e-2, i
+    store0 = P.Store(Wt)
+    oids0 = store0.compile(w.chunks, dummy_prefix=4)
+    ref0 = P.link(store0, [("cached", i) for i in oids0] + [("tokens", w.requests[0][-1].tokens)], "legolink0")
+    assert np.array_equal(res[0][1]["legolink0"], res[1][1]["legolink0"])
+    assert np.linalg.norm(res[0][1]["legolink0"] - ref0.logits) / np.linalg.norm(ref0.logits) < 2e-2
     # shard-exact weights: rank r's q rows are rows [r*256, (r+1)*256) of the global W_q
     for r in range(2):
         ref = sg.matrix(CFG.seed, sg.layer_tag(1, sg.TAG_Q), 4 * 128, 256, row0=r * 256, nrows=256)
