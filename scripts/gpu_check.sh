@@ -1,1 +1,1 @@
-timeout 900 python -m pytest tests/test_gpu_tp.py -q -x --timeout 800 --timeout_method thread 2>&1 | tail -5
+timeout 900 python -m pytest tests/test_gpu_decode.py -q -x --timeout 800 --timeout_method thread 2>&1 | tail -5

@@ -43,11 +43,18 @@ def segs_for(segs, ids):
     return [("cached", ids[s.chunk]) if s.cached else ("tokens", s.tokens) for s in segs]
 
 
-@pytest.mark.parametrize("alg", ["legolink:4", "naive", "fr"])
+@pytest.mark.parametrize("alg", ["legolink:4", "naive", "fr", "cacheblend:15", "legolink0"])
 def test_decode_steps_match_oracle(env, alg):
     cfg, w, eng, Wt, store, eids, oids, tol = env
-    out = eng.link(segs_for(w.requests[0], eids), alg, keep_linked=True)
-    ref = P.link(store, segs_for(w.requests[0], oids), alg)
+    if alg == "legolink0":                                   # chunks compiled behind 4 dummies (f2)
+        eids = eng.generate_context_cache(w.chunks, dummy_prefix=4)
+        store = P.Store(Wt)
+        oids = store.compile(w.chunks, dummy_prefix=4)
+    out = eng.link(segs_for(w.requests[0], eids), alg, keep_linked=True, want_selected=True)
+    # CacheBlend: the oracle continues from the GPU's own device-side selection (near-threshold swaps
+    # are a selection question, pinned separately; SURVEY §8(c).8 protocol (ii))
+    ref = P.link(store, segs_for(w.requests[0], oids), alg,
+                 sel_override=out.selected if alg.startswith("cacheblend") else None)
     K, V = ref.K, ref.V
     toks = sg.tokens(0xDEC0DE, 7, STEPS, cfg.vocab, None)
     N0 = out.n_tokens
