@@ -877,6 +877,19 @@ static GemmChoice choose_gemm(const pic_engine* e, int M, int N, int K) {
   }
   const int t128 = mt * ((N + 127) / 128), t256 = mt * ((N + 255) / 256);
   GemmChoice g = t128 <= 148 ? GemmChoice{128, 148 / t128} : GemmChoice{256, std::max(1, 148 / t256)};
+  if (mt == 1 && t128 > 148 && wave_fit()) {
+    // one m-tile, too many N-tiles for a wave at bn 128 (the LM head: N = vocab): each CTA streams
+    // bn·K weights per unit, so minimise waves x bn (vocab 32000: bn 224 -> 143 units, one wave)
+    int best = 256, best_cost = ((N + 255) / 256 + 147) / 148 * 256;
+    for (int bn : {224, 208, 192, 176, 160, 144}) {
+      const int cost = ((N + bn - 1) / bn + 147) / 148 * bn;
+      if (cost < best_cost) {
+        best = bn;
+        best_cost = cost;
+      }
+    }
+    g = GemmChoice{best, 1};
+  }
   g.splits = std::max(1, std::min(g.splits, kblk / 4));
   while (g.splits > 1 && (size_t)g.splits * M * N > e->ws_floats) --g.splits;
   return g;
