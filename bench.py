@@ -215,6 +215,9 @@ def main():
                     help="tensor parallel over all ranks (heads/MLP columns sharded, fused peer-memory all-reduce); "
                          "strong scaling of one request instead of data parallel requests")
     ap.add_argument("--layers", type=int, default=None, help="truncate depth (functional runs only; marked in config)")
+    ap.add_argument("--kv-share", type=int, default=0, choices=[0, 1],
+                    help="f3 shared-block link: chunk-store blocks linked by reference, keys re-based in the "
+                         "attention K-tile load (pic_link_params.kv_share)")
     ap.add_argument("--decode-steps", type=int, default=32,
                     help="f1: decode steps over the linked caches after the link measurement (0 = skip)")
     args = ap.parse_args()
@@ -230,6 +233,7 @@ def main():
             w.requests = w.requests * world            # single-request configs: one copy per GPU
         w.requests = D.shard(w.requests, rank, world)   # data parallel by independent request
     cfgd = describe(w)
+    cfgd["kv_share"] = bool(args.kv_share)
     N_tok = [sum(len(w.chunks[s.chunk]) if s.cached else len(s.tokens) for s in r) for r in w.requests]
 
     if args.impl == "reference":
@@ -282,6 +286,7 @@ def main():
         eng = B.Engine(m, num_blocks=(total_tokens + sum(N_tok)) // 16 + 2 * len(w.chunks) + 64 * len(w.requests),
                        max_rows=max(4096, rows_link), max_tokens=max(max_N + 2 * args.decode_steps + 16, 512) + 16,
                        max_requests=len(w.requests), device=dev, stream=stream, **tp_kw)
+        eng.kv_share = bool(args.kv_share)
         if args.tp and world > 1:
             D.tp_connect(eng)
         ids = eng.generate_context_cache(w.chunks, dummy_prefix=dummy_prefix(w.alg))

@@ -103,6 +103,14 @@ typedef struct {
   float* debug_hidden;       /* test hook (nullable, host): [n_layers][N][d_model] fp32; row r of layer l = residual of
                                 the r-th selected row after layer l (rows beyond that layer's k' untouched).
                                 Single-request pic_link only; disables graphs. */
+  int32_t kv_share;          /* 1 = shared-block link: a linked block whose 16 rows are all
+                                unselected rows of one cached chunk, aligned to one of its store blocks, points
+                                at that chunk-store block (reference counted) instead of a fresh copy; its keys
+                                keep their compile positions and the attention kernels re-base them by the
+                                block's Δ (R1) when they load the K tile, with the same arithmetic as the copy
+                                (a2), so results are bit-identical to kv_share = 0.  Only blocks holding a
+                                recomputed row, dynamic tokens or a chunk boundary are allocated and filled.
+                                Ignored for CacheBlend (its layer 0 rewrites every row).  Default 0 */
 } pic_link_params;
 
 /* Per-request result of a link. */
@@ -190,12 +198,15 @@ pic_status pic_link_batch(pic_engine* eng, int32_t n_req, const pic_segment* con
  *   sel[cap] sorted selected linked indices (pre-CacheBlend set; CacheBlend: dynamic ∪ {N-1});
  *   tok[cap] token ids; src[2*cap] (cache id low 31 bits, row) or (-1,-1) for dynamic rows;
  *   chunks[3*cap] (start, len, delta) per cached segment; block_table[cap] linked block ids that
- *   pic_link would allocate now (lowest-free-first); slot[cap] slot of each selected row
- *   (block_table[i/16]*16 + i%16). */
+ *   pic_link would use now (fresh blocks lowest-free-first; with kv_share, shared chunk-store blocks
+ *   in place); slot[cap] slot of each selected row (block_table[i/16]*16 + i%16). */
 typedef struct {
   int32_t capacity;
   int32_t n_tokens, n_sel, n_chunks, n_blocks;
   int32_t *sel, *tok, *src, *chunks, *block_table, *slot;
+  int32_t* block_delta;      /* [cap] (nullable): per linked block, the Δ the attention applies to a shared
+                                chunk-store block's keys (kv_share = 1), else 0 */
+  int32_t n_shared;          /* out: blocks linked by reference (kv_share = 1); n_blocks - n_shared are fresh */
 } pic_plan_out;
 pic_status pic_plan(pic_engine* eng, const pic_segment* segs, int32_t n_segs, const pic_link_params* params,
                     pic_plan_out* out);
@@ -205,6 +216,12 @@ pic_status pic_plan(pic_engine* eng, const pic_segment* segs, int32_t n_segs, co
 pic_status pic_linked_export(pic_engine* eng, const pic_linked* linked, int32_t layer, void* k_host, void* v_host);
 /* Number of tokens N and the block table (int32[ceil(N/16)], nullable) of a linked cache. */
 pic_status pic_linked_info(pic_engine* eng, const pic_linked* linked, int32_t* n_tokens, int32_t* block_table);
+/* Shared-block link (kv_share): number of blocks of `linked` that are chunk-store blocks
+ * linked by reference, and per block (int32[ceil(N/16)], nullable) the Δ the attention applies to its keys
+ * (0 for blocks the link owns).  Host-only bookkeeping. */
+pic_status pic_linked_sharing(pic_engine* eng, const pic_linked* linked, int32_t* n_shared, int32_t* block_delta);
+/* Release a linked cache: its own blocks return to the pool; shared chunk-store blocks drop one reference
+ * (they stay with the chunk store, or return to the pool if their chunk was expired meanwhile). */
 pic_status pic_linked_release(pic_engine* eng, pic_linked* linked);
 
 /* Open-loop Poisson serving of link requests ("each user compiles all immutable

@@ -268,10 +268,16 @@ def link(store: Store, segments, alg: str, rebase_keys: bool = True, check_layer
 # ----------------------------------------------------------------------------
 class BlockAllocator:
     """Model of the engine's block allocator: one block id spans all layers' K and V;
-    allocation takes the lowest free ids in increasing order; frees return ids."""
+    allocation takes the lowest free ids in increasing order; frees return ids.  Blocks are
+    reference counted (a chunk-store block linked by reference is also held by the linked
+    cache, see share_blocks): release returns an id to the free set at its last reference."""
 
     def __init__(self, num_blocks: int):
         self.free = set(range(num_blocks))
+        self.refs: Dict[int, int] = {}
+
+    def retain(self, b: int) -> None:
+        self.refs[int(b)] += 1
 
     def peek(self, n: int) -> List[int]:
         return sorted(self.free)[:n]
@@ -281,10 +287,39 @@ class BlockAllocator:
             raise MemoryError("pool full")
         ids = sorted(self.free)[:n]
         self.free.difference_update(ids)
+        for i in ids:
+            self.refs[i] = 1
         return ids
 
     def release(self, ids: Sequence[int]) -> None:
-        self.free.update(int(i) for i in ids)
+        for i in ids:
+            i = int(i)
+            self.refs[i] = self.refs.get(i, 1) - 1
+            if self.refs[i] == 0:
+                self.free.add(i)
+
+
+def share_blocks(pl: Plan, chunk_blocks: Dict[int, Sequence[int]], rebase: bool = True):
+    """Shared-block link layout: linked block b (rows 16b..16b+15)
+    is the chunk-store block of chunk c holding rows 16b − s_c .. 16b − s_c + 15 — linked by
+    reference instead of copied — iff s_c is a multiple of 16 and all 16 rows are unselected rows
+    of c; its keys then still carry Δ_c (0 without re-base) to apply when they are read.
+    CacheBlend shares nothing (its layer 0 rewrites every row).  Returns (shared, delta) per linked
+    block: store block id or -1, and Δ (0 for fresh blocks)."""
+    nb = n_blocks(pl.N)
+    shared, delta = [-1] * nb, [0] * nb
+    if pl.alg == "cacheblend":
+        return shared, delta
+    sel = set(int(i) for i in pl.sel)
+    for cid, s0, n, dl in pl.chunks:
+        if s0 % BLOCK:
+            continue
+        for j in range(0, n - BLOCK + 1, BLOCK):
+            if any(s0 + j + r in sel for r in range(BLOCK)):
+                continue
+            shared[(s0 + j) // BLOCK] = int(chunk_blocks[cid][j // BLOCK])
+            delta[(s0 + j) // BLOCK] = int(dl) if rebase else 0
+    return shared, delta
 
 
 def n_blocks(n_tokens: int) -> int:

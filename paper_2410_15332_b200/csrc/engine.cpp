@@ -308,7 +308,7 @@ static ArenaPlan plan_arena(const pic_model_config& c, const pic_engine_limits& 
   a.max_k2 = (int)std::min<size_t>((size_t)l.max_requests * l.max_tokens, (size_t)1 << 30);
   // per-row arrays (tok,pos,slot,seq,head) + tiles + seq offsets + bt + k2 (3) + CB (cand,forced,sel2,pos2,slot2,
   // keep,count) + tiles2 + head2
-  a.plan_ints = 5 * M + 3 * (size_t)a.max_tiles + a.max_seqs + a.max_bt + 3 * (size_t)a.max_k2 +
+  a.plan_ints = 5 * M + 3 * (size_t)a.max_tiles + a.max_seqs + 2 * (size_t)a.max_bt /* bt, bdelta */ + 3 * (size_t)a.max_k2 +
                 7 * (size_t)l.max_tokens + 3 * (size_t)a.max_tiles + M + 4096;
   a.off_plan = L.add(a.plan_ints * 4);
   // tensor parallel: two reduced-partial buffers (alternating per all-reduce), flags, epoch counter
@@ -783,6 +783,46 @@ static void select_rows(const pic_link_params* pr, LinkPlanHost& p) {
 
 static int32_t slot_of(const std::vector<int32_t>& bt, int32_t i) { return bt[i / 16] * 16 + i % 16; }
 
+// Shared-block link (pic_link_params.kv_share).  Linked block b (rows 16b..16b+15) is
+// linked by reference to a chunk-store block iff its 16 rows are all unselected rows of one cached
+// chunk c whose start s_c is 16-aligned (so they are exactly store block (16b − s_c)/16 of c); its keys
+// then keep their compile positions and carry Δ_c (0 without re-base), applied by the attention when it
+// loads them.  Every other block is fresh (a2 copies its unselected cached rows, a5 scatters the rest).
+// shared[b] = store block id or -1; delta[b] = Δ to apply (0 for fresh blocks).  Returns #fresh.
+static int plan_blocks(const pic_engine* e, const pic_link_params* pr, const LinkPlanHost& p,
+                       std::vector<int32_t>& shared, std::vector<int32_t>& delta) {
+  const int nb = (p.N + 15) / 16;
+  shared.assign(nb, -1);
+  delta.assign(nb, 0);
+  if (pr->kv_share && pr->alg != PIC_CACHEBLEND) {
+    std::vector<uint8_t> in_sel(p.N, 0);
+    for (int32_t i : p.sel) in_sel[i] = 1;
+    for (size_t c = 0; c < p.chunk_start.size(); ++c) {
+      const int s0 = p.chunk_start[c], n = p.chunk_len[c];
+      if (s0 % 16) continue;
+      const ChunkRec& ch = e->store.at(p.chunk_id[c]);
+      for (int j = 0; j + 16 <= n; j += 16) {
+        bool clean = true;
+        for (int r = 0; r < 16 && clean; ++r) clean = !in_sel[s0 + j + r];
+        if (!clean) continue;
+        shared[(s0 + j) / 16] = ch.blocks[j / 16];
+        delta[(s0 + j) / 16] = pr->rebase ? p.chunk_delta[c] : 0;
+      }
+    }
+  }
+  int fresh = 0;
+  for (int b = 0; b < nb; ++b) fresh += shared[b] < 0;
+  return fresh;
+}
+
+// Block table of a link: shared blocks in place, fresh ids (lowest-free-first, in block order) elsewhere.
+static std::vector<int32_t> merge_blocks(const std::vector<int32_t>& shared, const std::vector<int32_t>& fresh) {
+  std::vector<int32_t> bt(shared.size());
+  size_t k = 0;
+  for (size_t b = 0; b < shared.size(); ++b) bt[b] = shared[b] >= 0 ? shared[b] : fresh[k++];
+  return bt;
+}
+
 // LegoLink-0 links only chunks compiled with a dummy prefix (S:324 variant mismatch); its selection is
 // Naive's ("skips recomputation entirely").
 static pic_status check_variant(const pic_engine* e, const pic_link_params* pr, const LinkPlanHost& p) {
@@ -808,8 +848,13 @@ extern "C" pic_status pic_plan(pic_engine* e, const pic_segment* segs, int32_t n
   out->n_sel = (int)p.sel.size();
   out->n_chunks = (int)p.chunk_start.size();
   out->n_blocks = nb;
-  std::vector<int32_t> bt = e->alloc.peek(nb);
-  if ((int)bt.size() < nb) return fail(PIC_E_CAPACITY, "pool has %zu free blocks, need %d", bt.size(), nb);
+  std::vector<int32_t> shared, bdelta;
+  const int n_fresh = plan_blocks(e, pr, p, shared, bdelta);
+  std::vector<int32_t> fresh = e->alloc.peek(n_fresh);
+  if ((int)fresh.size() < n_fresh) return fail(PIC_E_CAPACITY, "pool has %zu free blocks, need %d", fresh.size(), n_fresh);
+  const std::vector<int32_t> bt = merge_blocks(shared, fresh);
+  out->n_shared = nb - n_fresh;
+  if (out->block_delta) std::copy(bdelta.begin(), bdelta.end(), out->block_delta);
   if (out->sel) std::copy(p.sel.begin(), p.sel.end(), out->sel);
   if (out->tok) std::copy(p.tok.begin(), p.tok.end(), out->tok);
   if (out->src)
@@ -930,7 +975,7 @@ struct Runner {
 
 // Enqueue the whole forward on `st`.  Plan arrays are already on the device at the given pointers.
 struct DevPlan {
-  int32_t *tok, *pos, *slot, *seq, *tiles, *seq_bt_off, *bt, *k2_src, *k2_dst, *k2_delta, *head_map;
+  int32_t *tok, *pos, *slot, *seq, *tiles, *seq_bt_off, *bt, *bdelta, *k2_src, *k2_dst, *k2_delta, *head_map;
   int32_t *cb_cand, *cb_forced, *cb_sel2, *cb_pos2, *cb_slot2, *cb_keep, *cb_count, *tiles2, *head_map2;
   int n_tiles, n_tiles2;
   int32_t *attn_work, *attn_nsplit, *attn_work2, *attn_nsplit2;
@@ -1087,6 +1132,9 @@ static pic_status enqueue_forward(pic_engine* e, const Fwd& f, const DevPlan& dp
       a.static_plan = (tiles == dp.tiles) ? 1 : 0;  // CacheBlend's post-selection tiles/positions are device-side
       a.kpool = nullptr;  // L2 prefetch of K/V pages: measured slower (TMA unit busy ahead of the real loads)
       a.vpool = e->Vpool;
+      a.bdelta = dp.bdelta;
+      a.cos_t = e->cos_t;
+      a.sin_t = e->sin_t;
       a.Q = e->Q;
       g_attn_trace_ctas = a.n_work * Hkv;
       a.o_part = e->o_part;
@@ -1101,7 +1149,7 @@ static pic_status enqueue_forward(pic_engine* e, const Fwd& f, const DevPlan& dp
     } else {
       ++R.launches;
       PROF("attention", attn_bytes, attn_flops, launch_attention_simt(e->Q, Kl, Vl, dp.seq, dp.seq_bt_off, dp.bt, pos, e->Obuf, M, Hq, Hkv, D,
-                               (float)(1.0 / std::sqrt((double)D)), st, e->f32));
+                               (float)(1.0 / std::sqrt((double)D)), st, e->f32, dp.bdelta, e->cos_t, e->sin_t));
     }
     if (use_chain) {
       ChainParams cp{};
@@ -1200,7 +1248,7 @@ static pic_status enqueue_forward(pic_engine* e, const Fwd& f, const DevPlan& dp
 static void add_sig(std::vector<int64_t>& sig, const Fwd& f, const DevPlan& dp) {
   sig = {f.M,  dp.n_tiles, (int64_t)f.seq_bt_off.size(), (int64_t)f.bt.size(), (int64_t)f.k2_src.size(), f.k2_layer0,
          f.n_head, f.compile, f.rebase, f.cb, f.cb_layer, f.cb_T, f.M2, f.cb_override, dp.n_tiles2, f.attn_n_work,
-         f.attn_n_work2};
+         f.attn_n_work2, f.kv_rot};
   // attention split choice depends on the per-sequence block-table lengths
   for (size_t q = 0; q < f.seq_bt_off.size(); ++q) sig.push_back(f.seq_bt_off[q]);
 }
@@ -1254,6 +1302,7 @@ static pic_status run_forward(pic_engine* e, const Fwd& f, cudaStream_t st, bool
   dp.tiles = pk.put(f.tiles);
   dp.seq_bt_off = pk.put(f.seq_bt_off);
   dp.bt = pk.put(f.bt);
+  dp.bdelta = f.kv_rot ? pk.put(f.bdelta) : nullptr;
   dp.k2_src = pk.put(f.k2_src);
   dp.k2_dst = pk.put(f.k2_dst);
   dp.k2_delta = pk.put(f.k2_delta);
@@ -1495,6 +1544,8 @@ extern "C" pic_status pic_generate_context_cache_ex(pic_engine* e, const int32_t
 struct ReqBuild {
   LinkPlanHost p;
   std::vector<int32_t> bt;
+  std::vector<int32_t> shared, bdelta;  // f3: per block, store block linked by reference (or -1) and its Δ
+  int n_fresh = 0;
 };
 
 // Append one request's rows / tiles / K2 work to a forward.
@@ -1504,6 +1555,8 @@ static void append_request(pic_engine* e, const pic_link_params* pr, ReqBuild& r
   const int seq = (int)f.seq_bt_off.size();
   f.seq_bt_off.push_back((int)f.bt.size());
   f.bt.insert(f.bt.end(), rb.bt.begin(), rb.bt.end());
+  f.bdelta.insert(f.bdelta.end(), rb.bdelta.begin(), rb.bdelta.end());
+  for (int32_t dl : rb.bdelta) f.kv_rot |= dl != 0;
   const bool cb = pr->alg == PIC_CACHEBLEND;
   const std::vector<int32_t>* rows = &p.sel;
   std::vector<int32_t> all;
@@ -1531,7 +1584,7 @@ static void append_request(pic_engine* e, const pic_link_params* pr, ReqBuild& r
     const ChunkRec& ch = e->store.at(p.chunk_id[c]);
     for (int j = 0; j < p.chunk_len[c]; ++j) {
       const int i = p.chunk_start[c] + j;
-      if (in_sel[i]) continue;
+      if (in_sel[i] || rb.shared[i / 16] >= 0) continue;  // recomputed, or linked by reference (f3)
       f.k2_src.push_back(slot_of(ch.blocks, j));
       f.k2_dst.push_back(slot_of(rb.bt, i));
       f.k2_delta.push_back(p.chunk_delta[c]);
@@ -1558,7 +1611,8 @@ static pic_status link_impl(pic_engine* e, int32_t n_req, const pic_segment* con
     TRY(assemble(e, segs[r], n_segs[r], reqs[r].p));
     TRY(check_variant(e, pr, reqs[r].p));
     select_rows(pr, reqs[r].p);
-    need += (reqs[r].p.N + 15) / 16;
+    reqs[r].n_fresh = plan_blocks(e, pr, reqs[r].p, reqs[r].shared, reqs[r].bdelta);
+    need += reqs[r].n_fresh;
   }
   if (!e->alloc.can(need)) return fail(PIC_E_CAPACITY, "pool has %zu free blocks, link needs %lld",
                                        e->alloc.free_ids.size(), (long long)need);
@@ -1566,7 +1620,11 @@ static pic_status link_impl(pic_engine* e, int32_t n_req, const pic_segment* con
   f.rebase = pr->rebase;
   f.n_head = n_req;
   f.debug_rows = reqs[0].p.N;
-  for (int r = 0; r < n_req; ++r) reqs[r].bt = e->alloc.alloc((reqs[r].p.N + 15) / 16);
+  for (int r = 0; r < n_req; ++r) {
+    reqs[r].bt = merge_blocks(reqs[r].shared, e->alloc.alloc(reqs[r].n_fresh));
+    for (int32_t b : reqs[r].shared)
+      if (b >= 0) e->alloc.retain(b);  // the linked cache holds the chunk-store block too
+  }
   auto rollback = [&]() {
     for (auto& rb : reqs) e->alloc.release(rb.bt);
   };
@@ -1695,6 +1753,8 @@ static pic_status link_impl(pic_engine* e, int32_t n_req, const pic_segment* con
       }
       h->n_tokens = reqs[r].p.N;
       h->blocks = reqs[r].bt;
+      h->bdelta = reqs[r].bdelta;
+      h->n_shared = (int32_t)reqs[r].bt.size() - reqs[r].n_fresh;
       out_linked[r] = h;
     } else {
       e->alloc.release(reqs[r].bt);  // stream-ordered reuse on the same stream
@@ -1729,11 +1789,13 @@ extern "C" pic_status pic_decode(pic_engine* e, pic_linked* const* linked, const
     if (linked[b]->n_tokens % 16 == 0) {
       grown[b] = e->alloc.alloc(1)[0];
       linked[b]->blocks.push_back(grown[b]);
+      linked[b]->bdelta.push_back(0);
     }
   auto rollback = [&]() {
     for (int b = 0; b < n; ++b)
       if (grown[b] >= 0) {
         linked[b]->blocks.pop_back();
+        linked[b]->bdelta.pop_back();
         e->alloc.release({grown[b]});
       }
   };
@@ -1745,6 +1807,8 @@ extern "C" pic_status pic_decode(pic_engine* e, pic_linked* const* linked, const
     const pic_linked& h = *linked[b];
     f.seq_bt_off.push_back((int)f.bt.size());
     f.bt.insert(f.bt.end(), h.blocks.begin(), h.blocks.end());
+    f.bdelta.insert(f.bdelta.end(), h.bdelta.begin(), h.bdelta.end());
+    for (int32_t dl : h.bdelta) f.kv_rot |= dl != 0;
     add_tiles(f.tiles, b, b, 1, qpt);
     f.tok.push_back(tokens[b]);
     f.pos.push_back(h.n_tokens);
@@ -1815,8 +1879,62 @@ extern "C" pic_status pic_link_batch(pic_engine* e, int32_t n_req, const pic_seg
 }
 
 // ============================================================================ exports / lifecycle
+static inline float bf16_to_f(uint16_t h) {
+  uint32_t u = (uint32_t)h << 16;
+  float f;
+  std::memcpy(&f, &u, 4);
+  return f;
+}
+static inline uint16_t f_to_bf16(float f) {  // round to nearest even (finite values)
+  uint32_t u;
+  std::memcpy(&u, &f, 4);
+  return (uint16_t)((u + 0x7FFFu + ((u >> 16) & 1u)) >> 16);
+}
+
+// Host copy of the attention kernels' K-tile re-base (rebase_pair): oa = fma(a, c, −(b·s)),
+// ob = fma(b, c, a·s), then the pool's precision — so exported rows of a shared block (f3) are the
+// rows the kernels attend to, bit for bit.
+static pic_status rebase_export(pic_engine* e, void* k_host, int n, const std::vector<int32_t>& bdelta) {
+  const int Hkv = e->cfg.n_kv_heads, D = e->cfg.head_dim, h = D / 2;
+  std::vector<float> cs(h), sn(h);
+  int cached = 0;
+  for (int i = 0; i < n; ++i) {
+    const int dl = bdelta[i / 16];
+    if (dl == 0) continue;
+    const int ad = dl < 0 ? -dl : dl;
+    const float sg = dl < 0 ? -1.f : 1.f;
+    if (ad != cached) {
+      CK(cudaMemcpy(cs.data(), e->cos_t + (size_t)ad * h, h * 4, cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(sn.data(), e->sin_t + (size_t)ad * h, h * 4, cudaMemcpyDeviceToHost));
+      cached = ad;
+    }
+    for (int g = 0; g < Hkv; ++g)
+      for (int j = 0; j < h; ++j) {
+        const size_t ia = ((size_t)i * Hkv + g) * D + j, ib = ia + h;
+        float a, b;
+        if (e->f32) {
+          a = reinterpret_cast<float*>(k_host)[ia];
+          b = reinterpret_cast<float*>(k_host)[ib];
+        } else {
+          a = bf16_to_f(reinterpret_cast<uint16_t*>(k_host)[ia]);
+          b = bf16_to_f(reinterpret_cast<uint16_t*>(k_host)[ib]);
+        }
+        const float s = sg * sn[j];
+        const float ra = std::fma(a, cs[j], -(b * s)), rb = std::fma(b, cs[j], a * s);
+        if (e->f32) {
+          reinterpret_cast<float*>(k_host)[ia] = ra;
+          reinterpret_cast<float*>(k_host)[ib] = rb;
+        } else {
+          reinterpret_cast<uint16_t*>(k_host)[ia] = f_to_bf16(ra);
+          reinterpret_cast<uint16_t*>(k_host)[ib] = f_to_bf16(rb);
+        }
+      }
+  }
+  return PIC_OK;
+}
+
 static pic_status export_rows(pic_engine* e, const std::vector<int32_t>& blocks, int n, int layer, void* k_host,
-                              void* v_host) {
+                              void* v_host, const std::vector<int32_t>* bdelta = nullptr) {
   if (e->host_only) return fail(PIC_E_NO_DEVICE, "host-only engine");
   if (layer < 0 || layer >= e->cfg.n_layers) return fail(PIC_E_INVALID_ARG, "layer out of range");
   const int Hkv = e->cfg.n_kv_heads, D = e->cfg.head_dim;
@@ -1834,18 +1952,26 @@ static pic_status export_rows(pic_engine* e, const std::vector<int32_t>& blocks,
         CK(cudaMemcpy(reinterpret_cast<char*>(v_host) + ((size_t)i * Hkv + g) * row,
                       reinterpret_cast<char*>(e->Vpool) + src * es, row, cudaMemcpyDeviceToHost));
     }
+  if (k_host && bdelta) TRY(rebase_export(e, k_host, n, *bdelta));
   return PIC_OK;
 }
 
 extern "C" pic_status pic_linked_export(pic_engine* e, const pic_linked* h, int32_t layer, void* k_host, void* v_host) {
   if (!e || !h) return fail(PIC_E_INVALID_ARG, "NULL argument");
-  return export_rows(e, h->blocks, h->n_tokens, layer, k_host, v_host);
+  return export_rows(e, h->blocks, h->n_tokens, layer, k_host, v_host, &h->bdelta);
 }
 
 extern "C" pic_status pic_linked_info(pic_engine* e, const pic_linked* h, int32_t* n_tokens, int32_t* block_table) {
   if (!e || !h) return fail(PIC_E_INVALID_ARG, "NULL argument");
   if (n_tokens) *n_tokens = h->n_tokens;
   if (block_table) std::copy(h->blocks.begin(), h->blocks.end(), block_table);
+  return PIC_OK;
+}
+
+extern "C" pic_status pic_linked_sharing(pic_engine* e, const pic_linked* h, int32_t* n_shared, int32_t* block_delta) {
+  if (!e || !h) return fail(PIC_E_INVALID_ARG, "NULL argument");
+  if (n_shared) *n_shared = h->n_shared;
+  if (block_delta) std::copy(h->bdelta.begin(), h->bdelta.end(), block_delta);
   return PIC_OK;
 }
 

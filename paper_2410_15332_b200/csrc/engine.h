@@ -14,12 +14,18 @@
 namespace pic {
 
 // Deterministic paged-block allocator: lowest free ids first (D3; modelled by oracle.pic.BlockAllocator).
+// Blocks are reference counted: a chunk-store block linked by reference (f3 shared-block link) is
+// held by the store and by every live linked cache that points at it; it returns to the free list
+// when the last holder releases it (expire_cache while a linked cache is live keeps it).
 struct BlockAllocator {
   std::set<int32_t> free_ids;
+  std::vector<int32_t> refs;
   void reset(int64_t n) {
     free_ids.clear();
+    refs.assign(n, 0);
     for (int64_t i = 0; i < n; ++i) free_ids.insert(free_ids.end(), (int32_t)i);
   }
+  void retain(int32_t b) { ++refs[b]; }
   bool can(int64_t n) const { return (int64_t)free_ids.size() >= n; }
   std::vector<int32_t> peek(int64_t n) const {
     std::vector<int32_t> v;
@@ -28,11 +34,15 @@ struct BlockAllocator {
   }
   std::vector<int32_t> alloc(int64_t n) {
     std::vector<int32_t> v = peek(n);
-    for (int32_t b : v) free_ids.erase(b);
+    for (int32_t b : v) {
+      free_ids.erase(b);
+      refs[b] = 1;
+    }
     return v;
   }
   void release(const std::vector<int32_t>& v) {
-    for (int32_t b : v) free_ids.insert(b);
+    for (int32_t b : v)
+      if (--refs[b] == 0) free_ids.insert(b);
   }
 };
 
@@ -55,6 +65,8 @@ struct Fwd {
   std::vector<int32_t> tok, pos, slot, seq;   // per row
   std::vector<int32_t> tiles;                 // attention q-tiles: (seq, row_start, row_count)
   std::vector<int32_t> seq_bt_off, bt;        // block tables (concatenated)
+  std::vector<int32_t> bdelta;                // per bt entry: Δ still to apply to a shared block's keys (f3)
+  bool kv_rot = false;                        // some bdelta != 0: attention re-bases K tiles on load
   std::vector<int32_t> k2_src, k2_dst, k2_delta;  // a2 work: cached rows gathered into linked blocks
   int k2_layer0 = 0;
   std::vector<int32_t> head_map;              // per final row: request index or -1
@@ -98,6 +110,8 @@ struct LinkPlanHost {
 struct pic_linked {
   int32_t n_tokens = 0;
   std::vector<int32_t> blocks;
+  std::vector<int32_t> bdelta;  // per block: Δ of a chunk-store block linked by reference (f3), else 0
+  int32_t n_shared = 0;         // blocks linked by reference
 };
 
 struct pic_engine {

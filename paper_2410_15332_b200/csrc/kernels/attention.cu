@@ -40,7 +40,7 @@ constexpr int kK = 0;                         // K stages: kStages x 2 halves
 constexpr int kV = kK + kStages * 2 * kTile;  // V stages
 constexpr int kX = kV + kStages * 2 * kTile;  // softmax pair exchange: [2 parity][2 halves][128] fp32
 constexpr int kBar = kX + 2 * 2 * 128 * 4;    // barriers
-constexpr int kNumBars = 1 + 4 * kStages + 6;
+constexpr int kNumBars = 1 + 5 * kStages + 6;  // + k_rot ring (shared-block link)
 constexpr int kSmem = kBar + kNumBars * 8 + 16;
 static_assert(kSmem <= 232448, "attention smem over the 227 KB limit");
 // TMEM columns (512 allocated)
@@ -51,8 +51,8 @@ constexpr uint32_t kTmQ = 384;  // Q (bf16 pairs) [384, 448)
 
 // Both MMAs take their A operand from TMEM (Q for S = Q·Kᵀ, P for O += P·V), so shared memory only
 // carries K and V: per 128-key tile the smem traffic is the two TMA writes and the two B-operand reads.
-template <int G>
-__global__ void __launch_bounds__(320, 1)
+template <int G, bool ROT>
+__global__ void __launch_bounds__(ROT ? 448 : 320, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
                    const __grid_constant__ CUtensorMap tmK8, const __grid_constant__ CUtensorMap tmV8, const AttnArgs a) {
   griddep_launch();
@@ -71,6 +71,7 @@ __global__ void __launch_bounds__(320, 1)
   const uint32_t v_full = smem_u32(bars + 1 + 2 * S), v_empty = smem_u32(bars + 1 + 3 * S);
   const uint32_t s_full = smem_u32(bars + 1 + 4 * S), p_full = smem_u32(bars + 3 + 4 * S);
   const uint32_t o_full = smem_u32(bars + 5 + 4 * S);
+  const uint32_t k_rot = smem_u32(bars + 7 + 4 * S);  // ROT: K tile re-based in smem (4 rotation warps)
 
   const int warp = warp_id(), lane = lane_id();
   // barriers and TMEM do not depend on upstream data: set them up while the previous kernel drains
@@ -81,6 +82,7 @@ __global__ void __launch_bounds__(320, 1)
       mbar_init(k_empty + 8 * s, 1);
       mbar_init(v_full + 8 * s, 1);
       mbar_init(v_empty + 8 * s, 1);
+      mbar_init(k_rot + 8 * s, 4);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(s_full + 8 * b, 1);
@@ -212,7 +214,7 @@ __global__ void __launch_bounds__(320, 1)
       for (int t = 0; t < n; ++t) {
         const int sb = t & 1, ks = t % S;
         if (tr) q0 = globaltimer();
-        mbar_wait(k_full + 8 * ks, (t / S) & 1);
+        mbar_wait((ROT ? k_rot : k_full) + 8 * ks, (t / S) & 1);
         if (tr) w_k += globaltimer() - q0;
         tc_fence_after();
         // S(t) overwrites the buffer holding P(t-2): PV(t-2) was issued before and MMAs run in order
@@ -231,6 +233,81 @@ __global__ void __launch_bounds__(320, 1)
         tr[12] = w_p;
         tr[13] = w_v;
       }
+    }
+  } else if (ROT && warp >= 10) {
+    // ------------------------------------------------------------------ K-tile re-base (f3)
+    // Keys of a chunk-store block linked by reference still sit at their compile positions: rotate
+    // every NeoX pair (j, j+64) of such rows by Δ of its block (the a2 arithmetic, rebase_pair, so the
+    // tile equals the one a copied-and-re-based linked block would give).  In the SWIZZLE_128B tile
+    // dims j and j+64 sit at the same offset of the two 64-column halves.  Thread u owns logical
+    // 16-B chunk cc = u & 7 (dims 8cc..8cc+7) of row rg = u >> 3 of each of the 8 paged blocks.
+    const int u = threadIdx.x - 320;
+    const int cc = u & 7, rg = u >> 3;
+    const uint32_t phys = (uint32_t)(((cc ^ (rg & 7)) << 4) + rg * 128);
+    const int* bd = a.bdelta + a.seq_bt_off[seq];
+    int dcache = 0;
+    float2 cs[4], sn[4], ns[4];  // cos, sin, −sin of dims (8cc + 2k, 8cc + 2k + 1) for Δ = dcache
+    auto load_angles = [&](int d) {
+      const int ad = d < 0 ? -d : d;
+      const float sg = d < 0 ? -1.f : 1.f;
+      const float4* cp = reinterpret_cast<const float4*>(a.cos_t + (size_t)ad * 64 + cc * 8);
+      const float4* sp = reinterpret_cast<const float4*>(a.sin_t + (size_t)ad * 64 + cc * 8);
+      const float4 c0 = cp[0], c1 = cp[1], s0 = sp[0], s1 = sp[1];
+      cs[0] = make_float2(c0.x, c0.y); cs[1] = make_float2(c0.z, c0.w);
+      cs[2] = make_float2(c1.x, c1.y); cs[3] = make_float2(c1.z, c1.w);
+      sn[0] = make_float2(sg * s0.x, sg * s0.y); sn[1] = make_float2(sg * s0.z, sg * s0.w);
+      sn[2] = make_float2(sg * s1.x, sg * s1.y); sn[3] = make_float2(sg * s1.z, sg * s1.w);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) ns[k] = make_float2(-sn[k].x, -sn[k].y);
+      dcache = d;
+    };
+    // (a, b) -> (a·c − b·s, b·c + a·s) on two NeoX pairs at once (FFMA2/FMUL2: per lane the same
+    // roundings as rebase_pair)
+    auto rot = [&](uint32_t& xa, uint32_t& xb, int k) {
+      const float2 av = make_float2(__uint_as_float(xa << 16), __uint_as_float(xa & 0xFFFF0000u));
+      const float2 bv = make_float2(__uint_as_float(xb << 16), __uint_as_float(xb & 0xFFFF0000u));
+      const float2 ra = fma2(av, cs[k], mul2(bv, ns[k]));
+      const float2 rb = fma2(bv, cs[k], mul2(av, sn[k]));
+      xa = pack_bf16(ra.x, ra.y);
+      xb = pack_bf16(rb.x, rb.y);
+    };
+    for (int t = 0; t < n; ++t) {
+      const int s = t % S;
+      int dl[8];
+#pragma unroll
+      for (int m = 0; m < 8; ++m) dl[m] = bd[min((j0 + t) * 8 + m, last_blk)];
+      // the common case (one Δ per tile): fetch its angles while the TMA is in flight
+      int dfirst = 0;
+#pragma unroll
+      for (int m = 7; m >= 0; --m) dfirst = dl[m] ? dl[m] : dfirst;
+      if (dfirst != 0 && dfirst != dcache) load_angles(dfirst);
+      mbar_wait(k_full + 8 * s, (t / S) & 1);
+      const uint32_t h0 = base + kK + (2 * s) * kTile + phys, h1 = h0 + kTile;
+#pragma unroll
+      for (int m0 = 0; m0 < 8; m0 += 4) {
+        uint4 xa[4], xb[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (dl[m0 + j]) {
+            xa[j] = lds128(h0 + (m0 + j) * 2048);
+            xb[j] = lds128(h1 + (m0 + j) * 2048);
+          }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int d = dl[m0 + j];
+          if (d == 0) continue;
+          if (d != dcache) load_angles(d);  // a chunk boundary inside the tile
+          rot(xa[j].x, xb[j].x, 0);
+          rot(xa[j].y, xb[j].y, 1);
+          rot(xa[j].z, xb[j].z, 2);
+          rot(xa[j].w, xb[j].w, 3);
+          sts128(h0 + (m0 + j) * 2048, xa[j]);
+          sts128(h1 + (m0 + j) * 2048, xb[j]);
+        }
+      }
+      fence_async_smem();  // generic-proxy smem writes -> visible to the tcgen05.mma operand reads
+      __syncwarp();
+      if (lane == 0) mbar_arrive(k_rot + 8 * s);
     }
   } else {
     // ------------------------------------------------------------------ softmax warps
@@ -450,15 +527,25 @@ static cudaError_t launch_attn_g(const CUtensorMap& tmQ, const CUtensorMap& tmK,
                                  const CUtensorMap& tmK8, const CUtensorMap& tmV8, const AttnArgs& a, cudaStream_t st) {
   dim3 grid(a.n_work, a.Hkv);
   (void)tmQ;  // Q rows are loaded into TMEM by the softmax warps (AttnArgs::Q)
-  CUDA_TRY_LAUNCH(launch_k(attn_tc_kernel<G>, dim3(grid), dim3(320), attn::kSmem, st, tmK, tmV, tmK8, tmV8, a));
+  if (a.bdelta)
+    CUDA_TRY_LAUNCH(launch_k(attn_tc_kernel<G, true>, dim3(grid), dim3(448), attn::kSmem, st, tmK, tmV, tmK8, tmV8, a));
+  else
+    CUDA_TRY_LAUNCH(launch_k(attn_tc_kernel<G, false>, dim3(grid), dim3(320), attn::kSmem, st, tmK, tmV, tmK8, tmV8, a));
   return cudaGetLastError();
 }
 
+template <int G>
+static cudaError_t prepare_g() {
+  cudaError_t e = cudaFuncSetAttribute(attn_tc_kernel<G, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, attn::kSmem);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(attn_tc_kernel<G, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, attn::kSmem);
+  return e;
+}
+
 cudaError_t prepare_attention() {
-  cudaError_t e = cudaFuncSetAttribute(attn_tc_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, attn::kSmem);
-  if (e == cudaSuccess) e = cudaFuncSetAttribute(attn_tc_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, attn::kSmem);
-  if (e == cudaSuccess) e = cudaFuncSetAttribute(attn_tc_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, attn::kSmem);
-  if (e == cudaSuccess) e = cudaFuncSetAttribute(attn_tc_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, attn::kSmem);
+  cudaError_t e = prepare_g<1>();
+  if (e == cudaSuccess) e = prepare_g<2>();
+  if (e == cudaSuccess) e = prepare_g<4>();
+  if (e == cudaSuccess) e = prepare_g<8>();
   return e;
 }
 
@@ -534,7 +621,9 @@ template <int D, bool F32>
 __global__ void attn_simt_kernel(const void* __restrict__ Q, const void* __restrict__ Kp, const void* __restrict__ Vp,
                                  const int32_t* __restrict__ row_seq, const int32_t* __restrict__ seq_bt_off,
                                  const int32_t* __restrict__ bt, const int32_t* __restrict__ row_pos,
-                                 void* __restrict__ O, int M, int Hq, int Hkv, float scale) {
+                                 void* __restrict__ O, int M, int Hq, int Hkv, float scale,
+                                 const int32_t* __restrict__ bdelta, const float* __restrict__ cos_t,
+                                 const float* __restrict__ sin_t) {
   PIC_PDL_ENTRY();
   const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
@@ -546,16 +635,42 @@ __global__ void attn_simt_kernel(const void* __restrict__ Q, const void* __restr
   float q[D];
 #pragma unroll
   for (int i = 0; i < D; ++i) q[i] = ldx<F32>(Q, ((size_t)row * Hq + head) * D + i);
+  const int* tbd = bdelta ? bdelta + seq_bt_off[row_seq[row]] : nullptr;
   auto kv_off = [&](int key) -> size_t {
     const int blk = tb[key / 16];
     return (((size_t)blk * Hkv + g) * 16 + (key % 16)) * D;
   };
+  // key row of `key` at its linked position: a shared chunk-store block (f3) is re-based by its Δ on
+  // load with the a2 arithmetic (rebase_pair, then the pool's precision), so the row equals the copy
+  // path's linked row
+  auto load_k = [&](int key, size_t off, float* kr) {
+#pragma unroll
+    for (int i = 0; i < D; ++i) kr[i] = ldx<F32>(Kp, off + i);
+    const int dl = tbd ? tbd[key / 16] : 0;
+    if (dl == 0) return;
+    const int ad = dl < 0 ? -dl : dl;
+    const float sg = dl < 0 ? -1.f : 1.f;
+#pragma unroll
+    for (int j = 0; j < D / 2; ++j) {
+      float ra, rb;
+      rebase_pair(kr[j], kr[j + D / 2], cos_t[(size_t)ad * (D / 2) + j], sg * sin_t[(size_t)ad * (D / 2) + j], ra, rb);
+      if constexpr (F32) {
+        kr[j] = ra;
+        kr[j + D / 2] = rb;
+      } else {
+        kr[j] = __bfloat162float(__float2bfloat16(ra));
+        kr[j + D / 2] = __bfloat162float(__float2bfloat16(rb));
+      }
+    }
+  };
   float mx = -INFINITY;
   for (int key = lane; key <= pos; key += 32) {
     const size_t off = kv_off(key);
+    float kr[D];
+    load_k(key, off, kr);
     float s = 0.f;
 #pragma unroll
-    for (int i = 0; i < D; ++i) s += q[i] * ldx<F32>(Kp, off + i);
+    for (int i = 0; i < D; ++i) s += q[i] * kr[i];
     mx = fmaxf(mx, s * scale);
   }
   mx = warp_max(mx);
@@ -564,9 +679,11 @@ __global__ void attn_simt_kernel(const void* __restrict__ Q, const void* __restr
   for (int i = 0; i < D; ++i) o[i] = 0.f;
   for (int key = lane; key <= pos; key += 32) {
     const size_t off = kv_off(key);
+    float kr[D];
+    load_k(key, off, kr);
     float s = 0.f;
 #pragma unroll
-    for (int i = 0; i < D; ++i) s += q[i] * ldx<F32>(Kp, off + i);
+    for (int i = 0; i < D; ++i) s += q[i] * kr[i];
     const float p = expf(s * scale - mx);
     l += p;
 #pragma unroll
@@ -589,12 +706,13 @@ __global__ void attn_simt_kernel(const void* __restrict__ Q, const void* __restr
 
 cudaError_t launch_attention_simt(const void* Q, const void* Kpool_l, const void* Vpool_l, const int32_t* row_seq,
                                   const int32_t* seq_bt_off, const int32_t* bt, const int32_t* row_pos, void* O,
-                                  int M, int Hq, int Hkv, int D, float scale, cudaStream_t st, int f32) {
+                                  int M, int Hq, int Hkv, int D, float scale, cudaStream_t st, int f32,
+                                  const int32_t* bdelta, const float* cos_t, const float* sin_t) {
   const int warps = M * Hq;
   dim3 grid((warps + 3) / 4), block(128);
 #define SIMT_L(DD, FF)                                                                                              \
   CUDA_TRY_LAUNCH(launch_k(attn_simt_kernel<DD, FF>, dim3(grid), dim3(block), 0, st, Q, Kpool_l, Vpool_l, row_seq,  \
-                           seq_bt_off, bt, row_pos, O, M, Hq, Hkv, scale))
+                           seq_bt_off, bt, row_pos, O, M, Hq, Hkv, scale, bdelta, cos_t, sin_t))
   if (f32) {
     switch (D) {
       case 16: SIMT_L(16, true); break;

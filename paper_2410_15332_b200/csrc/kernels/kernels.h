@@ -139,6 +139,13 @@ struct AttnArgs {
   int static_plan;           // 1: work/tiles/row_pos/bt were uploaded before the launch (read before PDL wait)
   const void* kpool;         // K/V pools (bf16 [L][NB][Hkv][16][128]) for the L2 prefetch; null: none
   const void* vpool;
+  // Shared-block link: per block-table entry, the re-base Δ still to apply to that
+  // block's keys (a chunk-store block linked by reference; 0 = a linked block already holding keys at
+  // their linked positions).  Null: no entry is shared.  The kernel rotates such K tiles in shared
+  // memory after TMA, with the a2 arithmetic (rebase_pair), before Q·Kᵀ.
+  const int32_t* bdelta;
+  const float* cos_t;        // [max_pos][64] fp32 RoPE table (re-base angles |Δ|·θ_j)
+  const float* sin_t;
 };
 // Balanced split-KV schedule: each q-tile t (KV extent n_kv[t] 128-key tiles) gets
 // ceil(n_kv[t] / budget) splits, budget = ceil(Σ n_kv · Hkv / target_ctas); splits <= 32.
@@ -151,9 +158,12 @@ cudaError_t launch_attention_tc(const CUtensorMap& tmQ, const CUtensorMap& tmK, 
 cudaError_t launch_attn_combine(const float* o_part, const float* ml_part, const int32_t* row_nsplit, void* O, int M,
                                 int Hq, int D, cudaStream_t st);
 // generic-D SIMT attention (tiny shapes D in {16,32,64}; any D <= 128 in the fp32 debug build); writes O directly
+// bdelta (nullable): per block-table entry, the re-base Δ to apply to that block's keys on load (f3 shared blocks)
 cudaError_t launch_attention_simt(const void* Q, const void* Kpool_l, const void* Vpool_l, const int32_t* row_seq,
                                   const int32_t* seq_bt_off, const int32_t* bt, const int32_t* row_pos, void* O,
-                                  int M, int Hq, int Hkv, int D, float scale, cudaStream_t st, int f32 = 0);
+                                  int M, int Hq, int Hkv, int D, float scale, cudaStream_t st, int f32 = 0,
+                                  const int32_t* bdelta = nullptr, const float* cos_t = nullptr,
+                                  const float* sin_t = nullptr);
 // fp32 debug build GEMM (CUDA cores, exact products): P[M][N] = A[M][K] (fp32) · B[N][K]^T (bf16 weights)
 cudaError_t launch_gemm_simt_f32(const float* A, const void* B, float* out, int M, int N, int K, cudaStream_t st);
 

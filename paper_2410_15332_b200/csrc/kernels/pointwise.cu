@@ -459,8 +459,11 @@ __global__ void kv_link_kernel(uint4* __restrict__ Kpool, uint4* __restrict__ Vp
       const float a0 = __uint_as_float(a4[k] << 16), a1 = __uint_as_float(a4[k] & 0xFFFF0000u);
       const float b0 = __uint_as_float(b4[k] << 16), b1 = __uint_as_float(b4[k] & 0xFFFF0000u);
       const float c0 = cs[2 * k], c1 = cs[2 * k + 1], s0 = sg * sn[2 * k], s1 = sg * sn[2 * k + 1];
-      oa[k] = pack_bf16(a0 * c0 - b0 * s0, a1 * c1 - b1 * s1);
-      ob[k] = pack_bf16(b0 * c0 + a0 * s0, b1 * c1 + a1 * s1);
+      float ra0, rb0, ra1, rb1;
+      rebase_pair(a0, b0, c0, s0, ra0, rb0);
+      rebase_pair(a1, b1, c1, s1, ra1, rb1);
+      oa[k] = pack_bf16(ra0, ra1);
+      ob[k] = pack_bf16(rb0, rb1);
     }
     Kpool[dof + c] = make_uint4(oa[0], oa[1], oa[2], oa[3]);
     Kpool[dof + c + cK] = make_uint4(ob[0], ob[1], ob[2], ob[3]);
@@ -496,8 +499,10 @@ __global__ void kv_link_f32_kernel(float* __restrict__ Kpool, float* __restrict_
     const int dl = rebase ? delta[w] : 0;
     const int ad = dl < 0 ? -dl : dl;
     const float c = cos_t[(size_t)ad * half + j], sn = (dl < 0 ? -1.f : 1.f) * sin_t[(size_t)ad * half + j];
-    Kpool[dof + j] = dl ? a * c - b * sn : a;
-    Kpool[dof + j + half] = dl ? b * c + a * sn : b;
+    float ra = a, rb = b;
+    if (dl) rebase_pair(a, b, c, sn, ra, rb);
+    Kpool[dof + j] = ra;
+    Kpool[dof + j + half] = rb;
   }
 }
 

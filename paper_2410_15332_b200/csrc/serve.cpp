@@ -77,11 +77,11 @@ extern "C" pic_status pic_serve_poisson(pic_engine* e, const pic_serve_config* c
   for (int k = 0; k < cfg->n_users; ++k) {
     const int cap = e->lim.max_tokens;
     std::vector<int32_t> sel(cap), tok(cap), src(2 * (size_t)cap), ch(3 * (size_t)cap), bt(cap), slot(cap);
-    pic_plan_out po{cap, 0, 0, 0, 0, sel.data(), tok.data(), src.data(), ch.data(), bt.data(), slot.data()};
+    pic_plan_out po{cap, 0, 0, 0, 0, sel.data(), tok.data(), src.data(), ch.data(), bt.data(), slot.data(), nullptr, 0};
     pic_status s = pic_plan(e, cfg->user_segs[k], cfg->user_n_segs[k], &cfg->params, &po);
     if (s != PIC_OK) return s;
     ntok[k] = po.n_tokens;
-    blocks[k] = (po.n_tokens + 15) / 16;
+    blocks[k] = po.n_blocks - po.n_shared;  // fresh blocks only (kv_share links chunk-store blocks by reference)
     rows[k] = cb ? po.n_tokens : po.n_sel;
     if (rows[k] > e->lim.max_rows) return PIC_E_CAPACITY;
   }

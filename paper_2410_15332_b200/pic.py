@@ -51,7 +51,7 @@ class CompileOptionsC(C.Structure):
 class LinkParamsC(C.Structure):
     _fields_ = [("alg", C.c_int32), ("k", C.c_int32), ("r_percent", C.c_int32), ("check_layer", C.c_int32),
                 ("rebase", C.c_int32), ("use_graph", C.c_int32), ("sel_override", C.POINTER(C.c_int32)),
-                ("n_sel_override", C.c_int32), ("debug_hidden", C.POINTER(C.c_float))]
+                ("n_sel_override", C.c_int32), ("debug_hidden", C.POINTER(C.c_float)), ("kv_share", C.c_int32)]
 
 
 class LinkResultC(C.Structure):
@@ -64,7 +64,8 @@ class PlanOutC(C.Structure):
     _fields_ = [("capacity", C.c_int32), ("n_tokens", C.c_int32), ("n_sel", C.c_int32), ("n_chunks", C.c_int32),
                 ("n_blocks", C.c_int32), ("sel", C.POINTER(C.c_int32)), ("tok", C.POINTER(C.c_int32)),
                 ("src", C.POINTER(C.c_int32)), ("chunks", C.POINTER(C.c_int32)),
-                ("block_table", C.POINTER(C.c_int32)), ("slot", C.POINTER(C.c_int32))]
+                ("block_table", C.POINTER(C.c_int32)), ("slot", C.POINTER(C.c_int32)),
+                ("block_delta", C.POINTER(C.c_int32)), ("n_shared", C.c_int32)]
 
 
 class DecodeResultC(C.Structure):
@@ -99,7 +100,7 @@ class KernelStatC(C.Structure):
 
 # every symbol include/pic.h and include/pic_test.h declare
 EXPORTS = ["pic_arena_bytes", "pic_engine_create", "pic_engine_destroy", "pic_generate_context_cache", "pic_link",
-           "pic_link_batch", "pic_plan", "pic_linked_export", "pic_linked_info", "pic_linked_release",
+           "pic_link_batch", "pic_plan", "pic_linked_export", "pic_linked_info", "pic_linked_sharing", "pic_linked_release",
            "pic_cache_export", "pic_cache_info", "pic_expire_cache", "pic_read_weights", "pic_get_stats",
            "pic_last_error", "pic_status_string", "pic_arena_bytes_tp", "pic_engine_create_tp", "pic_tp_ipc_handle",
            "pic_tp_connect", "pic_generate_context_cache_ex", "pic_decode", "pic_serve_poisson", "pic_serve_arrivals", "pic_set_profiling", "pic_get_profile", "pic_test_gemm", "pic_test_attention", "pic_test_kv_link", "pic_bench_gemm", "pic_bench_attention", "pic_test_gemm_swiglu"]
@@ -143,6 +144,7 @@ def lib() -> C.CDLL:
         L.pic_plan.argtypes = [C.c_void_p, P(SegmentC), C.c_int32, P(LinkParamsC), P(PlanOutC)]
         L.pic_linked_export.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p]
         L.pic_linked_info.argtypes = [C.c_void_p, C.c_void_p, P(C.c_int32), P(C.c_int32)]
+        L.pic_linked_sharing.argtypes = [C.c_void_p, C.c_void_p, P(C.c_int32), P(C.c_int32)]
         L.pic_linked_release.argtypes = [C.c_void_p, C.c_void_p]
         L.pic_cache_export.argtypes = [C.c_void_p, C.c_uint64, C.c_int32, C.c_void_p, C.c_void_p]
         L.pic_cache_info.argtypes = [C.c_void_p, C.c_uint64, P(C.c_int32), P(C.c_int32)]
@@ -268,6 +270,7 @@ class Engine:
         self._cfg = config_struct(cfg)
         self._lim = LimitsC(num_blocks, max_rows, max_tokens, max_requests)
         self.max_tokens = max_tokens
+        self.kv_share = False  # default of pic_link_params.kv_share (shared-block link, f3) for this engine's calls
         self._h = C.c_void_p()
         self.arena = None
         self.device = device
@@ -339,9 +342,11 @@ class Engine:
         return [int(ids[i]) for i in range(n)]
 
     # ------------------------------------------------------------------ link
-    def _params(self, alg, check_layer=1, rebase=True, use_graph=True, sel_override=None, debug_hidden=None):
+    def _params(self, alg, check_layer=1, rebase=True, use_graph=True, sel_override=None, debug_hidden=None,
+                kv_share=None):
         a, k, r = parse_alg(alg)
-        p = LinkParamsC(a, k, r, check_layer, int(rebase), int(use_graph), None, 0, None)
+        share = self.kv_share if kv_share is None else kv_share
+        p = LinkParamsC(a, k, r, check_layer, int(rebase), int(use_graph), None, 0, None, int(bool(share)))
         keep = []
         if sel_override is not None:
             so = np.ascontiguousarray(sel_override, dtype=np.int32)
@@ -354,13 +359,13 @@ class Engine:
 
     def link(self, segments, alg: str, *, check_layer: int = 1, rebase: bool = True, use_graph: bool = True,
              want_logits: bool = True, logits_dev=None, keep_linked: bool = False, sel_override=None,
-             debug_hidden: bool = False, want_selected: bool = False) -> LinkOutput:
+             debug_hidden: bool = False, want_selected: bool = False, kv_share: Optional[bool] = None) -> LinkOutput:
         segs = _Segs(segments)
         hid = None
         N = self.plan(segments, alg)["n_tokens"] if (debug_hidden or want_selected) else 0
         if debug_hidden:
             hid = np.full((self.cfg.n_layers, N, self.cfg.d_model), np.nan, dtype=np.float32)
-        p, keep = self._params(alg, check_layer, rebase, use_graph, sel_override, hid)
+        p, keep = self._params(alg, check_layer, rebase, use_graph, sel_override, hid, kv_share)
         res = LinkResultC()
         logits = None
         if want_logits:
@@ -380,12 +385,12 @@ class Engine:
                           hid)
 
     def link_batch(self, requests, alg: str, *, use_graph: bool = True, want_logits: bool = True,
-                   keep_linked: bool = False) -> List[LinkOutput]:
+                   keep_linked: bool = False, kv_share: Optional[bool] = None) -> List[LinkOutput]:
         n = len(requests)
         segs = [_Segs(r) for r in requests]
         arrp = (C.POINTER(SegmentC) * n)(*[C.cast(s.arr, C.POINTER(SegmentC)) for s in segs])
         ns = (C.c_int32 * n)(*[s.n for s in segs])
-        p, keep = self._params(alg, use_graph=use_graph)
+        p, keep = self._params(alg, use_graph=use_graph, kv_share=kv_share)
         res = (LinkResultC * n)()
         logits = None
         if want_logits:
@@ -420,33 +425,36 @@ class Engine:
                             np.array([res[i].n_tokens for i in range(n)], dtype=np.int64))
 
     def serve_poisson(self, requests, alg: str, rate: float, duration_s: float, *, seed: int = 0x5E12E,
-                      max_batch: Optional[int] = None, check_layer: int = 1, use_graph: bool = False) -> dict:
+                      max_batch: Optional[int] = None, check_layer: int = 1, use_graph: bool = False,
+                      kv_share: Optional[bool] = None) -> dict:
         """Open-loop Poisson serving (pic_serve_poisson, f4): user u resends requests[u] at rate/len(requests).
         Eager launches by default: batch compositions vary, so per-shape graphs would be captured per call."""
         n = len(requests)
         segs = [_Segs(r) for r in requests]
         arrp = (C.POINTER(SegmentC) * n)(*[C.cast(x.arr, C.POINTER(SegmentC)) for x in segs])
         ns = (C.c_int32 * n)(*[x.n for x in segs])
-        p, keep = self._params(alg, check_layer=check_layer, use_graph=use_graph)
+        p, keep = self._params(alg, check_layer=check_layer, use_graph=use_graph, kv_share=kv_share)
         cfgc = ServeConfigC(n, C.cast(arrp, C.c_void_p), ns, float(rate), float(duration_s), int(seed),
                             int(max_batch or self._lim.max_requests), p)
         out = ServeStatsC()
         check(lib().pic_serve_poisson(self._h, C.byref(cfgc), self._stream, C.byref(out)))
         return {k: getattr(out, k) for k, _ in ServeStatsC._fields_}
 
-    def plan(self, segments, alg: str) -> dict:
+    def plan(self, segments, alg: str, kv_share: Optional[bool] = None) -> dict:
         segs = _Segs(segments)
-        p, _ = self._params(alg)
+        p, _ = self._params(alg, kv_share=kv_share)
         cap = self.max_tokens
+        names = ("sel", "tok", "src", "chunks", "block_table", "slot", "block_delta")
         bufs = {k: np.zeros(n * cap, dtype=np.int32) for k, n in
-                (("sel", 1), ("tok", 1), ("src", 2), ("chunks", 3), ("block_table", 1), ("slot", 1))}
-        out = PlanOutC(cap, 0, 0, 0, 0, *[_ptr(bufs[k]) for k in
-                                          ("sel", "tok", "src", "chunks", "block_table", "slot")])
+                (("sel", 1), ("tok", 1), ("src", 2), ("chunks", 3), ("block_table", 1), ("slot", 1),
+                 ("block_delta", 1))}
+        out = PlanOutC(cap, 0, 0, 0, 0, *[_ptr(bufs[k]) for k in names], 0)
         check(lib().pic_plan(self._h, segs.arr, segs.n, C.byref(p), C.byref(out)))
         N, ns, nc, nb = out.n_tokens, out.n_sel, out.n_chunks, out.n_blocks
         return {"n_tokens": N, "sel": bufs["sel"][:ns].copy(), "tok": bufs["tok"][:N].copy(),
                 "src": bufs["src"][:2 * N].reshape(N, 2).copy(), "chunks": bufs["chunks"][:3 * nc].reshape(nc, 3).copy(),
-                "block_table": bufs["block_table"][:nb].copy(), "slot": bufs["slot"][:ns].copy()}
+                "block_table": bufs["block_table"][:nb].copy(), "slot": bufs["slot"][:ns].copy(),
+                "block_delta": bufs["block_delta"][:nb].copy(), "n_shared": out.n_shared}
 
     # ------------------------------------------------------------------ exports / lifecycle
     @property
@@ -473,6 +481,15 @@ class Engine:
         bt = np.zeros((n.value + 15) // 16, dtype=np.int32)
         check(lib().pic_linked_info(self._h, C.c_void_p(linked), C.byref(n), _ptr(bt)))
         return bt
+
+    def linked_sharing(self, linked: int) -> Tuple[int, np.ndarray]:
+        """(blocks linked by reference, per-block Δ) of a shared-block link (kv_share, f3)."""
+        n = C.c_int32()
+        check(lib().pic_linked_info(self._h, C.c_void_p(linked), C.byref(n), None))
+        bd = np.zeros((n.value + 15) // 16, dtype=np.int32)
+        ns = C.c_int32()
+        check(lib().pic_linked_sharing(self._h, C.c_void_p(linked), C.byref(ns), _ptr(bd)))
+        return ns.value, bd
 
     def release(self, linked: int) -> None:
         check(lib().pic_linked_release(self._h, C.c_void_p(linked)))

@@ -182,3 +182,58 @@ def test_legolink0_planner_and_variant_error():
     with pytest.raises(B.PicError) as e:
         eng.plan([("cached", plain[0]), ("cached", eids[1])], "legolink0")
     assert e.value.name == "PIC_E_VARIANT"
+
+
+def test_shared_block_plan_bit_exact_vs_oracle():
+    """f3 shared-block link (kv_share): the planner's block table / per-block Δ equal the oracle's
+    layout model (share_blocks + lowest-free-first fresh blocks) on cfg1 and 100 permutations
+    (dynamic-first, interleaved, repeated ids), for every algorithm; CacheBlend and FR share nothing."""
+    w = sg.cfg1()
+    eng = host_engine()
+    eids = eng.generate_context_cache(w.chunks)
+    st, oids = oracle_store(sg.TINY, w.chunks)
+    alloc = P.BlockAllocator(256)
+    chunk_blocks = {oid: alloc.alloc(P.n_blocks(len(c))) for oid, c in zip(oids, w.chunks)}
+    n_shared_total = 0
+    for segs in [w.requests[0]] + sg.permuted_requests(w, 100):
+        for alg in ("naive", "fr", "legolink:4", "legolink:16", "legolink:40", "cacheblend:15"):
+            pe = eng.plan(to_engine_segs(segs, eids), alg, kv_share=True)
+            po = P.plan(st, to_engine_segs(segs, oids), alg)
+            shared, delta = P.share_blocks(po, chunk_blocks)
+            n_fresh = sum(b < 0 for b in shared)
+            fresh = iter(alloc.peek(n_fresh))
+            bt = [b if b >= 0 else next(fresh) for b in shared]
+            assert pe["block_table"].tolist() == bt, (alg, segs)
+            assert pe["block_delta"].tolist() == delta
+            assert pe["n_shared"] == len(shared) - n_fresh
+            assert np.array_equal(pe["slot"], P.slot_map(bt, po.sel))
+            if alg in ("fr", "cacheblend:15"):
+                assert pe["n_shared"] == 0
+            n_shared_total += pe["n_shared"]
+            # without kv_share the plan is the copy layout
+            assert eng.plan(to_engine_segs(segs, eids), alg)["n_shared"] == 0
+    assert n_shared_total > 0
+
+
+def test_shared_block_plan_alignment_rules():
+    """A chunk placed at a 16-misaligned start shares nothing; a chunk's partial last block is never
+    shared; Naive shares every full block of an aligned chunk with Δ = s_c (0 for the index-0 chunk)."""
+    eng = host_engine()
+    ids = eng.generate_context_cache([np.ones(40, np.int32), np.ones(32, np.int32)])
+    blocks = [eng.cache_blocks(i).tolist() for i in ids]
+    # [C0 (40 rows: 2 full blocks + 8), C1 at 40 (misaligned), 5 dynamic]
+    pe = eng.plan([("cached", ids[0]), ("cached", ids[1]), ("tokens", np.ones(5, np.int32))], "naive",
+                  kv_share=True)
+    assert pe["block_table"][:2].tolist() == blocks[0][:2] and pe["block_delta"].tolist()[:2] == [0, 0]
+    assert pe["n_shared"] == 2
+    # [16 dynamic, C1 at 16 (aligned), C0 at 48 (aligned), query]
+    pe = eng.plan([("tokens", np.ones(16, np.int32)), ("cached", ids[1]), ("cached", ids[0]),
+                   ("tokens", np.ones(3, np.int32))], "naive", kv_share=True)
+    assert pe["block_table"][1:3].tolist() == blocks[1] and pe["block_delta"][1:3].tolist() == [16, 16]
+    assert pe["block_table"][3:5].tolist() == blocks[0][:2] and pe["block_delta"][3:5].tolist() == [48, 48]
+    assert pe["n_shared"] == 4
+    # LegoLink-16 recomputes the first block of each non-initial chunk
+    pe = eng.plan([("tokens", np.ones(16, np.int32)), ("cached", ids[1]), ("cached", ids[0]),
+                   ("tokens", np.ones(3, np.int32))], "legolink:16", kv_share=True)
+    assert pe["block_delta"].tolist() == [0, 0, 16, 0, 48, 0]
+    assert pe["n_shared"] == 2

@@ -1,0 +1,188 @@
+"""Shared-block link (pic_link_params.kv_share): chunk-store blocks are linked by
+reference and the attention kernels re-base their keys when they load them (rebase_pair, the a2
+arithmetic), so the result must be BIT-IDENTICAL to the copy path (kv_share = 0): logits, first
+token, every exported linked K/V row of every layer, and later decode steps.  The copy path itself
+is held to the oracle by test_gpu_link / test_gpu_decode; one oracle check is repeated here.
+
+Also: block accounting (only fresh blocks are taken from the pool; shared blocks are reference
+counted, so expiring a chunk under a live linked cache keeps its rows) and the fp32 debug build."""
+from dataclasses import replace
+
+import numpy as np
+import pytest
+
+import seedgen as sg
+from oracle import model as M
+from oracle import pic as P
+from paper_2410_15332_b200 import pic as B
+
+pytestmark = pytest.mark.gpu
+ALGS = ["naive", "legolink:4", "legolink:16", "fr"]
+
+
+def rel(a, b):
+    a, b = np.asarray(a, np.float64), np.asarray(b, np.float64)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+class Setup:
+    def __init__(self, cfg, dummy_prefix=0):
+        self.cfg = cfg
+        self.w = sg.cfg1(model=cfg)
+        self.eng = B.Engine(cfg, num_blocks=512, max_rows=1024, max_tokens=4096, max_requests=4, device=0)
+        self.eids = self.eng.generate_context_cache(self.w.chunks, dummy_prefix=dummy_prefix)
+
+    def segs(self, segs):
+        return [("cached", self.eids[s.chunk]) if s.cached else ("tokens", s.tokens) for s in segs]
+
+
+@pytest.fixture(scope="module", params=[sg.TINY, sg.TINY_GQA, sg.TINY_D128], ids=lambda c: c.name)
+def setup(request):
+    s = Setup(request.param)
+    yield s
+    s.eng.close()
+
+
+def link_both(s, segs, alg, **kw):
+    """(copy, shared) link outputs with their exported linked K/V of every layer."""
+    outs = []
+    for share in (False, True):
+        free0 = s.eng.stats()["free_blocks"]
+        o = s.eng.link(s.segs(segs), alg, keep_linked=True, kv_share=share, **kw)
+        used = free0 - s.eng.stats()["free_blocks"]
+        kv = [s.eng.linked_export(o.linked, l) for l in range(s.cfg.n_layers)]
+        ns, bd = s.eng.linked_sharing(o.linked)
+        outs.append((o, kv, used, ns, bd))
+    return outs
+
+
+def assert_identical(a, b):
+    (oa, kva, _, _, _), (ob, kvb, _, _, _) = a, b
+    assert np.array_equal(oa.logits, ob.logits)
+    assert oa.first_token == ob.first_token
+    for l, ((ka, va), (kb, vb)) in enumerate(zip(kva, kvb)):
+        assert np.array_equal(ka, kb), l
+        assert np.array_equal(va, vb), l
+
+
+@pytest.mark.parametrize("alg", ALGS)
+def test_shared_link_bit_identical_to_copy(setup, alg):
+    s = setup
+    any_shared = 0
+    for segs in [s.w.requests[0]] + sg.permuted_requests(s.w, 6):
+        copy, shared = link_both(s, segs, alg)
+        try:
+            assert_identical(copy, shared)
+            n_blocks = (copy[0].n_tokens + 15) // 16
+            assert copy[3] == 0 and copy[2] == n_blocks
+            assert shared[2] == n_blocks - shared[3]          # only fresh blocks come from the pool
+            if alg == "fr":
+                assert shared[3] == 0
+            any_shared += shared[3]
+            # the plan agrees with what the link did
+            pe = s.eng.plan(s.segs(segs), alg, kv_share=True)
+            assert pe["n_shared"] == shared[3] and pe["block_delta"].tolist() == shared[4].tolist()
+        finally:
+            s.eng.release(copy[0].linked)
+            s.eng.release(shared[0].linked)
+    if alg != "fr":
+        assert any_shared > 0
+
+
+def test_shared_link_matches_oracle(setup):
+    s = setup
+    store = P.Store(M.Weights(s.cfg))
+    oids = store.compile(s.w.chunks)
+    segs = s.w.requests[0]
+    out = s.eng.link(s.segs(segs), "legolink:4", keep_linked=True, kv_share=True)
+    ref = P.link(store, [("cached", oids[x.chunk]) if x.cached else ("tokens", x.tokens) for x in segs], "legolink:4")
+    try:
+        assert s.eng.linked_sharing(out.linked)[0] > 0
+        assert rel(out.logits, ref.logits) < 2e-2
+        for l in range(s.cfg.n_layers):
+            k, v = s.eng.linked_export(out.linked, l)
+            assert rel(B.bf16_bits_to_f32(k), ref.K[l]) < 2e-2, l
+            assert rel(B.bf16_bits_to_f32(v), ref.V[l]) < 2e-2, l
+    finally:
+        s.eng.release(out.linked)
+
+
+def test_shared_decode_bit_identical(setup):
+    s = setup
+    segs = s.w.requests[0]
+    hs = [s.eng.link(s.segs(segs), "legolink:4", keep_linked=True, kv_share=share).linked for share in (False, True)]
+    try:
+        toks = [5, 17, 99, 3, 250, 7, 11, 13, 2, 1, 0, 8, 9, 10, 12, 14, 15, 16, 18, 19]
+        for t in toks:  # crosses a block boundary (N = 112 -> 132)
+            a = s.eng.decode([hs[0]], [t])
+            b = s.eng.decode([hs[1]], [t])
+            assert np.array_equal(a.logits, b.logits)
+        for l in range(s.cfg.n_layers):
+            ka, va = s.eng.linked_export(hs[0], l)
+            kb, vb = s.eng.linked_export(hs[1], l)
+            assert np.array_equal(ka, kb) and np.array_equal(va, vb)
+    finally:
+        for h in hs:
+            s.eng.release(h)
+
+
+def test_shared_blocks_survive_expiry():
+    """Expire a chunk while a linked cache shares its blocks: the rows stay (reference counted) and
+    return to the pool only when the linked cache is released (S:467 in-flight snapshot)."""
+    s = Setup(sg.TINY_D128)
+    try:
+        segs = s.w.requests[0]
+        out = s.eng.link(s.segs(segs), "naive", keep_linked=True, kv_share=True)
+        n_shared, _ = s.eng.linked_sharing(out.linked)
+        assert n_shared > 0
+        before = [s.eng.linked_export(out.linked, l) for l in range(s.cfg.n_layers)]
+        free0 = s.eng.stats()["free_blocks"]
+        for cid in s.eids:
+            assert s.eng.expire(cid)
+        freed = s.eng.stats()["free_blocks"] - free0
+        total_chunk_blocks = sum((len(c) + 15) // 16 for c in s.w.chunks)
+        assert freed == total_chunk_blocks - n_shared          # shared blocks are still held
+        # new compiles reuse only the freed blocks; the linked cache is untouched
+        s.eng.generate_context_cache([np.full(64, 7, np.int32)])
+        after = [s.eng.linked_export(out.linked, l) for l in range(s.cfg.n_layers)]
+        for (ka, va), (kb, vb) in zip(before, after):
+            assert np.array_equal(ka, kb) and np.array_equal(va, vb)
+        free1 = s.eng.stats()["free_blocks"]
+        s.eng.release(out.linked)
+        assert s.eng.stats()["free_blocks"] == free1 + (out.n_tokens + 15) // 16
+    finally:
+        s.eng.close()
+
+
+def test_shared_legolink0_negative_delta():
+    """LegoLink-0 links dummy-prefix chunks with Δ = s_c − m (negative for the first chunk):
+    the shared path rotates by negative Δ exactly like the copy path."""
+    s = Setup(sg.TINY_D128, dummy_prefix=4)
+    try:
+        for segs in [s.w.requests[0]] + sg.permuted_requests(s.w, 3):
+            copy, shared = link_both(s, segs, "legolink0")
+            try:
+                assert_identical(copy, shared)
+                if not segs[0].cached:
+                    continue
+                assert shared[3] > 0 and (shared[4] < 0).any()
+            finally:
+                s.eng.release(copy[0].linked)
+                s.eng.release(shared[0].linked)
+    finally:
+        s.eng.close()
+
+
+def test_shared_link_fp32_debug_bit_identical():
+    s = Setup(replace(sg.TINY_D128, dtype=1))
+    try:
+        for alg in ("naive", "legolink:4"):
+            copy, shared = link_both(s, s.w.requests[0], alg)
+            try:
+                assert_identical(copy, shared)
+                assert shared[3] > 0
+            finally:
+                s.eng.release(copy[0].linked)
+                s.eng.release(shared[0].linked)
+    finally:
+        s.eng.close()
