@@ -215,7 +215,7 @@ def main():
                     help="tensor parallel over all ranks (heads/MLP columns sharded, fused peer-memory all-reduce); "
                          "strong scaling of one request instead of data parallel requests")
     ap.add_argument("--layers", type=int, default=None, help="truncate depth (functional runs only; marked in config)")
-    ap.add_argument("--kv-share", type=int, default=0, choices=[0, 1],
+    ap.add_argument("--kv-share", type=int, default=1, choices=[0, 1],
                     help="f3 shared-block link: chunk-store blocks linked by reference, keys re-based in the "
                          "attention K-tile load (pic_link_params.kv_share)")
     ap.add_argument("--decode-steps", type=int, default=32,

@@ -51,8 +51,12 @@ constexpr uint32_t kTmQ = 384;  // Q (bf16 pairs) [384, 448)
 
 // Both MMAs take their A operand from TMEM (Q for S = Q·Kᵀ, P for O += P·V), so shared memory only
 // carries K and V: per 128-key tile the smem traffic is the two TMA writes and the two B-operand reads.
+// ROT: kRotWarps extra warps re-base shared-block K tiles (f3), one per SMSP.  Measured (cfg4 attention,
+// 32 layers): 4 warps 26.3 ms, 2 warps 41.5 ms (the rotation is issue-bound and sits between the K TMA
+// and the S MMA); 4 warps cap the CTA at 128 registers per thread (14 warps), a few bytes of spill.
+constexpr int kRotWarps = 4;
 template <int G, bool ROT>
-__global__ void __launch_bounds__(ROT ? 448 : 320, 1)
+__global__ void __launch_bounds__(ROT ? 320 + 32 * kRotWarps : 320, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
                    const __grid_constant__ CUtensorMap tmK8, const __grid_constant__ CUtensorMap tmV8, const AttnArgs a) {
   griddep_launch();
@@ -82,7 +86,7 @@ __global__ void __launch_bounds__(ROT ? 448 : 320, 1)
       mbar_init(k_empty + 8 * s, 1);
       mbar_init(v_full + 8 * s, 1);
       mbar_init(v_empty + 8 * s, 1);
-      mbar_init(k_rot + 8 * s, 4);
+      mbar_init(k_rot + 8 * s, kRotWarps);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(s_full + 8 * b, 1);
@@ -240,7 +244,9 @@ __global__ void __launch_bounds__(ROT ? 448 : 320, 1)
     // every NeoX pair (j, j+64) of such rows by Δ of its block (the a2 arithmetic, rebase_pair, so the
     // tile equals the one a copied-and-re-based linked block would give).  In the SWIZZLE_128B tile
     // dims j and j+64 sit at the same offset of the two 64-column halves.  Thread u owns logical
-    // 16-B chunk cc = u & 7 (dims 8cc..8cc+7) of row rg = u >> 3 of each of the 8 paged blocks.
+    // 16-B chunk cc = u & 7 (dims 8cc..8cc+7) of rows rg + 8i (rg = u >> 3, i < 16/(4·kRotWarps)) of each
+    // of the 8 paged blocks (rows rg and rg + 8 share the swizzle phase).
+    constexpr int RPB = 16 / (4 * kRotWarps);  // rows per block per thread
     const int u = threadIdx.x - 320;
     const int cc = u & 7, rg = u >> 3;
     const uint32_t phys = (uint32_t)(((cc ^ (rg & 7)) << 4) + rg * 128);
@@ -283,26 +289,29 @@ __global__ void __launch_bounds__(ROT ? 448 : 320, 1)
       if (dfirst != 0 && dfirst != dcache) load_angles(dfirst);
       mbar_wait(k_full + 8 * s, (t / S) & 1);
       const uint32_t h0 = base + kK + (2 * s) * kTile + phys, h1 = h0 + kTile;
+      constexpr int BB = 4 / RPB;  // blocks per batch: 4 loads of each half in flight
 #pragma unroll
-      for (int m0 = 0; m0 < 8; m0 += 4) {
+      for (int m0 = 0; m0 < 8; m0 += BB) {
         uint4 xa[4], xb[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j)
-          if (dl[m0 + j]) {
-            xa[j] = lds128(h0 + (m0 + j) * 2048);
-            xb[j] = lds128(h1 + (m0 + j) * 2048);
+          if (dl[m0 + j / RPB]) {
+            const uint32_t o = (m0 + j / RPB) * 2048 + (j % RPB) * 1024;
+            xa[j] = lds128(h0 + o);
+            xb[j] = lds128(h1 + o);
           }
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          const int d = dl[m0 + j];
+          const int d = dl[m0 + j / RPB];
           if (d == 0) continue;
           if (d != dcache) load_angles(d);  // a chunk boundary inside the tile
           rot(xa[j].x, xb[j].x, 0);
           rot(xa[j].y, xb[j].y, 1);
           rot(xa[j].z, xb[j].z, 2);
           rot(xa[j].w, xb[j].w, 3);
-          sts128(h0 + (m0 + j) * 2048, xa[j]);
-          sts128(h1 + (m0 + j) * 2048, xb[j]);
+          const uint32_t o = (m0 + j / RPB) * 2048 + (j % RPB) * 1024;
+          sts128(h0 + o, xa[j]);
+          sts128(h1 + o, xb[j]);
         }
       }
       fence_async_smem();  // generic-proxy smem writes -> visible to the tcgen05.mma operand reads
@@ -528,7 +537,7 @@ static cudaError_t launch_attn_g(const CUtensorMap& tmQ, const CUtensorMap& tmK,
   dim3 grid(a.n_work, a.Hkv);
   (void)tmQ;  // Q rows are loaded into TMEM by the softmax warps (AttnArgs::Q)
   if (a.bdelta)
-    CUDA_TRY_LAUNCH(launch_k(attn_tc_kernel<G, true>, dim3(grid), dim3(448), attn::kSmem, st, tmK, tmV, tmK8, tmV8, a));
+    CUDA_TRY_LAUNCH(launch_k(attn_tc_kernel<G, true>, dim3(grid), dim3(320 + 32 * kRotWarps), attn::kSmem, st, tmK, tmV, tmK8, tmV8, a));
   else
     CUDA_TRY_LAUNCH(launch_k(attn_tc_kernel<G, false>, dim3(grid), dim3(320), attn::kSmem, st, tmK, tmV, tmK8, tmV8, a));
   return cudaGetLastError();

@@ -164,3 +164,30 @@ def test_long_context_16k_legolink_sampled_rows():
     eng.release(g.linked)
     eng.release(d.linked)
     eng.close()
+
+
+@pytest.mark.parametrize("which", ["cfg2", "cfg3", "cfg4"])
+def test_fullsize_shared_block_link_bit_identical(which):
+    """f3 shared-block link at full size in the bench's launch configuration (graphs, batched link for
+    cfg4): logits, first tokens and sampled layers' linked K/V are bit-identical to the copy path, which
+    the sampled-layer tests above hold to the oracle."""
+    w = {"cfg2": sg.cfg2, "cfg3": sg.cfg3}.get(which, lambda: sg.cfg4(n_requests=4))()
+    m = w.model
+    Ns = [sum(len(w.chunks[s.chunk]) if s.cached else len(s.tokens) for s in r) for r in w.requests]
+    eng = B.Engine(m, num_blocks=(sum(len(c) for c in w.chunks) + 2 * sum(Ns)) // 16 + 64, max_rows=4096,
+                   max_tokens=max(Ns) + 16, max_requests=len(w.requests), device=0)
+    try:
+        ids = eng.generate_context_cache(w.chunks)
+        reqs = [[("cached", ids[s.chunk]) if s.cached else ("tokens", s.tokens) for s in r] for r in w.requests]
+        outs = [eng.link_batch(reqs, w.alg, keep_linked=True, kv_share=share) for share in (False, True)]
+        shared = 0
+        for a, b in zip(*outs):
+            assert np.array_equal(a.logits, b.logits) and a.first_token == b.first_token
+            shared += eng.linked_sharing(b.linked)[0]
+            for l in (0, m.n_layers // 2, m.n_layers - 1):
+                ka, va = eng.linked_export(a.linked, l)
+                kb, vb = eng.linked_export(b.linked, l)
+                assert np.array_equal(ka, kb) and np.array_equal(va, vb), l
+        assert shared > 0
+    finally:
+        eng.close()
