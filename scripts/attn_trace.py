@@ -9,6 +9,7 @@ from paper_2410_15332_b200 import pic as B
 w = sg.cfg2() if len(sys.argv) < 2 else getattr(sg, sys.argv[1])()
 N = sum(len(w.chunks[s.chunk]) if s.cached else len(s.tokens) for s in w.requests[0])
 eng = B.Engine(w.model, num_blocks=(sum(len(c) for c in w.chunks) + 3 * N) // 16 + 64, max_rows=4096, max_tokens=N + 16, device=0)
+eng.kv_share = bool(int(os.environ.get("KV_SHARE", "1")))
 ids = eng.generate_context_cache(w.chunks)
 segs = [("cached", ids[s.chunk]) if s.cached else ("tokens", s.tokens) for s in w.requests[0]]
 for i in range(3):

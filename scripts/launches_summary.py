@@ -13,9 +13,12 @@ G, B = hdr.index("Grid Size"), hdr.index("Block Size")
 scale = {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3}
 seq = [(r[K].split("(")[0].replace("void ", ""), float(r[V].replace(",", "")) * scale[r[U]], r[G], r[B]) for r in data]
 ends = [i for i, s in enumerate(seq) if s[0].startswith("pic::logits_argmax") or s[0].startswith("logits_argmax")]
-starts = [i for i, s in enumerate(seq) if "kv_link" in s[0]]
+# a link step starts at its a2 launch (copy path) or, for the shared-block link (no a2), at its embed
+starts = [i for i, s in enumerate(seq) if "kv_link" in s[0] or "embed" in s[0]]
 end = ends[-1]
 start = max(i for i in starts if i < end)
+if "embed" in seq[start][0] and start > 0 and "kv_link" in seq[start - 1][0]:
+    start -= 1
 step = seq[start:end + 1]
 tot = sum(s[1] for s in step)
 agg = collections.OrderedDict()

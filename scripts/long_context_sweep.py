@@ -21,6 +21,7 @@ ap.add_argument("--chunks", default="4,8,16,32,64,94")
 ap.add_argument("--algs", default="legolink:16,cacheblend:15,fr")
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--out", default=None)
+ap.add_argument("--kv-share", default="0", help="comma list of kv_share settings to sweep (f3 shared-block link)")
 args = ap.parse_args()
 chunk_counts = [int(x) for x in args.chunks.split(",")]
 algs = args.algs.split(",")
@@ -40,8 +41,12 @@ with torch.cuda.stream(stream):
         w = sg.long_context(n_chunks)
         segs = [("cached", ids[s.chunk]) if s.cached else ("tokens", s.tokens) for s in w.requests[0]]
         N = sum(len(w.chunks[s.chunk]) if s.cached else len(s.tokens) for s in w.requests[0])
-        for alg in algs:
+        for alg, share in [(a, int(k)) for a in algs for k in args.kv_share.split(",")]:
+            eng.kv_share = bool(share)
             try:
+                pl = eng.plan(segs, alg)
+                kv_row = m.n_layers * m.n_kv_heads * m.head_dim * 2 * 2       # K + V bf16 per token, all layers
+                linked_gb = (len(pl["block_table"]) - pl["n_shared"]) * 16 * kv_row / 1e9
                 o = eng.link(segs, alg, want_logits=False, logits_dev=logits_dev[0])    # warm-up + graph capture
                 stream.synchronize()
                 ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -51,18 +56,23 @@ with torch.cuda.stream(stream):
                 ev1.record(stream)
                 ev1.synchronize()
                 ms = ev0.elapsed_time(ev1) / args.reps
-                r = {"alg": alg, "N": N, "chunks": n_chunks, "ttft_ms": ms, "tokens_per_s": N / ms * 1e3,
-                     "rows_layer0": o.n_selected_layer0, "rows_last": o.n_selected}
+                r = {"alg": alg, "kv_share": share, "N": N, "chunks": n_chunks, "ttft_ms": ms,
+                     "tokens_per_s": N / ms * 1e3, "rows_layer0": o.n_selected_layer0, "rows_last": o.n_selected,
+                     "linked_kv_gb_allocated": linked_gb}
             except B.PicError as e:
-                r = {"alg": alg, "N": N, "chunks": n_chunks, "error": str(e)}
+                r = {"alg": alg, "kv_share": share, "N": N, "chunks": n_chunks, "error": str(e)}
             rows.append(r)
             print(json.dumps(r), flush=True)
     eng.close()
 if args.out:
+    cols = [(a, int(k)) for a in algs for k in args.kv_share.split(",")]
+    name = lambda a, k: f"{a}{' shared' if k else ''}"
     with open(args.out, "w") as f:
         f.write("# Long-context sweep (f3; PAPER.md:307-316): TTFT vs N, 512-token chunks, Llama-3.1-8B shape, 1 B200\n\n")
-        f.write("| N | " + " | ".join(f"{a} TTFT ms" for a in algs) + " |\n|---|" + "---|" * len(algs) + "\n")
+        f.write("TTFT ms (linked KV GB allocated by the link)\n\n")
+        f.write("| N | " + " | ".join(name(a, k) for a, k in cols) + " |\n|---|" + "---|" * len(cols) + "\n")
         for n_chunks in chunk_counts:
             rs = [r for r in rows if r["chunks"] == n_chunks]
-            f.write(f"| {rs[0]['N']} | " + " | ".join(f"{r['ttft_ms']:.1f}" if "ttft_ms" in r else r["error"][:40]
-                                                     for r in rs) + " |\n")
+            f.write(f"| {rs[0]['N']} | " + " | ".join(
+                f"{r['ttft_ms']:.1f} ({r['linked_kv_gb_allocated']:.2f})" if "ttft_ms" in r else r["error"][:40]
+                for r in rs) + " |\n")
