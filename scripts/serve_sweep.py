@@ -24,6 +24,7 @@ ap.add_argument("--algs", default="legolink:16,cacheblend:15")
 ap.add_argument("--duration", type=float, default=3.0)
 ap.add_argument("--max-batch", type=int, default=32)
 ap.add_argument("--out", default=None)
+ap.add_argument("--kv-share", default="0", help="comma list of kv_share settings (f3 shared-block link)")
 args = ap.parse_args()
 m = sg.LLAMA31_8B
 d = args.users
@@ -42,12 +43,13 @@ with torch.cuda.stream(stream):
                        stream=stream)
         ids = [eng.generate_context_cache(c) for c in user_chunks]
         reqs = [[("cached", i) for i in ids[u]] + [("tokens", queries[u])] for u in range(d)]
-        for alg in args.algs.split(","):
+        for alg, share in [(a, int(k)) for a in args.algs.split(",") for k in args.kv_share.split(",")]:
+            eng.kv_share = bool(share)
             eng.link(reqs[0], alg)                                   # warm-up
             for rate in [float(x) for x in args.rates.split(",")]:
                 st = eng.serve_poisson(reqs, alg, rate, args.duration, seed=int(rate * 1000) ^ 0x5E12E,
                                        max_batch=args.max_batch)
-                r = {"alg": alg, "ccr": round(st["ccr"], 3), "rate": rate, **{k: st[k] for k in
+                r = {"alg": alg, "kv_share": share, "ccr": round(st["ccr"], 3), "rate": rate, **{k: st[k] for k in
                      ("n_completed", "throughput_rps", "ttft_mean_ms", "ttft_p50_ms", "ttft_p99_ms", "mean_batch",
                       "tokens_per_s")}}
                 rows.append(r)
@@ -57,8 +59,8 @@ if args.out:
     with open(args.out, "w") as f:
         f.write(f"# Open-loop Poisson serving (f4; PAPER.md:258, 293-305): {d} users x (10 x 512-token chunks + 64-token "
                 f"query), Llama-3.1-8B shape, 1 B200, {args.duration:.0f} s windows, eager launches\n\n")
-        f.write("| alg | CCR | rate (req/s) | throughput (req/s) | TTFT mean ms | p50 | p99 | mean batch |\n")
-        f.write("|---|---|---|---|---|---|---|---|\n")
+        f.write("| alg | kv_share | CCR | rate (req/s) | throughput (req/s) | TTFT mean ms | p50 | p99 | mean batch |\n")
+        f.write("|---|---|---|---|---|---|---|---|---|\n")
         for r in rows:
-            f.write(f"| {r['alg']} | {r['ccr']:.2f} | {r['rate']:.0f} | {r['throughput_rps']:.1f} | {r['ttft_mean_ms']:.1f} | "
+            f.write(f"| {r['alg']} | {r['kv_share']} | {r['ccr']:.2f} | {r['rate']:.0f} | {r['throughput_rps']:.1f} | {r['ttft_mean_ms']:.1f} | "
                     f"{r['ttft_p50_ms']:.1f} | {r['ttft_p99_ms']:.1f} | {r['mean_batch']:.2f} |\n")

@@ -42,6 +42,7 @@ def _rank(rank, world, port, q):
             o = eng.link(segs, alg)
             g = eng.link(segs, alg, use_graph=True)      # graph replay path too
             out[alg] = (o.logits, g.logits, o.first_token)
+            out["shared " + alg] = eng.link(segs, alg, kv_share=True).logits   # f3 shared-block link, sharded
         kq = eng.read_weights(0, 1, 0, 2 * 128)          # this rank's q-head rows of layer 1
         # decode over the linked cache (f1) and LegoLink-0 (f2) under tensor parallelism
         h = eng.link(segs, "legolink:4", keep_linked=True)
@@ -85,6 +86,8 @@ def test_tp2_matches_oracle_and_tp1():
         ref = P.link(store, segs, alg)
         err = np.linalg.norm(l0 - ref.logits) / np.linalg.norm(ref.logits)
         assert err < 2e-2, (alg, err)
+        for r in range(2):                                          # shared-block link: bit-identical
+            assert np.array_equal(res[r][1]["shared " + alg], res[r][1][alg][0]), (alg, r)
     # decode steps after a LegoLink-4 link (f1) and LegoLink-0 (f2), both sharded
     r4 = P.link(store, segs, "legolink:4")
     K, V = r4.K, r4.V
