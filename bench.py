@@ -188,6 +188,11 @@ def roofline(prof, P, src, nsteps):
         achieved = dom["flops"] / (dom["ms"] / 1e3) / 1e12
         roof = {"bound": "tensor", "achieved": achieved, "peak": P["bf16_tflops"], "unit": "TFLOP/s"}
     roof["frac"] = roof["achieved"] / roof["peak"]
+    if roof["bound"] == "tensor" and P.get("bf16_tflops_sustained"):
+        # the driver's sustained figure (back-to-back matmuls for seconds, power-capped clocks) applies to a
+        # kernel timed inside a long step; "peak" stays the burst figure (the conservative denominator)
+        roof["peak_sustained"] = P["bf16_tflops_sustained"]
+        roof["frac_sustained"] = roof["achieved"] / P["bf16_tflops_sustained"]
     roof["traffic"] = ncu_traffic(dom_name)
     roof["kernel"] = dom_name
     roof["share_of_step"] = dom["ms"] / tot

@@ -417,18 +417,23 @@ static pic_status init_device(pic_engine* e, void* arena, size_t bytes, cudaStre
   // [r·Hkv, ...), MLP columns [r·F, (r+1)·F) (local sizes); exponents use the GLOBAL fan-in.
   const int64_t tr = e->tp_rank, tp = e->tp_size;
   const int64_t gHqD = Hq * D * tp, gF = F * tp;
-  // gate/up interleave group for the fused SwiGLU epilogue: the g dividing F whose F/g tiles best fill
-  // one wave of 148 CTAs at skinny M (Mistral/Llama F = 14336: g = 112 -> 128 tiles of N = 224)
+  // gate/up interleave group for the fused SwiGLU epilogue (fixed when the weights are generated, so
+  // before any M is known): the g dividing F that minimises waves x per-unit cost (2g + 64: an N-tile
+  // of 2g weight rows plus the fixed A-tile / epilogue cost) summed over a skinny (1 m-tile) and a
+  // wide (8 m-tiles, per m-tile) forward.  Mistral/Llama F = 14336 and Llama-70B F = 28672: g = 112
+  // (N-tile 224; 128 tiles fill one wave at k' <= 128).  (A wave-fill-only rule picked g = 16 for
+  // F = 28672: N-tile 32, 3.5x slower GEMMs at k' = 1072.)
   e->f32 = c.dtype == 1;
   e->gu_group = 0;
   if (!getenv("PIC_NO_FUSED_SWIGLU") && !e->f32) {
-    double best = -1;
+    double best = 1e300;
     for (int g : {112, 128, 64, 32, 16}) {
       if (F % g || !gemm_bn_supported(2 * g, true)) continue;
-      const int tiles = (int)(F / g);
-      const double eff = (double)tiles / (148.0 * ((tiles + 147) / 148));
-      if (eff > best + 1e-9) {
-        best = eff;
+      const int64_t tiles = F / g;
+      double cost = 0;
+      for (int mt : {1, 8}) cost += (double)((mt * tiles + 147) / 148) * (2 * g + 64) / mt;
+      if (cost < best - 1e-9) {
+        best = cost;
         e->gu_group = g;
       }
     }
