@@ -21,6 +21,7 @@
 #include <cuda.h>
 
 #include <algorithm>
+#include <vector>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -499,22 +500,40 @@ __global__ void __launch_bounds__(ROT ? 320 + 32 * kRotWarps : 320, 1)
 
 int attn_schedule(const int32_t* tiles, int n_tiles, const int* n_kv, int Hkv, int target_ctas, int max_split,
                   int32_t* work, int* n_work, int32_t* row_nsplit) {
-  long total = 0;
-  for (int t = 0; t < n_tiles; ++t) total += n_kv[t];
+  // Split q-tile t's n_kv[t] KV tiles into p_t = min(max_split, ⌈n_kv/b⌉) equal pieces for the per-CTA
+  // budget b that minimises the estimated makespan on target_ctas SMs (one CTA per SM):
+  //   one wave (P <= target): the longest piece;  several waves: Σ/target + longest/2 (LPT bound)
+  // plus a fixed per-piece cost (prologue, epilogue, partial merge: ~kOvh KV tiles) per wave.  Pieces
+  // are then issued longest first (blockIdx order is dispatch order), so long pieces never start in
+  // the last wave (cfg5: 536 unsplit pieces of 5..257 tiles in q-tile order ran 2.3x the mean).
+  constexpr double kOvh = 4.0;
+  long max_kv = 1, total = 0;
+  for (int t = 0; t < n_tiles; ++t) {
+    max_kv = std::max<long>(max_kv, n_kv[t]);
+    total += n_kv[t];
+  }
   total *= Hkv;
-  long budget = std::max(1L, (total + target_ctas - 1) / target_ctas);
-  // grow the per-CTA budget until the work list fits in one wave of target_ctas CTAs (at most up
-  // to the longest tile: beyond that every tile is a single piece and nothing changes)
-  long max_kv = 1;
-  for (int t = 0; t < n_tiles; ++t) max_kv = std::max<long>(max_kv, n_kv[t]);
-  for (; budget < max_kv; ++budget) {
-    long ctas = 0;
-    for (int t = 0; t < n_tiles; ++t) ctas += std::min<long>(max_split, (n_kv[t] + budget - 1) / budget);
-    if (ctas * Hkv <= target_ctas) break;
+  long best_b = max_kv;
+  double best_cost = 1e300;
+  for (long b = 1; b <= max_kv; ++b) {
+    long P = 0, maxc = 0;
+    for (int t = 0; t < n_tiles; ++t) {
+      const long p = std::min<long>(max_split, std::max(1L, (n_kv[t] + b - 1) / b));
+      P += p;
+      maxc = std::max(maxc, (n_kv[t] + p - 1) / p);
+    }
+    P *= Hkv;
+    const long waves = (P + target_ctas - 1) / target_ctas;
+    const double span = P <= target_ctas ? (double)maxc : (double)total / target_ctas + 0.5 * maxc;
+    const double cost = span + kOvh * waves;
+    if (cost < best_cost - 1e-9) {
+      best_cost = cost;
+      best_b = b;
+    }
   }
   int w = 0, mx = 1;
   for (int t = 0; t < n_tiles; ++t) {
-    int pieces = (int)std::min<long>(max_split, std::max(1L, (n_kv[t] + budget - 1) / budget));
+    int pieces = (int)std::min<long>(max_split, std::max(1L, (n_kv[t] + best_b - 1) / best_b));
     const int chunk = (n_kv[t] + pieces - 1) / pieces;
     pieces = (n_kv[t] + chunk - 1) / chunk;
     for (int p = 0; p < pieces; ++p) {
@@ -527,6 +546,16 @@ int attn_schedule(const int32_t* tiles, int n_tiles, const int* n_kv, int Hkv, i
     for (int r = 0; r < tiles[3 * t + 2]; ++r) row_nsplit[tiles[3 * t + 1] + r] = pieces;
     mx = std::max(mx, pieces);
   }
+  // longest pieces first (stable: ties keep q-tile order); the split slot travels with the item
+  std::vector<int> ord(w);
+  for (int i = 0; i < w; ++i) ord[i] = i;
+  std::stable_sort(ord.begin(), ord.end(), [&](int x, int y) {
+    return work[4 * x + 2] - work[4 * x + 1] > work[4 * y + 2] - work[4 * y + 1];
+  });
+  std::vector<int32_t> sorted(4 * (size_t)w);
+  for (int i = 0; i < w; ++i)
+    for (int k = 0; k < 4; ++k) sorted[4 * i + k] = work[4 * ord[i] + k];
+  std::copy(sorted.begin(), sorted.end(), work);
   *n_work = w;
   return mx;
 }

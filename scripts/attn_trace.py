@@ -1,4 +1,5 @@
-"""Per-CTA attention timeline of the last layer of one cfg2 link (PIC_ATTN_TRACE=1 must be set)."""
+"""Per-CTA attention timeline of the last layer of one link (PIC_ATTN_TRACE=1 must be set).
+    python scripts/attn_trace.py [cfg2|cfg3|cfg5] [n_layers] [alg]"""
 import os
 import sys
 
@@ -6,9 +7,14 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import seedgen as sg
 from paper_2410_15332_b200 import pic as B
 
-w = sg.cfg2() if len(sys.argv) < 2 else getattr(sg, sys.argv[1])()
+name = sys.argv[1] if len(sys.argv) > 1 else "cfg2"
+kw = {"n_layers": int(sys.argv[2])} if len(sys.argv) > 2 and name != "cfg2" else {}
+if len(sys.argv) > 3:
+    kw["alg"] = sys.argv[3]
+w = getattr(sg, name)(**kw)
 N = sum(len(w.chunks[s.chunk]) if s.cached else len(s.tokens) for s in w.requests[0])
-eng = B.Engine(w.model, num_blocks=(sum(len(c) for c in w.chunks) + 3 * N) // 16 + 64, max_rows=4096, max_tokens=N + 16, device=0)
+eng = B.Engine(w.model, num_blocks=(sum(len(c) for c in w.chunks) + 3 * N) // 16 + 64, max_rows=max(4096, N),
+               max_tokens=N + 16, device=0)
 eng.kv_share = bool(int(os.environ.get("KV_SHARE", "1")))
 ids = eng.generate_context_cache(w.chunks)
 segs = [("cached", ids[s.chunk]) if s.cached else ("tokens", s.tokens) for s in w.requests[0]]
