@@ -48,3 +48,27 @@ def test_serve_poisson_tiny(alg):
         assert st["mean_batch"] > 1.0                                  # queued requests were batched
     assert eng.stats()["free_blocks"] == 1024 - sum((len(c) + 15) // 16 for c in w.chunks)
     eng.close()
+
+
+@pytest.mark.gpu
+def test_serve_poisson_shared_block_link_admits_more():
+    """f3 x f4: with the shared-block link the server admits by fresh blocks, so a pool that fits only
+    one copied link at a time batches several shared links; every request completes and the pool is
+    whole again afterwards (shared references dropped)."""
+    cfg = sg.TINY_D128
+    w = sg.cfg1(model=cfg)
+    n_chunk_blocks = sum((len(c) + 15) // 16 for c in w.chunks)
+    link_blocks = (sum(len(c) for c in w.chunks) + len(w.requests[0][-1].tokens) + 15) // 16
+    eng = B.Engine(cfg, num_blocks=n_chunk_blocks + link_blocks + 2, max_rows=1024, max_tokens=512,
+                   max_requests=8, device=0)
+    ids = eng.generate_context_cache(w.chunks)
+    reqs = [[("cached", ids[s.chunk]) if s.cached else ("tokens", s.tokens) for s in r]
+            for r in [w.requests[0]] + sg.permuted_requests(w, 3)]
+    out = {}
+    for share in (False, True):
+        st = eng.serve_poisson(reqs, "legolink:4", rate=2000.0, duration_s=0.25, seed=5, kv_share=share)
+        assert st["n_completed"] == st["n_requests"] > 0
+        assert eng.stats()["free_blocks"] == link_blocks + 2
+        out[share] = st["mean_batch"]
+    assert out[False] == 1.0 and out[True] > 1.0
+    eng.close()
