@@ -286,7 +286,9 @@ pic_status pic_cache_export(pic_engine* eng, pic_cache_id id, int32_t layer, voi
 pic_status pic_cache_info(pic_engine* eng, pic_cache_id id, int32_t* n_tokens, int32_t* blocks);
 
 /* Free a chunk's KV.  Idempotent: *was_present (nullable) says whether it existed
- * (S:203-211).  Live linked caches are unaffected (they own copies). */
+ * (S:203-211).  Live linked caches are unaffected: a copy-path link owns re-based copies, and a
+ * shared-block link (kv_share) holds a reference on each chunk-store block it points at, so those
+ * blocks return to the pool only when the last linked cache using them is released. */
 pic_status pic_expire_cache(pic_engine* eng, pic_cache_id id, int32_t* was_present);
 
 /* Test hook: copy generated bf16 weights to host (uint16 bf16 bits).  which: 0=q 1=k 2=v 3=o 4=gate
