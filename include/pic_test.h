@@ -14,7 +14,9 @@ extern "C" {
 #endif
 
 /* tcgen05 GEMM (a5/a7/a8/a10): out[m][n] = Σ_k A[m][k]·B[n][k] (fp32, summed over `splits` split-K
- * partials), A [M][K], B [N][K] bf16; bn ∈ {64,128,256}; K % 64 == 0, N % 32 == 0. */
+ * partials), A [M][K], B [N][K] bf16; bn ∈ {64,128,256}; K % 64 == 0, N % 32 == 0.  A negative bn selects
+ * the CTA-pair (cta_group::2, 256-row M-tile) kernel with N-tile |bn| ∈ {128,192,224,256} (also for
+ * pic_test_gemm_swiglu and pic_bench_gemm). */
 pic_status pic_test_gemm(const uint16_t* A, const uint16_t* B, int32_t M, int32_t N, int32_t K, int32_t bn,
                          int32_t splits, float* out);
 

@@ -896,7 +896,28 @@ struct PlanPack {  // dynamic packing of the plan arrays into one H2D copy
 
 struct GemmChoice {
   int bn, splits;
+  int pair = 0;  // 1: CTA-pair kernel (cta_group::2, 256-row M-tiles)
 };
+
+// CTA pairs (cta_group::2) halve the B operand bytes staged and read per SM and FLOP.  Measured
+// (scripts/gemm_pair_probe.py): 12-22% faster per unit of work on the cfg4 shapes with zero operands,
+// but only 3-5% with random operands — the tensor-bound GEMMs run power-capped (~1.5 GHz), and the
+// pair saves operand traffic, not tensor energy — and slower end to end in the engine (cfg4 128 vs
+// 118 ms, cfg3 CacheBlend-15 20.4 vs 18.3 ms).  Opt-in (PIC_PAIR=1); the choice then compares
+// waves x per-unit cost with pair units at kPairCost.
+constexpr double kPairCost = 0.85;
+static bool pairs_enabled() {
+  static const bool on = getenv("PIC_PAIR") != nullptr;
+  return on;
+}
+static double gemm_cost(int M, int N, int kblk, int bn, int sp, int pair) {
+  const int cl = pair ? 2 : 1;
+  const long units = (long)((M + 128 * cl - 1) / (128 * cl)) * ((N + bn - 1) / bn) * sp;
+  const long slots = 148 / cl;
+  const long waves = (units + slots - 1) / slots;
+  const int kper = (kblk + sp - 1) / sp;
+  return (double)waves * kper * (bn + 32) * (pair ? kPairCost : 1.0) + (sp - 1) * 0.02 * kblk * bn;
+}
 
 // Tile / split-K choice (measured, scripts/gemm_sweep.py): a CTA streams ~40 GB/s of weights, so a
 // GEMM wants every SM busy in ONE wave.  bn=128 with split-K when its tiles fit in a wave (skinny M:
@@ -942,7 +963,40 @@ static GemmChoice choose_gemm(const pic_engine* e, int M, int N, int K) {
   }
   g.splits = std::max(1, std::min(g.splits, kblk / 4));
   while (g.splits > 1 && (size_t)g.splits * M * N > e->ws_floats) --g.splits;
+  if (mt >= 2 && pairs_enabled()) {
+    double best = gemm_cost(M, N, kblk, g.bn, g.splits, 0);
+    for (int bn : {256, 224, 192, 128})
+      for (int sp = 1; sp <= 4; ++sp) {
+        if (!gemm_pair_supported(bn) || (sp > 1 && (sp > kblk / 4 || (size_t)sp * M * N > e->ws_floats))) continue;
+        const double c = gemm_cost(M, N, kblk, bn, sp, 1);
+        if (c < best - 1e-9) {
+          best = c;
+          g = GemmChoice{bn, sp, 1};
+        }
+      }
+  }
   return g;
+}
+
+// Fused gate/up + SwiGLU GEMM (N-tile fixed at 2g by the weight interleave): CTA pair when it costs less.
+static bool swiglu_pair(const pic_engine* e, int M, int N2) {
+  const int bn = 2 * e->gu_group;
+  if (M <= 128 || !pairs_enabled() || !gemm_pair_supported(bn)) return false;
+  return gemm_cost(M, N2, 1, bn, 1, 1) < gemm_cost(M, N2, 1, bn, 1, 0) - 1e-9;
+}
+
+// Weight tensor map with a `box`-row box (N-tiles other than 64/128/256, CTA-pair halves), built on
+// first use and cached per (matrix, box).
+static pic_status weight_map(pic_engine* e, const void* B_ptr, int N, int K, int box, const CUtensorMap** out) {
+  const auto key = std::make_pair(B_ptr, box);
+  auto it = e->wmaps.find(key);
+  if (it == e->wmaps.end()) {
+    CUtensorMap m;
+    TRY(make_tmap_2d(&m, const_cast<void*>(B_ptr), (uint64_t)N, (uint64_t)K, (uint32_t)box));
+    it = e->wmaps.emplace(key, m).first;
+  }
+  *out = &it->second;
+  return PIC_OK;
 }
 
 struct Runner {
@@ -962,18 +1016,11 @@ struct Runner {
     *splits_out = g.splits;
     if (debug_sync()) fprintf(stderr, "[pic] gemm M=%d N=%d K=%d bn=%d splits=%d\n", M, N, K, g.bn, g.splits);
     ++launches;
-    const CUtensorMap* Bm = (g.bn == 64 || g.bn == 128 || g.bn == 256) ? &B3[bn_index(g.bn)] : nullptr;
-    if (!Bm) {  // other N-tiles: weight tensor maps built on first use and cached per (matrix, bn)
-      const auto key = std::make_pair(B_ptr, g.bn);
-      auto it = e->wmaps.find(key);
-      if (it == e->wmaps.end()) {
-        CUtensorMap m;
-        TRY(make_tmap_2d(&m, const_cast<void*>(B_ptr), (uint64_t)N, (uint64_t)K, (uint32_t)g.bn));
-        it = e->wmaps.emplace(key, m).first;
-      }
-      Bm = &it->second;
-    }
-    PROF("gemm", (double)N * K * 2 + (double)M * K * 2 + (double)M * N * 4, 2.0 * M * N * K, launch_gemm_partial(A, *Bm, e->ws, M, N, K, g.splits, g.bn, st));
+    const int box = g.pair ? g.bn / 2 : g.bn;  // a CTA pair loads half of the N-tile per CTA
+    const CUtensorMap* Bm = (box == 64 || box == 128 || box == 256) ? &B3[bn_index(box)] : nullptr;
+    if (!Bm) TRY(weight_map(e, B_ptr, N, K, box, &Bm));
+    PROF("gemm", (double)N * K * 2 + (double)M * K * 2 + (double)M * N * 4, 2.0 * M * N * K,
+         launch_gemm_partial(A, *Bm, e->ws, M, N, K, g.splits, g.bn, st, 0, GemmNext{}, g.pair));
     return PIC_OK;
   }
 };
@@ -1225,8 +1272,11 @@ static pic_status enqueue_forward(pic_engine* e, const Fwd& f, const DevPlan& dp
     TRY(add_norm(e->ws, s, w.g2, e->x, nullptr, M, (double)M * d * 2));
     if (e->gu_group > 0) {
       ++R.launches;
+      const bool pair = swiglu_pair(e, M, 2 * F);
+      const CUtensorMap* Bg = &w.tm_gu_fused;
+      if (pair) TRY(weight_map(e, w.gu, 2 * F, d, e->gu_group, &Bg));  // each CTA: the gate or the up half
       PROF("gemm", (double)2 * F * d * 2 + (double)M * d * 2 + (double)M * F * 2, 2.0 * M * 2 * F * d,
-           launch_gemm_swiglu(e->tm_x, w.tm_gu_fused, e->u, M, 2 * F, d, 2 * e->gu_group, st));
+           launch_gemm_swiglu(e->tm_x, *Bg, e->u, M, 2 * F, d, 2 * e->gu_group, st, 0, GemmNext{}, pair ? 1 : 0));
     } else {
       TRY(R.gemm(e->tm_x, w.tm_gu, M, 2 * F, d, &s, e->x, w.gu));
       ++R.launches;

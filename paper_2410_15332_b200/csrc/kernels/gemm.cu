@@ -31,10 +31,10 @@ __device__ __forceinline__ bool weight_evict_first() { return c_weight_evict_fir
 
 enum { EPI_PARTIAL = 0, EPI_SWIGLU = 1 };
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, int CL = 1>
 struct GemmSmem {
   static constexpr int kA = 128 * 64 * 2;  // 16 KB
-  static constexpr int kB = BN * 64 * 2;
+  static constexpr int kB = (BN / CL) * 64 * 2;  // a CTA pair splits the N-tile: each CTA holds BN/2 rows of B
   static constexpr int kStage = kA + kB;
   static constexpr int kBars = 2 * STAGES + 4;
   static constexpr int kBytes = STAGES * kStage + kBars * 8 + 16;
@@ -44,7 +44,9 @@ struct GemmSmem {
   static_assert(kBytes <= 232448, "GEMM smem over the 227 KB limit");
 };
 
-constexpr int gemm_stages(int bn) { return (225 * 1024) / (16384 + bn * 128) > 8 ? 8 : (225 * 1024) / (16384 + bn * 128); }
+constexpr int gemm_stages(int bn, int cl = 1) {
+  return (225 * 1024) / (16384 + bn / cl * 128) > 8 ? 8 : (225 * 1024) / (16384 + bn / cl * 128);
+}
 
 // Persistent tcgen05 GEMM.  Work units (m-tile, n-tile, k-split) are dealt round-robin to
 // min(units, 148) CTAs; the smem ring runs continuously across units and the fp32 accumulator is
@@ -53,13 +55,19 @@ constexpr int gemm_stages(int bn) { return (225 * 1024) / (16384 + bn * 128) > 8
 //   EPI_SWIGLU (split-K = 1): B rows are W_gate/W_up interleaved in groups of BN/2 (n-tile = gate rows
 //     [n·BN/2, (n+1)·BN/2) then the matching up rows); out = bf16 u[M][N/2] = silu(gate) ⊙ up
 //     (the a8 SwiGLU fused into the GEMM epilogue; P:241 Llama-family MLP, reading R4).
-template <int BN, int STAGES, int EPI>
+// CL = 2: CTA pair (cta_group::2).  A unit is a 256-row M-tile: each CTA of the pair loads its 128 rows of A
+// and half of the N-tile's B rows into its own smem; the leader CTA issues M = 256 MMAs that read both
+// CTAs' smem and write each CTA's 128 accumulator rows into its own TMEM; both CTAs' loads complete on the
+// leader's full barrier, the MMA commits are multicast to both CTAs' empty / accumulator-full barriers,
+// and both epilogues release the accumulator on the leader's tempty barrier.  Per SM this halves the B
+// bytes staged and read by the tensor core per FLOP (the operand traffic that bounds one-CTA M = 128).
+template <int BN, int STAGES, int EPI, int CL = 1>
 __global__ void __launch_bounds__(192, 1)
     gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      void* __restrict__ out_, int M, int N, int kblk_total, int kblk_per_split, int splits,
                      int pack, unsigned long long* trace, const __grid_constant__ CUtensorMap tmN,
                      GemmNext nx) {
-  using S = GemmSmem<BN, STAGES>;
+  using S = GemmSmem<BN, STAGES, CL>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw;
   if (threadIdx.x == 0 && (smem_u32(smem) & 1023)) __trap();  // SWIZZLE_128B tiles need 1 KB alignment
@@ -71,7 +79,9 @@ __global__ void __launch_bounds__(192, 1)
   const uint32_t tfull0 = smem_u32(bars + 2 * STAGES), tempty0 = smem_u32(bars + 2 * STAGES + 2);
 
   const int warp = warp_id(), lane = lane_id();
-  const int mt = (M + 127) / 128, nt = (N + BN - 1) / BN;
+  const uint32_t rank = CL == 2 ? cluster_ctarank() : 0;
+  const int cid = blockIdx.x / CL, ncl = gridDim.x / CL;  // cluster (CTA pair) id / count
+  const int mt = (M + 128 * CL - 1) / (128 * CL), nt = (N + BN - 1) / BN;
   const int units = mt * nt * splits;
   griddep_launch();
   if (trace && threadIdx.x == 0) trace[blockIdx.x * 6 + 0] = globaltimer();
@@ -83,15 +93,26 @@ __global__ void __launch_bounds__(192, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(tfull0 + 8 * b, 1);
-      mbar_init(tempty0 + 8 * b, 128);
+      mbar_init(tempty0 + 8 * b, 128 * CL);
     }
     fence_mbar_init();
   }
-  if (warp == 2) tmem_alloc(smem_u32(tmem_slot), S::kTmemCols);
+  if (warp == 2) {
+    if constexpr (CL == 2)
+      tmem_alloc_2sm(smem_u32(tmem_slot), S::kTmemCols);
+    else
+      tmem_alloc(smem_u32(tmem_slot), S::kTmemCols);
+  }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CL == 2)
+    cluster_sync();  // barrier inits and TMEM allocations of both CTAs visible before any cross-CTA use
+  else
+    __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // the leader's full barriers (both CTAs' loads complete there) and accumulator-empty barriers
+  const uint32_t fullL = CL == 2 ? mapa_shared(full0, 0) : full0;
+  const uint32_t temptyL = CL == 2 ? mapa_shared(tempty0, 0) : tempty0;
 
   // unit u -> (m fastest, then split, then n): concurrently running CTAs share weight tiles in L2
   auto decode = [&](int u, int& m0, int& n_idx, int& kb0, int& nkb) {
@@ -99,7 +120,7 @@ __global__ void __launch_bounds__(192, 1)
     const int r = u / mt;
     const int sp = r % splits;
     n_idx = r / splits;
-    m0 = m * 128;
+    m0 = m * 128 * CL + (int)rank * 128;  // this CTA's 128 rows
     kb0 = sp * kblk_per_split;
     nkb = max(0, min(kblk_per_split, kblk_total - kb0));
   };
@@ -107,7 +128,12 @@ __global__ void __launch_bounds__(192, 1)
   // B tile of k-block kb: row-major weights -> one [BN x 64] box; packed weights (pack rows per
   // sub-tile, stored [N/pack][K/64][pack][64]) -> BN/pack contiguous boxes of pack x 128 B.
   const uint64_t wpol = l2_policy_evict_first();  // weights are streamed once per forward
+  const uint64_t apol = l2_policy_evict_normal();
   auto load_b = [&](uint32_t dst, uint32_t bar, int kb, int n_idx) {
+    if constexpr (CL == 2) {
+      tma_load_2d_2sm(dst, &tmB, bar, kb * 64, n_idx * BN + (int)rank * (BN / 2), weight_evict_first() ? wpol : apol);
+      return;
+    }
     if (pack == 0) {
       if (weight_evict_first())
         tma_load_2d_hint(dst, &tmB, bar, kb * 64, n_idx * BN, wpol);
@@ -128,33 +154,41 @@ __global__ void __launch_bounds__(192, 1)
       tma_prefetch(&tmB);
       int it = 0;
       bool waited = false;
-      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+      // A pair's loads complete on the leader's full barrier, which alone expects both CTAs' bytes
+      auto expect = [&](int s) {
+        if (rank == 0) mbar_expect_tx(full0 + 8 * s, S::kStage * CL);
+      };
+      auto load_a = [&](int s, int kc, int m0) {
+        if constexpr (CL == 2)
+          tma_load_2d_2sm(smem_u32(sA + s * S::kA), &tmA, fullL + 8 * s, kc, m0, apol);
+        else
+          tma_load_2d(smem_u32(sA + s * S::kA), &tmA, full0 + 8 * s, kc, m0);
+      };
+      for (int u = cid; u < units; u += ncl) {
         int m0, n_idx, kb0, nkb;
         decode(u, m0, n_idx, kb0, nkb);
-        const int n0 = n_idx * BN;
         int kk = 0;
         if (!waited) {
           // Weights do not depend on the previous kernel: stream the first stages of B while it
           // drains (PDL), then wait for it before loading the activations A.
           const int pre = min(nkb, STAGES);
           for (int i = 0; i < pre; ++i) {
-            mbar_expect_tx(full0 + 8 * i, S::kStage);
-            load_b(smem_u32(sB + i * S::kB), full0 + 8 * i, kb0 + i, n_idx);
+            expect(i);
+            load_b(smem_u32(sB + i * S::kB), fullL + 8 * i, kb0 + i, n_idx);
           }
           griddep_wait();
           if (trace) trace[blockIdx.x * 6 + 1] = globaltimer();
           waited = true;
-          for (int i = 0; i < pre; ++i) tma_load_2d(smem_u32(sA + i * S::kA), &tmA, full0 + 8 * i, (kb0 + i) * 64, m0);
+          for (int i = 0; i < pre; ++i) load_a(i, (kb0 + i) * 64, m0);
           kk = pre;
           it = pre;
         }
         for (; kk < nkb; ++kk, ++it) {
           const int s = it % STAGES;
           mbar_wait(empty0 + 8 * s, ((it / STAGES) & 1) ^ 1);
-          mbar_expect_tx(full0 + 8 * s, S::kStage);
-          const int kc = (kb0 + kk) * 64;
-          tma_load_2d(smem_u32(sA + s * S::kA), &tmA, full0 + 8 * s, kc, m0);
-          load_b(smem_u32(sB + s * S::kB), full0 + 8 * s, kb0 + kk, n_idx);
+          expect(s);
+          load_a(s, (kb0 + kk) * 64, m0);
+          load_b(smem_u32(sB + s * S::kB), fullL + 8 * s, kb0 + kk, n_idx);
         }
       }
       if (!waited) griddep_wait();
@@ -169,10 +203,10 @@ __global__ void __launch_bounds__(192, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      constexpr uint32_t idesc = idesc_bf16(128, BN, 0, 0);
+    if (lane == 0 && rank == 0) {  // a pair's MMAs are issued by the leader CTA
+      constexpr uint32_t idesc = idesc_bf16(128 * CL, BN, 0, 0);
       int it = 0, i = 0;
-      for (int u = blockIdx.x; u < units; u += gridDim.x, ++i) {
+      for (int u = cid; u < units; u += ncl, ++i) {
         int m0, n_idx, kb0, nkb;
         decode(u, m0, n_idx, kb0, nkb);
         const int ab = i & 1;
@@ -186,12 +220,23 @@ __global__ void __launch_bounds__(192, 1)
           tc_fence_after();
           const uint32_t a = smem_u32(sA + s * S::kA), b = smem_u32(sB + s * S::kB);
 #pragma unroll
-          for (int k4 = 0; k4 < 4; ++k4)
-            umma_bf16(d, sdesc_sw128(a + k4 * 32, 16, 1024), sdesc_sw128(b + k4 * 32, 16, 1024), idesc,
-                      (kk | k4) != 0);
-          umma_commit(empty0 + 8 * s);
+          for (int k4 = 0; k4 < 4; ++k4) {
+            if constexpr (CL == 2)
+              umma_bf16_2sm(d, sdesc_sw128(a + k4 * 32, 16, 1024), sdesc_sw128(b + k4 * 32, 16, 1024), idesc,
+                            (kk | k4) != 0);
+            else
+              umma_bf16(d, sdesc_sw128(a + k4 * 32, 16, 1024), sdesc_sw128(b + k4 * 32, 16, 1024), idesc,
+                        (kk | k4) != 0);
+          }
+          if constexpr (CL == 2)
+            umma_commit_2sm(empty0 + 8 * s, 3);
+          else
+            umma_commit(empty0 + 8 * s);
         }
-        umma_commit(tfull0 + 8 * ab);
+        if constexpr (CL == 2)
+          umma_commit_2sm(tfull0 + 8 * ab, 3);
+        else
+          umma_commit(tfull0 + 8 * ab);
       }
       if (trace) trace[blockIdx.x * 6 + 3] = globaltimer();
     }
@@ -199,7 +244,7 @@ __global__ void __launch_bounds__(192, 1)
     griddep_wait();  // `out` may still be read by the previous kernel
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     int i = 0;
-    for (int u = blockIdx.x; u < units; u += gridDim.x, ++i) {
+    for (int u = cid; u < units; u += ncl, ++i) {
       int m0, n_idx, kb0, nkb;
       decode(u, m0, n_idx, kb0, nkb);
       const int ab = i & 1;
@@ -211,7 +256,7 @@ __global__ void __launch_bounds__(192, 1)
       // The last unit of a CTA runs after its final MMA, when the smem ring is idle: stage the tile
       // through the ring so that global stores are full 128-B row segments (a row-per-thread store
       // pattern costs ~4 us per tile in uncoalesced 16-B transactions).
-      const bool stage = u + (int)gridDim.x >= units;
+      const bool stage = u + ncl >= units;
       uint8_t* stg = smem + (size_t)(warp - 2) * ((BN + 31) / 32) * 4096;
       const int mrow0 = m0 + q * 32;
       if constexpr (EPI == EPI_PARTIAL) {
@@ -292,15 +337,24 @@ __global__ void __launch_bounds__(192, 1)
         }
       }
       tc_fence_before();
-      mbar_arrive(tempty0 + 8 * ab);
+      if constexpr (CL == 2)
+        mbar_arrive_cluster(temptyL + 8 * ab);  // the leader's MMA reuses the pair's accumulator
+      else
+        mbar_arrive(tempty0 + 8 * ab);
       if (trace && threadIdx.x == 64 && u + (int)gridDim.x >= units) trace[blockIdx.x * 6 + 4] = globaltimer();
     }
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CL == 2)
+    cluster_sync();  // every MMA into either CTA's TMEM has been consumed by its epilogue
+  else
+    __syncthreads();
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc(tmem, S::kTmemCols);
+    if constexpr (CL == 2)
+      tmem_dealloc_2sm(tmem, S::kTmemCols);
+    else
+      tmem_dealloc(tmem, S::kTmemCols);
   }
 }
 
@@ -322,30 +376,54 @@ GemmNext gemm_next(const CUtensorMap* B, int M, int N, int K, int splits, int bn
   return nx;
 }
 
-template <int BN, int EPI>
+template <int BN, int EPI, int CL = 1>
 static cudaError_t launch_gemm_t(const CUtensorMap& A, const CUtensorMap& B, void* out, int M, int N, int K, int splits,
                                  int pack, cudaStream_t st, const GemmNext& nx) {
-  constexpr int ST = gemm_stages(BN);
-  using S = GemmSmem<BN, ST>;
-  auto kern = gemm_bf16_kernel<BN, ST, EPI>;
+  constexpr int ST = gemm_stages(BN, CL);
+  using S = GemmSmem<BN, ST, CL>;
+  auto kern = gemm_bf16_kernel<BN, ST, EPI, CL>;
   const int kblk = K / 64;
   const int per = (kblk + splits - 1) / splits;
-  const int units = ((N + BN - 1) / BN) * ((M + 127) / 128) * splits;
-  const int grid = units < 148 ? units : 148;  // persistent: one CTA per SM
-  CUDA_TRY_LAUNCH(launch_k(kern, dim3(grid), dim3(192), S::kBytes, st, A, B, out, M, N, kblk, per, splits, pack,
-                           g_gemm_trace, nx.tm ? *nx.tm : B, nx));
+  const int units = ((N + BN - 1) / BN) * ((M + 128 * CL - 1) / (128 * CL)) * splits;
+  const int max_cl = 148 / CL;
+  const int grid = CL * (units < max_cl ? units : max_cl);  // persistent: one CTA (pair) per SM (pair)
+  if constexpr (CL == 1) {
+    CUDA_TRY_LAUNCH(launch_k(kern, dim3(grid), dim3(192), S::kBytes, st, A, B, out, M, N, kblk, per, splits, pack,
+                             g_gemm_trace, nx.tm ? *nx.tm : B, nx));
+  } else {
+    if (pack) return cudaErrorInvalidValue;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(192);
+    cfg.dynamicSmemBytes = S::kBytes;
+    cfg.stream = st;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    at[1].id = cudaLaunchAttributeClusterDimension;
+    at[1].val.clusterDim.x = 2;
+    at[1].val.clusterDim.y = 1;
+    at[1].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 2;
+    unsigned long long* tr = nullptr;
+    const CUtensorMap tn = nx.tm ? *nx.tm : B;
+    CUDA_TRY_LAUNCH(cudaLaunchKernelEx(&cfg, kern, A, B, out, M, N, kblk, per, splits, pack, tr, tn, nx));
+  }
   return cudaGetLastError();
 }
 
-template <int BN, int EPI>
+template <int BN, int EPI, int CL = 1>
 static cudaError_t prep_t() {
-  constexpr int ST = gemm_stages(BN);
-  return cudaFuncSetAttribute(gemm_bf16_kernel<BN, ST, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              GemmSmem<BN, ST>::kBytes);
+  constexpr int ST = gemm_stages(BN, CL);
+  return cudaFuncSetAttribute(gemm_bf16_kernel<BN, ST, EPI, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              GemmSmem<BN, ST, CL>::kBytes);
 }
 
 #define PIC_GEMM_BNS(X) X(64) X(128) X(144) X(160) X(176) X(192) X(208) X(224) X(256)
 #define PIC_SWIGLU_BNS(X) X(32) X(64) X(128) X(224) X(256)
+// CTA-pair (cta_group::2) instantiations: N-tiles of the tensor-bound multi-m-tile GEMMs
+#define PIC_PAIR_BNS(X) X(128) X(192) X(224) X(256)
 
 cudaError_t prepare_gemm() {
   cudaError_t e = cudaSuccess;
@@ -361,7 +439,18 @@ cudaError_t prepare_gemm() {
   PIC_SWIGLU_BNS(P2)
 #undef P1
 #undef P2
+#define P3(bn)                                                   \
+  if (e == cudaSuccess) e = prep_t<bn, EPI_PARTIAL, 2>();        \
+  if (e == cudaSuccess) e = prep_t<bn, EPI_SWIGLU, 2>();
+  PIC_PAIR_BNS(P3)
+#undef P3
   return e;
+}
+
+bool gemm_pair_supported(int bn) {
+#define C1(b) || bn == b
+  return false PIC_PAIR_BNS(C1);
+#undef C1
 }
 
 bool gemm_bn_supported(int bn, bool swiglu) {
@@ -371,7 +460,17 @@ bool gemm_bn_supported(int bn, bool swiglu) {
 }
 
 cudaError_t launch_gemm_partial(const CUtensorMap& A, const CUtensorMap& B, float* out, int M, int N, int K,
-                                int splits, int bn, cudaStream_t st, int pack, const GemmNext& nx) {
+                                int splits, int bn, cudaStream_t st, int pack, const GemmNext& nx, int pair) {
+  if (pair) {
+    switch (bn) {
+#define L3(b) \
+  case b:     \
+    return launch_gemm_t<b, EPI_PARTIAL, 2>(A, B, out, M, N, K, splits, pack, st, nx);
+      PIC_PAIR_BNS(L3)
+#undef L3
+    }
+    return cudaErrorInvalidValue;
+  }
   switch (bn) {
 #define L1(b) \
   case b:     \
@@ -383,7 +482,17 @@ cudaError_t launch_gemm_partial(const CUtensorMap& A, const CUtensorMap& B, floa
 }
 
 cudaError_t launch_gemm_swiglu(const CUtensorMap& A, const CUtensorMap& B, void* u, int M, int N2, int K, int bn,
-                               cudaStream_t st, int pack, const GemmNext& nx) {
+                               cudaStream_t st, int pack, const GemmNext& nx, int pair) {
+  if (pair) {
+    switch (bn) {
+#define L4(b) \
+  case b:     \
+    return launch_gemm_t<b, EPI_SWIGLU, 2>(A, B, u, M, N2, K, 1, pack, st, nx);
+      PIC_PAIR_BNS(L4)
+#undef L4
+    }
+    return cudaErrorInvalidValue;
+  }
   switch (bn) {
 #define L2(b) \
   case b:     \

@@ -86,12 +86,16 @@ struct GemmNext {
   int units, mt, splits, kper, kblk_total, bn, pfk;
 };
 GemmNext gemm_next(const CUtensorMap* B, int M, int N, int K, int splits, int bn, int pfk);
+// pair = 1: CTA-pair (cta_group::2) kernel with 256-row M-tiles; B's tensor map box must then be bn/2 rows
+// (each CTA of the pair loads half of the N-tile); bn in gemm_pair_supported().
 cudaError_t launch_gemm_partial(const CUtensorMap& A, const CUtensorMap& B, float* out, int M, int N, int K,
-                                int splits, int bn, cudaStream_t st, int pack = 0, const GemmNext& nx = GemmNext{});
+                                int splits, int bn, cudaStream_t st, int pack = 0, const GemmNext& nx = GemmNext{},
+                                int pair = 0);
+bool gemm_pair_supported(int bn);
 // Gate/up GEMM with the SwiGLU epilogue fused: B = interleaved [gate|up] groups of bn/2 rows (N2 = 2F rows),
 // u[M][F] bf16 = silu(x·W_gᵀ) ⊙ (x·W_uᵀ).  Split-K 1.
 cudaError_t launch_gemm_swiglu(const CUtensorMap& A, const CUtensorMap& B, void* u, int M, int N2, int K, int bn,
-                               cudaStream_t st, int pack = 0, const GemmNext& nx = GemmNext{});
+                               cudaStream_t st, int pack = 0, const GemmNext& nx = GemmNext{}, int pair = 0);
 bool gemm_bn_supported(int bn, bool swiglu);
 
 // ---- persistent GEMM chain (gemm_chain.cu): O-proj -> residual+RMSNorm -> gate/up+SwiGLU -> down ->

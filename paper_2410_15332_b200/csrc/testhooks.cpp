@@ -50,7 +50,9 @@ static float g_attn_us = 0.f;
 extern "C" pic_status pic_test_gemm(const uint16_t* A, const uint16_t* B, int32_t M, int32_t N, int32_t K, int32_t bn,
                                     int32_t splits, float* out) {
   if (!A || !B || !out || M <= 0 || N <= 0 || K <= 0 || K % 64 || N % 32 || splits <= 0) return PIC_E_INVALID_ARG;
-  if (bn != 64 && bn != 128 && bn != 256) return PIC_E_INVALID_ARG;
+  const int pair = bn < 0;  // negative bn: CTA-pair kernel (cta_group::2) with N-tile |bn|
+  bn = bn < 0 ? -bn : bn;
+  if (pair ? !gemm_pair_supported(bn) : (bn != 64 && bn != 128 && bn != 256)) return PIC_E_INVALID_ARG;
   TCK(prepare_kernels());
   DevBuf a, b, p;
   TCK(cudaMalloc(&a.p, (size_t)M * K * 2));
@@ -60,9 +62,9 @@ extern "C" pic_status pic_test_gemm(const uint16_t* A, const uint16_t* B, int32_
   TCK(cudaMemcpy(b.p, B, (size_t)N * K * 2, cudaMemcpyHostToDevice));
   CUtensorMap ta, tb;
   uint64_t da[2] = {(uint64_t)K, (uint64_t)M}, db[2] = {(uint64_t)K, (uint64_t)N}, st[1] = {(uint64_t)K * 2};
-  uint32_t ba[2] = {64, 128}, bb[2] = {64, (uint32_t)bn};
+  uint32_t ba[2] = {64, 128}, bb[2] = {64, (uint32_t)(pair ? bn / 2 : bn)};
   if (!tmap(&ta, a.p, 2, da, st, ba) || !tmap(&tb, b.p, 2, db, st, bb)) return PIC_E_CUDA;
-  TCK(launch_gemm_partial(ta, tb, reinterpret_cast<float*>(p.p), M, N, K, splits, bn, 0));
+  TCK(launch_gemm_partial(ta, tb, reinterpret_cast<float*>(p.p), M, N, K, splits, bn, 0, 0, GemmNext{}, pair));
   TCK(cudaDeviceSynchronize());
   std::vector<float> part((size_t)splits * M * N);
   TCK(cudaMemcpy(part.data(), p.p, part.size() * 4, cudaMemcpyDeviceToHost));
@@ -222,6 +224,9 @@ extern "C" pic_status pic_test_kv_link(uint16_t* Kpool, uint16_t* Vpool, int32_t
 extern "C" pic_status pic_bench_gemm(int32_t M, int32_t N, int32_t K, int32_t bn, int32_t splits, int32_t iters,
                                      float* us_per_launch) {
   if (M <= 0 || N <= 0 || K % 64 || N % 32 || splits <= 0 || iters <= 0 || !us_per_launch) return PIC_E_INVALID_ARG;
+  const int pair = bn < 0;  // negative bn: CTA-pair kernel with N-tile |bn|
+  bn = bn < 0 ? -bn : bn;
+  if (pair && !gemm_pair_supported(bn)) return PIC_E_INVALID_ARG;
   TCK(prepare_kernels());
   const size_t wbytes = (size_t)N * K * 2;
   const int copies = (int)std::max<size_t>(2, (size_t)(512u << 20) / wbytes + 1);  // > L2 in total
@@ -229,13 +234,19 @@ extern "C" pic_status pic_bench_gemm(int32_t M, int32_t N, int32_t K, int32_t bn
   TCK(cudaMalloc(&a.p, (size_t)M * K * 2));
   TCK(cudaMalloc(&b.p, wbytes * copies));
   TCK(cudaMalloc(&p.p, (size_t)splits * M * N * 4));
-  TCK(cudaMemset(a.p, 0, (size_t)M * K * 2));
-  TCK(cudaMemset(b.p, 0, wbytes * copies));
+  if (getenv("PIC_BENCH_RANDOM")) {  // seeded random operands: tensor-core power (and clocks) as in the engine
+    TCK(launch_gen_matrix(a.p, M, K, 1, 1, 0, 0, 0));
+    TCK(launch_gen_matrix(b.p, (int64_t)N * copies, K, 2, 2, -6, 0, 0));
+    TCK(cudaDeviceSynchronize());
+  } else {
+    TCK(cudaMemset(a.p, 0, (size_t)M * K * 2));
+    TCK(cudaMemset(b.p, 0, wbytes * copies));
+  }
   CUtensorMap ta;
   std::vector<CUtensorMap> tb(copies);
   const int pack = getenv("PIC_BENCH_PACK") ? atoi(getenv("PIC_BENCH_PACK")) : 0;
   uint64_t da[2] = {(uint64_t)K, (uint64_t)M}, db[2] = {(uint64_t)K, (uint64_t)N}, st[1] = {(uint64_t)K * 2};
-  uint32_t ba[2] = {64, 128}, bb[2] = {64, (uint32_t)bn};
+  uint32_t ba[2] = {64, 128}, bb[2] = {64, (uint32_t)(pair ? bn / 2 : bn)};
   if (pack) {  // packed view: rows of 64 elements
     db[0] = 64;
     db[1] = (uint64_t)N * K / 64;
@@ -252,18 +263,19 @@ extern "C" pic_status pic_bench_gemm(int32_t M, int32_t N, int32_t K, int32_t bn
   TCK(cudaEventCreate(&e0));
   TCK(cudaEventCreate(&e1));
   for (int i = 0; i < 3; ++i)
-    TCK(launch_gemm_partial(ta, tb[i % copies], reinterpret_cast<float*>(p.p), M, N, K, splits, bn, s, pack));
+    TCK(launch_gemm_partial(ta, tb[i % copies], reinterpret_cast<float*>(p.p), M, N, K, splits, bn, s, pack,
+                            GemmNext{}, pair));
   const int pfk = getenv("PIC_BENCH_PFK") ? atoi(getenv("PIC_BENCH_PFK")) : 0;  // next-GEMM L2 prefetch depth
   TCK(cudaEventRecord(e0, s));
   for (int i = 0; i < iters; ++i)
     TCK(launch_gemm_partial(ta, tb[i % copies], reinterpret_cast<float*>(p.p), M, N, K, splits, bn, s, pack,
-                            gemm_next(pack ? nullptr : &tb[(i + 1) % copies], M, N, K, splits, bn, pfk)));
+                            gemm_next(pack || pair ? nullptr : &tb[(i + 1) % copies], M, N, K, splits, bn, pfk), pair));
   TCK(cudaEventRecord(e1, s));
   TCK(cudaEventSynchronize(e1));
   float ms = 0;
   TCK(cudaEventElapsedTime(&ms, e0, e1));
   *us_per_launch = ms * 1000.f / iters;
-  if (getenv("PIC_GEMM_TRACE")) {  // one more pair of launches with the per-CTA timeline of the second
+  if (getenv("PIC_GEMM_TRACE") && !pair) {  // one more pair of launches with the per-CTA timeline of the second
     DevBuf tr;
     TCK(cudaMalloc(&tr.p, 148 * 6 * 8));
     TCK(cudaMemset(tr.p, 0, 148 * 6 * 8));
@@ -305,7 +317,10 @@ extern "C" pic_status pic_bench_attention(const uint16_t* Q, const uint16_t* K, 
 
 extern "C" pic_status pic_test_gemm_swiglu(const uint16_t* A, const uint16_t* B, int32_t M, int32_t N2, int32_t K,
                                            int32_t bn, uint16_t* u) {
-  if (!A || !B || !u || M <= 0 || N2 <= 0 || K % 64 || N2 % bn || !gemm_bn_supported(bn, true)) return PIC_E_INVALID_ARG;
+  const int pair = bn < 0;  // negative bn: CTA-pair kernel with N-tile |bn|
+  bn = bn < 0 ? -bn : bn;
+  if (!A || !B || !u || M <= 0 || N2 <= 0 || K % 64 || N2 % bn) return PIC_E_INVALID_ARG;
+  if (pair ? !gemm_pair_supported(bn) : !gemm_bn_supported(bn, true)) return PIC_E_INVALID_ARG;
   TCK(prepare_kernels());
   DevBuf a, b, p;
   TCK(cudaMalloc(&a.p, (size_t)M * K * 2));
@@ -315,9 +330,9 @@ extern "C" pic_status pic_test_gemm_swiglu(const uint16_t* A, const uint16_t* B,
   TCK(cudaMemcpy(b.p, B, (size_t)N2 * K * 2, cudaMemcpyHostToDevice));
   CUtensorMap ta, tb;
   uint64_t da[2] = {(uint64_t)K, (uint64_t)M}, db[2] = {(uint64_t)K, (uint64_t)N2}, st[1] = {(uint64_t)K * 2};
-  uint32_t ba[2] = {64, 128}, bb[2] = {64, (uint32_t)bn};
+  uint32_t ba[2] = {64, 128}, bb[2] = {64, (uint32_t)(pair ? bn / 2 : bn)};
   if (!tmap(&ta, a.p, 2, da, st, ba) || !tmap(&tb, b.p, 2, db, st, bb)) return PIC_E_CUDA;
-  TCK(launch_gemm_swiglu(ta, tb, p.p, M, N2, K, bn, 0));
+  TCK(launch_gemm_swiglu(ta, tb, p.p, M, N2, K, bn, 0, 0, GemmNext{}, pair));
   TCK(cudaDeviceSynchronize());
   TCK(cudaMemcpy(u, p.p, (size_t)M * (N2 / 2) * 2, cudaMemcpyDeviceToHost));
   return PIC_OK;

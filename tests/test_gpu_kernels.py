@@ -63,7 +63,10 @@ def test_embed_lm_gains_bit_exact(tiny_engine):
 @pytest.mark.parametrize("M_,N_,K_,bn,splits", [
     (128, 256, 128, 128, 1), (100, 192, 64, 64, 1), (1, 512, 4096, 256, 3), (300, 512, 640, 128, 2),
     (128, 6144, 4096, 256, 6), (609, 256, 1024, 256, 1), (17, 96, 192, 64, 3),
-    (96, 512, 256, 64, 2), (96, 512, 256, 256, 2)])
+    (96, 512, 256, 64, 2), (96, 512, 256, 256, 2),
+    # CTA pair (cta_group::2, 256-row M-tiles; negative bn): ragged M, several units per pair, split-K
+    (256, 512, 256, -256, 1), (609, 1024, 512, -256, 2), (300, 768, 640, -128, 1), (100, 384, 128, -192, 1),
+    (1000, 448, 256, -224, 3), (3000, 2048, 256, -256, 1)])
 def test_gemm_vs_fp64(M_, N_, K_, bn, splits):
     A = rand_bf16(M_ * 7 + K_, (M_, K_))
     Bm = rand_bf16(N_ * 3 + K_, (N_, K_), 0.05)
@@ -73,9 +76,9 @@ def test_gemm_vs_fp64(M_, N_, K_, bn, splits):
 
 
 @pytest.mark.parametrize("M_,F,K_,bn", [(128, 14336 // 8, 512, 224), (37, 256, 128, 64), (300, 512, 256, 256),
-                                       (5, 64, 64, 32)])
+                                       (5, 64, 64, 32), (600, 14336 // 8, 512, -224), (300, 512, 256, -256)])
 def test_gemm_swiglu_vs_fp64(M_, F, K_, bn):
-    g = bn // 2
+    g = abs(bn) // 2
     A = rand_bf16(M_ + K_, (M_, K_))
     Wg = rand_bf16(F + 1, (F, K_), 0.05)
     Wu = rand_bf16(F + 2, (F, K_), 0.05)
