@@ -217,21 +217,27 @@ __global__ void __launch_bounds__(1024) residual_rmsnorm_kernel(float* __restric
                                                                  float eps) {
   PIC_PDL_ENTRY();
   __shared__ float red[32];
+  constexpr int VPT = 8;  // float4 per thread kept in registers between the two passes
   const int r = blockIdx.x;
   const int n4 = d / 4;
   float4* hr = reinterpret_cast<float4*>(h + (size_t)r * d);
+  float4 vc[VPT];
   float ss = 0.f;
-  for (int i = threadIdx.x; i < n4; i += blockDim.x) {
+#pragma unroll
+  for (int k = 0; k < VPT; ++k) {
+    const int i = threadIdx.x + k * blockDim.x;
+    if (i >= n4) break;
     float4 v = hr[i];
     if (srcs.n) {
       float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll 8
-      for (int k = 0; k < srcs.n; ++k)
-        add4(acc, __ldcg(reinterpret_cast<const float4*>(srcs.p[k]) + (size_t)r * n4 + i));
+      for (int s = 0; s < srcs.n; ++s)
+        add4(acc, __ldcg(reinterpret_cast<const float4*>(srcs.p[s]) + (size_t)r * n4 + i));
       add4(v, acc);
       hr[i] = v;
     }
     ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+    vc[k] = v;
   }
   if (!x) return;
   const int orow = out_map ? out_map[r] : r;
@@ -239,8 +245,11 @@ __global__ void __launch_bounds__(1024) residual_rmsnorm_kernel(float* __restric
   if (orow < 0) return;
   const float inv = rsqrtf(ss / d + eps);
   const float4* g4 = reinterpret_cast<const float4*>(g);
-  for (int i = threadIdx.x; i < n4; i += blockDim.x) {
-    const float4 v = hr[i], w = g4[i];
+#pragma unroll
+  for (int k = 0; k < VPT; ++k) {
+    const int i = threadIdx.x + k * blockDim.x;
+    if (i >= n4) break;
+    const float4 v = vc[k], w = g4[i];
     store4<F32>(x, (size_t)orow * d + 4 * i, v.x * inv * w.x, v.y * inv * w.y, v.z * inv * w.z, v.w * inv * w.w);
   }
 }
@@ -248,7 +257,13 @@ __global__ void __launch_bounds__(1024) residual_rmsnorm_kernel(float* __restric
 cudaError_t launch_residual_rmsnorm_srcs(float* h, const Srcs& srcs, const float* g, void* x, const int32_t* out_map,
                                          int M, int d, float eps, cudaStream_t st, int f32) {
   if (M == 0) return cudaSuccess;
-  const int nt = std::max(32, std::min(1024, d / 4));
+  // One CTA per row.  Few rows (a link's k'): one float4 per thread, the most threads in flight for a
+  // latency-bound launch between two GEMMs (cfg2 4.13 vs 4.28 ms with four).  Many rows (batched links,
+  // CacheBlend's layer 0): four float4 per thread, 8 rows resident per SM (cfg4 6.7 -> 5.0 ms per link).
+  const int n4 = d / 4;
+  const int vpt = M >= 2048 ? 4 : 1;
+  const int nt = std::max(32, std::min(1024, ((n4 + vpt - 1) / vpt + 31) / 32 * 32));
+  if ((n4 + nt - 1) / nt > 8) return cudaErrorInvalidValue;
   if (f32)
     CUDA_TRY_LAUNCH(launch_k(residual_rmsnorm_kernel<true>, dim3(M), dim3(nt), 0, st, h, srcs, g, x, out_map, M, d, eps));
   else
