@@ -351,6 +351,18 @@ def main():
             held = (eng.link_batch(reqs, w.alg, keep_linked=True) if len(reqs) > 1
                     else [eng.link(reqs[0], w.alg, keep_linked=True)])
             hs = [o.linked for o in held]
+            # shared-block links: re-base the shared blocks into owned ones once, instead of re-rotating
+            # them in every decode step (pic_linked_materialize; timed on its own)
+            mat_ms = None
+            if args.kv_share:
+                torch.cuda.synchronize(dev)
+                m0, m1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                m0.record(stream)
+                for h in hs:
+                    eng.materialize(h)
+                m1.record(stream)
+                m1.synchronize()
+                mat_ms = m0.elapsed_time(m1)
             forced = [int(t) for t in sg.tokens(0xDEC0DE, 7, len(hs), m.vocab, None)]
             dl = torch.empty((len(hs), m.vocab), dtype=torch.float32, device=f"cuda:{dev}")
             for _ in range(3):
@@ -374,9 +386,10 @@ def main():
             batch_all = D.sum_over_ranks(len(hs), device=red_dev)
             dec = {"tpot_ms": tpot, "tokens_per_s": batch_all / (tpot / 1e3), "batch_per_gpu": len(hs),
                    "context_tokens": int(max_N), "steps": args.decode_steps, "tpot_ms_host_greedy": tpot_host,
-                   "gpu_launches_per_step": int(dec_launches),
+                   "gpu_launches_per_step": int(dec_launches), "materialize_ms": mat_ms,
                    "how": "pic_decode over the linked caches of this rank's requests (f1), one token per cache per "
-                          "step, CUDA events on the bench stream (teacher-forced), then a greedy host loop"}
+                          "step, CUDA events on the bench stream (teacher-forced), then a greedy host loop; "
+                          "shared-block links are materialized first (pic_linked_materialize, materialize_ms)"}
             for h in hs:
                 eng.release(h)
 

@@ -220,6 +220,11 @@ pic_status pic_linked_info(pic_engine* eng, const pic_linked* linked, int32_t* n
  * linked by reference, and per block (int32[ceil(N/16)], nullable) the Δ the attention applies to its keys
  * (0 for blocks the link owns).  Host-only bookkeeping. */
 pic_status pic_linked_sharing(pic_engine* eng, const pic_linked* linked, int32_t* n_shared, int32_t* block_delta);
+/* Re-base the shared chunk-store blocks (Δ != 0) of a kv_share linked cache into blocks it owns, on
+ * `stream` (one a2 launch over their rows, all layers), dropping its references on them: later decode
+ * steps then read keys at their linked positions instead of re-rotating them every step.  Results are
+ * unchanged bit for bit.  PIC_E_CAPACITY if the pool lacks the blocks (the handle is unchanged). */
+pic_status pic_linked_materialize(pic_engine* eng, pic_linked* linked, void* stream);
 /* Release a linked cache: its own blocks return to the pool; shared chunk-store blocks drop one reference
  * (they stay with the chunk store, or return to the pool if their chunk was expired meanwhile). */
 pic_status pic_linked_release(pic_engine* eng, pic_linked* linked);

@@ -2030,6 +2030,53 @@ extern "C" pic_status pic_linked_sharing(pic_engine* e, const pic_linked* h, int
   return PIC_OK;
 }
 
+// Re-base the shared chunk-store blocks of a linked cache into blocks it owns (f3 -> copy layout), so
+// that later decode steps read keys at their linked positions without re-rotating them every step.
+// One a2 launch (all layers) over the rows of every shared block with Δ != 0; the arithmetic is a2's,
+// so exports and decode outputs are unchanged bit for bit.
+extern "C" pic_status pic_linked_materialize(pic_engine* e, pic_linked* h, void* stream) {
+  if (!e || !h) return fail(PIC_E_INVALID_ARG, "NULL argument");
+  if (e->host_only) return fail(PIC_E_NO_DEVICE, "host-only engine");
+  std::vector<int> idx;
+  for (size_t b = 0; b < h->bdelta.size(); ++b)
+    if (h->bdelta[b] != 0) idx.push_back((int)b);
+  if (idx.empty()) return PIC_OK;
+  const size_t n = idx.size() * 16;
+  if (3 * n > e->plan_cap_ints) return fail(PIC_E_CAPACITY, "materialize: %zu rows exceed the plan buffer", n);
+  if (!e->alloc.can((int64_t)idx.size()))
+    return fail(PIC_E_CAPACITY, "pool has %zu free blocks, materialize needs %zu", e->alloc.free_ids.size(), idx.size());
+  std::vector<int32_t> fresh = e->alloc.alloc((int64_t)idx.size());
+  std::vector<int32_t> host(3 * n);
+  for (size_t k = 0; k < idx.size(); ++k)
+    for (int j = 0; j < 16; ++j) {
+      host[k * 16 + j] = h->blocks[idx[k]] * 16 + j;          // src slot (chunk-store block)
+      host[n + k * 16 + j] = fresh[k] * 16 + j;               // dst slot (owned block)
+      host[2 * n + k * 16 + j] = h->bdelta[idx[k]];           // Δ
+    }
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  CK(cudaEventSynchronize(e->plan_ev));
+  std::memcpy(e->plan_host, host.data(), host.size() * 4);
+  CK(cudaMemcpyAsync(e->plan_dev, e->plan_host, host.size() * 4, cudaMemcpyHostToDevice, st));
+  CK(cudaEventRecord(e->plan_ev, st));
+  const cudaError_t ce = launch_kv_link(e->Kpool, e->Vpool, e->plan_dev, e->plan_dev + n, e->plan_dev + 2 * n, (int)n,
+                                        0, e->cfg.n_layers, e->layer_stride, e->cfg.n_kv_heads, e->cfg.head_dim,
+                                        e->cos_t, e->sin_t, 1, st, e->f32);
+  if (ce != cudaSuccess) {
+    e->alloc.release(fresh);
+    return fail(PIC_E_CUDA, "materialize: %s", cudaGetErrorString(ce));
+  }
+  // the chunk-store blocks lose this reference; later work on `stream` is ordered after the copy
+  std::vector<int32_t> old;
+  for (size_t k = 0; k < idx.size(); ++k) {
+    old.push_back(h->blocks[idx[k]]);
+    h->blocks[idx[k]] = fresh[k];
+    h->bdelta[idx[k]] = 0;
+  }
+  e->alloc.release(old);
+  h->n_shared -= (int32_t)idx.size();
+  return PIC_OK;
+}
+
 extern "C" pic_status pic_linked_release(pic_engine* e, pic_linked* h) {
   if (!e || !h) return fail(PIC_E_INVALID_ARG, "NULL argument");
   e->alloc.release(h->blocks);

@@ -100,7 +100,7 @@ class KernelStatC(C.Structure):
 
 # every symbol include/pic.h and include/pic_test.h declare
 EXPORTS = ["pic_arena_bytes", "pic_engine_create", "pic_engine_destroy", "pic_generate_context_cache", "pic_link",
-           "pic_link_batch", "pic_plan", "pic_linked_export", "pic_linked_info", "pic_linked_sharing", "pic_linked_release",
+           "pic_link_batch", "pic_plan", "pic_linked_export", "pic_linked_info", "pic_linked_sharing", "pic_linked_materialize", "pic_linked_release",
            "pic_cache_export", "pic_cache_info", "pic_expire_cache", "pic_read_weights", "pic_get_stats",
            "pic_last_error", "pic_status_string", "pic_arena_bytes_tp", "pic_engine_create_tp", "pic_tp_ipc_handle",
            "pic_tp_connect", "pic_generate_context_cache_ex", "pic_decode", "pic_serve_poisson", "pic_serve_arrivals", "pic_set_profiling", "pic_get_profile", "pic_test_gemm", "pic_test_attention", "pic_test_kv_link", "pic_bench_gemm", "pic_bench_attention", "pic_test_gemm_swiglu"]
@@ -145,6 +145,7 @@ def lib() -> C.CDLL:
         L.pic_linked_export.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p]
         L.pic_linked_info.argtypes = [C.c_void_p, C.c_void_p, P(C.c_int32), P(C.c_int32)]
         L.pic_linked_sharing.argtypes = [C.c_void_p, C.c_void_p, P(C.c_int32), P(C.c_int32)]
+        L.pic_linked_materialize.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
         L.pic_linked_release.argtypes = [C.c_void_p, C.c_void_p]
         L.pic_cache_export.argtypes = [C.c_void_p, C.c_uint64, C.c_int32, C.c_void_p, C.c_void_p]
         L.pic_cache_info.argtypes = [C.c_void_p, C.c_uint64, P(C.c_int32), P(C.c_int32)]
@@ -490,6 +491,10 @@ class Engine:
         ns = C.c_int32()
         check(lib().pic_linked_sharing(self._h, C.c_void_p(linked), C.byref(ns), _ptr(bd)))
         return ns.value, bd
+
+    def materialize(self, linked: int) -> None:
+        """Copy + re-base the shared chunk-store blocks of a kv_share linked cache into owned blocks."""
+        check(lib().pic_linked_materialize(self._h, C.c_void_p(linked), self._stream))
 
     def release(self, linked: int) -> None:
         check(lib().pic_linked_release(self._h, C.c_void_p(linked)))

@@ -186,3 +186,35 @@ def test_shared_link_fp32_debug_bit_identical():
                 s.eng.release(shared[0].linked)
     finally:
         s.eng.close()
+
+
+def test_materialize_bit_identical_and_accounting(setup):
+    """pic_linked_materialize copies + re-bases the shared blocks with Δ != 0 into owned blocks: exports
+    and later decode steps are bit-identical to the copy path, the handle no longer needs the K-tile
+    rotation (bdelta all zero), and the chunk-store blocks lose its references."""
+    s = setup
+    segs = s.w.requests[0]
+    hc = s.eng.link(s.segs(segs), "legolink:4", keep_linked=True, kv_share=False).linked
+    hs = s.eng.link(s.segs(segs), "legolink:4", keep_linked=True, kv_share=True).linked
+    try:
+        n_shared0, bd0 = s.eng.linked_sharing(hs)
+        n_rot = int((bd0 != 0).sum())
+        assert n_rot > 0
+        free0 = s.eng.stats()["free_blocks"]
+        s.eng.materialize(hs)
+        n_shared1, bd1 = s.eng.linked_sharing(hs)
+        assert n_shared1 == n_shared0 - n_rot and not bd1.any()
+        assert s.eng.stats()["free_blocks"] == free0 - n_rot      # fresh owned blocks; store blocks still cached
+        for l in range(s.cfg.n_layers):
+            kc, vc = s.eng.linked_export(hc, l)
+            ks, vs = s.eng.linked_export(hs, l)
+            assert np.array_equal(kc, ks) and np.array_equal(vc, vs), l
+        for t in (5, 17, 99, 3, 250):
+            a = s.eng.decode([hc], [t])
+            b = s.eng.decode([hs], [t])
+            assert np.array_equal(a.logits, b.logits)
+        s.eng.materialize(hs)                                    # idempotent: nothing left to re-base
+        assert s.eng.linked_sharing(hs)[0] == n_shared1
+    finally:
+        s.eng.release(hc)
+        s.eng.release(hs)
