@@ -55,15 +55,269 @@ constexpr int gemm_stages(int bn, int cl = 1) {
 //   EPI_SWIGLU (split-K = 1): B rows are W_gate/W_up interleaved in groups of BN/2 (n-tile = gate rows
 //     [n·BN/2, (n+1)·BN/2) then the matching up rows); out = bf16 u[M][N/2] = silu(gate) ⊙ up
 //     (the a8 SwiGLU fused into the GEMM epilogue; P:241 Llama-family MLP, reading R4).
-// CL = 2: CTA pair (cta_group::2).  A unit is a 256-row M-tile: each CTA of the pair loads its 128 rows of A
+template <int BN, int STAGES, int EPI>
+__global__ void __launch_bounds__(192, 1)
+    gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                     void* __restrict__ out_, int M, int N, int kblk_total, int kblk_per_split, int splits,
+                     int pack, unsigned long long* trace, const __grid_constant__ CUtensorMap tmN,
+                     GemmNext nx) {
+  using S = GemmSmem<BN, STAGES>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw;
+  if (threadIdx.x == 0 && (smem_u32(smem) & 1023)) __trap();  // SWIZZLE_128B tiles need 1 KB alignment
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * S::kA;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * S::kStage);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + S::kBars);
+  const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + STAGES);
+  const uint32_t tfull0 = smem_u32(bars + 2 * STAGES), tempty0 = smem_u32(bars + 2 * STAGES + 2);
+
+  const int warp = warp_id(), lane = lane_id();
+  const int mt = (M + 127) / 128, nt = (N + BN - 1) / BN;
+  const int units = mt * nt * splits;
+  griddep_launch();
+  if (trace && threadIdx.x == 0) trace[blockIdx.x * 6 + 0] = globaltimer();
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(full0 + 8 * s, 1);
+      mbar_init(empty0 + 8 * s, 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(tfull0 + 8 * b, 1);
+      mbar_init(tempty0 + 8 * b, 128);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc(smem_u32(tmem_slot), S::kTmemCols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  // unit u -> (m fastest, then split, then n): concurrently running CTAs share weight tiles in L2
+  auto decode = [&](int u, int& m0, int& n_idx, int& kb0, int& nkb) {
+    const int m = u % mt;
+    const int r = u / mt;
+    const int sp = r % splits;
+    n_idx = r / splits;
+    m0 = m * 128;
+    kb0 = sp * kblk_per_split;
+    nkb = max(0, min(kblk_per_split, kblk_total - kb0));
+  };
+
+  // B tile of k-block kb: row-major weights -> one [BN x 64] box; packed weights (pack rows per
+  // sub-tile, stored [N/pack][K/64][pack][64]) -> BN/pack contiguous boxes of pack x 128 B.
+  const uint64_t wpol = l2_policy_evict_first();  // weights are streamed once per forward
+  auto load_b = [&](uint32_t dst, uint32_t bar, int kb, int n_idx) {
+    if (pack == 0) {
+      if (weight_evict_first())
+        tma_load_2d_hint(dst, &tmB, bar, kb * 64, n_idx * BN, wpol);
+      else
+        tma_load_2d(dst, &tmB, bar, kb * 64, n_idx * BN);
+    } else {
+      const int per = BN / pack;
+      for (int j = 0; j < per; ++j) {
+        const int t = n_idx * per + j;
+        tma_load_2d(dst + j * pack * 128, &tmB, bar, 0, (t * kblk_total + kb) * pack);
+      }
+    }
+  };
+
+  if (warp == 0) {
+    if (lane == 0) {
+      tma_prefetch(&tmA);
+      tma_prefetch(&tmB);
+      int it = 0;
+      bool waited = false;
+      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        int m0, n_idx, kb0, nkb;
+        decode(u, m0, n_idx, kb0, nkb);
+        int kk = 0;
+        if (!waited) {
+          // Weights do not depend on the previous kernel: stream the first stages of B while it
+          // drains (PDL), then wait for it before loading the activations A.
+          const int pre = min(nkb, STAGES);
+          for (int i = 0; i < pre; ++i) {
+            mbar_expect_tx(full0 + 8 * i, S::kStage);
+            load_b(smem_u32(sB + i * S::kB), full0 + 8 * i, kb0 + i, n_idx);
+          }
+          griddep_wait();
+          if (trace) trace[blockIdx.x * 6 + 1] = globaltimer();
+          waited = true;
+          for (int i = 0; i < pre; ++i) tma_load_2d(smem_u32(sA + i * S::kA), &tmA, full0 + 8 * i, (kb0 + i) * 64, m0);
+          kk = pre;
+          it = pre;
+        }
+        for (; kk < nkb; ++kk, ++it) {
+          const int s = it % STAGES;
+          mbar_wait(empty0 + 8 * s, ((it / STAGES) & 1) ^ 1);
+          mbar_expect_tx(full0 + 8 * s, S::kStage);
+          const int kc = (kb0 + kk) * 64;
+          tma_load_2d(smem_u32(sA + s * S::kA), &tmA, full0 + 8 * s, kc, m0);
+          load_b(smem_u32(sB + s * S::kB), full0 + 8 * s, kb0 + kk, n_idx);
+        }
+      }
+      if (!waited) griddep_wait();
+      // All of this GEMM's loads are issued: pull the first k-blocks of the NEXT GEMM's weights into
+      // L2 so that its ring fill (at its launch) hits L2 instead of waiting on HBM.
+      for (int u2 = blockIdx.x; u2 < nx.units && nx.pfk > 0; u2 += gridDim.x) {
+        const int r2 = u2 / nx.mt;
+        if (u2 % nx.mt) continue;  // same weights for every m-tile
+        const int kb2 = (r2 % nx.splits) * nx.kper, n2 = r2 / nx.splits;
+        const int nk2 = min(nx.pfk, nx.kblk_total - kb2);
+        for (int i = 0; i < nk2; ++i) tma_prefetch_l2_2d(&tmN, (kb2 + i) * 64, n2 * nx.bn);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_bf16(128, BN, 0, 0);
+      int it = 0, i = 0;
+      for (int u = blockIdx.x; u < units; u += gridDim.x, ++i) {
+        int m0, n_idx, kb0, nkb;
+        decode(u, m0, n_idx, kb0, nkb);
+        const int ab = i & 1;
+        mbar_wait(tempty0 + 8 * ab, ((i >> 1) & 1) ^ 1);  // epilogue has drained this accumulator
+        tc_fence_after();
+        const uint32_t d = tmem + ab * S::kAcc;
+        for (int kk = 0; kk < nkb; ++kk, ++it) {
+          const int s = it % STAGES;
+          mbar_wait(full0 + 8 * s, (it / STAGES) & 1);
+          if (trace && it == 0) trace[blockIdx.x * 6 + 2] = globaltimer();
+          tc_fence_after();
+          const uint32_t a = smem_u32(sA + s * S::kA), b = smem_u32(sB + s * S::kB);
+#pragma unroll
+          for (int k4 = 0; k4 < 4; ++k4)
+            umma_bf16(d, sdesc_sw128(a + k4 * 32, 16, 1024), sdesc_sw128(b + k4 * 32, 16, 1024), idesc,
+                      (kk | k4) != 0);
+          umma_commit(empty0 + 8 * s);
+        }
+        umma_commit(tfull0 + 8 * ab);
+      }
+      if (trace) trace[blockIdx.x * 6 + 3] = globaltimer();
+    }
+  } else {
+    griddep_wait();  // `out` may still be read by the previous kernel
+    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    int i = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x, ++i) {
+      int m0, n_idx, kb0, nkb;
+      decode(u, m0, n_idx, kb0, nkb);
+      const int ab = i & 1;
+      const int row = m0 + q * 32 + lane;
+      const uint32_t tl = tmem + ab * S::kAcc + ((uint32_t)(q * 32) << 16);
+      const int n0 = n_idx * BN;
+      mbar_wait(tfull0 + 8 * ab, (i >> 1) & 1);
+      tc_fence_after();
+      // The last unit of a CTA runs after its final MMA, when the smem ring is idle: stage the tile
+      // through the ring so that global stores are full 128-B row segments (a row-per-thread store
+      // pattern costs ~4 us per tile in uncoalesced 16-B transactions).
+      const bool stage = u + (int)gridDim.x >= units;
+      uint8_t* stg = smem + (size_t)(warp - 2) * ((BN + 31) / 32) * 4096;
+      const int mrow0 = m0 + q * 32;
+      if constexpr (EPI == EPI_PARTIAL) {
+        const int sp = (u / mt) % splits;
+        float* obase = reinterpret_cast<float*>(out_) + (size_t)sp * M * N;
+        float* orow = obase + (size_t)row * N;
+        const int ncol = min(BN, N - n0);  // multiple of 16
+        if (nkb > 0 && stage) {
+#pragma unroll 1
+          for (int c = 0; c < BN; c += 32) {
+            float v[32];
+            tmem_ld32(tl + c, v);
+            float4* sb = reinterpret_cast<float4*>(stg + (c / 32) * 4096);  // [32 rows][8 float4], XOR-swizzled
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              sb[lane * 8 + (j ^ (lane & 7))] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+            __syncwarp();
+            const int jj = lane & 7;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const int r = i * 4 + (lane >> 3);
+              if (mrow0 + r < M && c + 4 * jj < ncol)
+                *reinterpret_cast<float4*>(obase + (size_t)(mrow0 + r) * N + n0 + c + 4 * jj) = sb[r * 8 + (jj ^ (r & 7))];
+            }
+          }
+        } else if (nkb > 0) {
+#pragma unroll 1
+          for (int c = 0; c < BN; c += 32) {
+            float v[32];
+            tmem_ld32(tl + c, v);  // columns beyond BN are allocated (power-of-2 TMEM) and ignored
+            if (row < M)
+#pragma unroll
+              for (int j = 0; j < 8; ++j)
+                if (c + 4 * j < ncol)
+                  reinterpret_cast<float4*>(orow + n0 + c)[j] =
+                      make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+          }
+        } else if (row < M) {
+          for (int col = n0; col < n0 + ncol; col += 4)
+            *reinterpret_cast<float4*>(orow + col) = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      } else {
+        constexpr int G = BN / 2;
+        constexpr int PR = G / 8;                 // 16-B pieces per row of the u tile
+        constexpr int PS = PR | 1;                // odd smem row stride (in pieces): conflict-free
+        const int F = N / 2;
+        uint16_t* urow = reinterpret_cast<uint16_t*>(out_) + (size_t)row * F + (size_t)n_idx * G;
+        uint4* sb = reinterpret_cast<uint4*>(stg);
+#pragma unroll 1
+        for (int c = 0; c < G; c += 16) {
+          float gv[16], uv[16];
+          tmem_ld16(tl + c, gv);
+          tmem_ld16(tl + G + c, uv);
+          uint32_t pk[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const float g0 = gv[2 * j], g1 = gv[2 * j + 1];
+            pk[j] = pack_bf16(g0 / (1.f + __expf(-g0)) * uv[2 * j], g1 / (1.f + __expf(-g1)) * uv[2 * j + 1]);
+          }
+          if (stage) {
+            sb[lane * PS + c / 8] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+            sb[lane * PS + c / 8 + 1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+          } else if (row < M && n_idx * G + c < F) {
+            uint4* dst = reinterpret_cast<uint4*>(urow + c);
+            dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+            dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+          }
+        }
+        if (stage) {
+          __syncwarp();
+          uint16_t* ubase = reinterpret_cast<uint16_t*>(out_) + (size_t)n_idx * G;
+#pragma unroll 1
+          for (int p = lane; p < 32 * PR; p += 32) {
+            const int r = p / PR, pc = p - r * PR;
+            if (mrow0 + r < M && n_idx * G + pc * 8 < F)
+              *reinterpret_cast<uint4*>(ubase + (size_t)(mrow0 + r) * F + pc * 8) = sb[r * PS + pc];
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(tempty0 + 8 * ab);
+      if (trace && threadIdx.x == 64 && u + (int)gridDim.x >= units) trace[blockIdx.x * 6 + 4] = globaltimer();
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem, S::kTmemCols);
+  }
+}
+
+// The one-CTA kernel above and the CTA-pair kernel below share their structure; they are kept as two
+// kernels because folding the pair path into the one-CTA kernel as a template parameter changed ptxas'
+// register allocation of the one-CTA instances (96 -> 123 registers, +17% instructions) and cost 4% on
+// cfg3 end to end (same-box A/B, scripts/ab_lib.sh).
+// CTA-pair GEMM (cta_group::2, CL = 2; CL = 1 compiles but is not instantiated).  A unit is a 256-row M-tile: each CTA of the pair loads its 128 rows of A
 // and half of the N-tile's B rows into its own smem; the leader CTA issues M = 256 MMAs that read both
 // CTAs' smem and write each CTA's 128 accumulator rows into its own TMEM; both CTAs' loads complete on the
 // leader's full barrier, the MMA commits are multicast to both CTAs' empty / accumulator-full barriers,
 // and both epilogues release the accumulator on the leader's tempty barrier.  Per SM this halves the B
 // bytes staged and read by the tensor core per FLOP (the operand traffic that bounds one-CTA M = 128).
-template <int BN, int STAGES, int EPI, int CL = 1>
+template <int BN, int STAGES, int EPI, int CL = 2>
 __global__ void __launch_bounds__(192, 1)
-    gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+    gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      void* __restrict__ out_, int M, int N, int kblk_total, int kblk_per_split, int splits,
                      int pack, unsigned long long* trace, const __grid_constant__ CUtensorMap tmN,
                      GemmNext nx) {
@@ -79,8 +333,13 @@ __global__ void __launch_bounds__(192, 1)
   const uint32_t tfull0 = smem_u32(bars + 2 * STAGES), tempty0 = smem_u32(bars + 2 * STAGES + 2);
 
   const int warp = warp_id(), lane = lane_id();
-  const uint32_t rank = CL == 2 ? cluster_ctarank() : 0;
-  const int cid = blockIdx.x / CL, ncl = gridDim.x / CL;  // cluster (CTA pair) id / count
+  uint32_t rank = 0;
+  int cid = blockIdx.x, ncl = gridDim.x;  // cluster (CTA pair) id / count
+  if constexpr (CL == 2) {
+    rank = cluster_ctarank();
+    cid = blockIdx.x / 2;
+    ncl = gridDim.x / 2;
+  }
   const int mt = (M + 128 * CL - 1) / (128 * CL), nt = (N + BN - 1) / BN;
   const int units = mt * nt * splits;
   griddep_launch();
@@ -110,8 +369,7 @@ __global__ void __launch_bounds__(192, 1)
     __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  // the leader's full barriers (both CTAs' loads complete there) and accumulator-empty barriers
-  const uint32_t fullL = CL == 2 ? mapa_shared(full0, 0) : full0;
+  // the leader's accumulator-empty barriers (both CTAs' epilogues release the pair's accumulator there)
   const uint32_t temptyL = CL == 2 ? mapa_shared(tempty0, 0) : tempty0;
 
   // unit u -> (m fastest, then split, then n): concurrently running CTAs share weight tiles in L2
@@ -120,7 +378,10 @@ __global__ void __launch_bounds__(192, 1)
     const int r = u / mt;
     const int sp = r % splits;
     n_idx = r / splits;
-    m0 = m * 128 * CL + (int)rank * 128;  // this CTA's 128 rows
+    if constexpr (CL == 1)
+      m0 = m * 128;
+    else
+      m0 = m * 128 * CL + (int)rank * 128;  // this CTA's 128 rows
     kb0 = sp * kblk_per_split;
     nkb = max(0, min(kblk_per_split, kblk_total - kb0));
   };
@@ -128,10 +389,10 @@ __global__ void __launch_bounds__(192, 1)
   // B tile of k-block kb: row-major weights -> one [BN x 64] box; packed weights (pack rows per
   // sub-tile, stored [N/pack][K/64][pack][64]) -> BN/pack contiguous boxes of pack x 128 B.
   const uint64_t wpol = l2_policy_evict_first();  // weights are streamed once per forward
-  const uint64_t apol = l2_policy_evict_normal();
   auto load_b = [&](uint32_t dst, uint32_t bar, int kb, int n_idx) {
     if constexpr (CL == 2) {
-      tma_load_2d_2sm(dst, &tmB, bar, kb * 64, n_idx * BN + (int)rank * (BN / 2), weight_evict_first() ? wpol : apol);
+      tma_load_2d_2sm(dst, &tmB, bar, kb * 64, n_idx * BN + (int)rank * (BN / 2),
+                      weight_evict_first() ? wpol : l2_policy_evict_normal());
       return;
     }
     if (pack == 0) {
@@ -154,41 +415,63 @@ __global__ void __launch_bounds__(192, 1)
       tma_prefetch(&tmB);
       int it = 0;
       bool waited = false;
-      // A pair's loads complete on the leader's full barrier, which alone expects both CTAs' bytes
-      auto expect = [&](int s) {
-        if (rank == 0) mbar_expect_tx(full0 + 8 * s, S::kStage * CL);
-      };
-      auto load_a = [&](int s, int kc, int m0) {
-        if constexpr (CL == 2)
-          tma_load_2d_2sm(smem_u32(sA + s * S::kA), &tmA, fullL + 8 * s, kc, m0, apol);
-        else
-          tma_load_2d(smem_u32(sA + s * S::kA), &tmA, full0 + 8 * s, kc, m0);
-      };
-      for (int u = cid; u < units; u += ncl) {
-        int m0, n_idx, kb0, nkb;
-        decode(u, m0, n_idx, kb0, nkb);
-        int kk = 0;
-        if (!waited) {
-          // Weights do not depend on the previous kernel: stream the first stages of B while it
-          // drains (PDL), then wait for it before loading the activations A.
-          const int pre = min(nkb, STAGES);
-          for (int i = 0; i < pre; ++i) {
-            expect(i);
-            load_b(smem_u32(sB + i * S::kB), fullL + 8 * i, kb0 + i, n_idx);
+      if constexpr (CL == 1) {
+        for (int u = blockIdx.x; u < units; u += gridDim.x) {
+          int m0, n_idx, kb0, nkb;
+          decode(u, m0, n_idx, kb0, nkb);
+          int kk = 0;
+          if (!waited) {
+            // Weights do not depend on the previous kernel: stream the first stages of B while it
+            // drains (PDL), then wait for it before loading the activations A.
+            const int pre = min(nkb, STAGES);
+            for (int i = 0; i < pre; ++i) {
+              mbar_expect_tx(full0 + 8 * i, S::kStage);
+              load_b(smem_u32(sB + i * S::kB), full0 + 8 * i, kb0 + i, n_idx);
+            }
+            griddep_wait();
+            if (trace) trace[blockIdx.x * 6 + 1] = globaltimer();
+            waited = true;
+            for (int i = 0; i < pre; ++i) tma_load_2d(smem_u32(sA + i * S::kA), &tmA, full0 + 8 * i, (kb0 + i) * 64, m0);
+            kk = pre;
+            it = pre;
           }
-          griddep_wait();
-          if (trace) trace[blockIdx.x * 6 + 1] = globaltimer();
-          waited = true;
-          for (int i = 0; i < pre; ++i) load_a(i, (kb0 + i) * 64, m0);
-          kk = pre;
-          it = pre;
+          for (; kk < nkb; ++kk, ++it) {
+            const int s = it % STAGES;
+            mbar_wait(empty0 + 8 * s, ((it / STAGES) & 1) ^ 1);
+            mbar_expect_tx(full0 + 8 * s, S::kStage);
+            const int kc = (kb0 + kk) * 64;
+            tma_load_2d(smem_u32(sA + s * S::kA), &tmA, full0 + 8 * s, kc, m0);
+            load_b(smem_u32(sB + s * S::kB), full0 + 8 * s, kb0 + kk, n_idx);
+          }
         }
-        for (; kk < nkb; ++kk, ++it) {
-          const int s = it % STAGES;
-          mbar_wait(empty0 + 8 * s, ((it / STAGES) & 1) ^ 1);
-          expect(s);
-          load_a(s, (kb0 + kk) * 64, m0);
-          load_b(smem_u32(sB + s * S::kB), fullL + 8 * s, kb0 + kk, n_idx);
+      } else {
+        // A pair's loads complete on the leader's full barrier, which alone expects both CTAs' bytes
+        const uint64_t apol = l2_policy_evict_normal();
+        const uint32_t fullL = mapa_shared(full0, 0);
+        for (int u = cid; u < units; u += ncl) {
+          int m0, n_idx, kb0, nkb;
+          decode(u, m0, n_idx, kb0, nkb);
+          int kk = 0;
+          if (!waited) {
+            const int pre = min(nkb, STAGES);
+            for (int i = 0; i < pre; ++i) {
+              if (rank == 0) mbar_expect_tx(full0 + 8 * i, S::kStage * CL);
+              load_b(smem_u32(sB + i * S::kB), fullL + 8 * i, kb0 + i, n_idx);
+            }
+            griddep_wait();
+            waited = true;
+            for (int i = 0; i < pre; ++i)
+              tma_load_2d_2sm(smem_u32(sA + i * S::kA), &tmA, fullL + 8 * i, (kb0 + i) * 64, m0, apol);
+            kk = pre;
+            it = pre;
+          }
+          for (; kk < nkb; ++kk, ++it) {
+            const int s = it % STAGES;
+            mbar_wait(empty0 + 8 * s, ((it / STAGES) & 1) ^ 1);
+            if (rank == 0) mbar_expect_tx(full0 + 8 * s, S::kStage * CL);
+            tma_load_2d_2sm(smem_u32(sA + s * S::kA), &tmA, fullL + 8 * s, (kb0 + kk) * 64, m0, apol);
+            load_b(smem_u32(sB + s * S::kB), fullL + 8 * s, kb0 + kk, n_idx);
+          }
         }
       }
       if (!waited) griddep_wait();
@@ -381,7 +664,12 @@ static cudaError_t launch_gemm_t(const CUtensorMap& A, const CUtensorMap& B, voi
                                  int pack, cudaStream_t st, const GemmNext& nx) {
   constexpr int ST = gemm_stages(BN, CL);
   using S = GemmSmem<BN, ST, CL>;
-  auto kern = gemm_bf16_kernel<BN, ST, EPI, CL>;
+  auto kern = [] {
+    if constexpr (CL == 1)
+      return gemm_bf16_kernel<BN, ST, EPI>;
+    else
+      return gemm_pair_kernel<BN, ST, EPI, CL>;
+  }();
   const int kblk = K / 64;
   const int per = (kblk + splits - 1) / splits;
   const int units = ((N + BN - 1) / BN) * ((M + 128 * CL - 1) / (128 * CL)) * splits;
@@ -416,8 +704,12 @@ static cudaError_t launch_gemm_t(const CUtensorMap& A, const CUtensorMap& B, voi
 template <int BN, int EPI, int CL = 1>
 static cudaError_t prep_t() {
   constexpr int ST = gemm_stages(BN, CL);
-  return cudaFuncSetAttribute(gemm_bf16_kernel<BN, ST, EPI, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              GemmSmem<BN, ST, CL>::kBytes);
+  if constexpr (CL == 2)
+    return cudaFuncSetAttribute(gemm_pair_kernel<BN, ST, EPI, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                GemmSmem<BN, ST, CL>::kBytes);
+  else
+    return cudaFuncSetAttribute(gemm_bf16_kernel<BN, ST, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                GemmSmem<BN, ST>::kBytes);
 }
 
 #define PIC_GEMM_BNS(X) X(64) X(128) X(144) X(160) X(176) X(192) X(208) X(224) X(256)

@@ -145,7 +145,8 @@ def lib() -> C.CDLL:
         L.pic_linked_export.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p]
         L.pic_linked_info.argtypes = [C.c_void_p, C.c_void_p, P(C.c_int32), P(C.c_int32)]
         L.pic_linked_sharing.argtypes = [C.c_void_p, C.c_void_p, P(C.c_int32), P(C.c_int32)]
-        L.pic_linked_materialize.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
+        if hasattr(L, "pic_linked_materialize") or "PIC_LIB_NAME" not in os.environ:  # older experiment builds lack it
+            L.pic_linked_materialize.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
         L.pic_linked_release.argtypes = [C.c_void_p, C.c_void_p]
         L.pic_cache_export.argtypes = [C.c_void_p, C.c_uint64, C.c_int32, C.c_void_p, C.c_void_p]
         L.pic_cache_info.argtypes = [C.c_void_p, C.c_uint64, P(C.c_int32), P(C.c_int32)]
@@ -164,7 +165,8 @@ def lib() -> C.CDLL:
         L.pic_test_gemm_swiglu.argtypes = [C.c_void_p, C.c_void_p] + [C.c_int32] * 4 + [C.c_void_p]
         L.pic_bench_attention.argtypes = [C.c_void_p] * 4 + [C.c_int32] * 4 + [C.c_void_p] + [C.c_int32] * 3 + [P(C.c_float)]
         for name in EXPORTS:
-            getattr(L, name)  # AttributeError if the library lacks a declared entry point
+            if "PIC_LIB_NAME" not in os.environ or hasattr(L, name):  # experiment builds may predate a call
+                getattr(L, name)  # AttributeError if the library lacks a declared entry point
         _lib = L
     return _lib
 
