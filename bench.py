@@ -314,16 +314,21 @@ def main():
         barrier()
         torch.cuda.synchronize(dev)
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]   # per-step boundaries
         with ClockSampler(dev) as clk:
             ev0.record(stream)
-            for _ in range(args.steps):
+            for i in range(args.steps):
                 outs = step()
+                evs[i].record(stream)
             ev1.record(stream)
             ev1.synchronize()
         torch.cuda.synchronize(dev)
         barrier()
         ms_max = D.max_over_ranks(ev0.elapsed_time(ev1), device=red_dev)
         ms_per_step = ms_max / args.steps
+        step_ms = sorted([ev0.elapsed_time(evs[0])] + [evs[i - 1].elapsed_time(evs[i]) for i in range(1, args.steps)])
+        ttft_dist = {"p50": float(np.percentile(step_ms, 50)), "p90": float(np.percentile(step_ms, 90)),
+                     "min": step_ms[0], "max": step_ms[-1], "how": "per-step CUDA events inside the timed region (rank 0)"}
         tokens_all = (sum(N_tok) if args.tp else D.sum_over_ranks(sum(N_tok), device=red_dev)) * args.steps
         value = tokens_all / (ms_max / 1e3)
 
@@ -411,6 +416,10 @@ def main():
     line = {"metric": "linked_prefill_tokens_per_s", "value": value, "unit": "tokens/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
             "ttft_ms_device": ms_per_step if len(reqs) == 1 else None,
+            "step_ms_distribution": ttft_dist,
+            "ttft_ms_requests": ({"mean": ms_per_step, "p99": float(np.percentile(step_ms, 99)),
+                                  "how": "SURVEY 8(d) cfg4: every request of a wave arrives at t=0, its TTFT is the "
+                                         "wave's completion (one wave per step)"} if len(reqs) > 1 else None),
             "higher_is_better": True, "scaling": "strong" if args.tp else "weak", "vs_baseline": None,
             "dtype": "bf16", "data": "synthetic",
             "config": dict(cfgd, parallelism=(f"tp{world} (heads/MLP sharded, fused peer-memory all-reduce)" if args.tp
