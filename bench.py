@@ -152,8 +152,18 @@ class OracleSample:
                                            f"+ LM head timed ({tl:.2f} s), extrapolated x{cfg.n_layers} layers")
 
 
-def oracle_sample(w):
-    return OracleSample(w).run()
+def oracle_sample(w, min_seconds: float = 10.0):
+    """cpu_baseline: the sampled oracle link repeated until >= min_seconds of CPU work,
+    reported as the mean over the repetitions."""
+    osamp = OracleSample(w)
+    vals, spent, sample = [], 0.0, ""
+    while spent < min_seconds or not vals:
+        t0 = time.perf_counter()
+        v, per_req, sample = osamp.run()
+        spent += time.perf_counter() - t0
+        vals.append(per_req)
+    per_req = float(np.mean(vals))
+    return osamp.N / per_req, per_req, f"{sample}; {len(vals)} repetitions, {spent:.1f} s of CPU work
 
 
 def cores_used():
