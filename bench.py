@@ -163,7 +163,7 @@ def oracle_sample(w, min_seconds: float = 10.0):
         spent += time.perf_counter() - t0
         vals.append(per_req)
     per_req = float(np.mean(vals))
-    return osamp.N / per_req, per_req, f"{sample}; {len(vals)} repetitions, {spent:.1f} s of CPU work
+    return osamp.N / per_req, per_req, f"{sample}; {len(vals)} repetitions, {spent:.1f} s of CPU work"
 
 
 def cores_used():
