@@ -113,6 +113,20 @@ static void attn_trace_print(int n_cta) {
       fprintf(stderr, "  attn per-tile %-9s min %6.3f med %6.3f max %6.3f us\n", an[k], v[0], v[v.size() / 2], v.back());
     }
   }
+  {
+    std::vector<double> a, b;  // softmax warp 64: Q global loads after the PDL wait, then the TMEM store
+    for (int c = 0; c < n_cta; ++c)
+      if (t[16 * c + 14] > t[16 * c + 1] && t[16 * c + 1] > 0) {
+        a.push_back((double)(t[16 * c + 14] - t[16 * c + 1]) / 1e3);
+        b.push_back((double)(t[16 * c + 15] - t[16 * c + 14]) / 1e3);
+      }
+    if (!a.empty()) {
+      std::sort(a.begin(), a.end());
+      std::sort(b.begin(), b.end());
+      fprintf(stderr, "  attn Q load   min %6.3f med %6.3f max %6.3f us; TMEM store min %6.3f med %6.3f max %6.3f us\n",
+              a[0], a[a.size() / 2], a.back(), b[0], b[b.size() / 2], b.back());
+    }
+  }
   for (int k = 0; k < 7; ++k) {
     std::vector<double> v;
     for (int c = 0; c < n_cta; ++c)

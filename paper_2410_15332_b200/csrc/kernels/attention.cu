@@ -352,8 +352,13 @@ __global__ void __launch_bounds__(ROT ? 320 + 32 * kRotWarps : 320, 1)
 #pragma unroll
         for (int i = 0; i < 32; ++i) qv[i] = 0u;
       }
+      if (tr && threadIdx.x == 64) {  // bench-only: Q rows arrived from global memory
+        asm volatile("" ::"r"(qv[0]), "r"(qv[31]));
+        tr[14] = globaltimer();
+      }
       tmem_st32u(tmem + lane_addr + kTmQ + hc * 32, qv);
       tmem_wait_st();
+      if (tr && threadIdx.x == 64) tr[15] = globaltimer();
       tc_fence_before();
       mbar_arrive(q_full);
     }
