@@ -39,7 +39,8 @@ constexpr int kTile = 16384;                  // one [128 rows][64 cols] bf16 SW
 constexpr int kStages = 3;                    // K and V ring depth
 constexpr int kK = 0;                         // K stages: kStages x 2 halves
 constexpr int kV = kK + kStages * 2 * kTile;  // V stages
-constexpr int kX = kV + kStages * 2 * kTile;  // softmax pair exchange: [2 parity][2 halves][128] fp32
+constexpr int kQ = kV + kStages * 2 * kTile;  // Q tile (2 halves), TMA-staged (A operand of S = Q·Kᵀ)
+constexpr int kX = kQ + 2 * kTile;            // softmax pair exchange: [2 parity][2 halves][128] fp32
 constexpr int kBar = kX + 2 * 2 * 128 * 4;    // barriers
 constexpr int kNumBars = 1 + 5 * kStages + 6;  // + k_rot ring (shared-block link)
 constexpr int kSmem = kBar + kNumBars * 8 + 16;
@@ -47,18 +48,18 @@ static_assert(kSmem <= 232448, "attention smem over the 227 KB limit");
 // TMEM columns (512 allocated)
 constexpr uint32_t kTmS = 0;    // S double buffer [0, 256); P(t) (bf16 pairs) overwrites S(t): half hc at +64·hc
 constexpr uint32_t kTmO = 256;  // O accumulator [256, 384)
-constexpr uint32_t kTmQ = 384;  // Q (bf16 pairs) [384, 448)
 }  // namespace attn
 
-// Both MMAs take their A operand from TMEM (Q for S = Q·Kᵀ, P for O += P·V), so shared memory only
-// carries K and V: per 128-key tile the smem traffic is the two TMA writes and the two B-operand reads.
+// Q is TMA-staged into shared memory once per CTA (the A operand of S = Q·Kᵀ); P is the TMEM A operand
+// of O += P·V.  (A TMEM-resident Q cost a 1.8 µs tcgen05.st + wait::st in every CTA's prologue.)
 // ROT: kRotWarps extra warps re-base shared-block K tiles (f3), one per SMSP.  Measured (cfg4 attention,
 // 32 layers): 4 warps 26.3 ms, 2 warps 41.5 ms (the rotation is issue-bound and sits between the K TMA
 // and the S MMA); 4 warps cap the CTA at 128 registers per thread (14 warps), a few bytes of spill.
 constexpr int kRotWarps = 4;
 template <int G, bool ROT>
 __global__ void __launch_bounds__(ROT ? 320 + 32 * kRotWarps : 320, 1)
-    attn_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
+    attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                   const __grid_constant__ CUtensorMap tmV,
                    const __grid_constant__ CUtensorMap tmK8, const __grid_constant__ CUtensorMap tmV8, const AttnArgs a) {
   griddep_launch();
   using namespace attn;
@@ -81,7 +82,7 @@ __global__ void __launch_bounds__(ROT ? 320 + 32 * kRotWarps : 320, 1)
   const int warp = warp_id(), lane = lane_id();
   // barriers and TMEM do not depend on upstream data: set them up while the previous kernel drains
   if (threadIdx.x == 0) {
-    mbar_init(q_full, 256);
+    mbar_init(q_full, 1);
     for (int s = 0; s < S; ++s) {
       mbar_init(k_full + 8 * s, 1);
       mbar_init(k_empty + 8 * s, 1);
@@ -137,6 +138,9 @@ __global__ void __launch_bounds__(ROT ? 320 + 32 * kRotWarps : 320, 1)
     // ------------------------------------------------------------------ TMA producer (K, V)
     if (n > 0) {
       if (lane == 0) {
+        // Q first: 128 MMA rows = (128/G queries) x (G heads of kv-head g), one 3-D box per 64-dim half
+        mbar_expect_tx(q_full, 2 * kTile);
+        for (int h = 0; h < 2; ++h) tma_load_3d(base + kQ + h * kTile, &tmQ, q_full, h * 64, g * G, row_start);
         tma_prefetch(&tmK);
         tma_prefetch(&tmV);
         tma_prefetch(&tmK8);
@@ -187,7 +191,7 @@ __global__ void __launch_bounds__(ROT ? 320 + 32 * kRotWarps : 320, 1)
   } else if (warp == 1) {
     // ------------------------------------------------------------------ MMA issuer
     if (lane == 0 && n > 0) {
-      constexpr uint32_t idS = idesc_bf16(128, 128, 0, 0);  // Q (TMEM, K-major) x K (smem, K-major)
+      constexpr uint32_t idS = idesc_bf16(128, 128, 0, 0);  // Q (smem, K-major) x K (smem, K-major)
       constexpr uint32_t idO = idesc_bf16(128, 128, 0, 1);  // P (TMEM, K-major) x V (smem, MN-major)
       unsigned long long w_k = 0, w_p = 0, w_v = 0, q0 = 0;
       mbar_wait(q_full, 0);
@@ -226,7 +230,8 @@ __global__ void __launch_bounds__(ROT ? 320 + 32 * kRotWarps : 320, 1)
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
           const uint32_t kb = base + kK + (2 * ks + (kk >> 2)) * kTile + (kk & 3) * 32;
-          umma_bf16_ts(tmem + kTmS + sb * 128, tmem + kTmQ + kk * 8, sdesc_sw128(kb, 16, 1024), idS, kk > 0);
+          const uint32_t qa = base + kQ + (kk >> 2) * kTile + (kk & 3) * 32;
+          umma_bf16(tmem + kTmS + sb * 128, sdesc_sw128(qa, 16, 1024), sdesc_sw128(kb, 16, 1024), idS, kk > 0);
         }
         umma_commit(s_full + 8 * sb);
         umma_commit(k_empty + 8 * ks);
@@ -334,34 +339,6 @@ __global__ void __launch_bounds__(ROT ? 320 + 32 * kRotWarps : 320, 1)
     const int pos = valid ? a.row_pos[row] : max_p;
     const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
     const uint32_t oAddr = tmem + lane_addr + kTmO + hc * 64;
-    // Q row -> TMEM: this thread's 64 dims as 32 bf16 pairs (the A operand of S = Q·Kᵀ)
-    {
-      uint32_t qv[32];
-      if (valid) {
-        const uint4* src = reinterpret_cast<const uint4*>(reinterpret_cast<const uint16_t*>(a.Q) +
-                                                          ((size_t)row * a.Hq + head) * 128 + hc * 64);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const uint4 x = src[i];
-          qv[4 * i] = x.x;
-          qv[4 * i + 1] = x.y;
-          qv[4 * i + 2] = x.z;
-          qv[4 * i + 3] = x.w;
-        }
-      } else {
-#pragma unroll
-        for (int i = 0; i < 32; ++i) qv[i] = 0u;
-      }
-      if (tr && threadIdx.x == 64) {  // bench-only: Q rows arrived from global memory
-        asm volatile("" ::"r"(qv[0]), "r"(qv[31]));
-        tr[14] = globaltimer();
-      }
-      tmem_st32u(tmem + lane_addr + kTmQ + hc * 32, qv);
-      tmem_wait_st();
-      if (tr && threadIdx.x == 64) tr[15] = globaltimer();
-      tc_fence_before();
-      mbar_arrive(q_full);
-    }
     float* xmax = reinterpret_cast<float*>(smem + kX);   // [2 parity][2 halves][128 rows]
     const float sc = a.scale_log2;
     // m_ref (log2 units): the max the current O / l are scaled to.  It is raised only when a row's
@@ -569,11 +546,10 @@ template <int G>
 static cudaError_t launch_attn_g(const CUtensorMap& tmQ, const CUtensorMap& tmK, const CUtensorMap& tmV,
                                  const CUtensorMap& tmK8, const CUtensorMap& tmV8, const AttnArgs& a, cudaStream_t st) {
   dim3 grid(a.n_work, a.Hkv);
-  (void)tmQ;  // Q rows are loaded into TMEM by the softmax warps (AttnArgs::Q)
   if (a.bdelta)
-    CUDA_TRY_LAUNCH(launch_k(attn_tc_kernel<G, true>, dim3(grid), dim3(320 + 32 * kRotWarps), attn::kSmem, st, tmK, tmV, tmK8, tmV8, a));
+    CUDA_TRY_LAUNCH(launch_k(attn_tc_kernel<G, true>, dim3(grid), dim3(320 + 32 * kRotWarps), attn::kSmem, st, tmQ, tmK, tmV, tmK8, tmV8, a));
   else
-    CUDA_TRY_LAUNCH(launch_k(attn_tc_kernel<G, false>, dim3(grid), dim3(320), attn::kSmem, st, tmK, tmV, tmK8, tmV8, a));
+    CUDA_TRY_LAUNCH(launch_k(attn_tc_kernel<G, false>, dim3(grid), dim3(320), attn::kSmem, st, tmQ, tmK, tmV, tmK8, tmV8, a));
   return cudaGetLastError();
 }
 
