@@ -1158,7 +1158,7 @@ static pic_status enqueue_forward(pic_engine* e, const Fwd& f, const DevPlan& dp
     } else {
       ++R.launches;
       PROF("qkv_rope_scatter", (double)M * qkv * 4 * s + (double)M * qkv * 2, 0, launch_qkv_rope_scatter(e->ws, s, M, nullptr, pos, slot, e->cos_t, e->sin_t, e->Q, Kl, Vl, M, Hq, Hkv, D,
-                                 st, e->f32));
+                                 st, e->f32, pos == dp.pos ? 1 : 0));
     }
     if (f.compile && l == L - 1) break;  // compile needs only the last layer's K/V
     if (k2_side && l == f.k2_layer0 + 1) CK(cudaStreamWaitEvent(st, e->k2_join, 0));  // side-stream K2 landed

@@ -64,7 +64,7 @@ cudaError_t launch_residual_rmsnorm(float* h, const float* P, int splits, const 
 cudaError_t launch_qkv_rope_scatter(const float* P, int splits, int P_rows, const int32_t* src_row,
                                     const int32_t* pos, const int32_t* slot, const float* cos_t, const float* sin_t,
                                     void* Q, void* Kpool_l, void* Vpool_l, int M, int Hq, int Hkv, int D,
-                                    cudaStream_t st, int f32 = 0);
+                                    cudaStream_t st, int f32 = 0, int static_plan = 0);  // 1: pos/slot host-uploaded
 
 // ---- a8 epilogue: u = bf16(silu(Σ gate) ⊙ Σ up) ----------------------------------------------
 cudaError_t launch_swiglu(const float* P, int splits, void* u, int M, int F, cudaStream_t st, int f32 = 0);

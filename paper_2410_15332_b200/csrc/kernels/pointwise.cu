@@ -215,11 +215,24 @@ __global__ void __launch_bounds__(1024) residual_rmsnorm_kernel(float* __restric
                                                                  void* __restrict__ x,
                                                                  const int32_t* __restrict__ out_map, int M, int d,
                                                                  float eps) {
-  PIC_PDL_ENTRY();
+  griddep_launch();
   __shared__ float red[32];
   constexpr int VPT = 8;  // float4 per thread kept in registers between the two passes
   const int r = blockIdx.x;
   const int n4 = d / 4;
+  // weights and the host-built row map do not depend on the upstream kernel: fetch them first
+  const float4* g4 = reinterpret_cast<const float4*>(g);
+  float4 gv[VPT];
+  const int orow = (x && out_map) ? out_map[r] : r;
+  if (x) {
+#pragma unroll
+    for (int k = 0; k < VPT; ++k) {
+      const int i = threadIdx.x + k * blockDim.x;
+      if (i >= n4) break;
+      gv[k] = g4[i];
+    }
+  }
+  griddep_wait();
   float4* hr = reinterpret_cast<float4*>(h + (size_t)r * d);
   float4 vc[VPT];
   float ss = 0.f;
@@ -240,16 +253,14 @@ __global__ void __launch_bounds__(1024) residual_rmsnorm_kernel(float* __restric
     vc[k] = v;
   }
   if (!x) return;
-  const int orow = out_map ? out_map[r] : r;
   ss = block_sum_dyn(ss, red);
   if (orow < 0) return;
   const float inv = rsqrtf(ss / d + eps);
-  const float4* g4 = reinterpret_cast<const float4*>(g);
 #pragma unroll
   for (int k = 0; k < VPT; ++k) {
     const int i = threadIdx.x + k * blockDim.x;
     if (i >= n4) break;
-    const float4 v = vc[k], w = g4[i];
+    const float4 v = vc[k], w = gv[k];
     store4<F32>(x, (size_t)orow * d + 4 * i, v.x * inv * w.x, v.y * inv * w.y, v.z * inv * w.z, v.w * inv * w.w);
   }
 }
@@ -343,27 +354,42 @@ __global__ void __launch_bounds__(128) qkv_rope_scatter_kernel(
     const float* __restrict__ P, int splits, int P_rows, const int32_t* __restrict__ src_row,
     const int32_t* __restrict__ pos, const int32_t* __restrict__ slot, const float* __restrict__ cos_t,
     const float* __restrict__ sin_t, void* __restrict__ Q, void* __restrict__ Kp, void* __restrict__ Vp, int Hq,
-    int Hkv, int D) {
-  PIC_PDL_ENTRY();
+    int Hkv, int D, int static_plan) {
+  griddep_launch();
   const int r = blockIdx.x;
   const int t = blockIdx.y * blockDim.x + threadIdx.x;
   const int half = D / 2, q8 = D / 8;
   const int n_rope = (Hq + Hkv) * q8, n_v = Hkv * (D / 4);
-  if (t >= n_rope + n_v) return;
+  if (t >= n_rope + n_v) {
+    griddep_wait();
+    return;
+  }
+  // host-uploaded positions / slots (and the RoPE angles they select) are complete before the graph
+  // starts: fetch them while the upstream GEMM drains; CacheBlend's re-selected rows are device-side
+  int p = 0, sl = 0;
+  float4 c = make_float4(0.f, 0.f, 0.f, 0.f), s = c;
+  const int j = (t % q8) * 4;
+  auto fetch_plan = [&]() {
+    sl = slot[r];
+    if (t < n_rope) {
+      p = pos[r];
+      c = *reinterpret_cast<const float4*>(cos_t + (size_t)p * half + j);
+      s = *reinterpret_cast<const float4*>(sin_t + (size_t)p * half + j);
+    }
+  };
+  if (static_plan) fetch_plan();
+  griddep_wait();
+  if (!static_plan) fetch_plan();
   const int srow = src_row ? src_row[r] : r;
   const int ncol4 = (Hq + 2 * Hkv) * D / 4;
   const size_t stride4 = (size_t)P_rows * ncol4;
   const float4* P4 = reinterpret_cast<const float4*>(P) + (size_t)srow * ncol4;
-  const int sl = slot[r];
   const size_t kv_base = ((size_t)(sl / 16) * Hkv) * 16 * D + (size_t)(sl % 16) * D;  // + g*16*D + d
   if (t < n_rope) {
-    const int hd = t / q8, j = (t % q8) * 4;
+    const int hd = t / q8;
     const int col4 = (hd * D + j) / 4;
     const float4 a = sum_splits4(P4, splits, stride4, col4);
     const float4 b = sum_splits4(P4, splits, stride4, col4 + half / 4);
-    const int p = pos[r];
-    const float4 c = *reinterpret_cast<const float4*>(cos_t + (size_t)p * half + j);
-    const float4 s = *reinterpret_cast<const float4*>(sin_t + (size_t)p * half + j);
     void* dst = hd < Hq ? Q : Kp;
     const size_t o = hd < Hq ? ((size_t)r * Hq + hd) * D : kv_base + (size_t)(hd - Hq) * 16 * D;
     store4<F32>(dst, o + j, a.x * c.x - b.x * s.x, a.y * c.y - b.y * s.y, a.z * c.z - b.z * s.z, a.w * c.w - b.w * s.w);
@@ -380,16 +406,16 @@ __global__ void __launch_bounds__(128) qkv_rope_scatter_kernel(
 cudaError_t launch_qkv_rope_scatter(const float* P, int splits, int P_rows, const int32_t* src_row, const int32_t* pos,
                                     const int32_t* slot, const float* cos_t, const float* sin_t, void* Q,
                                     void* Kpool_l, void* Vpool_l, int M, int Hq, int Hkv, int D, cudaStream_t st,
-                                    int f32) {
+                                    int f32, int static_plan) {
   if (M == 0) return cudaSuccess;
   const int threads = (Hq + Hkv) * (D / 8) + Hkv * (D / 4);
   dim3 grid(M, (threads + 127) / 128);
   if (f32)
     CUDA_TRY_LAUNCH(launch_k(qkv_rope_scatter_kernel<true>, dim3(grid), dim3(128), 0, st, P, splits, P_rows, src_row,
-                             pos, slot, cos_t, sin_t, Q, Kpool_l, Vpool_l, Hq, Hkv, D));
+                             pos, slot, cos_t, sin_t, Q, Kpool_l, Vpool_l, Hq, Hkv, D, static_plan));
   else
     CUDA_TRY_LAUNCH(launch_k(qkv_rope_scatter_kernel<false>, dim3(grid), dim3(128), 0, st, P, splits, P_rows, src_row,
-                             pos, slot, cos_t, sin_t, Q, Kpool_l, Vpool_l, Hq, Hkv, D));
+                             pos, slot, cos_t, sin_t, Q, Kpool_l, Vpool_l, Hq, Hkv, D, static_plan));
   return cudaGetLastError();
 }
 
