@@ -585,11 +585,13 @@ cudaError_t launch_attention_tc(const CUtensorMap& tmQ, const CUtensorMap& tmK, 
 __global__ void attn_combine_kernel(const float* __restrict__ o_part, const float* __restrict__ ml_part,
                                     const int32_t* __restrict__ row_nsplit, __nv_bfloat16* __restrict__ O, int M,
                                     int Hq) {
-  PIC_PDL_ENTRY();
+  griddep_launch();
   const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
+  // the split counts are host-built plan data: read them while the attention kernel drains
+  const int n_splits = wid < M * Hq ? row_nsplit[wid / Hq] : 0;
+  griddep_wait();
   if (wid >= M * Hq) return;
-  const int n_splits = row_nsplit[wid / Hq];
   const size_t stride = (size_t)M * Hq;
   float ms = -INFINITY, ls = 0.f;
   if (lane < n_splits) {
