@@ -218,3 +218,35 @@ def test_materialize_bit_identical_and_accounting(setup):
     finally:
         s.eng.release(hc)
         s.eng.release(hs)
+
+
+def test_shared_batch_same_chunks_refcounts(setup):
+    """A batched shared-block link whose requests reuse the same chunks (the cfg4 pattern): every request
+    is bit-identical to its own copy-path link, the store blocks carry one reference per request, and
+    releasing everything restores the pool exactly."""
+    s = setup
+    reqs = [s.w.requests[0]] + sg.permuted_requests(s.w, 2)
+    free0 = s.eng.stats()["free_blocks"]
+    outs = s.eng.link_batch([s.segs(r) for r in reqs], "legolink:4", keep_linked=True, kv_share=True)
+    try:
+        for r, o in zip(reqs, outs):
+            ref = s.eng.link(s.segs(r), "legolink:4", keep_linked=True, kv_share=False)
+            try:
+                assert np.array_equal(o.logits, ref.logits)
+                for l in range(s.cfg.n_layers):
+                    ka, va = s.eng.linked_export(o.linked, l)
+                    kb, vb = s.eng.linked_export(ref.linked, l)
+                    assert np.array_equal(ka, kb) and np.array_equal(va, vb), l
+            finally:
+                s.eng.release(ref.linked)
+        # the requests' block tables point at the chunk-store blocks themselves
+        shared_ids = set()
+        for o in outs:
+            n, bd = s.eng.linked_sharing(o.linked)
+            bt = s.eng.linked_blocks(o.linked)
+            shared_ids |= {int(b) for b in bt[:len(bd)]} & {int(b) for c in s.eids for b in s.eng.cache_blocks(c)}
+        assert shared_ids
+    finally:
+        for o in outs:
+            s.eng.release(o.linked)
+    assert s.eng.stats()["free_blocks"] == free0
