@@ -250,3 +250,17 @@ def test_shared_batch_same_chunks_refcounts(setup):
         for o in outs:
             s.eng.release(o.linked)
     assert s.eng.stats()["free_blocks"] == free0
+
+
+def test_shared_link_without_rebase_bit_identical(setup):
+    """SPEC's no-re-base reading (rebase = 0, reading R1): shared blocks then carry Δ = 0 and the result
+    equals the copy path's (cached keys left at their compile positions) bit for bit."""
+    s = setup
+    for segs in [s.w.requests[0]] + sg.permuted_requests(s.w, 2):
+        copy, shared = link_both(s, segs, "legolink:4", rebase=False)
+        try:
+            assert_identical(copy, shared)
+            assert not shared[4].any()          # nothing to rotate
+        finally:
+            s.eng.release(copy[0].linked)
+            s.eng.release(shared[0].linked)
