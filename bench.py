@@ -1,22 +1,34 @@
 #!/usr/bin/env python
-"""Linked-prefill benchmark (BASELINE.json metric: linked-prefill TTFT and linked tokens/s,
-with % of HBM / tensor roofline).
+"""Linked-prefill benchmark (BASELINE.json metric: linked-prefill TTFT and linked tokens/s at
+1/2/4/8 B200, with % of HBM / tensor roofline).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg2|cfg3|cfg4] [--alg ALG]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg4|cfg2|cfg3|cfg5] [--alg ALG]
                     [--impl ours|reference]
 
-A step = one linked prefill (pic_link, all rows of SURVEY §8(a)) of the workload's request(s)
-on synthetic random-init weights of the named shape.  Multi-GPU (torchrun): one process per
-GPU, each links its own independent requests (data parallel by request, no collective on the
-path; "scaling": "weak"); timing is the max over ranks of CUDA-event time.
+Default workload = cfg4, the configuration the metric is quoted on at 1/2/4/8 GPUs (SURVEY §8(d),
+BASELINE.json configs[3]; PAPER.md:254 512-token chunks, :258 multi-user RAG load, :301 LegoLink-16):
+a fixed batch of 256 independent RAG requests, each 10 distinct 512-token chunks drawn from a
+256-chunk corpus + a 64-token query (N = 5184), Llama-3.1-8B-shaped random-init bf16, LegoLink-16.
+Request r runs on rank r mod N (no collective on the data path); each rank links its 256/N requests
+in waves of 32 (one pic_link_batch per wave).  A step = the whole 256-request batch; its time is
+the makespan = the max over ranks of the CUDA-event time of the rank's waves.  Every request
+arrives at t = 0 of the step, so a request's TTFT is the completion time of its wave; the mean and
+p99 over all 256 requests are reported.  Total work is fixed as N grows: "scaling": "strong".
 
---impl reference times the fp64 CPU oracle (oracle/) on a bounded sample of the same workload
-(there is no reference implementation to install: the paper ships no code)."""
+--gpus N without a torchrun environment re-launches itself under torch.distributed.run with N
+ranks (one per GPU; several ranks share a GPU only when fewer are visible — a functional dry run,
+marked in `config.shared_gpu`).  cfg5 (Llama-3-70B shape) at N > 1 runs tensor-parallel over the
+ranks (heads / MLP columns sharded, fused peer-memory all-reduce).
+
+--impl reference times the fp64 CPU oracle (oracle/; the paper ships no code to install) on a
+bounded sample of the same workload: each step is the oracle's link of one sampled request at one
+layer of full width plus the LM head; `value` extrapolates that to the full depth (labelled)."""
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import subprocess
 import sys
 import threading
@@ -31,6 +43,9 @@ import seedgen as sg  # noqa: E402
 
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
 FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+METRIC = "linked_prefill_tokens_per_s"
+CFG4_REQUESTS = 256      # BASELINE.json configs[3]: "batch of 256 independent RAG requests"
+WAVE = 32                # requests per pic_link_batch (waves of 32, 21.7 GB linked KV)
 
 
 def peaks():
@@ -42,31 +57,42 @@ def peaks():
         return FALLBACK, "fallback"
 
 
-def workload(name: str, alg: str | None, world: int = 1, per_gpu: int = 32):
+def workload(name: str, alg: str | None, n_requests: int = CFG4_REQUESTS):
     if name == "cfg2":
-        w = sg.cfg2(alg or "legolink:16")
-    elif name == "cfg3":
-        w = sg.cfg3(alg or "legolink:32")
-    elif name == "cfg5":
-        w = sg.cfg5(alg or "legolink:16")             # 70B shape, 32K context: fits one B200 (141 GB bf16)
-    elif name == "cfg4":
-        # weak scaling: `per_gpu` independent requests per GPU, request r -> rank r mod world
-        w = sg.cfg4(n_requests=per_gpu * world, alg=alg or "legolink:16")
-    else:
-        raise SystemExit(f"unknown config {name}")
-    return w
+        return sg.cfg2(alg or "legolink:16")
+    if name == "cfg3":
+        return sg.cfg3(alg or "legolink:32")
+    if name == "cfg5":
+        return sg.cfg5(alg or "legolink:16")             # 70B shape, 32K context
+    if name == "cfg4":
+        return sg.cfg4(n_requests=n_requests, alg=alg or "legolink:16")
+    raise SystemExit(f"unknown config {name}")
 
 
-def describe(w) -> dict:
+def n_tokens(w, req) -> int:
+    return sum(len(w.chunks[s.chunk]) if s.cached else len(s.tokens) for s in req)
+
+
+def describe(w, world: int, tp: bool, wave: int, kv_share: bool, layers) -> dict:
+    """The bench's `config` — identical for both arms (`--impl ours|reference`)."""
     m = w.model
-    n_chunks = len(w.requests[0]) - (0 if w.requests[0][-1].cached else 1)
-    q = 0 if w.requests[0][-1].cached else len(w.requests[0][-1].tokens)
-    return {"workload": f"{w.name}: {m.name}-shaped random-init bf16, {n_chunks} chunks x {len(w.chunks[0])} tokens"
-                        f" + {q}-token query, {w.alg}, {len(w.requests)} request(s) per GPU",
-            "model": m.name, "n_layers": m.n_layers, "d_model": m.d_model, "vocab": m.vocab,
-            "chunk_len": len(w.chunks[0]), "n_chunks": n_chunks, "query_len": q, "alg": w.alg,
-            "requests_per_gpu_step": len(w.requests),
-            "l2": "inputs larger than L2 (weights 14+ GB re-read every step), no flush"}
+    r0 = w.requests[0]
+    n_chunks = sum(1 for s in r0 if s.cached)
+    q = sum(len(s.tokens) for s in r0 if not s.cached)
+    nreq = len(w.requests)
+    per_rank = -(-nreq // world) if not tp else nreq
+    d = {"workload": f"{w.name}: {nreq} request(s) x ({n_chunks} chunks x {len(w.chunks[0])} tokens + {q}-token "
+                     f"query), {m.name}-shaped random-init bf16, {w.alg}",
+         "model": m.name, "n_layers": m.n_layers, "d_model": m.d_model, "vocab": m.vocab,
+         "chunk_len": len(w.chunks[0]), "n_chunks": n_chunks, "query_len": q, "alg": w.alg,
+         "tokens_per_request": n_tokens(w, r0), "requests_total": nreq, "requests_per_gpu": per_rank,
+         "wave": min(wave, per_rank) if not tp else 1, "kv_share": bool(kv_share),
+         "parallelism": (f"tp{world} (heads/MLP sharded, fused peer-memory all-reduce)" if tp
+                         else f"dp{world} (request r -> rank r mod {world}, no collective)"),
+         "l2": "inputs larger than L2 (weights 15 GB re-read every wave), no flush"}
+    if layers:
+        d["truncated_layers"] = layers
+    return d
 
 
 # ------------------------------------------------------------------------------------- clocks
@@ -120,9 +146,11 @@ def dummy_prefix(alg):
 
 # ------------------------------------------------------------------------------------- CPU oracle
 class OracleSample:
-    """The fp64 oracle's link on a bounded sample: layer 0 of one request (all its work: re-base of
-    every cached row of that layer, the layer on the k' rows) plus the LM head, extrapolated to all
-    L layers.  Weights are generated once (not timed); each run() is one timed sample."""
+    """The fp64 oracle's link of one sampled request (request 0 of the workload) at ONE layer of full
+    width plus the LM head — a bounded sample of the link; all L layers cost the same, so the full-depth
+    time of the request is estimated as L·(t_sample − t_head) + t_head (labelled as an estimate).
+    Weights of that layer and the LM head are generated once (not timed); the chunks' compiled K/V are
+    supplied (compile is the untimed prerequisite a0; values do not change the link's work)."""
 
     def __init__(self, w):
         from oracle import model as M
@@ -133,13 +161,17 @@ class OracleSample:
         self.Wt.layer(0)
         self.Wt.lm_head
         self.store = P.Store(self.Wt)
-        over = [(np.zeros((1, len(c), cfg.n_kv_heads, cfg.head_dim)), np.zeros((1, len(c), cfg.n_kv_heads, cfg.head_dim)))
-                for c in w.chunks]
-        oids = self.store.compile(w.chunks, compiled_override=over, dummy_prefix=dummy_prefix(w.alg))
-        self.segs = [("cached", oids[s.chunk]) if s.cached else ("tokens", s.tokens) for s in w.requests[0]]
-        self.N = sum(len(w.chunks[s.chunk]) if s.cached else len(s.tokens) for s in w.requests[0])
+        req = w.requests[0]
+        used = sorted({s.chunk for s in req if s.cached})
+        over = [(np.zeros((1, len(w.chunks[c]), cfg.n_kv_heads, cfg.head_dim)),
+                 np.zeros((1, len(w.chunks[c]), cfg.n_kv_heads, cfg.head_dim))) for c in used]
+        oids = dict(zip(used, self.store.compile([w.chunks[c] for c in used], compiled_override=over,
+                                                 dummy_prefix=dummy_prefix(w.alg))))
+        self.segs = [("cached", oids[s.chunk]) if s.cached else ("tokens", s.tokens) for s in req]
+        self.N = n_tokens(w, req)
 
     def run(self):
+        """-> (sample seconds, estimated full-depth seconds of the request)."""
         cfg = self.w.model
         t0 = time.perf_counter()
         r = self.P.link(self.store, self.segs, self.w.alg, layers=1)
@@ -147,23 +179,24 @@ class OracleSample:
         t0 = time.perf_counter()
         self.M.logits_of(self.Wt, r.hidden[-1][-1])
         th = time.perf_counter() - t0
-        per_req = cfg.n_layers * (tl - th) + th
-        return self.N / per_req, per_req, (f"oracle fp64 link of 1 request (N={self.N}): layer 0 of {cfg.n_layers} "
-                                           f"+ LM head timed ({tl:.2f} s), extrapolated x{cfg.n_layers} layers")
+        return tl, cfg.n_layers * (tl - th) + th
+
+    def describe(self, n_runs, spent):
+        return (f"oracle fp64 link of request 0 (N={self.N}, {self.w.alg}) at 1 of {self.w.model.n_layers} layers "
+                f"(full width) + LM head per sample; full-depth request time ESTIMATED as L x layer + head; "
+                f"{n_runs} samples, {spent:.1f} s of CPU work")
 
 
 def oracle_sample(w, min_seconds: float = 10.0):
-    """cpu_baseline: the sampled oracle link repeated until >= min_seconds of CPU work,
-    reported as the mean over the repetitions."""
+    """cpu_baseline: the sampled oracle link repeated until >= min_seconds of CPU work."""
     osamp = OracleSample(w)
-    vals, spent, sample = [], 0.0, ""
-    while spent < min_seconds or not vals:
-        t0 = time.perf_counter()
-        v, per_req, sample = osamp.run()
-        spent += time.perf_counter() - t0
-        vals.append(per_req)
-    per_req = float(np.mean(vals))
-    return osamp.N / per_req, per_req, f"{sample}; {len(vals)} repetitions, {spent:.1f} s of CPU work"
+    ests, spent = [], 0.0
+    while spent < min_seconds or not ests:
+        tl, est = osamp.run()
+        spent += tl
+        ests.append(est)
+    per_req = float(np.mean(ests))
+    return osamp.N / per_req, osamp.describe(len(ests), spent)
 
 
 def cores_used():
@@ -173,24 +206,27 @@ def cores_used():
         return os.cpu_count()
 
 
-# ------------------------------------------------------------------------------------- main
-def ncu_traffic(kernel_class):
+# ------------------------------------------------------------------------------------- roofline
+def ncu_traffic(config_name, kernel_class):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch of this kernel class from the committed
-    ncu --set full capture (profiles/ncu_r1_traffic.json), or None."""
-    path = os.path.join(ROOT, "profiles", "ncu_r1_traffic.json")
+    `ncu --set full` capture of this configuration (profiles/ncu_traffic.json), or None."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(path) as f:
-            return json.load(f).get(kernel_class, {}).get("dram_bytes_per_launch")
+            return json.load(f).get(config_name, {}).get(kernel_class, {}).get("dram_bytes_per_launch")
     except (OSError, ValueError):
         return None
 
 
-def roofline(prof, P, src, nsteps):
-    """Dominant kernel class of the profiled steps against its roofline."""
+def roofline(prof, P, src, nsteps, config_name):
+    """Dominant kernel class of the profiled steps against its roofline.  Algorithmic
+    counts per launch come from the engine (GEMM: weight bytes, 2MNK FLOPs; attention: K/V read once,
+    4·H_q·D·Σ(p_i+1) FLOPs), durations from CUDA events around every launch on the launching stream."""
     tot = sum(v["ms"] for v in prof.values())
     dom_name, dom = max(prof.items(), key=lambda kv: kv[1]["ms"])
     intensity = dom["flops"] / max(dom["bytes"], 1)
     ridge = P["bf16_tflops"] * 1e12 / (P["hbm_gbs"] * 1e9)
+    n_launch = max(1, dom["launches"])
     if intensity < ridge:
         achieved = dom["bytes"] / (dom["ms"] / 1e3) / 1e9
         roof = {"bound": "hbm", "achieved": achieved, "peak": P["hbm_gbs"], "unit": "GB/s"}
@@ -203,175 +239,247 @@ def roofline(prof, P, src, nsteps):
         # kernel timed inside a long step; "peak" stays the burst figure (the conservative denominator)
         roof["peak_sustained"] = P["bf16_tflops_sustained"]
         roof["frac_sustained"] = roof["achieved"] / P["bf16_tflops_sustained"]
-    roof["traffic"] = ncu_traffic(dom_name)
+    traffic = ncu_traffic(config_name, dom_name)
+    roof["traffic"] = traffic
+    roof["algorithmic_bytes_per_launch"] = dom["bytes"] / n_launch
+    if traffic:
+        roof["traffic_over_algorithmic"] = traffic / (dom["bytes"] / n_launch)
     roof["kernel"] = dom_name
     roof["share_of_step"] = dom["ms"] / tot
     roof["peak_source"] = f"{src} (MEASURED_PEAKS.json burst)" if src == "measured" else "fallback (B200_PROFILING.md)"
     roof["launches_per_step"] = dom["launches"] / nsteps
     roof["how"] = (f"algorithmic bytes/FLOPs per launch (SURVEY §8(d)) over CUDA-event durations of every launch, "
-                   f"{nsteps} profiled steps on the bench stream (graphs off)")
+                   f"{nsteps} profiled step(s) on the bench stream (graphs off)")
     breakdown = {k: {"ms_per_step": v["ms"] / nsteps, "launches_per_step": v["launches"] / nsteps,
                      "GB/s": v["bytes"] / max(v["ms"], 1e-9) / 1e6, "TFLOP/s": v["flops"] / max(v["ms"], 1e-9) / 1e9}
                  for k, v in sorted(prof.items(), key=lambda kv: -kv[1]["ms"])}
     return roof, breakdown
 
 
+# ------------------------------------------------------------------------------------- launch
+def _free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def respawn_under_torchrun(n: int) -> int:
+    """`--gpus N` outside torchrun: one rank per GPU under torch.distributed.run (the driver's own launch
+    for N > 1).  Returns the launcher's exit code; only rank 0 prints the JSON line."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, env=dict(os.environ, PIC_BENCH_SPAWNED="1"))
+
+
+def reference_arm(args, w, cfgd, rank):
+    """--impl reference: the fp64 oracle as it stands, on the host cores, rank 0 only."""
+    if rank != 0:
+        return
+    osamp = OracleSample(w)
+    samples, ests = [], []
+    t_region = time.perf_counter()
+    for i in range(args.warmup + args.steps):
+        if i == args.warmup:
+            t_region = time.perf_counter()
+        tl, est = osamp.run()
+        if i >= args.warmup:
+            samples.append(tl)
+            ests.append(est)
+    region_s = time.perf_counter() - t_region
+    est = float(np.median(ests))
+    v = osamp.N / est
+    sample = osamp.describe(len(samples), sum(samples))
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "tokens/s",
+            "n_gpus": 0, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": region_s / args.steps * 1e3,
+            "ms_per_request_full_depth_estimate": est * 1e3,
+            "higher_is_better": True, "scaling": cfgd_scaling(cfgd), "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": cfgd,
+            "cpu_baseline": {"kind": "oracle", "value": v, "unit": "tokens/s", "cores": cores_used(),
+                             "sample": sample},
+            "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "note": "a step = one bounded oracle sample (1 layer of request 0 + LM head), ms_per_step is its "
+                    "measured time; value = request tokens / estimated full-depth oracle time"}
+    print(json.dumps(line), flush=True)
+
+
+def cfgd_scaling(cfgd) -> str:
+    # a fixed batch (cfg4: 256 requests) or one request split by TP: total work fixed as N grows
+    return "strong"
+
+
+# ------------------------------------------------------------------------------------- main
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="cfg2", choices=["cfg2", "cfg3", "cfg4", "cfg5"])
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="cfg4", choices=["cfg2", "cfg3", "cfg4", "cfg5"])
     ap.add_argument("--alg", default=None)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--requests", type=int, default=CFG4_REQUESTS, help="cfg4 batch size (default 256)")
+    ap.add_argument("--wave", type=int, default=WAVE, help="requests per pic_link_batch (cfg4)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--profile-steps", type=int, default=3)
+    ap.add_argument("--profile-steps", type=int, default=1)
     ap.add_argument("--tp", action="store_true",
-                    help="tensor parallel over all ranks (heads/MLP columns sharded, fused peer-memory all-reduce); "
-                         "strong scaling of one request instead of data parallel requests")
+                    help="tensor parallel over all ranks (default for cfg5 at N > 1): heads/MLP columns sharded, "
+                         "fused peer-memory all-reduce; one request split over the ranks")
     ap.add_argument("--layers", type=int, default=None, help="truncate depth (functional runs only; marked in config)")
     ap.add_argument("--kv-share", type=int, default=1, choices=[0, 1],
                     help="f3 shared-block link: chunk-store blocks linked by reference, keys re-based in the "
                          "attention K-tile load (pic_link_params.kv_share)")
-    ap.add_argument("--decode-steps", type=int, default=32,
-                    help="f1: decode steps over the linked caches after the link measurement (0 = skip)")
+    ap.add_argument("--decode-steps", type=int, default=16,
+                    help="f1: decode steps over the first wave's linked caches after the link measurement (0 = skip)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(respawn_under_torchrun(args.gpus))
+
     from paper_2410_15332_b200 import dist as D
     rank, world, local = D.env_rank()
-    w = workload(args.config, args.alg, 1 if args.tp else world)
+    tp = args.tp or (args.config == "cfg5" and world > 1)
+    w = workload(args.config, args.alg, args.requests)
     if args.layers:
         w.model = sg.truncated(w.model, args.layers)
-    if not args.tp:
-        if len(w.requests) == 1:
-            w.requests = w.requests * world            # single-request configs: one copy per GPU
-        w.requests = D.shard(w.requests, rank, world)   # data parallel by independent request
-    cfgd = describe(w)
-    cfgd["kv_share"] = bool(args.kv_share)
-    N_tok = [sum(len(w.chunks[s.chunk]) if s.cached else len(s.tokens) for s in r) for r in w.requests]
+    cfgd = describe(w, world, tp, args.wave, args.kv_share, args.layers)
 
     if args.impl == "reference":
-        if rank != 0:
-            return
-        vals = []
-        osamp = OracleSample(w)
-        for i in range(args.warmup + args.steps):
-            v, per_req, sample = osamp.run()
-            if i >= args.warmup:
-                vals.append((v, per_req))
-        v = float(np.median([x[0] for x in vals]))
-        ms = float(np.median([x[1] for x in vals])) * 1e3 * len(w.requests)
-        line = {"impl": "reference", "metric": "linked_prefill_tokens_per_s", "value": v, "unit": "tokens/s",
-                "n_gpus": 0, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-                "data": "synthetic", "config": cfgd,
-                "cpu_baseline": {"kind": "oracle", "value": v, "unit": "tokens/s", "cores": cores_used(),
-                                 "sample": sample},
-                "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-        print(json.dumps(line))
+        reference_arm(args, w, cfgd, rank)
         return
 
     import torch
     from paper_2410_15332_b200 import pic as B
 
-    dev = local % max(1, torch.cuda.device_count())
+    n_dev = max(1, torch.cuda.device_count())
+    dev = local % n_dev
     torch.cuda.set_device(dev)
+    shared_gpu = world > n_dev
+    cfgd["shared_gpu"] = shared_gpu
+    if shared_gpu:
+        cfgd["note"] = f"{world} ranks on {n_dev} visible GPU(s): functional dry run, times are not per-GPU numbers"
     red_dev = f"cuda:{dev}"
     if world > 1:
-        if args.tp:
-            D.init("gloo")        # TP data moves through peer memory; the group only exchanges handles/timings
+        if tp or shared_gpu:
+            D.init("gloo")        # TP data moves through peer memory; NCCL refuses two ranks on one GPU
             red_dev = None
         else:
             D.init("nccl", device_id=torch.device(f"cuda:{dev}"))
+
+    mine = list(range(len(w.requests))) if tp else D.shard(list(range(len(w.requests))), rank, world)
+    my_reqs = [w.requests[i] for i in mine]
+    waves = [my_reqs[i:i + args.wave] for i in range(0, len(my_reqs), args.wave)] if my_reqs else []
+    N_tok = [n_tokens(w, r) for r in my_reqs]
     stream = torch.cuda.Stream(dev)
     m = w.model
     total_tokens = sum(len(c) for c in w.chunks)
-    max_N = max(N_tok)
-    # rows recomputed per forward: Σ k' of the batch (host-only planner), N for CacheBlend
+    max_N = max(N_tok) if N_tok else 512
+    wave_max = max((len(x) for x in waves), default=1)
+    # rows recomputed per forward: Σ k' of the largest wave (host-only planner), N for CacheBlend
     planner = B.Engine(m, num_blocks=(total_tokens + max_N) // 16 + 2 * len(w.chunks) + 64, max_rows=64,
                        max_tokens=max(max_N, 512) + 16, max_requests=1, device=None)
     pids = planner.generate_context_cache(w.chunks, dummy_prefix=dummy_prefix(w.alg))
-    rows_link = sum(N_tok) if w.alg.startswith("cacheblend") else sum(
-        len(planner.plan([("cached", pids[s.chunk]) if s.cached else ("tokens", s.tokens) for s in r], w.alg)["sel"])
-        for r in w.requests)
+
+    def rows_of(r):
+        if w.alg.startswith("cacheblend"):
+            return n_tokens(w, r)
+        return len(planner.plan([("cached", pids[s.chunk]) if s.cached else ("tokens", s.tokens) for s in r],
+                                w.alg)["sel"])
+    rows_link = max((sum(rows_of(r) for r in x) for x in waves), default=64)
     planner.close()
+    wave_blocks = max((sum((n_tokens(w, r) + 15) // 16 for r in x) for x in waves), default=64)
     with torch.cuda.stream(stream):
-        tp_kw = dict(tp_rank=rank, tp_size=world) if args.tp else {}
-        eng = B.Engine(m, num_blocks=(total_tokens + sum(N_tok)) // 16 + 2 * len(w.chunks) + 64 * len(w.requests),
+        tp_kw = dict(tp_rank=rank, tp_size=world) if tp else {}
+        eng = B.Engine(m, num_blocks=total_tokens // 16 + 2 * len(w.chunks) + wave_blocks + 64 * wave_max,
                        max_rows=max(4096, rows_link), max_tokens=max(max_N + 2 * args.decode_steps + 16, 512) + 16,
-                       max_requests=len(w.requests), device=dev, stream=stream, **tp_kw)
+                       max_requests=wave_max, device=dev, stream=stream, **tp_kw)
         eng.kv_share = bool(args.kv_share)
-        if args.tp and world > 1:
+        if tp and world > 1:
             D.tp_connect(eng)
         ids = eng.generate_context_cache(w.chunks, dummy_prefix=dummy_prefix(w.alg))
-        reqs = [[("cached", ids[s.chunk]) if s.cached else ("tokens", s.tokens) for s in r] for r in w.requests]
-        logits_dev = torch.empty((len(reqs), m.vocab), dtype=torch.float32, device=f"cuda:{dev}")
+        wave_segs = [[[("cached", ids[s.chunk]) if s.cached else ("tokens", s.tokens) for s in r] for r in x]
+                     for x in waves]
+        logits_dev = torch.empty((1, m.vocab), dtype=torch.float32, device=f"cuda:{dev}")
 
-        def step():
-            if len(reqs) == 1:
-                return [eng.link(reqs[0], w.alg, want_logits=False, logits_dev=logits_dev[0])]
-            return eng.link_batch(reqs, w.alg, want_logits=False)
+        def link_wave(segs, want_logits):
+            if len(segs) == 1:
+                if want_logits:
+                    return [eng.link(segs[0], w.alg, want_logits=True)]
+                return [eng.link(segs[0], w.alg, want_logits=False, logits_dev=logits_dev[0])]
+            return eng.link_batch(segs, w.alg, want_logits=want_logits)
 
-        for _ in range(args.warmup):
-            step()
+        kernels_per_step = 0
+        for i in range(args.warmup):
+            for segs in wave_segs:
+                link_wave(segs, False)
+                if i == args.warmup - 1:
+                    kernels_per_step += eng.stats()["kernels_last_call"]
         stream.synchronize()
-        kernels_per_step = eng.stats()["kernels_last_call"]
-
-        barrier = D.barrier
 
         # ---------------- timed region: device-resident inputs, CUDA events on our stream
-        barrier()
+        D.barrier()
         torch.cuda.synchronize(dev)
-        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]   # per-step boundaries
+        mk = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+        ev_step = [mk() for _ in range(args.steps + 1)]
+        ev_wave = [[mk() for _ in wave_segs] for _ in range(args.steps)]
         with ClockSampler(dev) as clk:
-            ev0.record(stream)
+            ev_step[0].record(stream)
             for i in range(args.steps):
-                outs = step()
-                evs[i].record(stream)
-            ev1.record(stream)
-            ev1.synchronize()
+                for j, segs in enumerate(wave_segs):
+                    link_wave(segs, False)
+                    ev_wave[i][j].record(stream)
+                ev_step[i + 1].record(stream)
+            ev_step[-1].synchronize()
         torch.cuda.synchronize(dev)
-        barrier()
-        ms_max = D.max_over_ranks(ev0.elapsed_time(ev1), device=red_dev)
+        D.barrier()
+        ms_rank = ev_step[0].elapsed_time(ev_step[-1])
+        ms_max = D.max_over_ranks(ms_rank, device=red_dev)
         ms_per_step = ms_max / args.steps
-        step_ms = sorted([ev0.elapsed_time(evs[0])] + [evs[i - 1].elapsed_time(evs[i]) for i in range(1, args.steps)])
-        ttft_dist = {"p50": float(np.percentile(step_ms, 50)), "p90": float(np.percentile(step_ms, 90)),
-                     "min": step_ms[0], "max": step_ms[-1], "how": "per-step CUDA events inside the timed region (rank 0)"}
-        tokens_all = (sum(N_tok) if args.tp else D.sum_over_ranks(sum(N_tok), device=red_dev)) * args.steps
-        value = tokens_all / (ms_max / 1e3)
+        # per-request TTFT: completion of its wave, from the start of its step (all arrive at t = 0)
+        ttft = []
+        for i in range(args.steps):
+            for j, segs in enumerate(wave_segs):
+                ttft += [ev_step[i].elapsed_time(ev_wave[i][j])] * len(segs)
+        step_ms = [ev_step[i].elapsed_time(ev_step[i + 1]) for i in range(args.steps)]
+        if world > 1 and not tp:
+            import torch.distributed as dist
+            allt = [None] * world
+            dist.all_gather_object(allt, ttft)
+            ttft = [x for t in allt for x in t]
+        tokens_step = sum(N_tok) if tp else D.sum_over_ranks(sum(N_tok), device=red_dev)
+        value = tokens_step * args.steps / (ms_max / 1e3)
 
-        # ---------------- e2e: the public call with host buffers (plan H2D + logits D2H per step)
-        barrier()
+        # ---------------- e2e: the public call with host buffers (plan H2D + logits D2H per wave)
+        D.barrier()
         torch.cuda.synchronize(dev)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        h2d = d2h = 0
         t0 = time.perf_counter()
-        e0.record(stream)
         for _ in range(args.steps):
-            if len(reqs) == 1:
-                o = eng.link(reqs[0], w.alg, want_logits=True)
-            else:
-                o = eng.link_batch(reqs, w.alg, want_logits=True)[0]
-        e1.record(stream)
-        e1.synchronize()
+            h2d = d2h = 0
+            for segs in wave_segs:
+                link_wave(segs, True)
+                st = eng.stats()
+                h2d += int(st["h2d_bytes_last_call"])
+                d2h += int(st["d2h_bytes_last_call"])
+        torch.cuda.synchronize(dev)
         wall = time.perf_counter() - t0
-        st = eng.stats()
         wall_max = D.max_over_ranks(wall, device=red_dev)
-        e2e_value = tokens_all / wall_max
+        e2e_value = tokens_step * args.steps / wall_max
 
-        # ---------------- f1: decode over the linked caches (TPOT); batch = this rank's requests
+        # ---------------- f1: decode over the first wave's linked caches (TPOT)
         dec = None
-        if args.decode_steps > 0 and not args.tp:
-            held = (eng.link_batch(reqs, w.alg, keep_linked=True) if len(reqs) > 1
-                    else [eng.link(reqs[0], w.alg, keep_linked=True)])
+        if args.decode_steps > 0 and not tp and wave_segs:
+            first = wave_segs[0]
+            held = (eng.link_batch(first, w.alg, keep_linked=True) if len(first) > 1
+                    else [eng.link(first[0], w.alg, keep_linked=True)])
             hs = [o.linked for o in held]
-            # shared-block links: re-base the shared blocks into owned ones once, instead of re-rotating
-            # them in every decode step (pic_linked_materialize; timed on its own)
             mat_ms = None
             if args.kv_share:
+                # shared-block links: re-base the shared blocks into owned ones once (pic_linked_materialize)
                 torch.cuda.synchronize(dev)
-                m0, m1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                m0, m1 = mk(), mk()
                 m0.record(stream)
                 for h in hs:
                     eng.materialize(h)
@@ -383,36 +491,30 @@ def main():
             for _ in range(3):
                 eng.decode(hs, forced, want_logits=False, logits_dev=dl.data_ptr())
             dec_launches = eng.stats()["kernels_last_call"]
-            barrier()
+            D.barrier()
             torch.cuda.synchronize(dev)
-            d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            d0, d1 = mk(), mk()
             d0.record(stream)
             for _ in range(args.decode_steps):                    # teacher-forced: no host round trip
                 eng.decode(hs, forced, want_logits=False, logits_dev=dl.data_ptr())
             d1.record(stream)
             d1.synchronize()
-            barrier()
+            D.barrier()
             tpot = D.max_over_ranks(d0.elapsed_time(d1), device=red_dev) / args.decode_steps
-            t0 = time.perf_counter()
-            toks = forced
-            for _ in range(args.decode_steps // 2):               # greedy through the public call
-                toks = [int(t) for t in eng.decode(hs, toks, want_logits=False).next_token]
-            tpot_host = (time.perf_counter() - t0) / max(1, args.decode_steps // 2) * 1e3
-            batch_all = D.sum_over_ranks(len(hs), device=red_dev)
-            dec = {"tpot_ms": tpot, "tokens_per_s": batch_all / (tpot / 1e3), "batch_per_gpu": len(hs),
-                   "context_tokens": int(max_N), "steps": args.decode_steps, "tpot_ms_host_greedy": tpot_host,
-                   "gpu_launches_per_step": int(dec_launches), "materialize_ms": mat_ms,
-                   "how": "pic_decode over the linked caches of this rank's requests (f1), one token per cache per "
-                          "step, CUDA events on the bench stream (teacher-forced), then a greedy host loop; "
-                          "shared-block links are materialized first (pic_linked_materialize, materialize_ms)"}
+            dec = {"tpot_ms": tpot, "batch_per_gpu": len(hs), "context_tokens": int(max_N),
+                   "steps": args.decode_steps, "gpu_launches_per_step": int(dec_launches), "materialize_ms": mat_ms,
+                   "how": "pic_decode over the first wave's linked caches (f1), one token per cache per step, CUDA "
+                          "events on the bench stream (teacher-forced); shared-block links materialized first"}
             for h in hs:
                 eng.release(h)
 
-        # ---------------- per-kernel CUDA-event profile (separate pass, same stream)
+        # ---------------- per-kernel CUDA-event profile (separate pass, same stream, graphs off)
         eng.set_profiling(True)
         eng.profile(reset=True)
         for _ in range(args.profile_steps):
-            step()
+            for segs in wave_segs:
+                link_wave(segs, False)
+        stream.synchronize()
         prof = eng.profile(reset=True)
         eng.set_profiling(False)
 
@@ -422,31 +524,32 @@ def main():
             dist.destroy_process_group()
         return
     P, src = peaks()
-    roof, breakdown = roofline(prof, P, src, args.profile_steps) if prof else (None, {})
-    line = {"metric": "linked_prefill_tokens_per_s", "value": value, "unit": "tokens/s", "n_gpus": world,
+    roof, breakdown = roofline(prof, P, src, args.profile_steps, args.config) if prof else (None, {})
+    ttft_a = np.asarray(ttft)
+    line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-            "ttft_ms_device": ms_per_step if len(reqs) == 1 else None,
-            "step_ms_distribution": ttft_dist,
-            "ttft_ms_requests": ({"mean": ms_per_step, "p99": float(np.percentile(step_ms, 99)),
-                                  "how": "SURVEY 8(d) cfg4: every request of a wave arrives at t=0, its TTFT is the "
-                                         "wave's completion (one wave per step)"} if len(reqs) > 1 else None),
-            "higher_is_better": True, "scaling": "strong" if args.tp else "weak", "vs_baseline": None,
-            "dtype": "bf16", "data": "synthetic",
-            "config": dict(cfgd, parallelism=(f"tp{world} (heads/MLP sharded, fused peer-memory all-reduce)" if args.tp
-                                              else f"dp{world} (independent requests)"),
-                           **({"truncated_layers": args.layers} if args.layers else {})),
-            "clocks": clk.summary(), "gpu_launches": int(kernels_per_step * args.steps),
-            "e2e": {"value": e2e_value, "unit": "tokens/s", "ttft_ms_host": wall_max / args.steps * 1e3,
-                    "h2d_bytes_per_step": int(st["h2d_bytes_last_call"]),
-                    "d2h_bytes_per_step": int(st["d2h_bytes_last_call"])},
+            "ttft_ms": {"mean": float(ttft_a.mean()), "p50": float(np.percentile(ttft_a, 50)),
+                        "p99": float(np.percentile(ttft_a, 99)), "max": float(ttft_a.max()),
+                        "requests": int(len(ttft_a) // args.steps),
+                        "how": "every request arrives at t = 0 of its step; TTFT = device completion of its wave "
+                               "(CUDA events), over all requests of all ranks and timed steps"},
+            "step_ms_rank0": {"p50": float(np.median(step_ms)), "min": float(min(step_ms)), "max": float(max(step_ms))},
+            "waves_per_gpu": len(wave_segs),
+            "recomputed_rows_per_wave": rows_link,
+            "higher_is_better": True, "scaling": cfgd_scaling(cfgd), "vs_baseline": None,
+            "dtype": "bf16", "data": "synthetic (seeded random-init weights and tokens, SURVEY §8(c).6)",
+            "config": cfgd, "clocks": clk.summary(), "gpu_launches": int(kernels_per_step * args.steps),
+            "e2e": {"value": e2e_value, "unit": "tokens/s", "ms_per_step_host": wall_max / args.steps * 1e3,
+                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "how": "pic_link_batch with host logits (plan H2D, logits + first token D2H) per wave, host clock"},
             "roofline": roof, "kernel_breakdown": breakdown, "decode": dec,
             "context": "paper (A100-80GB, vLLM 0.4.1): LegoLink-16 up to 8x lower TTFT and 7x throughput vs "
                        "CacheBlend-15 under load (P:303-305); not comparable hardware/workload"}
     if world == 1 and not args.no_cpu_baseline:
-        v, per_req, sample = oracle_sample(w)
+        v, sample = oracle_sample(w)
         line["cpu_baseline"] = {"value": v, "unit": "tokens/s", "cores": cores_used(), "kind": "oracle",
                                 "sample": sample}
-    print(json.dumps(line))
+    print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()

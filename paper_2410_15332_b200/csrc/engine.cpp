@@ -19,13 +19,27 @@ using namespace pic;
 // ============================================================================ errors
 static thread_local std::string g_err;
 
-static pic_status fail(pic_status s, const char* fmt, ...) {
+static pic_status vfail(pic_status s, const char* fmt, va_list ap) {
   char buf[1024];
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  g_err = buf;
+  return s;
+}
+
+static pic_status fail(pic_status s, const char* fmt, ...) {
   va_list ap;
   va_start(ap, fmt);
-  vsnprintf(buf, sizeof buf, fmt, ap);
+  vfail(s, fmt, ap);
   va_end(ap);
-  g_err = buf;
+  return s;
+}
+
+// Same error path for the other translation units (serve.cpp): sets pic_last_error().
+pic_status pic_fail(pic_status s, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vfail(s, fmt, ap);
+  va_end(ap);
   return s;
 }
 
@@ -1033,7 +1047,9 @@ struct Runner {
     const int box = g.pair ? g.bn / 2 : g.bn;  // a CTA pair loads half of the N-tile per CTA
     const CUtensorMap* Bm = (box == 64 || box == 128 || box == 256) ? &B3[bn_index(box)] : nullptr;
     if (!Bm) TRY(weight_map(e, B_ptr, N, K, box, &Bm));
-    PROF("gemm", (double)N * K * 2 + (double)M * K * 2 + (double)M * N * 4, 2.0 * M * N * K,
+    // algorithmic bytes: the weights, read once per forward; activations and split-K
+    // partials are not counted (they are the non-algorithmic part of the measured DRAM traffic)
+    PROF("gemm", (double)N * K * 2, 2.0 * M * N * K,
          launch_gemm_partial(A, *Bm, e->ws, M, N, K, g.splits, g.bn, st, 0, GemmNext{}, g.pair));
     return PIC_OK;
   }
@@ -1059,7 +1075,8 @@ static pic_status enqueue_forward(pic_engine* e, const Fwd& f, const DevPlan& dp
   const size_t lbytes = (size_t)e->layer_stride * (e->f32 ? 4 : 2);
 
   // a2: the first K2 layer on the main stream; the other layers on a side stream, overlapping the
-  // first layers' weight streaming (layer l's attention waits for them; scatter writes disjoint slots)
+  // first layers' weight streaming (layer k2_layer0+1's attention waits for them — LegoLink/Naive scatter
+  // writes slots disjoint from K2's; CacheBlend waits before that layer's scatter, see below)
   const bool k2_side = !f.k2_src.empty() && f.k2_layer0 + 1 < L && !e->profiling && k2_overlap() && e->side_stream;
   if (!f.k2_src.empty() && f.k2_layer0 < L) {
     const int n_first = k2_side ? 1 : L - f.k2_layer0;
@@ -1133,6 +1150,9 @@ static pic_status enqueue_forward(pic_engine* e, const Fwd& f, const DevPlan& dp
       if (l > 0) TRY(capture(l - 1));
       TRY(R.gemm(e->tm_x, w.tm_qkv, M, qkv, d, &s, e->x, w.qkv));
     }
+    // CacheBlend: the side-stream K2 covers every cached row (the selection is device-side), including
+    // the rows this layer's scatter rewrites, so it must land before the scatter, not just before attention
+    if (k2_side && f.cb && l == f.k2_layer0 + 1) CK(cudaStreamWaitEvent(st, e->k2_join, 0));
     if (f.cb && l == f.cb_layer) {
       // a9: CacheBlend selection at the check layer (P:170 steps 3-4)
       if (!f.cb_override) {
@@ -1161,7 +1181,7 @@ static pic_status enqueue_forward(pic_engine* e, const Fwd& f, const DevPlan& dp
                                  st, e->f32, pos == dp.pos ? 1 : 0));
     }
     if (f.compile && l == L - 1) break;  // compile needs only the last layer's K/V
-    if (k2_side && l == f.k2_layer0 + 1) CK(cudaStreamWaitEvent(st, e->k2_join, 0));  // side-stream K2 landed
+    if (k2_side && !f.cb && l == f.k2_layer0 + 1) CK(cudaStreamWaitEvent(st, e->k2_join, 0));  // side-stream K2 landed
     // a6 attention — algorithmic work: 4·H_q·D·Σ(p_i+1) FLOPs, K/V of keys 0..max p read once
     double attn_flops = 0, attn_bytes = 0;
     if (e->profiling) {
@@ -1289,7 +1309,7 @@ static pic_status enqueue_forward(pic_engine* e, const Fwd& f, const DevPlan& dp
       const bool pair = swiglu_pair(e, M, 2 * F);
       const CUtensorMap* Bg = &w.tm_gu_fused;
       if (pair) TRY(weight_map(e, w.gu, 2 * F, d, e->gu_group, &Bg));  // each CTA: the gate or the up half
-      PROF("gemm", (double)2 * F * d * 2 + (double)M * d * 2 + (double)M * F * 2, 2.0 * M * 2 * F * d,
+      PROF("gemm", (double)2 * F * d * 2, 2.0 * M * 2 * F * d,
            launch_gemm_swiglu(e->tm_x, *Bg, e->u, M, 2 * F, d, 2 * e->gu_group, st, 0, GemmNext{}, pair ? 1 : 0));
     } else {
       TRY(R.gemm(e->tm_x, w.tm_gu, M, 2 * F, d, &s, e->x, w.gu));
@@ -1799,6 +1819,19 @@ static pic_status link_impl(pic_engine* e, int32_t n_req, const pic_segment* con
       return fail(PIC_E_CUDA, "link: %s", cudaGetErrorString(ce));
     }
   }
+  // every handle exists before any is handed out: a failed allocation leaves out_linked untouched
+  std::vector<pic_linked*> handles;
+  if (out_linked) {
+    for (int r = 0; r < n_req; ++r) {
+      pic_linked* h = new (std::nothrow) pic_linked();
+      if (!h) {
+        for (pic_linked* x : handles) delete x;
+        rollback();
+        return fail(PIC_E_OOM, "linked handle");
+      }
+      handles.push_back(h);
+    }
+  }
   for (int r = 0; r < n_req; ++r) {
     pic_link_result& res = results[r];
     res.n_tokens = reqs[r].p.N;
@@ -1815,11 +1848,7 @@ static pic_status link_impl(pic_engine* e, int32_t n_req, const pic_segment* con
         std::copy(reqs[r].p.sel.begin(), reqs[r].p.sel.end(), res.selected);
     }
     if (out_linked) {
-      pic_linked* h = new (std::nothrow) pic_linked();
-      if (!h) {
-        rollback();
-        return fail(PIC_E_OOM, "linked handle");
-      }
+      pic_linked* h = handles[r];
       h->n_tokens = reqs[r].p.N;
       h->blocks = reqs[r].bt;
       h->bdelta = reqs[r].bdelta;
@@ -2068,17 +2097,22 @@ extern "C" pic_status pic_linked_materialize(pic_engine* e, pic_linked* h, void*
       host[2 * n + k * 16 + j] = h->bdelta[idx[k]];           // Δ
     }
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  CK(cudaEventSynchronize(e->plan_ev));
+  // any failure after the allocation returns the fresh blocks (nothing observable changes on error)
+  auto undo = [&](cudaError_t ce, const char* what) {
+    e->alloc.release(fresh);
+    return fail(PIC_E_CUDA, "materialize %s: %s", what, cudaGetErrorString(ce));
+  };
+  cudaError_t ce = cudaEventSynchronize(e->plan_ev);
+  if (ce != cudaSuccess) return undo(ce, "plan event");
   std::memcpy(e->plan_host, host.data(), host.size() * 4);
-  CK(cudaMemcpyAsync(e->plan_dev, e->plan_host, host.size() * 4, cudaMemcpyHostToDevice, st));
-  CK(cudaEventRecord(e->plan_ev, st));
-  const cudaError_t ce = launch_kv_link(e->Kpool, e->Vpool, e->plan_dev, e->plan_dev + n, e->plan_dev + 2 * n, (int)n,
+  ce = cudaMemcpyAsync(e->plan_dev, e->plan_host, host.size() * 4, cudaMemcpyHostToDevice, st);
+  if (ce != cudaSuccess) return undo(ce, "plan copy");
+  ce = cudaEventRecord(e->plan_ev, st);
+  if (ce != cudaSuccess) return undo(ce, "plan event");
+  ce = launch_kv_link(e->Kpool, e->Vpool, e->plan_dev, e->plan_dev + n, e->plan_dev + 2 * n, (int)n,
                                         0, e->cfg.n_layers, e->layer_stride, e->cfg.n_kv_heads, e->cfg.head_dim,
                                         e->cos_t, e->sin_t, 1, st, e->f32);
-  if (ce != cudaSuccess) {
-    e->alloc.release(fresh);
-    return fail(PIC_E_CUDA, "materialize: %s", cudaGetErrorString(ce));
-  }
+  if (ce != cudaSuccess) return undo(ce, "kv_link");
   // the chunk-store blocks lose this reference; later work on `stream` is ordered after the copy
   std::vector<int32_t> old;
   for (size_t k = 0; k < idx.size(); ++k) {

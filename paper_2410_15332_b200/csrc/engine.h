@@ -11,6 +11,9 @@
 #include "../../include/pic.h"
 #include "kernels/kernels.h"
 
+// Record a formatted message for pic_last_error() and return `s` (defined in engine.cpp).
+pic_status pic_fail(pic_status s, const char* fmt, ...);
+
 namespace pic {
 
 // Deterministic paged-block allocator: lowest free ids first (D3; modelled by oracle.pic.BlockAllocator).

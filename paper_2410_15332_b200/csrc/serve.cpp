@@ -50,13 +50,13 @@ void arrivals(int n_users, double rate, double duration, uint64_t seed, std::vec
 
 extern "C" pic_status pic_serve_arrivals(int32_t n_users, double rate, double duration_s, uint64_t seed,
                                          double* times, int32_t* users, int32_t* n_inout) {
-  if (!n_inout || (*n_inout > 0 && (!times || !users))) return PIC_E_INVALID_ARG;
+  if (!n_inout || (*n_inout > 0 && (!times || !users))) return pic_fail(PIC_E_INVALID_ARG, "serve_arrivals: NULL output");
   std::vector<double> t;
   std::vector<int> u;
   arrivals(n_users, rate, duration_s, seed, t, u);
   if ((int64_t)t.size() > *n_inout) {
     *n_inout = (int32_t)t.size();
-    return PIC_E_CAPACITY;
+    return pic_fail(PIC_E_CAPACITY, "serve_arrivals: %zu arrivals exceed the output capacity", t.size());
   }
   for (size_t i = 0; i < t.size(); ++i) {
     times[i] = t[i];
@@ -68,8 +68,10 @@ extern "C" pic_status pic_serve_arrivals(int32_t n_users, double rate, double du
 
 extern "C" pic_status pic_serve_poisson(pic_engine* e, const pic_serve_config* cfg, void* stream,
                                         pic_serve_stats* out) {
-  if (!e || !cfg || !out || cfg->n_users <= 0 || !cfg->user_segs || !cfg->user_n_segs) return PIC_E_INVALID_ARG;
-  if (cfg->max_batch <= 0 || cfg->max_batch > e->lim.max_requests) return PIC_E_INVALID_ARG;
+  if (!e || !cfg || !out || cfg->n_users <= 0 || !cfg->user_segs || !cfg->user_n_segs)
+    return pic_fail(PIC_E_INVALID_ARG, "serve_poisson: NULL argument or no users");
+  if (cfg->max_batch <= 0 || cfg->max_batch > e->lim.max_requests)
+    return pic_fail(PIC_E_INVALID_ARG, "serve_poisson: max_batch %d outside [1, max_requests]", cfg->max_batch);
   const bool cb = cfg->params.alg == PIC_CACHEBLEND;
   const int max_batch = cb ? 1 : cfg->max_batch;
   // per-user footprint: linked blocks and recomputed rows (the planner's own numbers)
@@ -83,7 +85,8 @@ extern "C" pic_status pic_serve_poisson(pic_engine* e, const pic_serve_config* c
     ntok[k] = po.n_tokens;
     blocks[k] = po.n_blocks - po.n_shared;  // fresh blocks only (kv_share links chunk-store blocks by reference)
     rows[k] = cb ? po.n_tokens : po.n_sel;
-    if (rows[k] > e->lim.max_rows) return PIC_E_CAPACITY;
+    if (rows[k] > e->lim.max_rows)
+      return pic_fail(PIC_E_CAPACITY, "serve_poisson: user %d recomputes %d rows > max_rows", k, rows[k]);
   }
   pic_stats st0{};
   pic_get_stats(e, &st0);
@@ -126,7 +129,8 @@ extern "C" pic_status pic_serve_poisson(pic_engine* e, const pic_serve_config* c
       batch.push_back(q.front());
       q.pop_front();
     }
-    if (batch.empty()) return PIC_E_CAPACITY;  // one request alone does not fit the pool
+    if (batch.empty())  // one request alone does not fit the pool
+      return pic_fail(PIC_E_CAPACITY, "serve_poisson: one request alone does not fit the free pool");
     segs.clear();
     nsegs.clear();
     for (int i : batch) {

@@ -103,9 +103,36 @@ def matrix(seed: int, tag: int, rows: int, cols: int, fan_in: Optional[int] = No
         nrows = rows - row0
     fi = cols if fan_in is None else fan_in
     e = 0 if fi == 0 else weight_exponent(fi)
-    idx = (np.arange(row0 * cols, (row0 + nrows) * cols, dtype=np.uint64))
-    w = bf16_rne(uniform_pm1(U(seed, tag, idx))) * np.float32(2.0 ** e)
-    return w.reshape(nrows, cols)
+    out = np.empty(nrows * cols, dtype=np.float32)
+    scale = np.float32(2.0 ** e)
+
+    def fill(a: int, b: int) -> None:
+        idx = np.arange(row0 * cols + a, row0 * cols + b, dtype=np.uint64)
+        out[a:b] = bf16_rne(uniform_pm1(U(seed, tag, idx))) * scale
+
+    _parallel_ranges(nrows * cols, fill)
+    return out.reshape(nrows, cols)
+
+
+_POOL = None
+
+
+def _parallel_ranges(n: int, fn, grain: int = 1 << 22) -> None:
+    """fn(a, b) over [0, n) in slices on a thread pool (NumPy ufuncs release the GIL); element i
+    depends only on its counter, so the result is independent of the split."""
+    global _POOL
+    if n <= grain:
+        fn(0, n)
+        return
+    import concurrent.futures as cf
+    import os
+    if _POOL is None:
+        try:
+            nt = len(os.sched_getaffinity(0))
+        except AttributeError:
+            nt = os.cpu_count() or 1
+        _POOL = cf.ThreadPoolExecutor(max_workers=max(1, nt))
+    list(_POOL.map(lambda a: fn(a, min(n, a + grain)), range(0, n, grain)))
 
 
 def gains(seed: int, tag: int, n: int) -> np.ndarray:

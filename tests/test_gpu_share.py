@@ -256,11 +256,14 @@ def test_shared_link_without_rebase_bit_identical(setup):
     """SPEC's no-re-base reading (rebase = 0, reading R1): shared blocks then carry Δ = 0 and the result
     equals the copy path's (cached keys left at their compile positions) bit for bit."""
     s = setup
+    any_shared = 0
     for segs in [s.w.requests[0]] + sg.permuted_requests(s.w, 2):
         copy, shared = link_both(s, segs, "legolink:4", rebase=False)
         try:
             assert_identical(copy, shared)
             assert not shared[4].any()          # nothing to rotate
+            any_shared += shared[3]
         finally:
             s.eng.release(copy[0].linked)
             s.eng.release(shared[0].linked)
+    assert any_shared > 0                       # the planner did link blocks by reference
