@@ -100,9 +100,10 @@ typedef struct {
   int32_t use_graph;         /* 1 = replay a CUDA graph per plan shape (default 1) */
   const int32_t* sel_override; /* CacheBlend test hook: sorted linked indices to keep after the check (nullable) */
   int32_t n_sel_override;
-  float* debug_hidden;       /* test hook (nullable, host): [n_layers][N][d_model] fp32; row r of layer l = residual of
-                                the r-th selected row after layer l (rows beyond that layer's k' untouched).
-                                Single-request pic_link only; disables graphs. */
+  float* debug_hidden;       /* test hook (nullable, host): [n_layers][R][d_model] fp32 with R = max(N of request 0,
+                                Σ_requests k'); row r of layer l = residual after layer l of the r-th recomputed row
+                                of the forward (request 0's selected rows in order, then request 1's, ...; rows
+                                beyond that layer's count untouched).  Disables graphs. */
   int32_t kv_share;          /* 1 = shared-block link: a linked block whose 16 rows are all
                                 unselected rows of one cached chunk, aligned to one of its store blocks, points
                                 at that chunk-store block (reference counted) instead of a fresh copy; its keys
@@ -212,7 +213,9 @@ pic_status pic_plan(pic_engine* eng, const pic_segment* segs, int32_t n_segs, co
                     pic_plan_out* out);
 
 /* Copy layer `layer` of a linked KV cache to host: k_host, v_host are [N][H_kv][D] bf16 (uint16), or fp32 for a
- * PIC_DTYPE_FP32_DEBUG engine. */
+ * PIC_DTYPE_FP32_DEBUG engine.  Keys of shared blocks (kv_share) are exported at their linked positions: the
+ * device re-bases them (a2's kv_link kernel, this layer) into scratch pool blocks first, so the call needs one
+ * free block per shared block with Δ != 0 (PIC_E_CAPACITY otherwise).  Synchronises the device. */
 pic_status pic_linked_export(pic_engine* eng, const pic_linked* linked, int32_t layer, void* k_host, void* v_host);
 /* Number of tokens N and the block table (int32[ceil(N/16)], nullable) of a linked cache. */
 pic_status pic_linked_info(pic_engine* eng, const pic_linked* linked, int32_t* n_tokens, int32_t* block_table);

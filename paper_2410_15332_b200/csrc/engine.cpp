@@ -689,8 +689,21 @@ extern "C" pic_status pic_tp_connect(pic_engine* e, const void* handles, const u
     cudaIpcMemHandle_t h;
     std::memcpy(&h, reinterpret_cast<const char*>(handles) + 64 * r, sizeof h);
     void* base = nullptr;
-    CK(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
+    const cudaError_t oe = cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess);
+    if (oe != cudaSuccess)
+      return fail(PIC_E_CUDA, "tp rank %d cannot map rank %d's arena (%s): the fused all-reduce needs CUDA IPC "
+                  "and peer access between the ranks' GPUs", e->tp_rank, r, cudaGetErrorString(oe));
     e->ipc_opened.push_back(base);
+    // the peer's arena lives on its own GPU: this GPU must reach it with loads/stores (NVLink P2P)
+    cudaPointerAttributes pa{};
+    CK(cudaPointerGetAttributes(&pa, base));
+    if (pa.device != e->device) {
+      int can = 0;
+      CK(cudaDeviceCanAccessPeer(&can, e->device, pa.device));
+      if (!can)
+        return fail(PIC_E_CUDA, "tp rank %d: device %d has no peer access to device %d of rank %d", e->tp_rank,
+                    e->device, pa.device, r);
+    }
     char* peer = reinterpret_cast<char*>(base) + offsets[r];
     const ptrdiff_t d_ar0 = reinterpret_cast<char*>(e->ar_buf[0]) - e->arena;
     const ptrdiff_t d_ar1 = reinterpret_cast<char*>(e->ar_buf[1]) - e->arena;
@@ -1689,7 +1702,7 @@ static pic_status link_impl(pic_engine* e, int32_t n_req, const pic_segment* con
   if (n_req > e->lim.max_requests) return fail(PIC_E_CAPACITY, "%d requests exceed max_requests", n_req);
   TRY(check_params(pr));
   const bool cb = pr->alg == PIC_CACHEBLEND;
-  if ((cb || pr->debug_hidden) && n_req != 1) return fail(PIC_E_VARIANT, "CacheBlend/debug hooks are single-request");
+  if (cb && n_req != 1) return fail(PIC_E_VARIANT, "CacheBlend is single-request");
   if (pr->sel_override && !cb) return fail(PIC_E_VARIANT, "sel_override is a CacheBlend hook");
   if (e->host_only) return fail(PIC_E_NO_DEVICE, "host-only engine cannot link");
   if (e->tp_size > 1 && !e->tp_connected) return fail(PIC_E_INVALID_ARG, "tensor-parallel engine: call pic_tp_connect first");
@@ -1708,7 +1721,6 @@ static pic_status link_impl(pic_engine* e, int32_t n_req, const pic_segment* con
   Fwd f;
   f.rebase = pr->rebase;
   f.n_head = n_req;
-  f.debug_rows = reqs[0].p.N;
   for (int r = 0; r < n_req; ++r) {
     reqs[r].bt = merge_blocks(reqs[r].shared, e->alloc.alloc(reqs[r].n_fresh));
     for (int32_t b : reqs[r].shared)
@@ -1718,6 +1730,7 @@ static pic_status link_impl(pic_engine* e, int32_t n_req, const pic_segment* con
     for (auto& rb : reqs) e->alloc.release(rb.bt);
   };
   for (int r = 0; r < n_req; ++r) append_request(e, pr, reqs[r], r, f);
+  f.debug_rows = std::max(reqs[0].p.N, f.M);  // debug_hidden row stride (pic.h)
   if (cb) {
     const LinkPlanHost& p = reqs[0].p;
     const int N = p.N;
@@ -1977,86 +1990,73 @@ extern "C" pic_status pic_link_batch(pic_engine* e, int32_t n_req, const pic_seg
 }
 
 // ============================================================================ exports / lifecycle
-static inline float bf16_to_f(uint16_t h) {
-  uint32_t u = (uint32_t)h << 16;
-  float f;
-  std::memcpy(&f, &u, 4);
-  return f;
-}
-static inline uint16_t f_to_bf16(float f) {  // round to nearest even (finite values)
-  uint32_t u;
-  std::memcpy(&u, &f, 4);
-  return (uint16_t)((u + 0x7FFFu + ((u >> 16) & 1u)) >> 16);
-}
-
-// Host copy of the attention kernels' K-tile re-base (rebase_pair): oa = fma(a, c, −(b·s)),
-// ob = fma(b, c, a·s), then the pool's precision — so exported rows of a shared block (f3) are the
-// rows the kernels attend to, bit for bit.
-static pic_status rebase_export(pic_engine* e, void* k_host, int n, const std::vector<int32_t>& bdelta) {
-  const int Hkv = e->cfg.n_kv_heads, D = e->cfg.head_dim, h = D / 2;
-  std::vector<float> cs(h), sn(h);
-  int cached = 0;
-  for (int i = 0; i < n; ++i) {
-    const int dl = bdelta[i / 16];
-    if (dl == 0) continue;
-    const int ad = dl < 0 ? -dl : dl;
-    const float sg = dl < 0 ? -1.f : 1.f;
-    if (ad != cached) {
-      CK(cudaMemcpy(cs.data(), e->cos_t + (size_t)ad * h, h * 4, cudaMemcpyDeviceToHost));
-      CK(cudaMemcpy(sn.data(), e->sin_t + (size_t)ad * h, h * 4, cudaMemcpyDeviceToHost));
-      cached = ad;
-    }
-    for (int g = 0; g < Hkv; ++g)
-      for (int j = 0; j < h; ++j) {
-        const size_t ia = ((size_t)i * Hkv + g) * D + j, ib = ia + h;
-        float a, b;
-        if (e->f32) {
-          a = reinterpret_cast<float*>(k_host)[ia];
-          b = reinterpret_cast<float*>(k_host)[ib];
-        } else {
-          a = bf16_to_f(reinterpret_cast<uint16_t*>(k_host)[ia]);
-          b = bf16_to_f(reinterpret_cast<uint16_t*>(k_host)[ib]);
-        }
-        const float s = sg * sn[j];
-        const float ra = std::fma(a, cs[j], -(b * s)), rb = std::fma(b, cs[j], a * s);
-        if (e->f32) {
-          reinterpret_cast<float*>(k_host)[ia] = ra;
-          reinterpret_cast<float*>(k_host)[ib] = rb;
-        } else {
-          reinterpret_cast<uint16_t*>(k_host)[ia] = f_to_bf16(ra);
-          reinterpret_cast<uint16_t*>(k_host)[ib] = f_to_bf16(rb);
-        }
-      }
-  }
-  return PIC_OK;
-}
-
 static pic_status export_rows(pic_engine* e, const std::vector<int32_t>& blocks, int n, int layer, void* k_host,
-                              void* v_host, const std::vector<int32_t>* bdelta = nullptr) {
+                              void* v_host) {
   if (e->host_only) return fail(PIC_E_NO_DEVICE, "host-only engine");
   if (layer < 0 || layer >= e->cfg.n_layers) return fail(PIC_E_INVALID_ARG, "layer out of range");
   const int Hkv = e->cfg.n_kv_heads, D = e->cfg.head_dim;
   const size_t es = e->f32 ? 4 : 2;
   const size_t row = (size_t)D * es;
-  std::vector<uint16_t> kb((size_t)n * Hkv * D), vb((size_t)n * Hkv * D);
   CK(cudaDeviceSynchronize());
-  for (int i = 0; i < n; ++i)
+  // one strided copy per (block, head) slab: pool [blk][Hkv][16][D] -> host [n][Hkv][D]
+  for (int b = 0; b * 16 < n; ++b) {
+    const int rows = std::min(16, n - b * 16);
     for (int g = 0; g < Hkv; ++g) {
-      const size_t src = (size_t)layer * e->layer_stride + (((size_t)blocks[i / 16] * Hkv + g) * 16 + i % 16) * D;
+      const size_t src = (size_t)layer * e->layer_stride + ((size_t)blocks[b] * Hkv + g) * 16 * D;
+      const size_t dst = ((size_t)b * 16 * Hkv + g) * row;
       if (k_host)
-        CK(cudaMemcpy(reinterpret_cast<char*>(k_host) + ((size_t)i * Hkv + g) * row,
-                      reinterpret_cast<char*>(e->Kpool) + src * es, row, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy2D(reinterpret_cast<char*>(k_host) + dst, Hkv * row, reinterpret_cast<char*>(e->Kpool) + src * es,
+                        row, row, rows, cudaMemcpyDeviceToHost));
       if (v_host)
-        CK(cudaMemcpy(reinterpret_cast<char*>(v_host) + ((size_t)i * Hkv + g) * row,
-                      reinterpret_cast<char*>(e->Vpool) + src * es, row, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy2D(reinterpret_cast<char*>(v_host) + dst, Hkv * row, reinterpret_cast<char*>(e->Vpool) + src * es,
+                        row, row, rows, cudaMemcpyDeviceToHost));
     }
-  if (k_host && bdelta) TRY(rebase_export(e, k_host, n, *bdelta));
+  }
   return PIC_OK;
 }
 
 extern "C" pic_status pic_linked_export(pic_engine* e, const pic_linked* h, int32_t layer, void* k_host, void* v_host) {
   if (!e || !h) return fail(PIC_E_INVALID_ARG, "NULL argument");
-  return export_rows(e, h->blocks, h->n_tokens, layer, k_host, v_host, &h->bdelta);
+  if (e->host_only) return fail(PIC_E_NO_DEVICE, "host-only engine");
+  if (layer < 0 || layer >= e->cfg.n_layers) return fail(PIC_E_INVALID_ARG, "layer out of range");
+  std::vector<int> idx;
+  if (k_host)
+    for (size_t b = 0; b < h->bdelta.size(); ++b)
+      if (h->bdelta[b] != 0) idx.push_back((int)b);
+  if (idx.empty()) return export_rows(e, h->blocks, h->n_tokens, layer, k_host, v_host);
+  // Shared blocks (f3) hold keys at their compile positions.  Their re-based rows are produced on the
+  // device by a2's kernel (kv_link, this layer only) into scratch pool blocks — the arithmetic the
+  // attention kernels' K-tile rotation reproduces bit for bit — and exported from there.
+  const size_t n = idx.size() * 16;
+  if (3 * n > e->plan_cap_ints) return fail(PIC_E_CAPACITY, "export: %zu shared rows exceed the plan buffer", n);
+  if (!e->alloc.can((int64_t)idx.size()))
+    return fail(PIC_E_CAPACITY, "export of a shared-block link needs %zu free scratch blocks (pool has %zu)",
+                idx.size(), e->alloc.free_ids.size());
+  CK(cudaDeviceSynchronize());
+  std::vector<int32_t> fresh = e->alloc.alloc((int64_t)idx.size());
+  std::vector<int32_t> blocks = h->blocks;
+  std::vector<int32_t> host(3 * n);
+  for (size_t k = 0; k < idx.size(); ++k) {
+    for (int j = 0; j < 16; ++j) {
+      host[k * 16 + j] = h->blocks[idx[k]] * 16 + j;
+      host[n + k * 16 + j] = fresh[k] * 16 + j;
+      host[2 * n + k * 16 + j] = h->bdelta[idx[k]];
+    }
+    blocks[idx[k]] = fresh[k];
+  }
+  std::memcpy(e->plan_host, host.data(), host.size() * 4);
+  cudaError_t ce = cudaMemcpy(e->plan_dev, e->plan_host, host.size() * 4, cudaMemcpyHostToDevice);
+  if (ce == cudaSuccess)
+    ce = launch_kv_link(e->Kpool, e->Vpool, e->plan_dev, e->plan_dev + n, e->plan_dev + 2 * n, (int)n, layer, 1,
+                        e->layer_stride, e->cfg.n_kv_heads, e->cfg.head_dim, e->cos_t, e->sin_t, 1, 0, e->f32);
+  if (ce == cudaSuccess) ce = cudaDeviceSynchronize();
+  if (ce != cudaSuccess) {
+    e->alloc.release(fresh);
+    return fail(PIC_E_CUDA, "export re-base: %s", cudaGetErrorString(ce));
+  }
+  const pic_status s = export_rows(e, blocks, h->n_tokens, layer, k_host, v_host);
+  e->alloc.release(fresh);
+  return s;
 }
 
 extern "C" pic_status pic_linked_info(pic_engine* e, const pic_linked* h, int32_t* n_tokens, int32_t* block_table) {

@@ -388,12 +388,21 @@ class Engine:
                           hid)
 
     def link_batch(self, requests, alg: str, *, use_graph: bool = True, want_logits: bool = True,
-                   keep_linked: bool = False, kv_share: Optional[bool] = None) -> List[LinkOutput]:
+                   keep_linked: bool = False, kv_share: Optional[bool] = None,
+                   debug_hidden: bool = False) -> List[LinkOutput]:
+        """Batched link (pic_link_batch).  debug_hidden: every output's .hidden is the forward's
+        [L][R][d] residual array (R = max(N_0, Σ k'); request r's rows follow those of requests < r,
+        in selected order, see pic.h)."""
         n = len(requests)
         segs = [_Segs(r) for r in requests]
         arrp = (C.POINTER(SegmentC) * n)(*[C.cast(s.arr, C.POINTER(SegmentC)) for s in segs])
         ns = (C.c_int32 * n)(*[s.n for s in segs])
-        p, keep = self._params(alg, use_graph=use_graph, kv_share=kv_share)
+        hid = None
+        if debug_hidden:
+            plans = [self.plan(r, alg, kv_share=kv_share) for r in requests]
+            R = max(plans[0]["n_tokens"], sum(len(q["sel"]) for q in plans))
+            hid = np.full((self.cfg.n_layers, R, self.cfg.d_model), np.nan, dtype=np.float32)
+        p, keep = self._params(alg, use_graph=use_graph, kv_share=kv_share, debug_hidden=hid)
         res = (LinkResultC * n)()
         logits = None
         if want_logits:
@@ -404,7 +413,8 @@ class Engine:
         check(lib().pic_link_batch(self._h, n, arrp, ns, C.byref(p), self._stream, linked if keep_linked else None,
                                    res))
         return [LinkOutput(None if logits is None else logits[i], res[i].first_token, res[i].n_tokens,
-                           res[i].n_selected, res[i].n_selected_layer0, linked[i] if keep_linked else None)
+                           res[i].n_selected, res[i].n_selected_layer0, linked[i] if keep_linked else None,
+                           hidden=hid)
                 for i in range(n)]
 
     def decode(self, linked: Sequence[int], tokens: Sequence[int], *, use_graph: bool = True,

@@ -181,11 +181,12 @@ TINY = ModelConfig("tiny", 2, 64, 4, 4, 16, 128, 256, 1e4, 4096, 0x5EED0001)
 TINY_GQA = replace(TINY, name="tiny-gqa", n_kv_heads=2, seed=0x5EED0011)
 TINY_D128 = ModelConfig("tiny-d128", 2, 256, 2, 1, 128, 512, 512, 1e4, 4096, 0x5EED0021)
 TINY_TP = ModelConfig("tiny-tp", 2, 256, 4, 2, 128, 512, 512, 1e4, 4096, 0x5EED0031)   # shardable over 2 ranks
+TINY_TP8 = ModelConfig("tiny-tp8", 2, 1024, 16, 8, 128, 1024, 1024, 1e4, 4096, 0x5EED0041)  # 8 kv-heads: TP 2/4/8
 MISTRAL7B = ModelConfig("mistral7b", 32, 4096, 32, 8, 128, 14336, 32000, 1e6, 32768, 0x5EED0002)
 LLAMA31_8B = ModelConfig("llama31_8b", 32, 4096, 32, 8, 128, 14336, 128256, 5e5, 32768, 0x5EED0003)
 LLAMA3_70B = ModelConfig("llama3_70b", 80, 8192, 64, 8, 128, 28672, 128256, 5e5, 65536, 0x5EED0005)
 
-MODELS = {m.name: m for m in (TINY, TINY_GQA, TINY_D128, TINY_TP, MISTRAL7B, LLAMA31_8B, LLAMA3_70B)}
+MODELS = {m.name: m for m in (TINY, TINY_GQA, TINY_D128, TINY_TP, TINY_TP8, MISTRAL7B, LLAMA31_8B, LLAMA3_70B)}
 
 
 def truncated(cfg: ModelConfig, n_layers: int) -> ModelConfig:
