@@ -188,6 +188,12 @@ static bool k2_overlap() {
   return on;
 }
 
+// Consumers fused into unsplit GEMM epilogues (a5 RoPE + scatter, a7/a8 residual add); PIC_NO_EPI_FUSE=1
+// keeps the separate kernels (A/B and the bit-identity test only)
+static bool epi_fuse() {
+  static const bool on = getenv("PIC_NO_EPI_FUSE") == nullptr;
+  return on;
+}
 // Wave-quantised N-tile choice for multi-m-tile GEMMs (PIC_NO_WAVE_FIT=1: the bn 128/256 rule only)
 static bool wave_fit() {
   static const bool on = getenv("PIC_NO_WAVE_FIT") == nullptr;
@@ -1066,6 +1072,47 @@ struct Runner {
          launch_gemm_partial(A, *Bm, e->ws, M, N, K, g.splits, g.bn, st, 0, GemmNext{}, g.pair));
     return PIC_OK;
   }
+  // Unsplit (tensor-bound) choice whose N-tile has a fused-epilogue instance, else nullptr.
+  const CUtensorMap* fused_map(const CUtensorMap* B3, const void* B_ptr, int M, int N, int K, bool heads, int* bn,
+                               pic_status* err) {
+    *err = PIC_OK;
+    if (e->f32 || !epi_fuse()) return nullptr;
+    const GemmChoice g = choose_gemm(e, M, N, K);
+    if (g.splits != 1 || g.pair || !(heads ? (g.bn == 128 || g.bn == 256) : gemm_resid_supported(g.bn))) return nullptr;
+    const CUtensorMap* Bm = (g.bn == 64 || g.bn == 128 || g.bn == 256) ? &B3[bn_index(g.bn)] : nullptr;
+    if (!Bm) *err = weight_map(e, B_ptr, N, K, g.bn, &Bm);
+    *bn = g.bn;
+    return *err == PIC_OK ? Bm : nullptr;
+  }
+  // a7 / a8-down: h += A·Bᵀ in the epilogue of an unsplit GEMM (*splits_out = 0), else split-K partials
+  // for the residual kernel.  Not under tensor parallelism (the partials are all-reduced first).
+  pic_status gemm_resid(const CUtensorMap& A, const CUtensorMap* B3, int M, int N, int K, float* h, int* splits_out,
+                        const void* A_ptr, const void* B_ptr) {
+    int bn = 0;
+    pic_status err;
+    const CUtensorMap* Bm = e->tp_size == 1 ? fused_map(B3, B_ptr, M, N, K, false, &bn, &err) : nullptr;
+    if (e->tp_size == 1) TRY(err);
+    if (!Bm) return gemm(A, B3, M, N, K, splits_out, A_ptr, B_ptr);
+    *splits_out = 0;
+    ++launches;
+    PROF("gemm", (double)N * K * 2, 2.0 * M * N * K, launch_gemm_resid(A, *Bm, h, M, N, K, bn, st));
+    return PIC_OK;
+  }
+  // a5: QKV projection with RoPE + scatter in the epilogue of an unsplit GEMM (*fused = true), else
+  // split-K partials for qkv_rope_scatter.
+  pic_status gemm_qkv(const CUtensorMap& A, const CUtensorMap* B3, int M, int N, int K, const GemmEpi& ep,
+                      int* splits_out, bool* fused, const void* A_ptr, const void* B_ptr) {
+    int bn = 0;
+    pic_status err;
+    const CUtensorMap* Bm = e->cfg.head_dim == 128 ? fused_map(B3, B_ptr, M, N, K, true, &bn, &err) : nullptr;
+    if (e->cfg.head_dim == 128) TRY(err);
+    *fused = Bm != nullptr;
+    if (!Bm) return gemm(A, B3, M, N, K, splits_out, A_ptr, B_ptr);
+    *splits_out = 1;
+    ++launches;
+    PROF("gemm", (double)N * K * 2, 2.0 * M * N * K, launch_gemm_qkv(A, *Bm, ep, M, N, K, bn, st));
+    return PIC_OK;
+  }
 };
 
 // Enqueue the whole forward on `st`.  Plan arrays are already on the device at the given pointers.
@@ -1148,12 +1195,14 @@ static pic_status enqueue_forward(pic_engine* e, const Fwd& f, const DevPlan& dp
                          c.d_model <= 4096 &&
                          f.M > 0;
   bool qkv_done = false;  // this layer's QKV partials were produced by the previous layer's chain
+  bool qkv_fused = false;  // this layer's RoPE + scatter ran in the QKV GEMM's epilogue
   int s_chain_qkv = 0;
   for (int l = 0; l < L; ++l) {
     const LayerW& w = e->layers[l];
     char* Kl = Kp + l * lbytes;
     char* Vl = Vp + l * lbytes;
     int s = 0;
+    qkv_fused = false;
     if (qkv_done) {
       s = s_chain_qkv;
       qkv_done = false;
@@ -1161,7 +1210,12 @@ static pic_status enqueue_forward(pic_engine* e, const Fwd& f, const DevPlan& dp
       ++R.launches;
       TRY(add_norm(prevP, prev_s, w.g1, e->x, nullptr, M, (double)M * d * 2));
       if (l > 0) TRY(capture(l - 1));
-      TRY(R.gemm(e->tm_x, w.tm_qkv, M, qkv, d, &s, e->x, w.qkv));
+      if (f.cb && l == f.cb_layer) {  // CacheBlend's check needs the partials of all N rows
+        TRY(R.gemm(e->tm_x, w.tm_qkv, M, qkv, d, &s, e->x, w.qkv));
+      } else {
+        const GemmEpi ep{pos, slot, e->cos_t, e->sin_t, e->Q, Kl, Vl, Hq, Hkv};
+        TRY(R.gemm_qkv(e->tm_x, w.tm_qkv, M, qkv, d, ep, &s, &qkv_fused, e->x, w.qkv));
+      }
     }
     // CacheBlend: the side-stream K2 covers every cached row (the selection is device-side), including
     // the rows this layer's scatter rewrites, so it must land before the scatter, not just before attention
@@ -1188,7 +1242,7 @@ static pic_status enqueue_forward(pic_engine* e, const Fwd& f, const DevPlan& dp
       tiles = dp.tiles2;
       n_tiles = dp.n_tiles2;
       head_map = dp.head_map2;
-    } else {
+    } else if (!qkv_fused) {
       ++R.launches;
       PROF("qkv_rope_scatter", (double)M * qkv * 4 * s + (double)M * qkv * 2, 0, launch_qkv_rope_scatter(e->ws, s, M, nullptr, pos, slot, e->cos_t, e->sin_t, e->Q, Kl, Vl, M, Hq, Hkv, D,
                                  st, e->f32, pos == dp.pos ? 1 : 0));
@@ -1238,13 +1292,17 @@ static pic_status enqueue_forward(pic_engine* e, const Fwd& f, const DevPlan& dp
       g_attn_trace_ctas = a.n_work * Hkv;
       a.o_part = e->o_part;
       a.ml_part = e->ml_part;
-      R.launches += 2;
+      const bool main_tiles = tiles == dp.tiles;
+      a.row_nsplit = main_tiles ? dp.attn_nsplit : dp.attn_nsplit2;
+      a.O = e->Obuf;  // unsplit q-tiles write their normalised bf16 output here directly
+      const int max_split = main_tiles ? f.attn_max_split : f.attn_max_split2;
+      ++R.launches;
       PROF("attention", attn_bytes, attn_flops, launch_attention_tc(e->tm_Q, e->tm_K, e->tm_V, e->tm_K8, e->tm_V8, a, st));
-      PROF("attn_combine", (double)((tiles == dp.tiles) ? f.attn_max_split : f.attn_max_split2) * M * Hq * D * 4 +
-                                 (double)M * Hq * D * 2,
-           0,
-           launch_attn_combine(e->o_part, e->ml_part, (tiles == dp.tiles) ? dp.attn_nsplit : dp.attn_nsplit2, e->Obuf,
-                               M, Hq, D, st));
+      if (max_split > 1) {  // merge the split-KV partials of the split rows only
+        ++R.launches;
+        PROF("attn_combine", (double)max_split * M * Hq * D * 4 + (double)M * Hq * D * 2, 0,
+             launch_attn_combine(e->o_part, e->ml_part, a.row_nsplit, e->Obuf, M, Hq, D, st));
+      }
     } else {
       ++R.launches;
       PROF("attention", attn_bytes, attn_flops, launch_attention_simt(e->Q, Kl, Vl, dp.seq, dp.seq_bt_off, dp.bt, pos, e->Obuf, M, Hq, Hkv, D,
@@ -1314,9 +1372,9 @@ static pic_status enqueue_forward(pic_engine* e, const Fwd& f, const DevPlan& dp
       continue;
     }
     // a7 O projection, residual + a8 MLP
-    TRY(R.gemm(e->tm_O, w.tm_o, M, d, Hq * D, &s, e->Obuf, w.o));
+    TRY(R.gemm_resid(e->tm_O, w.tm_o, M, d, Hq * D, hc, &s, e->Obuf, w.o));
     ++R.launches;
-    TRY(add_norm(e->ws, s, w.g2, e->x, nullptr, M, (double)M * d * 2));
+    TRY(add_norm(s ? e->ws : nullptr, s, w.g2, e->x, nullptr, M, (double)M * d * 2));
     if (e->gu_group > 0) {
       ++R.launches;
       const bool pair = swiglu_pair(e, M, 2 * F);
@@ -1329,8 +1387,8 @@ static pic_status enqueue_forward(pic_engine* e, const Fwd& f, const DevPlan& dp
       ++R.launches;
       PROF("swiglu", (double)M * 2 * F * 4 * s + (double)M * F * 2, 0, launch_swiglu(e->ws, s, e->u, M, F, st, e->f32));
     }
-    TRY(R.gemm(e->tm_u, w.tm_down, M, d, F, &s, e->u, w.down));
-    prevP = e->ws;
+    TRY(R.gemm_resid(e->tm_u, w.tm_down, M, d, F, hc, &s, e->u, w.down));
+    prevP = s ? e->ws : nullptr;
     prev_s = s;
   }
   if (!f.compile) {

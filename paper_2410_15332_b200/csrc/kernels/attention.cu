@@ -437,9 +437,16 @@ __global__ void __launch_bounds__(ROT ? 320 + 32 * kRotWarps : 320, 1)
     }
     if (tr && threadIdx.x == 64) tr[5] = globaltimer();
     const size_t idx = ((size_t)split * a.M + row) * a.Hq + head;
+    // row sum = both halves' partial sums (parity slot n&1 was last read at tile n-2)
+    xmax[((n & 1) * 2 + hc) * 128 + r] = l;
+    named_bar_sync(1 + q, 64);
+    const float l_row = l + xmax[((n & 1) * 2 + (hc ^ 1)) * 128 + r];
+    // an unsplit q-tile is final here: normalise and write bf16 O (no partials, no combine)
+    const bool direct = a.row_nsplit[row_start] == 1;
     if (n > 0) {
       // every MMA has completed, so the K ring is idle: stage this warp's [32 rows][64 cols] fp32
-      // O slice there (XOR-swizzled float4 slots) and store full 256-B row segments
+      // O slice there (XOR-swizzled float4 slots) and store full row segments
+      const float inv = direct ? 1.f / l_row : 1.f;
       float4* stg = reinterpret_cast<float4*>(smem + kK + (warp - 2) * 8192);
 #pragma unroll 1
       for (int c = 0; c < 2; ++c) {
@@ -447,27 +454,31 @@ __global__ void __launch_bounds__(ROT ? 320 + 32 * kRotWarps : 320, 1)
         tmem_ld32(oAddr + c * 32, ov);  // warp-collective
 #pragma unroll
         for (int i = 0; i < 8; ++i)
-          stg[lane * 16 + ((c * 8 + i) ^ (lane & 7))] = make_float4(ov[4 * i], ov[4 * i + 1], ov[4 * i + 2], ov[4 * i + 3]);
+          stg[lane * 16 + ((c * 8 + i) ^ (lane & 7))] =
+              make_float4(ov[4 * i] * inv, ov[4 * i + 1] * inv, ov[4 * i + 2] * inv, ov[4 * i + 3] * inv);
       }
       __syncwarp();
       const int jj = lane & 15;
 #pragma unroll 4
       for (int i = 0; i < 16; ++i) {
         const int rr = 2 * i + (lane >> 4), rm = q * 32 + rr, qi2 = rm / G;
-        if (qi2 < row_count)
-          reinterpret_cast<float4*>(a.o_part + (((size_t)split * a.M + row_start + qi2) * a.Hq + g * G + rm % G) * 128 +
-                                    hc * 64)[jj] = stg[rr * 16 + (jj ^ (rr & 7))];
+        if (qi2 < row_count) {
+          const float4 v = stg[rr * 16 + (jj ^ (rr & 7))];
+          const size_t orow = ((size_t)(row_start + qi2) * a.Hq + g * G + rm % G) * 128 + hc * 64;
+          if (direct)
+            reinterpret_cast<uint2*>(reinterpret_cast<uint16_t*>(a.O) + orow)[jj] =
+                make_uint2(pack_bf16(v.x, v.y), pack_bf16(v.z, v.w));
+          else
+            reinterpret_cast<float4*>(a.o_part + (size_t)split * a.M * a.Hq * 128 + orow)[jj] = v;
+        }
       }
     } else if (valid) {
       float4* dst = reinterpret_cast<float4*>(a.o_part + idx * 128 + hc * 64);
       for (int i = 0; i < 16; ++i) dst[i] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
-    // row sum = both halves' partial sums (parity slot n&1 was last read at tile n-2)
-    xmax[((n & 1) * 2 + hc) * 128 + r] = l;
-    named_bar_sync(1 + q, 64);
-    if (valid && hc == 0) {
+    if (valid && hc == 0 && !direct) {
       a.ml_part[2 * idx] = m_ref;
-      a.ml_part[2 * idx + 1] = l + xmax[((n & 1) * 2 + 1) * 128 + r];
+      a.ml_part[2 * idx + 1] = l_row;
     }
     if (tr && threadIdx.x == 64) tr[6] = globaltimer();
   }
@@ -591,7 +602,7 @@ __global__ void attn_combine_kernel(const float* __restrict__ o_part, const floa
   // the split counts are host-built plan data: read them while the attention kernel drains
   const int n_splits = wid < M * Hq ? row_nsplit[wid / Hq] : 0;
   griddep_wait();
-  if (wid >= M * Hq) return;
+  if (wid >= M * Hq || n_splits <= 1) return;  // unsplit rows were written by the attention kernel
   const size_t stride = (size_t)M * Hq;
   float ms = -INFINITY, ls = 0.f;
   if (lane < n_splits) {

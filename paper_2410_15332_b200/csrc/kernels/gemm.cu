@@ -29,7 +29,27 @@ namespace pic {
 __constant__ int c_weight_evict_first = 0;
 __device__ __forceinline__ bool weight_evict_first() { return c_weight_evict_first != 0; }
 
-enum { EPI_PARTIAL = 0, EPI_SWIGLU = 1 };
+enum { EPI_PARTIAL = 0, EPI_SWIGLU = 1, EPI_RESID = 2, EPI_QKV = 3 };
+
+// EPI_QKV (split-K = 1, 128-column head tiles): a5's RoPE + scatter on the accumulator (P:213 steps
+// 2-3, the qkv_rope_scatter arithmetic): Q heads rotated at p_row -> dense Q; K heads rotated -> pool
+// slot of the row; V heads -> pool slot.  NeoX pairs (j, j+64) of a head sit in TMEM columns c and
+// c + 64 of the same thread's row.
+PIC_DEV void rope_pack16(const float* a, const float* b, const float* cs, const float* sn, uint4* oa, uint4* ob) {
+  uint32_t pa[8], pb[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    float ra0, rb0, ra1, rb1;
+    rope_pair(a[2 * j], b[2 * j], cs[2 * j], sn[2 * j], ra0, rb0);
+    rope_pair(a[2 * j + 1], b[2 * j + 1], cs[2 * j + 1], sn[2 * j + 1], ra1, rb1);
+    pa[j] = pack_bf16(ra0, ra1);
+    pb[j] = pack_bf16(rb0, rb1);
+  }
+  oa[0] = make_uint4(pa[0], pa[1], pa[2], pa[3]);
+  oa[1] = make_uint4(pa[4], pa[5], pa[6], pa[7]);
+  ob[0] = make_uint4(pb[0], pb[1], pb[2], pb[3]);
+  ob[1] = make_uint4(pb[4], pb[5], pb[6], pb[7]);
+}
 
 template <int BN, int STAGES, int CL = 1>
 struct GemmSmem {
@@ -60,7 +80,7 @@ __global__ void __launch_bounds__(192, 1)
     gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      void* __restrict__ out_, int M, int N, int kblk_total, int kblk_per_split, int splits,
                      int pack, unsigned long long* trace, const __grid_constant__ CUtensorMap tmN,
-                     GemmNext nx) {
+                     GemmNext nx, const GemmEpi ep) {
   using S = GemmSmem<BN, STAGES>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw;
@@ -215,11 +235,20 @@ __global__ void __launch_bounds__(192, 1)
       const bool stage = u + (int)gridDim.x >= units;
       uint8_t* stg = smem + (size_t)(warp - 2) * ((BN + 31) / 32) * 4096;
       const int mrow0 = m0 + q * 32;
-      if constexpr (EPI == EPI_PARTIAL) {
+      if constexpr (EPI == EPI_PARTIAL || EPI == EPI_RESID) {
+        // EPI_RESID (split-K = 1): out = the fp32 residual h, h += acc (the a7/a8 residual add: the same
+        // fp32 addition the residual kernel applies to a single partial)
         const int sp = (u / mt) % splits;
         float* obase = reinterpret_cast<float*>(out_) + (size_t)sp * M * N;
         float* orow = obase + (size_t)row * N;
         const int ncol = min(BN, N - n0);  // multiple of 16
+        auto put4 = [&](float* dst, float4 v) {
+          if constexpr (EPI == EPI_RESID) {
+            const float4 h = *reinterpret_cast<const float4*>(dst);
+            v = make_float4(h.x + v.x, h.y + v.y, h.z + v.z, h.w + v.w);
+          }
+          *reinterpret_cast<float4*>(dst) = v;
+        };
         if (nkb > 0 && stage) {
 #pragma unroll 1
           for (int c = 0; c < BN; c += 32) {
@@ -235,7 +264,7 @@ __global__ void __launch_bounds__(192, 1)
             for (int i = 0; i < 8; ++i) {
               const int r = i * 4 + (lane >> 3);
               if (mrow0 + r < M && c + 4 * jj < ncol)
-                *reinterpret_cast<float4*>(obase + (size_t)(mrow0 + r) * N + n0 + c + 4 * jj) = sb[r * 8 + (jj ^ (r & 7))];
+                put4(obase + (size_t)(mrow0 + r) * N + n0 + c + 4 * jj, sb[r * 8 + (jj ^ (r & 7))]);
             }
           }
         } else if (nkb > 0) {
@@ -247,12 +276,63 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll
               for (int j = 0; j < 8; ++j)
                 if (c + 4 * j < ncol)
-                  reinterpret_cast<float4*>(orow + n0 + c)[j] =
-                      make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+                  put4(orow + n0 + c + 4 * j, make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]));
           }
-        } else if (row < M) {
+        } else if (row < M && EPI == EPI_PARTIAL) {
           for (int col = n0; col < n0 + ncol; col += 4)
             *reinterpret_cast<float4*>(orow + col) = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      } else if constexpr (EPI == EPI_QKV) {
+        // every lane runs the (warp-collective) TMEM loads; rows beyond M only skip their stores
+        const bool ok = row < M;
+        const int p = ok ? ep.pos[row] : 0, sl = ok ? ep.slot[row] : 0;
+        const float* cp = ep.cos_t + (size_t)p * 64;
+        const float* spn = ep.sin_t + (size_t)p * 64;
+        const size_t kv_base = ((size_t)(sl / 16) * ep.Hkv) * 16 * 128 + (size_t)(sl % 16) * 128;
+#pragma unroll 1
+        for (int hh = 0; hh < BN / 128; ++hh) {
+          const int hd = (n0 >> 7) + hh;  // warp-uniform
+          if (hd >= ep.Hq + 2 * ep.Hkv) break;
+          const uint32_t th = tl + hh * 128;
+          if (hd < ep.Hq + ep.Hkv) {
+            uint16_t* dst = hd < ep.Hq ? reinterpret_cast<uint16_t*>(ep.Q) + ((size_t)row * ep.Hq + hd) * 128
+                                       : reinterpret_cast<uint16_t*>(ep.Kl) + kv_base + (size_t)(hd - ep.Hq) * 16 * 128;
+#pragma unroll 1
+            for (int c = 0; c < 64; c += 16) {
+              float a[16], b[16], cs[16], sn[16];
+              tmem_ld16(th + c, a);
+              tmem_ld16(th + 64 + c, b);
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                const float4 c4 = *reinterpret_cast<const float4*>(cp + c + 4 * j);
+                const float4 s4 = *reinterpret_cast<const float4*>(spn + c + 4 * j);
+                cs[4 * j] = c4.x, cs[4 * j + 1] = c4.y, cs[4 * j + 2] = c4.z, cs[4 * j + 3] = c4.w;
+                sn[4 * j] = s4.x, sn[4 * j + 1] = s4.y, sn[4 * j + 2] = s4.z, sn[4 * j + 3] = s4.w;
+              }
+              uint4 oa[2], ob[2];
+              rope_pack16(a, b, cs, sn, oa, ob);
+              if (ok) {
+                reinterpret_cast<uint4*>(dst + c)[0] = oa[0];
+                reinterpret_cast<uint4*>(dst + c)[1] = oa[1];
+                reinterpret_cast<uint4*>(dst + 64 + c)[0] = ob[0];
+                reinterpret_cast<uint4*>(dst + 64 + c)[1] = ob[1];
+              }
+            }
+          } else {
+            uint16_t* dst = reinterpret_cast<uint16_t*>(ep.Vl) + kv_base + (size_t)(hd - ep.Hq - ep.Hkv) * 16 * 128;
+#pragma unroll 1
+            for (int c = 0; c < 128; c += 32) {
+              float v[32];
+              tmem_ld32(th + c, v);
+              uint32_t pk[16];
+#pragma unroll
+              for (int j = 0; j < 16; ++j) pk[j] = pack_bf16(v[2 * j], v[2 * j + 1]);
+              if (ok)
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                  reinterpret_cast<uint4*>(dst + c)[j] = make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+            }
+          }
         }
       } else {
         constexpr int G = BN / 2;
@@ -320,7 +400,7 @@ __global__ void __launch_bounds__(192, 1)
     gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      void* __restrict__ out_, int M, int N, int kblk_total, int kblk_per_split, int splits,
                      int pack, unsigned long long* trace, const __grid_constant__ CUtensorMap tmN,
-                     GemmNext nx) {
+                     GemmNext nx, const GemmEpi ep) {
   using S = GemmSmem<BN, STAGES, CL>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw;
@@ -661,7 +741,7 @@ GemmNext gemm_next(const CUtensorMap* B, int M, int N, int K, int splits, int bn
 
 template <int BN, int EPI, int CL = 1>
 static cudaError_t launch_gemm_t(const CUtensorMap& A, const CUtensorMap& B, void* out, int M, int N, int K, int splits,
-                                 int pack, cudaStream_t st, const GemmNext& nx) {
+                                 int pack, cudaStream_t st, const GemmNext& nx, const GemmEpi& ep = GemmEpi{}) {
   constexpr int ST = gemm_stages(BN, CL);
   using S = GemmSmem<BN, ST, CL>;
   auto kern = [] {
@@ -677,7 +757,7 @@ static cudaError_t launch_gemm_t(const CUtensorMap& A, const CUtensorMap& B, voi
   const int grid = CL * (units < max_cl ? units : max_cl);  // persistent: one CTA (pair) per SM (pair)
   if constexpr (CL == 1) {
     CUDA_TRY_LAUNCH(launch_k(kern, dim3(grid), dim3(192), S::kBytes, st, A, B, out, M, N, kblk, per, splits, pack,
-                             g_gemm_trace, nx.tm ? *nx.tm : B, nx));
+                             g_gemm_trace, nx.tm ? *nx.tm : B, nx, ep));
   } else {
     if (pack) return cudaErrorInvalidValue;
     cudaLaunchConfig_t cfg = {};
@@ -696,7 +776,7 @@ static cudaError_t launch_gemm_t(const CUtensorMap& A, const CUtensorMap& B, voi
     cfg.numAttrs = 2;
     unsigned long long* tr = nullptr;
     const CUtensorMap tn = nx.tm ? *nx.tm : B;
-    CUDA_TRY_LAUNCH(cudaLaunchKernelEx(&cfg, kern, A, B, out, M, N, kblk, per, splits, pack, tr, tn, nx));
+    CUDA_TRY_LAUNCH(cudaLaunchKernelEx(&cfg, kern, A, B, out, M, N, kblk, per, splits, pack, tr, tn, nx, ep));
   }
   return cudaGetLastError();
 }
@@ -716,6 +796,9 @@ static cudaError_t prep_t() {
 #define PIC_SWIGLU_BNS(X) X(32) X(64) X(128) X(224) X(256)
 // CTA-pair (cta_group::2) instantiations: N-tiles of the tensor-bound multi-m-tile GEMMs
 #define PIC_PAIR_BNS(X) X(128) X(192) X(224) X(256)
+// fused-epilogue instantiations: residual add (any multi-m-tile N-tile), RoPE + scatter (whole heads)
+#define PIC_RESID_BNS(X) X(128) X(144) X(160) X(176) X(192) X(208) X(224) X(256)
+#define PIC_QKV_BNS(X) X(128) X(256)
 
 cudaError_t prepare_gemm() {
   cudaError_t e = cudaSuccess;
@@ -731,6 +814,14 @@ cudaError_t prepare_gemm() {
   PIC_SWIGLU_BNS(P2)
 #undef P1
 #undef P2
+#define P4(bn) \
+  if (e == cudaSuccess) e = prep_t<bn, EPI_RESID>();
+#define P5(bn) \
+  if (e == cudaSuccess) e = prep_t<bn, EPI_QKV>();
+  PIC_RESID_BNS(P4)
+  PIC_QKV_BNS(P5)
+#undef P4
+#undef P5
 #define P3(bn)                                                   \
   if (e == cudaSuccess) e = prep_t<bn, EPI_PARTIAL, 2>();        \
   if (e == cudaSuccess) e = prep_t<bn, EPI_SWIGLU, 2>();
@@ -743,6 +834,36 @@ bool gemm_pair_supported(int bn) {
 #define C1(b) || bn == b
   return false PIC_PAIR_BNS(C1);
 #undef C1
+}
+
+bool gemm_resid_supported(int bn) {
+#define C1(b) || bn == b
+  return false PIC_RESID_BNS(C1);
+#undef C1
+}
+
+cudaError_t launch_gemm_resid(const CUtensorMap& A, const CUtensorMap& B, float* h, int M, int N, int K, int bn,
+                              cudaStream_t st, const GemmNext& nx) {
+  switch (bn) {
+#define L5(b) \
+  case b:     \
+    return launch_gemm_t<b, EPI_RESID>(A, B, h, M, N, K, 1, 0, st, nx);
+    PIC_RESID_BNS(L5)
+#undef L5
+  }
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_gemm_qkv(const CUtensorMap& A, const CUtensorMap& B, const GemmEpi& ep, int M, int N, int K, int bn,
+                            cudaStream_t st, const GemmNext& nx) {
+  switch (bn) {
+#define L6(b) \
+  case b:     \
+    return launch_gemm_t<b, EPI_QKV>(A, B, nullptr, M, N, K, 1, 0, st, nx, ep);
+    PIC_QKV_BNS(L6)
+#undef L6
+  }
+  return cudaErrorInvalidValue;
 }
 
 bool gemm_bn_supported(int bn, bool swiglu) {

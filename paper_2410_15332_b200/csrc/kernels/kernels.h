@@ -86,12 +86,32 @@ struct GemmNext {
   int units, mt, splits, kper, kblk_total, bn, pfk;
 };
 GemmNext gemm_next(const CUtensorMap* B, int M, int N, int K, int splits, int bn, int pfk);
+// Fused a5 epilogue (EPI_QKV): per output row its position and pool slot, the RoPE tables, the dense Q
+// output [M][Hq][128] and this layer's K / V pools ([blocks][Hkv][16][128]).
+struct GemmEpi {
+  const int32_t* pos;
+  const int32_t* slot;
+  const float* cos_t;
+  const float* sin_t;
+  void* Q;
+  void* Kl;
+  void* Vl;
+  int Hq, Hkv;
+};
 // pair = 1: CTA-pair (cta_group::2) kernel with 256-row M-tiles; B's tensor map box must then be bn/2 rows
 // (each CTA of the pair loads half of the N-tile); bn in gemm_pair_supported().
 cudaError_t launch_gemm_partial(const CUtensorMap& A, const CUtensorMap& B, float* out, int M, int N, int K,
                                 int splits, int bn, cudaStream_t st, int pack = 0, const GemmNext& nx = GemmNext{},
                                 int pair = 0);
 bool gemm_pair_supported(int bn);
+// Split-K = 1 GEMMs with the consumer fused into the epilogue (tensor-bound shapes, no partials):
+//   resid: h[M][N] += A·Bᵀ (a7 O projection / a8 down projection + residual add, fp32 h)
+//   qkv:   A·W_qkvᵀ -> RoPE at pos -> Q dense, K/V -> pool slots (a5); bn = 128 or 256 (whole heads)
+cudaError_t launch_gemm_resid(const CUtensorMap& A, const CUtensorMap& B, float* h, int M, int N, int K, int bn,
+                              cudaStream_t st, const GemmNext& nx = GemmNext{});
+cudaError_t launch_gemm_qkv(const CUtensorMap& A, const CUtensorMap& B, const GemmEpi& ep, int M, int N, int K,
+                            int bn, cudaStream_t st, const GemmNext& nx = GemmNext{});
+bool gemm_resid_supported(int bn);
 // Gate/up GEMM with the SwiGLU epilogue fused: B = interleaved [gate|up] groups of bn/2 rows (N2 = 2F rows),
 // u[M][F] bf16 = silu(x·W_gᵀ) ⊙ (x·W_uᵀ).  Split-K 1.
 cudaError_t launch_gemm_swiglu(const CUtensorMap& A, const CUtensorMap& B, void* u, int M, int N2, int K, int bn,
@@ -150,6 +170,10 @@ struct AttnArgs {
   const int32_t* bdelta;
   const float* cos_t;        // [max_pos][64] fp32 RoPE table (re-base angles |Δ|·θ_j)
   const float* sin_t;
+  // Rows of a q-tile the schedule did not split (row_nsplit[row] == 1) are normalised in the kernel and
+  // written as bf16 to O [M][Hq][128] directly; split rows leave fp32 partials for attn_combine.
+  const int32_t* row_nsplit;
+  void* O;
 };
 // Balanced split-KV schedule: each q-tile t (KV extent n_kv[t] 128-key tiles) gets
 // ceil(n_kv[t] / budget) splits, budget = ceil(Σ n_kv · Hkv / target_ctas); splits <= 32.

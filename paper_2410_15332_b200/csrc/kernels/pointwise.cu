@@ -392,9 +392,13 @@ __global__ void __launch_bounds__(128) qkv_rope_scatter_kernel(
     const float4 b = sum_splits4(P4, splits, stride4, col4 + half / 4);
     void* dst = hd < Hq ? Q : Kp;
     const size_t o = hd < Hq ? ((size_t)r * Hq + hd) * D : kv_base + (size_t)(hd - Hq) * 16 * D;
-    store4<F32>(dst, o + j, a.x * c.x - b.x * s.x, a.y * c.y - b.y * s.y, a.z * c.z - b.z * s.z, a.w * c.w - b.w * s.w);
-    store4<F32>(dst, o + j + half, b.x * c.x + a.x * s.x, b.y * c.y + a.y * s.y, b.z * c.z + a.z * s.z,
-                b.w * c.w + a.w * s.w);
+    float ra[4], rb[4];
+    rope_pair(a.x, b.x, c.x, s.x, ra[0], rb[0]);
+    rope_pair(a.y, b.y, c.y, s.y, ra[1], rb[1]);
+    rope_pair(a.z, b.z, c.z, s.z, ra[2], rb[2]);
+    rope_pair(a.w, b.w, c.w, s.w, ra[3], rb[3]);
+    store4<F32>(dst, o + j, ra[0], ra[1], ra[2], ra[3]);
+    store4<F32>(dst, o + j + half, rb[0], rb[1], rb[2], rb[3]);
   } else {
     const int u = t - n_rope;
     const int hd = u / (D / 4), j = (u % (D / 4)) * 4;

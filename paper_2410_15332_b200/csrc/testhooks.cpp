@@ -162,6 +162,8 @@ extern "C" pic_status pic_test_attention(const uint16_t* Q, const uint16_t* K, c
   a.o_part = reinterpret_cast<float*>(dop.p);
   a.ml_part = reinterpret_cast<float*>(dml.p);
   a.Q = dq.p;
+  a.row_nsplit = reinterpret_cast<int32_t*>(dns.p);
+  a.O = dout.p;
   TCK(launch_attention_tc(tq, tk, tv, tk8, tv8, a, 0));
   TCK(launch_attn_combine(a.o_part, a.ml_part, reinterpret_cast<int32_t*>(dns.p), dout.p, M, Hq, D, 0));
   TCK(cudaDeviceSynchronize());
