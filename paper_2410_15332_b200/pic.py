@@ -314,7 +314,10 @@ class Engine:
         if self._h:
             lib().pic_engine_destroy(self._h)
             self._h = C.c_void_p()
-        self.arena = None
+        if self.arena is not None:
+            import torch
+            self.arena = None
+            torch.cuda.empty_cache()   # hand the arena back to the device, not just to torch's cache
 
     def __del__(self):
         try:

@@ -17,3 +17,16 @@ def pytest_collection_modifyitems(config, items):
     # GPU tests fail loudly (not skip) when selected without a GPU: the driver runs
     # `-m gpu` only on a B200 box.
     pass
+
+
+@pytest.fixture(autouse=True)
+def _release_device_memory():
+    """GPU tests build engines with arenas of tens of GB: after each test, return what torch's caching
+    allocator still holds to the device, so later tests (and the spawned tensor-parallel ranks) see it."""
+    yield
+    if "torch" in sys.modules:
+        import gc
+        torch = sys.modules["torch"]
+        gc.collect()
+        if torch.cuda.is_available() and torch.cuda.is_initialized():
+            torch.cuda.empty_cache()
