@@ -33,6 +33,13 @@ pic_status pic_test_attention(const uint16_t* Q, const uint16_t* K, const uint16
                               int32_t M, int32_t n_keys, int32_t Hq, int32_t Hkv, const int32_t* block_perm,
                               int32_t num_blocks, int32_t n_splits, uint16_t* O);
 
+/* As pic_test_attention with the kernel chosen: version 1 = one q-tile per CTA (attention.cu), 2 = the
+ * persistent ping-pong kernel (attention_pp.cu, the engine's default); grid > 0 caps the persistent grid
+ * (several items per CTA), 0 = 148.  pic_test_attention = version 2, grid 0. */
+pic_status pic_test_attention_v(const uint16_t* Q, const uint16_t* K, const uint16_t* V, const int32_t* pos,
+                                int32_t M, int32_t n_keys, int32_t Hq, int32_t Hkv, const int32_t* block_perm,
+                                int32_t num_blocks, int32_t n_splits, int32_t version, int32_t grid, uint16_t* O);
+
 /* a2 KV link on a raw pool: pool K/V [n_layers][num_blocks][Hkv][16][D] bf16 (in/out), rows
  * (src_slot -> dst_slot, delta) for layers layer0..n_layers-1, RoPE table for positions < max_pos. */
 pic_status pic_test_kv_link(uint16_t* Kpool, uint16_t* Vpool, int32_t n_layers, int32_t num_blocks, int32_t Hkv,

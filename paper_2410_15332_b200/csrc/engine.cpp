@@ -200,6 +200,12 @@ static bool wave_fit() {
   return on;
 }
 
+// a6 on the persistent ping-pong kernel (attention_pp.cu); PIC_ATTN_V1=1: the one-lane kernel (A/B only)
+static bool attn_pp_enabled() {
+  static const bool on = getenv("PIC_ATTN_V1") == nullptr;
+  return on;
+}
+
 static bool chain_enabled() {
   static const bool on = getenv("PIC_CHAIN") != nullptr;
   return on;
@@ -343,7 +349,7 @@ static ArenaPlan plan_arena(const pic_model_config& c, const pic_engine_limits& 
   // per-row arrays (tok,pos,slot,seq,head) + tiles + seq offsets + bt + k2 (3) + CB (cand,forced,sel2,pos2,slot2,
   // keep,count) + tiles2 + head2
   a.plan_ints = 5 * M + 3 * (size_t)a.max_tiles + a.max_seqs + 2 * (size_t)a.max_bt /* bt, bdelta */ + 3 * (size_t)a.max_k2 +
-                7 * (size_t)l.max_tokens + 3 * (size_t)a.max_tiles + M + 4096;
+                7 * (size_t)l.max_tokens + 8 * (size_t)a.max_tiles + M + 8192;  /* + attention items (8 ints) */
   a.off_plan = L.add(a.plan_ints * 4);
   // tensor parallel: two reduced-partial buffers (alternating per all-reduce), flags, epoch counter
   a.off_ar = L.add(2 * M * d * 4);
@@ -1297,7 +1303,11 @@ static pic_status enqueue_forward(pic_engine* e, const Fwd& f, const DevPlan& dp
       a.O = e->Obuf;  // unsplit q-tiles write their normalised bf16 output here directly
       const int max_split = main_tiles ? f.attn_max_split : f.attn_max_split2;
       ++R.launches;
-      PROF("attention", attn_bytes, attn_flops, launch_attention_tc(e->tm_Q, e->tm_K, e->tm_V, e->tm_K8, e->tm_V8, a, st));
+      if (f.attn_pp)
+        PROF("attention", attn_bytes, attn_flops,
+             launch_attention_pp(e->tm_Q, e->tm_K, e->tm_V, e->tm_K8, e->tm_V8, a, 148, st));
+      else
+        PROF("attention", attn_bytes, attn_flops, launch_attention_tc(e->tm_Q, e->tm_K, e->tm_V, e->tm_K8, e->tm_V8, a, st));
       if (max_split > 1) {  // merge the split-KV partials of the split rows only
         ++R.launches;
         PROF("attn_combine", (double)max_split * M * Hq * D * 4 + (double)M * Hq * D * 2, 0,
@@ -1408,7 +1418,7 @@ static pic_status enqueue_forward(pic_engine* e, const Fwd& f, const DevPlan& dp
 static void add_sig(std::vector<int64_t>& sig, const Fwd& f, const DevPlan& dp) {
   sig = {f.M,  dp.n_tiles, (int64_t)f.seq_bt_off.size(), (int64_t)f.bt.size(), (int64_t)f.k2_src.size(), f.k2_layer0,
          f.n_head, f.compile, f.rebase, f.cb, f.cb_layer, f.cb_T, f.M2, f.cb_override, dp.n_tiles2, f.attn_n_work,
-         f.attn_n_work2, f.kv_rot};
+         f.attn_n_work2, f.kv_rot, f.attn_pp};
   // attention split choice depends on the per-sequence block-table lengths
   for (size_t q = 0; q < f.seq_bt_off.size(); ++q) sig.push_back(f.seq_bt_off[q]);
 }
@@ -1434,9 +1444,15 @@ static void schedule_attention(pic_engine* e, Fwd& f) {
     for (int v : n_kv) total += v;
     work.assign(4 * (size_t)(total + nt), 0);
     nsplit.assign(M, 1);
+    if (f.attn_pp) {
+      max_split = attn_schedule_pp(tiles.data(), nt, n_kv.data(), Hkv, 148, cap, work, nsplit.data());
+      n_work = (int)work.size() / 8;
+      return;
+    }
     max_split = attn_schedule(tiles.data(), nt, n_kv.data(), Hkv, 148, cap, work.data(), &n_work, nsplit.data());
     work.resize(4 * (size_t)n_work);
   };
+  f.attn_pp = attn_pp_enabled() && e->cfg.head_dim == 128 && !e->f32;
   build(f.tiles, &f.pos, f.M, 0, f.attn_work, f.attn_nsplit, f.attn_n_work, f.attn_max_split);
   if (f.cb) {
     const int N = f.M;  // single request, all rows at layer 0

@@ -1,0 +1,671 @@
+// attention_pp.cu — a6, v2: persistent ping-pong sparse-query attention.
+//
+// Computes the same Eq. (1) as attention.cu (P:215 A = softmax(Q K_expᵀ · MASK), O = A V_exp
+// "allowing the k' tokens to attend to all N tokens"; P:217 causal MASK; reading R3: additive −∞,
+// scale 1/√D), with a different schedule:
+//   * Two query lanes per CTA (A, B).  Each lane is one GQA-packed q-tile (128 MMA rows = 128/G
+//     queries × G heads of kv-head g) and a KV range.  When both lanes belong to the same sequence and
+//     start at the same KV tile, every K/V tile is loaded ONCE and used by both lanes (half the
+//     L2→SMEM traffic per FLOP of the one-lane kernel, which ran at ~half the L2 throughput cap).
+//   * The lanes ping-pong on the tensor core (FA4-style issue order S_A, S_B, PV_A, S_A', PV_B, S_B', …):
+//     while one lane's softmax warpgroup turns S into P, the tensor core runs the other lane's MMAs.
+//   * One thread per MMA row (a warpgroup per lane), the whole 128-key row in registers: the row max
+//     is thread-local (3-input FMNMX), no cross-warp exchange.
+//   * Persistent: 148 CTAs walk a host-sorted item list (longest first); the producer fetches the
+//     next item's Q and K/V while the current item's last softmax and epilogue drain.  O stays in
+//     TMEM (lazy FA4 rescale: only when a row max grows by > 2^8) and unsplit lanes write normalised
+//     bf16 O directly; split lanes leave fp32 partials + (m, l) for attn_combine.
+// TMEM (512 columns): S_A [0,128), S_B [128,256) (P_X overwrites S_X as bf16 pairs), O_A [256,384),
+// O_B [384,512).  SMEM: Q_A, Q_B (64 KB), K ring 3 × 32 KB, V ring 2 × 32 KB (SWIZZLE_128B halves).
+#include <cuda.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "common.cuh"
+#include "kernels.h"
+
+#define CUDA_TRY_LAUNCH(x)              \
+  do {                                 \
+    cudaError_t e__ = (x);             \
+    if (e__ != cudaSuccess) return e__; \
+  } while (0)
+
+namespace pic {
+
+namespace attn2 {
+constexpr int kTile = 16384;  // one [128 rows][64 cols] bf16 SW128 half tile
+constexpr int kKS = 3, kVS = 2;
+constexpr int kQ = 0;                       // Q_A halves, Q_B halves
+constexpr int kK = kQ + 4 * kTile;          // K ring
+constexpr int kV = kK + kKS * 2 * kTile;    // V ring
+constexpr int kBar = kV + kVS * 2 * kTile;  // barriers
+constexpr int bQFull = 0, bQEmpty = 2, bKFull = 4, bKEmpty = bKFull + kKS, bKRot = bKEmpty + kKS,
+              bVFull = bKRot + kKS, bVEmpty = bVFull + kVS, bSFull = bVEmpty + kVS, bPFull = bSFull + 2,
+              bOFull = bPFull + 2, bOFree = bOFull + 2, kNumBars = bOFree + 2;
+constexpr int kSmem = kBar + kNumBars * 8 + 16;
+static_assert(kSmem <= 232448, "attention smem over the 227 KB limit");
+constexpr int kRotWarps = 4;
+}  // namespace attn2
+
+struct PPLane {
+  int tile, j0, n, split, seq, row_start, row_count, max_p;
+};
+
+PIC_DEV float fmax3(float a, float b, float c) {
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+
+// Item `item` of the host list (whole warp): lanes ordered so that A has the longer KV run; `sh`: both
+// lanes read the same K/V tiles (same sequence, same first tile).
+PIC_DEV void pp_lane(const AttnArgs& a, const int* wk, int x, PPLane& p) {
+  p.tile = wk[4 * x];
+  p.j0 = wk[4 * x + 1];
+  p.split = wk[4 * x + 3];
+  if (p.tile < 0) {
+    p.n = 0;
+    p.seq = -1 - x;
+    p.row_start = p.row_count = p.max_p = 0;
+    return;
+  }
+  p.seq = a.tiles[3 * p.tile];
+  p.row_start = a.tiles[3 * p.tile + 1];
+  p.row_count = a.tiles[3 * p.tile + 2];
+  int mp = 0;
+  for (int i = lane_id(); i < p.row_count; i += 32) mp = max(mp, a.row_pos[p.row_start + i]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mp = max(mp, __shfl_xor_sync(0xffffffffu, mp, o));
+  p.max_p = mp;
+  // positions may be device-side (CacheBlend's re-selected rows): clamp the host's range
+  p.n = max(0, min(mp / 128 + 1, wk[4 * x + 2]) - p.j0);
+}
+PIC_DEV void pp_decode(const AttnArgs& a, int item, PPLane& A, PPLane& Bn, int& g, bool& sh) {
+  const int* wk = a.work + 8 * (item / a.Hkv);
+  g = item % a.Hkv;
+  PPLane p0, p1;
+  pp_lane(a, wk, 0, p0);
+  pp_lane(a, wk, 1, p1);
+  const bool sw = p0.n < p1.n;
+  A = sw ? p1 : p0;
+  Bn = sw ? p0 : p1;
+  sh = Bn.n > 0 && A.seq == Bn.seq && A.j0 == Bn.j0;
+}
+
+// position of lane x's step-s K (or V) tile in the item's load order: shared → one tile per step;
+// otherwise A, B alternate while both run, then A alone
+PIC_DEV int pp_tidx(int x, int s, int nB, bool sh) {
+  if (sh) return s;
+  if (s < nB) return 2 * s + x;
+  return 2 * nB + (s - nB);
+}
+
+template <int G, bool ROT>
+__global__ void __launch_bounds__(ROT ? 512 : 384, 1)
+    attn_pp_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                   const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmK8,
+                   const __grid_constant__ CUtensorMap tmV8, const AttnArgs a) {
+  griddep_launch();
+  using namespace attn2;
+  constexpr int SM0 = ROT ? 8 : 4;  // first softmax warp (lane A: SM0..SM0+3, lane B: SM0+4..SM0+7)
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw;
+  if (threadIdx.x == 0 && (smem_u32(smem) & 1023)) __trap();  // SWIZZLE_128B tiles need 1 KB alignment
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kBar);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + kNumBars);
+  const uint32_t base = smem_u32(smem);
+  const uint32_t bar0 = smem_u32(bars);
+  auto B = [&](int i) -> uint32_t { return bar0 + 8 * i; };
+  const int warp = warp_id(), lane = lane_id();
+  if (threadIdx.x == 0) {
+    for (int x = 0; x < 2; ++x) {
+      mbar_init(B(bQFull + x), 1);
+      mbar_init(B(bQEmpty + x), 1);
+      mbar_init(B(bSFull + x), 1);
+      mbar_init(B(bPFull + x), 128);
+      mbar_init(B(bOFull + x), 1);
+      mbar_init(B(bOFree + x), 128);
+    }
+    for (int s = 0; s < kKS; ++s) {
+      mbar_init(B(bKFull + s), 1);
+      mbar_init(B(bKEmpty + s), 1);
+      mbar_init(B(bKRot + s), kRotWarps);
+    }
+    for (int s = 0; s < kVS; ++s) {
+      mbar_init(B(bVFull + s), 1);
+      mbar_init(B(bVEmpty + s), 1);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc(smem_u32(tmem_slot), 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  griddep_wait();  // Q, the recomputed rows' K/V and (CacheBlend) device-side positions come from upstream
+  const int n_items = a.n_work * a.Hkv;
+
+  if (warp < 4) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 56;\n" ::: "memory");
+    if (warp == 0) {
+      // ------------------------------------------------------------------ TMA producer
+      int kc = 0, vc = 0, qc0 = 0, qc1 = 0;
+      if (lane == 0) {
+        tma_prefetch(&tmQ);
+        tma_prefetch(&tmK);
+        tma_prefetch(&tmV);
+        tma_prefetch(&tmK8);
+        tma_prefetch(&tmV8);
+      }
+      // one 128-key K or V tile of (seq, kv tile j): 8 paged blocks, one 8-block box when contiguous
+      auto load_tile = [&](const CUtensorMap* t1, const CUtensorMap* t8, uint32_t dst, uint32_t full, uint32_t empty,
+                           uint32_t ph, const int* bt, int j, int last_blk, int g) {
+        const int kv_base = a.layer * a.num_blocks;
+        const int mine = lane < 8 ? bt[min(j * 8 + lane, last_blk)] : 0;
+        const int b0 = __shfl_sync(0xffffffffu, mine, 0);
+        const bool contig = __all_sync(0xffffffffu, lane >= 8 || mine == b0 + lane);
+        int blk[8];
+#pragma unroll
+        for (int b = 0; b < 8; ++b) blk[b] = __shfl_sync(0xffffffffu, mine, b);
+        if (lane == 0) {
+          mbar_wait(empty, ph ^ 1);
+          mbar_expect_tx(full, 2 * kTile);
+          if (contig) {
+            for (int h = 0; h < 2; ++h) tma_load_4d(dst + h * kTile, t8, full, h * 64, 0, g, kv_base + b0);
+          } else {
+#pragma unroll
+            for (int b = 0; b < 8; ++b)
+              for (int h = 0; h < 2; ++h) tma_load_4d(dst + h * kTile + b * 2048, t1, full, h * 64, 0, g, kv_base + blk[b]);
+          }
+        }
+        __syncwarp();
+      };
+      for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+        PPLane LA, LB;
+        int g;
+        bool sh;
+        pp_decode(a, item, LA, LB, g, sh);
+        const int nA = LA.n, nB = LB.n;
+        if (nA == 0) continue;
+        if (lane == 0) {
+#pragma unroll
+          for (int x = 0; x < 2; ++x) {
+            if ((x ? nB : nA) == 0) continue;
+            const int qc = x ? qc1 : qc0;
+            mbar_wait(B(bQEmpty + x), (qc & 1) ^ 1);
+            mbar_expect_tx(B(bQFull + x), 2 * kTile);
+            for (int h = 0; h < 2; ++h)
+              tma_load_3d(base + kQ + (2 * x + h) * kTile, &tmQ, B(bQFull + x), h * 64, g * G,
+                          x ? LB.row_start : LA.row_start);
+          }
+        }
+        ++qc0;
+        if (nB) ++qc1;
+        const int* btA = a.bt + a.seq_bt_off[LA.seq];
+        const int* btB = sh ? btA : (nB ? a.bt + a.seq_bt_off[LB.seq] : btA);
+        const int lastA = (sh ? max(LA.max_p, LB.max_p) : LA.max_p) / 16;
+        const int lastB = LB.max_p / 16;
+        for (int s = 0; s < nA; ++s) {
+          const bool two = s < nB && !sh;
+          {
+            const int k = kc++, sl = k % kKS;
+            load_tile(&tmK, &tmK8, base + kK + sl * 2 * kTile, B(bKFull + sl), B(bKEmpty + sl), (k / kKS) & 1, btA,
+                      LA.j0 + s, lastA, g);
+          }
+          if (two) {
+            const int k = kc++, sl = k % kKS;
+            load_tile(&tmK, &tmK8, base + kK + sl * 2 * kTile, B(bKFull + sl), B(bKEmpty + sl), (k / kKS) & 1, btB,
+                      LB.j0 + s, lastB, g);
+          }
+          {
+            const int k = vc++, sl = k % kVS;
+            load_tile(&tmV, &tmV8, base + kV + sl * 2 * kTile, B(bVFull + sl), B(bVEmpty + sl), (k / kVS) & 1, btA,
+                      LA.j0 + s, lastA, g);
+          }
+          if (two) {
+            const int k = vc++, sl = k % kVS;
+            load_tile(&tmV, &tmV8, base + kV + sl * 2 * kTile, B(bVFull + sl), B(bVEmpty + sl), (k / kVS) & 1, btB,
+                      LB.j0 + s, lastB, g);
+          }
+        }
+      }
+    } else if (warp == 1) {
+      // ------------------------------------------------------------------ MMA issuer (lane 0)
+      constexpr uint32_t idS = idesc_bf16(128, 128, 0, 0);  // Q (smem, K-major) x K (smem, K-major)
+      constexpr uint32_t idO = idesc_bf16(128, 128, 0, 1);  // P (TMEM, K-major) x V (smem, MN-major)
+      int kc = 0, vc = 0;
+      int qcA = 0, qcB = 0, pcA = 0, pcB = 0, ecA = 0, ecB = 0;  // Q loads, PV issues, items per lane
+      for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+        PPLane LA, LB;
+        int g;
+        bool sh;
+        pp_decode(a, item, LA, LB, g, sh);
+        const int nA = LA.n, nB = LB.n;
+        if (nA == 0) continue;
+        if (lane == 0) {
+          auto issue_S = [&](int x, int s) {
+            const int k = kc + pp_tidx(x, s, nB, sh), sl = k % kKS;
+            mbar_wait(B((ROT ? bKRot : bKFull) + sl), (k / kKS) & 1);
+            if (s == 0) mbar_wait(B(bQFull + x), (x ? qcB : qcA) & 1);
+            tc_fence_after();
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk) {
+              const uint32_t qa = base + kQ + (2 * x + (kk >> 2)) * kTile + (kk & 3) * 32;
+              const uint32_t kb = base + kK + (2 * sl + (kk >> 2)) * kTile + (kk & 3) * 32;
+              umma_bf16(tmem + 128 * x, sdesc_sw128(qa, 16, 1024), sdesc_sw128(kb, 16, 1024), idS, kk > 0);
+            }
+            umma_commit(B(bSFull + x));
+            if (!(sh && x == 0 && s < nB)) umma_commit(B(bKEmpty + sl));  // last reader of this K slot
+            if (s == (x ? nB : nA) - 1) umma_commit(B(bQEmpty + x));
+          };
+          auto issue_PV = [&](int x, int s) {
+            mbar_wait(B(bPFull + x), (x ? pcB : pcA) & 1);
+            const int v = vc + pp_tidx(x, s, nB, sh), sl = v % kVS;
+            mbar_wait(B(bVFull + sl), (v / kVS) & 1);
+            if (s == 0) mbar_wait(B(bOFree + x), ((x ? ecB : ecA) & 1) ^ 1);  // previous item's O_X read out
+            tc_fence_after();
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk) {
+              // keys 16kk..16kk+15: P at S_X column 64·(kk/4) + 8·(kk%4); V rows 16kk.. of the slot
+              const uint32_t pa = tmem + 128 * x + (kk >> 2) * 64 + (kk & 3) * 8;
+              const uint32_t vb = base + kV + (2 * sl) * kTile + kk * 2048;
+              umma_bf16_ts(tmem + 256 + 128 * x, pa, sdesc_sw128(vb, kTile, 1024), idO, (s | kk) != 0);
+            }
+            umma_commit(B(bOFull + x));
+            if (!(sh && x == 0 && s < nB)) umma_commit(B(bVEmpty + sl));
+            if (x) ++pcB; else ++pcA;
+          };
+          // issue order S_A(0), S_B(0), then per step: PV_A(s), S_A(s+1), PV_B(s), S_B(s+1)
+#pragma unroll 1
+          for (int s = -1; s < nA; ++s) {
+#pragma unroll 1
+            for (int x = 0; x < 2; ++x) {
+              const int nx = x ? nB : nA;
+              if (s >= 0 && s < nx) issue_PV(x, s);
+              if (s + 1 < nx) issue_S(x, s + 1);
+            }
+          }
+          ++qcA;
+          ++ecA;
+          if (nB) {
+            ++qcB;
+            ++ecB;
+          }
+        }
+        __syncwarp();
+        kc += nA + (sh ? 0 : nB);
+        vc += nA + (sh ? 0 : nB);
+      }
+    }
+  } else if (ROT && warp < 8) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 96;\n" ::: "memory");
+    // ------------------------------------------------------------------ K-tile re-base (f3)
+    // As attention.cu: keys of chunk-store blocks linked by reference are rotated by their block's Δ
+    // (rebase_pair arithmetic, so the tile equals the copy path's a2-re-based one).  Thread u owns the
+    // logical 16-B chunk cc = u & 7 of rows rg + 8i of each paged block; dims j and j+64 sit at the same
+    // offset of the two SW128 halves.
+    constexpr int RPB = 16 / (4 * kRotWarps);
+    const int u = threadIdx.x - 128;
+    const int cc = u & 7, rg = u >> 3;
+    const uint32_t phys = (uint32_t)(((cc ^ (rg & 7)) << 4) + rg * 128);
+    int dcache = 0;
+    float2 cs[4], sn[4];
+    auto load_angles = [&](int d) {
+      const int ad = d < 0 ? -d : d;
+      const float sg = d < 0 ? -1.f : 1.f;
+      const float4* cp = reinterpret_cast<const float4*>(a.cos_t + (size_t)ad * 64 + cc * 8);
+      const float4* sp = reinterpret_cast<const float4*>(a.sin_t + (size_t)ad * 64 + cc * 8);
+      const float4 c0 = cp[0], c1 = cp[1], s0 = sp[0], s1 = sp[1];
+      cs[0] = make_float2(c0.x, c0.y);
+      cs[1] = make_float2(c0.z, c0.w);
+      cs[2] = make_float2(c1.x, c1.y);
+      cs[3] = make_float2(c1.z, c1.w);
+      sn[0] = make_float2(sg * s0.x, sg * s0.y);
+      sn[1] = make_float2(sg * s0.z, sg * s0.w);
+      sn[2] = make_float2(sg * s1.x, sg * s1.y);
+      sn[3] = make_float2(sg * s1.z, sg * s1.w);
+      dcache = d;
+    };
+    auto rot = [&](uint32_t& xa, uint32_t& xb, int k) {
+      const float2 av = make_float2(__uint_as_float(xa << 16), __uint_as_float(xa & 0xFFFF0000u));
+      const float2 bv = make_float2(__uint_as_float(xb << 16), __uint_as_float(xb & 0xFFFF0000u));
+      const float2 ra = fma2(av, cs[k], mul2(bv, make_float2(-sn[k].x, -sn[k].y)));
+      const float2 rb = fma2(bv, cs[k], mul2(av, sn[k]));
+      xa = pack_bf16(ra.x, ra.y);
+      xb = pack_bf16(rb.x, rb.y);
+    };
+    auto rotate_tile = [&](int k, const int* bd, int j, int last_blk) {
+      const int sl = k % kKS;
+      int dl[8];
+#pragma unroll
+      for (int m = 0; m < 8; ++m) dl[m] = bd[min(j * 8 + m, last_blk)];
+      int dfirst = 0;
+#pragma unroll
+      for (int m = 7; m >= 0; --m) dfirst = dl[m] ? dl[m] : dfirst;
+      if (dfirst != 0 && dfirst != dcache) load_angles(dfirst);
+      mbar_wait(B(bKFull + sl), (k / kKS) & 1);
+      const uint32_t h0 = base + kK + (2 * sl) * kTile + phys, h1 = h0 + kTile;
+      constexpr int NB = 2;  // 16-B chunk pairs in flight per thread (registers: this warpgroup runs at 96)
+      constexpr int BB = NB / RPB;
+#pragma unroll
+      for (int m0 = 0; m0 < 8; m0 += BB) {
+        uint4 xa[NB], xb[NB];
+#pragma unroll
+        for (int jj = 0; jj < NB; ++jj)
+          if (dl[m0 + jj / RPB]) {
+            const uint32_t o = (m0 + jj / RPB) * 2048 + (jj % RPB) * 1024;
+            xa[jj] = lds128(h0 + o);
+            xb[jj] = lds128(h1 + o);
+          }
+#pragma unroll
+        for (int jj = 0; jj < NB; ++jj) {
+          const int d = dl[m0 + jj / RPB];
+          if (d == 0) continue;
+          if (d != dcache) load_angles(d);
+          rot(xa[jj].x, xb[jj].x, 0);
+          rot(xa[jj].y, xb[jj].y, 1);
+          rot(xa[jj].z, xb[jj].z, 2);
+          rot(xa[jj].w, xb[jj].w, 3);
+          const uint32_t o = (m0 + jj / RPB) * 2048 + (jj % RPB) * 1024;
+          sts128(h0 + o, xa[jj]);
+          sts128(h1 + o, xb[jj]);
+        }
+      }
+      fence_async_smem();  // generic-proxy smem writes -> visible to the tcgen05.mma operand reads
+      __syncwarp();
+      if (lane == 0) mbar_arrive(B(bKRot + sl));
+    };
+    int kc = 0;
+    for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+      PPLane LA, LB;
+      int g;
+      bool sh;
+      pp_decode(a, item, LA, LB, g, sh);
+      const int nA = LA.n, nB = LB.n;
+      if (nA == 0) continue;
+      const int* bdA = a.bdelta + a.seq_bt_off[LA.seq];
+      const int* bdB = sh ? bdA : (nB ? a.bdelta + a.seq_bt_off[LB.seq] : bdA);
+      const int lastA = (sh ? max(LA.max_p, LB.max_p) : LA.max_p) / 16;
+      const int lastB = LB.max_p / 16;
+      for (int s = 0; s < nA; ++s) {
+        rotate_tile(kc++, bdA, LA.j0 + s, lastA);
+        if (s < nB && !sh) rotate_tile(kc++, bdB, LB.j0 + s, lastB);
+      }
+    }
+  } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(ROT ? 176 : 224) : "memory");
+    // ------------------------------------------------------------------ softmax warpgroups
+    const int x = (warp - SM0) >> 2;       // lane
+    const int q = warp & 3;                // TMEM lane quarter
+    const int r = q * 32 + lane;           // MMA row = TMEM lane
+    const int qi = r / G, hh = r % G;
+    const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
+    const uint32_t sAddr = tmem + lane_addr + 128 * x;
+    const uint32_t oAddr = tmem + lane_addr + 256 + 128 * x;
+    const float sc = a.scale_log2;
+    int cs = 0;  // S tiles of this lane so far (s_full / p_full / o_full phases)
+    for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+      PPLane LA, LB;
+      int g;
+      bool sh;
+      pp_decode(a, item, LA, LB, g, sh);
+      const PPLane P = x ? LB : LA;
+      const bool valid = qi < P.row_count;
+      const int row = P.row_start + qi;
+      const int head = g * G + hh;
+      if (P.n == 0) {
+        // an empty split piece (device-side positions end before it): neutral partial for combine
+        if (P.tile >= 0 && valid) {
+          const size_t idx = ((size_t)P.split * a.M + row) * a.Hq + head;
+          float4* dst = reinterpret_cast<float4*>(a.o_part + idx * 128);
+          for (int i = 0; i < 32; ++i) dst[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+          a.ml_part[2 * idx] = -INFINITY;
+          a.ml_part[2 * idx + 1] = 0.f;
+        }
+        continue;
+      }
+      const int pos = valid ? a.row_pos[row] : P.max_p;
+      float m_ref = -INFINITY, l = 0.f;
+      for (int s = 0; s < P.n; ++s) {
+        mbar_wait(B(bSFull + x), cs & 1);
+        tc_fence_after();
+        float sv[128];
+        tmem_ld128_split(sAddr, sv);
+        const int key0 = (P.j0 + s) * 128;
+        if (key0 + 127 > pos) {
+#pragma unroll
+          for (int i = 0; i < 128; ++i) sv[i] = (key0 + i <= pos) ? sv[i] : -INFINITY;
+        }
+        float m4[4] = {sv[0], sv[1], sv[2], sv[3]};
+#pragma unroll
+        for (int i = 4; i < 128; i += 8) {
+          m4[0] = fmax3(m4[0], sv[i], sv[i + 1]);
+          m4[1] = fmax3(m4[1], sv[i + 2], sv[i + 3]);
+          m4[2] = fmax3(m4[2], sv[i + 4], sv[i + 5]);
+          m4[3] = fmax3(m4[3], sv[i + 6], sv[i + 7]);
+        }
+        const float mx = fmax3(m4[0], m4[1], fmaxf(m4[2], m4[3])) * sc;  // log2 units (sc > 0)
+        const bool grow = mx > m_ref + 8.f;
+        const bool need = grow && m_ref != -INFINITY;
+        if (__any_sync(0xffffffffu, need)) {
+          // rescale O_X (PV of the previous step must have landed) and l to the new reference
+          mbar_wait(B(bOFull + x), (cs - 1) & 1);
+          tc_fence_after();
+          const float alpha = need ? exp2f(m_ref - mx) : 1.f;
+#pragma unroll 1
+          for (int c = 0; c < 4; ++c) {
+            float ov[32];
+            tmem_ld32(oAddr + c * 32, ov);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) ov[i] *= alpha;
+            tmem_st32(oAddr + c * 32, ov);
+          }
+          tmem_wait_st();
+          l *= alpha;
+        }
+        if (grow) m_ref = mx;
+        const float nmu = (m_ref == -INFINITY) ? 0.f : -m_ref;
+        float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          uint32_t pk[32];
+#pragma unroll
+          for (int c = 0; c < 16; ++c) {  // p = 2^(s·scale − m_ref); masked keys are −inf → 0
+            const float* v = sv + 64 * h + 4 * c;
+            const float p0 = ex2_approx(fmaf(v[0], sc, nmu)), p1 = ex2_approx(fmaf(v[1], sc, nmu));
+            const float p2 = ex2_approx(fmaf(v[2], sc, nmu)), p3 = ex2_approx(fmaf(v[3], sc, nmu));
+            s0 += p0;
+            s1 += p1;
+            s2 += p2;
+            s3 += p3;
+            pk[2 * c] = pack_bf16(p0, p1);
+            pk[2 * c + 1] = pack_bf16(p2, p3);
+          }
+          // keys [64h, 64h+64) -> S_X columns [64h, 64h+32) as bf16 pairs (the TS MMA's A layout)
+          tmem_st32u(sAddr + 64 * h, pk);
+        }
+        l += (s0 + s1) + (s2 + s3);
+        tmem_wait_st();
+        tc_fence_before();
+        mbar_arrive(B(bPFull + x));
+        ++cs;
+      }
+      // epilogue: O_X once the last PV landed; unsplit tiles are final (normalised bf16), split ones
+      // leave fp32 partials and (m, l)
+      mbar_wait(B(bOFull + x), (cs - 1) & 1);
+      tc_fence_after();
+      const bool direct = a.row_nsplit[P.row_start] == 1;
+      const float inv = direct ? 1.f / l : 1.f;
+      const size_t orow = (size_t)row * a.Hq + head;
+#pragma unroll 1
+      for (int c = 0; c < 4; ++c) {
+        float ov[32];
+        tmem_ld32(oAddr + c * 32, ov);  // warp-collective
+        if (valid) {
+          if (direct) {
+            uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(a.O) + orow * 128 + c * 32);
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              dst[i] = make_uint4(pack_bf16(ov[8 * i] * inv, ov[8 * i + 1] * inv), pack_bf16(ov[8 * i + 2] * inv, ov[8 * i + 3] * inv),
+                                  pack_bf16(ov[8 * i + 4] * inv, ov[8 * i + 5] * inv), pack_bf16(ov[8 * i + 6] * inv, ov[8 * i + 7] * inv));
+          } else {
+            float4* dst = reinterpret_cast<float4*>(a.o_part + ((size_t)P.split * a.M * a.Hq + orow) * 128 + c * 32);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) dst[i] = make_float4(ov[4 * i], ov[4 * i + 1], ov[4 * i + 2], ov[4 * i + 3]);
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(B(bOFree + x));  // O_X may be overwritten by the next item's first PV
+      if (valid && !direct) {
+        const size_t idx = (size_t)P.split * a.M * a.Hq + orow;
+        a.ml_part[2 * idx] = m_ref;
+        a.ml_part[2 * idx + 1] = l;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+// ------------------------------------------------------------------------------------------------
+// Host schedule: split-KV pieces from attn_schedule (sized for 2 lanes per SM), then paired into items.
+// Pieces of one sequence that start at the same KV tile share their loads (both lanes read the same
+// K/V tiles); they are paired longest with next-longest.  Left-over pieces are paired with another of
+// similar length (no shared loads; the lanes still ping-pong).  Pairing stops where fewer than n_sms
+// items would remain.  Items are sorted by their longer lane, longest first (the persistent CTAs walk
+// the list with stride gridDim.x).
+int attn_schedule_pp(const int32_t* tiles, int n_tiles, const int* n_kv, int Hkv, int n_sms, int max_split,
+                     std::vector<int32_t>& items, int32_t* row_nsplit) {
+  long total = 0;
+  for (int t = 0; t < n_tiles; ++t) total += n_kv[t];
+  std::vector<int32_t> work(4 * (size_t)(total + n_tiles));
+  int n_work = 0;
+  const int mx = attn_schedule(tiles, n_tiles, n_kv, Hkv, 2 * n_sms, max_split, work.data(), &n_work, row_nsplit);
+  struct Pc {
+    int t, j0, j1, slot, len, seq;
+  };
+  std::vector<Pc> pc(n_work);
+  for (int i = 0; i < n_work; ++i) {
+    const int32_t* w = &work[4 * i];
+    pc[i] = {w[0], w[1], w[2], w[3], w[2] - w[1], tiles[3 * w[0]]};
+  }
+  std::vector<int> ord(n_work);
+  for (int i = 0; i < n_work; ++i) ord[i] = i;
+  std::stable_sort(ord.begin(), ord.end(), [&](int x, int y) {
+    if (pc[x].seq != pc[y].seq) return pc[x].seq < pc[y].seq;
+    if (pc[x].j0 != pc[y].j0) return pc[x].j0 < pc[y].j0;
+    return pc[x].len > pc[y].len;
+  });
+  struct Cand {
+    int a, b;
+    double gain;
+  };
+  std::vector<Cand> cand;
+  std::vector<char> in_shared(n_work, 0);
+  for (int i = 0; i + 1 < n_work;) {
+    const Pc &p = pc[ord[i]], &q = pc[ord[i + 1]];
+    if (p.seq == q.seq && p.j0 == q.j0) {
+      cand.push_back({ord[i], ord[i + 1], (double)q.len});  // q.len steps run two lanes on one load
+      in_shared[ord[i]] = in_shared[ord[i + 1]] = 1;
+      i += 2;
+    } else {
+      ++i;
+    }
+  }
+  std::vector<int> left;
+  for (int i = 0; i < n_work; ++i)
+    if (!in_shared[i]) left.push_back(i);
+  std::stable_sort(left.begin(), left.end(), [&](int x, int y) { return pc[x].len > pc[y].len; });
+  for (size_t i = 0; i + 1 < left.size(); i += 2) {
+    const Pc &p = pc[left[i]], &q = pc[left[i + 1]];
+    if (2 * q.len >= p.len) cand.push_back({left[i], left[i + 1], 0.5 * q.len});
+  }
+  std::stable_sort(cand.begin(), cand.end(), [](const Cand& x, const Cand& y) { return x.gain > y.gain; });
+  std::vector<int> partner(n_work, -1);
+  long n_items = n_work;
+  for (const Cand& c : cand) {
+    if ((n_items - 1) * Hkv < n_sms) break;
+    partner[c.a] = c.b;
+    partner[c.b] = c.a;
+    --n_items;
+  }
+  struct It {
+    int a, b, len;
+  };
+  std::vector<It> its;
+  for (int i = 0; i < n_work; ++i) {
+    if (partner[i] >= 0 && partner[i] < i) continue;
+    const int b = partner[i];
+    its.push_back({i, b, std::max(pc[i].len, b >= 0 ? pc[b].len : 0)});
+  }
+  std::stable_sort(its.begin(), its.end(), [](const It& x, const It& y) { return x.len > y.len; });
+  items.assign(8 * its.size(), -1);
+  for (size_t k = 0; k < its.size(); ++k) {
+    const Pc& p = pc[its[k].a];
+    int32_t* o = &items[8 * k];
+    o[0] = p.t;
+    o[1] = p.j0;
+    o[2] = p.j1;
+    o[3] = p.slot;
+    if (its[k].b >= 0) {
+      const Pc& q = pc[its[k].b];
+      o[4] = q.t;
+      o[5] = q.j0;
+      o[6] = q.j1;
+      o[7] = q.slot;
+    } else {
+      o[4] = -1;
+      o[5] = o[6] = o[7] = 0;
+    }
+  }
+  return mx;
+}
+
+template <int G>
+static cudaError_t launch_pp_g(const CUtensorMap& tmQ, const CUtensorMap& tmK, const CUtensorMap& tmV,
+                               const CUtensorMap& tmK8, const CUtensorMap& tmV8, const AttnArgs& a, int n_sms,
+                               cudaStream_t st) {
+  const int n_items = a.n_work * a.Hkv;
+  dim3 grid(std::min(n_items, n_sms));
+  if (a.bdelta)
+    CUDA_TRY_LAUNCH(launch_k(attn_pp_kernel<G, true>, grid, dim3(512), attn2::kSmem, st, tmQ, tmK, tmV, tmK8, tmV8, a));
+  else
+    CUDA_TRY_LAUNCH(launch_k(attn_pp_kernel<G, false>, grid, dim3(384), attn2::kSmem, st, tmQ, tmK, tmV, tmK8, tmV8, a));
+  return cudaGetLastError();
+}
+
+template <int G>
+static cudaError_t prepare_pp_g() {
+  cudaError_t e = cudaFuncSetAttribute(attn_pp_kernel<G, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, attn2::kSmem);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(attn_pp_kernel<G, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, attn2::kSmem);
+  return e;
+}
+
+cudaError_t prepare_attention_pp() {
+  cudaError_t e = prepare_pp_g<1>();
+  if (e == cudaSuccess) e = prepare_pp_g<2>();
+  if (e == cudaSuccess) e = prepare_pp_g<4>();
+  if (e == cudaSuccess) e = prepare_pp_g<8>();
+  return e;
+}
+
+cudaError_t launch_attention_pp(const CUtensorMap& tmQ, const CUtensorMap& tmK, const CUtensorMap& tmV,
+                                const CUtensorMap& tmK8, const CUtensorMap& tmV8, const AttnArgs& a, int n_sms,
+                                cudaStream_t st) {
+  if (a.n_work <= 0) return cudaSuccess;
+  switch (a.Hq / a.Hkv) {
+    case 1: return launch_pp_g<1>(tmQ, tmK, tmV, tmK8, tmV8, a, n_sms, st);
+    case 2: return launch_pp_g<2>(tmQ, tmK, tmV, tmK8, tmV8, a, n_sms, st);
+    case 4: return launch_pp_g<4>(tmQ, tmK, tmV, tmK8, tmV8, a, n_sms, st);
+    case 8: return launch_pp_g<8>(tmQ, tmK, tmV, tmK8, tmV8, a, n_sms, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace pic

@@ -5,6 +5,7 @@
 #include <stdint.h>
 
 #include <utility>
+#include <vector>
 
 namespace pic {
 
@@ -183,6 +184,14 @@ int attn_schedule(const int32_t* tiles, int n_tiles, const int* n_kv, int Hkv, i
 // tmK/tmV: pool maps with a one-block box (64, 16, 1, 1); tmK8/tmV8: eight-block box (64, 16, 1, 8)
 cudaError_t launch_attention_tc(const CUtensorMap& tmQ, const CUtensorMap& tmK, const CUtensorMap& tmV,
                                 const CUtensorMap& tmK8, const CUtensorMap& tmV8, const AttnArgs& a, cudaStream_t st);
+// a6 v2 (attention_pp.cu): persistent ping-pong kernel, two q-tile lanes per CTA sharing the K/V stream.
+// attn_schedule_pp writes items [n][8] = (tile, j0, j1, split slot) for lane A then lane B (tile -1: none);
+// AttnArgs.work = items, AttnArgs.n_work = n; n * Hkv CTA items walked by min(n * Hkv, n_sms) CTAs.
+int attn_schedule_pp(const int32_t* tiles, int n_tiles, const int* n_kv, int Hkv, int n_sms, int max_split,
+                     std::vector<int32_t>& items, int32_t* row_nsplit);
+cudaError_t launch_attention_pp(const CUtensorMap& tmQ, const CUtensorMap& tmK, const CUtensorMap& tmV,
+                                const CUtensorMap& tmK8, const CUtensorMap& tmV8, const AttnArgs& a, int n_sms,
+                                cudaStream_t st);
 cudaError_t launch_attn_combine(const float* o_part, const float* ml_part, const int32_t* row_nsplit, void* O, int M,
                                 int Hq, int D, cudaStream_t st);
 // generic-D SIMT attention (tiny shapes D in {16,32,64}; any D <= 128 in the fp32 debug build); writes O directly

@@ -18,6 +18,7 @@ namespace pic {
 
 cudaError_t prepare_gemm();
 cudaError_t prepare_attention();
+cudaError_t prepare_attention_pp();
 bool pdl_enabled() {
   static int v = -1;
   if (v < 0) v = getenv("PIC_NO_PDL") ? 0 : 1;
@@ -27,7 +28,8 @@ bool pdl_enabled() {
 cudaError_t prepare_kernels() {
   cudaError_t e = prepare_gemm();
   if (e == cudaSuccess) e = prepare_gemm_chain();
-  return e == cudaSuccess ? prepare_attention() : e;
+  if (e == cudaSuccess) e = prepare_attention();
+  return e == cudaSuccess ? prepare_attention_pp() : e;
 }
 
 // ================================================================================ generator

@@ -76,6 +76,23 @@ extern "C" pic_status pic_test_gemm(const uint16_t* A, const uint16_t* B, int32_
   return PIC_OK;
 }
 
+static int g_attn_version = 2, g_attn_grid = 0;
+
+extern "C" pic_status pic_test_attention_v(const uint16_t* Q, const uint16_t* K, const uint16_t* V, const int32_t* pos,
+                                           int32_t M, int32_t n_keys, int32_t Hq, int32_t Hkv,
+                                           const int32_t* block_perm, int32_t num_blocks, int32_t n_splits,
+                                           int32_t version, int32_t grid, uint16_t* O) {
+  if (version != 1 && version != 2) return PIC_E_INVALID_ARG;
+  g_attn_version = version;
+  g_attn_grid = grid;
+  extern pic_status pic_test_attention(const uint16_t*, const uint16_t*, const uint16_t*, const int32_t*, int32_t,
+                                       int32_t, int32_t, int32_t, const int32_t*, int32_t, int32_t, uint16_t*);
+  const pic_status s = pic_test_attention(Q, K, V, pos, M, n_keys, Hq, Hkv, block_perm, num_blocks, n_splits, O);
+  g_attn_version = 2;
+  g_attn_grid = 0;
+  return s;
+}
+
 extern "C" pic_status pic_test_attention(const uint16_t* Q, const uint16_t* K, const uint16_t* V, const int32_t* pos,
                                          int32_t M, int32_t n_keys, int32_t Hq, int32_t Hkv,
                                          const int32_t* block_perm, int32_t num_blocks, int32_t n_splits,
@@ -107,12 +124,23 @@ extern "C" pic_status pic_test_attention(const uint16_t* Q, const uint16_t* K, c
   std::vector<int32_t> work(4 * (n_kv.size() + 64 * n_tiles)), nsplit(M, 1);
   int n_work = 0;
   // the test forces up to n_splits pieces per tile by asking for n_splits x more CTAs than tiles
-  attn_schedule(tiles.data(), n_tiles, n_kv.data(), Hkv, n_tiles * Hkv * n_splits, n_splits, work.data(), &n_work,
-                nsplit.data());
+  const bool pp = g_attn_version == 2;
+  if (pp) {  // same split targets as the one-lane schedule: 2 lanes per "SM" of the pairing rule
+    std::vector<int32_t> items;
+    attn_schedule_pp(tiles.data(), n_tiles, n_kv.data(), Hkv, std::max(1, n_tiles * Hkv * n_splits / 2), n_splits,
+                     items, nsplit.data());
+    n_work = (int)items.size() / 8;
+    work = items;
+  } else {
+    attn_schedule(tiles.data(), n_tiles, n_kv.data(), Hkv, n_tiles * Hkv * n_splits, n_splits, work.data(), &n_work,
+                  nsplit.data());
+  }
+  const int wints = pp ? 8 : 4;
+  const int grid = g_attn_grid > 0 ? g_attn_grid : 148;
   DevBuf dw, dns;
-  TCK(cudaMalloc(&dw.p, 4 * n_work * 4));
+  TCK(cudaMalloc(&dw.p, wints * n_work * 4));
   TCK(cudaMalloc(&dns.p, M * 4));
-  TCK(cudaMemcpy(dw.p, work.data(), 4 * n_work * 4, cudaMemcpyHostToDevice));
+  TCK(cudaMemcpy(dw.p, work.data(), wints * n_work * 4, cudaMemcpyHostToDevice));
   TCK(cudaMemcpy(dns.p, nsplit.data(), M * 4, cudaMemcpyHostToDevice));
   DevBuf dq, dk, dv, dpos, dt, dbt, doff, dop, dml, dout;
   TCK(cudaMalloc(&dq.p, (size_t)M * Hq * D * 2));
@@ -164,7 +192,10 @@ extern "C" pic_status pic_test_attention(const uint16_t* Q, const uint16_t* K, c
   a.Q = dq.p;
   a.row_nsplit = reinterpret_cast<int32_t*>(dns.p);
   a.O = dout.p;
-  TCK(launch_attention_tc(tq, tk, tv, tk8, tv8, a, 0));
+  auto launch = [&]() -> cudaError_t {
+    return pp ? launch_attention_pp(tq, tk, tv, tk8, tv8, a, grid, 0) : launch_attention_tc(tq, tk, tv, tk8, tv8, a, 0);
+  };
+  TCK(launch());
   TCK(launch_attn_combine(a.o_part, a.ml_part, reinterpret_cast<int32_t*>(dns.p), dout.p, M, Hq, D, 0));
   TCK(cudaDeviceSynchronize());
   if (g_attn_iters > 0) {
@@ -172,7 +203,7 @@ extern "C" pic_status pic_test_attention(const uint16_t* Q, const uint16_t* K, c
     TCK(cudaEventCreate(&e0));
     TCK(cudaEventCreate(&e1));
     TCK(cudaEventRecord(e0, 0));
-    for (int i = 0; i < g_attn_iters; ++i) TCK(launch_attention_tc(tq, tk, tv, tk8, tv8, a, 0));
+    for (int i = 0; i < g_attn_iters; ++i) TCK(launch());
     TCK(cudaEventRecord(e1, 0));
     TCK(cudaEventSynchronize(e1));
     float ms = 0;

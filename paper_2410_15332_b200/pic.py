@@ -103,7 +103,7 @@ EXPORTS = ["pic_arena_bytes", "pic_engine_create", "pic_engine_destroy", "pic_ge
            "pic_link_batch", "pic_plan", "pic_linked_export", "pic_linked_info", "pic_linked_sharing", "pic_linked_materialize", "pic_linked_release",
            "pic_cache_export", "pic_cache_info", "pic_expire_cache", "pic_read_weights", "pic_get_stats",
            "pic_last_error", "pic_status_string", "pic_arena_bytes_tp", "pic_engine_create_tp", "pic_tp_ipc_handle",
-           "pic_tp_connect", "pic_generate_context_cache_ex", "pic_decode", "pic_serve_poisson", "pic_serve_arrivals", "pic_set_profiling", "pic_get_profile", "pic_test_gemm", "pic_test_attention", "pic_test_kv_link", "pic_bench_gemm", "pic_bench_attention", "pic_test_gemm_swiglu"]
+           "pic_tp_connect", "pic_generate_context_cache_ex", "pic_decode", "pic_serve_poisson", "pic_serve_arrivals", "pic_set_profiling", "pic_get_profile", "pic_test_gemm", "pic_test_attention", "pic_test_attention_v", "pic_test_kv_link", "pic_bench_gemm", "pic_bench_attention", "pic_test_gemm_swiglu"]
 
 _lib = None
 
@@ -159,6 +159,7 @@ def lib() -> C.CDLL:
                                     C.c_void_p]
         L.pic_test_attention.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32,
                                          C.c_int32, C.c_int32, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p]
+        L.pic_test_attention_v.argtypes = L.pic_test_attention.argtypes[:11] + [C.c_int32, C.c_int32, C.c_void_p]
         L.pic_test_kv_link.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p,
                                        C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_double, C.c_int32]
         L.pic_bench_gemm.argtypes = [C.c_int32] * 6 + [P(C.c_float)]
@@ -583,7 +584,7 @@ def test_gemm_swiglu(A: np.ndarray, B: np.ndarray, bn: int) -> np.ndarray:
     return u
 
 
-def test_attention(Q, K, V, pos, block_perm, num_blocks, n_splits=1) -> np.ndarray:
+def test_attention(Q, K, V, pos, block_perm, num_blocks, n_splits=1, version=2, grid=0) -> np.ndarray:
     Q = np.ascontiguousarray(Q, dtype=np.uint16)
     K = np.ascontiguousarray(K, dtype=np.uint16)
     V = np.ascontiguousarray(V, dtype=np.uint16)
@@ -592,8 +593,8 @@ def test_attention(Q, K, V, pos, block_perm, num_blocks, n_splits=1) -> np.ndarr
     M, Hq, D = Q.shape
     n, Hkv, _ = K.shape
     O = np.empty((M, Hq, D), dtype=np.uint16)
-    check(lib().pic_test_attention(Q.ctypes.data, K.ctypes.data, V.ctypes.data, pos.ctypes.data, M, n, Hq, Hkv,
-                                   bp.ctypes.data, num_blocks, n_splits, O.ctypes.data))
+    check(lib().pic_test_attention_v(Q.ctypes.data, K.ctypes.data, V.ctypes.data, pos.ctypes.data, M, n, Hq, Hkv,
+                                     bp.ctypes.data, num_blocks, n_splits, version, grid, O.ctypes.data))
     return O
 
 

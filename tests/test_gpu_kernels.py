@@ -94,7 +94,10 @@ def test_gemm_swiglu_vs_fp64(M_, F, K_, bn):
 @pytest.mark.parametrize("Hq,Hkv,n_keys,M_,splits", [
     (4, 4, 300, 40, 1), (8, 2, 257, 70, 2), (32, 8, 700, 128, 3), (64, 8, 1000, 33, 4), (8, 1, 130, 130, 1),
     (2, 1, 112, 96, 1), (2, 1, 2624, 128, 5)])
-def test_attention_vs_oracle(Hq, Hkv, n_keys, M_, splits):
+@pytest.mark.parametrize("version,grid,contig", [(2, 0, False), (2, 3, True), (1, 0, False)])
+def test_attention_vs_oracle(Hq, Hkv, n_keys, M_, splits, version, grid, contig):
+    """version 2 = the engine's persistent ping-pong kernel (grid 3: several items per CTA; contig: the
+    8-block TMA box path), version 1 = one q-tile per CTA."""
     D = 128
     Q = rand_bf16(1 + Hq, (M_, Hq, D))
     K = rand_bf16(2 + Hq, (n_keys, Hkv, D))
@@ -106,7 +109,9 @@ def test_attention_vs_oracle(Hq, Hkv, n_keys, M_, splits):
     Q = Q[:M_]
     nb = (n_keys + 15) // 16
     perm = np.argsort(sg.U(5, nb, np.arange(nb + 5, dtype=np.uint64)))[:nb].astype(np.int32)  # distinct ids
-    got = B.test_attention(Q, K, V, pos, perm, nb + 5, splits)
+    if contig:
+        perm = np.arange(2, nb + 2, dtype=np.int32)
+    got = B.test_attention(Q, K, V, pos, perm, nb + 5, splits, version=version, grid=grid)
     ref = M.causal_attention(f32(Q), f32(K), f32(V), pos)
     assert rel(f32(got), ref) < 1e-2, rel(f32(got), ref)
     # per-row check too (a wrong causal limit shows up on one row)
