@@ -40,6 +40,11 @@ pic_status pic_test_attention_v(const uint16_t* Q, const uint16_t* K, const uint
                                 int32_t M, int32_t n_keys, int32_t Hq, int32_t Hkv, const int32_t* block_perm,
                                 int32_t num_blocks, int32_t n_splits, int32_t version, int32_t grid, uint16_t* O);
 
+/* Engine-wide attention kernel override for later pic_link / pic_link_batch / pic_decode calls:
+ * 0 = the engine's choice (default), 1 = one q-tile per CTA, 2 = ping-pong (also for shared-block links).
+ * Tests and A/B measurements only. */
+pic_status pic_test_set_attention_kernel(int32_t version);
+
 /* a2 KV link on a raw pool: pool K/V [n_layers][num_blocks][Hkv][16][D] bf16 (in/out), rows
  * (src_slot -> dst_slot, delta) for layers layer0..n_layers-1, RoPE table for positions < max_pos. */
 pic_status pic_test_kv_link(uint16_t* Kpool, uint16_t* Vpool, int32_t n_layers, int32_t num_blocks, int32_t Hkv,

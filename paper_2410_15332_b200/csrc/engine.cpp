@@ -102,7 +102,35 @@ static unsigned long long* attn_trace_buffer() {
   if (on && !buf && cudaMalloc(&buf, 16 * 8192 * sizeof(unsigned long long)) != cudaSuccess) buf = nullptr;
   return on ? buf : nullptr;
 }
+// ping-pong kernel (attention_pp.cu): per-CTA cycle accounting, 32 counters per CTA
+static void attn_pp_trace_print(int n_cta) {
+  unsigned long long* buf = attn_trace_buffer();
+  if (!buf || n_cta <= 0) return;
+  std::vector<unsigned long long> t((size_t)32 * n_cta);
+  if (cudaMemcpy(t.data(), buf, t.size() * 8, cudaMemcpyDeviceToHost) != cudaSuccess) return;
+  static const char* nm[23] = {"start", "end", "prod wait K-empty", "prod wait V-empty", "prod wait Q-empty", "prod tiles",
+                               "mma wait K", "mma wait P", "mma wait V", "mma wait Q", "mma wait O-free",
+                               "smA wait S", "smA compute", "smA epilogue", "smA steps", "smB wait S", "smB compute",
+                               "smB epilogue", "smB steps", "rot wait K", "rot compute", "items", "-"};
+  std::vector<double> span;
+  for (int c = 0; c < n_cta; ++c) span.push_back((double)(t[32 * c + 1] - t[32 * c]));
+  std::sort(span.begin(), span.end());
+  fprintf(stderr, "  attn_pp CTA span (cycles): min %.0f med %.0f max %.0f\n", span[0], span[span.size() / 2], span.back());
+  for (int k = 2; k < 22; ++k) {
+    std::vector<double> v;
+    for (int c = 0; c < n_cta; ++c) v.push_back((double)t[32 * c + k]);
+    std::sort(v.begin(), v.end());
+    fprintf(stderr, "  attn_pp %-18s min %10.0f med %10.0f max %10.0f (%.1f%% of median span)\n", nm[k], v[0],
+            v[v.size() / 2], v.back(), 100.0 * v[v.size() / 2] / span[span.size() / 2]);
+  }
+}
+static bool g_attn_trace_pp = false;
+
 static void attn_trace_print(int n_cta) {
+  if (g_attn_trace_pp) {
+    attn_pp_trace_print(n_cta);
+    return;
+  }
   unsigned long long* buf = attn_trace_buffer();
   if (!buf || n_cta <= 0) return;
   std::vector<unsigned long long> t((size_t)16 * n_cta);
@@ -200,6 +228,10 @@ static bool wave_fit() {
   return on;
 }
 
+// test hook: 0 = the engine's choice, 1 / 2 = force the one-lane / ping-pong attention kernel
+namespace pic {
+int g_attn_force = 0;
+}
 // a6 on the persistent ping-pong kernel (attention_pp.cu); PIC_ATTN_V1=1: the one-lane kernel (A/B only)
 static bool attn_pp_enabled() {
   static const bool on = getenv("PIC_ATTN_V1") == nullptr;
@@ -353,7 +385,7 @@ static ArenaPlan plan_arena(const pic_model_config& c, const pic_engine_limits& 
   a.off_plan = L.add(a.plan_ints * 4);
   // tensor parallel: two reduced-partial buffers (alternating per all-reduce), flags, epoch counter
   a.off_ar = L.add(2 * M * d * 4);
-  a.off_tpflags = L.add(8 * 8 + 8 + 16);  // TP epoch flags + counter, then the GEMM-chain barrier counters
+  a.off_tpflags = L.add(8 * 8 + 8 + 16 + 16);  // TP epoch flags + counter, GEMM-chain barrier, attention item counters
   a.total = L.total + 1024;
   return a;
 }
@@ -596,7 +628,8 @@ static pic_status init_device(pic_engine* e, void* arena, size_t bytes, cudaStre
   e->tp_flags = reinterpret_cast<long long*>(b + a.off_tpflags);
   e->tp_counter = e->tp_flags + 8;
   e->chain_bar = reinterpret_cast<unsigned*>(e->tp_flags + 9);
-  CK(cudaMemsetAsync(e->tp_flags, 0, 9 * 8 + 16, st));
+  e->attn_ctr = reinterpret_cast<unsigned*>(e->tp_flags + 11);
+  CK(cudaMemsetAsync(e->tp_flags, 0, 9 * 8 + 16 + 16, st));
   for (int r = 0; r < 8; ++r) {
     e->peer_flags.p[r] = nullptr;
     e->peer_ar[0][r] = e->peer_ar[1][r] = nullptr;
@@ -615,6 +648,8 @@ static pic_status init_device(pic_engine* e, void* arena, size_t bytes, cudaStre
   CK(cudaStreamCreateWithFlags(&e->side_stream, cudaStreamNonBlocking));
   CK(cudaEventCreateWithFlags(&e->k2_fork, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&e->k2_join, cudaEventDisableTiming));
+  e->k2_layer_done.assign(e->cfg.n_layers, nullptr);
+  for (auto& ev : e->k2_layer_done) CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
   CK(prepare_kernels());
   CK(cudaStreamSynchronize(st));
   return PIC_OK;
@@ -744,6 +779,8 @@ extern "C" void pic_engine_destroy(pic_engine* e) {
     if (e->side_stream) cudaStreamDestroy(e->side_stream);
     if (e->k2_fork) cudaEventDestroy(e->k2_fork);
     if (e->k2_join) cudaEventDestroy(e->k2_join);
+    for (auto ev : e->k2_layer_done)
+      if (ev) cudaEventDestroy(ev);
     for (void* p : e->ipc_opened) cudaIpcCloseMemHandle(p);
     for (cudaEvent_t ev : e->ev_pool) cudaEventDestroy(ev);
   }
@@ -1140,9 +1177,10 @@ static pic_status enqueue_forward(pic_engine* e, const Fwd& f, const DevPlan& dp
   char* Vp = reinterpret_cast<char*>(e->Vpool);
   const size_t lbytes = (size_t)e->layer_stride * (e->f32 ? 4 : 2);
 
-  // a2: the first K2 layer on the main stream; the other layers on a side stream, overlapping the
-  // first layers' weight streaming (layer k2_layer0+1's attention waits for them — LegoLink/Naive scatter
-  // writes slots disjoint from K2's; CacheBlend waits before that layer's scatter, see below)
+  // a2: the first K2 layer on the main stream; every later layer as its own launch on a side stream,
+  // each recording an event that the main stream waits for just before that layer needs the rows (its
+  // attention; CacheBlend: its scatter, see below).  The side stream runs ahead, so the HBM-bound re-base
+  // overlaps the tensor-bound projections of the first layers instead of delaying layer k2_layer0+1.
   const bool k2_side = !f.k2_src.empty() && f.k2_layer0 + 1 < L && !e->profiling && k2_overlap() && e->side_stream;
   if (!f.k2_src.empty() && f.k2_layer0 < L) {
     const int n_first = k2_side ? 1 : L - f.k2_layer0;
@@ -1152,11 +1190,13 @@ static pic_status enqueue_forward(pic_engine* e, const Fwd& f, const DevPlan& dp
     if (k2_side) {
       CK(cudaEventRecord(e->k2_fork, st));
       CK(cudaStreamWaitEvent(e->side_stream, e->k2_fork, 0));
-      ++R.launches;
-      CKL(launch_kv_link(e->Kpool, e->Vpool, dp.k2_src, dp.k2_dst, dp.k2_delta, (int)f.k2_src.size(), f.k2_layer0 + 1,
-                         L - f.k2_layer0 - 1, e->layer_stride, Hkv, D, e->cos_t, e->sin_t, f.rebase, e->side_stream,
-                         e->f32));
-      CK(cudaEventRecord(e->k2_join, e->side_stream));
+      for (int l = f.k2_layer0 + 1; l < L; ++l) {
+        ++R.launches;
+        // one CTA per SM: it shares each SM with the persistent GEMM CTA instead of crowding it out
+        CKL(launch_kv_link(e->Kpool, e->Vpool, dp.k2_src, dp.k2_dst, dp.k2_delta, (int)f.k2_src.size(), l, 1,
+                           e->layer_stride, Hkv, D, e->cos_t, e->sin_t, f.rebase, e->side_stream, e->f32, 148));
+        CK(cudaEventRecord(e->k2_layer_done[l], e->side_stream));  // joined by layer l (the last by layer L-1)
+      }
     }
   }
   ++R.launches;
@@ -1225,7 +1265,7 @@ static pic_status enqueue_forward(pic_engine* e, const Fwd& f, const DevPlan& dp
     }
     // CacheBlend: the side-stream K2 covers every cached row (the selection is device-side), including
     // the rows this layer's scatter rewrites, so it must land before the scatter, not just before attention
-    if (k2_side && f.cb && l == f.k2_layer0 + 1) CK(cudaStreamWaitEvent(st, e->k2_join, 0));
+    if (k2_side && f.cb && l > f.k2_layer0) CK(cudaStreamWaitEvent(st, e->k2_layer_done[l], 0));
     if (f.cb && l == f.cb_layer) {
       // a9: CacheBlend selection at the check layer (P:170 steps 3-4)
       if (!f.cb_override) {
@@ -1254,7 +1294,7 @@ static pic_status enqueue_forward(pic_engine* e, const Fwd& f, const DevPlan& dp
                                  st, e->f32, pos == dp.pos ? 1 : 0));
     }
     if (f.compile && l == L - 1) break;  // compile needs only the last layer's K/V
-    if (k2_side && !f.cb && l == f.k2_layer0 + 1) CK(cudaStreamWaitEvent(st, e->k2_join, 0));  // side-stream K2 landed
+    if (k2_side && !f.cb && l > f.k2_layer0) CK(cudaStreamWaitEvent(st, e->k2_layer_done[l], 0));  // this layer's a2 landed
     // a6 attention — algorithmic work: 4·H_q·D·Σ(p_i+1) FLOPs, K/V of keys 0..max p read once
     double attn_flops = 0, attn_bytes = 0;
     if (e->profiling) {
@@ -1295,12 +1335,14 @@ static pic_status enqueue_forward(pic_engine* e, const Fwd& f, const DevPlan& dp
       a.cos_t = e->cos_t;
       a.sin_t = e->sin_t;
       a.Q = e->Q;
-      g_attn_trace_ctas = a.n_work * Hkv;
+      g_attn_trace_ctas = f.attn_pp ? std::min(a.n_work * Hkv, 148) : a.n_work * Hkv;
+      g_attn_trace_pp = f.attn_pp;
       a.o_part = e->o_part;
       a.ml_part = e->ml_part;
       const bool main_tiles = tiles == dp.tiles;
       a.row_nsplit = main_tiles ? dp.attn_nsplit : dp.attn_nsplit2;
       a.O = e->Obuf;  // unsplit q-tiles write their normalised bf16 output here directly
+      a.item_ctr = e->attn_ctr;
       const int max_split = main_tiles ? f.attn_max_split : f.attn_max_split2;
       ++R.launches;
       if (f.attn_pp)
@@ -1452,7 +1494,23 @@ static void schedule_attention(pic_engine* e, Fwd& f) {
     max_split = attn_schedule(tiles.data(), nt, n_kv.data(), Hkv, 148, cap, work.data(), &n_work, nsplit.data());
     work.resize(4 * (size_t)n_work);
   };
-  f.attn_pp = attn_pp_enabled() && e->cfg.head_dim == 128 && !e->f32;
+  // Kernel choice (D = 128, bf16): the ping-pong kernel needs enough tile work to keep 148 persistent
+  // CTAs busy with paired lanes (cfg4 wave: 53 k KV-tile iterations, 1.25x faster; cfg2: 544, slower than
+  // the one-lane kernel's finer split-KV); shared-block links (K tiles re-based in smem) stay on the
+  // one-lane kernel, whose four rotation warps keep up where the ping-pong kernel's two do not (cfg4:
+  // 310 vs 200 ms per step).  pic_test_set_attention_kernel(1|2) forces one (tests and A/B only).
+  bool pp = attn_pp_enabled() && e->cfg.head_dim == 128 && !e->f32 && !f.kv_rot;
+  if (pp) {
+    long work = 0;
+    for (size_t t = 0; t + 2 < f.tiles.size(); t += 3) {
+      int mx = 0;
+      for (int r = 0; r < f.tiles[t + 2]; ++r) mx = std::max(mx, f.pos[f.tiles[t + 1] + r]);
+      work += mx / 128 + 1;
+    }
+    pp = work * Hkv >= 148L * 16;
+  }
+  if (g_attn_force) pp = g_attn_force == 2 && e->cfg.head_dim == 128 && !e->f32;
+  f.attn_pp = pp;
   build(f.tiles, &f.pos, f.M, 0, f.attn_work, f.attn_nsplit, f.attn_n_work, f.attn_max_split);
   if (f.cb) {
     const int N = f.M;  // single request, all rows at layer 0
@@ -2060,7 +2118,12 @@ extern "C" pic_status pic_link(pic_engine* e, const pic_segment* segs, int32_t n
 extern "C" pic_status pic_link_batch(pic_engine* e, int32_t n_req, const pic_segment* const* segs,
                                      const int32_t* n_segs, const pic_link_params* params, void* stream,
                                      pic_linked** out_linked, pic_link_result* results) {
-  return link_impl(e, n_req, segs, n_segs, params, stream, out_linked, results);
+  const pic_status st = link_impl(e, n_req, segs, n_segs, params, stream, out_linked, results);
+  if (st == PIC_OK && attn_trace_buffer()) {
+    cudaStreamSynchronize(reinterpret_cast<cudaStream_t>(stream));
+    attn_trace_print(g_attn_trace_ctas);
+  }
+  return st;
 }
 
 // ============================================================================ exports / lifecycle

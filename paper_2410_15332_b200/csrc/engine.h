@@ -126,6 +126,7 @@ struct pic_engine {
   bool tp_connected = false;
   float* ar_buf[2] = {nullptr, nullptr};       // reduced partials exchanged across ranks (alternating)
   long long *tp_flags = nullptr, *tp_counter = nullptr;
+  unsigned* attn_ctr = nullptr;   // 2 self-resetting counters of the persistent attention's item queue
   unsigned* chain_bar = nullptr;  // 2 self-resetting counters of the persistent GEMM chain's grid barrier
   float* peer_ar[2][8];                        // every rank's ar_buf (peer memory), own included
   pic::Peers peer_flags{};
@@ -170,6 +171,7 @@ struct pic_engine {
   cudaStream_t cap_stream = nullptr;
   cudaStream_t side_stream = nullptr;   // a2 layers >= 1 overlap the first layers (joined before their attention)
   cudaEvent_t k2_fork = nullptr, k2_join = nullptr;
+  std::vector<cudaEvent_t> k2_layer_done;  // per layer: the side-stream a2 of that layer landed
   int32_t* last_cb_sel2 = nullptr;  // device: CacheBlend selection of the last forward
   // profiling
   bool profiling = false;

@@ -40,12 +40,17 @@ constexpr int kQ = 0;                       // Q_A halves, Q_B halves
 constexpr int kK = kQ + 4 * kTile;          // K ring
 constexpr int kV = kK + kKS * 2 * kTile;    // V ring
 constexpr int kBar = kV + kVS * 2 * kTile;  // barriers
+constexpr int kIR = 4;  // item-index ring (producer -> every other role)
 constexpr int bQFull = 0, bQEmpty = 2, bKFull = 4, bKEmpty = bKFull + kKS, bKRot = bKEmpty + kKS,
               bVFull = bKRot + kKS, bVEmpty = bVFull + kVS, bSFull = bVEmpty + kVS, bPFull = bSFull + 2,
-              bOFull = bPFull + 2, bOFree = bOFull + 2, kNumBars = bOFree + 2;
-constexpr int kSmem = kBar + kNumBars * 8 + 16;
+              bOFull = bPFull + 2, bOFree = bOFull + 2, bIFull = bOFree + 2, bIEmpty = bIFull + kIR,
+              kNumBars = bIEmpty + kIR;
+constexpr int kSmem = kBar + kNumBars * 8 + 16 + kIR * 4;
 static_assert(kSmem <= 232448, "attention smem over the 227 KB limit");
-constexpr int kRotWarps = 4;
+constexpr int kRotWarps = 2;  // warps 2-3 of the producer / MMA warpgroup
+// register split of the 384-thread CTA: 128·(producer, MMA, rotation) + 256·softmax <= 64 K
+constexpr int kRegW0Rot = 104, kRegSmRot = 200;
+static_assert(128 * kRegW0Rot + 256 * kRegSmRot <= 65536, "register split over the file");
 }  // namespace attn2
 
 struct PPLane {
@@ -82,8 +87,9 @@ PIC_DEV void pp_lane(const AttnArgs& a, const int* wk, int x, PPLane& p) {
   p.n = max(0, min(mp / 128 + 1, wk[4 * x + 2]) - p.j0);
 }
 PIC_DEV void pp_decode(const AttnArgs& a, int item, PPLane& A, PPLane& Bn, int& g, bool& sh) {
-  const int* wk = a.work + 8 * (item / a.Hkv);
-  g = item % a.Hkv;
+  // head-major item order: the CTAs work through one kv-head's K/V (L2-resident) at a time
+  const int* wk = a.work + 8 * (item % a.n_work);
+  g = item / a.n_work;
   PPLane p0, p1;
   pp_lane(a, wk, 0, p0);
   pp_lane(a, wk, 1, p1);
@@ -91,6 +97,44 @@ PIC_DEV void pp_decode(const AttnArgs& a, int item, PPLane& A, PPLane& Bn, int& 
   A = sw ? p1 : p0;
   Bn = sw ? p0 : p1;
   sh = Bn.n > 0 && A.seq == Bn.seq && A.j0 == Bn.j0;
+}
+
+// Bench-only cycle accounting (AttnArgs.trace, PIC_ATTN_TRACE=1): per CTA 32 counters, see kTr*.
+enum {
+  kTrStart = 0, kTrEnd, kTrPwK, kTrPwV, kTrPwQ, kTrPtiles, kTrMwK, kTrMwP, kTrMwV, kTrMwQ, kTrMwO,
+  kTrSwS0, kTrSc0, kTrSe0, kTrSn0, kTrSwS1, kTrSc1, kTrSe1, kTrSn1, kTrRw, kTrRc, kTrItems, kTrPwI
+};
+PIC_DEV unsigned long long clk() { return clock64(); }
+// mbar_wait that adds the cycles it spent to *acc (acc may be null)
+PIC_DEV void mbar_wait_acc(uint32_t bar, uint32_t ph, unsigned long long* acc) {
+  if (!acc) {
+    mbar_wait(bar, ph);
+    return;
+  }
+  const unsigned long long t0 = clk();
+  mbar_wait(bar, ph);
+  *acc += clk() - t0;
+}
+
+// 2^x for a pair on the FMA pipe (FA4's trick: part of the exponentials leave the 16/clk/SM MUFU):
+// x = j + f with j = rint(x) (magic-number rounding), 2^f on [-1/2, 1/2] by a degree-3 fit (max relative
+// error 1.3e-4, far below the bf16 rounding P gets next), 2^j added to the exponent field.  x >= -125
+// after the clamp (masked keys, x = -inf, give 2^-125 ~ 2e-38 instead of 0: negligible against l >= 1).
+#ifndef PIC_POLY8
+#define PIC_POLY8 3  // pairs of every 8 on the polynomial
+#endif
+PIC_DEV float2 exp2_poly2(float2 x) {
+  constexpr float kM = 12582912.f;  // 1.5 * 2^23
+  x.x = fmaxf(x.x, -125.f);
+  x.y = fmaxf(x.y, -125.f);
+  const float2 t = add2(x, make_float2(kM, kM));
+  const float2 j = add2(t, make_float2(-kM, -kM));
+  const float2 f = fma2(j, make_float2(-1.f, -1.f), x);
+  float2 p = fma2(f, make_float2(0.05504054f, 0.05504054f), make_float2(0.24228513f, 0.24228513f));
+  p = fma2(p, f, make_float2(0.69325425f, 0.69325425f));
+  p = fma2(p, f, make_float2(0.99995032f, 0.99995032f));
+  return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23)),
+                     __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
 }
 
 // position of lane x's step-s K (or V) tile in the item's load order: shared → one tile per step;
@@ -102,13 +146,13 @@ PIC_DEV int pp_tidx(int x, int s, int nB, bool sh) {
 }
 
 template <int G, bool ROT>
-__global__ void __launch_bounds__(ROT ? 512 : 384, 1)
+__global__ void __launch_bounds__(384, 1)
     attn_pp_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                    const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmK8,
                    const __grid_constant__ CUtensorMap tmV8, const AttnArgs a) {
   griddep_launch();
   using namespace attn2;
-  constexpr int SM0 = ROT ? 8 : 4;  // first softmax warp (lane A: SM0..SM0+3, lane B: SM0+4..SM0+7)
+  constexpr int SM0 = 4;  // first softmax warp (lane A: warps 4-7, lane B: warps 8-11)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw;
   if (threadIdx.x == 0 && (smem_u32(smem) & 1023)) __trap();  // SWIZZLE_128B tiles need 1 KB alignment
@@ -136,6 +180,10 @@ __global__ void __launch_bounds__(ROT ? 512 : 384, 1)
       mbar_init(B(bVFull + s), 1);
       mbar_init(B(bVEmpty + s), 1);
     }
+    for (int s = 0; s < kIR; ++s) {
+      mbar_init(B(bIFull + s), 1);
+      mbar_init(B(bIEmpty + s), ROT ? 11 : 9);  // MMA warp, rotation warps, softmax warps
+    }
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc(smem_u32(tmem_slot), 512);
@@ -143,11 +191,28 @@ __global__ void __launch_bounds__(ROT ? 512 : 384, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  int* const iring = reinterpret_cast<int*>(tmem_slot + 4);
+  unsigned long long* const tr = a.trace ? a.trace + 32 * blockIdx.x : nullptr;
+  unsigned long long tacc[4] = {0, 0, 0, 0};  // per-role accumulators (flushed at the end)
+  if (tr && threadIdx.x == 0) tr[kTrStart] = clk();
   griddep_wait();  // Q, the recomputed rows' K/V and (CacheBlend) device-side positions come from upstream
   const int n_items = a.n_work * a.Hkv;
+  // Dynamic item queue: the producer takes the next item from the global counter (list order = longest
+  // first within each kv-head) and hands its index to the other roles through a smem ring; -1 ends.
+  auto next_item = [&](int k) -> int {  // consumers (whole warp)
+    const int sl = k % kIR;
+    mbar_wait(B(bIFull + sl), (k / kIR) & 1);
+    const int it = *reinterpret_cast<volatile int*>(iring + sl);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(B(bIEmpty + sl));
+    return it;
+  };
 
   if (warp < 4) {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 56;\n" ::: "memory");
+    if constexpr (ROT)
+      asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(kRegW0Rot) : "memory");
+    else
+      asm volatile("setmaxnreg.dec.sync.aligned.u32 56;\n" ::: "memory");
     if (warp == 0) {
       // ------------------------------------------------------------------ TMA producer
       int kc = 0, vc = 0, qc0 = 0, qc1 = 0;
@@ -169,7 +234,7 @@ __global__ void __launch_bounds__(ROT ? 512 : 384, 1)
 #pragma unroll
         for (int b = 0; b < 8; ++b) blk[b] = __shfl_sync(0xffffffffu, mine, b);
         if (lane == 0) {
-          mbar_wait(empty, ph ^ 1);
+          mbar_wait_acc(empty, ph ^ 1, tr ? (t1 == &tmK ? &tacc[0] : &tacc[1]) : nullptr);
           mbar_expect_tx(full, 2 * kTile);
           if (contig) {
             for (int h = 0; h < 2; ++h) tma_load_4d(dst + h * kTile, t8, full, h * 64, 0, g, kv_base + b0);
@@ -181,7 +246,19 @@ __global__ void __launch_bounds__(ROT ? 512 : 384, 1)
         }
         __syncwarp();
       };
-      for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+      for (int k = 0;; ++k) {
+        int item = 0;
+        if (lane == 0) {
+          const int sl = k % kIR;
+          mbar_wait(B(bIEmpty + sl), ((k / kIR) & 1) ^ 1);
+          item = (int)atomicAdd(a.item_ctr, 1u);
+          if (tr) ++tacc[3];
+          if (item >= n_items) item = -1;
+          iring[sl] = item;
+          mbar_arrive(B(bIFull + sl));
+        }
+        item = __shfl_sync(0xffffffffu, item, 0);
+        if (item < 0) break;
         PPLane LA, LB;
         int g;
         bool sh;
@@ -193,7 +270,7 @@ __global__ void __launch_bounds__(ROT ? 512 : 384, 1)
           for (int x = 0; x < 2; ++x) {
             if ((x ? nB : nA) == 0) continue;
             const int qc = x ? qc1 : qc0;
-            mbar_wait(B(bQEmpty + x), (qc & 1) ^ 1);
+            mbar_wait_acc(B(bQEmpty + x), (qc & 1) ^ 1, tr ? &tacc[2] : nullptr);
             mbar_expect_tx(B(bQFull + x), 2 * kTile);
             for (int h = 0; h < 2; ++h)
               tma_load_3d(base + kQ + (2 * x + h) * kTile, &tmQ, B(bQFull + x), h * 64, g * G,
@@ -230,83 +307,101 @@ __global__ void __launch_bounds__(ROT ? 512 : 384, 1)
           }
         }
       }
+      if (tr && lane == 0) {
+        tr[kTrPwK] = tacc[0];
+        tr[kTrPwV] = tacc[1];
+        tr[kTrPwQ] = tacc[2];
+        tr[kTrItems] = tacc[3];
+        tr[kTrPtiles] = kc;
+      }
     } else if (warp == 1) {
       // ------------------------------------------------------------------ MMA issuer (lane 0)
       constexpr uint32_t idS = idesc_bf16(128, 128, 0, 0);  // Q (smem, K-major) x K (smem, K-major)
       constexpr uint32_t idO = idesc_bf16(128, 128, 0, 1);  // P (TMEM, K-major) x V (smem, MN-major)
       int kc = 0, vc = 0;
       int qcA = 0, qcB = 0, pcA = 0, pcB = 0, ecA = 0, ecB = 0;  // Q loads, PV issues, items per lane
-      for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+      unsigned long long tmw_o = 0;
+      // base descriptors (slot / k-step offsets are added to the 14-bit address field, which never carries)
+      const uint64_t dQ0 = sdesc_sw128(base + kQ, 16, 1024), dQ1 = sdesc_sw128(base + kQ + 2 * kTile, 16, 1024);
+      const uint64_t dK0 = sdesc_sw128(base + kK, 16, 1024), dV0 = sdesc_sw128(base + kV, kTile, 1024);
+      for (int k = 0;; ++k) {
+        const int item = next_item(k);
+        if (item < 0) break;
         PPLane LA, LB;
         int g;
         bool sh;
         pp_decode(a, item, LA, LB, g, sh);
         const int nA = LA.n, nB = LB.n;
         if (nA == 0) continue;
-        if (lane == 0) {
-          auto issue_S = [&](int x, int s) {
-            const int k = kc + pp_tidx(x, s, nB, sh), sl = k % kKS;
-            mbar_wait(B((ROT ? bKRot : bKFull) + sl), (k / kKS) & 1);
-            if (s == 0) mbar_wait(B(bQFull + x), (x ? qcB : qcA) & 1);
-            tc_fence_after();
+        // the whole warp runs the issue loop (convergent, uniform state); elect.sync issues
+        auto issue_S = [&](int x, int s) {
+          const int k = kc + pp_tidx(x, s, nB, sh), sl = k % kKS;
+          mbar_wait_acc(B((ROT ? bKRot : bKFull) + sl), (k / kKS) & 1, tr ? &tacc[0] : nullptr);
+          if (s == 0) mbar_wait_acc(B(bQFull + x), (x ? qcB : qcA) & 1, tr ? &tacc[3] : nullptr);
+          tc_fence_after();
+          const uint64_t dq = x ? dQ1 : dQ0, dk = dK0 + (uint64_t)(sl * (2 * kTile / 16));
 #pragma unroll
-            for (int kk = 0; kk < 8; ++kk) {
-              const uint32_t qa = base + kQ + (2 * x + (kk >> 2)) * kTile + (kk & 3) * 32;
-              const uint32_t kb = base + kK + (2 * sl + (kk >> 2)) * kTile + (kk & 3) * 32;
-              umma_bf16(tmem + 128 * x, sdesc_sw128(qa, 16, 1024), sdesc_sw128(kb, 16, 1024), idS, kk > 0);
-            }
-            umma_commit(B(bSFull + x));
-            if (!(sh && x == 0 && s < nB)) umma_commit(B(bKEmpty + sl));  // last reader of this K slot
-            if (s == (x ? nB : nA) - 1) umma_commit(B(bQEmpty + x));
-          };
-          auto issue_PV = [&](int x, int s) {
-            mbar_wait(B(bPFull + x), (x ? pcB : pcA) & 1);
-            const int v = vc + pp_tidx(x, s, nB, sh), sl = v % kVS;
-            mbar_wait(B(bVFull + sl), (v / kVS) & 1);
-            if (s == 0) mbar_wait(B(bOFree + x), ((x ? ecB : ecA) & 1) ^ 1);  // previous item's O_X read out
-            tc_fence_after();
+          for (int kk = 0; kk < 8; ++kk) {
+            const uint64_t o = (uint64_t)(((kk >> 2) * kTile + (kk & 3) * 32) >> 4);
+            umma_bf16_e(tmem + 128 * x, dq + o, dk + o, idS, kk > 0);
+          }
+          umma_commit_e(B(bSFull + x));
+          if (!(sh && x == 0 && s < nB)) umma_commit_e(B(bKEmpty + sl));  // last reader of this K slot
+          if (s == (x ? nB : nA) - 1) umma_commit_e(B(bQEmpty + x));
+        };
+        auto issue_PV = [&](int x, int s) {
+          mbar_wait_acc(B(bPFull + x), (x ? pcB : pcA) & 1, tr ? &tacc[1] : nullptr);
+          const int v = vc + pp_tidx(x, s, nB, sh), sl = v % kVS;
+          mbar_wait_acc(B(bVFull + sl), (v / kVS) & 1, tr ? &tacc[2] : nullptr);
+          if (s == 0)  // previous item's O_X read out
+            mbar_wait_acc(B(bOFree + x), ((x ? ecB : ecA) & 1) ^ 1, tr ? &tmw_o : nullptr);
+          tc_fence_after();
+          const uint64_t dv = dV0 + (uint64_t)(sl * (2 * kTile / 16));
 #pragma unroll
-            for (int kk = 0; kk < 8; ++kk) {
-              // keys 16kk..16kk+15: P at S_X column 64·(kk/4) + 8·(kk%4); V rows 16kk.. of the slot
-              const uint32_t pa = tmem + 128 * x + (kk >> 2) * 64 + (kk & 3) * 8;
-              const uint32_t vb = base + kV + (2 * sl) * kTile + kk * 2048;
-              umma_bf16_ts(tmem + 256 + 128 * x, pa, sdesc_sw128(vb, kTile, 1024), idO, (s | kk) != 0);
-            }
-            umma_commit(B(bOFull + x));
-            if (!(sh && x == 0 && s < nB)) umma_commit(B(bVEmpty + sl));
-            if (x) ++pcB; else ++pcA;
-          };
-          // issue order S_A(0), S_B(0), then per step: PV_A(s), S_A(s+1), PV_B(s), S_B(s+1)
-#pragma unroll 1
-          for (int s = -1; s < nA; ++s) {
-#pragma unroll 1
-            for (int x = 0; x < 2; ++x) {
-              const int nx = x ? nB : nA;
-              if (s >= 0 && s < nx) issue_PV(x, s);
-              if (s + 1 < nx) issue_S(x, s + 1);
-            }
+          for (int kk = 0; kk < 8; ++kk) {
+            // keys 16kk..16kk+15: P at S_X column 64·(kk/4) + 8·(kk%4); V rows 16kk.. of the slot
+            const uint32_t pa = tmem + 128 * x + (kk >> 2) * 64 + (kk & 3) * 8;
+            umma_bf16_ts_e(tmem + 256 + 128 * x, pa, dv + (uint64_t)(kk * 2048 / 16), idO, (s | kk) != 0);
           }
-          ++qcA;
-          ++ecA;
-          if (nB) {
-            ++qcB;
-            ++ecB;
+          umma_commit_e(B(bOFull + x));
+          if (!(sh && x == 0 && s < nB)) umma_commit_e(B(bVEmpty + sl));
+          if (x) ++pcB; else ++pcA;
+        };
+        // issue order S_A(0), S_B(0), then per step: PV_A(s), S_A(s+1), PV_B(s), S_B(s+1)
+#pragma unroll 1
+        for (int s = -1; s < nA; ++s) {
+#pragma unroll 1
+          for (int x = 0; x < 2; ++x) {
+            const int nx = x ? nB : nA;
+            if (s >= 0 && s < nx) issue_PV(x, s);
+            if (s + 1 < nx) issue_S(x, s + 1);
           }
+        }
+        ++qcA;
+        ++ecA;
+        if (nB) {
+          ++qcB;
+          ++ecB;
         }
         __syncwarp();
         kc += nA + (sh ? 0 : nB);
         vc += nA + (sh ? 0 : nB);
       }
-    }
-  } else if (ROT && warp < 8) {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 96;\n" ::: "memory");
+      if (tr && lane == 0) {  // (every lane accumulated the same waits)
+        tr[kTrMwK] = tacc[0];
+        tr[kTrMwP] = tacc[1];
+        tr[kTrMwV] = tacc[2];
+        tr[kTrMwQ] = tacc[3];
+        tr[kTrMwO] = tmw_o;
+      }
+    } else if (ROT) {
     // ------------------------------------------------------------------ K-tile re-base (f3)
     // As attention.cu: keys of chunk-store blocks linked by reference are rotated by their block's Δ
     // (rebase_pair arithmetic, so the tile equals the copy path's a2-re-based one).  Thread u owns the
     // logical 16-B chunk cc = u & 7 of rows rg + 8i of each paged block; dims j and j+64 sit at the same
     // offset of the two SW128 halves.
     constexpr int RPB = 16 / (4 * kRotWarps);
-    const int u = threadIdx.x - 128;
+    const int u = threadIdx.x - 64;
     const int cc = u & 7, rg = u >> 3;
     const uint32_t phys = (uint32_t)(((cc ^ (rg & 7)) << 4) + rg * 128);
     int dcache = 0;
@@ -344,9 +439,12 @@ __global__ void __launch_bounds__(ROT ? 512 : 384, 1)
 #pragma unroll
       for (int m = 7; m >= 0; --m) dfirst = dl[m] ? dl[m] : dfirst;
       if (dfirst != 0 && dfirst != dcache) load_angles(dfirst);
+      const unsigned long long tw = tr ? clk() : 0;
       mbar_wait(B(bKFull + sl), (k / kKS) & 1);
+      const unsigned long long tw1 = tr ? clk() : 0;
+      if (tr) tacc[0] += tw1 - tw;
       const uint32_t h0 = base + kK + (2 * sl) * kTile + phys, h1 = h0 + kTile;
-      constexpr int NB = 2;  // 16-B chunk pairs in flight per thread (registers: this warpgroup runs at 96)
+      constexpr int NB = 2;  // 16-B chunk pairs in flight per thread
       constexpr int BB = NB / RPB;
 #pragma unroll
       for (int m0 = 0; m0 < 8; m0 += BB) {
@@ -375,9 +473,12 @@ __global__ void __launch_bounds__(ROT ? 512 : 384, 1)
       fence_async_smem();  // generic-proxy smem writes -> visible to the tcgen05.mma operand reads
       __syncwarp();
       if (lane == 0) mbar_arrive(B(bKRot + sl));
+      if (tr) tacc[1] += clk() - tw1;
     };
     int kc = 0;
-    for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+    for (int k = 0;; ++k) {
+      const int item = next_item(k);
+      if (item < 0) break;
       PPLane LA, LB;
       int g;
       bool sh;
@@ -393,8 +494,13 @@ __global__ void __launch_bounds__(ROT ? 512 : 384, 1)
         if (s < nB && !sh) rotate_tile(kc++, bdB, LB.j0 + s, lastB);
       }
     }
+    if (tr && threadIdx.x == 64) {
+      tr[kTrRw] = tacc[0];
+      tr[kTrRc] = tacc[1];
+    }
+    }
   } else {
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(ROT ? 176 : 224) : "memory");
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(ROT ? kRegSmRot : 224) : "memory");
     // ------------------------------------------------------------------ softmax warpgroups
     const int x = (warp - SM0) >> 2;       // lane
     const int q = warp & 3;                // TMEM lane quarter
@@ -405,7 +511,9 @@ __global__ void __launch_bounds__(ROT ? 512 : 384, 1)
     const uint32_t oAddr = tmem + lane_addr + 256 + 128 * x;
     const float sc = a.scale_log2;
     int cs = 0;  // S tiles of this lane so far (s_full / p_full / o_full phases)
-    for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+    for (int k = 0;; ++k) {
+      const int item = next_item(k);
+      if (item < 0) break;
       PPLane LA, LB;
       int g;
       bool sh;
@@ -428,7 +536,10 @@ __global__ void __launch_bounds__(ROT ? 512 : 384, 1)
       const int pos = valid ? a.row_pos[row] : P.max_p;
       float m_ref = -INFINITY, l = 0.f;
       for (int s = 0; s < P.n; ++s) {
+        const unsigned long long tw = tr ? clk() : 0;
         mbar_wait(B(bSFull + x), cs & 1);
+        const unsigned long long tw1 = tr ? clk() : 0;
+        if (tr) tacc[0] += tw1 - tw;
         tc_fence_after();
         float sv[128];
         tmem_ld128_split(sAddr, sv);
@@ -466,31 +577,40 @@ __global__ void __launch_bounds__(ROT ? 512 : 384, 1)
         }
         if (grow) m_ref = mx;
         const float nmu = (m_ref == -INFINITY) ? 0.f : -m_ref;
-        float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+        const float2 sc2 = make_float2(sc, sc), nmu2 = make_float2(nmu, nmu);
+        float2 la = make_float2(0.f, 0.f), lb = make_float2(0.f, 0.f);
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           uint32_t pk[32];
 #pragma unroll
-          for (int c = 0; c < 16; ++c) {  // p = 2^(s·scale − m_ref); masked keys are −inf → 0
-            const float* v = sv + 64 * h + 4 * c;
-            const float p0 = ex2_approx(fmaf(v[0], sc, nmu)), p1 = ex2_approx(fmaf(v[1], sc, nmu));
-            const float p2 = ex2_approx(fmaf(v[2], sc, nmu)), p3 = ex2_approx(fmaf(v[3], sc, nmu));
-            s0 += p0;
-            s1 += p1;
-            s2 += p2;
-            s3 += p3;
-            pk[2 * c] = pack_bf16(p0, p1);
-            pk[2 * c + 1] = pack_bf16(p2, p3);
+          for (int c = 0; c < 32; ++c) {  // pair c: p = 2^(s·scale − m_ref); masked keys are −inf → 0
+            const float2 xv = fma2(make_float2(sv[64 * h + 2 * c], sv[64 * h + 2 * c + 1]), sc2, nmu2);
+            float2 pv;
+            if ((c & 7) < PIC_POLY8)
+              pv = exp2_poly2(xv);
+            else
+              pv = make_float2(ex2_approx(xv.x), ex2_approx(xv.y));
+            if (c & 1)
+              lb = add2(lb, pv);
+            else
+              la = add2(la, pv);
+            pk[c] = pack_bf16(pv.x, pv.y);
           }
           // keys [64h, 64h+64) -> S_X columns [64h, 64h+32) as bf16 pairs (the TS MMA's A layout)
           tmem_st32u(sAddr + 64 * h, pk);
         }
+        const float s0 = la.x, s1 = la.y, s2 = lb.x, s3 = lb.y;
         l += (s0 + s1) + (s2 + s3);
         tmem_wait_st();
         tc_fence_before();
         mbar_arrive(B(bPFull + x));
         ++cs;
+        if (tr) {
+          tacc[1] += clk() - tw1;
+          ++tacc[3];
+        }
       }
+      const unsigned long long te = tr ? clk() : 0;
       // epilogue: O_X once the last PV landed; unsplit tiles are final (normalised bf16), split ones
       // leave fp32 partials and (m, l)
       mbar_wait(B(bOFull + x), (cs - 1) & 1);
@@ -523,6 +643,13 @@ __global__ void __launch_bounds__(ROT ? 512 : 384, 1)
         a.ml_part[2 * idx] = m_ref;
         a.ml_part[2 * idx + 1] = l;
       }
+      if (tr) tacc[2] += clk() - te;
+    }
+    if (tr && (warp - SM0) % 4 == 0 && lane == 0) {
+      tr[x ? kTrSwS1 : kTrSwS0] = tacc[0];
+      tr[x ? kTrSc1 : kTrSc0] = tacc[1];
+      tr[x ? kTrSe1 : kTrSe0] = tacc[2];
+      tr[x ? kTrSn1 : kTrSn0] = tacc[3];
     }
   }
   tc_fence_before();
@@ -530,6 +657,15 @@ __global__ void __launch_bounds__(ROT ? 512 : 384, 1)
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc(tmem, 512);
+  }
+  if (tr && threadIdx.x == 0) tr[kTrEnd] = clk();
+  if (threadIdx.x == 0) {  // every producer has drawn its final -1: the last CTA re-arms the queue
+    __threadfence();
+    if (atomicAdd(a.item_ctr + 1, 1u) == gridDim.x - 1) {
+      a.item_ctr[0] = 0;
+      a.item_ctr[1] = 0;
+      __threadfence();
+    }
   }
 }
 
@@ -634,7 +770,7 @@ static cudaError_t launch_pp_g(const CUtensorMap& tmQ, const CUtensorMap& tmK, c
   const int n_items = a.n_work * a.Hkv;
   dim3 grid(std::min(n_items, n_sms));
   if (a.bdelta)
-    CUDA_TRY_LAUNCH(launch_k(attn_pp_kernel<G, true>, grid, dim3(512), attn2::kSmem, st, tmQ, tmK, tmV, tmK8, tmV8, a));
+    CUDA_TRY_LAUNCH(launch_k(attn_pp_kernel<G, true>, grid, dim3(384), attn2::kSmem, st, tmQ, tmK, tmV, tmK8, tmV8, a));
   else
     CUDA_TRY_LAUNCH(launch_k(attn_pp_kernel<G, false>, grid, dim3(384), attn2::kSmem, st, tmQ, tmK, tmV, tmK8, tmV8, a));
   return cudaGetLastError();

@@ -74,7 +74,7 @@ cudaError_t launch_swiglu(const float* P, int splits, void* u, int M, int F, cud
 cudaError_t launch_kv_link(void* Kpool, void* Vpool, const int32_t* src_slot, const int32_t* dst_slot,
                            const int32_t* delta, int n_rows, int layer0, int n_layers, int64_t layer_stride_elems,
                            int Hkv, int D, const float* cos_t, const float* sin_t, int rebase, cudaStream_t st,
-                           int f32 = 0);
+                           int f32 = 0, int max_ctas = 148 * 4);
 
 // ---- GEMM (tcgen05): P[split][M][N] = A[M][K] · B[N][K]^T --------------------------------------
 // pack > 0: B is stored pre-tiled [N/pack][K/64][pack][64] (every TMA box contiguous); the tensor map
@@ -175,6 +175,8 @@ struct AttnArgs {
   // written as bf16 to O [M][Hq][128] directly; split rows leave fp32 partials for attn_combine.
   const int32_t* row_nsplit;
   void* O;
+  // ping-pong kernel: [next item, CTAs done], zero before the launch; the last CTA resets both
+  unsigned* item_ctr;
 };
 // Balanced split-KV schedule: each q-tile t (KV extent n_kv[t] 128-key tiles) gets
 // ceil(n_kv[t] / budget) splits, budget = ceil(Σ n_kv · Hkv / target_ctas); splits <= 32.

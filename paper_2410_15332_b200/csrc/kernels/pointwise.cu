@@ -461,59 +461,68 @@ cudaError_t launch_swiglu(const float* P, int splits, void* u, int M, int F, cud
 // (P:213 step 3: "incorporating the cached KV vectors of the N − k' unselected tokens at correct
 // positions").  One thread = one 16-byte chunk of the first half of a K head-row plus its RoPE
 // partner chunk D/2 further (NeoX pairs), or one 16-byte chunk of a V head-row.
-__global__ void kv_link_kernel(uint4* __restrict__ Kpool, uint4* __restrict__ Vpool, const int32_t* __restrict__ src_slot,
-                               const int32_t* __restrict__ dst_slot, const int32_t* __restrict__ delta, int n_rows,
-                               int layer0, int n_layers, int64_t layer_stride16, int Hkv, int D,
-                               const float* __restrict__ cos_t, const float* __restrict__ sin_t, int rebase) {
+// One warp per (layer, linked row): src / dst slots and Δ are read once per row, lane (g, c) covers the
+// 16-B chunk c of head g's first K half plus its NeoX partner chunk c + D/16 (rotated together) and V
+// chunks c and c + D/16; every load of the row is in flight before the first store.  A (row, layer) moves
+// 4·H_kv·D bytes each way.  (The earlier one-thread-per-chunk kernel spent its issue slots on 64-bit
+// index arithmetic and reached 70% of HBM.)
+__global__ void __launch_bounds__(256) kv_link_kernel(uint4* __restrict__ Kpool, uint4* __restrict__ Vpool,
+                                                      const int32_t* __restrict__ src_slot,
+                                                      const int32_t* __restrict__ dst_slot,
+                                                      const int32_t* __restrict__ delta, int n_rows, int layer0,
+                                                      int n_layers, int64_t layer_stride16, int Hkv, int D,
+                                                      const float* __restrict__ cos_t, const float* __restrict__ sin_t,
+                                                      int rebase) {
   PIC_PDL_ENTRY();
-  const int cK = D / 16, cV = D / 8;  // 16-byte chunks per half row (K) / per row (V)
-  const int64_t nK = (int64_t)n_layers * n_rows * Hkv * cK;
-  const int64_t nV = (int64_t)n_layers * n_rows * Hkv * cV;
-  const int rowq = D / 8;             // 16-byte chunks per head-row
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nK + nV; t += (int64_t)gridDim.x * blockDim.x) {
-    const bool isK = t < nK;
-    int64_t u = isK ? t : t - nK;
-    const int per = isK ? cK : cV;
-    const int c = (int)(u % per);
-    u /= per;
-    const int g = (int)(u % Hkv);
-    u /= Hkv;
+  const int cK = D / 16;              // 16-B chunks per half row
+  const int rowq = D / 8;             // 16-B chunks per head-row
+  const int per = Hkv * cK;           // (head, chunk) lanes of a row
+  const int lane = threadIdx.x & 31;
+  const int64_t units = (int64_t)n_layers * n_rows;
+  const int64_t wstride = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t u = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); u < units; u += wstride) {
     const int w = (int)(u % n_rows);
     const int l = layer0 + (int)(u / n_rows);
     const int ss = src_slot[w], ds = dst_slot[w];
+    const int dl = rebase ? delta[w] : 0;
     const int64_t lo = (int64_t)l * layer_stride16;
-    const int64_t so = lo + ((int64_t)(ss / 16) * Hkv + g) * 16 * rowq + (int64_t)(ss % 16) * rowq;
-    const int64_t dof = lo + ((int64_t)(ds / 16) * Hkv + g) * 16 * rowq + (int64_t)(ds % 16) * rowq;
-    if (!isK) {
-      Vpool[dof + c] = Vpool[so + c];
-      continue;
-    }
-    const uint4 xa = Kpool[so + c], xb = Kpool[so + c + cK];
-    const int dl = delta[w];
-    if (!rebase || dl == 0) {
-      Kpool[dof + c] = xa;
-      Kpool[dof + c + cK] = xb;
-      continue;
-    }
-    const int ad = dl < 0 ? -dl : dl;
-    const float sg = dl < 0 ? -1.f : 1.f;
-    const float* cs = cos_t + (size_t)ad * (D / 2) + c * 8;
-    const float* sn = sin_t + (size_t)ad * (D / 2) + c * 8;
-    const uint32_t a4[4] = {xa.x, xa.y, xa.z, xa.w}, b4[4] = {xb.x, xb.y, xb.z, xb.w};
-    uint32_t oa[4], ob[4];
+    const int64_t sb = lo + (int64_t)(ss >> 4) * Hkv * 16 * rowq + (ss & 15) * rowq;
+    const int64_t db = lo + (int64_t)(ds >> 4) * Hkv * 16 * rowq + (ds & 15) * rowq;
+    for (int i0 = 0; i0 < per; i0 += 32) {
+      const int i = i0 + lane;
+      if (i >= per) break;
+      const int g = i / cK, c = i % cK;
+      const int64_t so = sb + (int64_t)g * 16 * rowq + c, dof = db + (int64_t)g * 16 * rowq + c;
+      const uint4 xa = Kpool[so], xb = Kpool[so + cK], va = Vpool[so], vb = Vpool[so + cK];
+      Vpool[dof] = va;
+      Vpool[dof + cK] = vb;
+      if (dl == 0) {
+        Kpool[dof] = xa;
+        Kpool[dof + cK] = xb;
+        continue;
+      }
+      const int ad = dl < 0 ? -dl : dl;
+      const float sg = dl < 0 ? -1.f : 1.f;
+      const float4* cp = reinterpret_cast<const float4*>(cos_t + (size_t)ad * (D / 2) + c * 8);
+      const float4* sp = reinterpret_cast<const float4*>(sin_t + (size_t)ad * (D / 2) + c * 8);
+      const float4 c0 = cp[0], c1 = cp[1], s0 = sp[0], s1 = sp[1];
+      const float cs[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+      const float sn[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+      const uint32_t a4[4] = {xa.x, xa.y, xa.z, xa.w}, b4[4] = {xb.x, xb.y, xb.z, xb.w};
+      uint32_t oa[4], ob[4];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const float a0 = __uint_as_float(a4[k] << 16), a1 = __uint_as_float(a4[k] & 0xFFFF0000u);
-      const float b0 = __uint_as_float(b4[k] << 16), b1 = __uint_as_float(b4[k] & 0xFFFF0000u);
-      const float c0 = cs[2 * k], c1 = cs[2 * k + 1], s0 = sg * sn[2 * k], s1 = sg * sn[2 * k + 1];
-      float ra0, rb0, ra1, rb1;
-      rebase_pair(a0, b0, c0, s0, ra0, rb0);
-      rebase_pair(a1, b1, c1, s1, ra1, rb1);
-      oa[k] = pack_bf16(ra0, ra1);
-      ob[k] = pack_bf16(rb0, rb1);
+      for (int k = 0; k < 4; ++k) {
+        const float a0 = __uint_as_float(a4[k] << 16), a1 = __uint_as_float(a4[k] & 0xFFFF0000u);
+        const float b0 = __uint_as_float(b4[k] << 16), b1 = __uint_as_float(b4[k] & 0xFFFF0000u);
+        float ra0, rb0, ra1, rb1;
+        rebase_pair(a0, b0, cs[2 * k], sg * sn[2 * k], ra0, rb0);
+        rebase_pair(a1, b1, cs[2 * k + 1], sg * sn[2 * k + 1], ra1, rb1);
+        oa[k] = pack_bf16(ra0, ra1);
+        ob[k] = pack_bf16(rb0, rb1);
+      }
+      Kpool[dof] = make_uint4(oa[0], oa[1], oa[2], oa[3]);
+      Kpool[dof + cK] = make_uint4(ob[0], ob[1], ob[2], ob[3]);
     }
-    Kpool[dof + c] = make_uint4(oa[0], oa[1], oa[2], oa[3]);
-    Kpool[dof + c + cK] = make_uint4(ob[0], ob[1], ob[2], ob[3]);
   }
 }
 
@@ -556,7 +565,7 @@ __global__ void kv_link_f32_kernel(float* __restrict__ Kpool, float* __restrict_
 cudaError_t launch_kv_link(void* Kpool, void* Vpool, const int32_t* src_slot, const int32_t* dst_slot,
                            const int32_t* delta, int n_rows, int layer0, int n_layers, int64_t layer_stride_elems,
                            int Hkv, int D, const float* cos_t, const float* sin_t, int rebase, cudaStream_t st,
-                           int f32) {
+                           int f32, int max_ctas) {
   if (n_rows == 0 || n_layers == 0) return cudaSuccess;
   if (f32) {
     CUDA_TRY_LAUNCH(launch_k(kv_link_f32_kernel, dim3(148 * 8), dim3(256), 0, st, reinterpret_cast<float*>(Kpool),
@@ -564,8 +573,8 @@ cudaError_t launch_kv_link(void* Kpool, void* Vpool, const int32_t* src_slot, co
                              layer_stride_elems, Hkv, D, cos_t, sin_t, rebase));
     return cudaGetLastError();
   }
-  const int64_t total = (int64_t)n_layers * n_rows * Hkv * (D / 16 + D / 8);
-  const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
+  const int64_t warps = (int64_t)n_layers * n_rows;  // one warp per (layer, row)
+  const int blocks = (int)std::min<int64_t>((warps + 7) / 8, max_ctas);
   CUDA_TRY_LAUNCH(launch_k(kv_link_kernel, dim3(blocks), dim3(256), 0, st, reinterpret_cast<uint4*>(Kpool), reinterpret_cast<uint4*>(Vpool), src_slot,
                                          dst_slot, delta, n_rows, layer0, n_layers, layer_stride_elems / 8, Hkv, D,
                                          cos_t, sin_t, rebase));

@@ -78,6 +78,15 @@ extern "C" pic_status pic_test_gemm(const uint16_t* A, const uint16_t* B, int32_
 
 static int g_attn_version = 2, g_attn_grid = 0;
 
+namespace pic {
+extern int g_attn_force;
+}
+extern "C" pic_status pic_test_set_attention_kernel(int32_t version) {
+  if (version < 0 || version > 2) return PIC_E_INVALID_ARG;
+  pic::g_attn_force = version;
+  return PIC_OK;
+}
+
 extern "C" pic_status pic_test_attention_v(const uint16_t* Q, const uint16_t* K, const uint16_t* V, const int32_t* pos,
                                            int32_t M, int32_t n_keys, int32_t Hq, int32_t Hkv,
                                            const int32_t* block_perm, int32_t num_blocks, int32_t n_splits,
@@ -192,6 +201,10 @@ extern "C" pic_status pic_test_attention(const uint16_t* Q, const uint16_t* K, c
   a.Q = dq.p;
   a.row_nsplit = reinterpret_cast<int32_t*>(dns.p);
   a.O = dout.p;
+  DevBuf dctr;
+  TCK(cudaMalloc(&dctr.p, 8));
+  TCK(cudaMemset(dctr.p, 0, 8));
+  a.item_ctr = reinterpret_cast<unsigned*>(dctr.p);
   auto launch = [&]() -> cudaError_t {
     return pp ? launch_attention_pp(tq, tk, tv, tk8, tv8, a, grid, 0) : launch_attention_tc(tq, tk, tv, tk8, tv8, a, 0);
   };

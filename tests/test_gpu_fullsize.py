@@ -166,11 +166,14 @@ def test_long_context_16k_legolink_sampled_rows():
     eng.close()
 
 
+@pytest.mark.parametrize("kernel", [1, 2])
 @pytest.mark.parametrize("which", ["cfg2", "cfg3", "cfg4"])
-def test_fullsize_shared_block_link_bit_identical(which):
+def test_fullsize_shared_block_link_bit_identical(which, kernel):
     """f3 shared-block link at full size in the bench's launch configuration (graphs, batched link for
     cfg4): logits, first tokens and sampled layers' linked K/V are bit-identical to the copy path, which
-    the sampled-layer tests above hold to the oracle."""
+    the sampled-layer tests above hold to the oracle — on the same attention kernel for both paths
+    (1 = one q-tile per CTA, 2 = ping-pong: the engine picks per link, so it is forced here)."""
+    B.set_attention_kernel(kernel)
     w = {"cfg2": sg.cfg2, "cfg3": sg.cfg3}.get(which, lambda: sg.cfg4(n_requests=4))()
     m = w.model
     Ns = [sum(len(w.chunks[s.chunk]) if s.cached else len(s.tokens) for s in r) for r in w.requests]
@@ -190,4 +193,5 @@ def test_fullsize_shared_block_link_bit_identical(which):
                 assert np.array_equal(ka, kb) and np.array_equal(va, vb), l
         assert shared > 0
     finally:
+        B.set_attention_kernel(0)
         eng.close()

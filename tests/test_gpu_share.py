@@ -36,6 +36,15 @@ class Setup:
         return [("cached", self.eids[s.chunk]) if s.cached else ("tokens", s.tokens) for s in segs]
 
 
+@pytest.fixture(scope="module", autouse=True, params=[1, 2], ids=lambda k: f"attn-kernel{k}")
+def attention_kernel(request):
+    """Copy and shared links on the same attention kernel (the engine picks per link: forced here), both
+    the one-lane (1) and the ping-pong (2) kernel's K-tile re-base; D < 128 configs use the SIMT kernel."""
+    B.set_attention_kernel(request.param)
+    yield request.param
+    B.set_attention_kernel(0)
+
+
 @pytest.fixture(scope="module", params=[sg.TINY, sg.TINY_GQA, sg.TINY_D128], ids=lambda c: c.name)
 def setup(request):
     s = Setup(request.param)
