@@ -210,9 +210,11 @@ static void chain_trace_dump(int layer) {
 // The persistent GEMM chain is opt-in (PIC_CHAIN=1): measured on cfg2 it streams each phase at the
 // same rate as the separate kernels, and its norm phases and grid barriers add ~18 µs per layer
 // (4.77 vs 4.28 ms per link), so the separate PDL-chained kernels remain the default.
-// a2 on a side stream overlapping the first layers (PIC_NO_K2_OVERLAP=1: everything on the main stream)
+// a2 on a side stream overlapping the projections (PIC_K2_OVERLAP=1).  Off by default: measured at cfg4
+// (copy path, 32-request waves) the co-running copy kernels slow the tensor-bound GEMMs more than they
+// save — 949 ms per step with a2 on the main stream vs 999 with per-layer side-stream launches.
 static bool k2_overlap() {
-  static const bool on = getenv("PIC_NO_K2_OVERLAP") == nullptr;
+  static const bool on = getenv("PIC_K2_OVERLAP") != nullptr;
   return on;
 }
 
@@ -235,6 +237,13 @@ int g_attn_force = 0;
 // a6 on the persistent ping-pong kernel (attention_pp.cu); PIC_ATTN_V1=1: the one-lane kernel (A/B only)
 static bool attn_pp_enabled() {
   static const bool on = getenv("PIC_ATTN_V1") == nullptr;
+  return on;
+}
+
+// a4 RMSNorm fused across unsplit GEMM boundaries (residual epilogue writes bf16(h·g) + Σh² partials, the
+// consumer's epilogue applies the row scale); PIC_NO_NORM_FUSE=1 keeps the residual_rmsnorm kernel
+static bool norm_fuse() {
+  static const bool on = getenv("PIC_NO_NORM_FUSE") == nullptr;
   return on;
 }
 
@@ -325,6 +334,7 @@ struct ArenaPlan {
   size_t w_qkv, w_o, w_gu, w_down, w_g;  // per layer sizes
   size_t off_layers, layer_bytes;
   size_t off_E, off_lm, off_gf, off_cos, off_sin, off_K, off_V;
+  size_t off_ssq;
   size_t off_h, off_h2, off_ws, off_x, off_O, off_u, off_Q, off_xlast, off_opart, off_ml, off_logits, off_amax,
       off_cbdev, off_plan;
   size_t off_ar, off_tpflags;
@@ -359,6 +369,7 @@ static ArenaPlan plan_arena(const pic_model_config& c, const pic_engine_limits& 
   const size_t M = l.max_rows;
   a.off_h = L.add(M * d * 4);
   a.off_h2 = L.add(M * d * 4);
+  a.off_ssq = L.add(M * kSsqStride * 4);  // fused-norm row partials (Σ h² per n-tile)
   size_t wsf = std::max({M * qkv, M * 2 * F, M * d, (size_t)l.max_requests * V});
   wsf = std::max(wsf, (size_t)148 * 128 * 256 * 2);
   a.ws_floats = wsf;
@@ -596,6 +607,7 @@ static pic_status init_device(pic_engine* e, void* arena, size_t bytes, cudaStre
   const int64_t M = e->lim.max_rows;
   e->h = reinterpret_cast<float*>(b + a.off_h);
   e->h2 = reinterpret_cast<float*>(b + a.off_h2);
+  e->ssq = reinterpret_cast<float*>(b + a.off_ssq);
   e->ws = reinterpret_cast<float*>(b + a.off_ws);
   e->ws_floats = a.ws_floats;
   e->x = b + a.off_x;
@@ -1129,8 +1141,11 @@ struct Runner {
   }
   // a7 / a8-down: h += A·Bᵀ in the epilogue of an unsplit GEMM (*splits_out = 0), else split-K partials
   // for the residual kernel.  Not under tensor parallelism (the partials are all-reduced first).
+  // norm_gain (nullable): also write x = bf16(h_new·g) + Σh² partials (*norm_tiles = n-tiles, 0 if not fused)
   pic_status gemm_resid(const CUtensorMap& A, const CUtensorMap* B3, int M, int N, int K, float* h, int* splits_out,
-                        const void* A_ptr, const void* B_ptr) {
+                        const void* A_ptr, const void* B_ptr, const float* norm_gain = nullptr, void* xg = nullptr,
+                        int* norm_tiles = nullptr) {
+    if (norm_tiles) *norm_tiles = 0;
     int bn = 0;
     pic_status err;
     const CUtensorMap* Bm = e->tp_size == 1 ? fused_map(B3, B_ptr, M, N, K, false, &bn, &err) : nullptr;
@@ -1138,8 +1153,23 @@ struct Runner {
     if (!Bm) return gemm(A, B3, M, N, K, splits_out, A_ptr, B_ptr);
     *splits_out = 0;
     ++launches;
-    PROF("gemm", (double)N * K * 2, 2.0 * M * N * K, launch_gemm_resid(A, *Bm, h, M, N, K, bn, st));
+    GemmEpi ep{};
+    if (norm_gain && (N + bn - 1) / bn <= kSsqStride) {
+      ep.norm_gain = norm_gain;
+      ep.xg = xg;
+      ep.ssq = e->ssq;
+      if (norm_tiles) *norm_tiles = (N + bn - 1) / bn;
+    }
+    PROF("gemm", (double)N * K * 2, 2.0 * M * N * K, launch_gemm_resid(A, *Bm, h, M, N, K, bn, st, GemmNext{}, ep));
     return PIC_OK;
+  }
+  // will this QKV projection run on the fused-epilogue GEMM (so it can take a fused-norm input)?
+  bool qkv_fusable(const LayerW& w, int M) {
+    if (e->cfg.head_dim != 128) return false;
+    int bn = 0;
+    pic_status err;
+    const int qkv = (e->cfg.n_heads + 2 * e->cfg.n_kv_heads) * 128;
+    return fused_map(w.tm_qkv, w.qkv, M, qkv, e->cfg.d_model, true, &bn, &err) != nullptr && err == PIC_OK;
   }
   // a5: QKV projection with RoPE + scatter in the epilogue of an unsplit GEMM (*fused = true), else
   // split-K partials for qkv_rope_scatter.
@@ -1241,6 +1271,16 @@ static pic_status enqueue_forward(pic_engine* e, const Fwd& f, const DevPlan& dp
                          c.d_model <= 4096 &&
                          f.M > 0;
   bool qkv_done = false;  // this layer's QKV partials were produced by the previous layer's chain
+  // fused norm state: x holds bf16(h·g) and e->ssq the row partials of `norm_tiles` n-tiles (0: x is normalised)
+  int norm_tiles = 0;
+  const bool nf = norm_fuse() && !e->f32 && e->tp_size == 1 && !f.cb && !use_chain;
+  auto ep_norm_in = [&](GemmEpi& ep) {
+    if (!norm_tiles) return;
+    ep.ssq_in = e->ssq;
+    ep.ssq_in_n = norm_tiles;
+    ep.inv_d = 1.f / (float)d;
+    ep.eps = eps;
+  };
   bool qkv_fused = false;  // this layer's RoPE + scatter ran in the QKV GEMM's epilogue
   int s_chain_qkv = 0;
   for (int l = 0; l < L; ++l) {
@@ -1253,15 +1293,20 @@ static pic_status enqueue_forward(pic_engine* e, const Fwd& f, const DevPlan& dp
       s = s_chain_qkv;
       qkv_done = false;
     } else {
-      ++R.launches;
-      TRY(add_norm(prevP, prev_s, w.g1, e->x, nullptr, M, (double)M * d * 2));
+      if (!norm_tiles) {
+        ++R.launches;
+        TRY(add_norm(prevP, prev_s, w.g1, e->x, nullptr, M, (double)M * d * 2));
+      }
       if (l > 0) TRY(capture(l - 1));
       if (f.cb && l == f.cb_layer) {  // CacheBlend's check needs the partials of all N rows
         TRY(R.gemm(e->tm_x, w.tm_qkv, M, qkv, d, &s, e->x, w.qkv));
       } else {
-        const GemmEpi ep{pos, slot, e->cos_t, e->sin_t, e->Q, Kl, Vl, Hq, Hkv};
+        GemmEpi ep{pos, slot, e->cos_t, e->sin_t, e->Q, Kl, Vl, Hq, Hkv};
+        ep_norm_in(ep);
         TRY(R.gemm_qkv(e->tm_x, w.tm_qkv, M, qkv, d, ep, &s, &qkv_fused, e->x, w.qkv));
+        if (norm_tiles && !qkv_fused) return fail(PIC_E_CUDA, "internal: fused-norm input reached an unfused QKV GEMM");
       }
+      norm_tiles = 0;
     }
     // CacheBlend: the side-stream K2 covers every cached row (the selection is device-side), including
     // the rows this layer's scatter rewrites, so it must land before the scatter, not just before attention
@@ -1424,22 +1469,32 @@ static pic_status enqueue_forward(pic_engine* e, const Fwd& f, const DevPlan& dp
       continue;
     }
     // a7 O projection, residual + a8 MLP
-    TRY(R.gemm_resid(e->tm_O, w.tm_o, M, d, Hq * D, hc, &s, e->Obuf, w.o));
-    ++R.launches;
-    TRY(add_norm(s ? e->ws : nullptr, s, w.g2, e->x, nullptr, M, (double)M * d * 2));
+    const bool gu_pair = e->gu_group > 0 && swiglu_pair(e, M, 2 * F);
+    const bool fuse_g2 = nf && e->gu_group > 0 && !gu_pair;
+    TRY(R.gemm_resid(e->tm_O, w.tm_o, M, d, Hq * D, hc, &s, e->Obuf, w.o, fuse_g2 ? w.g2 : nullptr, e->x,
+                     &norm_tiles));
+    if (!norm_tiles) {
+      ++R.launches;
+      TRY(add_norm(s ? e->ws : nullptr, s, w.g2, e->x, nullptr, M, (double)M * d * 2));
+    }
     if (e->gu_group > 0) {
       ++R.launches;
-      const bool pair = swiglu_pair(e, M, 2 * F);
       const CUtensorMap* Bg = &w.tm_gu_fused;
-      if (pair) TRY(weight_map(e, w.gu, 2 * F, d, e->gu_group, &Bg));  // each CTA: the gate or the up half
+      if (gu_pair) TRY(weight_map(e, w.gu, 2 * F, d, e->gu_group, &Bg));  // each CTA: the gate or the up half
+      GemmEpi ep{};
+      ep_norm_in(ep);
+      norm_tiles = 0;
       PROF("gemm", (double)2 * F * d * 2, 2.0 * M * 2 * F * d,
-           launch_gemm_swiglu(e->tm_x, *Bg, e->u, M, 2 * F, d, 2 * e->gu_group, st, 0, GemmNext{}, pair ? 1 : 0));
+           launch_gemm_swiglu(e->tm_x, *Bg, e->u, M, 2 * F, d, 2 * e->gu_group, st, 0, GemmNext{}, gu_pair ? 1 : 0, ep));
     } else {
       TRY(R.gemm(e->tm_x, w.tm_gu, M, 2 * F, d, &s, e->x, w.gu));
       ++R.launches;
       PROF("swiglu", (double)M * 2 * F * 4 * s + (double)M * F * 2, 0, launch_swiglu(e->ws, s, e->u, M, F, st, e->f32));
     }
-    TRY(R.gemm_resid(e->tm_u, w.tm_down, M, d, F, hc, &s, e->u, w.down));
+    // the next layer's a4 fused into this epilogue when its QKV GEMM takes the fused input
+    const bool fuse_g1 = nf && l + 1 < L && R.qkv_fusable(e->layers[l + 1], M);
+    TRY(R.gemm_resid(e->tm_u, w.tm_down, M, d, F, hc, &s, e->u, w.down, fuse_g1 ? e->layers[l + 1].g1 : nullptr,
+                     e->x, &norm_tiles));
     prevP = s ? e->ws : nullptr;
     prev_s = s;
   }

@@ -152,6 +152,7 @@ struct pic_engine {
   CUtensorMap tm_K, tm_V, tm_K8, tm_V8;  // one-block and eight-block boxes
   // activations / workspaces
   float *h = nullptr, *h2 = nullptr, *ws = nullptr;
+  float* ssq = nullptr;  // fused-norm row partials [max_rows][kSsqStride]
   size_t ws_floats = 0;
   void *x = nullptr, *Obuf = nullptr, *u = nullptr, *Q = nullptr, *x_last = nullptr;
   float *o_part = nullptr, *ml_part = nullptr;

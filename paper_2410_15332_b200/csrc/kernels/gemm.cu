@@ -75,6 +75,15 @@ constexpr int gemm_stages(int bn, int cl = 1) {
 //   EPI_SWIGLU (split-K = 1): B rows are W_gate/W_up interleaved in groups of BN/2 (n-tile = gate rows
 //     [n·BN/2, (n+1)·BN/2) then the matching up rows); out = bf16 u[M][N/2] = silu(gate) ⊙ up
 //     (the a8 SwiGLU fused into the GEMM epilogue; P:241 Llama-family MLP, reading R4).
+// r of a fused-norm consumer row (1 when the A operand was normalised by the residual kernel)
+PIC_DEV float norm_scale(const GemmEpi& ep, int row, int M) {
+  if (!ep.ssq_in || row >= M) return 1.f;
+  const float* p = ep.ssq_in + (size_t)row * kSsqStride;
+  float s = 0.f;
+  for (int t = 0; t < ep.ssq_in_n; ++t) s += p[t];
+  return rsqrtf(s * ep.inv_d + ep.eps);
+}
+
 template <int BN, int STAGES, int EPI>
 __global__ void __launch_bounds__(192, 1)
     gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -242,14 +251,21 @@ __global__ void __launch_bounds__(192, 1)
         float* obase = reinterpret_cast<float*>(out_) + (size_t)sp * M * N;
         float* orow = obase + (size_t)row * N;
         const int ncol = min(BN, N - n0);  // multiple of 16
-        auto put4 = [&](float* dst, float4 v) {
+        // fused norm: xg = bf16(h_new · g) and Σ h_new² of this n-tile per row (EPI_RESID, ep.norm_gain set)
+        const bool fnorm = EPI == EPI_RESID && ep.norm_gain != nullptr;
+        auto put4 = [&](float* dst, float4 v, float4 h, float4 g, float& ss) {
           if constexpr (EPI == EPI_RESID) {
-            const float4 h = *reinterpret_cast<const float4*>(dst);
             v = make_float4(h.x + v.x, h.y + v.y, h.z + v.z, h.w + v.w);
+            if (fnorm) {
+              ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+              *reinterpret_cast<uint2*>(reinterpret_cast<uint16_t*>(ep.xg) + (dst - obase)) =
+                  make_uint2(pack_bf16(v.x * g.x, v.y * g.y), pack_bf16(v.z * g.z, v.w * g.w));
+            }
           }
           *reinterpret_cast<float4*>(dst) = v;
         };
         if (nkb > 0 && stage) {
+          float ssr[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};  // rows i * 4 + lane / 8 of this warp
 #pragma unroll 1
           for (int c = 0; c < BN; c += 32) {
             float v[32];
@@ -260,24 +276,61 @@ __global__ void __launch_bounds__(192, 1)
               sb[lane * 8 + (j ^ (lane & 7))] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
             __syncwarp();
             const int jj = lane & 7;
+            const bool cok = c + 4 * jj < ncol;
+            // all residual loads of the chunk first: the xg stores below may alias h as far as the
+            // compiler knows, and would otherwise serialise every load behind the previous store
+            float4 hv[8];
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
               const int r = i * 4 + (lane >> 3);
-              if (mrow0 + r < M && c + 4 * jj < ncol)
-                put4(obase + (size_t)(mrow0 + r) * N + n0 + c + 4 * jj, sb[r * 8 + (jj ^ (r & 7))]);
+              hv[i] = (EPI == EPI_RESID && mrow0 + r < M && cok)
+                          ? *reinterpret_cast<const float4*>(obase + (size_t)(mrow0 + r) * N + n0 + c + 4 * jj)
+                          : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+            const float4 gq = fnorm && cok ? *reinterpret_cast<const float4*>(ep.norm_gain + n0 + c + 4 * jj)
+                                           : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const int r = i * 4 + (lane >> 3);
+              if (mrow0 + r < M && cok)
+                put4(obase + (size_t)(mrow0 + r) * N + n0 + c + 4 * jj, sb[r * 8 + (jj ^ (r & 7))], hv[i], gq, ssr[i]);
+            }
+          }
+          if (fnorm) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              float t = ssr[i];
+              t += __shfl_xor_sync(0xffffffffu, t, 1);
+              t += __shfl_xor_sync(0xffffffffu, t, 2);
+              t += __shfl_xor_sync(0xffffffffu, t, 4);
+              const int r = i * 4 + (lane >> 3);
+              if ((lane & 7) == 0 && mrow0 + r < M) ep.ssq[(size_t)(mrow0 + r) * kSsqStride + n_idx] = t;
             }
           }
         } else if (nkb > 0) {
+          float ss = 0.f;
 #pragma unroll 1
           for (int c = 0; c < BN; c += 32) {
             float v[32];
             tmem_ld32(tl + c, v);  // columns beyond BN are allocated (power-of-2 TMEM) and ignored
-            if (row < M)
+            if (row < M) {
+              float4 hv[8], gq[8];
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {  // loads first (see the staged path)
+                const bool cok = c + 4 * j < ncol;
+                hv[j] = EPI == EPI_RESID && cok ? *reinterpret_cast<const float4*>(orow + n0 + c + 4 * j)
+                                                : make_float4(0.f, 0.f, 0.f, 0.f);
+                gq[j] = fnorm && cok ? *reinterpret_cast<const float4*>(ep.norm_gain + n0 + c + 4 * j)
+                                     : make_float4(0.f, 0.f, 0.f, 0.f);
+              }
 #pragma unroll
               for (int j = 0; j < 8; ++j)
                 if (c + 4 * j < ncol)
-                  put4(orow + n0 + c + 4 * j, make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]));
+                  put4(orow + n0 + c + 4 * j, make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]), hv[j],
+                       gq[j], ss);
+            }
           }
+          if (fnorm && row < M) ep.ssq[(size_t)row * kSsqStride + n_idx] = ss;
         } else if (row < M && EPI == EPI_PARTIAL) {
           for (int col = n0; col < n0 + ncol; col += 4)
             *reinterpret_cast<float4*>(orow + col) = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -285,6 +338,7 @@ __global__ void __launch_bounds__(192, 1)
       } else if constexpr (EPI == EPI_QKV) {
         // every lane runs the (warp-collective) TMEM loads; rows beyond M only skip their stores
         const bool ok = row < M;
+        const float rs = norm_scale(ep, row, M);  // fused RMSNorm row scale (1 if the input was normalised)
         const int p = ok ? ep.pos[row] : 0, sl = ok ? ep.slot[row] : 0;
         const float* cp = ep.cos_t + (size_t)p * 64;
         const float* spn = ep.sin_t + (size_t)p * 64;
@@ -302,6 +356,11 @@ __global__ void __launch_bounds__(192, 1)
               float a[16], b[16], cs[16], sn[16];
               tmem_ld16(th + c, a);
               tmem_ld16(th + 64 + c, b);
+#pragma unroll
+              for (int j = 0; j < 16; ++j) {
+                a[j] *= rs;
+                b[j] *= rs;
+              }
 #pragma unroll
               for (int j = 0; j < 4; ++j) {
                 const float4 c4 = *reinterpret_cast<const float4*>(cp + c + 4 * j);
@@ -326,7 +385,7 @@ __global__ void __launch_bounds__(192, 1)
               tmem_ld32(th + c, v);
               uint32_t pk[16];
 #pragma unroll
-              for (int j = 0; j < 16; ++j) pk[j] = pack_bf16(v[2 * j], v[2 * j + 1]);
+              for (int j = 0; j < 16; ++j) pk[j] = pack_bf16(v[2 * j] * rs, v[2 * j + 1] * rs);
               if (ok)
 #pragma unroll
                 for (int j = 0; j < 4; ++j)
@@ -341,6 +400,7 @@ __global__ void __launch_bounds__(192, 1)
         const int F = N / 2;
         uint16_t* urow = reinterpret_cast<uint16_t*>(out_) + (size_t)row * F + (size_t)n_idx * G;
         uint4* sb = reinterpret_cast<uint4*>(stg);
+        const float rs = norm_scale(ep, row, M);  // fused RMSNorm row scale (1 if the input was normalised)
 #pragma unroll 1
         for (int c = 0; c < G; c += 16) {
           float gv[16], uv[16];
@@ -349,8 +409,8 @@ __global__ void __launch_bounds__(192, 1)
           uint32_t pk[8];
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
-            const float g0 = gv[2 * j], g1 = gv[2 * j + 1];
-            pk[j] = pack_bf16(g0 / (1.f + __expf(-g0)) * uv[2 * j], g1 / (1.f + __expf(-g1)) * uv[2 * j + 1]);
+            const float g0 = gv[2 * j] * rs, g1 = gv[2 * j + 1] * rs;
+            pk[j] = pack_bf16(g0 / (1.f + __expf(-g0)) * (uv[2 * j] * rs), g1 / (1.f + __expf(-g1)) * (uv[2 * j + 1] * rs));
           }
           if (stage) {
             sb[lane * PS + c / 8] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
@@ -843,11 +903,12 @@ bool gemm_resid_supported(int bn) {
 }
 
 cudaError_t launch_gemm_resid(const CUtensorMap& A, const CUtensorMap& B, float* h, int M, int N, int K, int bn,
-                              cudaStream_t st, const GemmNext& nx) {
+                              cudaStream_t st, const GemmNext& nx, const GemmEpi& ep) {
+  if (ep.norm_gain && (N + bn - 1) / bn > kSsqStride) return cudaErrorInvalidValue;
   switch (bn) {
 #define L5(b) \
   case b:     \
-    return launch_gemm_t<b, EPI_RESID>(A, B, h, M, N, K, 1, 0, st, nx);
+    return launch_gemm_t<b, EPI_RESID>(A, B, h, M, N, K, 1, 0, st, nx, ep);
     PIC_RESID_BNS(L5)
 #undef L5
   }
@@ -895,8 +956,9 @@ cudaError_t launch_gemm_partial(const CUtensorMap& A, const CUtensorMap& B, floa
 }
 
 cudaError_t launch_gemm_swiglu(const CUtensorMap& A, const CUtensorMap& B, void* u, int M, int N2, int K, int bn,
-                               cudaStream_t st, int pack, const GemmNext& nx, int pair) {
+                               cudaStream_t st, int pack, const GemmNext& nx, int pair, const GemmEpi& ep) {
   if (pair) {
+    if (ep.ssq_in) return cudaErrorInvalidValue;  // the CTA-pair epilogue has no fused-norm row scale
     switch (bn) {
 #define L4(b) \
   case b:     \
@@ -909,7 +971,7 @@ cudaError_t launch_gemm_swiglu(const CUtensorMap& A, const CUtensorMap& B, void*
   switch (bn) {
 #define L2(b) \
   case b:     \
-    return launch_gemm_t<b, EPI_SWIGLU>(A, B, u, M, N2, K, 1, pack, st, nx);
+    return launch_gemm_t<b, EPI_SWIGLU>(A, B, u, M, N2, K, 1, pack, st, nx, ep);
     PIC_SWIGLU_BNS(L2)
 #undef L2
   }

@@ -98,7 +98,18 @@ struct GemmEpi {
   void* Kl;
   void* Vl;
   int Hq, Hkv;
+  // a4 fused across the GEMM boundary (unsplit GEMMs): the residual epilogue (EPI_RESID, norm_gain set)
+  // also writes xg = bf16(h_new · g) [M][N] and per (row, n-tile) Σ h_new² into ssq [M][kSsqStride]; the
+  // consuming GEMM's epilogue (EPI_QKV / EPI_SWIGLU, ssq_in set) scales its accumulator rows by
+  // r = rsqrt(Σ_t ssq_in[row][t] / d + eps): x·W = r · (h·g)·W, so RMSNorm needs no kernel of its own.
+  const float* norm_gain;
+  void* xg;
+  float* ssq;
+  const float* ssq_in;
+  int ssq_in_n;
+  float inv_d, eps;
 };
+constexpr int kSsqStride = 32;  // max n-tiles per row of a fused-norm residual GEMM
 // pair = 1: CTA-pair (cta_group::2) kernel with 256-row M-tiles; B's tensor map box must then be bn/2 rows
 // (each CTA of the pair loads half of the N-tile); bn in gemm_pair_supported().
 cudaError_t launch_gemm_partial(const CUtensorMap& A, const CUtensorMap& B, float* out, int M, int N, int K,
@@ -109,14 +120,15 @@ bool gemm_pair_supported(int bn);
 //   resid: h[M][N] += A·Bᵀ (a7 O projection / a8 down projection + residual add, fp32 h)
 //   qkv:   A·W_qkvᵀ -> RoPE at pos -> Q dense, K/V -> pool slots (a5); bn = 128 or 256 (whole heads)
 cudaError_t launch_gemm_resid(const CUtensorMap& A, const CUtensorMap& B, float* h, int M, int N, int K, int bn,
-                              cudaStream_t st, const GemmNext& nx = GemmNext{});
+                              cudaStream_t st, const GemmNext& nx = GemmNext{}, const GemmEpi& ep = GemmEpi{});
 cudaError_t launch_gemm_qkv(const CUtensorMap& A, const CUtensorMap& B, const GemmEpi& ep, int M, int N, int K,
                             int bn, cudaStream_t st, const GemmNext& nx = GemmNext{});
 bool gemm_resid_supported(int bn);
 // Gate/up GEMM with the SwiGLU epilogue fused: B = interleaved [gate|up] groups of bn/2 rows (N2 = 2F rows),
 // u[M][F] bf16 = silu(x·W_gᵀ) ⊙ (x·W_uᵀ).  Split-K 1.
 cudaError_t launch_gemm_swiglu(const CUtensorMap& A, const CUtensorMap& B, void* u, int M, int N2, int K, int bn,
-                               cudaStream_t st, int pack = 0, const GemmNext& nx = GemmNext{}, int pair = 0);
+                               cudaStream_t st, int pack = 0, const GemmNext& nx = GemmNext{}, int pair = 0,
+                               const GemmEpi& ep = GemmEpi{});
 bool gemm_bn_supported(int bn, bool swiglu);
 
 // ---- persistent GEMM chain (gemm_chain.cu): O-proj -> residual+RMSNorm -> gate/up+SwiGLU -> down ->
