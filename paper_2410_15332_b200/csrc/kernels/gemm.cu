@@ -57,7 +57,12 @@ struct GemmSmem {
   static constexpr int kB = (BN / CL) * 64 * 2;  // a CTA pair splits the N-tile: each CTA holds BN/2 rows of B
   static constexpr int kStage = kA + kB;
   static constexpr int kBars = 2 * STAGES + 4;
-  static constexpr int kBytes = STAGES * kStage + kBars * 8 + 16;
+  static constexpr int kRing = STAGES * kStage + kBars * 8 + 16;
+  // dedicated epilogue staging (4 warps x [32 rows][32 fp32]) when it fits beside the ring: every unit's
+  // residual / partial stores leave as full 128-B row segments, not only the last unit's
+  static constexpr int kStgOff = (kRing + 1023) / 1024 * 1024;
+  static constexpr int kStg = (CL == 1 && kStgOff + 16384 <= 232448) ? 16384 : 0;
+  static constexpr int kBytes = kStg ? kStgOff + kStg : kRing;
   static constexpr int kAcc = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;  // TMEM cols per accumulator
   static constexpr int kTmemCols = 2 * kAcc;                                              // double buffered
   static_assert(BN % 16 == 0 && BN <= 256, "UMMA N (M=128): multiple of 16, <= 256");
@@ -241,8 +246,12 @@ __global__ void __launch_bounds__(192, 1)
       // The last unit of a CTA runs after its final MMA, when the smem ring is idle: stage the tile
       // through the ring so that global stores are full 128-B row segments (a row-per-thread store
       // pattern costs ~4 us per tile in uncoalesced 16-B transactions).
-      const bool stage = u + (int)gridDim.x >= units;
-      uint8_t* stg = smem + (size_t)(warp - 2) * ((BN + 31) / 32) * 4096;
+      const bool last = u + (int)gridDim.x >= units;
+      const bool stage = last || ((EPI == EPI_PARTIAL || EPI == EPI_RESID) && S::kStg > 0);
+      // the ring is idle after the last unit's MMAs; otherwise the dedicated 4 KB per warp (one chunk)
+      uint8_t* stg = last ? smem + (size_t)(warp - 2) * ((BN + 31) / 32) * 4096
+                          : smem + S::kStgOff + (size_t)(warp - 2) * 4096;
+      const int stg_chunk = last ? 4096 : 0;  // bytes between consecutive 32-column chunks
       const int mrow0 = m0 + q * 32;
       if constexpr (EPI == EPI_PARTIAL || EPI == EPI_RESID) {
         // EPI_RESID (split-K = 1): out = the fp32 residual h, h += acc (the a7/a8 residual add: the same
@@ -270,7 +279,8 @@ __global__ void __launch_bounds__(192, 1)
           for (int c = 0; c < BN; c += 32) {
             float v[32];
             tmem_ld32(tl + c, v);
-            float4* sb = reinterpret_cast<float4*>(stg + (c / 32) * 4096);  // [32 rows][8 float4], XOR-swizzled
+            __syncwarp();  // the previous chunk's reads of a reused staging buffer are done
+            float4* sb = reinterpret_cast<float4*>(stg + (c / 32) * stg_chunk);  // [32 rows][8 float4], XOR-swizzled
 #pragma unroll
             for (int j = 0; j < 8; ++j)
               sb[lane * 8 + (j ^ (lane & 7))] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
@@ -681,6 +691,7 @@ __global__ void __launch_bounds__(192, 1)
       // pattern costs ~4 us per tile in uncoalesced 16-B transactions).
       const bool stage = u + ncl >= units;
       uint8_t* stg = smem + (size_t)(warp - 2) * ((BN + 31) / 32) * 4096;
+      constexpr int stg_chunk = 4096;
       const int mrow0 = m0 + q * 32;
       if constexpr (EPI == EPI_PARTIAL) {
         const int sp = (u / mt) % splits;
@@ -692,7 +703,8 @@ __global__ void __launch_bounds__(192, 1)
           for (int c = 0; c < BN; c += 32) {
             float v[32];
             tmem_ld32(tl + c, v);
-            float4* sb = reinterpret_cast<float4*>(stg + (c / 32) * 4096);  // [32 rows][8 float4], XOR-swizzled
+            __syncwarp();  // the previous chunk's reads of a reused staging buffer are done
+            float4* sb = reinterpret_cast<float4*>(stg + (c / 32) * stg_chunk);  // [32 rows][8 float4], XOR-swizzled
 #pragma unroll
             for (int j = 0; j < 8; ++j)
               sb[lane * 8 + (j ^ (lane & 7))] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
