@@ -15,6 +15,9 @@
 // reduction order is fixed and the result deterministic.
 #include <cuda.h>
 
+#include <algorithm>
+#include <cmath>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -129,10 +132,17 @@ __global__ void __launch_bounds__(192, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  // unit u -> (m fastest, then split, then n): concurrently running CTAs share weight tiles in L2
+  // unit u -> (m fastest, then split, then n): concurrently running CTAs share weight tiles in L2.  With
+  // ep.raster_gm > 0 (split-K 1, A larger than L2 wants) the m-tiles go in groups of raster_gm, each group
+  // sweeping all n-tiles before the next: one wave reuses raster_gm A row-blocks and 148 / raster_gm
+  // weight n-tiles from L2 instead of streaming all of A once per n-tile band.
+  const int GM = (ep.raster_gm > 0 && splits == 1) ? min(ep.raster_gm, mt) : mt;
   auto decode = [&](int u, int& m0, int& n_idx, int& kb0, int& nkb) {
-    const int m = u % mt;
-    const int r = u / mt;
+    const int grp = u / (GM * nt * splits);
+    const int mb = grp * GM, gme = min(GM, mt - mb);
+    const int v = u - grp * GM * nt * splits;
+    const int m = mb + v % gme;
+    const int r = v / gme;
     const int sp = r % splits;
     n_idx = r / splits;
     m0 = m * 128;
@@ -828,8 +838,19 @@ static cudaError_t launch_gemm_t(const CUtensorMap& A, const CUtensorMap& B, voi
   const int max_cl = 148 / CL;
   const int grid = CL * (units < max_cl ? units : max_cl);  // persistent: one CTA (pair) per SM (pair)
   if constexpr (CL == 1) {
+    GemmEpi e2 = ep;
+    if (splits == 1 && e2.raster_gm == 0) {
+      // traffic of a wave order with groups of gm m-tiles: A·(nt·gm/148) + B·(mt/gm); when A fits in L2
+      // beside the weight tiles (< 64 MB) the plain m-fastest order already reads it once
+      const double a_mb = (double)M * K * 2 / 1e6, b_mb = (double)N * K * 2 / 1e6;
+      const int mt = (M + 127) / 128, nt = (N + BN - 1) / BN;
+      if (a_mb > 64.0 && mt > 1) {
+        const double g = std::sqrt(b_mb * mt * 148.0 / (a_mb * nt));
+        e2.raster_gm = std::max(1, std::min(mt, (int)(g + 0.5)));
+      }
+    }
     CUDA_TRY_LAUNCH(launch_k(kern, dim3(grid), dim3(192), S::kBytes, st, A, B, out, M, N, kblk, per, splits, pack,
-                             g_gemm_trace, nx.tm ? *nx.tm : B, nx, ep));
+                             g_gemm_trace, nx.tm ? *nx.tm : B, nx, e2));
   } else {
     if (pack) return cudaErrorInvalidValue;
     cudaLaunchConfig_t cfg = {};

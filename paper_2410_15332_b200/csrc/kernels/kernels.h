@@ -108,6 +108,7 @@ struct GemmEpi {
   const float* ssq_in;
   int ssq_in_n;
   float inv_d, eps;
+  int raster_gm;  // m-tiles per raster group (0: the launcher chooses; see gemm.cu decode)
 };
 constexpr int kSsqStride = 32;  // max n-tiles per row of a fused-norm residual GEMM
 // pair = 1: CTA-pair (cta_group::2) kernel with 256-row M-tiles; B's tensor map box must then be bn/2 rows
