@@ -1388,6 +1388,8 @@ static pic_status enqueue_forward(pic_engine* e, const Fwd& f, const DevPlan& dp
       a.row_nsplit = main_tiles ? dp.attn_nsplit : dp.attn_nsplit2;
       a.O = e->Obuf;  // unsplit q-tiles write their normalised bf16 output here directly
       a.item_ctr = e->attn_ctr;
+      static const int attn_debug = getenv("PIC_ATTN_DEBUG") ? atoi(getenv("PIC_ATTN_DEBUG")) : 0;
+      a.debug = attn_debug;
       const int max_split = main_tiles ? f.attn_max_split : f.attn_max_split2;
       ++R.launches;
       if (f.attn_pp)

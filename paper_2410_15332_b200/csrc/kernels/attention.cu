@@ -190,13 +190,18 @@ __global__ void __launch_bounds__(ROT ? 320 + 32 * kRotWarps : 320, 1)
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------------ MMA issuer
-    if (lane == 0 && n > 0) {
+    // The whole warp runs the loop (convergent: descriptors and loop state stay uniform) and elect.sync
+    // issues; a lane-0 branch with per-MMA descriptor arithmetic capped issue at ~88 cycles per MMA, above
+    // the 64-cycle M=128 N=128 K=16 pipe time (scripts/probe_tc.cu).
+    if (n > 0) {
       constexpr uint32_t idS = idesc_bf16(128, 128, 0, 0);  // Q (smem, K-major) x K (smem, K-major)
       constexpr uint32_t idO = idesc_bf16(128, 128, 0, 1);  // P (TMEM, K-major) x V (smem, MN-major)
+      const uint64_t dQ = sdesc_sw128(base + kQ, 16, 1024), dK0 = sdesc_sw128(base + kK, 16, 1024);
+      const uint64_t dV0 = sdesc_sw128(base + kV, kTile, 1024);
       unsigned long long w_k = 0, w_p = 0, w_v = 0, q0 = 0;
       mbar_wait(q_full, 0);
       tc_fence_after();
-      if (tr) tr[2] = globaltimer();
+      if (tr && lane == 0) tr[2] = globaltimer();
       auto issue_pv = [&](int u) {
         const int pb = u & 1, vs = u % S;
         if (tr) q0 = globaltimer();
@@ -209,16 +214,16 @@ __global__ void __launch_bounds__(ROT ? 320 + 32 * kRotWarps : 320, 1)
         mbar_wait(v_full + 8 * vs, (u / S) & 1);
         if (tr) w_v += globaltimer() - q0;
         tc_fence_after();
+        const uint64_t dv = dV0 + (uint64_t)(vs * (2 * kTile / 16));
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
           // keys 16kk..16kk+15: P half kk/4 at S-buffer column 64·(kk/4), 8 columns per 16 keys
           const uint32_t pa = tmem + kTmS + pb * 128 + (kk >> 2) * 64 + (kk & 3) * 8;
-          const uint32_t vb = base + kV + (2 * vs) * kTile + kk * 2048;  // 16 keys x 128 B
           // O accumulates in TMEM across KV tiles (rescaled by the softmax warps when needed)
-          umma_bf16_ts(tmem + kTmO, pa, sdesc_sw128(vb, kTile, 1024), idO, (u | kk) != 0);
+          umma_bf16_ts_e(tmem + kTmO, pa, dv + (uint64_t)(kk * 2048 / 16), idO, (u | kk) != 0);
         }
-        umma_commit(o_full + 8 * pb);
-        umma_commit(v_empty + 8 * vs);
+        umma_commit_e(o_full + 8 * pb);
+        umma_commit_e(v_empty + 8 * vs);
       };
       for (int t = 0; t < n; ++t) {
         const int sb = t & 1, ks = t % S;
@@ -227,18 +232,18 @@ __global__ void __launch_bounds__(ROT ? 320 + 32 * kRotWarps : 320, 1)
         if (tr) w_k += globaltimer() - q0;
         tc_fence_after();
         // S(t) overwrites the buffer holding P(t-2): PV(t-2) was issued before and MMAs run in order
+        const uint64_t dk = dK0 + (uint64_t)(ks * (2 * kTile / 16));
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
-          const uint32_t kb = base + kK + (2 * ks + (kk >> 2)) * kTile + (kk & 3) * 32;
-          const uint32_t qa = base + kQ + (kk >> 2) * kTile + (kk & 3) * 32;
-          umma_bf16(tmem + kTmS + sb * 128, sdesc_sw128(qa, 16, 1024), sdesc_sw128(kb, 16, 1024), idS, kk > 0);
+          const uint64_t o = (uint64_t)(((kk >> 2) * kTile + (kk & 3) * 32) >> 4);
+          umma_bf16_e(tmem + kTmS + sb * 128, dQ + o, dk + o, idS, kk > 0);
         }
-        umma_commit(s_full + 8 * sb);
-        umma_commit(k_empty + 8 * ks);
+        umma_commit_e(s_full + 8 * sb);
+        umma_commit_e(k_empty + 8 * ks);
         if (t >= 1) issue_pv(t - 1);
       }
       issue_pv(n - 1);
-      if (tr) {
+      if (tr && lane == 0) {
         tr[11] = w_k;
         tr[12] = w_p;
         tr[13] = w_v;

@@ -541,6 +541,12 @@ __global__ void __launch_bounds__(384, 1)
         const unsigned long long tw1 = tr ? clk() : 0;
         if (tr) tacc[0] += tw1 - tw;
         tc_fence_after();
+        if (a.debug == 1) {  // ablation: hand S straight back as P (timing only)
+          tc_fence_before();
+          mbar_arrive(B(bPFull + x));
+          ++cs;
+          continue;
+        }
         float sv[128];
         tmem_ld128_split(sAddr, sv);
         const int key0 = (P.j0 + s) * 128;

@@ -214,8 +214,11 @@ __global__ void __launch_bounds__(192, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    {
+      // whole warp, elect.sync issue, base descriptors + constant offsets (a lane-0 branch recomputing
+      // descriptors per MMA issues at ~88 cycles per MMA: above the pipe time of N <= 224)
       constexpr uint32_t idesc = idesc_bf16(128, BN, 0, 0);
+      const uint64_t dA0 = sdesc_sw128(smem_u32(sA), 16, 1024), dB0 = sdesc_sw128(smem_u32(sB), 16, 1024);
       int it = 0, i = 0;
       for (int u = blockIdx.x; u < units; u += gridDim.x, ++i) {
         int m0, n_idx, kb0, nkb;
@@ -227,18 +230,16 @@ __global__ void __launch_bounds__(192, 1)
         for (int kk = 0; kk < nkb; ++kk, ++it) {
           const int s = it % STAGES;
           mbar_wait(full0 + 8 * s, (it / STAGES) & 1);
-          if (trace && it == 0) trace[blockIdx.x * 6 + 2] = globaltimer();
+          if (trace && it == 0 && lane == 0) trace[blockIdx.x * 6 + 2] = globaltimer();
           tc_fence_after();
-          const uint32_t a = smem_u32(sA + s * S::kA), b = smem_u32(sB + s * S::kB);
+          const uint64_t da = dA0 + (uint64_t)(s * (S::kA / 16)), db = dB0 + (uint64_t)(s * (S::kB / 16));
 #pragma unroll
-          for (int k4 = 0; k4 < 4; ++k4)
-            umma_bf16(d, sdesc_sw128(a + k4 * 32, 16, 1024), sdesc_sw128(b + k4 * 32, 16, 1024), idesc,
-                      (kk | k4) != 0);
-          umma_commit(empty0 + 8 * s);
+          for (int k4 = 0; k4 < 4; ++k4) umma_bf16_e(d, da + 2 * k4, db + 2 * k4, idesc, (kk | k4) != 0);
+          umma_commit_e(empty0 + 8 * s);
         }
-        umma_commit(tfull0 + 8 * ab);
+        umma_commit_e(tfull0 + 8 * ab);
       }
-      if (trace) trace[blockIdx.x * 6 + 3] = globaltimer();
+      if (trace && lane == 0) trace[blockIdx.x * 6 + 3] = globaltimer();
     }
   } else {
     griddep_wait();  // `out` may still be read by the previous kernel

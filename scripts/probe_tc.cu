@@ -29,23 +29,33 @@ __global__ void __launch_bounds__(320, 1) probe(int mode, int n_mma, int n_ld, u
   tc_fence_after();
   const uint32_t tmem = tslot;
   const bool do_mma = mode & 1, ts = mode & 2, do_ldtm = mode & 4, do_lds = mode & 8, do_ex2 = mode & 16;
+  const int nsel = (mode >> 8) & 3;  // 0: N=128, 1: N=64, 2: N=256
+  const int nacc = (mode >> 10) & 3;   // independent accumulators cycled (0 -> 1)
   unsigned long long t0 = clock64();
   float acc = 0.f;
   if (warp == 1) {
-    if (do_mma && lane == 0) {
-      constexpr uint32_t idS = idesc_bf16(128, 128, 0, 0);
+    if (do_mma) {  // whole warp, elect.sync issue, descriptors precomputed, unrolled
+      const uint32_t idS = nsel == 1 ? idesc_bf16(128, 64, 0, 0) : idesc_bf16(128, 128, 0, 0);
       constexpr uint32_t idO = idesc_bf16(128, 128, 0, 1);
-      for (int i = 0; i < n_mma; ++i) {
-        const uint32_t kk = i & 7;
-        if (ts)
-          umma_bf16_ts(tmem + 256, tmem + 384 + kk * 8, sdesc_sw128(base + 32768 + kk * 2048, 16384, 1024), idO, 1);
-        else
-          umma_bf16(tmem + 0, sdesc_sw128(base + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024),
-                    sdesc_sw128(base + 32768 + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024), idS, 1);
+      const uint64_t dA = sdesc_sw128(base, 16, 1024), dB = sdesc_sw128(base + 32768, 16, 1024);
+      const uint64_t dV = sdesc_sw128(base + 32768, 16384, 1024);
+      const uint32_t d1 = nacc ? 128u : 0u, d1o = nacc ? 128u : 0u;
+      for (int i = 0; i < n_mma; i += 16) {
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint64_t o = (uint64_t)(((kk >> 2) * 16384 + (kk & 3) * 32) >> 4);
+          if (ts) {
+            umma_bf16_ts_e(tmem + 256, tmem + 384 + kk * 8, dV + (uint64_t)(kk * 128), idO, 1);
+            umma_bf16_ts_e(tmem + 256 - d1o, tmem + 384 + kk * 8, dV + (uint64_t)(kk * 128), idO, 1);
+          } else {
+            umma_bf16_e(tmem + 0, dA + o, dB + o, idS, 1);
+            umma_bf16_e(tmem + d1, dA + o, dB + o, idS, 1);
+          }
+        }
       }
-      umma_commit(smem_u32(&bar));
+      umma_commit_e(smem_u32(&bar));
       mbar_wait(smem_u32(&bar), 0);
-      out[blockIdx.x * 8 + 0] = clock64() - t0;
+      if (lane == 0) out[blockIdx.x * 8 + 0] = clock64() - t0;
     }
   } else if (warp >= 2) {
     const int q = warp & 3;
@@ -96,10 +106,10 @@ int main() {
   cudaMalloc(&d, 148 * 8 * 8);
   cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536 + 1024);
   const char* names[] = {"SS mma", "TS mma", "LDTM x64 (8 warps)", "SS mma + LDTM", "TS mma + LDTM", "LDS 128 (8 warps)",
-                         "SS mma + LDS", "EX2 (8 warps, 4 chains, 64/iter)", "SS mma + EX2"};
-  const int modes[] = {1, 3, 4, 5, 7, 8, 9, 16, 17};
+                         "SS mma + LDS", "EX2 (8 warps, 4 chains, 64/iter)", "SS mma + EX2", "SS mma N=64", "SS mma 2 accumulators", "SS mma 3 accumulators", "TS mma 2 accumulators"};
+  const int modes[] = {1, 3, 4, 5, 7, 8, 9, 16, 17, 1 | 256, 1 | 1024, 1 | 2048, 3 | 1024};
   const int n_mma = 8192, n_ld = 1024;
-  for (int m = 0; m < 9; ++m) {
+  for (int m = 0; m < 13; ++m) {
     cudaMemset(d, 0, 148 * 8 * 8);
     probe<<<148, 320, 65536 + 1024>>>(modes[m], n_mma, n_ld, d);
     probe<<<148, 320, 65536 + 1024>>>(modes[m], n_mma, n_ld, d);
