@@ -57,11 +57,6 @@ struct PPLane {
   int tile, j0, n, split, seq, row_start, row_count, max_p;
 };
 
-PIC_DEV float fmax3(float a, float b, float c) {
-  float d;
-  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
-  return d;
-}
 
 // Item `item` of the host list (whole warp): lanes ordered so that A has the longer KV run; `sh`: both
 // lanes read the same K/V tiles (same sequence, same first tile).
@@ -114,27 +109,6 @@ PIC_DEV void mbar_wait_acc(uint32_t bar, uint32_t ph, unsigned long long* acc) {
   const unsigned long long t0 = clk();
   mbar_wait(bar, ph);
   *acc += clk() - t0;
-}
-
-// 2^x for a pair on the FMA pipe (FA4's trick: part of the exponentials leave the 16/clk/SM MUFU):
-// x = j + f with j = rint(x) (magic-number rounding), 2^f on [-1/2, 1/2] by a degree-3 fit (max relative
-// error 1.3e-4, far below the bf16 rounding P gets next), 2^j added to the exponent field.  x >= -125
-// after the clamp (masked keys, x = -inf, give 2^-125 ~ 2e-38 instead of 0: negligible against l >= 1).
-#ifndef PIC_POLY8
-#define PIC_POLY8 3  // pairs of every 8 on the polynomial
-#endif
-PIC_DEV float2 exp2_poly2(float2 x) {
-  constexpr float kM = 12582912.f;  // 1.5 * 2^23
-  x.x = fmaxf(x.x, -125.f);
-  x.y = fmaxf(x.y, -125.f);
-  const float2 t = add2(x, make_float2(kM, kM));
-  const float2 j = add2(t, make_float2(-kM, -kM));
-  const float2 f = fma2(j, make_float2(-1.f, -1.f), x);
-  float2 p = fma2(f, make_float2(0.05504054f, 0.05504054f), make_float2(0.24228513f, 0.24228513f));
-  p = fma2(p, f, make_float2(0.69325425f, 0.69325425f));
-  p = fma2(p, f, make_float2(0.99995032f, 0.99995032f));
-  return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23)),
-                     __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
 }
 
 // position of lane x's step-s K (or V) tile in the item's load order: shared → one tile per step;
