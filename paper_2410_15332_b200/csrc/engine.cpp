@@ -1556,7 +1556,8 @@ static void schedule_attention(pic_engine* e, Fwd& f) {
   // the one-lane kernel's finer split-KV); shared-block links (K tiles re-based in smem) stay on the
   // one-lane kernel, whose four rotation warps keep up where the ping-pong kernel's two do not (cfg4:
   // 310 vs 200 ms per step).  pic_test_set_attention_kernel(1|2) forces one (tests and A/B only).
-  bool pp = attn_pp_enabled() && e->cfg.head_dim == 128 && !e->f32 && !f.kv_rot;
+  static const bool pp_rot = getenv("PIC_ATTN_PP_ROT") != nullptr;  // A/B: ping-pong also for shared-block links
+  bool pp = attn_pp_enabled() && e->cfg.head_dim == 128 && !e->f32 && (!f.kv_rot || pp_rot);
   if (pp) {
     long work = 0;
     for (size_t t = 0; t + 2 < f.tiles.size(); t += 3) {

@@ -398,7 +398,7 @@ __global__ void __launch_bounds__(ROT ? 320 + 32 * kRotWarps : 320, 1)
           tmem_ld32(oAddr + c * 32, ov);
 #pragma unroll
           for (int i = 0; i < 32; ++i) ov[i] *= alpha;
-          tmem_st32(oAddr + c * 32, ov);
+          tmem_st32_wait(oAddr + c * 32, ov);  // registers reused next iteration
         }
         tmem_wait_st();
         l *= alpha;

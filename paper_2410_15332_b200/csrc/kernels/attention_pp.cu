@@ -47,10 +47,12 @@ constexpr int bQFull = 0, bQEmpty = 2, bKFull = 4, bKEmpty = bKFull + kKS, bKRot
               kNumBars = bIEmpty + kIR;
 constexpr int kSmem = kBar + kNumBars * 8 + 16 + kIR * 4;
 static_assert(kSmem <= 232448, "attention smem over the 227 KB limit");
-constexpr int kRotWarps = 2;  // warps 2-3 of the producer / MMA warpgroup
+constexpr int kRotWarps = 4;  // ROT: warpgroup 1 (warps 4-7) re-bases shared K tiles
 // register split of the 384-thread CTA: 128·(producer, MMA, rotation) + 256·softmax <= 64 K
-constexpr int kRegW0Rot = 104, kRegSmRot = 200;
-static_assert(128 * kRegW0Rot + 256 * kRegSmRot <= 65536, "register split over the file");
+// ROT register split of the 512-thread CTA: producer/MMA warpgroup 48, rotation warpgroup 104, softmax
+// warpgroups 176 (two-pass over TMEM: half a row in registers)
+constexpr int kRegW0Rot = 48, kRegRotWG = 104, kRegSmRot = 176;
+static_assert(128 * kRegW0Rot + 128 * kRegRotWG + 256 * kRegSmRot <= 65536, "register split over the file");
 }  // namespace attn2
 
 struct PPLane {
@@ -120,13 +122,13 @@ PIC_DEV int pp_tidx(int x, int s, int nB, bool sh) {
 }
 
 template <int G, bool ROT>
-__global__ void __launch_bounds__(384, 1)
+__global__ void __launch_bounds__(ROT ? 512 : 384, 1)
     attn_pp_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                    const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmK8,
                    const __grid_constant__ CUtensorMap tmV8, const AttnArgs a) {
   griddep_launch();
   using namespace attn2;
-  constexpr int SM0 = 4;  // first softmax warp (lane A: warps 4-7, lane B: warps 8-11)
+  constexpr int SM0 = ROT ? 8 : 4;  // first softmax warp (lane A: SM0..SM0+3, lane B: SM0+4..SM0+7)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw;
   if (threadIdx.x == 0 && (smem_u32(smem) & 1023)) __trap();  // SWIZZLE_128B tiles need 1 KB alignment
@@ -156,7 +158,7 @@ __global__ void __launch_bounds__(384, 1)
     }
     for (int s = 0; s < kIR; ++s) {
       mbar_init(B(bIFull + s), 1);
-      mbar_init(B(bIEmpty + s), ROT ? 11 : 9);  // MMA warp, rotation warps, softmax warps
+      mbar_init(B(bIEmpty + s), ROT ? 13 : 9);  // MMA warp, rotation warps, softmax warps
     }
     fence_mbar_init();
   }
@@ -183,10 +185,7 @@ __global__ void __launch_bounds__(384, 1)
   };
 
   if (warp < 4) {
-    if constexpr (ROT)
-      asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(kRegW0Rot) : "memory");
-    else
-      asm volatile("setmaxnreg.dec.sync.aligned.u32 56;\n" ::: "memory");
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(ROT ? kRegW0Rot : 56) : "memory");
     if (warp == 0) {
       // ------------------------------------------------------------------ TMA producer
       int kc = 0, vc = 0, qc0 = 0, qc1 = 0;
@@ -310,7 +309,7 @@ __global__ void __launch_bounds__(384, 1)
         // the whole warp runs the issue loop (convergent, uniform state); elect.sync issues
         auto issue_S = [&](int x, int s) {
           const int k = kc + pp_tidx(x, s, nB, sh), sl = k % kKS;
-          mbar_wait_acc(B((ROT ? bKRot : bKFull) + sl), (k / kKS) & 1, tr ? &tacc[0] : nullptr);
+          mbar_wait_acc(B((ROT && a.debug != 3 ? bKRot : bKFull) + sl), (k / kKS) & 1, tr ? &tacc[0] : nullptr);
           if (s == 0) mbar_wait_acc(B(bQFull + x), (x ? qcB : qcA) & 1, tr ? &tacc[3] : nullptr);
           tc_fence_after();
           const uint64_t dq = x ? dQ1 : dQ0, dk = dK0 + (uint64_t)(sl * (2 * kTile / 16));
@@ -368,14 +367,16 @@ __global__ void __launch_bounds__(384, 1)
         tr[kTrMwQ] = tacc[3];
         tr[kTrMwO] = tmw_o;
       }
-    } else if (ROT) {
+    }
+  } else if (ROT && warp < 8) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(kRegRotWG) : "memory");
     // ------------------------------------------------------------------ K-tile re-base (f3)
     // As attention.cu: keys of chunk-store blocks linked by reference are rotated by their block's Δ
     // (rebase_pair arithmetic, so the tile equals the copy path's a2-re-based one).  Thread u owns the
     // logical 16-B chunk cc = u & 7 of rows rg + 8i of each paged block; dims j and j+64 sit at the same
     // offset of the two SW128 halves.
     constexpr int RPB = 16 / (4 * kRotWarps);
-    const int u = threadIdx.x - 64;
+    const int u = threadIdx.x - 128;
     const int cc = u & 7, rg = u >> 3;
     const uint32_t phys = (uint32_t)(((cc ^ (rg & 7)) << 4) + rg * 128);
     int dcache = 0;
@@ -417,8 +418,12 @@ __global__ void __launch_bounds__(384, 1)
       mbar_wait(B(bKFull + sl), (k / kKS) & 1);
       const unsigned long long tw1 = tr ? clk() : 0;
       if (tr) tacc[0] += tw1 - tw;
+      if (a.debug == 2 || a.debug == 4) {  // ablation: no rotation work (4: nor its proxy fence; timing only)
+#pragma unroll
+        for (int m = 0; m < 8; ++m) dl[m] = 0;
+      }
       const uint32_t h0 = base + kK + (2 * sl) * kTile + phys, h1 = h0 + kTile;
-      constexpr int NB = 2;  // 16-B chunk pairs in flight per thread
+      constexpr int NB = 2;  // 16-B chunk pairs in flight per thread (104 registers)
       constexpr int BB = NB / RPB;
 #pragma unroll
       for (int m0 = 0; m0 < 8; m0 += BB) {
@@ -444,7 +449,7 @@ __global__ void __launch_bounds__(384, 1)
           sts128(h1 + o, xb[jj]);
         }
       }
-      fence_async_smem();  // generic-proxy smem writes -> visible to the tcgen05.mma operand reads
+      if (a.debug != 4) fence_async_smem();  // generic-proxy smem writes -> visible to the tcgen05.mma operand reads
       __syncwarp();
       if (lane == 0) mbar_arrive(B(bKRot + sl));
       if (tr) tacc[1] += clk() - tw1;
@@ -453,6 +458,7 @@ __global__ void __launch_bounds__(384, 1)
     for (int k = 0;; ++k) {
       const int item = next_item(k);
       if (item < 0) break;
+      if (a.debug == 3) continue;  // ablation: rotation warps idle, MMA reads unrotated K (timing only)
       PPLane LA, LB;
       int g;
       bool sh;
@@ -468,10 +474,9 @@ __global__ void __launch_bounds__(384, 1)
         if (s < nB && !sh) rotate_tile(kc++, bdB, LB.j0 + s, lastB);
       }
     }
-    if (tr && threadIdx.x == 64) {
+    if (tr && threadIdx.x == 128) {
       tr[kTrRw] = tacc[0];
       tr[kTrRc] = tacc[1];
-    }
     }
   } else {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(ROT ? kRegSmRot : 224) : "memory");
@@ -521,50 +526,30 @@ __global__ void __launch_bounds__(384, 1)
           ++cs;
           continue;
         }
-        float sv[128];
-        tmem_ld128_split(sAddr, sv);
         const int key0 = (P.j0 + s) * 128;
-        if (key0 + 127 > pos) {
+        // row max of v[0..n) (FMNMX3 tree), masking keys beyond the row's causal limit first
+        auto mask_max = [&](float* v, int n, int k0) -> float {
+          if (k0 + n - 1 > pos) {
 #pragma unroll
-          for (int i = 0; i < 128; ++i) sv[i] = (key0 + i <= pos) ? sv[i] : -INFINITY;
-        }
-        float m4[4] = {sv[0], sv[1], sv[2], sv[3]};
-#pragma unroll
-        for (int i = 4; i < 128; i += 8) {
-          m4[0] = fmax3(m4[0], sv[i], sv[i + 1]);
-          m4[1] = fmax3(m4[1], sv[i + 2], sv[i + 3]);
-          m4[2] = fmax3(m4[2], sv[i + 4], sv[i + 5]);
-          m4[3] = fmax3(m4[3], sv[i + 6], sv[i + 7]);
-        }
-        const float mx = fmax3(m4[0], m4[1], fmaxf(m4[2], m4[3])) * sc;  // log2 units (sc > 0)
-        const bool grow = mx > m_ref + 8.f;
-        const bool need = grow && m_ref != -INFINITY;
-        if (__any_sync(0xffffffffu, need)) {
-          // rescale O_X (PV of the previous step must have landed) and l to the new reference
-          mbar_wait(B(bOFull + x), (cs - 1) & 1);
-          tc_fence_after();
-          const float alpha = need ? exp2f(m_ref - mx) : 1.f;
-#pragma unroll 1
-          for (int c = 0; c < 4; ++c) {
-            float ov[32];
-            tmem_ld32(oAddr + c * 32, ov);
-#pragma unroll
-            for (int i = 0; i < 32; ++i) ov[i] *= alpha;
-            tmem_st32(oAddr + c * 32, ov);
+            for (int i = 0; i < n; ++i) v[i] = (k0 + i <= pos) ? v[i] : -INFINITY;
           }
-          tmem_wait_st();
-          l *= alpha;
-        }
-        if (grow) m_ref = mx;
-        const float nmu = (m_ref == -INFINITY) ? 0.f : -m_ref;
-        const float2 sc2 = make_float2(sc, sc), nmu2 = make_float2(nmu, nmu);
-        float2 la = make_float2(0.f, 0.f), lb = make_float2(0.f, 0.f);
+          float m4[4] = {fmaxf(v[0], v[1]), fmaxf(v[2], v[3]), fmaxf(v[4], v[5]), fmaxf(v[6], v[7])};
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
+          for (int i = 8; i < n; i += 8) {  // n is a multiple of 8: v[i..i+7] stays in range
+            m4[0] = fmax3(m4[0], v[i], v[i + 1]);
+            m4[1] = fmax3(m4[1], v[i + 2], v[i + 3]);
+            m4[2] = fmax3(m4[2], v[i + 4], v[i + 5]);
+            m4[3] = fmax3(m4[3], v[i + 6], v[i + 7]);
+          }
+          return fmax3(m4[0], m4[1], fmaxf(m4[2], m4[3]));
+        };
+        float2 la = make_float2(0.f, 0.f), lb = make_float2(0.f, 0.f);
+        // p = 2^(s·scale − m_ref) for 64 keys; masked keys are −inf → 0; P as bf16 pairs into `dst`
+        auto exp_half = [&](const float* v, uint32_t dst, float2 sc2, float2 nmu2) {
           uint32_t pk[32];
 #pragma unroll
-          for (int c = 0; c < 32; ++c) {  // pair c: p = 2^(s·scale − m_ref); masked keys are −inf → 0
-            const float2 xv = fma2(make_float2(sv[64 * h + 2 * c], sv[64 * h + 2 * c + 1]), sc2, nmu2);
+          for (int c = 0; c < 32; ++c) {
+            const float2 xv = fma2(make_float2(v[2 * c], v[2 * c + 1]), sc2, nmu2);
             float2 pv;
             if ((c & 7) < PIC_POLY8)
               pv = exp2_poly2(xv);
@@ -576,8 +561,59 @@ __global__ void __launch_bounds__(384, 1)
               la = add2(la, pv);
             pk[c] = pack_bf16(pv.x, pv.y);
           }
-          // keys [64h, 64h+64) -> S_X columns [64h, 64h+32) as bf16 pairs (the TS MMA's A layout)
-          tmem_st32u(sAddr + 64 * h, pk);
+          tmem_st32u_wait(dst, pk);
+        };
+        auto rescale = [&](float mx) {
+          const bool grow = mx > m_ref + 8.f;
+          const bool need = grow && m_ref != -INFINITY;
+          if (__any_sync(0xffffffffu, need)) {
+            // rescale O_X (PV of the previous step must have landed) and l to the new reference
+            mbar_wait(B(bOFull + x), (cs - 1) & 1);
+            tc_fence_after();
+            const float alpha = need ? exp2f(m_ref - mx) : 1.f;
+#pragma unroll 1
+            for (int c = 0; c < 4; ++c) {
+              float ov[32];
+              tmem_ld32(oAddr + c * 32, ov);
+#pragma unroll
+              for (int i = 0; i < 32; ++i) ov[i] *= alpha;
+              tmem_st32_wait(oAddr + c * 32, ov);  // registers reused next iteration
+            }
+            tmem_wait_st();
+            l *= alpha;
+          }
+          if (grow) m_ref = mx;
+        };
+        const float2 sc2 = make_float2(sc, sc);
+        if constexpr (ROT) {
+          // two passes over TMEM (this warpgroup runs at 160 registers beside the rotation warpgroup):
+          // max over both halves, exp of the half still in registers, reload the first half
+          float sv[64];
+          tmem_ld64(sAddr, sv);
+          float m = mask_max(sv, 64, key0);
+          tmem_ld64(sAddr + 64, sv);
+          m = fmaxf(m, mask_max(sv, 64, key0 + 64));
+          rescale(m * sc);  // log2 units (sc > 0)
+          const float nmu = (m_ref == -INFINITY) ? 0.f : -m_ref;
+          const float2 nmu2 = make_float2(nmu, nmu);
+          exp_half(sv, sAddr + 64, sc2, nmu2);  // keys 64..127 -> columns [64, 96): S cols 64.. already read
+          tmem_ld64(sAddr, sv);
+          mask_max(sv, 64, key0);
+          exp_half(sv, sAddr, sc2, nmu2);       // keys 0..63 -> columns [0, 32)
+        } else {
+          float sv[128];
+          // two x64 loads, each with its own wait in the same asm statement: a load whose wait sits in a
+          // later statement lets the compiler copy destination registers before the data has landed
+          tmem_ld64(sAddr, sv);
+          tmem_ld64(sAddr + 64, sv + 64);
+          const float m = fmaxf(mask_max(sv, 64, key0), mask_max(sv + 64, 64, key0 + 64));
+          rescale(m * sc);
+          const float nmu = (m_ref == -INFINITY) ? 0.f : -m_ref;
+          const float2 nmu2 = make_float2(nmu, nmu);
+          // keys [64h, 64h+64) -> S_X columns [64h, 64h+32) as bf16 pairs (the TS MMA's A layout); the
+          // second half first, in the two-pass variant's order, so both accumulate l identically
+          exp_half(sv + 64, sAddr + 64, sc2, nmu2);
+          exp_half(sv, sAddr, sc2, nmu2);
         }
         const float s0 = la.x, s1 = la.y, s2 = lb.x, s3 = lb.y;
         l += (s0 + s1) + (s2 + s3);
@@ -750,7 +786,7 @@ static cudaError_t launch_pp_g(const CUtensorMap& tmQ, const CUtensorMap& tmK, c
   const int n_items = a.n_work * a.Hkv;
   dim3 grid(std::min(n_items, n_sms));
   if (a.bdelta)
-    CUDA_TRY_LAUNCH(launch_k(attn_pp_kernel<G, true>, grid, dim3(384), attn2::kSmem, st, tmQ, tmK, tmV, tmK8, tmV8, a));
+    CUDA_TRY_LAUNCH(launch_k(attn_pp_kernel<G, true>, grid, dim3(512), attn2::kSmem, st, tmQ, tmK, tmV, tmK8, tmV8, a));
   else
     CUDA_TRY_LAUNCH(launch_k(attn_pp_kernel<G, false>, grid, dim3(384), attn2::kSmem, st, tmQ, tmK, tmV, tmK8, tmV8, a));
   return cudaGetLastError();

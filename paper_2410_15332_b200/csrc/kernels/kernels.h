@@ -190,7 +190,8 @@ struct AttnArgs {
   void* O;
   // ping-pong kernel: [next item, CTAs done], zero before the launch; the last CTA resets both
   unsigned* item_ctr;
-  int debug;  // bench-only ablation (PIC_ATTN_DEBUG): 1 = softmax skipped (S -> P handoff only); results invalid
+  int debug;  // bench-only ablation (PIC_ATTN_DEBUG), results invalid: 1 = softmax skipped, 2 = no K re-base
+             // arithmetic, 3 = rotation warpgroup idle, 4 = as 2 without the proxy fence
 };
 // Balanced split-KV schedule: each q-tile t (KV extent n_kv[t] 128-key tiles) gets
 // ceil(n_kv[t] / budget) splits, budget = ceil(Σ n_kv · Hkv / target_ctas); splits <= 32.
