@@ -1081,9 +1081,12 @@ static GemmChoice choose_gemm(const pic_engine* e, int M, int N, int K) {
 }
 
 // Fused gate/up + SwiGLU GEMM (N-tile fixed at 2g by the weight interleave): CTA pair when it costs less.
+// Default on (PIC_NO_PAIR_SWIGLU=1: off): with the convergent MMA issue the pair kernel measured 3% faster
+// per cfg4 step for the gate/up GEMM (830 vs 854-859 ms, same box), the largest GEMM of the layer.
 static bool swiglu_pair(const pic_engine* e, int M, int N2) {
+  static const bool sw = getenv("PIC_NO_PAIR_SWIGLU") == nullptr;
   const int bn = 2 * e->gu_group;
-  if (M <= 128 || !pairs_enabled() || !gemm_pair_supported(bn)) return false;
+  if (M <= 128 || !(pairs_enabled() || sw) || !gemm_pair_supported(bn) || e->f32) return false;
   return gemm_cost(M, N2, 1, bn, 1, 1) < gemm_cost(M, N2, 1, bn, 1, 0) - 1e-9;
 }
 
@@ -1472,7 +1475,7 @@ static pic_status enqueue_forward(pic_engine* e, const Fwd& f, const DevPlan& dp
     }
     // a7 O projection, residual + a8 MLP
     const bool gu_pair = e->gu_group > 0 && swiglu_pair(e, M, 2 * F);
-    const bool fuse_g2 = nf && e->gu_group > 0 && !gu_pair;
+    const bool fuse_g2 = nf && e->gu_group > 0;
     TRY(R.gemm_resid(e->tm_O, w.tm_o, M, d, Hq * D, hc, &s, e->Obuf, w.o, fuse_g2 ? w.g2 : nullptr, e->x,
                      &norm_tiles));
     if (!norm_tiles) {

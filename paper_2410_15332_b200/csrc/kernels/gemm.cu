@@ -647,8 +647,9 @@ __global__ void __launch_bounds__(192, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0 && rank == 0) {  // a pair's MMAs are issued by the leader CTA
+    if (rank == 0) {  // a pair's MMAs are issued by the leader CTA: whole warp, elect.sync issue
       constexpr uint32_t idesc = idesc_bf16(128 * CL, BN, 0, 0);
+      const uint64_t dA0 = sdesc_sw128(smem_u32(sA), 16, 1024), dB0 = sdesc_sw128(smem_u32(sB), 16, 1024);
       int it = 0, i = 0;
       for (int u = cid; u < units; u += ncl, ++i) {
         int m0, n_idx, kb0, nkb;
@@ -660,29 +661,27 @@ __global__ void __launch_bounds__(192, 1)
         for (int kk = 0; kk < nkb; ++kk, ++it) {
           const int s = it % STAGES;
           mbar_wait(full0 + 8 * s, (it / STAGES) & 1);
-          if (trace && it == 0) trace[blockIdx.x * 6 + 2] = globaltimer();
+          if (trace && it == 0 && lane == 0) trace[blockIdx.x * 6 + 2] = globaltimer();
           tc_fence_after();
-          const uint32_t a = smem_u32(sA + s * S::kA), b = smem_u32(sB + s * S::kB);
+          const uint64_t da = dA0 + (uint64_t)(s * (S::kA / 16)), db = dB0 + (uint64_t)(s * (S::kB / 16));
 #pragma unroll
           for (int k4 = 0; k4 < 4; ++k4) {
             if constexpr (CL == 2)
-              umma_bf16_2sm(d, sdesc_sw128(a + k4 * 32, 16, 1024), sdesc_sw128(b + k4 * 32, 16, 1024), idesc,
-                            (kk | k4) != 0);
+              umma_bf16_2sm_e(d, da + 2 * k4, db + 2 * k4, idesc, (kk | k4) != 0);
             else
-              umma_bf16(d, sdesc_sw128(a + k4 * 32, 16, 1024), sdesc_sw128(b + k4 * 32, 16, 1024), idesc,
-                        (kk | k4) != 0);
+              umma_bf16_e(d, da + 2 * k4, db + 2 * k4, idesc, (kk | k4) != 0);
           }
           if constexpr (CL == 2)
-            umma_commit_2sm(empty0 + 8 * s, 3);
+            umma_commit_2sm_e(empty0 + 8 * s, 3);
           else
-            umma_commit(empty0 + 8 * s);
+            umma_commit_e(empty0 + 8 * s);
         }
         if constexpr (CL == 2)
-          umma_commit_2sm(tfull0 + 8 * ab, 3);
+          umma_commit_2sm_e(tfull0 + 8 * ab, 3);
         else
-          umma_commit(tfull0 + 8 * ab);
+          umma_commit_e(tfull0 + 8 * ab);
       }
-      if (trace) trace[blockIdx.x * 6 + 3] = globaltimer();
+      if (trace && lane == 0) trace[blockIdx.x * 6 + 3] = globaltimer();
     }
   } else {
     griddep_wait();  // `out` may still be read by the previous kernel
@@ -751,6 +750,7 @@ __global__ void __launch_bounds__(192, 1)
         const int F = N / 2;
         uint16_t* urow = reinterpret_cast<uint16_t*>(out_) + (size_t)row * F + (size_t)n_idx * G;
         uint4* sb = reinterpret_cast<uint4*>(stg);
+        const float rs = norm_scale(ep, row, M);  // fused RMSNorm row scale (1 if the input was normalised)
 #pragma unroll 1
         for (int c = 0; c < G; c += 16) {
           float gv[16], uv[16];
@@ -759,8 +759,8 @@ __global__ void __launch_bounds__(192, 1)
           uint32_t pk[8];
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
-            const float g0 = gv[2 * j], g1 = gv[2 * j + 1];
-            pk[j] = pack_bf16(g0 / (1.f + __expf(-g0)) * uv[2 * j], g1 / (1.f + __expf(-g1)) * uv[2 * j + 1]);
+            const float g0 = gv[2 * j] * rs, g1 = gv[2 * j + 1] * rs;
+            pk[j] = pack_bf16(g0 / (1.f + __expf(-g0)) * (uv[2 * j] * rs), g1 / (1.f + __expf(-g1)) * (uv[2 * j + 1] * rs));
           }
           if (stage) {
             sb[lane * PS + c / 8] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
@@ -992,11 +992,10 @@ cudaError_t launch_gemm_partial(const CUtensorMap& A, const CUtensorMap& B, floa
 cudaError_t launch_gemm_swiglu(const CUtensorMap& A, const CUtensorMap& B, void* u, int M, int N2, int K, int bn,
                                cudaStream_t st, int pack, const GemmNext& nx, int pair, const GemmEpi& ep) {
   if (pair) {
-    if (ep.ssq_in) return cudaErrorInvalidValue;  // the CTA-pair epilogue has no fused-norm row scale
     switch (bn) {
 #define L4(b) \
   case b:     \
-    return launch_gemm_t<b, EPI_SWIGLU, 2>(A, B, u, M, N2, K, 1, pack, st, nx);
+    return launch_gemm_t<b, EPI_SWIGLU, 2>(A, B, u, M, N2, K, 1, pack, st, nx, ep);
       PIC_PAIR_BNS(L4)
 #undef L4
     }

@@ -1,0 +1,12 @@
+#!/bin/bash
+# CTA-pair GEMM (convergent issue now): kernel tests; cfg4 A/B default vs pair SwiGLU only vs PIC_PAIR
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_kernels.py -x -q -k "gemm" > gpurun_out/pa_t.log 2>&1; tail -1 gpurun_out/pa_t.log
+for v in none sw all none; do
+  unset PIC_PAIR PIC_PAIR_SWIGLU
+  if [ $v = sw ]; then export PIC_PAIR_SWIGLU=1; fi
+  if [ $v = all ]; then export PIC_PAIR=1; fi
+  timeout 900 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --decode-steps 0 > gpurun_out/pa.json 2> gpurun_out/pa.err
+  python -c "import json;d=json.loads(open('gpurun_out/pa.json').read().strip().splitlines()[-1]);print('$v', round(d['ms_per_step'],2), {k:round(v['ms_per_step'],2) for k,v in d['kernel_breakdown'].items()}, d['clocks']['sm_mhz'])" || tail -3 gpurun_out/pa.err
+done
