@@ -1012,6 +1012,13 @@ static bool pairs_enabled() {
   static const bool on = getenv("PIC_PAIR") != nullptr;
   return on;
 }
+// CTA pairs for the fused-epilogue (unsplit) GEMMs: QKV + RoPE/scatter, O / down + residual (+ fused norm).
+// Opt-in (PIC_PAIR_FUSED=1): measured neutral at cfg4 (819.7 / 822.2 vs 818.3 / 819.3 ms per step, same box),
+// unlike the gate/up GEMM (default pair, 4.9% faster).
+static bool fused_pairs() {
+  static const bool on = getenv("PIC_PAIR_FUSED") != nullptr;
+  return on;
+}
 static double gemm_cost(int M, int N, int kblk, int bn, int sp, int pair) {
   const int cl = pair ? 2 : 1;
   const long units = (long)((M + 128 * cl - 1) / (128 * cl)) * ((N + bn - 1) / bn) * sp;
@@ -1132,14 +1139,30 @@ struct Runner {
   }
   // Unsplit (tensor-bound) choice whose N-tile has a fused-epilogue instance, else nullptr.
   const CUtensorMap* fused_map(const CUtensorMap* B3, const void* B_ptr, int M, int N, int K, bool heads, int* bn,
-                               pic_status* err) {
+                               pic_status* err, int* pair = nullptr) {
     *err = PIC_OK;
+    if (pair) *pair = 0;
     if (e->f32 || !epi_fuse()) return nullptr;
-    const GemmChoice g = choose_gemm(e, M, N, K);
-    if (g.splits != 1 || g.pair || !(heads ? (g.bn == 128 || g.bn == 256) : gemm_resid_supported(g.bn))) return nullptr;
-    const CUtensorMap* Bm = (g.bn == 64 || g.bn == 128 || g.bn == 256) ? &B3[bn_index(g.bn)] : nullptr;
-    if (!Bm) *err = weight_map(e, B_ptr, N, K, g.bn, &Bm);
+    GemmChoice g = choose_gemm(e, M, N, K);
+    if (g.pair) return nullptr;  // PIC_PAIR's split choice: not a fused shape
+    if (g.splits != 1 || !(heads ? (g.bn == 128 || g.bn == 256) : gemm_resid_supported(g.bn))) return nullptr;
+    if (pair && fused_pairs() && M > 256) {
+      // CTA pair (256-row M-tiles) when its waves x per-unit cost is lower (same N-tile candidates)
+      double best = gemm_cost(M, N, K / 64, g.bn, 1, 0);
+      for (int b : {256, 224, 192, 128}) {
+        if (!gemm_pair_supported(b) || (heads && b != 128 && b != 256)) continue;
+        const double c = gemm_cost(M, N, K / 64, b, 1, 1);
+        if (c < best - 1e-9) {
+          best = c;
+          g = GemmChoice{b, 1, 1};
+        }
+      }
+    }
+    const int box = g.pair ? g.bn / 2 : g.bn;  // a CTA pair loads half of the N-tile per CTA
+    const CUtensorMap* Bm = (box == 64 || box == 128 || box == 256) ? &B3[bn_index(box)] : nullptr;
+    if (!Bm) *err = weight_map(e, B_ptr, N, K, box, &Bm);
     *bn = g.bn;
+    if (pair) *pair = g.pair;
     return *err == PIC_OK ? Bm : nullptr;
   }
   // a7 / a8-down: h += A·Bᵀ in the epilogue of an unsplit GEMM (*splits_out = 0), else split-K partials
@@ -1149,9 +1172,9 @@ struct Runner {
                         const void* A_ptr, const void* B_ptr, const float* norm_gain = nullptr, void* xg = nullptr,
                         int* norm_tiles = nullptr) {
     if (norm_tiles) *norm_tiles = 0;
-    int bn = 0;
+    int bn = 0, pair = 0;
     pic_status err;
-    const CUtensorMap* Bm = e->tp_size == 1 ? fused_map(B3, B_ptr, M, N, K, false, &bn, &err) : nullptr;
+    const CUtensorMap* Bm = e->tp_size == 1 ? fused_map(B3, B_ptr, M, N, K, false, &bn, &err, &pair) : nullptr;
     if (e->tp_size == 1) TRY(err);
     if (!Bm) return gemm(A, B3, M, N, K, splits_out, A_ptr, B_ptr);
     *splits_out = 0;
@@ -1163,7 +1186,7 @@ struct Runner {
       ep.ssq = e->ssq;
       if (norm_tiles) *norm_tiles = (N + bn - 1) / bn;
     }
-    PROF("gemm", (double)N * K * 2, 2.0 * M * N * K, launch_gemm_resid(A, *Bm, h, M, N, K, bn, st, GemmNext{}, ep));
+    PROF("gemm", (double)N * K * 2, 2.0 * M * N * K, launch_gemm_resid(A, *Bm, h, M, N, K, bn, st, GemmNext{}, ep, pair));
     return PIC_OK;
   }
   // will this QKV projection run on the fused-epilogue GEMM (so it can take a fused-norm input)?
@@ -1178,15 +1201,15 @@ struct Runner {
   // split-K partials for qkv_rope_scatter.
   pic_status gemm_qkv(const CUtensorMap& A, const CUtensorMap* B3, int M, int N, int K, const GemmEpi& ep,
                       int* splits_out, bool* fused, const void* A_ptr, const void* B_ptr) {
-    int bn = 0;
+    int bn = 0, pair = 0;
     pic_status err;
-    const CUtensorMap* Bm = e->cfg.head_dim == 128 ? fused_map(B3, B_ptr, M, N, K, true, &bn, &err) : nullptr;
+    const CUtensorMap* Bm = e->cfg.head_dim == 128 ? fused_map(B3, B_ptr, M, N, K, true, &bn, &err, &pair) : nullptr;
     if (e->cfg.head_dim == 128) TRY(err);
     *fused = Bm != nullptr;
     if (!Bm) return gemm(A, B3, M, N, K, splits_out, A_ptr, B_ptr);
     *splits_out = 1;
     ++launches;
-    PROF("gemm", (double)N * K * 2, 2.0 * M * N * K, launch_gemm_qkv(A, *Bm, ep, M, N, K, bn, st));
+    PROF("gemm", (double)N * K * 2, 2.0 * M * N * K, launch_gemm_qkv(A, *Bm, ep, M, N, K, bn, st, GemmNext{}, pair));
     return PIC_OK;
   }
 };

@@ -92,176 +92,20 @@ PIC_DEV float norm_scale(const GemmEpi& ep, int row, int M) {
   return rsqrtf(s * ep.inv_d + ep.eps);
 }
 
-template <int BN, int STAGES, int EPI>
-__global__ void __launch_bounds__(192, 1)
-    gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                     void* __restrict__ out_, int M, int N, int kblk_total, int kblk_per_split, int splits,
-                     int pack, unsigned long long* trace, const __grid_constant__ CUtensorMap tmN,
-                     GemmNext nx, const GemmEpi ep) {
-  using S = GemmSmem<BN, STAGES>;
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = smem_raw;
-  if (threadIdx.x == 0 && (smem_u32(smem) & 1023)) __trap();  // SWIZZLE_128B tiles need 1 KB alignment
-  uint8_t* sA = smem;
-  uint8_t* sB = smem + STAGES * S::kA;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * S::kStage);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + S::kBars);
-  const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + STAGES);
-  const uint32_t tfull0 = smem_u32(bars + 2 * STAGES), tempty0 = smem_u32(bars + 2 * STAGES + 2);
-
+// Epilogue of one unit (m-tile rows of this CTA x one n-tile), shared by the one-CTA and the CTA-pair
+// kernel: EPI_PARTIAL / EPI_RESID (+ fused-norm outputs) / EPI_QKV / EPI_SWIGLU on the accumulator rows
+// this warp may read from TMEM (lane quarter q).  `last`: the CTA's final unit (its smem ring is idle).
+template <int BN, int EPI, int KSTG, int KSTGOFF>
+PIC_DEV void gemm_epilogue(uint8_t* smem, bool last, void* __restrict__ out_, int M, int N, int mt, int splits, int u,
+                           int m0, int n_idx, int nkb, uint32_t tl, const GemmEpi& ep) {
   const int warp = warp_id(), lane = lane_id();
-  const int mt = (M + 127) / 128, nt = (N + BN - 1) / BN;
-  const int units = mt * nt * splits;
-  griddep_launch();
-  if (trace && threadIdx.x == 0) trace[blockIdx.x * 6 + 0] = globaltimer();
-
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES; ++s) {
-      mbar_init(full0 + 8 * s, 1);
-      mbar_init(empty0 + 8 * s, 1);
-    }
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(tfull0 + 8 * b, 1);
-      mbar_init(tempty0 + 8 * b, 128);
-    }
-    fence_mbar_init();
-  }
-  if (warp == 2) tmem_alloc(smem_u32(tmem_slot), S::kTmemCols);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-
-  // unit u -> (m fastest, then split, then n): concurrently running CTAs share weight tiles in L2.  With
-  // ep.raster_gm > 0 (split-K 1, A larger than L2 wants) the m-tiles go in groups of raster_gm, each group
-  // sweeping all n-tiles before the next: one wave reuses raster_gm A row-blocks and 148 / raster_gm
-  // weight n-tiles from L2 instead of streaming all of A once per n-tile band.
-  const int GM = (ep.raster_gm > 0 && splits == 1) ? min(ep.raster_gm, mt) : mt;
-  auto decode = [&](int u, int& m0, int& n_idx, int& kb0, int& nkb) {
-    const int grp = u / (GM * nt * splits);
-    const int mb = grp * GM, gme = min(GM, mt - mb);
-    const int v = u - grp * GM * nt * splits;
-    const int m = mb + v % gme;
-    const int r = v / gme;
-    const int sp = r % splits;
-    n_idx = r / splits;
-    m0 = m * 128;
-    kb0 = sp * kblk_per_split;
-    nkb = max(0, min(kblk_per_split, kblk_total - kb0));
-  };
-
-  // B tile of k-block kb: row-major weights -> one [BN x 64] box; packed weights (pack rows per
-  // sub-tile, stored [N/pack][K/64][pack][64]) -> BN/pack contiguous boxes of pack x 128 B.
-  const uint64_t wpol = l2_policy_evict_first();  // weights are streamed once per forward
-  auto load_b = [&](uint32_t dst, uint32_t bar, int kb, int n_idx) {
-    if (pack == 0) {
-      if (weight_evict_first())
-        tma_load_2d_hint(dst, &tmB, bar, kb * 64, n_idx * BN, wpol);
-      else
-        tma_load_2d(dst, &tmB, bar, kb * 64, n_idx * BN);
-    } else {
-      const int per = BN / pack;
-      for (int j = 0; j < per; ++j) {
-        const int t = n_idx * per + j;
-        tma_load_2d(dst + j * pack * 128, &tmB, bar, 0, (t * kblk_total + kb) * pack);
-      }
-    }
-  };
-
-  if (warp == 0) {
-    if (lane == 0) {
-      tma_prefetch(&tmA);
-      tma_prefetch(&tmB);
-      int it = 0;
-      bool waited = false;
-      for (int u = blockIdx.x; u < units; u += gridDim.x) {
-        int m0, n_idx, kb0, nkb;
-        decode(u, m0, n_idx, kb0, nkb);
-        int kk = 0;
-        if (!waited) {
-          // Weights do not depend on the previous kernel: stream the first stages of B while it
-          // drains (PDL), then wait for it before loading the activations A.
-          const int pre = min(nkb, STAGES);
-          for (int i = 0; i < pre; ++i) {
-            mbar_expect_tx(full0 + 8 * i, S::kStage);
-            load_b(smem_u32(sB + i * S::kB), full0 + 8 * i, kb0 + i, n_idx);
-          }
-          griddep_wait();
-          if (trace) trace[blockIdx.x * 6 + 1] = globaltimer();
-          waited = true;
-          for (int i = 0; i < pre; ++i) tma_load_2d(smem_u32(sA + i * S::kA), &tmA, full0 + 8 * i, (kb0 + i) * 64, m0);
-          kk = pre;
-          it = pre;
-        }
-        for (; kk < nkb; ++kk, ++it) {
-          const int s = it % STAGES;
-          mbar_wait(empty0 + 8 * s, ((it / STAGES) & 1) ^ 1);
-          mbar_expect_tx(full0 + 8 * s, S::kStage);
-          const int kc = (kb0 + kk) * 64;
-          tma_load_2d(smem_u32(sA + s * S::kA), &tmA, full0 + 8 * s, kc, m0);
-          load_b(smem_u32(sB + s * S::kB), full0 + 8 * s, kb0 + kk, n_idx);
-        }
-      }
-      if (!waited) griddep_wait();
-      // All of this GEMM's loads are issued: pull the first k-blocks of the NEXT GEMM's weights into
-      // L2 so that its ring fill (at its launch) hits L2 instead of waiting on HBM.
-      for (int u2 = blockIdx.x; u2 < nx.units && nx.pfk > 0; u2 += gridDim.x) {
-        const int r2 = u2 / nx.mt;
-        if (u2 % nx.mt) continue;  // same weights for every m-tile
-        const int kb2 = (r2 % nx.splits) * nx.kper, n2 = r2 / nx.splits;
-        const int nk2 = min(nx.pfk, nx.kblk_total - kb2);
-        for (int i = 0; i < nk2; ++i) tma_prefetch_l2_2d(&tmN, (kb2 + i) * 64, n2 * nx.bn);
-      }
-    }
-  } else if (warp == 1) {
-    {
-      // whole warp, elect.sync issue, base descriptors + constant offsets (a lane-0 branch recomputing
-      // descriptors per MMA issues at ~88 cycles per MMA: above the pipe time of N <= 224)
-      constexpr uint32_t idesc = idesc_bf16(128, BN, 0, 0);
-      const uint64_t dA0 = sdesc_sw128(smem_u32(sA), 16, 1024), dB0 = sdesc_sw128(smem_u32(sB), 16, 1024);
-      int it = 0, i = 0;
-      for (int u = blockIdx.x; u < units; u += gridDim.x, ++i) {
-        int m0, n_idx, kb0, nkb;
-        decode(u, m0, n_idx, kb0, nkb);
-        const int ab = i & 1;
-        mbar_wait(tempty0 + 8 * ab, ((i >> 1) & 1) ^ 1);  // epilogue has drained this accumulator
-        tc_fence_after();
-        const uint32_t d = tmem + ab * S::kAcc;
-        for (int kk = 0; kk < nkb; ++kk, ++it) {
-          const int s = it % STAGES;
-          mbar_wait(full0 + 8 * s, (it / STAGES) & 1);
-          if (trace && it == 0 && lane == 0) trace[blockIdx.x * 6 + 2] = globaltimer();
-          tc_fence_after();
-          const uint64_t da = dA0 + (uint64_t)(s * (S::kA / 16)), db = dB0 + (uint64_t)(s * (S::kB / 16));
-#pragma unroll
-          for (int k4 = 0; k4 < 4; ++k4) umma_bf16_e(d, da + 2 * k4, db + 2 * k4, idesc, (kk | k4) != 0);
-          umma_commit_e(empty0 + 8 * s);
-        }
-        umma_commit_e(tfull0 + 8 * ab);
-      }
-      if (trace && lane == 0) trace[blockIdx.x * 6 + 3] = globaltimer();
-    }
-  } else {
-    griddep_wait();  // `out` may still be read by the previous kernel
-    const int q = warp & 3;  // TMEM lane quarter this warp may access
-    int i = 0;
-    for (int u = blockIdx.x; u < units; u += gridDim.x, ++i) {
-      int m0, n_idx, kb0, nkb;
-      decode(u, m0, n_idx, kb0, nkb);
-      const int ab = i & 1;
-      const int row = m0 + q * 32 + lane;
-      const uint32_t tl = tmem + ab * S::kAcc + ((uint32_t)(q * 32) << 16);
-      const int n0 = n_idx * BN;
-      mbar_wait(tfull0 + 8 * ab, (i >> 1) & 1);
-      tc_fence_after();
-      // The last unit of a CTA runs after its final MMA, when the smem ring is idle: stage the tile
-      // through the ring so that global stores are full 128-B row segments (a row-per-thread store
-      // pattern costs ~4 us per tile in uncoalesced 16-B transactions).
-      const bool last = u + (int)gridDim.x >= units;
-      const bool stage = last || ((EPI == EPI_PARTIAL || EPI == EPI_RESID) && S::kStg > 0);
+  const int q = warp & 3;
+  const int row = m0 + q * 32 + lane;
+  const int n0 = n_idx * BN;
+      const bool stage = last || ((EPI == EPI_PARTIAL || EPI == EPI_RESID) && KSTG > 0);
       // the ring is idle after the last unit's MMAs; otherwise the dedicated 4 KB per warp (one chunk)
       uint8_t* stg = last ? smem + (size_t)(warp - 2) * ((BN + 31) / 32) * 4096
-                          : smem + S::kStgOff + (size_t)(warp - 2) * 4096;
+                          : smem + KSTGOFF + (size_t)(warp - 2) * 4096;
       const int stg_chunk = last ? 4096 : 0;  // bytes between consecutive 32-column chunks
       const int mrow0 = m0 + q * 32;
       if constexpr (EPI == EPI_PARTIAL || EPI == EPI_RESID) {
@@ -453,6 +297,173 @@ __global__ void __launch_bounds__(192, 1)
           }
         }
       }
+}
+
+template <int BN, int STAGES, int EPI>
+__global__ void __launch_bounds__(192, 1)
+    gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                     void* __restrict__ out_, int M, int N, int kblk_total, int kblk_per_split, int splits,
+                     int pack, unsigned long long* trace, const __grid_constant__ CUtensorMap tmN,
+                     GemmNext nx, const GemmEpi ep) {
+  using S = GemmSmem<BN, STAGES>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw;
+  if (threadIdx.x == 0 && (smem_u32(smem) & 1023)) __trap();  // SWIZZLE_128B tiles need 1 KB alignment
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * S::kA;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * S::kStage);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + S::kBars);
+  const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + STAGES);
+  const uint32_t tfull0 = smem_u32(bars + 2 * STAGES), tempty0 = smem_u32(bars + 2 * STAGES + 2);
+
+  const int warp = warp_id(), lane = lane_id();
+  const int mt = (M + 127) / 128, nt = (N + BN - 1) / BN;
+  const int units = mt * nt * splits;
+  griddep_launch();
+  if (trace && threadIdx.x == 0) trace[blockIdx.x * 6 + 0] = globaltimer();
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(full0 + 8 * s, 1);
+      mbar_init(empty0 + 8 * s, 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(tfull0 + 8 * b, 1);
+      mbar_init(tempty0 + 8 * b, 128);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc(smem_u32(tmem_slot), S::kTmemCols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  // unit u -> (m fastest, then split, then n): concurrently running CTAs share weight tiles in L2.  With
+  // ep.raster_gm > 0 (split-K 1, A larger than L2 wants) the m-tiles go in groups of raster_gm, each group
+  // sweeping all n-tiles before the next: one wave reuses raster_gm A row-blocks and 148 / raster_gm
+  // weight n-tiles from L2 instead of streaming all of A once per n-tile band.
+  const int GM = (ep.raster_gm > 0 && splits == 1) ? min(ep.raster_gm, mt) : mt;
+  auto decode = [&](int u, int& m0, int& n_idx, int& kb0, int& nkb) {
+    const int grp = u / (GM * nt * splits);
+    const int mb = grp * GM, gme = min(GM, mt - mb);
+    const int v = u - grp * GM * nt * splits;
+    const int m = mb + v % gme;
+    const int r = v / gme;
+    const int sp = r % splits;
+    n_idx = r / splits;
+    m0 = m * 128;
+    kb0 = sp * kblk_per_split;
+    nkb = max(0, min(kblk_per_split, kblk_total - kb0));
+  };
+
+  // B tile of k-block kb: row-major weights -> one [BN x 64] box; packed weights (pack rows per
+  // sub-tile, stored [N/pack][K/64][pack][64]) -> BN/pack contiguous boxes of pack x 128 B.
+  const uint64_t wpol = l2_policy_evict_first();  // weights are streamed once per forward
+  auto load_b = [&](uint32_t dst, uint32_t bar, int kb, int n_idx) {
+    if (pack == 0) {
+      if (weight_evict_first())
+        tma_load_2d_hint(dst, &tmB, bar, kb * 64, n_idx * BN, wpol);
+      else
+        tma_load_2d(dst, &tmB, bar, kb * 64, n_idx * BN);
+    } else {
+      const int per = BN / pack;
+      for (int j = 0; j < per; ++j) {
+        const int t = n_idx * per + j;
+        tma_load_2d(dst + j * pack * 128, &tmB, bar, 0, (t * kblk_total + kb) * pack);
+      }
+    }
+  };
+
+  if (warp == 0) {
+    if (lane == 0) {
+      tma_prefetch(&tmA);
+      tma_prefetch(&tmB);
+      int it = 0;
+      bool waited = false;
+      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        int m0, n_idx, kb0, nkb;
+        decode(u, m0, n_idx, kb0, nkb);
+        int kk = 0;
+        if (!waited) {
+          // Weights do not depend on the previous kernel: stream the first stages of B while it
+          // drains (PDL), then wait for it before loading the activations A.
+          const int pre = min(nkb, STAGES);
+          for (int i = 0; i < pre; ++i) {
+            mbar_expect_tx(full0 + 8 * i, S::kStage);
+            load_b(smem_u32(sB + i * S::kB), full0 + 8 * i, kb0 + i, n_idx);
+          }
+          griddep_wait();
+          if (trace) trace[blockIdx.x * 6 + 1] = globaltimer();
+          waited = true;
+          for (int i = 0; i < pre; ++i) tma_load_2d(smem_u32(sA + i * S::kA), &tmA, full0 + 8 * i, (kb0 + i) * 64, m0);
+          kk = pre;
+          it = pre;
+        }
+        for (; kk < nkb; ++kk, ++it) {
+          const int s = it % STAGES;
+          mbar_wait(empty0 + 8 * s, ((it / STAGES) & 1) ^ 1);
+          mbar_expect_tx(full0 + 8 * s, S::kStage);
+          const int kc = (kb0 + kk) * 64;
+          tma_load_2d(smem_u32(sA + s * S::kA), &tmA, full0 + 8 * s, kc, m0);
+          load_b(smem_u32(sB + s * S::kB), full0 + 8 * s, kb0 + kk, n_idx);
+        }
+      }
+      if (!waited) griddep_wait();
+      // All of this GEMM's loads are issued: pull the first k-blocks of the NEXT GEMM's weights into
+      // L2 so that its ring fill (at its launch) hits L2 instead of waiting on HBM.
+      for (int u2 = blockIdx.x; u2 < nx.units && nx.pfk > 0; u2 += gridDim.x) {
+        const int r2 = u2 / nx.mt;
+        if (u2 % nx.mt) continue;  // same weights for every m-tile
+        const int kb2 = (r2 % nx.splits) * nx.kper, n2 = r2 / nx.splits;
+        const int nk2 = min(nx.pfk, nx.kblk_total - kb2);
+        for (int i = 0; i < nk2; ++i) tma_prefetch_l2_2d(&tmN, (kb2 + i) * 64, n2 * nx.bn);
+      }
+    }
+  } else if (warp == 1) {
+    {
+      // whole warp, elect.sync issue, base descriptors + constant offsets (a lane-0 branch recomputing
+      // descriptors per MMA issues at ~88 cycles per MMA: above the pipe time of N <= 224)
+      constexpr uint32_t idesc = idesc_bf16(128, BN, 0, 0);
+      const uint64_t dA0 = sdesc_sw128(smem_u32(sA), 16, 1024), dB0 = sdesc_sw128(smem_u32(sB), 16, 1024);
+      int it = 0, i = 0;
+      for (int u = blockIdx.x; u < units; u += gridDim.x, ++i) {
+        int m0, n_idx, kb0, nkb;
+        decode(u, m0, n_idx, kb0, nkb);
+        const int ab = i & 1;
+        mbar_wait(tempty0 + 8 * ab, ((i >> 1) & 1) ^ 1);  // epilogue has drained this accumulator
+        tc_fence_after();
+        const uint32_t d = tmem + ab * S::kAcc;
+        for (int kk = 0; kk < nkb; ++kk, ++it) {
+          const int s = it % STAGES;
+          mbar_wait(full0 + 8 * s, (it / STAGES) & 1);
+          if (trace && it == 0 && lane == 0) trace[blockIdx.x * 6 + 2] = globaltimer();
+          tc_fence_after();
+          const uint64_t da = dA0 + (uint64_t)(s * (S::kA / 16)), db = dB0 + (uint64_t)(s * (S::kB / 16));
+#pragma unroll
+          for (int k4 = 0; k4 < 4; ++k4) umma_bf16_e(d, da + 2 * k4, db + 2 * k4, idesc, (kk | k4) != 0);
+          umma_commit_e(empty0 + 8 * s);
+        }
+        umma_commit_e(tfull0 + 8 * ab);
+      }
+      if (trace && lane == 0) trace[blockIdx.x * 6 + 3] = globaltimer();
+    }
+  } else {
+    griddep_wait();  // `out` may still be read by the previous kernel
+    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    int i = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x, ++i) {
+      int m0, n_idx, kb0, nkb;
+      decode(u, m0, n_idx, kb0, nkb);
+      const int ab = i & 1;
+      const uint32_t tl = tmem + ab * S::kAcc + ((uint32_t)(q * 32) << 16);
+      mbar_wait(tfull0 + 8 * ab, (i >> 1) & 1);
+      tc_fence_after();
+      // The last unit of a CTA runs after its final MMA, when the smem ring is idle: stage the tile
+      // through the ring so that global stores are full 128-B row segments (a row-per-thread store
+      // pattern costs ~4 us per tile in uncoalesced 16-B transactions).
+      gemm_epilogue<BN, EPI, S::kStg, S::kStgOff>(smem, u + (int)gridDim.x >= units, out_, M, N, mt, splits, u, m0,
+                                                   n_idx, nkb, tl, ep);
       tc_fence_before();
       mbar_arrive(tempty0 + 8 * ab);
       if (trace && threadIdx.x == 64 && u + (int)gridDim.x >= units) trace[blockIdx.x * 6 + 4] = globaltimer();
@@ -691,97 +702,10 @@ __global__ void __launch_bounds__(192, 1)
       int m0, n_idx, kb0, nkb;
       decode(u, m0, n_idx, kb0, nkb);
       const int ab = i & 1;
-      const int row = m0 + q * 32 + lane;
       const uint32_t tl = tmem + ab * S::kAcc + ((uint32_t)(q * 32) << 16);
-      const int n0 = n_idx * BN;
       mbar_wait(tfull0 + 8 * ab, (i >> 1) & 1);
       tc_fence_after();
-      // The last unit of a CTA runs after its final MMA, when the smem ring is idle: stage the tile
-      // through the ring so that global stores are full 128-B row segments (a row-per-thread store
-      // pattern costs ~4 us per tile in uncoalesced 16-B transactions).
-      const bool stage = u + ncl >= units;
-      uint8_t* stg = smem + (size_t)(warp - 2) * ((BN + 31) / 32) * 4096;
-      constexpr int stg_chunk = 4096;
-      const int mrow0 = m0 + q * 32;
-      if constexpr (EPI == EPI_PARTIAL) {
-        const int sp = (u / mt) % splits;
-        float* obase = reinterpret_cast<float*>(out_) + (size_t)sp * M * N;
-        float* orow = obase + (size_t)row * N;
-        const int ncol = min(BN, N - n0);  // multiple of 16
-        if (nkb > 0 && stage) {
-#pragma unroll 1
-          for (int c = 0; c < BN; c += 32) {
-            float v[32];
-            tmem_ld32(tl + c, v);
-            __syncwarp();  // the previous chunk's reads of a reused staging buffer are done
-            float4* sb = reinterpret_cast<float4*>(stg + (c / 32) * stg_chunk);  // [32 rows][8 float4], XOR-swizzled
-#pragma unroll
-            for (int j = 0; j < 8; ++j)
-              sb[lane * 8 + (j ^ (lane & 7))] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
-            __syncwarp();
-            const int jj = lane & 7;
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              const int r = i * 4 + (lane >> 3);
-              if (mrow0 + r < M && c + 4 * jj < ncol)
-                *reinterpret_cast<float4*>(obase + (size_t)(mrow0 + r) * N + n0 + c + 4 * jj) = sb[r * 8 + (jj ^ (r & 7))];
-            }
-          }
-        } else if (nkb > 0) {
-#pragma unroll 1
-          for (int c = 0; c < BN; c += 32) {
-            float v[32];
-            tmem_ld32(tl + c, v);  // columns beyond BN are allocated (power-of-2 TMEM) and ignored
-            if (row < M)
-#pragma unroll
-              for (int j = 0; j < 8; ++j)
-                if (c + 4 * j < ncol)
-                  reinterpret_cast<float4*>(orow + n0 + c)[j] =
-                      make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
-          }
-        } else if (row < M) {
-          for (int col = n0; col < n0 + ncol; col += 4)
-            *reinterpret_cast<float4*>(orow + col) = make_float4(0.f, 0.f, 0.f, 0.f);
-        }
-      } else {
-        constexpr int G = BN / 2;
-        constexpr int PR = G / 8;                 // 16-B pieces per row of the u tile
-        constexpr int PS = PR | 1;                // odd smem row stride (in pieces): conflict-free
-        const int F = N / 2;
-        uint16_t* urow = reinterpret_cast<uint16_t*>(out_) + (size_t)row * F + (size_t)n_idx * G;
-        uint4* sb = reinterpret_cast<uint4*>(stg);
-        const float rs = norm_scale(ep, row, M);  // fused RMSNorm row scale (1 if the input was normalised)
-#pragma unroll 1
-        for (int c = 0; c < G; c += 16) {
-          float gv[16], uv[16];
-          tmem_ld16(tl + c, gv);
-          tmem_ld16(tl + G + c, uv);
-          uint32_t pk[8];
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const float g0 = gv[2 * j] * rs, g1 = gv[2 * j + 1] * rs;
-            pk[j] = pack_bf16(g0 / (1.f + __expf(-g0)) * (uv[2 * j] * rs), g1 / (1.f + __expf(-g1)) * (uv[2 * j + 1] * rs));
-          }
-          if (stage) {
-            sb[lane * PS + c / 8] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-            sb[lane * PS + c / 8 + 1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
-          } else if (row < M && n_idx * G + c < F) {
-            uint4* dst = reinterpret_cast<uint4*>(urow + c);
-            dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-            dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
-          }
-        }
-        if (stage) {
-          __syncwarp();
-          uint16_t* ubase = reinterpret_cast<uint16_t*>(out_) + (size_t)n_idx * G;
-#pragma unroll 1
-          for (int p = lane; p < 32 * PR; p += 32) {
-            const int r = p / PR, pc = p - r * PR;
-            if (mrow0 + r < M && n_idx * G + pc * 8 < F)
-              *reinterpret_cast<uint4*>(ubase + (size_t)(mrow0 + r) * F + pc * 8) = sb[r * PS + pc];
-          }
-        }
-      }
+      gemm_epilogue<BN, EPI, 0, 0>(smem, u + ncl >= units, out_, M, N, mt, splits, u, m0, n_idx, nkb, tl, ep);
       tc_fence_before();
       if constexpr (CL == 2)
         mbar_arrive_cluster(temptyL + 8 * ab);  // the leader's MMA reuses the pair's accumulator
@@ -918,9 +842,12 @@ cudaError_t prepare_gemm() {
 #undef P5
 #define P3(bn)                                                   \
   if (e == cudaSuccess) e = prep_t<bn, EPI_PARTIAL, 2>();        \
-  if (e == cudaSuccess) e = prep_t<bn, EPI_SWIGLU, 2>();
+  if (e == cudaSuccess) e = prep_t<bn, EPI_SWIGLU, 2>();         \
+  if (e == cudaSuccess) e = prep_t<bn, EPI_RESID, 2>();
   PIC_PAIR_BNS(P3)
 #undef P3
+  if (e == cudaSuccess) e = prep_t<128, EPI_QKV, 2>();
+  if (e == cudaSuccess) e = prep_t<256, EPI_QKV, 2>();
   return e;
 }
 
@@ -937,8 +864,18 @@ bool gemm_resid_supported(int bn) {
 }
 
 cudaError_t launch_gemm_resid(const CUtensorMap& A, const CUtensorMap& B, float* h, int M, int N, int K, int bn,
-                              cudaStream_t st, const GemmNext& nx, const GemmEpi& ep) {
+                              cudaStream_t st, const GemmNext& nx, const GemmEpi& ep, int pair) {
   if (ep.norm_gain && (N + bn - 1) / bn > kSsqStride) return cudaErrorInvalidValue;
+  if (pair) {
+    switch (bn) {
+#define L7(b) \
+  case b:     \
+    return launch_gemm_t<b, EPI_RESID, 2>(A, B, h, M, N, K, 1, 0, st, nx, ep);
+      PIC_PAIR_BNS(L7)
+#undef L7
+    }
+    return cudaErrorInvalidValue;
+  }
   switch (bn) {
 #define L5(b) \
   case b:     \
@@ -950,7 +887,12 @@ cudaError_t launch_gemm_resid(const CUtensorMap& A, const CUtensorMap& B, float*
 }
 
 cudaError_t launch_gemm_qkv(const CUtensorMap& A, const CUtensorMap& B, const GemmEpi& ep, int M, int N, int K, int bn,
-                            cudaStream_t st, const GemmNext& nx) {
+                            cudaStream_t st, const GemmNext& nx, int pair) {
+  if (pair) {
+    if (bn == 128) return launch_gemm_t<128, EPI_QKV, 2>(A, B, nullptr, M, N, K, 1, 0, st, nx, ep);
+    if (bn == 256) return launch_gemm_t<256, EPI_QKV, 2>(A, B, nullptr, M, N, K, 1, 0, st, nx, ep);
+    return cudaErrorInvalidValue;
+  }
   switch (bn) {
 #define L6(b) \
   case b:     \

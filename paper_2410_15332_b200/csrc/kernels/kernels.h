@@ -120,10 +120,12 @@ bool gemm_pair_supported(int bn);
 // Split-K = 1 GEMMs with the consumer fused into the epilogue (tensor-bound shapes, no partials):
 //   resid: h[M][N] += A·Bᵀ (a7 O projection / a8 down projection + residual add, fp32 h)
 //   qkv:   A·W_qkvᵀ -> RoPE at pos -> Q dense, K/V -> pool slots (a5); bn = 128 or 256 (whole heads)
+// pair = 1: CTA-pair kernel (256-row M-tiles; B's tensor map box must then be bn/2 rows)
 cudaError_t launch_gemm_resid(const CUtensorMap& A, const CUtensorMap& B, float* h, int M, int N, int K, int bn,
-                              cudaStream_t st, const GemmNext& nx = GemmNext{}, const GemmEpi& ep = GemmEpi{});
+                              cudaStream_t st, const GemmNext& nx = GemmNext{}, const GemmEpi& ep = GemmEpi{},
+                              int pair = 0);
 cudaError_t launch_gemm_qkv(const CUtensorMap& A, const CUtensorMap& B, const GemmEpi& ep, int M, int N, int K,
-                            int bn, cudaStream_t st, const GemmNext& nx = GemmNext{});
+                            int bn, cudaStream_t st, const GemmNext& nx = GemmNext{}, int pair = 0);
 bool gemm_resid_supported(int bn);
 // Gate/up GEMM with the SwiGLU epilogue fused: B = interleaved [gate|up] groups of bn/2 rows (N2 = 2F rows),
 // u[M][F] bf16 = silu(x·W_gᵀ) ⊙ (x·W_uᵀ).  Split-K 1.
