@@ -537,8 +537,9 @@ __global__ void __launch_bounds__(192, 1)
   tc_fence_before();
   if constexpr (CL == 2)
     cluster_sync();  // barrier inits and TMEM allocations of both CTAs visible before any cross-CTA use
-  else
-    __syncthreads();
+  // (also a CTA barrier for the pair: compute-sanitizer's racecheck does not treat the cluster barrier as
+  // ordering the allocator's smem write of the TMEM address against the read below)
+  __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   // the leader's accumulator-empty barriers (both CTAs' epilogues release the pair's accumulator there)
