@@ -426,6 +426,8 @@ __global__ void __launch_bounds__(ROT ? 320 + 32 * kRotWarps : 320, 1)
       // P(t) overwrites this half's S(t) columns (already in registers); PV(t) reads it from TMEM
       tmem_st32u(sAddr, pk);
       tmem_wait_st();
+      // consume every o_full phase (PV(t-1) has long finished here): no barrier phase completes unobserved
+      if (t >= 1) mbar_wait(o_full + 8 * ((t - 1) & 1), ((t - 1) >> 1) & 1);
       tc_fence_before();
       mbar_arrive(p_full + 8 * sb);
       if (trc) acc_ex += globaltimer() - tt0;

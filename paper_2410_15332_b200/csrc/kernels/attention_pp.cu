@@ -618,6 +618,8 @@ __global__ void __launch_bounds__(ROT ? 512 : 384, 1)
         const float s0 = la.x, s1 = la.y, s2 = lb.x, s3 = lb.y;
         l += (s0 + s1) + (s2 + s3);
         tmem_wait_st();
+        // consume every o_full phase (PV of the previous step has long finished): none completes unobserved
+        if (s >= 1) mbar_wait(B(bOFull + x), (cs - 1) & 1);
         tc_fence_before();
         mbar_arrive(B(bPFull + x));
         ++cs;
