@@ -520,6 +520,10 @@ static pic_status init_device(pic_engine* e, void* arena, size_t bytes, cudaStre
         e->gu_group = g;
       }
     }
+    if (const char* ge = getenv("PIC_GU_GROUP")) {  // A/B override of the interleave group
+      const int g = atoi(ge);
+      if (g > 0 && F % g == 0 && gemm_bn_supported(2 * g, true)) e->gu_group = g;
+    }
   }
   e->layers.resize(c.n_layers);
   for (int l = 0; l < c.n_layers; ++l) {

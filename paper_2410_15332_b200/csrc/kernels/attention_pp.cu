@@ -407,9 +407,11 @@ __global__ void __launch_bounds__(ROT ? 512 : 384, 1)
     };
     auto rotate_tile = [&](int k, const int* bd, int j, int last_blk) {
       const int sl = k % kKS;
+      // the tile's 8 block deltas: one load by lanes 0-7, broadcast by shuffles (not 8 loads per thread)
+      const int mine = lane < 8 ? bd[min(j * 8 + lane, last_blk)] : 0;
       int dl[8];
 #pragma unroll
-      for (int m = 0; m < 8; ++m) dl[m] = bd[min(j * 8 + m, last_blk)];
+      for (int m = 0; m < 8; ++m) dl[m] = __shfl_sync(0xffffffffu, mine, m);
       int dfirst = 0;
 #pragma unroll
       for (int m = 7; m >= 0; --m) dfirst = dl[m] ? dl[m] : dfirst;
