@@ -86,7 +86,7 @@ def describe(w, world: int, tp: bool, wave: int, kv_share: bool, layers) -> dict
          "model": m.name, "n_layers": m.n_layers, "d_model": m.d_model, "vocab": m.vocab,
          "chunk_len": len(w.chunks[0]), "n_chunks": n_chunks, "query_len": q, "alg": w.alg,
          "tokens_per_request": n_tokens(w, r0), "requests_total": nreq, "requests_per_gpu": per_rank,
-         "wave": min(wave, per_rank) if not tp else 1, "kv_share": bool(kv_share),
+         "wave": min(wave, per_rank) if not tp else 1, "kv_share": int(kv_share),
          "parallelism": (f"tp{world} (heads/MLP sharded, fused peer-memory all-reduce)" if tp
                          else f"dp{world} (request r -> rank r mod {world}, no collective)"),
          "l2": "inputs larger than L2 (weights 15 GB re-read every wave), no flush"}
@@ -327,9 +327,10 @@ def main():
                     help="tensor parallel over all ranks (default for cfg5 at N > 1): heads/MLP columns sharded, "
                          "fused peer-memory all-reduce; one request split over the ranks")
     ap.add_argument("--layers", type=int, default=None, help="truncate depth (functional runs only; marked in config)")
-    ap.add_argument("--kv-share", type=int, default=1, choices=[0, 1],
-                    help="f3 shared-block link: chunk-store blocks linked by reference, keys re-based in the "
-                         "attention K-tile load (pic_link_params.kv_share)")
+    ap.add_argument("--kv-share", type=int, default=1, choices=[0, 1, 2],
+                    help="0: copy path (a2 copies K+V); 1: f3 shared-block link (chunk-store blocks linked by "
+                         "reference, keys re-based in the attention K-tile load); 2: V by reference, keys "
+                         "re-based by a2 into fresh blocks (pic_link_params.kv_share)")
     ap.add_argument("--decode-steps", type=int, default=16,
                     help="f1: decode steps over the first wave's linked caches after the link measurement (0 = skip)")
     args = ap.parse_args()
@@ -395,7 +396,7 @@ def main():
         eng = B.Engine(m, num_blocks=total_tokens // 16 + 2 * len(w.chunks) + wave_blocks + 64 * wave_max,
                        max_rows=max(4096, rows_link), max_tokens=max(max_N + 2 * args.decode_steps + 16, 512) + 16,
                        max_requests=wave_max, device=dev, stream=stream, **tp_kw)
-        eng.kv_share = bool(args.kv_share)
+        eng.kv_share = int(args.kv_share)
         if tp and world > 1:
             D.tp_connect(eng)
         ids = eng.generate_context_cache(w.chunks, dummy_prefix=dummy_prefix(w.alg))
@@ -476,7 +477,7 @@ def main():
                     else [eng.link(first[0], w.alg, keep_linked=True)])
             hs = [o.linked for o in held]
             mat_ms = None
-            if args.kv_share:
+            if args.kv_share == 1:
                 # shared-block links: re-base the shared blocks into owned ones once (pic_linked_materialize)
                 torch.cuda.synchronize(dev)
                 m0, m1 = mk(), mk()

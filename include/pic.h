@@ -111,7 +111,12 @@ typedef struct {
                                 block's Δ (R1) when they load the K tile, with the same arithmetic as the copy
                                 (a2), so results are bit-identical to kv_share = 0.  Only blocks holding a
                                 recomputed row, dynamic tokens or a chunk boundary are allocated and filled.
-                                Ignored for CacheBlend (its layer 0 rewrites every row).  Default 0 */
+                                2 = V by reference only: the same blocks keep their V rows in the chunk-store
+                                block (reference counted, read through a separate V block table) while their
+                                keys are re-based by a2 into fresh blocks, so the attention reads K without
+                                re-basing it; results are again bit-identical to kv_share = 0 (a2's keys, the
+                                store's values).  Ignored for CacheBlend (its layer 0 rewrites every row).
+                                Default 0 */
 } pic_link_params;
 
 /* Per-request result of a link. */
@@ -220,8 +225,9 @@ pic_status pic_linked_export(pic_engine* eng, const pic_linked* linked, int32_t 
 /* Number of tokens N and the block table (int32[ceil(N/16)], nullable) of a linked cache. */
 pic_status pic_linked_info(pic_engine* eng, const pic_linked* linked, int32_t* n_tokens, int32_t* block_table);
 /* Shared-block link (kv_share): number of blocks of `linked` that are chunk-store blocks
- * linked by reference, and per block (int32[ceil(N/16)], nullable) the Δ the attention applies to its keys
- * (0 for blocks the link owns).  Host-only bookkeeping. */
+ * linked by reference (kv_share 1: K and V; kv_share 2: V only), and per block (int32[ceil(N/16)],
+ * nullable) the Δ the attention applies to its keys (0 for blocks the link owns and for kv_share 2).
+ * Host-only bookkeeping. */
 pic_status pic_linked_sharing(pic_engine* eng, const pic_linked* linked, int32_t* n_shared, int32_t* block_delta);
 /* Re-base the shared chunk-store blocks (Δ != 0) of a kv_share linked cache into blocks it owns, on
  * `stream` (one a2 launch over their rows, all layers), dropping its references on them: later decode

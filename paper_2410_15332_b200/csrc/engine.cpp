@@ -391,7 +391,7 @@ static ArenaPlan plan_arena(const pic_model_config& c, const pic_engine_limits& 
   a.max_k2 = (int)std::min<size_t>((size_t)l.max_requests * l.max_tokens, (size_t)1 << 30);
   // per-row arrays (tok,pos,slot,seq,head) + tiles + seq offsets + bt + k2 (3) + CB (cand,forced,sel2,pos2,slot2,
   // keep,count) + tiles2 + head2
-  a.plan_ints = 5 * M + 3 * (size_t)a.max_tiles + a.max_seqs + 2 * (size_t)a.max_bt /* bt, bdelta */ + 3 * (size_t)a.max_k2 +
+  a.plan_ints = 5 * M + 3 * (size_t)a.max_tiles + a.max_seqs + 3 * (size_t)a.max_bt /* bt, bdelta, vbt */ + 4 * (size_t)a.max_k2 +
                 7 * (size_t)l.max_tokens + 8 * (size_t)a.max_tiles + M + 8192;  /* + attention items (8 ints) */
   a.off_plan = L.add(a.plan_ints * 4);
   // tensor parallel: two reduced-partial buffers (alternating per all-reduce), flags, epoch counter
@@ -900,11 +900,14 @@ static int32_t slot_of(const std::vector<int32_t>& bt, int32_t i) { return bt[i 
 // then keep their compile positions and carry Δ_c (0 without re-base), applied by the attention when it
 // loads them.  Every other block is fresh (a2 copies its unselected cached rows, a5 scatters the rest).
 // shared[b] = store block id or -1; delta[b] = Δ to apply (0 for fresh blocks).  Returns #fresh.
+// kv_share 2: the same blocks qualify, but only their V is linked by reference (vshared[b] = store block);
+// K gets a fresh block that a2 fills with the re-based keys, so the attention reads K without re-basing.
 static int plan_blocks(const pic_engine* e, const pic_link_params* pr, const LinkPlanHost& p,
-                       std::vector<int32_t>& shared, std::vector<int32_t>& delta) {
+                       std::vector<int32_t>& shared, std::vector<int32_t>& delta, std::vector<int32_t>* vshared = nullptr) {
   const int nb = (p.N + 15) / 16;
   shared.assign(nb, -1);
   delta.assign(nb, 0);
+  if (vshared) vshared->assign(nb, -1);
   if (pr->kv_share && pr->alg != PIC_CACHEBLEND) {
     std::vector<uint8_t> in_sel(p.N, 0);
     for (int32_t i : p.sel) in_sel[i] = 1;
@@ -916,6 +919,10 @@ static int plan_blocks(const pic_engine* e, const pic_link_params* pr, const Lin
         bool clean = true;
         for (int r = 0; r < 16 && clean; ++r) clean = !in_sel[s0 + j + r];
         if (!clean) continue;
+        if (pr->kv_share == 2) {
+          if (vshared) (*vshared)[(s0 + j) / 16] = ch.blocks[j / 16];
+          continue;
+        }
         shared[(s0 + j) / 16] = ch.blocks[j / 16];
         delta[(s0 + j) / 16] = pr->rebase ? p.chunk_delta[c] : 0;
       }
@@ -1221,6 +1228,7 @@ struct Runner {
 // Enqueue the whole forward on `st`.  Plan arrays are already on the device at the given pointers.
 struct DevPlan {
   int32_t *tok, *pos, *slot, *seq, *tiles, *seq_bt_off, *bt, *bdelta, *k2_src, *k2_dst, *k2_delta, *head_map;
+  int32_t *vbt = nullptr, *k2_vcopy = nullptr;  // kv_share 2: V block table, per-a2-row V copy flag
   int32_t *cb_cand, *cb_forced, *cb_sel2, *cb_pos2, *cb_slot2, *cb_keep, *cb_count, *tiles2, *head_map2;
   int n_tiles, n_tiles2;
   int32_t *attn_work, *attn_nsplit, *attn_work2, *attn_nsplit2;
@@ -1246,7 +1254,7 @@ static pic_status enqueue_forward(pic_engine* e, const Fwd& f, const DevPlan& dp
     const int n_first = k2_side ? 1 : L - f.k2_layer0;
     ++R.launches;
     PROF("kv_link", 8.0 * D * Hkv * (double)f.k2_src.size() * n_first, 0, launch_kv_link(e->Kpool, e->Vpool, dp.k2_src, dp.k2_dst, dp.k2_delta, (int)f.k2_src.size(), f.k2_layer0,
-                      n_first, e->layer_stride, Hkv, D, e->cos_t, e->sin_t, f.rebase, st, e->f32));
+                      n_first, e->layer_stride, Hkv, D, e->cos_t, e->sin_t, f.rebase, st, e->f32, 148 * 4, dp.k2_vcopy));
     if (k2_side) {
       CK(cudaEventRecord(e->k2_fork, st));
       CK(cudaStreamWaitEvent(e->side_stream, e->k2_fork, 0));
@@ -1254,7 +1262,8 @@ static pic_status enqueue_forward(pic_engine* e, const Fwd& f, const DevPlan& dp
         ++R.launches;
         // one CTA per SM: it shares each SM with the persistent GEMM CTA instead of crowding it out
         CKL(launch_kv_link(e->Kpool, e->Vpool, dp.k2_src, dp.k2_dst, dp.k2_delta, (int)f.k2_src.size(), l, 1,
-                           e->layer_stride, Hkv, D, e->cos_t, e->sin_t, f.rebase, e->side_stream, e->f32, 148));
+                           e->layer_stride, Hkv, D, e->cos_t, e->sin_t, f.rebase, e->side_stream, e->f32, 148,
+                           dp.k2_vcopy));
         CK(cudaEventRecord(e->k2_layer_done[l], e->side_stream));  // joined by layer l (the last by layer L-1)
       }
     }
@@ -1407,6 +1416,7 @@ static pic_status enqueue_forward(pic_engine* e, const Fwd& f, const DevPlan& dp
       a.kpool = nullptr;  // L2 prefetch of K/V pages: measured slower (TMA unit busy ahead of the real loads)
       a.vpool = e->Vpool;
       a.bdelta = dp.bdelta;
+      a.vbt = dp.vbt;
       a.cos_t = e->cos_t;
       a.sin_t = e->sin_t;
       a.Q = e->Q;
@@ -1435,7 +1445,7 @@ static pic_status enqueue_forward(pic_engine* e, const Fwd& f, const DevPlan& dp
     } else {
       ++R.launches;
       PROF("attention", attn_bytes, attn_flops, launch_attention_simt(e->Q, Kl, Vl, dp.seq, dp.seq_bt_off, dp.bt, pos, e->Obuf, M, Hq, Hkv, D,
-                               (float)(1.0 / std::sqrt((double)D)), st, e->f32, dp.bdelta, e->cos_t, e->sin_t));
+                               (float)(1.0 / std::sqrt((double)D)), st, e->f32, dp.bdelta, e->cos_t, e->sin_t, dp.vbt));
     }
     if (use_chain) {
       ChainParams cp{};
@@ -1547,7 +1557,7 @@ static pic_status enqueue_forward(pic_engine* e, const Fwd& f, const DevPlan& dp
 static void add_sig(std::vector<int64_t>& sig, const Fwd& f, const DevPlan& dp) {
   sig = {f.M,  dp.n_tiles, (int64_t)f.seq_bt_off.size(), (int64_t)f.bt.size(), (int64_t)f.k2_src.size(), f.k2_layer0,
          f.n_head, f.compile, f.rebase, f.cb, f.cb_layer, f.cb_T, f.M2, f.cb_override, dp.n_tiles2, f.attn_n_work,
-         f.attn_n_work2, f.kv_rot, f.attn_pp};
+         f.attn_n_work2, f.kv_rot, f.attn_pp, f.has_vbt, f.k2_konly};
   // attention split choice depends on the per-sequence block-table lengths
   for (size_t q = 0; q < f.seq_bt_off.size(); ++q) sig.push_back(f.seq_bt_off[q]);
 }
@@ -1625,6 +1635,8 @@ static pic_status run_forward(pic_engine* e, const Fwd& f, cudaStream_t st, bool
   dp.seq_bt_off = pk.put(f.seq_bt_off);
   dp.bt = pk.put(f.bt);
   dp.bdelta = f.kv_rot ? pk.put(f.bdelta) : nullptr;
+  dp.vbt = f.has_vbt ? pk.put(f.vbt) : nullptr;
+  dp.k2_vcopy = f.k2_konly ? pk.put(f.k2_vcopy) : nullptr;
   dp.k2_src = pk.put(f.k2_src);
   dp.k2_dst = pk.put(f.k2_dst);
   dp.k2_delta = pk.put(f.k2_delta);
@@ -1867,6 +1879,7 @@ struct ReqBuild {
   LinkPlanHost p;
   std::vector<int32_t> bt;
   std::vector<int32_t> shared, bdelta;  // f3: per block, store block linked by reference (or -1) and its Δ
+  std::vector<int32_t> vshared;         // kv_share 2: per block, store block holding its V (or -1)
   int n_fresh = 0;
 };
 
@@ -1879,6 +1892,11 @@ static void append_request(pic_engine* e, const pic_link_params* pr, ReqBuild& r
   f.bt.insert(f.bt.end(), rb.bt.begin(), rb.bt.end());
   f.bdelta.insert(f.bdelta.end(), rb.bdelta.begin(), rb.bdelta.end());
   for (int32_t dl : rb.bdelta) f.kv_rot |= dl != 0;
+  for (size_t b = 0; b < rb.bt.size(); ++b) {
+    const bool vs = b < rb.vshared.size() && rb.vshared[b] >= 0;
+    f.vbt.push_back(vs ? rb.vshared[b] : rb.bt[b]);
+    f.has_vbt |= vs;
+  }
   const bool cb = pr->alg == PIC_CACHEBLEND;
   const std::vector<int32_t>* rows = &p.sel;
   std::vector<int32_t> all;
@@ -1910,6 +1928,9 @@ static void append_request(pic_engine* e, const pic_link_params* pr, ReqBuild& r
       f.k2_src.push_back(slot_of(ch.blocks, j));
       f.k2_dst.push_back(slot_of(rb.bt, i));
       f.k2_delta.push_back(p.chunk_delta[c]);
+      const bool vref = !rb.vshared.empty() && rb.vshared[i / 16] >= 0;  // kv_share 2: V stays in the store
+      f.k2_vcopy.push_back(vref ? 0 : 1);
+      f.k2_konly |= vref;
     }
   }
 }
@@ -1933,7 +1954,7 @@ static pic_status link_impl(pic_engine* e, int32_t n_req, const pic_segment* con
     TRY(assemble(e, segs[r], n_segs[r], reqs[r].p));
     TRY(check_variant(e, pr, reqs[r].p));
     select_rows(pr, reqs[r].p);
-    reqs[r].n_fresh = plan_blocks(e, pr, reqs[r].p, reqs[r].shared, reqs[r].bdelta);
+    reqs[r].n_fresh = plan_blocks(e, pr, reqs[r].p, reqs[r].shared, reqs[r].bdelta, &reqs[r].vshared);
     need += reqs[r].n_fresh;
   }
   if (!e->alloc.can(need)) return fail(PIC_E_CAPACITY, "pool has %zu free blocks, link needs %lld",
@@ -1945,9 +1966,15 @@ static pic_status link_impl(pic_engine* e, int32_t n_req, const pic_segment* con
     reqs[r].bt = merge_blocks(reqs[r].shared, e->alloc.alloc(reqs[r].n_fresh));
     for (int32_t b : reqs[r].shared)
       if (b >= 0) e->alloc.retain(b);  // the linked cache holds the chunk-store block too
+    for (int32_t b : reqs[r].vshared)
+      if (b >= 0) e->alloc.retain(b);  // kv_share 2: the store block holding this block's V
   }
   auto rollback = [&]() {
-    for (auto& rb : reqs) e->alloc.release(rb.bt);
+    for (auto& rb : reqs) {
+      e->alloc.release(rb.bt);
+      for (int32_t b : rb.vshared)
+        if (b >= 0) e->alloc.release({b});
+    }
   };
   for (int r = 0; r < n_req; ++r) append_request(e, pr, reqs[r], r, f);
   f.debug_rows = std::max(reqs[0].p.N, f.M);  // debug_hidden row stride (pic.h)
@@ -2086,9 +2113,18 @@ static pic_status link_impl(pic_engine* e, int32_t n_req, const pic_segment* con
       h->blocks = reqs[r].bt;
       h->bdelta = reqs[r].bdelta;
       h->n_shared = (int32_t)reqs[r].bt.size() - reqs[r].n_fresh;
+      h->n_vshared = 0;
+      for (int32_t b : reqs[r].vshared) h->n_vshared += b >= 0;
+      if (h->n_vshared) {
+        h->vblocks.resize(h->blocks.size());
+        for (size_t b = 0; b < h->blocks.size(); ++b)
+          h->vblocks[b] = reqs[r].vshared[b] >= 0 ? reqs[r].vshared[b] : h->blocks[b];
+      }
       out_linked[r] = h;
     } else {
       e->alloc.release(reqs[r].bt);  // stream-ordered reuse on the same stream
+      for (int32_t b : reqs[r].vshared)
+        if (b >= 0) e->alloc.release({b});
     }
   }
   return PIC_OK;
@@ -2121,12 +2157,14 @@ extern "C" pic_status pic_decode(pic_engine* e, pic_linked* const* linked, const
       grown[b] = e->alloc.alloc(1)[0];
       linked[b]->blocks.push_back(grown[b]);
       linked[b]->bdelta.push_back(0);
+      if (!linked[b]->vblocks.empty()) linked[b]->vblocks.push_back(grown[b]);
     }
   auto rollback = [&]() {
     for (int b = 0; b < n; ++b)
       if (grown[b] >= 0) {
         linked[b]->blocks.pop_back();
         linked[b]->bdelta.pop_back();
+        if (!linked[b]->vblocks.empty()) linked[b]->vblocks.pop_back();
         e->alloc.release({grown[b]});
       }
   };
@@ -2140,6 +2178,9 @@ extern "C" pic_status pic_decode(pic_engine* e, pic_linked* const* linked, const
     f.bt.insert(f.bt.end(), h.blocks.begin(), h.blocks.end());
     f.bdelta.insert(f.bdelta.end(), h.bdelta.begin(), h.bdelta.end());
     for (int32_t dl : h.bdelta) f.kv_rot |= dl != 0;
+    const std::vector<int32_t>& vb = h.vblocks.empty() ? h.blocks : h.vblocks;
+    f.vbt.insert(f.vbt.end(), vb.begin(), vb.end());
+    f.has_vbt |= h.n_vshared > 0;
     add_tiles(f.tiles, b, b, 1, qpt);
     f.tok.push_back(tokens[b]);
     f.pos.push_back(h.n_tokens);
@@ -2216,7 +2257,8 @@ extern "C" pic_status pic_link_batch(pic_engine* e, int32_t n_req, const pic_seg
 
 // ============================================================================ exports / lifecycle
 static pic_status export_rows(pic_engine* e, const std::vector<int32_t>& blocks, int n, int layer, void* k_host,
-                              void* v_host) {
+                              void* v_host, const std::vector<int32_t>* vblocks = nullptr) {
+  if (vblocks && vblocks->empty()) vblocks = nullptr;
   if (e->host_only) return fail(PIC_E_NO_DEVICE, "host-only engine");
   if (layer < 0 || layer >= e->cfg.n_layers) return fail(PIC_E_INVALID_ARG, "layer out of range");
   const int Hkv = e->cfg.n_kv_heads, D = e->cfg.head_dim;
@@ -2232,9 +2274,11 @@ static pic_status export_rows(pic_engine* e, const std::vector<int32_t>& blocks,
       if (k_host)
         CK(cudaMemcpy2D(reinterpret_cast<char*>(k_host) + dst, Hkv * row, reinterpret_cast<char*>(e->Kpool) + src * es,
                         row, row, rows, cudaMemcpyDeviceToHost));
-      if (v_host)
-        CK(cudaMemcpy2D(reinterpret_cast<char*>(v_host) + dst, Hkv * row, reinterpret_cast<char*>(e->Vpool) + src * es,
+      if (v_host) {  // V from its own block when linked by reference (kv_share 2)
+        const size_t vsrc = vblocks ? (size_t)layer * e->layer_stride + ((size_t)(*vblocks)[b] * Hkv + g) * 16 * D : src;
+        CK(cudaMemcpy2D(reinterpret_cast<char*>(v_host) + dst, Hkv * row, reinterpret_cast<char*>(e->Vpool) + vsrc * es,
                         row, row, rows, cudaMemcpyDeviceToHost));
+      }
     }
   }
   return PIC_OK;
@@ -2248,7 +2292,7 @@ extern "C" pic_status pic_linked_export(pic_engine* e, const pic_linked* h, int3
   if (k_host)
     for (size_t b = 0; b < h->bdelta.size(); ++b)
       if (h->bdelta[b] != 0) idx.push_back((int)b);
-  if (idx.empty()) return export_rows(e, h->blocks, h->n_tokens, layer, k_host, v_host);
+  if (idx.empty()) return export_rows(e, h->blocks, h->n_tokens, layer, k_host, v_host, &h->vblocks);
   // Shared blocks (f3) hold keys at their compile positions.  Their re-based rows are produced on the
   // device by a2's kernel (kv_link, this layer only) into scratch pool blocks — the arithmetic the
   // attention kernels' K-tile rotation reproduces bit for bit — and exported from there.
@@ -2293,7 +2337,7 @@ extern "C" pic_status pic_linked_info(pic_engine* e, const pic_linked* h, int32_
 
 extern "C" pic_status pic_linked_sharing(pic_engine* e, const pic_linked* h, int32_t* n_shared, int32_t* block_delta) {
   if (!e || !h) return fail(PIC_E_INVALID_ARG, "NULL argument");
-  if (n_shared) *n_shared = h->n_shared;
+  if (n_shared) *n_shared = h->n_shared + h->n_vshared;  // K-and-V (kv_share 1) or V-only (kv_share 2) by reference
   if (block_delta) std::copy(h->bdelta.begin(), h->bdelta.end(), block_delta);
   return PIC_OK;
 }
@@ -2353,6 +2397,8 @@ extern "C" pic_status pic_linked_materialize(pic_engine* e, pic_linked* h, void*
 extern "C" pic_status pic_linked_release(pic_engine* e, pic_linked* h) {
   if (!e || !h) return fail(PIC_E_INVALID_ARG, "NULL argument");
   e->alloc.release(h->blocks);
+  for (size_t b = 0; b < h->vblocks.size(); ++b)  // kv_share 2: the chunk-store blocks holding V
+    if (h->vblocks[b] != h->blocks[b]) e->alloc.release({h->vblocks[b]});
   delete h;
   return PIC_OK;
 }

@@ -70,7 +70,11 @@ struct Fwd {
   std::vector<int32_t> seq_bt_off, bt;        // block tables (concatenated)
   std::vector<int32_t> bdelta;                // per bt entry: Δ still to apply to a shared block's keys (f3)
   bool kv_rot = false;                        // some bdelta != 0: attention re-bases K tiles on load
+  std::vector<int32_t> vbt;                   // per bt entry: V's block (kv_share 2: the chunk-store block)
+  bool has_vbt = false;                       // some vbt entry differs from bt
   std::vector<int32_t> k2_src, k2_dst, k2_delta;  // a2 work: cached rows gathered into linked blocks
+  std::vector<int32_t> k2_vcopy;              // per a2 row: 1 = copy V too, 0 = K only (V by reference)
+  bool k2_konly = false;                      // some a2 row copies K only
   int k2_layer0 = 0;
   std::vector<int32_t> head_map;              // per final row: request index or -1
   int n_head = 0;                             // requests producing logits (0 = compile)
@@ -116,6 +120,10 @@ struct pic_linked {
   std::vector<int32_t> blocks;
   std::vector<int32_t> bdelta;  // per block: Δ of a chunk-store block linked by reference (f3), else 0
   int32_t n_shared = 0;         // blocks linked by reference
+  // kv_share 2: per block, the block holding its V rows — the chunk-store block (referenced, V by reference)
+  // or blocks[b]; empty = blocks
+  std::vector<int32_t> vblocks;
+  int32_t n_vshared = 0;        // blocks whose V is linked by reference
 };
 
 struct pic_engine {

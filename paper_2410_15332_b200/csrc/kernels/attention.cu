@@ -147,18 +147,28 @@ __global__ void __launch_bounds__(ROT ? 320 + 32 * kRotWarps : 320, 1)
         tma_prefetch(&tmV8);
       }
       const int kv_base = a.layer * a.num_blocks;
-      // the 8 paged-block ids of a 128-key tile: one coalesced load by lanes 0-7, one tile ahead
+      // the 8 paged-block ids of a 128-key tile: one coalesced load by lanes 0-7, one tile ahead; V's
+      // own table when V is linked by reference (kv_share 2)
+      const int* vbt = a.vbt ? a.vbt + a.seq_bt_off[seq] : bt;
       int blk_next = lane < 8 ? bt[min(j0 * 8 + lane, last_blk)] : 0;
+      int vblk_next = lane < 8 ? vbt[min(j0 * 8 + lane, last_blk)] : 0;
       for (int t = 0; t < n; ++t) {
         const int s = t % S;
         const uint32_t ph = (t / S) & 1;
-        const int blk_mine = blk_next;
-        if (t + 1 < n && lane < 8) blk_next = bt[min((j0 + t + 1) * 8 + lane, last_blk)];
-        int blk[8];
+        const int blk_mine = blk_next, vblk_mine = vblk_next;
+        if (t + 1 < n && lane < 8) {
+          blk_next = bt[min((j0 + t + 1) * 8 + lane, last_blk)];
+          vblk_next = vbt[min((j0 + t + 1) * 8 + lane, last_blk)];
+        }
+        int blk[8], vblk[8];
 #pragma unroll
-        for (int b = 0; b < 8; ++b) blk[b] = __shfl_sync(0xffffffffu, blk_mine, b);
+        for (int b = 0; b < 8; ++b) {
+          blk[b] = __shfl_sync(0xffffffffu, blk_mine, b);
+          vblk[b] = __shfl_sync(0xffffffffu, vblk_mine, b);
+        }
         // 8 consecutive block ids: one 8-block box per half instead of 8 one-block boxes
         const bool contig = __all_sync(0xffffffffu, lane >= 8 || blk_mine == blk[0] + lane);
+        const bool vcontig = __all_sync(0xffffffffu, lane >= 8 || vblk_mine == vblk[0] + lane);
         if (lane == 0) {
           mbar_wait(k_empty + 8 * s, ph ^ 1);
           mbar_expect_tx(k_full + 8 * s, 2 * kTile);
@@ -174,15 +184,15 @@ __global__ void __launch_bounds__(ROT ? 320 + 32 * kRotWarps : 320, 1)
           }
           mbar_wait(v_empty + 8 * s, ph ^ 1);
           mbar_expect_tx(v_full + 8 * s, 2 * kTile);
-          if (contig) {
+          if (vcontig) {
             for (int h = 0; h < 2; ++h)
-              tma_load_4d(base + kV + (2 * s + h) * kTile, &tmV8, v_full + 8 * s, h * 64, 0, g, kv_base + blk[0]);
+              tma_load_4d(base + kV + (2 * s + h) * kTile, &tmV8, v_full + 8 * s, h * 64, 0, g, kv_base + vblk[0]);
           } else {
 #pragma unroll
             for (int b = 0; b < 8; ++b)
               for (int h = 0; h < 2; ++h)
                 tma_load_4d(base + kV + (2 * s + h) * kTile + b * 2048, &tmV, v_full + 8 * s, h * 64, 0, g,
-                            kv_base + blk[b]);
+                            kv_base + vblk[b]);
           }
         }
         __syncwarp();
@@ -662,7 +672,7 @@ __global__ void attn_simt_kernel(const void* __restrict__ Q, const void* __restr
                                  const int32_t* __restrict__ bt, const int32_t* __restrict__ row_pos,
                                  void* __restrict__ O, int M, int Hq, int Hkv, float scale,
                                  const int32_t* __restrict__ bdelta, const float* __restrict__ cos_t,
-                                 const float* __restrict__ sin_t) {
+                                 const float* __restrict__ sin_t, const int32_t* __restrict__ vbt) {
   PIC_PDL_ENTRY();
   const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
@@ -677,6 +687,11 @@ __global__ void attn_simt_kernel(const void* __restrict__ Q, const void* __restr
   const int* tbd = bdelta ? bdelta + seq_bt_off[row_seq[row]] : nullptr;
   auto kv_off = [&](int key) -> size_t {
     const int blk = tb[key / 16];
+    return (((size_t)blk * Hkv + g) * 16 + (key % 16)) * D;
+  };
+  const int* vtb = vbt ? vbt + seq_bt_off[row_seq[row]] : tb;  // V linked by reference (kv_share 2)
+  auto v_off = [&](int key) -> size_t {
+    const int blk = vtb[key / 16];
     return (((size_t)blk * Hkv + g) * 16 + (key % 16)) * D;
   };
   // key row of `key` at its linked position: a shared chunk-store block (f3) is re-based by its Δ on
@@ -725,8 +740,9 @@ __global__ void attn_simt_kernel(const void* __restrict__ Q, const void* __restr
     for (int i = 0; i < D; ++i) s += q[i] * kr[i];
     const float p = expf(s * scale - mx);
     l += p;
+    const size_t voff = v_off(key);
 #pragma unroll
-    for (int i = 0; i < D; ++i) o[i] += p * ldx<F32>(Vp, off + i);
+    for (int i = 0; i < D; ++i) o[i] += p * ldx<F32>(Vp, voff + i);
   }
   l = warp_sum(l);
 #pragma unroll
@@ -746,12 +762,12 @@ __global__ void attn_simt_kernel(const void* __restrict__ Q, const void* __restr
 cudaError_t launch_attention_simt(const void* Q, const void* Kpool_l, const void* Vpool_l, const int32_t* row_seq,
                                   const int32_t* seq_bt_off, const int32_t* bt, const int32_t* row_pos, void* O,
                                   int M, int Hq, int Hkv, int D, float scale, cudaStream_t st, int f32,
-                                  const int32_t* bdelta, const float* cos_t, const float* sin_t) {
+                                  const int32_t* bdelta, const float* cos_t, const float* sin_t, const int32_t* vbt) {
   const int warps = M * Hq;
   dim3 grid((warps + 3) / 4), block(128);
 #define SIMT_L(DD, FF)                                                                                              \
   CUDA_TRY_LAUNCH(launch_k(attn_simt_kernel<DD, FF>, dim3(grid), dim3(block), 0, st, Q, Kpool_l, Vpool_l, row_seq,  \
-                           seq_bt_off, bt, row_pos, O, M, Hq, Hkv, scale, bdelta, cos_t, sin_t))
+                           seq_bt_off, bt, row_pos, O, M, Hq, Hkv, scale, bdelta, cos_t, sin_t, vbt))
   if (f32) {
     switch (D) {
       case 16: SIMT_L(16, true); break;

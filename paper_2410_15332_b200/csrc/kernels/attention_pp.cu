@@ -257,6 +257,9 @@ __global__ void __launch_bounds__(ROT ? 512 : 384, 1)
         if (nB) ++qc1;
         const int* btA = a.bt + a.seq_bt_off[LA.seq];
         const int* btB = sh ? btA : (nB ? a.bt + a.seq_bt_off[LB.seq] : btA);
+        // V's own block table when V is linked by reference (kv_share 2)
+        const int* vbA = a.vbt ? a.vbt + a.seq_bt_off[LA.seq] : btA;
+        const int* vbB = a.vbt ? (sh ? vbA : (nB ? a.vbt + a.seq_bt_off[LB.seq] : vbA)) : btB;
         const int lastA = (sh ? max(LA.max_p, LB.max_p) : LA.max_p) / 16;
         const int lastB = LB.max_p / 16;
         for (int s = 0; s < nA; ++s) {
@@ -273,12 +276,12 @@ __global__ void __launch_bounds__(ROT ? 512 : 384, 1)
           }
           {
             const int k = vc++, sl = k % kVS;
-            load_tile(&tmV, &tmV8, base + kV + sl * 2 * kTile, B(bVFull + sl), B(bVEmpty + sl), (k / kVS) & 1, btA,
+            load_tile(&tmV, &tmV8, base + kV + sl * 2 * kTile, B(bVFull + sl), B(bVEmpty + sl), (k / kVS) & 1, vbA,
                       LA.j0 + s, lastA, g);
           }
           if (two) {
             const int k = vc++, sl = k % kVS;
-            load_tile(&tmV, &tmV8, base + kV + sl * 2 * kTile, B(bVFull + sl), B(bVEmpty + sl), (k / kVS) & 1, btB,
+            load_tile(&tmV, &tmV8, base + kV + sl * 2 * kTile, B(bVFull + sl), B(bVEmpty + sl), (k / kVS) & 1, vbB,
                       LB.j0 + s, lastB, g);
           }
         }

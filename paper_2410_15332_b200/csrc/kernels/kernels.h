@@ -71,10 +71,13 @@ cudaError_t launch_qkv_rope_scatter(const float* P, int splits, int P_rows, cons
 cudaError_t launch_swiglu(const float* P, int splits, void* u, int M, int F, cudaStream_t st, int f32 = 0);
 
 // ---- a2: KV link — gather cached rows into the linked blocks, RoPE re-base K by Δ -----------
+// vcopy (nullable = all rows): per row, 1 = copy its V too, 0 = K only (V linked by reference);
+// copy_k = 0: V only (materializing a V-by-reference block)
 cudaError_t launch_kv_link(void* Kpool, void* Vpool, const int32_t* src_slot, const int32_t* dst_slot,
                            const int32_t* delta, int n_rows, int layer0, int n_layers, int64_t layer_stride_elems,
                            int Hkv, int D, const float* cos_t, const float* sin_t, int rebase, cudaStream_t st,
-                           int f32 = 0, int max_ctas = 148 * 4);
+                           int f32 = 0, int max_ctas = 148 * 4,
+                           const int32_t* vcopy = nullptr, int copy_k = 1);
 
 // ---- GEMM (tcgen05): P[split][M][N] = A[M][K] · B[N][K]^T --------------------------------------
 // pack > 0: B is stored pre-tiled [N/pack][K/64][pack][64] (every TMA box contiguous); the tensor map
@@ -192,6 +195,9 @@ struct AttnArgs {
   void* O;
   // ping-pong kernel: [next item, CTAs done], zero before the launch; the last CTA resets both
   unsigned* item_ctr;
+  // V block table (nullable: V lives in the same blocks as K).  kv_share 2 links V by reference to the
+  // chunk-store blocks while K is a re-based copy in fresh blocks.
+  const int32_t* vbt;
   int debug;  // bench-only ablation (PIC_ATTN_DEBUG), results invalid: 1 = softmax skipped, 2 = no K re-base
              // arithmetic, 3 = rotation warpgroup idle, 4 = as 2 without the proxy fence
 };
@@ -219,7 +225,7 @@ cudaError_t launch_attention_simt(const void* Q, const void* Kpool_l, const void
                                   const int32_t* seq_bt_off, const int32_t* bt, const int32_t* row_pos, void* O,
                                   int M, int Hq, int Hkv, int D, float scale, cudaStream_t st, int f32 = 0,
                                   const int32_t* bdelta = nullptr, const float* cos_t = nullptr,
-                                  const float* sin_t = nullptr);
+                                  const float* sin_t = nullptr, const int32_t* vbt = nullptr);
 // fp32 debug build GEMM (CUDA cores, exact products): P[M][N] = A[M][K] (fp32) · B[N][K]^T (bf16 weights)
 cudaError_t launch_gemm_simt_f32(const float* A, const void* B, float* out, int M, int N, int K, cudaStream_t st);
 

@@ -472,7 +472,7 @@ __global__ void __launch_bounds__(256) kv_link_kernel(uint4* __restrict__ Kpool,
                                                       const int32_t* __restrict__ delta, int n_rows, int layer0,
                                                       int n_layers, int64_t layer_stride16, int Hkv, int D,
                                                       const float* __restrict__ cos_t, const float* __restrict__ sin_t,
-                                                      int rebase) {
+                                                      int rebase, const int32_t* __restrict__ vcopy, int copy_k) {
   PIC_PDL_ENTRY();
   const int cK = D / 16;              // 16-B chunks per half row
   const int rowq = D / 8;             // 16-B chunks per head-row
@@ -485,6 +485,7 @@ __global__ void __launch_bounds__(256) kv_link_kernel(uint4* __restrict__ Kpool,
     const int l = layer0 + (int)(u / n_rows);
     const int ss = src_slot[w], ds = dst_slot[w];
     const int dl = rebase ? delta[w] : 0;
+    const bool cv = vcopy == nullptr || vcopy[w] != 0;
     const int64_t lo = (int64_t)l * layer_stride16;
     const int64_t sb = lo + (int64_t)(ss >> 4) * Hkv * 16 * rowq + (ss & 15) * rowq;
     const int64_t db = lo + (int64_t)(ds >> 4) * Hkv * 16 * rowq + (ds & 15) * rowq;
@@ -493,9 +494,13 @@ __global__ void __launch_bounds__(256) kv_link_kernel(uint4* __restrict__ Kpool,
       if (i >= per) break;
       const int g = i / cK, c = i % cK;
       const int64_t so = sb + (int64_t)g * 16 * rowq + c, dof = db + (int64_t)g * 16 * rowq + c;
-      const uint4 xa = Kpool[so], xb = Kpool[so + cK], va = Vpool[so], vb = Vpool[so + cK];
-      Vpool[dof] = va;
-      Vpool[dof + cK] = vb;
+      if (cv) {
+        const uint4 va = Vpool[so], vb = Vpool[so + cK];
+        Vpool[dof] = va;
+        Vpool[dof + cK] = vb;
+      }
+      if (!copy_k) continue;
+      const uint4 xa = Kpool[so], xb = Kpool[so + cK];
       if (dl == 0) {
         Kpool[dof] = xa;
         Kpool[dof + cK] = xb;
@@ -530,7 +535,8 @@ __global__ void __launch_bounds__(256) kv_link_kernel(uint4* __restrict__ Kpool,
 __global__ void kv_link_f32_kernel(float* __restrict__ Kpool, float* __restrict__ Vpool, const int32_t* __restrict__ src_slot,
                                    const int32_t* __restrict__ dst_slot, const int32_t* __restrict__ delta, int n_rows,
                                    int layer0, int n_layers, int64_t layer_stride, int Hkv, int D,
-                                   const float* __restrict__ cos_t, const float* __restrict__ sin_t, int rebase) {
+                                   const float* __restrict__ cos_t, const float* __restrict__ sin_t, int rebase,
+                                   const int32_t* __restrict__ vcopy, int copy_k) {
   PIC_PDL_ENTRY();
   const int half = D / 2;
   const int64_t per_row = (int64_t)Hkv * (half + D);
@@ -548,9 +554,10 @@ __global__ void kv_link_f32_kernel(float* __restrict__ Kpool, float* __restrict_
     const int64_t so = (int64_t)l * layer_stride + ((int64_t)(ss / 16) * Hkv + g) * 16 * D + (int64_t)(ss % 16) * D;
     const int64_t dof = (int64_t)l * layer_stride + ((int64_t)(ds / 16) * Hkv + g) * 16 * D + (int64_t)(ds % 16) * D;
     if (!isK) {
-      Vpool[dof + j] = Vpool[so + j];
+      if (vcopy == nullptr || vcopy[w] != 0) Vpool[dof + j] = Vpool[so + j];
       continue;
     }
+    if (!copy_k) continue;
     const float a = Kpool[so + j], b = Kpool[so + j + half];
     const int dl = rebase ? delta[w] : 0;
     const int ad = dl < 0 ? -dl : dl;
@@ -565,19 +572,19 @@ __global__ void kv_link_f32_kernel(float* __restrict__ Kpool, float* __restrict_
 cudaError_t launch_kv_link(void* Kpool, void* Vpool, const int32_t* src_slot, const int32_t* dst_slot,
                            const int32_t* delta, int n_rows, int layer0, int n_layers, int64_t layer_stride_elems,
                            int Hkv, int D, const float* cos_t, const float* sin_t, int rebase, cudaStream_t st,
-                           int f32, int max_ctas) {
+                           int f32, int max_ctas, const int32_t* vcopy, int copy_k) {
   if (n_rows == 0 || n_layers == 0) return cudaSuccess;
   if (f32) {
     CUDA_TRY_LAUNCH(launch_k(kv_link_f32_kernel, dim3(148 * 8), dim3(256), 0, st, reinterpret_cast<float*>(Kpool),
                              reinterpret_cast<float*>(Vpool), src_slot, dst_slot, delta, n_rows, layer0, n_layers,
-                             layer_stride_elems, Hkv, D, cos_t, sin_t, rebase));
+                             layer_stride_elems, Hkv, D, cos_t, sin_t, rebase, vcopy, copy_k));
     return cudaGetLastError();
   }
   const int64_t warps = (int64_t)n_layers * n_rows;  // one warp per (layer, row)
   const int blocks = (int)std::min<int64_t>((warps + 7) / 8, max_ctas);
   CUDA_TRY_LAUNCH(launch_k(kv_link_kernel, dim3(blocks), dim3(256), 0, st, reinterpret_cast<uint4*>(Kpool), reinterpret_cast<uint4*>(Vpool), src_slot,
                                          dst_slot, delta, n_rows, layer0, n_layers, layer_stride_elems / 8, Hkv, D,
-                                         cos_t, sin_t, rebase));
+                                         cos_t, sin_t, rebase, vcopy, copy_k));
   return cudaGetLastError();
 }
 

@@ -275,7 +275,8 @@ class Engine:
         self._cfg = config_struct(cfg)
         self._lim = LimitsC(num_blocks, max_rows, max_tokens, max_requests)
         self.max_tokens = max_tokens
-        self.kv_share = False  # default of pic_link_params.kv_share (shared-block link, f3) for this engine's calls
+        self.kv_share = 0  # default of pic_link_params.kv_share for this engine's calls: 0 copy, 1 shared-block
+        #                    link (f3), 2 V by reference with re-based key copies
         self._h = C.c_void_p()
         self.arena = None
         self.device = device
@@ -354,7 +355,7 @@ class Engine:
                 kv_share=None):
         a, k, r = parse_alg(alg)
         share = self.kv_share if kv_share is None else kv_share
-        p = LinkParamsC(a, k, r, check_layer, int(rebase), int(use_graph), None, 0, None, int(bool(share)))
+        p = LinkParamsC(a, k, r, check_layer, int(rebase), int(use_graph), None, 0, None, int(share))
         keep = []
         if sel_override is not None:
             so = np.ascontiguousarray(sel_override, dtype=np.int32)
@@ -367,7 +368,7 @@ class Engine:
 
     def link(self, segments, alg: str, *, check_layer: int = 1, rebase: bool = True, use_graph: bool = True,
              want_logits: bool = True, logits_dev=None, keep_linked: bool = False, sel_override=None,
-             debug_hidden: bool = False, want_selected: bool = False, kv_share: Optional[bool] = None) -> LinkOutput:
+             debug_hidden: bool = False, want_selected: bool = False, kv_share: Optional[int] = None) -> LinkOutput:
         segs = _Segs(segments)
         hid = None
         N = self.plan(segments, alg)["n_tokens"] if (debug_hidden or want_selected) else 0
@@ -393,7 +394,7 @@ class Engine:
                           hid)
 
     def link_batch(self, requests, alg: str, *, use_graph: bool = True, want_logits: bool = True,
-                   keep_linked: bool = False, kv_share: Optional[bool] = None,
+                   keep_linked: bool = False, kv_share: Optional[int] = None,
                    debug_hidden: bool = False) -> List[LinkOutput]:
         """Batched link (pic_link_batch).  debug_hidden: every output's .hidden is the forward's
         [L][R][d] residual array (R = max(N_0, Σ k'); request r's rows follow those of requests < r,
@@ -444,7 +445,7 @@ class Engine:
 
     def serve_poisson(self, requests, alg: str, rate: float, duration_s: float, *, seed: int = 0x5E12E,
                       max_batch: Optional[int] = None, check_layer: int = 1, use_graph: bool = False,
-                      kv_share: Optional[bool] = None) -> dict:
+                      kv_share: Optional[int] = None) -> dict:
         """Open-loop Poisson serving (pic_serve_poisson, f4): user u resends requests[u] at rate/len(requests).
         Eager launches by default: batch compositions vary, so per-shape graphs would be captured per call."""
         n = len(requests)
@@ -458,7 +459,7 @@ class Engine:
         check(lib().pic_serve_poisson(self._h, C.byref(cfgc), self._stream, C.byref(out)))
         return {k: getattr(out, k) for k, _ in ServeStatsC._fields_}
 
-    def plan(self, segments, alg: str, kv_share: Optional[bool] = None) -> dict:
+    def plan(self, segments, alg: str, kv_share: Optional[int] = None) -> dict:
         segs = _Segs(segments)
         p, _ = self._params(alg, kv_share=kv_share)
         cap = self.max_tokens

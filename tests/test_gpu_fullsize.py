@@ -166,9 +166,9 @@ def test_long_context_16k_legolink_sampled_rows():
     eng.close()
 
 
-@pytest.mark.parametrize("kernel", [1, 2])
+@pytest.mark.parametrize("kernel,mode", [(1, 1), (2, 1), (2, 2)])
 @pytest.mark.parametrize("which", ["cfg2", "cfg3", "cfg4"])
-def test_fullsize_shared_block_link_bit_identical(which, kernel):
+def test_fullsize_shared_block_link_bit_identical(which, kernel, mode):
     """f3 shared-block link at full size in the bench's launch configuration (graphs, batched link for
     cfg4): logits, first tokens and sampled layers' linked K/V are bit-identical to the copy path, which
     the sampled-layer tests above hold to the oracle — on the same attention kernel for both paths
@@ -182,7 +182,7 @@ def test_fullsize_shared_block_link_bit_identical(which, kernel):
     try:
         ids = eng.generate_context_cache(w.chunks)
         reqs = [[("cached", ids[s.chunk]) if s.cached else ("tokens", s.tokens) for s in r] for r in w.requests]
-        outs = [eng.link_batch(reqs, w.alg, keep_linked=True, kv_share=share) for share in (False, True)]
+        outs = [eng.link_batch(reqs, w.alg, keep_linked=True, kv_share=share) for share in (0, mode)]
         shared = 0
         for a, b in zip(*outs):
             assert np.array_equal(a.logits, b.logits) and a.first_token == b.first_token

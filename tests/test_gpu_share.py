@@ -52,10 +52,10 @@ def setup(request):
     s.eng.close()
 
 
-def link_both(s, segs, alg, **kw):
+def link_both(s, segs, alg, modes=(0, 1), **kw):
     """(copy, shared) link outputs with their exported linked K/V of every layer."""
     outs = []
-    for share in (False, True):
+    for share in modes:
         free0 = s.eng.stats()["free_blocks"]
         o = s.eng.link(s.segs(segs), alg, keep_linked=True, kv_share=share, **kw)
         used = free0 - s.eng.stats()["free_blocks"]
@@ -96,6 +96,51 @@ def test_shared_link_bit_identical_to_copy(setup, alg):
             s.eng.release(shared[0].linked)
     if alg != "fr":
         assert any_shared > 0
+
+
+@pytest.mark.parametrize("alg", ALGS)
+def test_vshare_link_bit_identical_to_copy(setup, alg):
+    """kv_share 2: V linked by reference to the chunk-store blocks (separate V block table), keys re-based
+    by a2 into fresh blocks: bit-identical to the copy path; every block is fresh for K, the V-shared
+    blocks hold one extra reference on their store block, and releasing returns the pool exactly."""
+    s = setup
+    any_shared = 0
+    free0 = s.eng.stats()["free_blocks"]
+    for segs in [s.w.requests[0]] + sg.permuted_requests(s.w, 6):
+        copy, vsh = link_both(s, segs, alg, modes=(0, 2))
+        try:
+            assert_identical(copy, vsh)
+            n_blocks = (copy[0].n_tokens + 15) // 16
+            assert vsh[2] == n_blocks                        # K needs a fresh block everywhere
+            assert not vsh[4].any()                          # nothing for the attention to re-base
+            if alg == "fr":
+                assert vsh[3] == 0
+            any_shared += vsh[3]
+        finally:
+            s.eng.release(copy[0].linked)
+            s.eng.release(vsh[0].linked)
+    assert s.eng.stats()["free_blocks"] == free0
+    if alg != "fr":
+        assert any_shared > 0
+
+
+def test_vshare_decode_bit_identical(setup):
+    """Decode over a kv_share 2 linked cache reads V through the V block table: identical to the copy path."""
+    s = setup
+    segs = s.w.requests[0]
+    hs = [s.eng.link(s.segs(segs), "legolink:4", keep_linked=True, kv_share=share).linked for share in (0, 2)]
+    try:
+        for t in [5, 17, 99, 3, 250, 7, 11, 13, 2, 1, 0, 8, 9, 10, 12, 14, 15, 16, 18, 19]:
+            a = s.eng.decode([hs[0]], [t])
+            b = s.eng.decode([hs[1]], [t])
+            assert np.array_equal(a.logits, b.logits)
+        for l in range(s.cfg.n_layers):
+            ka, va = s.eng.linked_export(hs[0], l)
+            kb, vb = s.eng.linked_export(hs[1], l)
+            assert np.array_equal(ka, kb) and np.array_equal(va, vb), l
+    finally:
+        for h in hs:
+            s.eng.release(h)
 
 
 def test_shared_link_matches_oracle(setup):
