@@ -918,6 +918,8 @@ static int plan_blocks(const pic_engine* e, const pic_link_params* pr, const Lin
       for (int j = 0; j + 16 <= n; j += 16) {
         bool clean = true;
         for (int r = 0; r < 16 && clean; ++r) clean = !in_sel[s0 + j + r];
+        // kv_share 3: every block inside an aligned chunk keeps the chunk's compile frame (Δ), fresh or not
+        if (pr->kv_share == 3) delta[(s0 + j) / 16] = pr->rebase ? p.chunk_delta[c] : 0;
         if (!clean) continue;
         if (pr->kv_share == 2) {
           if (vshared) (*vshared)[(s0 + j) / 16] = ch.blocks[j / 16];
@@ -1229,6 +1231,7 @@ struct Runner {
 struct DevPlan {
   int32_t *tok, *pos, *slot, *seq, *tiles, *seq_bt_off, *bt, *bdelta, *k2_src, *k2_dst, *k2_delta, *head_map;
   int32_t *vbt = nullptr, *k2_vcopy = nullptr;  // kv_share 2: V block table, per-a2-row V copy flag
+  int32_t* kpos = nullptr;                       // kv_share 3: K heads' RoPE positions (chunk frames)
   int32_t *cb_cand, *cb_forced, *cb_sel2, *cb_pos2, *cb_slot2, *cb_keep, *cb_count, *tiles2, *head_map2;
   int n_tiles, n_tiles2;
   int32_t *attn_work, *attn_nsplit, *attn_work2, *attn_nsplit2;
@@ -1342,6 +1345,7 @@ static pic_status enqueue_forward(pic_engine* e, const Fwd& f, const DevPlan& dp
       } else {
         GemmEpi ep{pos, slot, e->cos_t, e->sin_t, e->Q, Kl, Vl, Hq, Hkv};
         ep_norm_in(ep);
+        if (pos == dp.pos) ep.kpos = dp.kpos;  // chunk-frame keys (kv_share 3); not CacheBlend's rows
         TRY(R.gemm_qkv(e->tm_x, w.tm_qkv, M, qkv, d, ep, &s, &qkv_fused, e->x, w.qkv));
         if (norm_tiles && !qkv_fused) return fail(PIC_E_CUDA, "internal: fused-norm input reached an unfused QKV GEMM");
       }
@@ -1375,7 +1379,7 @@ static pic_status enqueue_forward(pic_engine* e, const Fwd& f, const DevPlan& dp
     } else if (!qkv_fused) {
       ++R.launches;
       PROF("qkv_rope_scatter", (double)M * qkv * 4 * s + (double)M * qkv * 2, 0, launch_qkv_rope_scatter(e->ws, s, M, nullptr, pos, slot, e->cos_t, e->sin_t, e->Q, Kl, Vl, M, Hq, Hkv, D,
-                                 st, e->f32, pos == dp.pos ? 1 : 0));
+                                 st, e->f32, pos == dp.pos ? 1 : 0, pos == dp.pos ? dp.kpos : nullptr));
     }
     if (f.compile && l == L - 1) break;  // compile needs only the last layer's K/V
     if (k2_side && !f.cb && l > f.k2_layer0) CK(cudaStreamWaitEvent(st, e->k2_layer_done[l], 0));  // this layer's a2 landed
@@ -1557,7 +1561,7 @@ static pic_status enqueue_forward(pic_engine* e, const Fwd& f, const DevPlan& dp
 static void add_sig(std::vector<int64_t>& sig, const Fwd& f, const DevPlan& dp) {
   sig = {f.M,  dp.n_tiles, (int64_t)f.seq_bt_off.size(), (int64_t)f.bt.size(), (int64_t)f.k2_src.size(), f.k2_layer0,
          f.n_head, f.compile, f.rebase, f.cb, f.cb_layer, f.cb_T, f.M2, f.cb_override, dp.n_tiles2, f.attn_n_work,
-         f.attn_n_work2, f.kv_rot, f.attn_pp, f.has_vbt, f.k2_konly};
+         f.attn_n_work2, f.kv_rot, f.attn_pp, f.has_vbt, f.k2_konly, f.has_kpos, f.attn_qrot};
   // attention split choice depends on the per-sequence block-table lengths
   for (size_t q = 0; q < f.seq_bt_off.size(); ++q) sig.push_back(f.seq_bt_off[q]);
 }
@@ -1636,6 +1640,7 @@ static pic_status run_forward(pic_engine* e, const Fwd& f, cudaStream_t st, bool
   dp.bt = pk.put(f.bt);
   dp.bdelta = f.kv_rot ? pk.put(f.bdelta) : nullptr;
   dp.vbt = f.has_vbt ? pk.put(f.vbt) : nullptr;
+  dp.kpos = f.has_kpos ? pk.put(f.kpos) : nullptr;
   dp.k2_vcopy = f.k2_konly ? pk.put(f.k2_vcopy) : nullptr;
   dp.k2_src = pk.put(f.k2_src);
   dp.k2_dst = pk.put(f.k2_dst);
@@ -1907,9 +1912,13 @@ static void append_request(pic_engine* e, const pic_link_params* pr, ReqBuild& r
   }
   const int r0 = f.M;
   add_tiles(f.tiles, seq, r0, (int)rows->size(), qpt);
+  const bool frames = pr->kv_share == 3 && !cb;  // chunk-frame blocks: K stored at compile positions
   for (int32_t i : *rows) {
     f.tok.push_back(p.tok[i]);
     f.pos.push_back(i);  // p_i = i (R18)
+    const int32_t fr = frames ? rb.bdelta[i / 16] : 0;
+    f.kpos.push_back(i - fr);
+    f.has_kpos |= fr != 0;
     f.slot.push_back(slot_of(rb.bt, i));
     f.seq.push_back(seq);
     f.head_map.push_back(-1);
@@ -1927,7 +1936,8 @@ static void append_request(pic_engine* e, const pic_link_params* pr, ReqBuild& r
       if (in_sel[i] || rb.shared[i / 16] >= 0) continue;  // recomputed, or linked by reference (f3)
       f.k2_src.push_back(slot_of(ch.blocks, j));
       f.k2_dst.push_back(slot_of(rb.bt, i));
-      f.k2_delta.push_back(p.chunk_delta[c]);
+      // a chunk-frame block (kv_share 3) keeps the copied keys at their compile positions
+      f.k2_delta.push_back(frames && rb.bdelta[i / 16] != 0 ? 0 : p.chunk_delta[c]);
       const bool vref = !rb.vshared.empty() && rb.vshared[i / 16] >= 0;  // kv_share 2: V stays in the store
       f.k2_vcopy.push_back(vref ? 0 : 1);
       f.k2_konly |= vref;

@@ -70,6 +70,9 @@ struct Fwd {
   std::vector<int32_t> seq_bt_off, bt;        // block tables (concatenated)
   std::vector<int32_t> bdelta;                // per bt entry: Δ still to apply to a shared block's keys (f3)
   bool kv_rot = false;                        // some bdelta != 0: attention re-bases K tiles on load
+  std::vector<int32_t> kpos;                  // per row: RoPE position of its K heads (kv_share 3 chunk frames)
+  bool has_kpos = false;
+  bool attn_qrot = false;                     // attention re-bases by rotating Q per uniform-frame K tile
   std::vector<int32_t> vbt;                   // per bt entry: V's block (kv_share 2: the chunk-store block)
   bool has_vbt = false;                       // some vbt entry differs from bt
   std::vector<int32_t> k2_src, k2_dst, k2_delta;  // a2 work: cached rows gathered into linked blocks

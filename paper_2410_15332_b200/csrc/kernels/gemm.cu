@@ -205,8 +205,7 @@ PIC_DEV void gemm_epilogue(uint8_t* smem, bool last, void* __restrict__ out_, in
         const bool ok = row < M;
         const float rs = norm_scale(ep, row, M);  // fused RMSNorm row scale (1 if the input was normalised)
         const int p = ok ? ep.pos[row] : 0, sl = ok ? ep.slot[row] : 0;
-        const float* cp = ep.cos_t + (size_t)p * 64;
-        const float* spn = ep.sin_t + (size_t)p * 64;
+        const int pk_ = ok && ep.kpos ? ep.kpos[row] : p;  // K heads: chunk-frame position (kv_share 3)
         const size_t kv_base = ((size_t)(sl / 16) * ep.Hkv) * 16 * 128 + (size_t)(sl % 16) * 128;
 #pragma unroll 1
         for (int hh = 0; hh < BN / 128; ++hh) {
@@ -214,6 +213,9 @@ PIC_DEV void gemm_epilogue(uint8_t* smem, bool last, void* __restrict__ out_, in
           if (hd >= ep.Hq + 2 * ep.Hkv) break;
           const uint32_t th = tl + hh * 128;
           if (hd < ep.Hq + ep.Hkv) {
+            const int pr = hd < ep.Hq ? p : pk_;
+            const float* cp = ep.cos_t + (size_t)pr * 64;
+            const float* spn = ep.sin_t + (size_t)pr * 64;
             uint16_t* dst = hd < ep.Hq ? reinterpret_cast<uint16_t*>(ep.Q) + ((size_t)row * ep.Hq + hd) * 128
                                        : reinterpret_cast<uint16_t*>(ep.Kl) + kv_base + (size_t)(hd - ep.Hq) * 16 * 128;
 #pragma unroll 1

@@ -65,7 +65,8 @@ cudaError_t launch_residual_rmsnorm(float* h, const float* P, int splits, const 
 cudaError_t launch_qkv_rope_scatter(const float* P, int splits, int P_rows, const int32_t* src_row,
                                     const int32_t* pos, const int32_t* slot, const float* cos_t, const float* sin_t,
                                     void* Q, void* Kpool_l, void* Vpool_l, int M, int Hq, int Hkv, int D,
-                                    cudaStream_t st, int f32 = 0, int static_plan = 0);  // 1: pos/slot host-uploaded
+                                    cudaStream_t st, int f32 = 0, int static_plan = 0,  // 1: pos/slot host-uploaded
+                                    const int32_t* kpos = nullptr);  // K heads' RoPE positions (null: pos)
 
 // ---- a8 epilogue: u = bf16(silu(Σ gate) ⊙ Σ up) ----------------------------------------------
 cudaError_t launch_swiglu(const float* P, int splits, void* u, int M, int F, cudaStream_t st, int f32 = 0);
@@ -111,6 +112,8 @@ struct GemmEpi {
   const float* ssq_in;
   int ssq_in_n;
   float inv_d, eps;
+  // EPI_QKV: per row, the RoPE position of its K heads (null: pos) — chunk-frame blocks (kv_share 3)
+  const int32_t* kpos;
   int raster_gm;  // m-tiles per raster group (0: the launcher chooses; see gemm.cu decode)
 };
 constexpr int kSsqStride = 32;  // max n-tiles per row of a fused-norm residual GEMM

@@ -356,7 +356,7 @@ __global__ void __launch_bounds__(128) qkv_rope_scatter_kernel(
     const float* __restrict__ P, int splits, int P_rows, const int32_t* __restrict__ src_row,
     const int32_t* __restrict__ pos, const int32_t* __restrict__ slot, const float* __restrict__ cos_t,
     const float* __restrict__ sin_t, void* __restrict__ Q, void* __restrict__ Kp, void* __restrict__ Vp, int Hq,
-    int Hkv, int D, int static_plan) {
+    int Hkv, int D, int static_plan, const int32_t* __restrict__ kpos) {
   griddep_launch();
   const int r = blockIdx.x;
   const int t = blockIdx.y * blockDim.x + threadIdx.x;
@@ -374,7 +374,8 @@ __global__ void __launch_bounds__(128) qkv_rope_scatter_kernel(
   auto fetch_plan = [&]() {
     sl = slot[r];
     if (t < n_rope) {
-      p = pos[r];
+      // K heads of a row in a chunk-frame block are rotated at the row's compile position (kpos)
+      p = (kpos && t >= Hq * q8) ? kpos[r] : pos[r];
       c = *reinterpret_cast<const float4*>(cos_t + (size_t)p * half + j);
       s = *reinterpret_cast<const float4*>(sin_t + (size_t)p * half + j);
     }
@@ -412,16 +413,16 @@ __global__ void __launch_bounds__(128) qkv_rope_scatter_kernel(
 cudaError_t launch_qkv_rope_scatter(const float* P, int splits, int P_rows, const int32_t* src_row, const int32_t* pos,
                                     const int32_t* slot, const float* cos_t, const float* sin_t, void* Q,
                                     void* Kpool_l, void* Vpool_l, int M, int Hq, int Hkv, int D, cudaStream_t st,
-                                    int f32, int static_plan) {
+                                    int f32, int static_plan, const int32_t* kpos) {
   if (M == 0) return cudaSuccess;
   const int threads = (Hq + Hkv) * (D / 8) + Hkv * (D / 4);
   dim3 grid(M, (threads + 127) / 128);
   if (f32)
     CUDA_TRY_LAUNCH(launch_k(qkv_rope_scatter_kernel<true>, dim3(grid), dim3(128), 0, st, P, splits, P_rows, src_row,
-                             pos, slot, cos_t, sin_t, Q, Kpool_l, Vpool_l, Hq, Hkv, D, static_plan));
+                             pos, slot, cos_t, sin_t, Q, Kpool_l, Vpool_l, Hq, Hkv, D, static_plan, kpos));
   else
     CUDA_TRY_LAUNCH(launch_k(qkv_rope_scatter_kernel<false>, dim3(grid), dim3(128), 0, st, P, splits, P_rows, src_row,
-                             pos, slot, cos_t, sin_t, Q, Kpool_l, Vpool_l, Hq, Hkv, D, static_plan));
+                             pos, slot, cos_t, sin_t, Q, Kpool_l, Vpool_l, Hq, Hkv, D, static_plan, kpos));
   return cudaGetLastError();
 }
 

@@ -143,6 +143,35 @@ def test_vshare_decode_bit_identical(setup):
             s.eng.release(h)
 
 
+@pytest.mark.parametrize("alg", ["naive", "legolink:4", "legolink:16"])
+def test_chunkframe_link_matches_oracle(setup, alg):
+    """kv_share 3: every block inside an aligned cached chunk keeps the chunk's compile frame (recomputed
+    rows' keys are RoPE'd at their compile positions, a2 copies unselected rows without re-base) and the
+    attention applies R(Δ) per block — or, when every K tile has one frame, rotates the queries by −Δ
+    instead.  Not bit-identical to the copy path (one more bf16 rounding of the rotated operand): held to
+    the oracle at the north star's 2e-2, and its linked K/V exports (re-based to the linked positions on
+    export) to the copy path's within bf16 rounding."""
+    s = setup
+    store = P.Store(M.Weights(s.cfg))
+    oids = store.compile(s.w.chunks)
+    for segs in [s.w.requests[0]] + sg.permuted_requests(s.w, 3):
+        ref = P.link(store, [("cached", oids[x.chunk]) if x.cached else ("tokens", x.tokens) for x in segs], alg)
+        copy, cf = link_both(s, segs, alg, modes=(0, 3))
+        try:
+            assert rel(cf[0].logits, ref.logits) < 2e-2
+            assert rel(cf[0].logits, copy[0].logits) < 2e-2
+            for l in range(s.cfg.n_layers):
+                (kc, vc), (kf, vf) = copy[1][l], cf[1][l]
+                if l == 0:                                   # before any attention: V identical
+                    assert np.array_equal(vc, vf)
+                assert rel(B.bf16_bits_to_f32(vf), B.bf16_bits_to_f32(vc)) < 2e-2, l
+                assert rel(B.bf16_bits_to_f32(kf), B.bf16_bits_to_f32(kc)) < 2e-2, l
+                assert rel(B.bf16_bits_to_f32(kf), ref.K[l]) < 2e-2, l
+        finally:
+            s.eng.release(copy[0].linked)
+            s.eng.release(cf[0].linked)
+
+
 def test_shared_link_matches_oracle(setup):
     s = setup
     store = P.Store(M.Weights(s.cfg))
