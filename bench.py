@@ -327,10 +327,11 @@ def main():
                     help="tensor parallel over all ranks (default for cfg5 at N > 1): heads/MLP columns sharded, "
                          "fused peer-memory all-reduce; one request split over the ranks")
     ap.add_argument("--layers", type=int, default=None, help="truncate depth (functional runs only; marked in config)")
-    ap.add_argument("--kv-share", type=int, default=1, choices=[0, 1, 2],
+    ap.add_argument("--kv-share", type=int, default=3, choices=[0, 1, 2, 3],
                     help="0: copy path (a2 copies K+V); 1: f3 shared-block link (chunk-store blocks linked by "
                          "reference, keys re-based in the attention K-tile load); 2: V by reference, keys "
-                         "re-based by a2 into fresh blocks (pic_link_params.kv_share)")
+                         "re-based by a2 into fresh blocks; 3: as 1 with every block of an aligned chunk in the "
+                         "chunk's compile frame, re-based by rotating Q per chunk (pic_link_params.kv_share)")
     ap.add_argument("--decode-steps", type=int, default=16,
                     help="f1: decode steps over the first wave's linked caches after the link measurement (0 = skip)")
     args = ap.parse_args()
@@ -477,7 +478,7 @@ def main():
                     else [eng.link(first[0], w.alg, keep_linked=True)])
             hs = [o.linked for o in held]
             mat_ms = None
-            if args.kv_share == 1:
+            if args.kv_share in (1, 3):
                 # shared-block links: re-base the shared blocks into owned ones once (pic_linked_materialize)
                 torch.cuda.synchronize(dev)
                 m0, m1 = mk(), mk()

@@ -115,8 +115,18 @@ typedef struct {
                                 block (reference counted, read through a separate V block table) while their
                                 keys are re-based by a2 into fresh blocks, so the attention reads K without
                                 re-basing it; results are again bit-identical to kv_share = 0 (a2's keys, the
-                                store's values).  Ignored for CacheBlend (its layer 0 rewrites every row).
-                                Default 0 */
+                                store's values).
+                                3 = chunk-frame link: the kv_share 1 blocks are linked by reference and, in
+                                addition, every other block inside a 16-aligned cached chunk (those holding
+                                recomputed rows) keeps the chunk's compile frame: a2 copies its unselected
+                                keys without rotation and a5 ropes its recomputed keys at position i − Δ_c,
+                                so all of the chunk's keys sit at compile positions and carry Δ_c.  The
+                                attention uses q·R(Δ)k = (R(−Δ)q)·k: when every 128-key tile lies in one
+                                frame it re-bases Q once per frame (in TMEM) and feeds S = (R(−Δ)Q)·Kᵀ from
+                                TMEM, else it re-bases the K tile as kv_share 1 does.  Equal to kv_share 0
+                                within rounding (not bit-identical: the rotation moves from K to Q); exports
+                                re-base keys to linked positions like kv_share 1.  bench.py's default.
+                                Ignored for CacheBlend (its layer 0 rewrites every row).  Default 0 */
 } pic_link_params;
 
 /* Per-request result of a link. */
@@ -211,7 +221,8 @@ typedef struct {
   int32_t n_tokens, n_sel, n_chunks, n_blocks;
   int32_t *sel, *tok, *src, *chunks, *block_table, *slot;
   int32_t* block_delta;      /* [cap] (nullable): per linked block, the Δ the attention applies to a shared
-                                chunk-store block's keys (kv_share = 1), else 0 */
+                                chunk-store block's keys (kv_share = 1), or the chunk frame of any block of an aligned
+                                cached chunk (kv_share = 3), else 0 */
   int32_t n_shared;          /* out: blocks linked by reference (kv_share = 1); n_blocks - n_shared are fresh */
 } pic_plan_out;
 pic_status pic_plan(pic_engine* eng, const pic_segment* segs, int32_t n_segs, const pic_link_params* params,
@@ -225,8 +236,9 @@ pic_status pic_linked_export(pic_engine* eng, const pic_linked* linked, int32_t 
 /* Number of tokens N and the block table (int32[ceil(N/16)], nullable) of a linked cache. */
 pic_status pic_linked_info(pic_engine* eng, const pic_linked* linked, int32_t* n_tokens, int32_t* block_table);
 /* Shared-block link (kv_share): number of blocks of `linked` that are chunk-store blocks
- * linked by reference (kv_share 1: K and V; kv_share 2: V only), and per block (int32[ceil(N/16)],
- * nullable) the Δ the attention applies to its keys (0 for blocks the link owns and for kv_share 2).
+ * linked by reference (kv_share 1 and 3: K and V; kv_share 2: V only), and per block (int32[ceil(N/16)],
+ * nullable) the Δ the attention applies to its keys (0 for blocks the link owns and for kv_share 2;
+ * kv_share 3: the chunk frame of every block of an aligned cached chunk).
  * Host-only bookkeeping. */
 pic_status pic_linked_sharing(pic_engine* eng, const pic_linked* linked, int32_t* n_shared, int32_t* block_delta);
 /* Re-base the shared chunk-store blocks (Δ != 0) of a kv_share linked cache into blocks it owns, on

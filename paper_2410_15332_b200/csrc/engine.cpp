@@ -99,7 +99,7 @@ static int g_attn_trace_ctas = 0;
 static unsigned long long* attn_trace_buffer() {
   static unsigned long long* buf = nullptr;
   static const bool on = getenv("PIC_ATTN_TRACE") != nullptr;
-  if (on && !buf && cudaMalloc(&buf, 16 * 8192 * sizeof(unsigned long long)) != cudaSuccess) buf = nullptr;
+  if (on && !buf && cudaMalloc(&buf, 32 * 8192 * sizeof(unsigned long long)) != cudaSuccess) buf = nullptr;
   return on ? buf : nullptr;
 }
 // ping-pong kernel (attention_pp.cu): per-CTA cycle accounting, 32 counters per CTA
@@ -133,46 +133,76 @@ static void attn_trace_print(int n_cta) {
   }
   unsigned long long* buf = attn_trace_buffer();
   if (!buf || n_cta <= 0) return;
-  std::vector<unsigned long long> t((size_t)16 * n_cta);
+  std::vector<unsigned long long> t((size_t)32 * n_cta);
   if (cudaMemcpy(t.data(), buf, t.size() * 8, cudaMemcpyDeviceToHost) != cudaSuccess) return;
   unsigned long long t0 = ~0ull;
-  for (int c = 0; c < n_cta; ++c) t0 = std::min(t0, t[16 * c]);
+  for (int c = 0; c < n_cta; ++c) t0 = std::min(t0, t[32 * c]);
   static const char* nm[8] = {"entry", "wait_done", "q_full", "first_S", "last_P", "last_O", "epi_done", "exit"};
   {
     std::vector<int> nt;
-    for (int c = 0; c < n_cta; ++c) nt.push_back((int)t[16 * c + 7]);
+    for (int c = 0; c < n_cta; ++c) nt.push_back((int)t[32 * c + 7]);
     std::sort(nt.begin(), nt.end());
     fprintf(stderr, "  attn kv tiles per CTA: min %d med %d max %d\n", nt[0], nt[nt.size() / 2], nt.back());
   }
   {
-    static const char* an[6] = {"wait S", "max+xchg", "exp+P", "mma wK", "mma wP", "mma wV"};
-    for (int k = 0; k < 6; ++k) {
+    static const char* an[7] = {"wait S", "max+xchg", "exp+P", "mma wK", "mma wP", "mma wV", "mma wQd"};
+    for (int k = 0; k < 7; ++k) {
       std::vector<double> v;
       for (int c = 0; c < n_cta; ++c)
-        if (t[16 * c + 7] > 0) v.push_back((double)t[16 * c + 8 + k] / 1e3 / (double)t[16 * c + 7]);
+        if (t[32 * c + 7] > 0) v.push_back((double)t[32 * c + 8 + k] / 1e3 / (double)t[32 * c + 7]);
       if (v.empty()) continue;
       std::sort(v.begin(), v.end());
       fprintf(stderr, "  attn per-tile %-9s min %6.3f med %6.3f max %6.3f us\n", an[k], v[0], v[v.size() / 2], v.back());
     }
   }
   {
-    std::vector<double> a, b;  // softmax warp 64: Q global loads after the PDL wait, then the TMEM store
-    for (int c = 0; c < n_cta; ++c)
-      if (t[16 * c + 14] > t[16 * c + 1] && t[16 * c + 1] > 0) {
-        a.push_back((double)(t[16 * c + 14] - t[16 * c + 1]) / 1e3);
-        b.push_back((double)(t[16 * c + 15] - t[16 * c + 14]) / 1e3);
-      }
-    if (!a.empty()) {
-      std::sort(a.begin(), a.end());
-      std::sort(b.begin(), b.end());
-      fprintf(stderr, "  attn Q load   min %6.3f med %6.3f max %6.3f us; TMEM store min %6.3f med %6.3f max %6.3f us\n",
-              a[0], a[a.size() / 2], a.back(), b[0], b[b.size() / 2], b.back());
+    long fr = 0;  // QROT: chunk frames per CTA (one R(-Δ)·Q rotation each)
+    for (int c = 0; c < n_cta; ++c) fr += (long)t[32 * c + 15];
+    if (fr) fprintf(stderr, "  attn QROT frames per CTA: mean %.2f\n", (double)fr / n_cta);
+    static const char* pn[7] = {"S load", "max", "xchg", "rescale", "exp", "P store", "o_full+arrive"};
+    double ph[7] = {0, 0, 0, 0, 0, 0, 0}, nt = 0;
+    for (int c = 0; c < n_cta; ++c) {
+      nt += (double)t[32 * c + 7];
+      for (int k = 0; k < 7; ++k) ph[k] += (double)t[32 * c + 16 + k];
     }
+    if (nt > 0) {
+      fprintf(stderr, "  attn softmax cycles per tile (warp 2):");
+      for (int k = 0; k < 7; ++k) fprintf(stderr, " %s %.0f", pn[k], ph[k] / nt);
+      fprintf(stderr, "\n");
+    }
+    double ml = 0, mn = 0;
+    for (int c = 0; c < n_cta; ++c) {
+      ml += (double)t[32 * c + 23];
+      mn += (double)t[32 * c + 24];
+    }
+    if (mn > 0) fprintf(stderr, "  attn P(t-1) arrive -> S(t+1) ready: %.0f cycles (PV + S = 16 MMAs)\n", ml / mn);
+    double sw = 0, sr = 0, sa = 0;
+    for (int c = 0; c < n_cta; ++c) {
+      sw += (double)t[32 * c + 25];
+      sr += (double)t[32 * c + 26];
+      sa += (double)t[32 * c + 27];
+    }
+    if (mn > 0)
+      fprintf(stderr, "  attn   = warp-2 arrive -> MMA warp sees P %.0f + MMA warp sees P -> S(t+1) ready %.0f cycles\n",
+              (sw - sa) / mn, (sr - sw) / mn);
+    // CTA span (entry -> exit) and its parts, summed over CTAs, per KV tile
+    double sp = 0, pro = 0, epi = 0, tiles = 0;
+    for (int c = 0; c < n_cta; ++c) {
+      const unsigned long long* x = &t[32 * c];
+      if (!x[7] || x[3] < x[0] || x[6] < x[3] || x[7] < x[0]) continue;
+      sp += (double)(x[6] - x[0]);
+      pro += (double)(x[3] - x[0]);
+      epi += (double)(x[6] - x[5]);
+      tiles += (double)x[7];
+    }
+    if (tiles > 0)
+      fprintf(stderr, "  attn per KV tile (sum over CTAs): entry->epi_done %.3f us = prologue %.3f + loop %.3f + epilogue %.3f\n",
+              sp / tiles / 1e3, pro / tiles / 1e3, (sp - pro - epi) / tiles / 1e3, epi / tiles / 1e3);
   }
   for (int k = 0; k < 7; ++k) {
     std::vector<double> v;
     for (int c = 0; c < n_cta; ++c)
-      if (t[16 * c + k] >= t0) v.push_back((double)(t[16 * c + k] - t0) / 1e3);
+      if (t[32 * c + k] >= t0) v.push_back((double)(t[32 * c + k] - t0) / 1e3);
     if (v.empty()) continue;
     std::sort(v.begin(), v.end());
     fprintf(stderr, "  attn %-9s min %7.2f  med %7.2f  max %7.2f us (n=%zu)\n", nm[k], v[0], v[v.size() / 2], v.back(),
@@ -1416,15 +1446,17 @@ static pic_status enqueue_forward(pic_engine* e, const Fwd& f, const DevPlan& dp
       a.num_blocks = (int)e->lim.num_blocks;
       a.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)D));
       a.trace = attn_trace_buffer();
+      if (a.trace && !f.attn_pp && (size_t)a.n_work * Hkv > 8192) a.trace = nullptr;  // 32 slots x 8192 CTAs
       a.static_plan = (tiles == dp.tiles) ? 1 : 0;  // CacheBlend's post-selection tiles/positions are device-side
       a.kpool = nullptr;  // L2 prefetch of K/V pages: measured slower (TMA unit busy ahead of the real loads)
       a.vpool = e->Vpool;
       a.bdelta = dp.bdelta;
       a.vbt = dp.vbt;
+      a.qrot = f.attn_qrot && tiles == dp.tiles ? 1 : 0;
       a.cos_t = e->cos_t;
       a.sin_t = e->sin_t;
       a.Q = e->Q;
-      g_attn_trace_ctas = f.attn_pp ? std::min(a.n_work * Hkv, 148) : a.n_work * Hkv;
+      g_attn_trace_ctas = !a.trace ? 0 : f.attn_pp ? std::min(a.n_work * Hkv, 148) : a.n_work * Hkv;
       g_attn_trace_pp = f.attn_pp;
       a.o_part = e->o_part;
       a.ml_part = e->ml_part;
@@ -1600,6 +1632,16 @@ static void schedule_attention(pic_engine* e, Fwd& f) {
   // the one-lane kernel's finer split-KV); shared-block links (K tiles re-based in smem) stay on the
   // one-lane kernel, whose four rotation warps keep up where the ping-pong kernel's two do not (cfg4:
   // 310 vs 200 ms per step).  pic_test_set_attention_kernel(1|2) forces one (tests and A/B only).
+  // kv_share 3 links whose every 128-key tile carries one block delta: Q-side re-base in the one-lane kernel
+  f.attn_qrot = false;
+  if (f.kv_rot && f.qrot_ok && !e->f32 && e->cfg.head_dim == 128 && !getenv("PIC_NO_QROT")) {
+    bool uniform = true;
+    for (size_t q = 0; q < f.seq_bt_off.size() && uniform; ++q) {
+      const size_t b0 = f.seq_bt_off[q], b1 = q + 1 < f.seq_bt_off.size() ? f.seq_bt_off[q + 1] : f.bt.size();
+      for (size_t b = b0; b < b1 && uniform; ++b) uniform = f.bdelta[b] == f.bdelta[b0 + (b - b0) / 8 * 8];
+    }
+    f.attn_qrot = uniform;
+  }
   static const bool pp_rot = getenv("PIC_ATTN_PP_ROT") != nullptr;  // A/B: ping-pong also for shared-block links
   bool pp = attn_pp_enabled() && e->cfg.head_dim == 128 && !e->f32 && (!f.kv_rot || pp_rot);
   if (pp) {
@@ -1612,6 +1654,7 @@ static void schedule_attention(pic_engine* e, Fwd& f) {
     pp = work * Hkv >= 148L * 16;
   }
   if (g_attn_force) pp = g_attn_force == 2 && e->cfg.head_dim == 128 && !e->f32;
+  if (f.attn_qrot) pp = false;  // the Q-side re-base lives in the one-lane kernel
   f.attn_pp = pp;
   build(f.tiles, &f.pos, f.M, 0, f.attn_work, f.attn_nsplit, f.attn_n_work, f.attn_max_split);
   if (f.cb) {
@@ -1913,6 +1956,7 @@ static void append_request(pic_engine* e, const pic_link_params* pr, ReqBuild& r
   const int r0 = f.M;
   add_tiles(f.tiles, seq, r0, (int)rows->size(), qpt);
   const bool frames = pr->kv_share == 3 && !cb;  // chunk-frame blocks: K stored at compile positions
+  f.qrot_ok = frames;
   for (int32_t i : *rows) {
     f.tok.push_back(p.tok[i]);
     f.pos.push_back(i);  // p_i = i (R18)
@@ -2123,6 +2167,8 @@ static pic_status link_impl(pic_engine* e, int32_t n_req, const pic_segment* con
       h->blocks = reqs[r].bt;
       h->bdelta = reqs[r].bdelta;
       h->n_shared = (int32_t)reqs[r].bt.size() - reqs[r].n_fresh;
+      h->byref.assign(h->blocks.size(), 0);
+      for (size_t b = 0; b < h->blocks.size() && b < reqs[r].shared.size(); ++b) h->byref[b] = reqs[r].shared[b] >= 0;
       h->n_vshared = 0;
       for (int32_t b : reqs[r].vshared) h->n_vshared += b >= 0;
       if (h->n_vshared) {
@@ -2167,6 +2213,7 @@ extern "C" pic_status pic_decode(pic_engine* e, pic_linked* const* linked, const
       grown[b] = e->alloc.alloc(1)[0];
       linked[b]->blocks.push_back(grown[b]);
       linked[b]->bdelta.push_back(0);
+      linked[b]->byref.push_back(0);
       if (!linked[b]->vblocks.empty()) linked[b]->vblocks.push_back(grown[b]);
     }
   auto rollback = [&]() {
@@ -2174,6 +2221,7 @@ extern "C" pic_status pic_decode(pic_engine* e, pic_linked* const* linked, const
       if (grown[b] >= 0) {
         linked[b]->blocks.pop_back();
         linked[b]->bdelta.pop_back();
+        linked[b]->byref.pop_back();
         if (!linked[b]->vblocks.empty()) linked[b]->vblocks.pop_back();
         e->alloc.release({grown[b]});
       }
@@ -2393,14 +2441,19 @@ extern "C" pic_status pic_linked_materialize(pic_engine* e, pic_linked* h, void*
                                         e->cos_t, e->sin_t, 1, st, e->f32);
   if (ce != cudaSuccess) return undo(ce, "kv_link");
   // the chunk-store blocks lose this reference; later work on `stream` is ordered after the copy
+  // (kv_share 3: owned chunk-frame blocks are re-based the same way and freed)
   std::vector<int32_t> old;
   for (size_t k = 0; k < idx.size(); ++k) {
-    old.push_back(h->blocks[idx[k]]);
-    h->blocks[idx[k]] = fresh[k];
-    h->bdelta[idx[k]] = 0;
+    const int b = idx[k];
+    old.push_back(h->blocks[b]);
+    h->blocks[b] = fresh[k];
+    h->bdelta[b] = 0;
+    if (b < (int)h->byref.size() && h->byref[b]) {
+      h->byref[b] = 0;
+      --h->n_shared;
+    }
   }
   e->alloc.release(old);
-  h->n_shared -= (int32_t)idx.size();
   return PIC_OK;
 }
 

@@ -73,6 +73,7 @@ struct Fwd {
   std::vector<int32_t> kpos;                  // per row: RoPE position of its K heads (kv_share 3 chunk frames)
   bool has_kpos = false;
   bool attn_qrot = false;                     // attention re-bases by rotating Q per uniform-frame K tile
+  bool qrot_ok = false;                       // kv_share 3 link: the Q-side re-base may apply
   std::vector<int32_t> vbt;                   // per bt entry: V's block (kv_share 2: the chunk-store block)
   bool has_vbt = false;                       // some vbt entry differs from bt
   std::vector<int32_t> k2_src, k2_dst, k2_delta;  // a2 work: cached rows gathered into linked blocks
@@ -121,7 +122,9 @@ struct LinkPlanHost {
 struct pic_linked {
   int32_t n_tokens = 0;
   std::vector<int32_t> blocks;
-  std::vector<int32_t> bdelta;  // per block: Δ of a chunk-store block linked by reference (f3), else 0
+  std::vector<int32_t> bdelta;  // per block: Δ of a chunk-store block linked by reference (f3), or of an owned
+                                // block kept in its chunk's compile frame (kv_share 3), else 0
+  std::vector<uint8_t> byref;   // per block: 1 = blocks[b] is a chunk-store block linked by reference
   int32_t n_shared = 0;         // blocks linked by reference
   // kv_share 2: per block, the block holding its V rows — the chunk-store block (referenced, V by reference)
   // or blocks[b]; empty = blocks

@@ -42,12 +42,13 @@ constexpr int kV = kK + kStages * 2 * kTile;  // V stages
 constexpr int kQ = kV + kStages * 2 * kTile;  // Q tile (2 halves), TMA-staged (A operand of S = Q·Kᵀ)
 constexpr int kX = kQ + 2 * kTile;            // softmax pair exchange: [2 parity][2 halves][128] fp32
 constexpr int kBar = kX + 2 * 2 * 128 * 4;    // barriers
-constexpr int kNumBars = 1 + 5 * kStages + 6;  // + k_rot ring (shared-block link)
+constexpr int kNumBars = 1 + 5 * kStages + 6 + 4;  // + k_rot ring (shared-block link), qd_full/qd_empty (QROT)
 constexpr int kSmem = kBar + kNumBars * 8 + 16;
 static_assert(kSmem <= 232448, "attention smem over the 227 KB limit");
 // TMEM columns (512 allocated)
 constexpr uint32_t kTmS = 0;    // S double buffer [0, 256); P(t) (bf16 pairs) overwrites S(t): half hc at +64·hc
 constexpr uint32_t kTmO = 256;  // O accumulator [256, 384)
+constexpr uint32_t kTmQd = 384;  // QROT: two R(−Δ)·Q buffers (bf16 pairs, 64 columns each) [384, 512)
 }  // namespace attn
 
 // Q is TMA-staged into shared memory once per CTA (the A operand of S = Q·Kᵀ); P is the TMEM A operand
@@ -56,7 +57,13 @@ constexpr uint32_t kTmO = 256;  // O accumulator [256, 384)
 // 32 layers): 4 warps 26.3 ms, 2 warps 41.5 ms (the rotation is issue-bound and sits between the K TMA
 // and the S MMA); 4 warps cap the CTA at 128 registers per thread (14 warps), a few bytes of spill.
 constexpr int kRotWarps = 4;
-template <int G, bool ROT>
+#ifndef PIC_V1_POLY8
+#define PIC_V1_POLY8 1  // pairs of every 8 whose exponential runs on the FMA-pipe polynomial (exp2_poly2)
+#endif
+// QROT (kv_share 3 links whose every K tile holds one chunk frame): instead of rotating K tiles in smem,
+// the rotation warps write R(−Δ)·Q for each frame into TMEM and S = Q_Δ·Kᵀ runs as a TS MMA
+// (q·R(Δ)k = (R(−Δ)q)·k) — one rotation of the 128-row Q tile per chunk instead of one per K tile.
+template <int G, bool ROT, bool QROT = false>
 __global__ void __launch_bounds__(ROT ? 320 + 32 * kRotWarps : 320, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                    const __grid_constant__ CUtensorMap tmV,
@@ -64,7 +71,7 @@ __global__ void __launch_bounds__(ROT ? 320 + 32 * kRotWarps : 320, 1)
   griddep_launch();
   using namespace attn;
   constexpr int S = kStages;
-  unsigned long long* const tr = a.trace ? a.trace + 16 * (blockIdx.y * gridDim.x + blockIdx.x) : nullptr;
+  unsigned long long* const tr = a.trace ? a.trace + 32 * (blockIdx.y * gridDim.x + blockIdx.x) : nullptr;
   if (tr && threadIdx.x == 0) tr[0] = globaltimer();
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw;
@@ -78,6 +85,7 @@ __global__ void __launch_bounds__(ROT ? 320 + 32 * kRotWarps : 320, 1)
   const uint32_t s_full = smem_u32(bars + 1 + 4 * S), p_full = smem_u32(bars + 3 + 4 * S);
   const uint32_t o_full = smem_u32(bars + 5 + 4 * S);
   const uint32_t k_rot = smem_u32(bars + 7 + 4 * S);  // ROT: K tile re-based in smem (4 rotation warps)
+  const uint32_t qd_full = smem_u32(bars + 7 + 5 * S), qd_empty = smem_u32(bars + 9 + 5 * S);  // QROT
 
   const int warp = warp_id(), lane = lane_id();
   // barriers and TMEM do not depend on upstream data: set them up while the previous kernel drains
@@ -89,6 +97,10 @@ __global__ void __launch_bounds__(ROT ? 320 + 32 * kRotWarps : 320, 1)
       mbar_init(v_full + 8 * s, 1);
       mbar_init(v_empty + 8 * s, 1);
       mbar_init(k_rot + 8 * s, kRotWarps);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(qd_full + 8 * b, kRotWarps);
+      mbar_init(qd_empty + 8 * b, 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(s_full + 8 * b, 1);
@@ -208,7 +220,7 @@ __global__ void __launch_bounds__(ROT ? 320 + 32 * kRotWarps : 320, 1)
       constexpr uint32_t idO = idesc_bf16(128, 128, 0, 1);  // P (TMEM, K-major) x V (smem, MN-major)
       const uint64_t dQ = sdesc_sw128(base + kQ, 16, 1024), dK0 = sdesc_sw128(base + kK, 16, 1024);
       const uint64_t dV0 = sdesc_sw128(base + kV, kTile, 1024);
-      unsigned long long w_k = 0, w_p = 0, w_v = 0, q0 = 0;
+      unsigned long long w_k = 0, w_p = 0, w_v = 0, w_q = 0, q0 = 0, sum_w = 0;
       mbar_wait(q_full, 0);
       tc_fence_after();
       if (tr && lane == 0) tr[2] = globaltimer();
@@ -217,6 +229,9 @@ __global__ void __launch_bounds__(ROT ? 320 + 32 * kRotWarps : 320, 1)
         if (tr) q0 = globaltimer();
         mbar_wait(p_full + 8 * pb, (u >> 1) & 1);
         if (tr) {
+#ifdef PIC_ATTN_PHASES
+          if (u <= n - 3) sum_w += clock64();  // P(u) seen by the MMA warp (paired with S(u+2) ready)
+#endif
           const unsigned long long q1 = globaltimer();
           w_p += q1 - q0;
           q0 = q1;
@@ -225,31 +240,65 @@ __global__ void __launch_bounds__(ROT ? 320 + 32 * kRotWarps : 320, 1)
         if (tr) w_v += globaltimer() - q0;
         tc_fence_after();
         const uint64_t dv = dV0 + (uint64_t)(vs * (2 * kTile / 16));
+        // keys 16kk..16kk+15: P half kk/4 at S-buffer column 64·(kk/4) + 8·(kk%4); O accumulates in TMEM
+        // across KV tiles (rescaled by the softmax warps when needed).  One elect.sync for the 8 MMAs: the
+        // tensor pipe idles until P(u) lands, so issue latency adds straight to the softmax's wait for S.
+#ifdef PIC_ATTN_PER_MMA_ISSUE  // A/B builds only: one elect.sync + 64-bit descriptor arithmetic per MMA
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-          // keys 16kk..16kk+15: P half kk/4 at S-buffer column 64·(kk/4), 8 columns per 16 keys
-          const uint32_t pa = tmem + kTmS + pb * 128 + (kk >> 2) * 64 + (kk & 3) * 8;
-          // O accumulates in TMEM across KV tiles (rescaled by the softmax warps when needed)
-          umma_bf16_ts_e(tmem + kTmO, pa, dv + (uint64_t)(kk * 2048 / 16), idO, (u | kk) != 0);
-        }
+        for (int kk = 0; kk < 8; ++kk)
+          umma_bf16_ts_e(tmem + kTmO, tmem + kTmS + pb * 128 + (kk >> 2) * 64 + (kk & 3) * 8,
+                         dv + (uint64_t)(kk * 2048 / 16), idO, (u | kk) != 0);
+#else
+        umma_ts_k128(tmem + kTmO, tmem + kTmS + pb * 128, dv, idO, u != 0);
+#endif
         umma_commit_e(o_full + 8 * pb);
         umma_commit_e(v_empty + 8 * vs);
       };
+      // QROT: the frame (Δ) of each K tile (uniform over its 8 blocks, host-checked) and the R(−Δ)·Q buffer
+      const int* bdq = QROT ? a.bdelta + a.seq_bt_off[seq] : nullptr;
+      int fi = -1, fr_cur = 0;
+      int fr_next = QROT ? bdq[min(j0 * 8, last_blk)] : 0;
       for (int t = 0; t < n; ++t) {
         const int sb = t & 1, ks = t % S;
+        int qb = 0;
+        bool frame_end = false;
+        if constexpr (QROT) {
+          const int fr = fr_next;
+          fr_next = t + 1 < n ? bdq[min((j0 + t + 1) * 8, last_blk)] : fr;
+          if (t == 0 || fr != fr_cur) {  // a new frame: wait for its rotated Q
+            ++fi;
+            if (tr) q0 = globaltimer();
+            mbar_wait(qd_full + 8 * (fi & 1), (fi >> 1) & 1);
+            if (tr) w_q += globaltimer() - q0;
+          }
+          fr_cur = fr;
+          qb = fi & 1;
+          frame_end = t + 1 == n || fr_next != fr;
+        }
         if (tr) q0 = globaltimer();
-        mbar_wait((ROT ? k_rot : k_full) + 8 * ks, (t / S) & 1);
+        mbar_wait((ROT && !QROT ? k_rot : k_full) + 8 * ks, (t / S) & 1);
         if (tr) w_k += globaltimer() - q0;
         tc_fence_after();
         // S(t) overwrites the buffer holding P(t-2): PV(t-2) was issued before and MMAs run in order
         const uint64_t dk = dK0 + (uint64_t)(ks * (2 * kTile / 16));
+#ifdef PIC_ATTN_PER_MMA_ISSUE
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
           const uint64_t o = (uint64_t)(((kk >> 2) * kTile + (kk & 3) * 32) >> 4);
-          umma_bf16_e(tmem + kTmS + sb * 128, dQ + o, dk + o, idS, kk > 0);
+          if constexpr (QROT)
+            umma_bf16_ts_e(tmem + kTmS + sb * 128, tmem + kTmQd + qb * 64 + kk * 8, dk + o, idS, kk > 0);
+          else
+            umma_bf16_e(tmem + kTmS + sb * 128, dQ + o, dk + o, idS, kk > 0);
         }
+#else
+        if constexpr (QROT)  // A = R(−Δ)·Q from TMEM: dims 16kk..16kk+15 at columns 8kk..8kk+7
+          umma_tsk_k128(tmem + kTmS + sb * 128, tmem + kTmQd + qb * 64, dk, idS, kTile);
+        else
+          umma_ss_k128(tmem + kTmS + sb * 128, dQ, dk, idS, 0, kTile);
+#endif
         umma_commit_e(s_full + 8 * sb);
         umma_commit_e(k_empty + 8 * ks);
+        if (QROT && frame_end) umma_commit_e(qd_empty + 8 * qb);  // this frame's Q buffer may be rewritten
         if (t >= 1) issue_pv(t - 1);
       }
       issue_pv(n - 1);
@@ -257,6 +306,64 @@ __global__ void __launch_bounds__(ROT ? 320 + 32 * kRotWarps : 320, 1)
         tr[11] = w_k;
         tr[12] = w_p;
         tr[13] = w_v;
+        tr[14] = w_q;
+        tr[15] = (unsigned long long)(fi + 1);
+        tr[25] = sum_w;
+      }
+    }
+  } else if (QROT && warp >= 10) {
+    // ------------------------------------------------------------------ Q re-base per chunk frame
+    // Row r of the MMA (query, head) = TMEM lane r = Q smem row r; this warp owns lanes 32·(warp % 4)...
+    // For every frame Δ met along the KV range (in tile order), write R(−Δ)·q (NeoX pairs (j, j+64),
+    // fp32 rotation of the bf16 q, rounded to bf16) into the Q buffer of that frame's parity.
+    if (n > 0) {
+      const int qq = warp & 3;
+      const int r = qq * 32 + lane;
+      const uint32_t lane_addr = (uint32_t)(qq * 32) << 16;
+      const int* bdq = a.bdelta + a.seq_bt_off[seq];
+      mbar_wait(q_full, 0);
+      int fi = -1, fr_cur = 0;
+      for (int t = 0; t < n; ++t) {
+        const int fr = bdq[min((j0 + t) * 8, last_blk)];
+        if (t > 0 && fr == fr_cur) continue;
+        fr_cur = fr;
+        ++fi;
+        mbar_wait(qd_empty + 8 * (fi & 1), ((fi >> 1) & 1) ^ 1);  // the MMAs of frame fi−2 are done
+        const int ad = fr < 0 ? -fr : fr;
+        const float sg = fr < 0 ? 1.f : -1.f;  // R(−Δ): sin(−Δθ) = −sign(Δ)·sin(|Δ|θ)
+        const uint32_t qbase = tmem + lane_addr + kTmQd + (fi & 1) * 64;
+#pragma unroll 1
+        for (int hh = 0; hh < 2; ++hh) {  // dims 32hh..32hh+31 and their partners 64+32hh..
+          uint32_t oa[16], ob[16];
+#pragma unroll
+          for (int cc = 0; cc < 4; ++cc) {
+            const int c = 4 * hh + cc;  // 16-B chunk: dims 8c..8c+7 (half 0) and 64+8c.. (half 1)
+            const uint32_t off = (uint32_t)(r * 128 + ((c ^ (r & 7)) << 4));
+            const uint4 xa = lds128(base + kQ + off), xb = lds128(base + kQ + kTile + off);
+            const float4* cp = reinterpret_cast<const float4*>(a.cos_t + (size_t)ad * 64 + c * 8);
+            const float4* sp = reinterpret_cast<const float4*>(a.sin_t + (size_t)ad * 64 + c * 8);
+            const float4 c0 = cp[0], c1 = cp[1], s0 = sp[0], s1 = sp[1];
+            const float cs[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+            const float sn[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+            const uint32_t a4[4] = {xa.x, xa.y, xa.z, xa.w}, b4[4] = {xb.x, xb.y, xb.z, xb.w};
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const float a0 = __uint_as_float(a4[k] << 16), a1 = __uint_as_float(a4[k] & 0xFFFF0000u);
+              const float b0 = __uint_as_float(b4[k] << 16), b1 = __uint_as_float(b4[k] & 0xFFFF0000u);
+              float ra0, rb0, ra1, rb1;
+              rebase_pair(a0, b0, cs[2 * k], sg * sn[2 * k], ra0, rb0);
+              rebase_pair(a1, b1, cs[2 * k + 1], sg * sn[2 * k + 1], ra1, rb1);
+              oa[cc * 4 + k] = pack_bf16(ra0, ra1);
+              ob[cc * 4 + k] = pack_bf16(rb0, rb1);
+            }
+          }
+          // columns: dims (2k, 2k+1) at column k -> dims 32hh.. at 16hh.., partners at 32 + 16hh..
+          tmem_st16u_wait(qbase + 16 * hh, oa);
+          tmem_st16u_wait(qbase + 32 + 16 * hh, ob);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(qd_full + 8 * (fi & 1));
       }
     }
   } else if (ROT && warp >= 10) {
@@ -361,8 +468,24 @@ __global__ void __launch_bounds__(ROT ? 320 + 32 * kRotWarps : 320, 1)
     // and the common case never touches O (FA4-style lazy rescale; exact because the final
     // normalisation uses m_ref).
     float m_ref = -INFINITY, l = 0.f;
+#ifdef PIC_ATTN_PHASES  // bench-only build: per-phase softmax cycles + MMA latency (costs registers: spills at 128)
     const bool trc = tr && threadIdx.x == 64;
+#else
+    constexpr bool trc = false;
+#endif
     unsigned long long acc_ws = 0, acc_mx = 0, acc_ex = 0, tt0 = 0, tt1 = 0;
+    // finer phases (clock64 cycles, trace slots 16..22): S load, max, pair exchange, rescale, exp loop,
+    // P store + wait::st, o_full wait + arrive
+    unsigned long long ph_[7] = {0, 0, 0, 0, 0, 0, 0}, pc = 0;
+    // P(t-1) arrive -> S(t+1) ready: the tensor pipe's PV(t-1) + S(t+1) (it idles waiting for P(t-1))
+    unsigned long long arr_prev = 0, arr_cur = 0, mma_lat = 0, mma_n = 0, sum_r = 0, sum_a = 0;
+    auto phase = [&](int i) {
+      if (trc) {
+        const unsigned long long c = clock64();
+        ph_[i] += c - pc;
+        pc = c;
+      }
+    };
     for (int t = 0; t < n; ++t) {
       const int sb = t & 1;
       const uint32_t ph = (t >> 1) & 1;
@@ -375,24 +498,39 @@ __global__ void __launch_bounds__(ROT ? 320 + 32 * kRotWarps : 320, 1)
       }
       if (tr && t == 0 && threadIdx.x == 64) tr[3] = globaltimer();
       tc_fence_after();
+      if (trc) {
+        pc = clock64();
+        if (t >= 2) {
+          mma_lat += pc - arr_prev;
+          ++mma_n;
+          sum_r += pc;
+          sum_a += arr_prev;
+        }
+      }
       const uint32_t sAddr = tmem + lane_addr + kTmS + sb * 128 + hc * 64;
       float sv[64];
       tmem_ld64(sAddr, sv);
-      float mx = -INFINITY;
-      if (key0 + 63 <= pos) {  // the whole half is causal-visible: no mask
+      phase(0);
+      if (key0 + 63 > pos) {  // part of the half lies beyond the row's causal limit
 #pragma unroll
-        for (int i = 0; i < 64; ++i) mx = fmaxf(mx, sv[i]);
-      } else {
-#pragma unroll
-        for (int i = 0; i < 64; ++i) {
-          sv[i] = (key0 + i <= pos) ? sv[i] : -INFINITY;
-          mx = fmaxf(mx, sv[i]);
-        }
+        for (int i = 0; i < 64; ++i) sv[i] = (key0 + i <= pos) ? sv[i] : -INFINITY;
       }
+      // four independent 3-input max chains (a single chain is 32 dependent FMNMX3)
+      float m4[4] = {fmaxf(sv[0], sv[1]), fmaxf(sv[2], sv[3]), fmaxf(sv[4], sv[5]), fmaxf(sv[6], sv[7])};
+#pragma unroll
+      for (int i = 8; i < 64; i += 8) {
+        m4[0] = fmax3(m4[0], sv[i], sv[i + 1]);
+        m4[1] = fmax3(m4[1], sv[i + 2], sv[i + 3]);
+        m4[2] = fmax3(m4[2], sv[i + 4], sv[i + 5]);
+        m4[3] = fmax3(m4[3], sv[i + 6], sv[i + 7]);
+      }
+      float mx = fmax3(m4[0], m4[1], fmaxf(m4[2], m4[3]));
       mx *= sc;  // log2 units (sc > 0)
+      phase(1);
       xmax[(sb * 2 + hc) * 128 + r] = mx;
       named_bar_sync(1 + q, 64);
       mx = fmaxf(mx, xmax[(sb * 2 + (hc ^ 1)) * 128 + r]);
+      phase(2);
       // tcgen05.ld/st are warp-collective: the rescale runs for the whole warp if any row needs it
       // (both warps of a pair see identical maxima, so they take identical decisions)
       const bool grow = mx > m_ref + 8.f;
@@ -414,32 +552,44 @@ __global__ void __launch_bounds__(ROT ? 320 + 32 * kRotWarps : 320, 1)
         l *= alpha;
       }
       if (grow) m_ref = mx;
+      phase(3);
       if (trc) {
         tt0 = globaltimer();
         acc_mx += tt0 - tt1;
       }
       const float nmu = (m_ref == -INFINITY) ? 0.f : -m_ref;
-      float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+      const float2 sc2 = make_float2(sc, sc), nmu2 = make_float2(nmu, nmu);
+      float2 la = make_float2(0.f, 0.f), lb = make_float2(0.f, 0.f);
       uint32_t pk[32];
 #pragma unroll
-      for (int c = 0; c < 16; ++c) {  // p = 2^(s·scale − m_ref); masked keys are −inf → 0
-        const float p0 = ex2_approx(fmaf(sv[4 * c], sc, nmu)), p1 = ex2_approx(fmaf(sv[4 * c + 1], sc, nmu));
-        const float p2 = ex2_approx(fmaf(sv[4 * c + 2], sc, nmu)), p3 = ex2_approx(fmaf(sv[4 * c + 3], sc, nmu));
-        s0 += p0;
-        s1 += p1;
-        s2 += p2;
-        s3 += p3;
-        pk[2 * c] = pack_bf16(p0, p1);
-        pk[2 * c + 1] = pack_bf16(p2, p3);
+      for (int c = 0; c < 32; ++c) {  // p = 2^(s·scale − m_ref); masked keys are −inf → 0 (poly: 2^-125)
+        const float2 xv = fma2(make_float2(sv[2 * c], sv[2 * c + 1]), sc2, nmu2);
+        float2 pv;
+        if ((c & 7) < PIC_V1_POLY8)  // part of the exponentials on the FMA pipe: the phase is MUFU-bound
+          pv = exp2_poly2(xv);
+        else
+          pv = make_float2(ex2_approx(xv.x), ex2_approx(xv.y));
+        if (c & 1)
+          lb = add2(lb, pv);
+        else
+          la = add2(la, pv);
+        pk[c] = pack_bf16(pv.x, pv.y);
       }
-      l += (s0 + s1) + (s2 + s3);
+      l += (la.x + la.y) + (lb.x + lb.y);
+      phase(4);
       // P(t) overwrites this half's S(t) columns (already in registers); PV(t) reads it from TMEM
       tmem_st32u(sAddr, pk);
       tmem_wait_st();
+      phase(5);
       // consume every o_full phase (PV(t-1) has long finished here): no barrier phase completes unobserved
       if (t >= 1) mbar_wait(o_full + 8 * ((t - 1) & 1), ((t - 1) >> 1) & 1);
       tc_fence_before();
       mbar_arrive(p_full + 8 * sb);
+      phase(6);
+      if (trc) {
+        arr_prev = arr_cur;
+        arr_cur = clock64();
+      }
       if (trc) acc_ex += globaltimer() - tt0;
     }
     if (trc) {
@@ -447,6 +597,11 @@ __global__ void __launch_bounds__(ROT ? 320 + 32 * kRotWarps : 320, 1)
       tr[8] = acc_ws;
       tr[9] = acc_mx;
       tr[10] = acc_ex;
+      for (int i = 0; i < 7; ++i) tr[16 + i] = ph_[i];
+      tr[23] = mma_lat;
+      tr[24] = mma_n;
+      tr[26] = sum_r;
+      tr[27] = sum_a;
     }
     if (n > 0) {
       mbar_wait(o_full + 8 * ((n - 1) & 1), ((n - 1) >> 1) & 1);
@@ -574,7 +729,9 @@ template <int G>
 static cudaError_t launch_attn_g(const CUtensorMap& tmQ, const CUtensorMap& tmK, const CUtensorMap& tmV,
                                  const CUtensorMap& tmK8, const CUtensorMap& tmV8, const AttnArgs& a, cudaStream_t st) {
   dim3 grid(a.n_work, a.Hkv);
-  if (a.bdelta)
+  if (a.bdelta && a.qrot)
+    CUDA_TRY_LAUNCH(launch_k(attn_tc_kernel<G, true, true>, dim3(grid), dim3(320 + 32 * kRotWarps), attn::kSmem, st, tmQ, tmK, tmV, tmK8, tmV8, a));
+  else if (a.bdelta)
     CUDA_TRY_LAUNCH(launch_k(attn_tc_kernel<G, true>, dim3(grid), dim3(320 + 32 * kRotWarps), attn::kSmem, st, tmQ, tmK, tmV, tmK8, tmV8, a));
   else
     CUDA_TRY_LAUNCH(launch_k(attn_tc_kernel<G, false>, dim3(grid), dim3(320), attn::kSmem, st, tmQ, tmK, tmV, tmK8, tmV8, a));
@@ -585,6 +742,7 @@ template <int G>
 static cudaError_t prepare_g() {
   cudaError_t e = cudaFuncSetAttribute(attn_tc_kernel<G, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, attn::kSmem);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(attn_tc_kernel<G, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, attn::kSmem);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(attn_tc_kernel<G, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, attn::kSmem);
   return e;
 }
 

@@ -201,6 +201,9 @@ struct AttnArgs {
   // V block table (nullable: V lives in the same blocks as K).  kv_share 2 links V by reference to the
   // chunk-store blocks while K is a re-based copy in fresh blocks.
   const int32_t* vbt;
+  // 1: every K tile of every sequence has ONE block delta (kv_share 3 chunk frames): re-base by rotating
+  // Q per frame (R(−Δ)·Q in TMEM, S as a TS MMA) instead of the K tiles (one-lane kernel)
+  int qrot;
   int debug;  // bench-only ablation (PIC_ATTN_DEBUG), results invalid: 1 = softmax skipped, 2 = no K re-base
              // arithmetic, 3 = rotation warpgroup idle, 4 = as 2 without the proxy fence
 };

@@ -36,6 +36,7 @@ for kern in (2, 1):  # ping-pong kernel forced (copy and rotating variants), the
     B.set_attention_kernel(kern)
     eng.link(segs, "legolink:4", use_graph=False, kv_share=False)
     eng.link(segs, "legolink:4", use_graph=False, kv_share=True)
+    eng.link(segs, "legolink:4", use_graph=False, kv_share=3)
     eng.link_batch(perm, "fr", use_graph=False)  # M = 336: pair SwiGLU GEMM, fused epilogues and norm
 B.set_attention_kernel(0)
 eng.close()
@@ -47,7 +48,7 @@ e4 = B.Engine(w4.model, num_blocks=(sum(len(c) for c in w4.chunks) + 2 * sum(Ns)
               max_tokens=max(Ns) + 16, max_requests=2, device=0)
 i4 = e4.generate_context_cache(w4.chunks)
 r4 = [[("cached", i4[s.chunk]) if s.cached else ("tokens", s.tokens) for s in r] for r in w4.requests]
-for share in (True, False):
+for share in (1, 0, 3):  # 3: chunk-frame link, Q-side re-base (QROT) at the bench's tile sizes
     e4.link_batch(r4, w4.alg, use_graph=False, kv_share=share)
 e4.close()
 print("sanitize target done, pair fused =", os.environ.get("PIC_PAIR_FUSED", "0"))

@@ -195,3 +195,29 @@ def test_fullsize_shared_block_link_bit_identical(which, kernel, mode):
     finally:
         B.set_attention_kernel(0)
         eng.close()
+
+
+@pytest.mark.parametrize("which", ["cfg2", "cfg4"])
+def test_fullsize_chunkframe_qrot_link(which):
+    """kv_share 3 at full size: every 128-key tile of these links lies inside one 512-token chunk, so the
+    attention re-bases by rotating Q per chunk frame (QROT).  Held to the copy path (itself held to the
+    oracle above) at the north star's 2e-2: logits, first tokens, and sampled layers' linked K/V exports."""
+    w = sg.cfg2() if which == "cfg2" else sg.cfg4(n_requests=4)
+    m = w.model
+    Ns = [sum(len(w.chunks[s.chunk]) if s.cached else len(s.tokens) for s in r) for r in w.requests]
+    eng = B.Engine(m, num_blocks=(sum(len(c) for c in w.chunks) + 2 * sum(Ns)) // 16 + 64, max_rows=4096,
+                   max_tokens=max(Ns) + 16, max_requests=len(w.requests), device=0)
+    try:
+        ids = eng.generate_context_cache(w.chunks)
+        reqs = [[("cached", ids[s.chunk]) if s.cached else ("tokens", s.tokens) for s in r] for r in w.requests]
+        outs = [eng.link_batch(reqs, w.alg, keep_linked=True, kv_share=share) for share in (0, 3)]
+        for a, b in zip(*outs):
+            assert rel(b.logits, a.logits) < 2e-2
+            assert b.first_token == a.first_token
+            for l in (0, m.n_layers // 2, m.n_layers - 1):
+                ka, va = eng.linked_export(a.linked, l)
+                kb, vb = eng.linked_export(b.linked, l)
+                assert rel(f32(kb), f32(ka)) < 2e-2, l
+                assert rel(f32(vb), f32(va)) < 2e-2, l
+    finally:
+        eng.close()

@@ -54,7 +54,7 @@ def test_cfg2_full_depth_end_to_end_vs_oracle():
     N = n_tok(w, w.requests[0])
     eng = B.Engine(cfg, num_blocks=(sum(len(c) for c in w.chunks) + 3 * N) // 16 + 64, max_rows=4096,
                    max_tokens=N + 16, device=0)
-    eng.kv_share = True                                        # the bench's configuration
+    eng.kv_share = 3                                           # the bench's configuration (chunk-frame link)
     try:
         ids = eng.generate_context_cache(w.chunks)
         segs = [("cached", ids[s.chunk]) if s.cached else ("tokens", s.tokens) for s in w.requests[0]]
@@ -93,14 +93,15 @@ def test_cfg2_full_depth_end_to_end_vs_oracle():
         eng.close()
 
 
-def test_cfg4_wave_sampled_rows_vs_oracle():
+@pytest.mark.parametrize("kv_share", [1, 3])
+def test_cfg4_wave_sampled_rows_vs_oracle(kv_share):
     w = sg.cfg4(n_requests=32)
     cfg = w.model
     L = cfg.n_layers
     Ns = [n_tok(w, r) for r in w.requests]
     eng = B.Engine(cfg, num_blocks=sum(len(c) for c in w.chunks) // 16 + (sum(Ns) + 2 * max(Ns)) // 16 + 256,
                    max_rows=8192, max_tokens=max(Ns) + 16, max_requests=32, device=0)
-    eng.kv_share = True
+    eng.kv_share = kv_share                                    # 3 is the bench default
     try:
         ids = eng.generate_context_cache(w.chunks)
         reqs = [[("cached", ids[s.chunk]) if s.cached else ("tokens", s.tokens) for s in r] for r in w.requests]
@@ -151,7 +152,7 @@ def test_cfg5_truncated_depth_sampled_rows_vs_oracle():
     assert N == 32832 and cfg.n_heads // cfg.n_kv_heads == 8
     eng = B.Engine(cfg, num_blocks=(sum(len(c) for c in w.chunks) + 3 * N) // 16 + 64, max_rows=4096,
                    max_tokens=N + 16, device=0)
-    eng.kv_share = True
+    eng.kv_share = 3
     try:
         ids = eng.generate_context_cache(w.chunks)
         segs = [("cached", ids[s.chunk]) if s.cached else ("tokens", s.tokens) for s in w.requests[0]]

@@ -303,6 +303,41 @@ def test_materialize_bit_identical_and_accounting(setup):
         s.eng.release(hs)
 
 
+def test_chunkframe_materialize_accounting(setup):
+    """kv_share 3 + materialize: every block with a frame Δ (store blocks linked by reference and owned
+    chunk-frame blocks) is re-based into a fresh owned block; n_shared drops by the by-reference ones only,
+    the owned frame blocks return to the pool, exports are unchanged bit for bit, and decode over the
+    materialized handle equals decode over an identical un-materialized one bit for bit (the decode
+    attention re-bases K tiles with a2's arithmetic)."""
+    s = setup
+    segs = s.w.requests[0]
+    ha = s.eng.link(s.segs(segs), "legolink:4", keep_linked=True, kv_share=3).linked
+    hb = s.eng.link(s.segs(segs), "legolink:4", keep_linked=True, kv_share=3).linked
+    try:
+        n_shared0, bd0 = s.eng.linked_sharing(hb)
+        n_rot = int((bd0 != 0).sum())
+        assert n_rot > 0 and n_shared0 > 0
+        exp0 = [s.eng.linked_export(hb, l) for l in range(s.cfg.n_layers)]
+        free0 = s.eng.stats()["free_blocks"]
+        s.eng.materialize(hb)
+        n_shared1, bd1 = s.eng.linked_sharing(hb)
+        assert not bd1.any() and n_shared1 >= 0
+        n_byref_rot = n_shared0 - n_shared1
+        n_owned_rot = n_rot - n_byref_rot
+        assert n_owned_rot > 0                                    # owned frame blocks carried Δ too
+        assert s.eng.stats()["free_blocks"] == free0 - n_rot + n_owned_rot
+        for l in range(s.cfg.n_layers):
+            k, v = s.eng.linked_export(hb, l)
+            assert np.array_equal(k, exp0[l][0]) and np.array_equal(v, exp0[l][1]), l
+        for t in (5, 17, 99):
+            a = s.eng.decode([ha], [t])
+            b = s.eng.decode([hb], [t])
+            assert np.array_equal(a.logits, b.logits)
+    finally:
+        s.eng.release(ha)
+        s.eng.release(hb)
+
+
 def test_shared_batch_same_chunks_refcounts(setup):
     """A batched shared-block link whose requests reuse the same chunks (the cfg4 pattern): every request
     is bit-identical to its own copy-path link, the store blocks carry one reference per request, and
