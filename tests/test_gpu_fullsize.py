@@ -213,7 +213,15 @@ def test_fullsize_chunkframe_qrot_link(which):
         outs = [eng.link_batch(reqs, w.alg, keep_linked=True, kv_share=share) for share in (0, 3)]
         for a, b in zip(*outs):
             assert rel(b.logits, a.logits) < 2e-2
-            assert b.first_token == a.first_token
+            # different re-base arithmetic (Q rotated instead of K): the argmax is held to the copy path's
+            # unless its top-1/top-2 gap is within 4x the measured logit error (SURVEY §8(c).8 near ties)
+            assert b.first_token == int(np.argmax(b.logits))
+            top = np.argsort(-a.logits)[:2]
+            err = float(np.max(np.abs(np.asarray(b.logits, np.float64) - a.logits)))
+            if a.logits[top[0]] - a.logits[top[1]] > 4 * err:
+                assert b.first_token == a.first_token
+            else:
+                assert b.first_token in set(top.tolist())
             for l in (0, m.n_layers // 2, m.n_layers - 1):
                 ka, va = eng.linked_export(a.linked, l)
                 kb, vb = eng.linked_export(b.linked, l)
