@@ -48,8 +48,15 @@ static_assert(kSmem <= 232448, "attention smem over the 227 KB limit");
 // TMEM columns (512 allocated)
 constexpr uint32_t kTmS = 0;    // S double buffer [0, 256); P(t) (bf16 pairs) overwrites S(t): half hc at +64·hc
 constexpr uint32_t kTmO = 256;  // O accumulator [256, 384)
-constexpr uint32_t kTmQd = 384;  // QROT: two R(−Δ)·Q buffers (bf16 pairs, 64 columns each) [384, 512)
+constexpr uint32_t kTmQd = 384;  // QROT in TMEM (PIC_QROT_SMEM=0): two R(−Δ)·Q buffers (bf16 pairs) [384, 512)
+// QROT in shared memory (default): the two R(−Δ)·Q buffers take V slot 2 and the Q tile ([kV + 2 slots, kX)),
+// so the QROT kernel runs a 2-slot V ring; S = Q_Δ·Kᵀ stays an SS MMA.
+constexpr int kQd = kV + 2 * 2 * kTile;
+static_assert(kQd + 2 * 2 * kTile == kX, "QROT smem buffers must end where the Q tile ends");
 }  // namespace attn
+#ifndef PIC_QROT_SMEM
+#define PIC_QROT_SMEM 0  // smem variant (2-slot V ring) measured equal at cfg4: 178-180 vs 177-178 ms per step
+#endif
 
 // Q is TMA-staged into shared memory once per CTA (the A operand of S = Q·Kᵀ); P is the TMEM A operand
 // of O += P·V.  (A TMEM-resident Q cost a 1.8 µs tcgen05.st + wait::st in every CTA's prologue.)
@@ -57,6 +64,17 @@ constexpr uint32_t kTmQd = 384;  // QROT: two R(−Δ)·Q buffers (bf16 pairs, 6
 // 32 layers): 4 warps 26.3 ms, 2 warps 41.5 ms (the rotation is issue-bound and sits between the K TMA
 // and the S MMA); 4 warps cap the CTA at 128 registers per thread (14 warps), a few bytes of spill.
 constexpr int kRotWarps = 4;
+#ifndef PIC_QROT_WARPS
+#define PIC_QROT_WARPS 4
+#endif
+// QROT with R(−Δ)·Q in smem: the frame rotation has no TMEM lane-quarter constraint, so it may run on
+// fewer warps (1, 2 or 4; a frame changes every ~4 K tiles)
+constexpr int kQrotWarpsSm = PIC_QROT_WARPS;
+static_assert(kQrotWarpsSm == 1 || kQrotWarpsSm == 2 || kQrotWarpsSm == 4, "PIC_QROT_WARPS: 1, 2 or 4");
+template <bool ROT, bool QROT>
+constexpr int attn_threads() {
+  return !ROT ? 320 : (QROT && PIC_QROT_SMEM) ? 320 + 32 * kQrotWarpsSm : 320 + 32 * kRotWarps;
+}
 #ifndef PIC_V1_POLY8
 #define PIC_V1_POLY8 1  // pairs of every 8 whose exponential runs on the FMA-pipe polynomial (exp2_poly2)
 #endif
@@ -64,13 +82,16 @@ constexpr int kRotWarps = 4;
 // the rotation warps write R(−Δ)·Q for each frame into TMEM and S = Q_Δ·Kᵀ runs as a TS MMA
 // (q·R(Δ)k = (R(−Δ)q)·k) — one rotation of the 128-row Q tile per chunk instead of one per K tile.
 template <int G, bool ROT, bool QROT = false>
-__global__ void __launch_bounds__(ROT ? 320 + 32 * kRotWarps : 320, 1)
+__global__ void __launch_bounds__(attn_threads<ROT, QROT>(), 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                    const __grid_constant__ CUtensorMap tmV,
                    const __grid_constant__ CUtensorMap tmK8, const __grid_constant__ CUtensorMap tmV8, const AttnArgs a) {
   griddep_launch();
   using namespace attn;
   constexpr int S = kStages;
+  // QROT_SM: R(−Δ)·Q lives in smem (SS MMA for S) in place of V slot 2 and the Q tile
+  constexpr bool QROT_SM = QROT && PIC_QROT_SMEM;
+  constexpr int SV = QROT_SM ? 2 : S;  // V ring depth
   unsigned long long* const tr = a.trace ? a.trace + 32 * (blockIdx.y * gridDim.x + blockIdx.x) : nullptr;
   if (tr && threadIdx.x == 0) tr[0] = globaltimer();
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -99,7 +120,7 @@ __global__ void __launch_bounds__(ROT ? 320 + 32 * kRotWarps : 320, 1)
       mbar_init(k_rot + 8 * s, kRotWarps);
     }
     for (int b = 0; b < 2; ++b) {
-      mbar_init(qd_full + 8 * b, kRotWarps);
+      mbar_init(qd_full + 8 * b, (QROT && PIC_QROT_SMEM) ? kQrotWarpsSm : kRotWarps);
       mbar_init(qd_empty + 8 * b, 1);
     }
     for (int b = 0; b < 2; ++b) {
@@ -151,8 +172,11 @@ __global__ void __launch_bounds__(ROT ? 320 + 32 * kRotWarps : 320, 1)
     if (n > 0) {
       if (lane == 0) {
         // Q first: 128 MMA rows = (128/G queries) x (G heads of kv-head g), one 3-D box per 64-dim half
-        mbar_expect_tx(q_full, 2 * kTile);
-        for (int h = 0; h < 2; ++h) tma_load_3d(base + kQ + h * kTile, &tmQ, q_full, h * 64, g * G, row_start);
+        // (QROT_SM: the rotation warps build every frame's R(−Δ)·Q straight from global Q instead)
+        if (!QROT_SM) {
+          mbar_expect_tx(q_full, 2 * kTile);
+          for (int h = 0; h < 2; ++h) tma_load_3d(base + kQ + h * kTile, &tmQ, q_full, h * 64, g * G, row_start);
+        }
         tma_prefetch(&tmK);
         tma_prefetch(&tmV);
         tma_prefetch(&tmK8);
@@ -164,6 +188,25 @@ __global__ void __launch_bounds__(ROT ? 320 + 32 * kRotWarps : 320, 1)
       const int* vbt = a.vbt ? a.vbt + a.seq_bt_off[seq] : bt;
       int blk_next = lane < 8 ? bt[min(j0 * 8 + lane, last_blk)] : 0;
       int vblk_next = lane < 8 ? vbt[min(j0 * 8 + lane, last_blk)] : 0;
+      // V(t) is issued after K(t+1): the MMA warp consumes S(t+1) before PV(t), and a V slot still held by
+      // PV(t-SV) must not hold back the next K tile (measured with the 2-slot V ring of QROT_SM)
+      auto load_v = [&](int u, int vb0, const int* vb, bool vc) {
+        const int vs = u % SV;
+        mbar_wait(v_empty + 8 * vs, ((u / SV) & 1) ^ 1);
+        mbar_expect_tx(v_full + 8 * vs, 2 * kTile);
+        if (vc) {
+          for (int h = 0; h < 2; ++h)
+            tma_load_4d(base + kV + (2 * vs + h) * kTile, &tmV8, v_full + 8 * vs, h * 64, 0, g, kv_base + vb0);
+        } else {
+#pragma unroll
+          for (int b = 0; b < 8; ++b)
+            for (int h = 0; h < 2; ++h)
+              tma_load_4d(base + kV + (2 * vs + h) * kTile + b * 2048, &tmV, v_full + 8 * vs, h * 64, 0, g,
+                          kv_base + vb[b]);
+        }
+      };
+      int vprev[8];
+      bool vcprev = false;
       for (int t = 0; t < n; ++t) {
         const int s = t % S;
         const uint32_t ph = (t / S) & 1;
@@ -194,21 +237,15 @@ __global__ void __launch_bounds__(ROT ? 320 + 32 * kRotWarps : 320, 1)
                 tma_load_4d(base + kK + (2 * s + h) * kTile + b * 2048, &tmK, k_full + 8 * s, h * 64, 0, g,
                             kv_base + blk[b]);
           }
-          mbar_wait(v_empty + 8 * s, ph ^ 1);
-          mbar_expect_tx(v_full + 8 * s, 2 * kTile);
-          if (vcontig) {
-            for (int h = 0; h < 2; ++h)
-              tma_load_4d(base + kV + (2 * s + h) * kTile, &tmV8, v_full + 8 * s, h * 64, 0, g, kv_base + vblk[0]);
-          } else {
-#pragma unroll
-            for (int b = 0; b < 8; ++b)
-              for (int h = 0; h < 2; ++h)
-                tma_load_4d(base + kV + (2 * s + h) * kTile + b * 2048, &tmV, v_full + 8 * s, h * 64, 0, g,
-                            kv_base + vblk[b]);
-          }
+          if (t > 0) load_v(t - 1, vprev[0], vprev, vcprev);
         }
+#pragma unroll
+        for (int b = 0; b < 8; ++b) vprev[b] = vblk[b];
+        vcprev = vcontig;
         __syncwarp();
       }
+      if (lane == 0) load_v(n - 1, vprev[0], vprev, vcprev);
+      __syncwarp();
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------------ MMA issuer
@@ -220,12 +257,13 @@ __global__ void __launch_bounds__(ROT ? 320 + 32 * kRotWarps : 320, 1)
       constexpr uint32_t idO = idesc_bf16(128, 128, 0, 1);  // P (TMEM, K-major) x V (smem, MN-major)
       const uint64_t dQ = sdesc_sw128(base + kQ, 16, 1024), dK0 = sdesc_sw128(base + kK, 16, 1024);
       const uint64_t dV0 = sdesc_sw128(base + kV, kTile, 1024);
+      const uint64_t dQd = sdesc_sw128(base + kQd, 16, 1024);  // QROT_SM: R(−Δ)·Q buffer 0 (buffer 1: +32 KB)
       unsigned long long w_k = 0, w_p = 0, w_v = 0, w_q = 0, q0 = 0, sum_w = 0;
-      mbar_wait(q_full, 0);
+      if (!QROT_SM) mbar_wait(q_full, 0);
       tc_fence_after();
       if (tr && lane == 0) tr[2] = globaltimer();
       auto issue_pv = [&](int u) {
-        const int pb = u & 1, vs = u % S;
+        const int pb = u & 1, vs = u % SV;
         if (tr) q0 = globaltimer();
         mbar_wait(p_full + 8 * pb, (u >> 1) & 1);
         if (tr) {
@@ -236,7 +274,7 @@ __global__ void __launch_bounds__(ROT ? 320 + 32 * kRotWarps : 320, 1)
           w_p += q1 - q0;
           q0 = q1;
         }
-        mbar_wait(v_full + 8 * vs, (u / S) & 1);
+        mbar_wait(v_full + 8 * vs, (u / SV) & 1);
         if (tr) w_v += globaltimer() - q0;
         tc_fence_after();
         const uint64_t dv = dV0 + (uint64_t)(vs * (2 * kTile / 16));
@@ -285,13 +323,16 @@ __global__ void __launch_bounds__(ROT ? 320 + 32 * kRotWarps : 320, 1)
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
           const uint64_t o = (uint64_t)(((kk >> 2) * kTile + (kk & 3) * 32) >> 4);
-          if constexpr (QROT)
+          if constexpr (QROT && !QROT_SM)
             umma_bf16_ts_e(tmem + kTmS + sb * 128, tmem + kTmQd + qb * 64 + kk * 8, dk + o, idS, kk > 0);
           else
-            umma_bf16_e(tmem + kTmS + sb * 128, dQ + o, dk + o, idS, kk > 0);
+            umma_bf16_e(tmem + kTmS + sb * 128, (QROT_SM ? dQd + (uint64_t)(qb * (2 * kTile / 16)) : dQ) + o, dk + o,
+                        idS, kk > 0);
         }
 #else
-        if constexpr (QROT)  // A = R(−Δ)·Q from TMEM: dims 16kk..16kk+15 at columns 8kk..8kk+7
+        if constexpr (QROT_SM)  // A = R(−Δ)·Q buffer qb in smem
+          umma_ss_k128(tmem + kTmS + sb * 128, dQd + (uint64_t)(qb * (2 * kTile / 16)), dk, idS, 0, kTile);
+        else if constexpr (QROT)  // A = R(−Δ)·Q from TMEM: dims 16kk..16kk+15 at columns 8kk..8kk+7
           umma_tsk_k128(tmem + kTmS + sb * 128, tmem + kTmQd + qb * 64, dk, idS, kTile);
         else
           umma_ss_k128(tmem + kTmS + sb * 128, dQ, dk, idS, 0, kTile);
@@ -309,6 +350,80 @@ __global__ void __launch_bounds__(ROT ? 320 + 32 * kRotWarps : 320, 1)
         tr[14] = w_q;
         tr[15] = (unsigned long long)(fi + 1);
         tr[25] = sum_w;
+      }
+    }
+  } else if (QROT_SM && warp >= 10) {
+    // ------------------------------------------------------------------ Q re-base per chunk frame (smem)
+    // For every frame Δ met along the KV range (in tile order), build R(−Δ)·q for the tile's 128 MMA rows
+    // (row r = (query r / G, head g·G + r % G); NeoX pairs (j, j+64), fp32 rotation of the bf16 q rounded to
+    // bf16, as the TMEM variant) straight from global Q into the smem buffer of that frame's parity, in the
+    // SWIZZLE_128B K-major layout the TMA would give (rows past the tile are zero).  Thread u owns the
+    // 16-B chunk cc = u & 7 (dims 8cc..8cc+7 and their partners 64+8cc..) of rows rg + RS·i, rg = u >> 3,
+    // RS = 4·kQrotWarpsSm; each warp-wide load covers 4 rows x 128 contiguous bytes.
+    if (n > 0) {
+      constexpr int RS = 4 * kQrotWarpsSm, NR = 128 / RS;  // row stride, rows per thread
+      const int u = threadIdx.x - 320;
+      const int cc = u & 7, rg = u >> 3;
+      const int* bdq = a.bdelta + a.seq_bt_off[seq];
+      const uint16_t* Qg = reinterpret_cast<const uint16_t*>(a.Q);
+      int fi = -1, fr_cur = 0;
+      for (int t = 0; t < n; ++t) {
+        const int fr = bdq[min((j0 + t) * 8, last_blk)];
+        if (t > 0 && fr == fr_cur) continue;
+        fr_cur = fr;
+        ++fi;
+        const int ad = fr < 0 ? -fr : fr;
+        const float sg = fr < 0 ? 1.f : -1.f;  // R(−Δ): sin(−Δθ) = −sign(Δ)·sin(|Δ|θ)
+        const float4* cp = reinterpret_cast<const float4*>(a.cos_t + (size_t)ad * 64 + cc * 8);
+        const float4* sp = reinterpret_cast<const float4*>(a.sin_t + (size_t)ad * 64 + cc * 8);
+        const float4 c0 = __ldg(cp), c1 = __ldg(cp + 1), s0 = __ldg(sp), s1 = __ldg(sp + 1);
+        const float cs[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+        const float sn[8] = {sg * s0.x, sg * s0.y, sg * s0.z, sg * s0.w, sg * s1.x, sg * s1.y, sg * s1.z, sg * s1.w};
+        const uint32_t qb = base + kQd + (fi & 1) * (2 * kTile);
+#pragma unroll 1
+        for (int i0 = 0; i0 < NR; i0 += 4) {
+          uint4 xa[4], xb[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int r = rg + RS * (i0 + i), qi = r / G;
+            if (qi < row_count) {
+              const uint4* src = reinterpret_cast<const uint4*>(
+                  Qg + ((size_t)(row_start + qi) * a.Hq + g * G + r % G) * 128 + cc * 8);
+              xa[i] = __ldg(src);
+              xb[i] = __ldg(src + 8);
+            } else {
+              xa[i] = make_uint4(0u, 0u, 0u, 0u);
+              xb[i] = xa[i];
+            }
+          }
+          // the first rows' loads are in flight: wait until the MMAs of frame fi−2 are done with the buffer
+          if (i0 == 0) mbar_wait(qd_empty + 8 * (fi & 1), ((fi >> 1) & 1) ^ 1);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            if (fr != 0) {
+              uint32_t a4[4] = {xa[i].x, xa[i].y, xa[i].z, xa[i].w}, b4[4] = {xb[i].x, xb[i].y, xb[i].z, xb[i].w};
+#pragma unroll
+              for (int k = 0; k < 4; ++k) {
+                const float a0 = __uint_as_float(a4[k] << 16), a1 = __uint_as_float(a4[k] & 0xFFFF0000u);
+                const float b0 = __uint_as_float(b4[k] << 16), b1 = __uint_as_float(b4[k] & 0xFFFF0000u);
+                float ra0, rb0, ra1, rb1;
+                rebase_pair(a0, b0, cs[2 * k], sn[2 * k], ra0, rb0);
+                rebase_pair(a1, b1, cs[2 * k + 1], sn[2 * k + 1], ra1, rb1);
+                a4[k] = pack_bf16(ra0, ra1);
+                b4[k] = pack_bf16(rb0, rb1);
+              }
+              xa[i] = make_uint4(a4[0], a4[1], a4[2], a4[3]);
+              xb[i] = make_uint4(b4[0], b4[1], b4[2], b4[3]);
+            }
+            const int r = rg + RS * (i0 + i);
+            const uint32_t o = (uint32_t)(r * 128 + ((cc ^ (r & 7)) << 4));  // SW128: chunk cc of row r
+            sts128(qb + o, xa[i]);
+            sts128(qb + kTile + o, xb[i]);
+          }
+        }
+        fence_async_smem();  // generic-proxy smem writes -> visible to the tcgen05.mma operand reads
+        __syncwarp();
+        if (lane == 0) mbar_arrive(qd_full + 8 * (fi & 1));
       }
     }
   } else if (QROT && warp >= 10) {
@@ -730,7 +845,7 @@ static cudaError_t launch_attn_g(const CUtensorMap& tmQ, const CUtensorMap& tmK,
                                  const CUtensorMap& tmK8, const CUtensorMap& tmV8, const AttnArgs& a, cudaStream_t st) {
   dim3 grid(a.n_work, a.Hkv);
   if (a.bdelta && a.qrot)
-    CUDA_TRY_LAUNCH(launch_k(attn_tc_kernel<G, true, true>, dim3(grid), dim3(320 + 32 * kRotWarps), attn::kSmem, st, tmQ, tmK, tmV, tmK8, tmV8, a));
+    CUDA_TRY_LAUNCH(launch_k(attn_tc_kernel<G, true, true>, dim3(grid), dim3(attn_threads<true, true>()), attn::kSmem, st, tmQ, tmK, tmV, tmK8, tmV8, a));
   else if (a.bdelta)
     CUDA_TRY_LAUNCH(launch_k(attn_tc_kernel<G, true>, dim3(grid), dim3(320 + 32 * kRotWarps), attn::kSmem, st, tmQ, tmK, tmV, tmK8, tmV8, a));
   else

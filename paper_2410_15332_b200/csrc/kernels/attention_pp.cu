@@ -51,6 +51,16 @@ constexpr int bQFull = 0, bQEmpty = 2, bKFull = 4, bKEmpty = bKFull + kKS, bKRot
 constexpr int kSmem = kBar + kNumBars * 8 + 16 + kIR * 4;
 static_assert(kSmem <= 232448, "attention smem over the 227 KB limit");
 constexpr int kRotWarps = 4;  // ROT: warpgroup 1 (warps 4-7) re-bases shared K tiles
+#ifndef PIC_PP_TURN
+#define PIC_PP_TURN 0
+#endif
+// PIC_PP_TURN=1 (A/B only): the two softmax warpgroups take strict turns (named barriers 1 and 2,
+// FA3-style): lane B's step s starts when lane A's step s is done, lane A's step s+1 when lane B's step s
+// is done, to break the lanes' convoy (both softmaxes at once, then both waiting on the back-to-back MMAs
+// of both lanes).  Measured at cfg4 (copy path): 178-179 vs 175.7-176.3 ms per step without turns; the
+// softmax step does not get faster alone (~1900 cycles per 128x128 lane step either way): it is latency-,
+// not MUFU-bound, so serialising the lanes only lengthens the period.
+constexpr int kBarTurnA = 1, kBarTurnB = 2;
 // register split of the 384-thread CTA: 128·(producer, MMA, rotation) + 256·softmax <= 64 K
 // ROT register split of the 512-thread CTA: producer/MMA warpgroup 48, rotation warpgroup 104, softmax
 // warpgroups 176 (two-pass over TMEM: half a row in registers)
@@ -522,9 +532,17 @@ __global__ void __launch_bounds__(ROT ? 512 : 384, 1)
       }
       const int pos = valid ? a.row_pos[row] : P.max_p;
       float m_ref = -INFINITY, l = 0.f;
+      const int nA = LA.n, nB = LB.n;  // nA >= nB (pp_decode)
       for (int s = 0; s < P.n; ++s) {
         const unsigned long long tw = tr ? clk() : 0;
         mbar_wait(B(bSFull + x), cs & 1);
+        if (PIC_PP_TURN && a.debug != 1) {  // my turn: the other lane's previous softmax step is done
+          if (x == 0) {
+            if (s >= 1 && s - 1 < nB) named_bar_sync(kBarTurnA, 256);
+          } else {
+            named_bar_sync(kBarTurnB, 256);
+          }
+        }
         const unsigned long long tw1 = tr ? clk() : 0;
         if (tr) tacc[0] += tw1 - tw;
         tc_fence_after();
@@ -626,6 +644,13 @@ __global__ void __launch_bounds__(ROT ? 512 : 384, 1)
         const float s0 = la.x, s1 = la.y, s2 = lb.x, s3 = lb.y;
         l += (s0 + s1) + (s2 + s3);
         tmem_wait_st();
+        if (PIC_PP_TURN) {  // the other lane's turn
+          if (x == 0) {
+            if (s < nB) named_bar_arrive(kBarTurnB, 256);
+          } else {
+            if (s + 1 < nA) named_bar_arrive(kBarTurnA, 256);
+          }
+        }
         // consume every o_full phase (PV of the previous step has long finished): none completes unobserved
         if (s >= 1) mbar_wait(B(bOFull + x), (cs - 1) & 1);
         tc_fence_before();
