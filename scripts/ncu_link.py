@@ -20,7 +20,7 @@ ap.add_argument("--requests", type=int, default=32)
 ap.add_argument("--layers", type=int, default=None)
 ap.add_argument("--graph", type=int, default=1)
 ap.add_argument("--alg", default=None)
-ap.add_argument("--kv-share", type=int, default=1)
+ap.add_argument("--kv-share", type=int, default=3)
 a = ap.parse_args()
 w = {"cfg2": lambda: sg.cfg2(a.alg or "legolink:16", a.layers), "cfg3": lambda: sg.cfg3(a.alg or "legolink:32", a.layers),
      "cfg5": lambda: sg.cfg5(a.alg or "legolink:16", a.layers),
@@ -29,7 +29,7 @@ Ns = [sum(len(w.chunks[s.chunk]) if s.cached else len(s.tokens) for s in r) for 
 eng = B.Engine(w.model, num_blocks=(sum(len(c) for c in w.chunks) + sum(Ns)) // 16 + 64 * len(Ns) + 64,
                max_rows=max(4096, sum(Ns) if (a.alg or "").startswith("cacheblend") else 8192),
                max_tokens=max(Ns) + 16, max_requests=len(Ns), device=0)
-eng.kv_share = bool(a.kv_share)
+eng.kv_share = int(a.kv_share)
 ids = eng.generate_context_cache(w.chunks)
 reqs = [[("cached", ids[s.chunk]) if s.cached else ("tokens", s.tokens) for s in r] for r in w.requests]
 run = (lambda: eng.link_batch(reqs, w.alg, want_logits=False, use_graph=bool(a.graph))) if len(reqs) > 1 else \
