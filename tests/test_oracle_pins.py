@@ -465,3 +465,196 @@ def test_C17_decode_equals_link_with_the_token_as_literal(tiny):
         r2 = P.link(store, segs[:-1] + [("tokens", q)], alg)
         assert rel(lg, r2.logits) < 1e-12, alg
         assert rel(K, r2.K) < 1e-12 and rel(V, r2.V) < 1e-12, alg
+
+
+# ----------------------------------------------------------------------------
+# C18: LegoLink with 0 < k < n_c by an independent construction
+# ----------------------------------------------------------------------------
+def _complex_rebase(k_post, delta, cfg):
+    """R(Δ) on post-RoPE keys [H, n, D] as complex multiplication of the rotate-half pairs
+    (x_j + i·x_{j+D/2})·e^{iΔθ_j}, θ_j = rope_theta^(−2j/D) — the definition pinned by C7."""
+    D = cfg.head_dim
+    th = cfg.rope_theta ** (-np.arange(0, D, 2, dtype=np.float64) / D)
+    z = (k_post[..., : D // 2] + 1j * k_post[..., D // 2:]) * np.exp(1j * delta * th)
+    return np.concatenate([z.real, z.imag], axis=-1)
+
+
+def hf_legolink(cfg, Wt, parts, k):
+    """PAPER.md:213 (LegoLink, §4.2) built from HuggingFace Llama alone, in message order: a cached chunk
+    at message index 0 is linked as is; every later cached chunk contributes its first k tokens as an
+    ordinary HF forward over the KV cache built so far, then its remaining rows' KV from a standalone HF
+    prefill of the chunk (positions 0..n−1) re-based to their linked positions; dynamic tokens are an
+    ordinary forward.  The recomputed rows therefore attend to every earlier cached and recomputed row,
+    layer by layer (Eq. 1).  Returns the last forward's final logits and the per-layer K/V
+    [L][N][H_kv][D] of the whole linked cache."""
+    torch = pytest.importorskip("torch")
+    tf = pytest.importorskip("transformers")
+    m = hf_model(cfg, Wt)
+    cache = tf.DynamicCache(config=m.config)
+    pos, logits = 0, None
+
+    def fwd(tok, p0):
+        with torch.no_grad():
+            return m(torch.from_numpy(np.asarray(tok, np.int64))[None], past_key_values=cache, use_cache=True,
+                     position_ids=torch.arange(p0, p0 + len(tok))[None])
+
+    for idx, (kind, tok) in enumerate(parts):
+        n = len(tok)
+        if kind == "tokens":
+            logits = fwd(tok, pos).logits[0, -1].numpy()
+        else:
+            kk = 0 if idx == 0 else min(k, n)  # the message-index-0 chunk is exempt (reading R9, SPEC)
+            # the prompt's last token is always recomputed (its logits give the first token)
+            ke = n - 1 if idx == len(parts) - 1 else n
+            if kk:
+                logits = fwd(tok[:kk], pos).logits[0, -1].numpy()
+            if kk < ke:
+                with torch.no_grad():
+                    alone = m(torch.from_numpy(np.asarray(tok, np.int64))[None], use_cache=True).past_key_values
+                for l in range(cfg.n_layers):
+                    kc = alone.layers[l].keys[0].numpy()[:, kk:ke]        # [H_kv, ke - kk, D] at kk..ke-1
+                    vc = alone.layers[l].values[0].numpy()[:, kk:ke]
+                    kr = _complex_rebase(kc, pos, cfg)
+                    cache.update(torch.from_numpy(kr[None].copy()), torch.from_numpy(vc[None].copy()), l)
+            if ke < n and kk < n:
+                logits = fwd(tok[n - 1:], pos + n - 1).logits[0, -1].numpy()
+        pos += n
+    K = [cache.layers[l].keys[0].numpy().transpose(1, 0, 2) for l in range(cfg.n_layers)]
+    V = [cache.layers[l].values[0].numpy().transpose(1, 0, 2) for l in range(cfg.n_layers)]
+    return logits, K, V
+
+
+@pytest.mark.parametrize("cfg", [sg.TINY, sg.TINY_GQA, sg.TINY_D128], ids=lambda c: c.name)
+@pytest.mark.parametrize("k", [1, 4, 16])
+def test_C18_legolink_equals_hf_sequential_construction(cfg, k):
+    """Pins LegoLink for 0 < k < n_c (previously 'parity unpinned'): the oracle's layer-by-layer
+    recomputation of the selected rows over the linked cache equals the HF construction above, for the
+    canonical request and a permuted one (dynamic tokens first, chunks out of order, the prompt ending in a
+    cached chunk whose last token is recomputed)."""
+    w = sg.cfg1(model=cfg)
+    Wt = M.Weights(cfg)
+    store = P.Store(Wt)
+    ids = store.compile(w.chunks)
+    q = w.requests[0][-1].tokens
+    for order in ([0, 1, 2, "q"], ["q", 2, 0, 1]):
+        segs = [("tokens", q) if c == "q" else ("cached", ids[c]) for c in order]
+        parts = [("tokens", q) if c == "q" else ("chunk", w.chunks[c]) for c in order]
+        r = P.link(store, segs, f"legolink:{k}")
+        logits, K, V = hf_legolink(cfg, Wt, parts, k)
+        assert rel(r.logits, logits) < HF_TOL
+        for l in range(cfg.n_layers):
+            assert rel(r.K[l], K[l]) < HF_TOL, l
+            assert rel(r.V[l], V[l]) < HF_TOL, l
+
+
+# ----------------------------------------------------------------------------
+# C19: CacheBlend with a non-trivial selection by an independent construction
+# ----------------------------------------------------------------------------
+class _PrefixKV:
+    """Duck-typed HF cache for one decoder-layer call: keys/values already in the linked cache (any
+    order: the mask carries the positions) followed by the rows the call computes."""
+
+    def __init__(self, k, v):
+        self.k, self.v = k, v
+
+    def update(self, k, v, layer_idx, *args, **kwargs):
+        return torch_cat(self.k, k), torch_cat(self.v, v)
+
+
+def torch_cat(a, b):
+    import torch
+    return b if a is None else torch.cat([a, b], dim=2)
+
+
+def hf_cacheblend(cfg, Wt, parts, r_pct, check_layer=1):
+    """PAPER.md:170 (CacheBlend, as the paper describes it) built from HuggingFace Llama's own decoder
+    layers, RoPE and LM head: layer 0 recomputed for all N rows (ordinary causal prefill layer); at the
+    check layer the fresh K/V of every row (the layer's own projections + RoPE) are compared with the
+    linked cached K/V (standalone HF prefill of each chunk, keys re-based by complex rotation) by
+    squared L2 (reading R10); the T = ⌈r·N_cached/100⌉ most deviating cached rows (ties: lower index,
+    R13; the forced last row excluded, R11), every dynamic row and the last row are recomputed from the
+    check layer on, attending to the cached K/V of all other rows (explicit position mask).  Returns
+    (logits, selected rows, per-layer linked K)."""
+    import torch
+    m = hf_model(cfg, Wt)
+    tok = np.concatenate([t for _, t in parts]).astype(np.int64)
+    N = len(tok)
+    pos = torch.arange(N)
+    Kc = np.zeros((cfg.n_layers, cfg.n_kv_heads, N, cfg.head_dim))
+    Vc = np.zeros_like(Kc)
+    dyn = np.zeros(N, bool)
+    s = 0
+    for kind, t in parts:
+        if kind == "tokens":
+            dyn[s:s + len(t)] = True
+        else:
+            with torch.no_grad():
+                alone = m(torch.from_numpy(t.astype(np.int64))[None], use_cache=True).past_key_values
+            for l in range(cfg.n_layers):
+                Kc[l, :, s:s + len(t)] = _complex_rebase(alone.layers[l].keys[0].numpy(), s, cfg)
+                Vc[l, :, s:s + len(t)] = alone.layers[l].values[0].numpy()
+        s += len(t)
+    rot = m.model.rotary_emb
+
+    def mask(qpos, kpos):
+        ok = kpos[None, :] <= qpos[:, None]
+        return torch.where(ok, 0.0, float("-inf")).to(torch.float64)[None, None]
+
+    K = Kc.copy()
+    with torch.no_grad():
+        h = m.model.embed_tokens(torch.from_numpy(tok)[None])
+        sel = np.arange(N)
+        for l, layer in enumerate(m.model.layers):
+            if l == check_layer:
+                x = layer.input_layernorm(h)
+                cs, sn = rot(x, pos[None])
+                k_new = layer.self_attn.k_proj(x).view(1, N, cfg.n_kv_heads, cfg.head_dim).transpose(1, 2)
+                v_new = layer.self_attn.v_proj(x).view(1, N, cfg.n_kv_heads, cfg.head_dim).transpose(1, 2)
+                _, k_new = _hf_rope(k_new, k_new, cs, sn)
+                dev = ((k_new[0].numpy() - Kc[l]) ** 2).sum(axis=(0, 2)) + ((v_new[0].numpy() - Vc[l]) ** 2).sum(axis=(0, 2))
+                n_cached = int((~dyn).sum())
+                T = (r_pct * n_cached + 99) // 100
+                cand = sorted((i for i in range(N) if not dyn[i] and i != N - 1), key=lambda i: (-dev[i], i))[:T]
+                sel = np.asarray(sorted(set(cand) | set(np.nonzero(dyn)[0].tolist()) | {N - 1}))
+                h = h[:, torch.from_numpy(sel)]
+            unsel = np.setdiff1d(np.arange(N), sel)
+            cache = _PrefixKV(torch.from_numpy(Kc[l][:, unsel][None].copy()), torch.from_numpy(Vc[l][:, unsel][None].copy()))
+            qpos = pos[torch.from_numpy(sel)]
+            cs, sn = rot(h, qpos[None])
+            x = layer.input_layernorm(h)
+            kq = layer.self_attn.k_proj(x).view(1, len(sel), cfg.n_kv_heads, cfg.head_dim).transpose(1, 2)
+            _, kq = _hf_rope(kq, kq, cs, sn)
+            K[l][:, sel] = kq[0].numpy()
+            h = layer(h, attention_mask=mask(qpos, torch.cat([pos[torch.from_numpy(unsel)], qpos])), past_key_values=cache,
+                      position_embeddings=(cs, sn))
+            if isinstance(h, tuple):
+                h = h[0]
+        logits = m.lm_head(m.model.norm(h))[0, -1].numpy()
+    return logits, sel, [K[l].transpose(1, 0, 2) for l in range(cfg.n_layers)]
+
+
+def _hf_rope(q, k, cos, sin):
+    from transformers.models.llama.modeling_llama import apply_rotary_pos_emb
+    return apply_rotary_pos_emb(q, k, cos, sin)
+
+
+@pytest.mark.parametrize("cfg", [sg.TINY, sg.TINY_GQA, sg.TINY_D128], ids=lambda c: c.name)
+@pytest.mark.parametrize("r_pct", [15, 40])
+def test_C19_cacheblend_equals_hf_layerwise_construction(cfg, r_pct):
+    """Pins CacheBlend with a real selection (previously 'parity unpinned'): the selected set, the
+    logits and every layer's linked K equal the HF construction above, canonical and permuted orders."""
+    w = sg.cfg1(model=cfg)
+    Wt = M.Weights(cfg)
+    store = P.Store(Wt)
+    ids = store.compile(w.chunks)
+    q = w.requests[0][-1].tokens
+    for order in ([0, 1, 2, "q"], ["q", 2, 0, 1]):
+        segs = [("tokens", q) if c == "q" else ("cached", ids[c]) for c in order]
+        parts = [("tokens", q) if c == "q" else ("chunk", w.chunks[c]) for c in order]
+        r = P.link(store, segs, f"cacheblend:{r_pct}")
+        logits, sel, K = hf_cacheblend(cfg, Wt, parts, r_pct)
+        assert np.array_equal(r.sel_per_layer[-1], sel)
+        assert 0 < len(sel) < r.plan.N
+        assert rel(r.logits, logits) < HF_TOL
+        for l in range(cfg.n_layers):
+            assert rel(r.K[l], K[l]) < HF_TOL, l
