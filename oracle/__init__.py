@@ -12,9 +12,11 @@ Plain, slow, obviously-correct NumPy float64:
   * ``oracle.pic``   — compile, assemble/plan, link for Naive / FR / LegoLink-k /
     CacheBlend-r, the paged-layout (block allocator / slot map) model.
 
-Pins: tests/test_oracle_pins.py (C1–C13 of SURVEY §8(c).4).  Functions with no pin
-other than their own construction are marked "parity unpinned" below and in
-DESIGN.md §3: LegoLink for 0 < k < n_c and CacheBlend with a non-trivial selection
-(bracketed by pins C4/C5/C6/C9/C11 but without a closed form).
+Pins: tests/test_oracle_pins.py (C1–C13 of SURVEY §8(c).4, plus C14–C19).  LegoLink for
+0 < k < n_c and CacheBlend with a non-trivial selection have no closed form in the paper;
+they are pinned by independent constructions from HuggingFace Llama's own forward, KV cache
+and decoder layers (C18: sequential forwards over a cache of re-based standalone-prefill
+chunk KV; C19: layer-wise recomputation under an explicit position mask, the selection rule
+restated), so no oracle function is left "parity unpinned".
 """
 from . import model, pic  # noqa: F401
