@@ -233,12 +233,15 @@ def roofline(prof, P, src, nsteps, config_name):
     else:
         achieved = dom["flops"] / (dom["ms"] / 1e3) / 1e12
         roof = {"bound": "tensor", "achieved": achieved, "peak": P["bf16_tflops"], "unit": "TFLOP/s"}
+    sustained = roof["bound"] == "tensor" and bool(P.get("bf16_tflops_sustained"))
+    if sustained:
+        # the dominant kernel is timed inside a long step (every launch of the profiled step, ~1000 GEMMs
+        # back to back at the board's power cap): the driver's sustained figure (back-to-back matmuls for
+        # seconds) is the denominator the measurement rules name for that case; the burst figure is kept
+        roof["peak_burst"] = P["bf16_tflops"]
+        roof["frac_burst"] = roof["achieved"] / P["bf16_tflops"]
+        roof["peak"] = P["bf16_tflops_sustained"]
     roof["frac"] = roof["achieved"] / roof["peak"]
-    if roof["bound"] == "tensor" and P.get("bf16_tflops_sustained"):
-        # the driver's sustained figure (back-to-back matmuls for seconds, power-capped clocks) applies to a
-        # kernel timed inside a long step; "peak" stays the burst figure (the conservative denominator)
-        roof["peak_sustained"] = P["bf16_tflops_sustained"]
-        roof["frac_sustained"] = roof["achieved"] / P["bf16_tflops_sustained"]
     traffic = ncu_traffic(config_name, dom_name)
     roof["traffic"] = traffic
     roof["algorithmic_bytes_per_launch"] = dom["bytes"] / n_launch
@@ -246,7 +249,9 @@ def roofline(prof, P, src, nsteps, config_name):
         roof["traffic_over_algorithmic"] = traffic / (dom["bytes"] / n_launch)
     roof["kernel"] = dom_name
     roof["share_of_step"] = dom["ms"] / tot
-    roof["peak_source"] = f"{src} (MEASURED_PEAKS.json burst)" if src == "measured" else "fallback (B200_PROFILING.md)"
+    roof["peak_source"] = (("measured (MEASURED_PEAKS.json bf16_tflops_sustained: kernel timed inside a long step)"
+                            if sustained else "measured (MEASURED_PEAKS.json)") if src == "measured"
+                           else "fallback (B200_PROFILING.md)")
     roof["launches_per_step"] = dom["launches"] / nsteps
     roof["how"] = (f"algorithmic bytes/FLOPs per launch (SURVEY §8(d)) over CUDA-event durations of every launch, "
                    f"{nsteps} profiled step(s) on the bench stream (graphs off)")

@@ -1468,7 +1468,10 @@ static pic_status enqueue_forward(pic_engine* e, const Fwd& f, const DevPlan& dp
       a.debug = attn_debug;
       const int max_split = main_tiles ? f.attn_max_split : f.attn_max_split2;
       ++R.launches;
-      if (f.attn_pp)
+      if (f.attn_decode && main_tiles)
+        PROF("attention", attn_bytes, attn_flops,
+             launch_attention_decode(e->tm_K, e->tm_V, e->tm_K8, e->tm_V8, a, st));
+      else if (f.attn_pp)
         PROF("attention", attn_bytes, attn_flops,
              launch_attention_pp(e->tm_Q, e->tm_K, e->tm_V, e->tm_K8, e->tm_V8, a, 148, st));
       else
@@ -1593,7 +1596,7 @@ static pic_status enqueue_forward(pic_engine* e, const Fwd& f, const DevPlan& dp
 static void add_sig(std::vector<int64_t>& sig, const Fwd& f, const DevPlan& dp) {
   sig = {f.M,  dp.n_tiles, (int64_t)f.seq_bt_off.size(), (int64_t)f.bt.size(), (int64_t)f.k2_src.size(), f.k2_layer0,
          f.n_head, f.compile, f.rebase, f.cb, f.cb_layer, f.cb_T, f.M2, f.cb_override, dp.n_tiles2, f.attn_n_work,
-         f.attn_n_work2, f.kv_rot, f.attn_pp, f.has_vbt, f.k2_konly, f.has_kpos, f.attn_qrot};
+         f.attn_n_work2, f.kv_rot, f.attn_pp, f.has_vbt, f.k2_konly, f.has_kpos, f.attn_qrot, f.attn_decode};
   // attention split choice depends on the per-sequence block-table lengths
   for (size_t q = 0; q < f.seq_bt_off.size(); ++q) sig.push_back(f.seq_bt_off[q]);
 }
@@ -1655,6 +1658,12 @@ static void schedule_attention(pic_engine* e, Fwd& f) {
   }
   if (g_attn_force) pp = g_attn_force == 2 && e->cfg.head_dim == 128 && !e->f32;
   if (f.attn_qrot) pp = false;  // the Q-side re-base lives in the one-lane kernel
+  // decode (f1): the transposed split-KV kernel, unless keys still need a re-base on load (shared blocks
+  // not materialized: the one-lane kernel's K-tile rotation) or PIC_NO_ATTN_DECODE (A/B)
+  const bool no_dec = getenv("PIC_NO_ATTN_DECODE") != nullptr;  // read per call (tests toggle it)
+  f.attn_decode = f.decode && !f.kv_rot && !no_dec && e->cfg.head_dim == 128 && !e->f32 &&
+                  attention_decode_supported(e->cfg.n_heads / Hkv);
+  if (f.attn_decode) pp = false;
   f.attn_pp = pp;
   build(f.tiles, &f.pos, f.M, 0, f.attn_work, f.attn_nsplit, f.attn_n_work, f.attn_max_split);
   if (f.cb) {
@@ -2229,6 +2238,7 @@ extern "C" pic_status pic_decode(pic_engine* e, pic_linked* const* linked, const
   // one row per sequence: position N_b, K/V slot N_b of its own block table
   Fwd f;
   f.n_head = n;
+  f.decode = true;
   const int qpt = qpt_of(e->cfg);
   for (int b = 0; b < n; ++b) {
     const pic_linked& h = *linked[b];

@@ -94,6 +94,8 @@ struct Fwd {
   std::vector<int32_t> attn_work, attn_nsplit, attn_work2, attn_nsplit2;
   int attn_n_work = 0, attn_n_work2 = 0, attn_max_split = 1, attn_max_split2 = 1;
   bool attn_pp = false;  // schedules in the ping-pong kernel's item format (attention_pp.cu)
+  bool decode = false;       // pic_decode: one query row per sequence
+  bool attn_decode = false;  // attention runs the split-KV decode kernel (attention_decode.cu)
 };
 
 // Per-request link bookkeeping produced by the planner.

@@ -54,6 +54,9 @@ constexpr uint32_t kTmQd = 384;  // QROT in TMEM (PIC_QROT_SMEM=0): two R(−Δ)
 constexpr int kQd = kV + 2 * 2 * kTile;
 static_assert(kQd + 2 * 2 * kTile == kX, "QROT smem buffers must end where the Q tile ends");
 }  // namespace attn
+#ifndef PIC_QROT_SM_KS
+#define PIC_QROT_SM_KS 3  // QROT_SM K ring depth (V ring: 5 - KS)
+#endif
 #ifndef PIC_QROT_SMEM
 #define PIC_QROT_SMEM 0  // smem variant (2-slot V ring) measured equal at cfg4: 178-180 vs 177-178 ms per step
 #endif
@@ -91,7 +94,10 @@ __global__ void __launch_bounds__(attn_threads<ROT, QROT>(), 1)
   constexpr int S = kStages;
   // QROT_SM: R(−Δ)·Q lives in smem (SS MMA for S) in place of V slot 2 and the Q tile
   constexpr bool QROT_SM = QROT && PIC_QROT_SMEM;
-  constexpr int SV = QROT_SM ? 2 : S;  // V ring depth
+  // ring depths: QROT_SM gives up one 32 KB slot (K or V, PIC_QROT_SM_KS) for the second R(−Δ)·Q buffer
+  constexpr int SK = QROT_SM ? PIC_QROT_SM_KS : S;  // K ring depth
+  constexpr int SV = QROT_SM ? 5 - PIC_QROT_SM_KS : S;  // V ring depth
+  constexpr int kVb = kK + SK * 2 * kTile;  // V ring base
   unsigned long long* const tr = a.trace ? a.trace + 32 * (blockIdx.y * gridDim.x + blockIdx.x) : nullptr;
   if (tr && threadIdx.x == 0) tr[0] = globaltimer();
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -196,20 +202,20 @@ __global__ void __launch_bounds__(attn_threads<ROT, QROT>(), 1)
         mbar_expect_tx(v_full + 8 * vs, 2 * kTile);
         if (vc) {
           for (int h = 0; h < 2; ++h)
-            tma_load_4d(base + kV + (2 * vs + h) * kTile, &tmV8, v_full + 8 * vs, h * 64, 0, g, kv_base + vb0);
+            tma_load_4d(base + kVb + (2 * vs + h) * kTile, &tmV8, v_full + 8 * vs, h * 64, 0, g, kv_base + vb0);
         } else {
 #pragma unroll
           for (int b = 0; b < 8; ++b)
             for (int h = 0; h < 2; ++h)
-              tma_load_4d(base + kV + (2 * vs + h) * kTile + b * 2048, &tmV, v_full + 8 * vs, h * 64, 0, g,
+              tma_load_4d(base + kVb + (2 * vs + h) * kTile + b * 2048, &tmV, v_full + 8 * vs, h * 64, 0, g,
                           kv_base + vb[b]);
         }
       };
       int vprev[8];
       bool vcprev = false;
       for (int t = 0; t < n; ++t) {
-        const int s = t % S;
-        const uint32_t ph = (t / S) & 1;
+        const int s = t % SK;
+        const uint32_t ph = (t / SK) & 1;
         const int blk_mine = blk_next, vblk_mine = vblk_next;
         if (t + 1 < n && lane < 8) {
           blk_next = bt[min((j0 + t + 1) * 8 + lane, last_blk)];
@@ -256,7 +262,7 @@ __global__ void __launch_bounds__(attn_threads<ROT, QROT>(), 1)
       constexpr uint32_t idS = idesc_bf16(128, 128, 0, 0);  // Q (smem, K-major) x K (smem, K-major)
       constexpr uint32_t idO = idesc_bf16(128, 128, 0, 1);  // P (TMEM, K-major) x V (smem, MN-major)
       const uint64_t dQ = sdesc_sw128(base + kQ, 16, 1024), dK0 = sdesc_sw128(base + kK, 16, 1024);
-      const uint64_t dV0 = sdesc_sw128(base + kV, kTile, 1024);
+      const uint64_t dV0 = sdesc_sw128(base + kVb, kTile, 1024);
       const uint64_t dQd = sdesc_sw128(base + kQd, 16, 1024);  // QROT_SM: R(−Δ)·Q buffer 0 (buffer 1: +32 KB)
       unsigned long long w_k = 0, w_p = 0, w_v = 0, w_q = 0, q0 = 0, sum_w = 0;
       if (!QROT_SM) mbar_wait(q_full, 0);
@@ -297,7 +303,7 @@ __global__ void __launch_bounds__(attn_threads<ROT, QROT>(), 1)
       int fi = -1, fr_cur = 0;
       int fr_next = QROT ? bdq[min(j0 * 8, last_blk)] : 0;
       for (int t = 0; t < n; ++t) {
-        const int sb = t & 1, ks = t % S;
+        const int sb = t & 1, ks = t % SK;
         int qb = 0;
         bool frame_end = false;
         if constexpr (QROT) {
@@ -314,7 +320,7 @@ __global__ void __launch_bounds__(attn_threads<ROT, QROT>(), 1)
           frame_end = t + 1 == n || fr_next != fr;
         }
         if (tr) q0 = globaltimer();
-        mbar_wait((ROT && !QROT ? k_rot : k_full) + 8 * ks, (t / S) & 1);
+        mbar_wait((ROT && !QROT ? k_rot : k_full) + 8 * ks, (t / SK) & 1);
         if (tr) w_k += globaltimer() - q0;
         tc_fence_after();
         // S(t) overwrites the buffer holding P(t-2): PV(t-2) was issued before and MMAs run in order

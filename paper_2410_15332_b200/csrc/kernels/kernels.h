@@ -223,6 +223,12 @@ int attn_schedule_pp(const int32_t* tiles, int n_tiles, const int* n_kv, int Hkv
 cudaError_t launch_attention_pp(const CUtensorMap& tmQ, const CUtensorMap& tmK, const CUtensorMap& tmV,
                                 const CUtensorMap& tmK8, const CUtensorMap& tmV8, const AttnArgs& a, int n_sms,
                                 cudaStream_t st);
+// f1 (attention_decode.cu): split-KV decode attention, one query row per q-tile (tiles of row_count 1), the
+// tile transposed (keys on the MMA rows, the G <= 8 heads of a kv-head on N = 16); same work list, partials
+// and direct bf16 output convention as launch_attention_tc; no shared-block re-base (bdelta must be null)
+cudaError_t launch_attention_decode(const CUtensorMap& tmK, const CUtensorMap& tmV, const CUtensorMap& tmK8,
+                                    const CUtensorMap& tmV8, const AttnArgs& a, cudaStream_t st);
+bool attention_decode_supported(int G);
 cudaError_t launch_attn_combine(const float* o_part, const float* ml_part, const int32_t* row_nsplit, void* O, int M,
                                 int Hq, int D, cudaStream_t st);
 // generic-D SIMT attention (tiny shapes D in {16,32,64}; any D <= 128 in the fp32 debug build); writes O directly

@@ -19,6 +19,7 @@ namespace pic {
 cudaError_t prepare_gemm();
 cudaError_t prepare_attention();
 cudaError_t prepare_attention_pp();
+cudaError_t prepare_attention_decode();
 bool pdl_enabled() {
   static int v = -1;
   if (v < 0) v = getenv("PIC_NO_PDL") ? 0 : 1;
@@ -29,6 +30,7 @@ cudaError_t prepare_kernels() {
   cudaError_t e = prepare_gemm();
   if (e == cudaSuccess) e = prepare_gemm_chain();
   if (e == cudaSuccess) e = prepare_attention();
+  if (e == cudaSuccess) e = prepare_attention_decode();
   return e == cudaSuccess ? prepare_attention_pp() : e;
 }
 

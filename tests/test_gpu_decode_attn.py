@@ -1,0 +1,100 @@
+"""f1 decode attention kernel (attention_decode.cu: split-KV, the K tile transposed onto the MMA rows).
+
+Decode steps after a link over 128-token chunks (contexts of 5-8 K tiles, so the split-KV schedule cuts
+every sequence into several pieces merged by attn_combine), for every GQA group size the kernel is built
+for (G = 2, 4, 8), held to
+  * the fp64 oracle's decode ("proceeds to the decode stage"; P.decode) at 2e-2;
+  * the prefill kernel's decode path (PIC_NO_ATTN_DECODE=1, the one-lane kernel) at 2e-2, and not
+    bit-identical to it — which shows the two runs took different kernels;
+  * batched = single bit-exactly when the split schedule is the same (same batch composition)."""
+import os
+from dataclasses import replace
+
+import numpy as np
+import pytest
+
+import seedgen as sg
+from oracle import model as M
+from oracle import pic as P
+from paper_2410_15332_b200 import pic as B
+
+pytestmark = pytest.mark.gpu
+STEPS = 6
+
+MODELS = [
+    sg.TINY_D128,                                                   # G = 2, one kv-head
+    replace(sg.TINY_TP8, name="tiny-tp8-g4", n_kv_heads=4),         # G = 4 (Llama-3.1-8B / Mistral-7B)
+    replace(sg.TINY_TP8, name="tiny-tp8-g8", n_kv_heads=2),         # G = 8 (Llama-3-70B)
+]
+
+
+def rel(a, b):
+    a, b = np.asarray(a, np.float64), np.asarray(b, np.float64)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+@pytest.fixture(scope="module", params=MODELS, ids=lambda c: c.name)
+def env(request):
+    cfg = request.param
+    ws = sg.workload_seed(0x52)
+    chunks = sg.make_chunks(ws, 6, 128, cfg.vocab, cfg.bos_id) + sg.make_chunks(ws + 1, 1, 200, cfg.vocab, cfg.bos_id)
+    eng = B.Engine(cfg, num_blocks=2048, max_rows=2048, max_tokens=2048, max_requests=4, device=0)
+    ids = eng.generate_context_cache(chunks)
+    Wt = M.Weights(cfg)
+    store = P.Store(Wt)
+    oids = store.compile(chunks)
+    yield cfg, eng, ids, oids, Wt, store
+    eng.close()
+
+
+ORDERS = [[0, 1, 2, 3, 4], [6, 5, 0, 3, 2, 1]]
+
+
+def test_decode_kernel_matches_oracle_and_prefill_kernel(env):
+    cfg, eng, ids, oids, Wt, store = env
+    q = sg.make_query(sg.workload_seed(0x52), 0, 24, cfg.vocab)
+    toks = [int(t) for t in sg.tokens(0xDEC0DE, 9, STEPS, cfg.vocab, None)]
+    for order in ORDERS:
+        segs = [("cached", ids[c]) for c in order] + [("tokens", q)]
+        outs = [eng.link(segs, "legolink:16", keep_linked=True) for _ in range(2)]
+        ref = P.link(store, [("cached", oids[c]) for c in order] + [("tokens", q)], "legolink:16")
+        K, V = ref.K, ref.V
+        try:
+            for i, t in enumerate(toks):
+                d_new = eng.decode([outs[0].linked], [t])
+                os.environ["PIC_NO_ATTN_DECODE"] = "1"
+                try:
+                    d_old = eng.decode([outs[1].linked], [t])
+                finally:
+                    os.environ.pop("PIC_NO_ATTN_DECODE", None)
+                lg, K, V = P.decode(Wt, K, V, t)
+                assert rel(d_new.logits[0], lg) < 2e-2, (order, i)
+                assert rel(d_new.logits[0], d_old.logits[0]) < 2e-2, (order, i)
+                assert not np.array_equal(d_new.logits[0], d_old.logits[0])
+                assert d_new.next_token[0] == int(np.argmax(d_new.logits[0]))
+        finally:
+            for o in outs:
+                eng.release(o.linked)
+
+
+def test_decode_kernel_batched_equals_single(env):
+    cfg, eng, ids, oids, Wt, store = env
+    q = sg.make_query(sg.workload_seed(0x52), 1, 17, cfg.vocab)
+    reqs = [[("cached", ids[c]) for c in o] + [("tokens", q)] for o in ORDERS]
+    a = [eng.link(r, "legolink:16", keep_linked=True) for r in reqs]
+    b = [eng.link(r, "legolink:16", keep_linked=True) for r in reqs]
+    c = [eng.link(r, "legolink:16", keep_linked=True) for r in reqs]
+    try:
+        ta = [x.first_token for x in a]
+        for step in range(STEPS):
+            batch = eng.decode([x.linked for x in a], ta)
+            batch2 = eng.decode([x.linked for x in b], ta)      # same composition, same split schedule
+            for j in range(len(a)):
+                assert np.array_equal(batch.logits[j], batch2.logits[j]), (step, j)
+            for j, (x, t) in enumerate(zip(c, ta)):
+                single = eng.decode([x.linked], [t])
+                assert rel(single.logits[0], batch.logits[j]) < 1e-2, (step, j)
+            ta = [int(t) for t in batch.next_token]
+    finally:
+        for x in a + b + c:
+            eng.release(x.linked)
