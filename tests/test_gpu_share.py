@@ -6,6 +6,7 @@ is held to the oracle by test_gpu_link / test_gpu_decode; one oracle check is re
 
 Also: block accounting (only fresh blocks are taken from the pool; shared blocks are reference
 counted, so expiring a chunk under a live linked cache keeps its rows) and the fp32 debug build."""
+import os
 from dataclasses import replace
 
 import numpy as np
@@ -190,6 +191,18 @@ def test_shared_link_matches_oracle(setup):
         s.eng.release(out.linked)
 
 
+class prefill_kernel_decode:
+    """Decode steps through the prefill attention kernel (PIC_NO_ATTN_DECODE=1): a cache that still
+    re-bases keys on load always decodes there, so bit-identity against a copy-path cache is a property
+    of that one kernel (the transposed decode kernel, attention_decode.cu, serves caches without Δ)."""
+
+    def __enter__(self):
+        os.environ["PIC_NO_ATTN_DECODE"] = "1"
+
+    def __exit__(self, *exc):
+        os.environ.pop("PIC_NO_ATTN_DECODE", None)
+
+
 def test_shared_decode_bit_identical(setup):
     s = setup
     segs = s.w.requests[0]
@@ -197,8 +210,9 @@ def test_shared_decode_bit_identical(setup):
     try:
         toks = [5, 17, 99, 3, 250, 7, 11, 13, 2, 1, 0, 8, 9, 10, 12, 14, 15, 16, 18, 19]
         for t in toks:  # crosses a block boundary (N = 112 -> 132)
-            a = s.eng.decode([hs[0]], [t])
-            b = s.eng.decode([hs[1]], [t])
+            with prefill_kernel_decode():
+                a = s.eng.decode([hs[0]], [t])
+                b = s.eng.decode([hs[1]], [t])
             assert np.array_equal(a.logits, b.logits)
         for l in range(s.cfg.n_layers):
             ka, va = s.eng.linked_export(hs[0], l)
@@ -330,9 +344,14 @@ def test_chunkframe_materialize_accounting(setup):
             k, v = s.eng.linked_export(hb, l)
             assert np.array_equal(k, exp0[l][0]) and np.array_equal(v, exp0[l][1]), l
         for t in (5, 17, 99):
-            a = s.eng.decode([ha], [t])
-            b = s.eng.decode([hb], [t])
+            with prefill_kernel_decode():
+                a = s.eng.decode([ha], [t])
+                b = s.eng.decode([hb], [t])
             assert np.array_equal(a.logits, b.logits)
+        c = s.eng.decode([hb], [7])                               # materialized: the decode kernel may serve it
+        with prefill_kernel_decode():
+            d = s.eng.decode([ha], [7])
+        assert rel(c.logits, d.logits) < 2e-2
     finally:
         s.eng.release(ha)
         s.eng.release(hb)
