@@ -1468,9 +1468,13 @@ static pic_status enqueue_forward(pic_engine* e, const Fwd& f, const DevPlan& dp
       a.debug = attn_debug;
       const int max_split = main_tiles ? f.attn_max_split : f.attn_max_split2;
       ++R.launches;
+      // chunk-frame links: the persistent Q-side re-base kernel (PIC_NO_ATTN_PERSIST=1: one CTA per item, A/B)
+      const bool qp = a.qrot && getenv("PIC_NO_ATTN_PERSIST") == nullptr;
       if (f.attn_decode && main_tiles)
         PROF("attention", attn_bytes, attn_flops,
              launch_attention_decode(e->tm_K, e->tm_V, e->tm_K8, e->tm_V8, a, st));
+      else if (qp)
+        PROF("attention", attn_bytes, attn_flops, launch_attention_qp(e->tm_Q, e->tm_K, e->tm_V, e->tm_K8, e->tm_V8, a, 148, st));
       else if (f.attn_pp)
         PROF("attention", attn_bytes, attn_flops,
              launch_attention_pp(e->tm_Q, e->tm_K, e->tm_V, e->tm_K8, e->tm_V8, a, 148, st));

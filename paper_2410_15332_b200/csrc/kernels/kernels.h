@@ -229,6 +229,12 @@ cudaError_t launch_attention_pp(const CUtensorMap& tmQ, const CUtensorMap& tmK, 
 cudaError_t launch_attention_decode(const CUtensorMap& tmK, const CUtensorMap& tmV, const CUtensorMap& tmK8,
                                     const CUtensorMap& tmV8, const AttnArgs& a, cudaStream_t st);
 bool attention_decode_supported(int G);
+// a6 for chunk-frame links (attention_qp.cu): the one-lane Q-side re-base kernel (attn_tc_kernel<G, true,
+// true>) made persistent — min(n_work·Hkv, n_sms) CTAs walk the work list with every ring running across
+// items; same arithmetic, bit for bit
+cudaError_t launch_attention_qp(const CUtensorMap& tmQ, const CUtensorMap& tmK, const CUtensorMap& tmV,
+                                const CUtensorMap& tmK8, const CUtensorMap& tmV8, const AttnArgs& a, int n_sms,
+                                cudaStream_t st);
 cudaError_t launch_attn_combine(const float* o_part, const float* ml_part, const int32_t* row_nsplit, void* O, int M,
                                 int Hq, int D, cudaStream_t st);
 // generic-D SIMT attention (tiny shapes D in {16,32,64}; any D <= 128 in the fp32 debug build); writes O directly

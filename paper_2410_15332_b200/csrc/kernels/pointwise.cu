@@ -20,6 +20,7 @@ cudaError_t prepare_gemm();
 cudaError_t prepare_attention();
 cudaError_t prepare_attention_pp();
 cudaError_t prepare_attention_decode();
+cudaError_t prepare_attention_qp();
 bool pdl_enabled() {
   static int v = -1;
   if (v < 0) v = getenv("PIC_NO_PDL") ? 0 : 1;
@@ -31,6 +32,7 @@ cudaError_t prepare_kernels() {
   if (e == cudaSuccess) e = prepare_gemm_chain();
   if (e == cudaSuccess) e = prepare_attention();
   if (e == cudaSuccess) e = prepare_attention_decode();
+  if (e == cudaSuccess) e = prepare_attention_qp();
   return e == cudaSuccess ? prepare_attention_pp() : e;
 }
 

@@ -229,3 +229,33 @@ def test_fullsize_chunkframe_qrot_link(which):
                 assert rel(f32(vb), f32(va)) < 2e-2, l
     finally:
         eng.close()
+
+
+def test_fullsize_qrot_persistent_bit_identical():
+    """cfg4 (4 requests, full depth, eager): the persistent QROT attention kernel (default for kv_share 3)
+    equals the one-CTA-per-item QROT kernel bit for bit (logits, sampled layers' linked K/V)."""
+    import os
+    w = sg.cfg4(n_requests=4)
+    m = w.model
+    Ns = [sum(len(w.chunks[s.chunk]) if s.cached else len(s.tokens) for s in r) for r in w.requests]
+    eng = B.Engine(m, num_blocks=(sum(len(c) for c in w.chunks) + 3 * sum(Ns)) // 16 + 64, max_rows=4096,
+                   max_tokens=max(Ns) + 16, max_requests=len(w.requests), device=0)
+    try:
+        ids = eng.generate_context_cache(w.chunks)
+        reqs = [[("cached", ids[s.chunk]) if s.cached else ("tokens", s.tokens) for s in r] for r in w.requests]
+        outs = []
+        for off in (False, True):
+            if off:
+                os.environ["PIC_NO_ATTN_PERSIST"] = "1"
+            try:
+                outs.append(eng.link_batch(reqs, w.alg, keep_linked=True, kv_share=3, use_graph=False))
+            finally:
+                os.environ.pop("PIC_NO_ATTN_PERSIST", None)
+        for a, b in zip(*outs):
+            assert np.array_equal(a.logits, b.logits)
+            for l in (0, m.n_layers - 1):
+                ka, va = eng.linked_export(a.linked, l)
+                kb, vb = eng.linked_export(b.linked, l)
+                assert np.array_equal(ka, kb) and np.array_equal(va, vb), l
+    finally:
+        eng.close()

@@ -95,3 +95,32 @@ def test_qrot_batch_matches_oracle(env):
     for o, b in zip(ORDERS[:2], batch):
         ref = P.link(store, [("cached", oids[c]) for c in o] + [("tokens", q)], "legolink:16")
         assert rel(b.logits, ref.logits) < 2e-2
+
+
+def _eager_links(eng, reqs, persistent):
+    if not persistent:
+        os.environ["PIC_NO_ATTN_PERSIST"] = "1"
+    try:
+        return eng.link_batch(reqs, "legolink:16", kv_share=3, use_graph=False, keep_linked=True)
+    finally:
+        os.environ.pop("PIC_NO_ATTN_PERSIST", None)
+
+
+def test_qrot_persistent_kernel_bit_identical(env):
+    """attention_qp.cu (the persistent QROT kernel, the default for these links) against the one-CTA-per-item
+    QROT kernel (PIC_NO_ATTN_PERSIST=1): same arithmetic, so logits and every layer's linked K/V are equal bit
+    for bit, for a batch whose items cross CTA boundaries (eager launches: the env switch picks the kernel)."""
+    cfg, eng, ids, oids, store, q = env
+    reqs = [[("cached", ids[c]) for c in o] + [("tokens", q)] for o in ORDERS[:2]]
+    a = _eager_links(eng, reqs, True)
+    b = _eager_links(eng, reqs, False)
+    try:
+        for x, y in zip(a, b):
+            assert np.array_equal(x.logits, y.logits)
+            for l in range(cfg.n_layers):
+                kx, vx = eng.linked_export(x.linked, l)
+                ky, vy = eng.linked_export(y.linked, l)
+                assert np.array_equal(kx, ky) and np.array_equal(vx, vy), l
+    finally:
+        for o in a + b:
+            eng.release(o.linked)
