@@ -46,6 +46,16 @@ static_assert(kSmem <= 232448, "attention smem over the 227 KB limit");
 constexpr uint32_t kTmS = 0;    // S double buffer [0, 256); P(t) (bf16 pairs) overwrites S(t)
 constexpr uint32_t kTmO = 256;  // O accumulator [256, 384)
 constexpr uint32_t kTmQd = 384;  // two R(−Δ)·Q buffers (bf16 pairs, 64 columns each) [384, 512)
+// PIC_QP_SMEMQ=1: R(−Δ)·Q in shared memory instead (S = Q_Δ·Kᵀ an SS MMA, no TS A-operand reads competing
+// with the softmax's TMEM loads): the two buffers take V slot 2 and the Q tile, the rotation warps keep the
+// item's q rows in registers (loaded once per item from global Q) and write every frame's R(−Δ)·q as SW128
+#ifndef PIC_QP_SMEMQ
+#define PIC_QP_SMEMQ 0  // measured at cfg4: attention 181-185 vs 167-168 ms per step (the 2-slot V ring costs more)
+#endif
+constexpr bool kQsm = PIC_QP_SMEMQ != 0;
+constexpr int kSV = kQsm ? 2 : kStages;  // V ring depth
+constexpr int kQd = kV + 2 * 2 * kTile;  // kQsm: R(−Δ)·Q buffers [2][two 16 KB halves]
+static_assert(kQd + 2 * 2 * kTile == kX, "smem R(-Δ)Q buffers must end where the Q tile ends");
 constexpr int kThreads = 448;   // warp 0 TMA, warp 1 MMA, warps 2-9 softmax, warps 10-13 frame rotation
 }  // namespace attnq
 
@@ -189,7 +199,7 @@ __global__ void __launch_bounds__(attnq::kThreads, 1)
       if (item < 0) break;
       const QpItem it = qp_item(a, item);
       if (it.n == 0) continue;
-      if (lane == 0) {
+      if (!kQsm && lane == 0) {
         // Q: 128 MMA rows = (128/G queries) x (G heads of kv-head g), one 3-D box per 64-dim half, once the
         // rotation warps are done with the previous item's frames
         mbar_wait(q_empty, (kq & 1) ^ 1);
@@ -203,7 +213,9 @@ __global__ void __launch_bounds__(attnq::kThreads, 1)
         const int s = kt % S;
         const uint32_t ph = (kt / S) & 1;
         load(&tmK, &tmK8, bt, base + kK + 2 * s * kTile, k_full + 8 * s, k_empty + 8 * s, ph, it.j0 + t, it.last_blk, it.g);
-        load(&tmV, &tmV8, vbt, base + kV + 2 * s * kTile, v_full + 8 * s, v_empty + 8 * s, ph, it.j0 + t, it.last_blk, it.g);
+        const int vs = kt % kSV;
+        load(&tmV, &tmV8, vbt, base + kV + 2 * vs * kTile, v_full + 8 * vs, v_empty + 8 * vs, (kt / kSV) & 1, it.j0 + t,
+             it.last_blk, it.g);
       }
     }
   } else if (warp == 1) {
@@ -211,11 +223,12 @@ __global__ void __launch_bounds__(attnq::kThreads, 1)
     constexpr uint32_t idS = idesc_bf16(128, 128, 0, 0);  // R(−Δ)Q (TMEM, K-major) x K (smem, K-major)
     constexpr uint32_t idO = idesc_bf16(128, 128, 0, 1);  // P (TMEM, K-major) x V (smem, MN-major)
     const uint64_t dK0 = sdesc_sw128(base + kK, 16, 1024), dV0 = sdesc_sw128(base + kV, kTile, 1024);
+    const uint64_t dQd = sdesc_sw128(base + kQd, 16, 1024);  // kQsm: R(−Δ)·Q buffer 0 (buffer 1: +32 KB)
     int kt = 0, fi = -1, kdone = 0;
     auto issue_pv = [&](int u, bool first) {
-      const int pb = u & 1, vs = u % S;
+      const int pb = u & 1, vs = u % kSV;
       mbar_wait(p_full + 8 * pb, (u >> 1) & 1);
-      mbar_wait(v_full + 8 * vs, (u / S) & 1);
+      mbar_wait(v_full + 8 * vs, (u / kSV) & 1);
       if (first && kdone > 0) mbar_wait(o_free, (kdone - 1) & 1);  // previous item's epilogue has read O
       tc_fence_after();
       const uint64_t dv = dV0 + (uint64_t)(vs * (2 * kTile / 16));
@@ -245,7 +258,10 @@ __global__ void __launch_bounds__(attnq::kThreads, 1)
         tc_fence_after();
         // S(kt) overwrites the buffer of P(kt-2): PV(kt-2) was issued before and MMAs run in order
         const uint64_t dk = dK0 + (uint64_t)(ks * (2 * kTile / 16));
-        umma_tsk_k128(tmem + kTmS + sb * 128, tmem + kTmQd + qb * 64, dk, idS, kTile);
+        if constexpr (kQsm)
+          umma_ss_k128(tmem + kTmS + sb * 128, dQd + (uint64_t)(qb * (2 * kTile / 16)), dk, idS, 0, kTile);
+        else
+          umma_tsk_k128(tmem + kTmS + sb * 128, tmem + kTmQd + qb * 64, dk, idS, kTile);
         umma_commit_e(s_full + 8 * sb);
         umma_commit_e(k_empty + 8 * ks);
         if (frame_end) umma_commit_e(qd_empty + 8 * qb);  // this frame's Q buffer may be rewritten
@@ -253,6 +269,75 @@ __global__ void __launch_bounds__(attnq::kThreads, 1)
       }
       issue_pv(kt - 1, it.n == 1);
       ++kdone;
+    }
+  } else if (kQsm && warp >= 10) {
+    // ------------------------------------------------------------------ Q re-base per chunk frame (smem)
+    // Thread u owns the 16-B chunk cc = u & 7 (dims 8cc.. and partners 64+8cc..) of rows rg + 16i, rg = u >> 3:
+    // the item's 8 rows x 2 chunks stay in registers (one global load per item), every frame writes its
+    // R(−Δ)·q chunk pairs in the SW128 K-major layout of the S MMA's A operand.
+    const int u = threadIdx.x - 320;
+    const int cc = u & 7, rg = u >> 3;
+    const uint16_t* Qg = reinterpret_cast<const uint16_t*>(a.Q);
+    int fi = -1;
+    for (int k = 0;; ++k) {
+      const int item = next_item(k);
+      if (item < 0) break;
+      const QpItem it = qp_item(a, item);
+      if (it.n == 0) continue;
+      const int* bdq = a.bdelta + a.seq_bt_off[it.seq];
+      uint4 xa[8], xb[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int r = rg + 16 * i, qi = r / G;
+        xa[i] = xb[i] = make_uint4(0u, 0u, 0u, 0u);
+        if (qi < it.row_count) {
+          const uint4* src = reinterpret_cast<const uint4*>(Qg + ((size_t)(it.row_start + qi) * a.Hq + it.g * G + r % G) * 128 + cc * 8);
+          xa[i] = __ldg(src);
+          xb[i] = __ldg(src + 8);
+        }
+      }
+      int fr_cur = 0;
+      for (int t = 0; t < it.n; ++t) {
+        const int fr = bdq[min((it.j0 + t) * 8, it.last_blk)];
+        if (t > 0 && fr == fr_cur) continue;
+        fr_cur = fr;
+        ++fi;
+        const int ad = fr < 0 ? -fr : fr;
+        const float sg = fr < 0 ? 1.f : -1.f;  // R(−Δ): sin(−Δθ) = −sign(Δ)·sin(|Δ|θ)
+        const float4* cp = reinterpret_cast<const float4*>(a.cos_t + (size_t)ad * 64 + cc * 8);
+        const float4* sp = reinterpret_cast<const float4*>(a.sin_t + (size_t)ad * 64 + cc * 8);
+        const float4 c0 = __ldg(cp), c1 = __ldg(cp + 1), s0 = __ldg(sp), s1 = __ldg(sp + 1);
+        const float cs[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+        const float sn[8] = {sg * s0.x, sg * s0.y, sg * s0.z, sg * s0.w, sg * s1.x, sg * s1.y, sg * s1.z, sg * s1.w};
+        mbar_wait(qd_empty + 8 * (fi & 1), ((fi >> 1) & 1) ^ 1);  // the MMAs of frame fi−2 are done
+        const uint32_t qb = base + kQd + (fi & 1) * (2 * kTile);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          uint4 oa = xa[i], ob = xb[i];
+          if (fr != 0) {
+            uint32_t a4[4] = {xa[i].x, xa[i].y, xa[i].z, xa[i].w}, b4[4] = {xb[i].x, xb[i].y, xb[i].z, xb[i].w};
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) {
+              const float a0 = __uint_as_float(a4[kk] << 16), a1 = __uint_as_float(a4[kk] & 0xFFFF0000u);
+              const float b0 = __uint_as_float(b4[kk] << 16), b1 = __uint_as_float(b4[kk] & 0xFFFF0000u);
+              float ra0, rb0, ra1, rb1;
+              rebase_pair(a0, b0, cs[2 * kk], sn[2 * kk], ra0, rb0);
+              rebase_pair(a1, b1, cs[2 * kk + 1], sn[2 * kk + 1], ra1, rb1);
+              a4[kk] = pack_bf16(ra0, ra1);
+              b4[kk] = pack_bf16(rb0, rb1);
+            }
+            oa = make_uint4(a4[0], a4[1], a4[2], a4[3]);
+            ob = make_uint4(b4[0], b4[1], b4[2], b4[3]);
+          }
+          const int r = rg + 16 * i;
+          const uint32_t off = (uint32_t)(r * 128 + ((cc ^ (r & 7)) << 4));  // SW128: chunk cc of row r
+          sts128(qb + off, oa);
+          sts128(qb + kTile + off, ob);
+        }
+        fence_async_smem();  // generic-proxy smem writes -> visible to the tcgen05.mma operand reads
+        __syncwarp();
+        if (lane == 0) mbar_arrive(qd_full + 8 * (fi & 1));
+      }
     }
   } else if (warp >= 10) {
     // ------------------------------------------------------------------ Q re-base per chunk frame
