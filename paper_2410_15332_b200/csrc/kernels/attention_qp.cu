@@ -39,9 +39,11 @@ constexpr int kQ = kV + kStages * 2 * kTile;  // the item's Q tile (TMA, 2 halve
 constexpr int kX = kQ + 2 * kTile;            // softmax pair exchange: [2 parity][2 halves][128] fp32
 constexpr int kBar = kX + 2 * 2 * 128 * 4;
 constexpr int kIR = 4;  // item-index ring (producer -> the other 13 warps)
-// k/v full/empty; s_full, p_full, o_full, qd_full, qd_empty; o_free; item ring full/empty; q_full, q_empty
-constexpr int kNumBars = 4 * kStages + 2 * 5 + 1 + 2 * kIR + 2;
-constexpr int kSmem = kBar + kNumBars * 8 + 16 + kIR * 4;
+// k/v full/empty; s_full, p_full, o_full, qd_full, qd_empty; o_free; item ring full/empty; q_full, q_empty;
+// l_full
+constexpr int kNumBars = 4 * kStages + 2 * 5 + 1 + 2 * kIR + 2 + 1;
+// + TMEM address slot (16 B), item ring, l_row[128] (the softmax's row sums for the offloaded epilogue)
+constexpr int kSmem = kBar + kNumBars * 8 + 16 + kIR * 4 + 128 * 4 + 16;
 static_assert(kSmem <= 232448, "attention smem over the 227 KB limit");
 constexpr uint32_t kTmS = 0;    // S double buffer [0, 256); P(t) (bf16 pairs) overwrites S(t)
 constexpr uint32_t kTmO = 256;  // O accumulator [256, 384)
@@ -56,6 +58,13 @@ constexpr bool kQsm = PIC_QP_SMEMQ != 0;
 constexpr int kSV = kQsm ? 2 : kStages;  // V ring depth
 constexpr int kQd = kV + 2 * 2 * kTile;  // kQsm: R(−Δ)·Q buffers [2][two 16 KB halves]
 static_assert(kQd + 2 * 2 * kTile == kX, "smem R(-Δ)Q buffers must end where the Q tile ends");
+// The rotation warps (idle once an item's frames are rotated) write unsplit items' O: the softmax warps hand
+// over the row sums and go straight on to the next item instead of waiting for its last PV and storing O
+// (TMEM R(−Δ)Q variant; split items keep the softmax epilogue)
+#ifndef PIC_QP_OFFLOAD
+#define PIC_QP_OFFLOAD 1
+#endif
+constexpr bool kOffload = !kQsm && PIC_QP_OFFLOAD;
 constexpr int kThreads = 448;   // warp 0 TMA, warp 1 MMA, warps 2-9 softmax, warps 10-13 frame rotation
 }  // namespace attnq
 
@@ -110,6 +119,7 @@ __global__ void __launch_bounds__(attnq::kThreads, 1)
   const uint32_t o_free = smem_u32(bars + 4 * S + 10);
   const uint32_t i_full = smem_u32(bars + 4 * S + 11), i_empty = smem_u32(bars + 4 * S + 11 + kIR);
   const uint32_t q_full = smem_u32(bars + 4 * S + 11 + 2 * kIR), q_empty = smem_u32(bars + 4 * S + 12 + 2 * kIR);
+  const uint32_t l_full = smem_u32(bars + 4 * S + 13 + 2 * kIR);
   const int warp = warp_id(), lane = lane_id();
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
@@ -125,7 +135,8 @@ __global__ void __launch_bounds__(attnq::kThreads, 1)
       mbar_init(qd_full + 8 * b, 4);
       mbar_init(qd_empty + 8 * b, 1);
     }
-    mbar_init(o_free, 8);
+    mbar_init(o_free, kOffload ? 12 : 8);  // 8 softmax warps (+ 4 rotation warps when they store O)
+    mbar_init(l_full, 128);                // the hc = 0 softmax threads, one row sum each
     mbar_init(q_full, 1);
     mbar_init(q_empty, 4);  // the 4 rotation warps, after an item's last frame
     for (int s = 0; s < kIR; ++s) {
@@ -144,6 +155,7 @@ __global__ void __launch_bounds__(attnq::kThreads, 1)
   // Dynamic item queue (list order: head-major, longest pieces first — LPT over the 148 CTAs): the producer
   // draws the next item from the global counter and hands it to the other warps through a smem ring; -1 ends.
   int* const iring = reinterpret_cast<int*>(tmem_slot + 4);
+  float* const lrow = reinterpret_cast<float*>(iring + kIR);  // [128] row sums of the item in its epilogue
   auto next_item = [&](int k) -> int {  // consumer warps (whole warp)
     const int sl = k % kIR;
     mbar_wait(i_full + 8 * sl, (k / kIR) & 1);
@@ -340,15 +352,89 @@ __global__ void __launch_bounds__(attnq::kThreads, 1)
       }
     }
   } else if (warp >= 10) {
-    // ------------------------------------------------------------------ Q re-base per chunk frame
+    // ------------------------------------------------------------------ Q re-base per chunk frame + O epilogue
     // Row r of the MMA (query r / G, head g·G + r % G) = TMEM lane r; this warp owns lanes 32·(warp % 4)...
     // For every frame Δ met along an item's KV range (in tile order), write R(−Δ)·q (NeoX pairs (j, j+64),
     // fp32 rotation of the bf16 q, rounded to bf16 — the one-lane QROT arithmetic) into the buffer of the
-    // frame's parity; q comes from global Q (rows of consecutive lanes are consecutive 256-B rows).
+    // frame's parity, from the item's TMA-staged Q tile.  Between the first frame of item k and its later
+    // frames, store the O rows of item k-1 (unsplit items): frame 0 of item k is ready before the MMA warp
+    // needs it, and the softmax warps are already on item k.
     const int qq = warp & 3;
     const int r = qq * 32 + lane;
     const uint32_t lane_addr = (uint32_t)(qq * 32) << 16;
-    int fi = -1, kq = 0;
+    int fi = -1, kq = 0, kt = 0, kd = 0;
+    auto rotate_frame = [&](int fr) {
+      ++fi;
+      const int ad = fr < 0 ? -fr : fr;
+      const float sg = fr < 0 ? 1.f : -1.f;  // R(−Δ): sin(−Δθ) = −sign(Δ)·sin(|Δ|θ)
+      mbar_wait(qd_empty + 8 * (fi & 1), ((fi >> 1) & 1) ^ 1);  // the MMAs of frame fi−2 are done
+      const uint32_t qbase = tmem + lane_addr + kTmQd + (fi & 1) * 64;
+#pragma unroll 1
+      for (int hh = 0; hh < 2; ++hh) {  // dims 32hh..32hh+31 and their partners 64+32hh..
+        uint32_t oa[16], ob[16];
+#pragma unroll
+        for (int cc = 0; cc < 4; ++cc) {
+          const int c = 4 * hh + cc;  // 16-B chunk: dims 8c..8c+7 (half 0) and 64+8c.. (half 1)
+          const uint32_t off = (uint32_t)(r * 128 + ((c ^ (r & 7)) << 4));
+          const uint4 xa = lds128(base + kQ + off), xb = lds128(base + kQ + kTile + off);
+          const float4* cp = reinterpret_cast<const float4*>(a.cos_t + (size_t)ad * 64 + c * 8);
+          const float4* sp = reinterpret_cast<const float4*>(a.sin_t + (size_t)ad * 64 + c * 8);
+          const float4 c0 = __ldg(cp), c1 = __ldg(cp + 1), s0 = __ldg(sp), s1 = __ldg(sp + 1);
+          const float cs[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+          const float sn[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+          const uint32_t a4[4] = {xa.x, xa.y, xa.z, xa.w}, b4[4] = {xb.x, xb.y, xb.z, xb.w};
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const float a0 = __uint_as_float(a4[k] << 16), a1 = __uint_as_float(a4[k] & 0xFFFF0000u);
+            const float b0 = __uint_as_float(b4[k] << 16), b1 = __uint_as_float(b4[k] & 0xFFFF0000u);
+            float ra0, rb0, ra1, rb1;
+            rebase_pair(a0, b0, cs[2 * k], sg * sn[2 * k], ra0, rb0);
+            rebase_pair(a1, b1, cs[2 * k + 1], sg * sn[2 * k + 1], ra1, rb1);
+            oa[cc * 4 + k] = pack_bf16(ra0, ra1);
+            ob[cc * 4 + k] = pack_bf16(rb0, rb1);
+          }
+        }
+        // columns: dims (2k, 2k+1) at column k -> dims 32hh.. at 16hh.., partners at 32 + 16hh..
+        tmem_st16u_wait(qbase + 16 * hh, oa);
+        tmem_st16u_wait(qbase + 32 + 16 * hh, ob);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(qd_full + 8 * (fi & 1));
+    };
+    // O of an unsplit item: its last PV (u_last) has landed and the softmax published the row sums
+    auto epilogue = [&](int row_start, int row_count, int g, int u_last, int kdi) {
+      mbar_wait(l_full, kdi & 1);
+      if (a.row_nsplit[row_start] != 1) {  // split item: the softmax warps store the partials
+        __syncwarp();
+        if (lane == 0) mbar_arrive(o_free);
+        return;
+      }
+      mbar_wait(o_full + 8 * (u_last & 1), (u_last >> 1) & 1);
+      tc_fence_after();
+      const int qi = r / G;
+      const bool valid = qi < row_count;
+      const float inv = 1.f / lrow[r];
+      const size_t orow = ((size_t)(row_start + qi) * a.Hq + g * G + r % G) * 128;
+#pragma unroll 1
+      for (int c = 0; c < 4; ++c) {
+        float ov[32];
+        tmem_ld32(tmem + lane_addr + kTmO + c * 32, ov);  // warp-collective
+        if (c == 3) {  // O fully read: the next item's first PV may overwrite it
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(o_free);
+        }
+        if (valid) {
+          uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(a.O) + orow + c * 32);
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            dst[i] = make_uint4(pack_bf16(ov[8 * i] * inv, ov[8 * i + 1] * inv), pack_bf16(ov[8 * i + 2] * inv, ov[8 * i + 3] * inv),
+                                pack_bf16(ov[8 * i + 4] * inv, ov[8 * i + 5] * inv), pack_bf16(ov[8 * i + 6] * inv, ov[8 * i + 7] * inv));
+        }
+      }
+    };
+    int prv_rs = 0, prv_rc = 0, prv_g = 0, prv_last = -1;  // the previous item's q-tile and last tile
     for (int k = 0;; ++k) {
       const int item = next_item(k);
       if (item < 0) break;
@@ -362,47 +448,22 @@ __global__ void __launch_bounds__(attnq::kThreads, 1)
         const int fr = bdq[min((it.j0 + t) * 8, it.last_blk)];
         if (t > 0 && fr == fr_cur) continue;
         fr_cur = fr;
-        ++fi;
-        const int ad = fr < 0 ? -fr : fr;
-        const float sg = fr < 0 ? 1.f : -1.f;  // R(−Δ): sin(−Δθ) = −sign(Δ)·sin(|Δ|θ)
-        mbar_wait(qd_empty + 8 * (fi & 1), ((fi >> 1) & 1) ^ 1);  // the MMAs of frame fi−2 are done
-        const uint32_t qbase = tmem + lane_addr + kTmQd + (fi & 1) * 64;
-#pragma unroll 1
-        for (int hh = 0; hh < 2; ++hh) {  // dims 32hh..32hh+31 and their partners 64+32hh..
-          uint32_t oa[16], ob[16];
-#pragma unroll
-          for (int cc = 0; cc < 4; ++cc) {
-            const int c = 4 * hh + cc;  // 16-B chunk: dims 8c..8c+7 (half 0) and 64+8c.. (half 1)
-            const uint32_t off = (uint32_t)(r * 128 + ((c ^ (r & 7)) << 4));
-            const uint4 xa = lds128(base + kQ + off), xb = lds128(base + kQ + kTile + off);
-            const float4* cp = reinterpret_cast<const float4*>(a.cos_t + (size_t)ad * 64 + c * 8);
-            const float4* sp = reinterpret_cast<const float4*>(a.sin_t + (size_t)ad * 64 + c * 8);
-            const float4 c0 = __ldg(cp), c1 = __ldg(cp + 1), s0 = __ldg(sp), s1 = __ldg(sp + 1);
-            const float cs[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
-            const float sn[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
-            const uint32_t a4[4] = {xa.x, xa.y, xa.z, xa.w}, b4[4] = {xb.x, xb.y, xb.z, xb.w};
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              const float a0 = __uint_as_float(a4[k] << 16), a1 = __uint_as_float(a4[k] & 0xFFFF0000u);
-              const float b0 = __uint_as_float(b4[k] << 16), b1 = __uint_as_float(b4[k] & 0xFFFF0000u);
-              float ra0, rb0, ra1, rb1;
-              rebase_pair(a0, b0, cs[2 * k], sg * sn[2 * k], ra0, rb0);
-              rebase_pair(a1, b1, cs[2 * k + 1], sg * sn[2 * k + 1], ra1, rb1);
-              oa[cc * 4 + k] = pack_bf16(ra0, ra1);
-              ob[cc * 4 + k] = pack_bf16(rb0, rb1);
-            }
-          }
-          // columns: dims (2k, 2k+1) at column k -> dims 32hh.. at 16hh.., partners at 32 + 16hh..
-          tmem_st16u_wait(qbase + 16 * hh, oa);
-          tmem_st16u_wait(qbase + 32 + 16 * hh, ob);
+        rotate_frame(fr);
+        if (kOffload && prv_last >= 0) {  // after this item's first frame: the previous item's O
+          epilogue(prv_rs, prv_rc, prv_g, prv_last, kd - 1);
+          prv_last = -1;
         }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(qd_full + 8 * (fi & 1));
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(q_empty);  // every frame of this item rotated: the Q tile may be reloaded
+      kt += it.n;
+      prv_rs = it.row_start;
+      prv_rc = it.row_count;
+      prv_g = it.g;
+      prv_last = kt - 1;
+      ++kd;
     }
+    if (kOffload && prv_last >= 0) epilogue(prv_rs, prv_rc, prv_g, prv_last, kd - 1);
   } else {
     // ------------------------------------------------------------------ softmax warps (2-9) + epilogue
     // warps w and w+4 share TMEM lane quarter q = w % 4 (rows 32q..32q+31); warp half hc owns keys
@@ -415,7 +476,7 @@ __global__ void __launch_bounds__(attnq::kThreads, 1)
     const uint32_t oAddr = tmem + lane_addr + kTmO + hc * 64;
     float* xmax = reinterpret_cast<float*>(smem + kX);  // [2 parity][2 halves][128 rows]
     const float sc = a.scale_log2;
-    int kt = 0;
+    int kt = 0, ks = 0;  // tiles and (non-empty) items this CTA's softmax has processed
     for (int k = 0;; ++k) {
       const int item = next_item(k);
       if (item < 0) break;
@@ -508,16 +569,29 @@ __global__ void __launch_bounds__(attnq::kThreads, 1)
         tc_fence_before();
         mbar_arrive(p_full + 8 * sb);
       }
-      // epilogue: the item's last PV, then O
-      const int u = kt - 1;
-      mbar_wait(o_full + 8 * (u & 1), (u >> 1) & 1);
-      tc_fence_after();
       // row sum = both halves' partial sums, through the exchange slot of the next tile's parity, then a
       // second barrier before that slot is reused by the next item's row max
       xmax[((kt & 1) * 2 + hc) * 128 + r] = l;
       named_bar_sync(1 + q, 64);
       const float l_row = l + xmax[((kt & 1) * 2 + (hc ^ 1)) * 128 + r];
       named_bar_sync(1 + q, 64);
+      if (kOffload) {
+        if (hc == 0) {  // hand the row sums to the rotation warps (they read lrow of item ks-1 before o_free)
+          if (ks > 0) mbar_wait(o_free, (ks - 1) & 1);
+          lrow[r] = l_row;
+          mbar_arrive(l_full);
+        }
+      }
+      ++ks;
+      if (kOffload && direct) {  // the rotation warps store O; this warp never reads it again
+        __syncwarp();
+        if (lane == 0) mbar_arrive(o_free);
+        continue;
+      }
+      // epilogue: the item's last PV, then O
+      const int u = kt - 1;
+      mbar_wait(o_full + 8 * (u & 1), (u >> 1) & 1);
+      tc_fence_after();
       const float inv = direct ? 1.f / l_row : 1.f;
       // O straight from TMEM to global (the K ring is busy with the next item's tiles): this thread's row,
       // 64 columns of half hc = one 128-B bf16 segment (direct) or 256 B of fp32 partials (split)
