@@ -337,6 +337,9 @@ def main():
                          "reference, keys re-based in the attention K-tile load); 2: V by reference, keys "
                          "re-based by a2 into fresh blocks; 3: as 1 with every block of an aligned chunk in the "
                          "chunk's compile frame, re-based by rotating Q per chunk (pic_link_params.kv_share)")
+    ap.add_argument("--ncu-range", action="store_true",
+                    help="wrap the timed steps in cudaProfilerStart/Stop, for an `ncu --profile-from-start off` "
+                         "launch list of exactly the timed region (numbers printed by such a run are not bench values)")
     ap.add_argument("--decode-steps", type=int, default=16,
                     help="f1: decode steps over the first wave's linked caches after the link measurement (0 = skip)")
     args = ap.parse_args()
@@ -432,6 +435,9 @@ def main():
         ev_step = [mk() for _ in range(args.steps + 1)]
         ev_wave = [[mk() for _ in wave_segs] for _ in range(args.steps)]
         with ClockSampler(dev) as clk:
+            if args.ncu_range:
+                torch.cuda.synchronize(dev)
+                torch.cuda.profiler.start()
             ev_step[0].record(stream)
             for i in range(args.steps):
                 for j, segs in enumerate(wave_segs):
@@ -439,6 +445,8 @@ def main():
                     ev_wave[i][j].record(stream)
                 ev_step[i + 1].record(stream)
             ev_step[-1].synchronize()
+            if args.ncu_range:
+                torch.cuda.profiler.stop()
         torch.cuda.synchronize(dev)
         D.barrier()
         ms_rank = ev_step[0].elapsed_time(ev_step[-1])
