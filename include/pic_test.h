@@ -44,6 +44,10 @@ pic_status pic_test_attention_v(const uint16_t* Q, const uint16_t* K, const uint
  * 0 = the engine's choice (default), 1 = one q-tile per CTA, 2 = ping-pong (also for shared-block links).
  * Tests and A/B measurements only. */
 pic_status pic_test_set_attention_kernel(int32_t version);
+/* The attention kernel the last forward launched (host-side record, set at launch or graph capture):
+ * 1 one q-tile per CTA, 2 ping-pong, 3 chunk-frame one CTA per item, 4 chunk-frame persistent, 5 decode,
+ * 6 SIMT (tiny head dims, fp32 debug build). */
+int32_t pic_test_last_attention_kernel(void);
 
 /* a2 KV link on a raw pool: pool K/V [n_layers][num_blocks][Hkv][16][D] bf16 (in/out), rows
  * (src_slot -> dst_slot, delta) for layers layer0..n_layers-1, RoPE table for positions < max_pos. */

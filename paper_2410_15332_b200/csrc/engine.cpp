@@ -263,6 +263,9 @@ static bool wave_fit() {
 // test hook: 0 = the engine's choice, 1 / 2 = force the one-lane / ping-pong attention kernel
 namespace pic {
 int g_attn_force = 0;
+// test hook: the attention kernel the last forward launched (1 one-lane, 2 ping-pong, 3 one-CTA chunk-frame,
+// 4 persistent chunk-frame, 5 decode, 6 SIMT) — set on the host at launch (or graph capture)
+int g_attn_last_kind = 0;
 }
 // a6 on the persistent ping-pong kernel (attention_pp.cu); PIC_ATTN_V1=1: the one-lane kernel (A/B only)
 static bool attn_pp_enabled() {
@@ -1468,8 +1471,13 @@ static pic_status enqueue_forward(pic_engine* e, const Fwd& f, const DevPlan& dp
       a.debug = attn_debug;
       const int max_split = main_tiles ? f.attn_max_split : f.attn_max_split2;
       ++R.launches;
-      // chunk-frame links: the persistent Q-side re-base kernel (PIC_NO_ATTN_PERSIST=1: one CTA per item, A/B)
-      const bool qp = a.qrot && getenv("PIC_NO_ATTN_PERSIST") == nullptr;
+      // chunk-frame links: the persistent Q-side re-base kernel when there are several items per SM (cfg4 wave:
+      // 1792 items, attention 178 -> 163 ms per step); with about one item per SM (cfg2, cfg3: split pieces
+      // sized for 148 CTAs) the one-CTA-per-item kernel measured faster (cfg2 0.60 vs 0.67 ms, cfg3 2.19 vs
+      // 2.31 ms per step).  PIC_NO_ATTN_PERSIST=1 / PIC_ATTN_PERSIST=1 force either kernel (tests, A/B).
+      const bool qp = a.qrot && getenv("PIC_NO_ATTN_PERSIST") == nullptr &&
+                      ((long)a.n_work * a.Hkv >= 2L * 148 || getenv("PIC_ATTN_PERSIST") != nullptr);
+      g_attn_last_kind = (f.attn_decode && main_tiles) ? 5 : qp ? 4 : f.attn_pp ? 2 : a.qrot ? 3 : 1;
       if (f.attn_decode && main_tiles)
         PROF("attention", attn_bytes, attn_flops,
              launch_attention_decode(e->tm_K, e->tm_V, e->tm_K8, e->tm_V8, a, st));
@@ -1487,6 +1495,7 @@ static pic_status enqueue_forward(pic_engine* e, const Fwd& f, const DevPlan& dp
       }
     } else {
       ++R.launches;
+      g_attn_last_kind = 6;
       PROF("attention", attn_bytes, attn_flops, launch_attention_simt(e->Q, Kl, Vl, dp.seq, dp.seq_bt_off, dp.bt, pos, e->Obuf, M, Hq, Hkv, D,
                                (float)(1.0 / std::sqrt((double)D)), st, e->f32, dp.bdelta, e->cos_t, e->sin_t, dp.vbt));
     }

@@ -80,7 +80,10 @@ static int g_attn_version = 2, g_attn_grid = 0;
 
 namespace pic {
 extern int g_attn_force;
+extern int g_attn_last_kind;
 }
+extern "C" int32_t pic_test_last_attention_kernel(void) { return pic::g_attn_last_kind; }
+
 extern "C" pic_status pic_test_set_attention_kernel(int32_t version) {
   if (version < 0 || version > 2) return PIC_E_INVALID_ARG;
   pic::g_attn_force = version;

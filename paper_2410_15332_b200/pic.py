@@ -103,7 +103,7 @@ EXPORTS = ["pic_arena_bytes", "pic_engine_create", "pic_engine_destroy", "pic_ge
            "pic_link_batch", "pic_plan", "pic_linked_export", "pic_linked_info", "pic_linked_sharing", "pic_linked_materialize", "pic_linked_release",
            "pic_cache_export", "pic_cache_info", "pic_expire_cache", "pic_read_weights", "pic_get_stats",
            "pic_last_error", "pic_status_string", "pic_arena_bytes_tp", "pic_engine_create_tp", "pic_tp_ipc_handle",
-           "pic_tp_connect", "pic_generate_context_cache_ex", "pic_decode", "pic_serve_poisson", "pic_serve_arrivals", "pic_set_profiling", "pic_get_profile", "pic_test_gemm", "pic_test_attention", "pic_test_attention_v", "pic_test_set_attention_kernel", "pic_test_kv_link", "pic_bench_gemm", "pic_bench_attention", "pic_test_gemm_swiglu"]
+           "pic_tp_connect", "pic_generate_context_cache_ex", "pic_decode", "pic_serve_poisson", "pic_serve_arrivals", "pic_set_profiling", "pic_get_profile", "pic_test_gemm", "pic_test_attention", "pic_test_attention_v", "pic_test_set_attention_kernel", "pic_test_last_attention_kernel", "pic_test_kv_link", "pic_bench_gemm", "pic_bench_attention", "pic_test_gemm_swiglu"]
 
 _lib = None
 
@@ -161,6 +161,8 @@ def lib() -> C.CDLL:
                                          C.c_int32, C.c_int32, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p]
         L.pic_test_attention_v.argtypes = L.pic_test_attention.argtypes[:11] + [C.c_int32, C.c_int32, C.c_void_p]
         L.pic_test_set_attention_kernel.argtypes = [C.c_int32]
+        L.pic_test_last_attention_kernel.argtypes = []
+        L.pic_test_last_attention_kernel.restype = C.c_int32
         L.pic_test_kv_link.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p,
                                        C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_double, C.c_int32]
         L.pic_bench_gemm.argtypes = [C.c_int32] * 6 + [P(C.c_float)]
@@ -584,6 +586,11 @@ def test_gemm_swiglu(A: np.ndarray, B: np.ndarray, bn: int) -> np.ndarray:
     u = np.empty((M, N2 // 2), dtype=np.uint16)
     check(lib().pic_test_gemm_swiglu(A.ctypes.data, B.ctypes.data, M, N2, K, bn, u.ctypes.data))
     return u
+
+
+def last_attention_kernel() -> int:
+    """Test hook: the attention kernel the last forward launched (see pic_test.h)."""
+    return int(lib().pic_test_last_attention_kernel())
 
 
 def set_attention_kernel(version: int) -> None:

@@ -61,10 +61,12 @@ def test_decode_kernel_matches_oracle_and_prefill_kernel(env):
         K, V = ref.K, ref.V
         try:
             for i, t in enumerate(toks):
-                d_new = eng.decode([outs[0].linked], [t])
+                d_new = eng.decode([outs[0].linked], [t], use_graph=False)
+                assert B.last_attention_kernel() == 5                      # the split-KV decode kernel
                 os.environ["PIC_NO_ATTN_DECODE"] = "1"
                 try:
-                    d_old = eng.decode([outs[1].linked], [t])
+                    d_old = eng.decode([outs[1].linked], [t], use_graph=False)
+                    assert B.last_attention_kernel() in (1, 2)             # a prefill kernel
                 finally:
                     os.environ.pop("PIC_NO_ATTN_DECODE", None)
                 lg, K, V = P.decode(Wt, K, V, t)

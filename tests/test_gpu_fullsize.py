@@ -244,13 +244,13 @@ def test_fullsize_qrot_persistent_bit_identical():
         ids = eng.generate_context_cache(w.chunks)
         reqs = [[("cached", ids[s.chunk]) if s.cached else ("tokens", s.tokens) for s in r] for r in w.requests]
         outs = []
-        for off in (False, True):
-            if off:
-                os.environ["PIC_NO_ATTN_PERSIST"] = "1"
+        for key in ("PIC_ATTN_PERSIST", "PIC_NO_ATTN_PERSIST"):  # 224 items: force either kernel
+            os.environ[key] = "1"
             try:
                 outs.append(eng.link_batch(reqs, w.alg, keep_linked=True, kv_share=3, use_graph=False))
+                assert B.last_attention_kernel() == (4 if key == "PIC_ATTN_PERSIST" else 3)
             finally:
-                os.environ.pop("PIC_NO_ATTN_PERSIST", None)
+                os.environ.pop(key, None)
         for a, b in zip(*outs):
             assert np.array_equal(a.logits, b.logits)
             for l in (0, m.n_layers - 1):

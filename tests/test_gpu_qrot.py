@@ -61,13 +61,14 @@ def test_qrot_link_matches_oracle_and_copy(env, alg, order):
     cfg, eng, ids, oids, store, q = env
     segs = [("cached", ids[c]) for c in order] + [("tokens", q)]
     ref = P.link(store, [("cached", oids[c]) for c in order] + [("tokens", q)], alg)
-    outs = {}
+    outs, kinds = {}, {}
     try:
         for name, share, noq in (("copy", 0, False), ("qrot", 3, False), ("krot", 3, True)):
             if noq:
                 os.environ["PIC_NO_QROT"] = "1"
             try:
-                outs[name] = eng.link(segs, alg, keep_linked=True, kv_share=share)
+                outs[name] = eng.link(segs, alg, keep_linked=True, kv_share=share, use_graph=False)
+                kinds[name] = B.last_attention_kernel()
             finally:
                 os.environ.pop("PIC_NO_QROT", None)
         qr, cp, kr = outs["qrot"], outs["copy"], outs["krot"]
@@ -77,6 +78,7 @@ def test_qrot_link_matches_oracle_and_copy(env, alg, order):
         assert qr.first_token == int(np.argmax(qr.logits))
         # Q-side and K-side re-base round different operands: equal results would mean one kernel ran twice
         assert not np.array_equal(qr.logits, kr.logits)
+        assert kinds["qrot"] in (3, 4) and kinds["krot"] in (1, 2), kinds
         for l in range(cfg.n_layers):
             k, v = eng.linked_export(qr.linked, l)
             assert rel(B.bf16_bits_to_f32(k), ref.K[l]) < 2e-2, l
@@ -98,12 +100,15 @@ def test_qrot_batch_matches_oracle(env):
 
 
 def _eager_links(eng, reqs, persistent):
-    if not persistent:
-        os.environ["PIC_NO_ATTN_PERSIST"] = "1"
+    # small batches run the one-CTA kernel by default (fewer than 2 items per SM): force either kernel
+    key = "PIC_ATTN_PERSIST" if persistent else "PIC_NO_ATTN_PERSIST"
+    os.environ[key] = "1"
     try:
-        return eng.link_batch(reqs, "legolink:16", kv_share=3, use_graph=False, keep_linked=True)
+        out = eng.link_batch(reqs, "legolink:16", kv_share=3, use_graph=False, keep_linked=True)
+        assert B.last_attention_kernel() == (4 if persistent else 3)  # persistent / one-CTA chunk-frame kernel
+        return out
     finally:
-        os.environ.pop("PIC_NO_ATTN_PERSIST", None)
+        os.environ.pop(key, None)
 
 
 def test_qrot_persistent_kernel_bit_identical(env):
