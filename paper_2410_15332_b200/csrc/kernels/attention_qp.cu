@@ -65,6 +65,14 @@ static_assert(kQd + 2 * 2 * kTile == kX, "smem R(-Δ)Q buffers must end where th
 #define PIC_QP_OFFLOAD 1
 #endif
 constexpr bool kOffload = !kQsm && PIC_QP_OFFLOAD;
+// PIC_QP_PSMEM=1: P goes to shared memory (the Q tile's 32 KB, SW128 K-major) and O += P·V is an SS MMA, so
+// the only TMEM A-operand reads left are R(−Δ)Q's; the rotation warps keep the item's q rows in registers
+// (one global load per item) instead of reading a TMA'd Q tile
+#ifndef PIC_QP_PSMEM
+#define PIC_QP_PSMEM 0  // measured at cfg4: attention 188.5 vs 162.4 ms per step (the smem port saturates)
+#endif
+constexpr bool kPsm = PIC_QP_PSMEM != 0 && !kQsm;
+constexpr int kP = kQ;  // kPsm: the P tile [128 rows][128 keys] bf16, two 64-key halves
 constexpr int kThreads = 448;   // warp 0 TMA, warp 1 MMA, warps 2-9 softmax, warps 10-13 frame rotation
 }  // namespace attnq
 
@@ -211,7 +219,7 @@ __global__ void __launch_bounds__(attnq::kThreads, 1)
       if (item < 0) break;
       const QpItem it = qp_item(a, item);
       if (it.n == 0) continue;
-      if (!kQsm && lane == 0) {
+      if (!kQsm && !kPsm && lane == 0) {
         // Q: 128 MMA rows = (128/G queries) x (G heads of kv-head g), one 3-D box per 64-dim half, once the
         // rotation warps are done with the previous item's frames
         mbar_wait(q_empty, (kq & 1) ^ 1);
@@ -244,7 +252,15 @@ __global__ void __launch_bounds__(attnq::kThreads, 1)
       if (first && kdone > 0) mbar_wait(o_free, (kdone - 1) & 1);  // previous item's epilogue has read O
       tc_fence_after();
       const uint64_t dv = dV0 + (uint64_t)(vs * (2 * kTile / 16));
-      umma_ts_k128(tmem + kTmO, tmem + kTmS + pb * 128, dv, idO, first ? 0u : 1u);
+      if constexpr (kPsm) {  // A = P in smem (K-major: keys 16kk.. at half kk/4, +32 B per 16 keys)
+        const uint64_t dP = sdesc_sw128(base + kP, 16, 1024);
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)
+          umma_bf16_e(tmem + kTmO, dP + (uint64_t)(((kk >> 2) * kTile + (kk & 3) * 32) >> 4),
+                      dv + (uint64_t)(kk * 2048 / 16), idO, (first && kk == 0) ? 0u : 1u);
+      } else {
+        umma_ts_k128(tmem + kTmO, tmem + kTmS + pb * 128, dv, idO, first ? 0u : 1u);
+      }
       umma_commit_e(o_full + 8 * pb);
       umma_commit_e(v_empty + 8 * vs);
     };
@@ -363,45 +379,7 @@ __global__ void __launch_bounds__(attnq::kThreads, 1)
     const int r = qq * 32 + lane;
     const uint32_t lane_addr = (uint32_t)(qq * 32) << 16;
     int fi = -1, kq = 0, kt = 0, kd = 0;
-    auto rotate_frame = [&](int fr) {
-      ++fi;
-      const int ad = fr < 0 ? -fr : fr;
-      const float sg = fr < 0 ? 1.f : -1.f;  // R(−Δ): sin(−Δθ) = −sign(Δ)·sin(|Δ|θ)
-      mbar_wait(qd_empty + 8 * (fi & 1), ((fi >> 1) & 1) ^ 1);  // the MMAs of frame fi−2 are done
-      const uint32_t qbase = tmem + lane_addr + kTmQd + (fi & 1) * 64;
-#pragma unroll 1
-      for (int hh = 0; hh < 2; ++hh) {  // dims 32hh..32hh+31 and their partners 64+32hh..
-        uint32_t oa[16], ob[16];
-#pragma unroll
-        for (int cc = 0; cc < 4; ++cc) {
-          const int c = 4 * hh + cc;  // 16-B chunk: dims 8c..8c+7 (half 0) and 64+8c.. (half 1)
-          const uint32_t off = (uint32_t)(r * 128 + ((c ^ (r & 7)) << 4));
-          const uint4 xa = lds128(base + kQ + off), xb = lds128(base + kQ + kTile + off);
-          const float4* cp = reinterpret_cast<const float4*>(a.cos_t + (size_t)ad * 64 + c * 8);
-          const float4* sp = reinterpret_cast<const float4*>(a.sin_t + (size_t)ad * 64 + c * 8);
-          const float4 c0 = __ldg(cp), c1 = __ldg(cp + 1), s0 = __ldg(sp), s1 = __ldg(sp + 1);
-          const float cs[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
-          const float sn[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
-          const uint32_t a4[4] = {xa.x, xa.y, xa.z, xa.w}, b4[4] = {xb.x, xb.y, xb.z, xb.w};
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const float a0 = __uint_as_float(a4[k] << 16), a1 = __uint_as_float(a4[k] & 0xFFFF0000u);
-            const float b0 = __uint_as_float(b4[k] << 16), b1 = __uint_as_float(b4[k] & 0xFFFF0000u);
-            float ra0, rb0, ra1, rb1;
-            rebase_pair(a0, b0, cs[2 * k], sg * sn[2 * k], ra0, rb0);
-            rebase_pair(a1, b1, cs[2 * k + 1], sg * sn[2 * k + 1], ra1, rb1);
-            oa[cc * 4 + k] = pack_bf16(ra0, ra1);
-            ob[cc * 4 + k] = pack_bf16(rb0, rb1);
-          }
-        }
-        // columns: dims (2k, 2k+1) at column k -> dims 32hh.. at 16hh.., partners at 32 + 16hh..
-        tmem_st16u_wait(qbase + 16 * hh, oa);
-        tmem_st16u_wait(qbase + 32 + 16 * hh, ob);
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(qd_full + 8 * (fi & 1));
-    };
+    uint4 qreg[16];  // kPsm: this row's q (chunks 0..7 of half 0, then half 1), loaded once per item
     // O of an unsplit item: its last PV (u_last) has landed and the softmax published the row sums
     auto epilogue = [&](int row_start, int row_count, int g, int u_last, int kdi) {
       mbar_wait(l_full, kdi & 1);
@@ -441,21 +419,74 @@ __global__ void __launch_bounds__(attnq::kThreads, 1)
       const QpItem it = qp_item(a, item);
       if (it.n == 0) continue;
       const int* bdq = a.bdelta + a.seq_bt_off[it.seq];
-      mbar_wait(q_full, kq & 1);  // this item's Q tile
-      ++kq;
+      if constexpr (kPsm) {
+        const int qi = r / G;
+        const uint4* src = reinterpret_cast<const uint4*>(reinterpret_cast<const uint16_t*>(a.Q) +
+                                                          ((size_t)(it.row_start + qi) * a.Hq + it.g * G + r % G) * 128);
+#pragma unroll
+        for (int c = 0; c < 16; ++c) qreg[c] = qi < it.row_count ? __ldg(src + c) : make_uint4(0u, 0u, 0u, 0u);
+      } else {
+        mbar_wait(q_full, kq & 1);  // this item's Q tile
+        ++kq;
+      }
       int fr_cur = 0;
       for (int t = 0; t < it.n; ++t) {
         const int fr = bdq[min((it.j0 + t) * 8, it.last_blk)];
         if (t > 0 && fr == fr_cur) continue;
         fr_cur = fr;
-        rotate_frame(fr);
+        {  // rotate frame fr into the next R(−Δ)Q buffer
+        ++fi;
+        const int ad = fr < 0 ? -fr : fr;
+        const float sg = fr < 0 ? 1.f : -1.f;  // R(−Δ): sin(−Δθ) = −sign(Δ)·sin(|Δ|θ)
+        mbar_wait(qd_empty + 8 * (fi & 1), ((fi >> 1) & 1) ^ 1);  // the MMAs of frame fi−2 are done
+        const uint32_t qbase = tmem + lane_addr + kTmQd + (fi & 1) * 64;
+  #pragma unroll 1
+        for (int hh = 0; hh < 2; ++hh) {  // dims 32hh..32hh+31 and their partners 64+32hh..
+          uint32_t oa[16], ob[16];
+  #pragma unroll
+          for (int cc = 0; cc < 4; ++cc) {
+            const int c = 4 * hh + cc;  // 16-B chunk: dims 8c..8c+7 (half 0) and 64+8c.. (half 1)
+            uint4 xa, xb;
+            if constexpr (kPsm) {
+              xa = qreg[c];
+              xb = qreg[8 + c];
+            } else {
+              const uint32_t off = (uint32_t)(r * 128 + ((c ^ (r & 7)) << 4));
+              xa = lds128(base + kQ + off);
+              xb = lds128(base + kQ + kTile + off);
+            }
+            const float4* cp = reinterpret_cast<const float4*>(a.cos_t + (size_t)ad * 64 + c * 8);
+            const float4* sp = reinterpret_cast<const float4*>(a.sin_t + (size_t)ad * 64 + c * 8);
+            const float4 c0 = __ldg(cp), c1 = __ldg(cp + 1), s0 = __ldg(sp), s1 = __ldg(sp + 1);
+            const float cs[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+            const float sn[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+            const uint32_t a4[4] = {xa.x, xa.y, xa.z, xa.w}, b4[4] = {xb.x, xb.y, xb.z, xb.w};
+  #pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const float a0 = __uint_as_float(a4[k] << 16), a1 = __uint_as_float(a4[k] & 0xFFFF0000u);
+              const float b0 = __uint_as_float(b4[k] << 16), b1 = __uint_as_float(b4[k] & 0xFFFF0000u);
+              float ra0, rb0, ra1, rb1;
+              rebase_pair(a0, b0, cs[2 * k], sg * sn[2 * k], ra0, rb0);
+              rebase_pair(a1, b1, cs[2 * k + 1], sg * sn[2 * k + 1], ra1, rb1);
+              oa[cc * 4 + k] = pack_bf16(ra0, ra1);
+              ob[cc * 4 + k] = pack_bf16(rb0, rb1);
+            }
+          }
+          // columns: dims (2k, 2k+1) at column k -> dims 32hh.. at 16hh.., partners at 32 + 16hh..
+          tmem_st16u_wait(qbase + 16 * hh, oa);
+          tmem_st16u_wait(qbase + 32 + 16 * hh, ob);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(qd_full + 8 * (fi & 1));
+        }
         if (kOffload && prv_last >= 0) {  // after this item's first frame: the previous item's O
           epilogue(prv_rs, prv_rc, prv_g, prv_last, kd - 1);
           prv_last = -1;
         }
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(q_empty);  // every frame of this item rotated: the Q tile may be reloaded
+      if (!kPsm && lane == 0) mbar_arrive(q_empty);  // every frame of this item rotated: the Q tile may be reloaded
       kt += it.n;
       prv_rs = it.row_start;
       prv_rc = it.row_count;
@@ -562,10 +593,21 @@ __global__ void __launch_bounds__(attnq::kThreads, 1)
           pk[c] = pack_bf16(pv.x, pv.y);
         }
         l += (la.x + la.y) + (lb.x + lb.y);
-        tmem_st32u(sAddr, pk);  // P(t) overwrites this half's S(t) columns; PV(t) reads it from TMEM
-        tmem_wait_st();
-        // consume every o_full phase (PV(t-1) of this item has long finished): none completes unobserved
-        if (t >= 1) mbar_wait(o_full + 8 * ((kt - 1) & 1), ((kt - 1) >> 1) & 1);
+        if constexpr (kPsm) {
+          // the single P tile was last read by PV(kt-1) (this item's or the previous item's last): wait for it
+          if (kt >= 1) mbar_wait(o_full + 8 * ((kt - 1) & 1), ((kt - 1) >> 1) & 1);
+          // this thread's 64 keys of row r = one 128-B SW128 row of half hc
+          const uint32_t prow = base + kP + hc * kTile + r * 128;
+#pragma unroll
+          for (int c = 0; c < 8; ++c)
+            sts128(prow + ((c ^ (r & 7)) << 4), make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]));
+          fence_async_smem();  // generic-proxy smem writes -> visible to the PV MMA's operand reads
+        } else {
+          tmem_st32u(sAddr, pk);  // P(t) overwrites this half's S(t) columns; PV(t) reads it from TMEM
+          tmem_wait_st();
+          // consume every o_full phase (PV(t-1) of this item has long finished): none completes unobserved
+          if (t >= 1) mbar_wait(o_full + 8 * ((kt - 1) & 1), ((kt - 1) >> 1) & 1);
+        }
         tc_fence_before();
         mbar_arrive(p_full + 8 * sb);
       }
