@@ -1,5 +1,5 @@
 // attention_qp.cu — a6 for chunk-frame links (kv_share 3 with one frame Δ per 128-key K tile, reading
-// R23): the one-lane Q-side re-base kernel (attention.cu, attn_tc_kernel<G, true, true>) made PERSISTENT.
+// R24): the one-lane Q-side re-base kernel (attention.cu, attn_tc_kernel<G, true, true>) made PERSISTENT.
 //
 // Same Eq. (1) (P:215 A = softmax(Q K_expᵀ · MASK), O = A V_exp; P:213 sparse queries, P:217 causal mask,
 // reading R3) and the same arithmetic as the one-lane QROT kernel, bit for bit: q·R(Δ)k = (R(−Δ)q)·k with

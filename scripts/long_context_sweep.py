@@ -42,7 +42,7 @@ with torch.cuda.stream(stream):
         segs = [("cached", ids[s.chunk]) if s.cached else ("tokens", s.tokens) for s in w.requests[0]]
         N = sum(len(w.chunks[s.chunk]) if s.cached else len(s.tokens) for s in w.requests[0])
         for alg, share in [(a, int(k)) for a in algs for k in args.kv_share.split(",")]:
-            eng.kv_share = bool(share)
+            eng.kv_share = int(share)
             try:
                 pl = eng.plan(segs, alg)
                 kv_row = m.n_layers * m.n_kv_heads * m.head_dim * 2 * 2       # K + V bf16 per token, all layers

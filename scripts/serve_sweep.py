@@ -44,7 +44,7 @@ with torch.cuda.stream(stream):
         ids = [eng.generate_context_cache(c) for c in user_chunks]
         reqs = [[("cached", i) for i in ids[u]] + [("tokens", queries[u])] for u in range(d)]
         for alg, share in [(a, int(k)) for a in args.algs.split(",") for k in args.kv_share.split(",")]:
-            eng.kv_share = bool(share)
+            eng.kv_share = int(share)
             eng.link(reqs[0], alg)                                   # warm-up
             for rate in [float(x) for x in args.rates.split(",")]:
                 st = eng.serve_poisson(reqs, alg, rate, args.duration, seed=int(rate * 1000) ^ 0x5E12E,
