@@ -107,6 +107,8 @@ def test_cfg4_wave_sampled_rows_vs_oracle(kv_share):
         reqs = [[("cached", ids[s.chunk]) if s.cached else ("tokens", s.tokens) for s in r] for r in w.requests]
         g = eng.link_batch(reqs, w.alg, keep_linked=True)                      # bench configuration
         d = eng.link_batch(reqs, w.alg, keep_linked=True, use_graph=False, debug_hidden=True)
+        if kv_share == 3:  # the bench path: the persistent chunk-frame attention kernel (1792 items per layer)
+            assert B.last_attention_kernel() == 4, B.last_attention_kernel()
         for a, b in zip(g, d):
             assert np.array_equal(a.logits, b.logits) and a.first_token == b.first_token
         plans = [eng.plan(r, w.alg) for r in reqs]
