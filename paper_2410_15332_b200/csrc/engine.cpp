@@ -1630,7 +1630,10 @@ static void schedule_attention(pic_engine* e, Fwd& f) {
       }
       n_kv[t] = mx / 128 + 1;
     }
-    const int cap = std::max(1, std::min(32, e->attn_rows_cap / std::max(M, 1)));
+    int cap = std::max(1, std::min(32, e->attn_rows_cap / std::max(M, 1)));
+    // decode kernel: HBM-bound, so with at least one (sequence, kv-head) item per SM the pieces need no split
+    // (cfg4 batch 32: 256 items; 6.22 vs 6.04 TB/s and no combine launch, TPOT -0.2 ms); PIC_DEC_SPLIT=1: A/B
+    if (f.attn_decode && (long)nt * Hkv >= 148 && !getenv("PIC_DEC_SPLIT")) cap = 1;
     long total = 0;
     for (int v : n_kv) total += v;
     work.assign(4 * (size_t)(total + nt), 0);

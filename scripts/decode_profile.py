@@ -15,7 +15,7 @@ steps = int(sys.argv[2]) if len(sys.argv) > 2 else 8
 w = sg.cfg4(n_requests=nr)
 Ns = [sum(len(w.chunks[s.chunk]) if s.cached else len(s.tokens) for s in r) for r in w.requests]
 eng = B.Engine(w.model, num_blocks=(sum(len(c) for c in w.chunks) + 2 * sum(Ns)) // 16 + 64 * nr + 64, max_rows=8192,
-               max_tokens=max(Ns) + 64, max_requests=nr, device=0)
+               max_tokens=max(Ns) + 160, max_requests=nr, device=0)
 ids = eng.generate_context_cache(w.chunks)
 reqs = [[("cached", ids[s.chunk]) if s.cached else ("tokens", s.tokens) for s in r] for r in w.requests]
 hs = [o.linked for o in eng.link_batch(reqs, w.alg, keep_linked=True, want_logits=False, kv_share=3)]
@@ -33,6 +33,12 @@ for _ in range(steps):
 e1.record()
 e1.synchronize()
 print(f"decode TPOT (graph) {e0.elapsed_time(e1) / steps:.3f} ms at batch {nr}, context ~{Ns[0]}")
+if os.environ.get("DECODE_NCU"):  # one eager decode step inside a profiler range (ncu --profile-from-start off)
+    torch.cuda.synchronize()
+    torch.cuda.profiler.start()
+    eng.decode(hs, toks, want_logits=False, logits_dev=dl.data_ptr(), use_graph=False)
+    torch.cuda.synchronize()
+    torch.cuda.profiler.stop()
 eng.set_profiling(True)
 eng.profile(reset=True)
 for _ in range(steps):

@@ -100,3 +100,43 @@ def test_decode_kernel_batched_equals_single(env):
     finally:
         for x in a + b + c:
             eng.release(x.linked)
+
+
+def test_decode_kernel_unsplit_large_batch():
+    """>= 148 (sequence, kv-head) items: the decode kernel runs them unsplit (no combine; the bench's batch-32
+    decode takes this path).  20 sequences x 8 kv-heads of TINY_TP8 against the oracle's decode, and against
+    the split schedule (PIC_DEC_SPLIT=1) within bf16 rounding."""
+    cfg = sg.TINY_TP8
+    ws = sg.workload_seed(0x55)
+    chunks = sg.make_chunks(ws, 6, 128, cfg.vocab, cfg.bos_id)
+    eng = B.Engine(cfg, num_blocks=4096, max_rows=4096, max_tokens=1024, max_requests=20, device=0)
+    try:
+        ids = eng.generate_context_cache(chunks)
+        Wt = M.Weights(cfg)
+        store = P.Store(Wt)
+        oids = store.compile(chunks)
+        orders = [[(i + j) % 6 for j in range(3 + i % 3)] for i in range(20)]
+        qs = [sg.make_query(ws, i, 8 + i, cfg.vocab) for i in range(20)]
+        reqs = [[("cached", ids[c]) for c in o] + [("tokens", q)] for o, q in zip(orders, qs)]
+        hs = [o.linked for o in eng.link_batch(reqs, "legolink:16", keep_linked=True)]
+        hs2 = [o.linked for o in eng.link_batch(reqs, "legolink:16", keep_linked=True)]
+        refs = [P.link(store, [("cached", oids[c]) for c in o] + [("tokens", q)], "legolink:16")
+                for o, q in zip(orders, qs)]
+        KV = [(r.K, r.V) for r in refs]
+        for t in (3, 11):
+            d = eng.decode(hs, [t] * 20, use_graph=False)
+            assert B.last_attention_kernel() == 5
+            os.environ["PIC_DEC_SPLIT"] = "1"
+            try:
+                d2 = eng.decode(hs2, [t] * 20, use_graph=False)
+            finally:
+                os.environ.pop("PIC_DEC_SPLIT", None)
+            for b in range(20):
+                lg, K, V = P.decode(Wt, KV[b][0], KV[b][1], t)
+                KV[b] = (K, V)
+                assert rel(d.logits[b], lg) < 2e-2, (t, b)
+                assert rel(d.logits[b], d2.logits[b]) < 1e-2, (t, b)
+        for h in hs + hs2:
+            eng.release(h)
+    finally:
+        eng.close()
