@@ -2142,12 +2142,32 @@ static pic_status link_impl(pic_engine* e, int32_t n_req, const pic_segment* con
       return fail(PIC_E_CUDA, "selection copy: %s", cudaGetErrorString(ce));
     }
   }
+  bool direct_logits = false;
   if (want_host) {
     bool any_logits = false;
     for (int r = 0; r < n_req; ++r) any_logits |= results[r].logits != nullptr;
     cudaError_t ce = cudaSuccess;
+    // caller buffers in page-locked memory (cudaHostAlloc / cudaHostRegister): copy the logits straight into
+    // them (one copy when they are rows of one array); pageable buffers go through the pinned staging area
+    direct_logits = any_logits;
+    for (int r = 0; r < n_req && direct_logits; ++r) {
+      if (!results[r].logits) continue;
+      cudaPointerAttributes at{};
+      direct_logits = cudaPointerGetAttributes(&at, results[r].logits) == cudaSuccess && at.type == cudaMemoryTypeHost;
+    }
+    cudaGetLastError();  // (older runtimes report a pageable pointer as an error: do not leave it pending)
     if (any_logits) {
-      ce = cudaMemcpyAsync(e->host_logits, e->logits, (size_t)n_req * V * 4, cudaMemcpyDeviceToHost, st);
+      bool rows = direct_logits;
+      for (int r = 0; r < n_req && rows; ++r) rows = results[r].logits == results[0].logits + (size_t)r * V;
+      if (rows) {
+        ce = cudaMemcpyAsync(results[0].logits, e->logits, (size_t)n_req * V * 4, cudaMemcpyDeviceToHost, st);
+      } else if (direct_logits) {
+        for (int r = 0; r < n_req && ce == cudaSuccess; ++r)
+          if (results[r].logits)
+            ce = cudaMemcpyAsync(results[r].logits, e->logits + (size_t)r * V, (size_t)V * 4, cudaMemcpyDeviceToHost, st);
+      } else {
+        ce = cudaMemcpyAsync(e->host_logits, e->logits, (size_t)n_req * V * 4, cudaMemcpyDeviceToHost, st);
+      }
       e->d2h_last += (int64_t)n_req * V * 4;
     }
     if (ce == cudaSuccess) ce = cudaMemcpyAsync(e->host_amax, e->amax, (size_t)n_req * 4, cudaMemcpyDeviceToHost, st);
@@ -2177,7 +2197,7 @@ static pic_status link_impl(pic_engine* e, int32_t n_req, const pic_segment* con
     res.n_selected_layer0 = cb ? reqs[r].p.N : (int)reqs[r].p.sel.size();
     res.n_selected = cb ? (f.cb ? f.M2 : reqs[r].p.N) : (int)reqs[r].p.sel.size();
     res.first_token = want_host ? e->host_amax[r] : -1;
-    if (res.logits) std::memcpy(res.logits, e->host_logits + (size_t)r * V, (size_t)V * 4);
+    if (res.logits && !direct_logits) std::memcpy(res.logits, e->host_logits + (size_t)r * V, (size_t)V * 4);
     if (res.selected) {
       if (f.cb)
         std::copy(cb_sel_host.begin(), cb_sel_host.end(), res.selected);

@@ -397,10 +397,12 @@ class Engine:
 
     def link_batch(self, requests, alg: str, *, use_graph: bool = True, want_logits: bool = True,
                    keep_linked: bool = False, kv_share: Optional[int] = None,
-                   debug_hidden: bool = False) -> List[LinkOutput]:
+                   debug_hidden: bool = False, logits_out: Optional[np.ndarray] = None) -> List[LinkOutput]:
         """Batched link (pic_link_batch).  debug_hidden: every output's .hidden is the forward's
         [L][R][d] residual array (R = max(N_0, Σ k'); request r's rows follow those of requests < r,
-        in selected order, see pic.h)."""
+        in selected order, see pic.h).  logits_out: caller-owned float32 [n][vocab] C-contiguous host array
+        to receive the logits (page-locked memory, e.g. a pinned torch tensor's .numpy(), is filled by one
+        direct device-to-host copy); the outputs' .logits are views of it."""
         n = len(requests)
         segs = [_Segs(r) for r in requests]
         arrp = (C.POINTER(SegmentC) * n)(*[C.cast(s.arr, C.POINTER(SegmentC)) for s in segs])
@@ -414,7 +416,13 @@ class Engine:
         res = (LinkResultC * n)()
         logits = None
         if want_logits:
-            logits = np.empty((n, self.cfg.vocab), dtype=np.float32)
+            if logits_out is not None:
+                if (logits_out.dtype != np.float32 or logits_out.shape != (n, self.cfg.vocab)
+                        or not logits_out.flags["C_CONTIGUOUS"]):
+                    raise ValueError("logits_out must be a C-contiguous float32 [n][vocab] array")
+                logits = logits_out
+            else:
+                logits = np.empty((n, self.cfg.vocab), dtype=np.float32)
             for i in range(n):
                 res[i].logits = logits[i].ctypes.data_as(C.POINTER(C.c_float))
         linked = (C.c_void_p * n)()

@@ -203,3 +203,29 @@ def test_full_width_truncated_depth(which):
         assert rel(out.hidden[l, :len(ref.sel_per_layer[l])], ref.hidden[l]) < TOL
     eng.release(out.linked)
     eng.close()
+
+
+def test_link_batch_logits_into_caller_buffers():
+    """pic_link_batch fills caller-owned logits buffers: a page-locked [n][vocab] array (one direct
+    device-to-host copy), a pageable one, and the default allocation all give the same logits and first tokens."""
+    import torch
+    cfg = sg.TINY_D128
+    w = sg.cfg1(model=cfg)
+    eng = B.Engine(cfg, num_blocks=256, max_rows=512, max_tokens=1024, max_requests=4, device=0)
+    try:
+        ids = eng.generate_context_cache(w.chunks)
+        reqs = [[("cached", ids[s.chunk]) if s.cached else ("tokens", s.tokens) for s in r]
+                for r in [w.requests[0]] + sg.permuted_requests(w, 2)]
+        ref = eng.link_batch(reqs, "legolink:4")
+        pinned = torch.empty((len(reqs), cfg.vocab), dtype=torch.float32, pin_memory=True).numpy()
+        pageable = np.empty((len(reqs), cfg.vocab), dtype=np.float32)
+        for buf in (pinned, pageable):
+            buf[:] = np.nan
+            out = eng.link_batch(reqs, "legolink:4", logits_out=buf)
+            for a, b in zip(ref, out):
+                assert np.array_equal(a.logits, b.logits) and a.first_token == b.first_token
+            assert np.array_equal(buf, np.stack([a.logits for a in ref]))
+        with pytest.raises(ValueError):
+            eng.link_batch(reqs, "legolink:4", logits_out=np.empty((1, cfg.vocab), np.float32))
+    finally:
+        eng.close()
