@@ -131,7 +131,10 @@ typedef struct {
 
 /* Per-request result of a link. */
 typedef struct {
-  float* logits;             /* caller-owned host buffer [vocab] fp32 (nullable); first-token logits */
+  float* logits;             /* caller-owned host buffer [vocab] fp32 (nullable); first-token logits.
+                              * Page-locked buffers (cudaHostAlloc / cudaHostRegister) are filled by direct
+                              * device-to-host copies (one copy when the requests' buffers are consecutive rows
+                              * of one array); pageable ones through the engine's staging buffer. */
   float* logits_dev;         /* caller-owned device buffer [vocab] fp32 (nullable); filled on `stream` */
   int32_t first_token;       /* argmax of the logits (ties -> lowest id, R20); -1 if no host output was requested */
   int32_t n_tokens;          /* N: linked prompt length */
