@@ -411,7 +411,9 @@ def main():
         ids = eng.generate_context_cache(w.chunks, dummy_prefix=dummy_prefix(w.alg))
         wave_segs = [[[("cached", ids[s.chunk]) if s.cached else ("tokens", s.tokens) for s in r] for r in x]
                      for x in waves]
-        logits_dev = torch.empty((1, m.vocab), dtype=torch.float32, device=f"cuda:{dev}")
+        # device-resident results for the device-timed loop: a wave's logits stay in HBM (first tokens too), so
+        # the public call does not synchronise and consecutive waves run back to back on the stream
+        logits_dev = torch.empty((max(len(x) for x in waves), m.vocab), dtype=torch.float32, device=f"cuda:{dev}")
 
         # e2e: the caller's host logits buffer in page-locked memory, allocated once (the public call then copies
         # the logits straight into it instead of through the engine's staging buffer + a host memcpy)
@@ -424,7 +426,8 @@ def main():
                     return [eng.link(segs[0], w.alg, want_logits=True)]
                 return [eng.link(segs[0], w.alg, want_logits=False, logits_dev=logits_dev[0])]
             return eng.link_batch(segs, w.alg, want_logits=want_logits,
-                                  logits_out=host_logits[:len(segs)] if want_logits else None)
+                                  logits_out=host_logits[:len(segs)] if want_logits else None,
+                                  logits_dev=None if want_logits else logits_dev)
 
         kernels_per_step = 0
         for i in range(args.warmup):

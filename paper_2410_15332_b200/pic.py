@@ -397,12 +397,15 @@ class Engine:
 
     def link_batch(self, requests, alg: str, *, use_graph: bool = True, want_logits: bool = True,
                    keep_linked: bool = False, kv_share: Optional[int] = None,
-                   debug_hidden: bool = False, logits_out: Optional[np.ndarray] = None) -> List[LinkOutput]:
+                   debug_hidden: bool = False, logits_out: Optional[np.ndarray] = None,
+                   logits_dev=None) -> List[LinkOutput]:
         """Batched link (pic_link_batch).  debug_hidden: every output's .hidden is the forward's
         [L][R][d] residual array (R = max(N_0, Σ k'); request r's rows follow those of requests < r,
         in selected order, see pic.h).  logits_out: caller-owned float32 [n][vocab] C-contiguous host array
         to receive the logits (page-locked memory, e.g. a pinned torch tensor's .numpy(), is filled by one
-        direct device-to-host copy); the outputs' .logits are views of it."""
+        direct device-to-host copy); the outputs' .logits are views of it.  logits_dev: a device fp32 [n][vocab]
+        tensor (or its address) filled on the stream; with want_logits=False the call then does not synchronise
+        (first tokens stay on the device), so consecutive calls run back to back."""
         n = len(requests)
         segs = [_Segs(r) for r in requests]
         arrp = (C.POINTER(SegmentC) * n)(*[C.cast(s.arr, C.POINTER(SegmentC)) for s in segs])
@@ -425,6 +428,10 @@ class Engine:
                 logits = np.empty((n, self.cfg.vocab), dtype=np.float32)
             for i in range(n):
                 res[i].logits = logits[i].ctypes.data_as(C.POINTER(C.c_float))
+        if logits_dev is not None:
+            base = int(logits_dev.data_ptr()) if hasattr(logits_dev, "data_ptr") else int(logits_dev)
+            for i in range(n):
+                res[i].logits_dev = C.c_void_p(base + 4 * i * self.cfg.vocab)
         linked = (C.c_void_p * n)()
         check(lib().pic_link_batch(self._h, n, arrp, ns, C.byref(p), self._stream, linked if keep_linked else None,
                                    res))
