@@ -26,3 +26,27 @@ def test_reference_arm_json_line():
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1 and d["cpu_baseline"]["sample"]
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
     assert d["value"] > 0 and d["steps"] == 1 and d["warmup"] >= 3
+
+
+import pytest  # noqa: E402
+
+
+@pytest.mark.gpu
+def test_gpu_arm_json_line():
+    """The GPU arm on one 32-request wave: every key of the contract, a live roofline measured from CUDA
+    events, the clocks sample, the engine's own launch count, an e2e with the bytes it copied."""
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--requests", "32", "--steps", "2",
+                        "--warmup", "3", "--decode-steps", "2", "--no-cpu-baseline"],
+                       capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    d = json.loads([l for l in r.stdout.strip().splitlines() if l.startswith("{")][-1])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+              "vs_baseline", "dtype", "data", "config", "clocks", "gpu_launches", "e2e", "roofline", "ttft_ms"):
+        assert k in d, k
+    assert d["n_gpus"] == 1 and d["steps"] == 2 and d["warmup"] == 3 and d["dtype"] == "bf16"
+    assert d["gpu_launches"] > 0 and d["value"] > 0
+    roof = d["roofline"]
+    assert roof["bound"] in ("tensor", "hbm") and 0 < roof["frac"] < 1.2 and roof["achieved"] > 0
+    assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0 and d["e2e"]["value"] > 0
+    assert d["clocks"]["sm_mhz"] > 0 and d["ttft_ms"]["requests"] == 32
+    assert d["decode"]["tpot_ms"] > 0
