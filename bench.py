@@ -500,8 +500,9 @@ def main():
                     else [eng.link(first[0], w.alg, keep_linked=True)])
             hs = [o.linked for o in held]
             mat_ms = None
-            if args.kv_share in (1, 3):
-                # shared-block links: re-base the shared blocks into owned ones once (pic_linked_materialize)
+            if args.kv_share in (1, 2):
+                # shared-block links: re-base the shared blocks into owned ones once (pic_linked_materialize);
+                # chunk-frame links (kv_share 3) are decoded as they are (the decode kernel rotates q per frame)
                 torch.cuda.synchronize(dev)
                 m0, m1 = mk(), mk()
                 m0.record(stream)
@@ -528,7 +529,8 @@ def main():
             dec = {"tpot_ms": tpot, "batch_per_gpu": len(hs), "context_tokens": int(max_N),
                    "steps": args.decode_steps, "gpu_launches_per_step": int(dec_launches), "materialize_ms": mat_ms,
                    "how": "pic_decode over the first wave's linked caches (f1), one token per cache per step, CUDA "
-                          "events on the bench stream (teacher-forced); shared-block links materialized first"}
+                          "events on the bench stream (teacher-forced); shared-block links (kv_share 1/2) materialized "
+                          "first, chunk-frame links (kv_share 3) decoded directly with the per-frame query rotation"}
             for h in hs:
                 eng.release(h)
 

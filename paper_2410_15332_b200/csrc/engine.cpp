@@ -1456,6 +1456,7 @@ static pic_status enqueue_forward(pic_engine* e, const Fwd& f, const DevPlan& dp
       a.bdelta = dp.bdelta;
       a.vbt = dp.vbt;
       a.qrot = f.attn_qrot && tiles == dp.tiles ? 1 : 0;
+      if (f.attn_decode && tiles == dp.tiles) a.qrot = f.kv_rot ? 1 : 0;  // decode over chunk frames
       a.cos_t = e->cos_t;
       a.sin_t = e->sin_t;
       a.Q = e->Q;
@@ -1677,7 +1678,17 @@ static void schedule_attention(pic_engine* e, Fwd& f) {
   // decode (f1): the transposed split-KV kernel, unless keys still need a re-base on load (shared blocks
   // not materialized: the one-lane kernel's K-tile rotation) or PIC_NO_ATTN_DECODE (A/B)
   const bool no_dec = getenv("PIC_NO_ATTN_DECODE") != nullptr;  // read per call (tests toggle it)
-  f.attn_decode = f.decode && !f.kv_rot && !no_dec && e->cfg.head_dim == 128 && !e->f32 &&
+  // a cache that still re-bases keys on load qualifies when every 128-key tile carries one Δ (chunk-frame
+  // links, kv_share 3): the decode kernel then rotates the query by −Δ per frame
+  bool dec_frames = !f.kv_rot;
+  if (f.decode && f.kv_rot) {
+    dec_frames = true;
+    for (size_t q = 0; q < f.seq_bt_off.size() && dec_frames; ++q) {
+      const size_t b0 = f.seq_bt_off[q], b1 = q + 1 < f.seq_bt_off.size() ? f.seq_bt_off[q + 1] : f.bt.size();
+      for (size_t b = b0; b < b1 && dec_frames; ++b) dec_frames = f.bdelta[b] == f.bdelta[b0 + (b - b0) / 8 * 8];
+    }
+  }
+  f.attn_decode = f.decode && dec_frames && !no_dec && e->cfg.head_dim == 128 && !e->f32 &&
                   attention_decode_supported(e->cfg.n_heads / Hkv);
   if (f.attn_decode) pp = false;
   f.attn_pp = pp;

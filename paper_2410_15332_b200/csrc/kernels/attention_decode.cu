@@ -35,8 +35,12 @@ constexpr int kHalf16 = 16 * 128;             // [16 rows][64 elements] bf16 SW1
 constexpr int kQ = kV + kStages * 2 * kTile;  // Q_g: [16 heads][128 dims], two halves
 constexpr int kP = kQ + 2 * kHalf16;          // P: 2 buffers x [16 heads][128 keys], two halves each
 constexpr int kRed = kP + 2 * 2 * kHalf16;    // [2 parity][2 (max, sum)][4 warps][16] fp32
-constexpr int kBar = kRed + 2 * 2 * 4 * 16 * 4;
-constexpr int kNumBars = 4 * kStages + 2 + 2 + 2;  // k/v full/empty, s_full[2], p_full[2], o_full[2]
+// chunk-frame links (a.qrot): a second Q_g buffer and the raw q rows the frame rotation starts from
+constexpr int kQ1 = kRed + 2 * 2 * 4 * 16 * 4;
+constexpr int kQraw = kQ1 + 2 * kHalf16;
+constexpr int kBar = kQraw + 2 * kHalf16;
+// k/v full/empty, s_full[2], p_full[2], o_full[2], qd_full[2], qd_empty[2]
+constexpr int kNumBars = 4 * kStages + 2 + 2 + 2 + 2 + 2;
 constexpr int kSmem = kBar + kNumBars * 8 + 16;
 static_assert(kSmem <= 232448, "decode attention smem over the 227 KB limit");
 constexpr uint32_t kTmS = 0;   // Sᵀ double buffer: columns [0, 16), [16, 32)
@@ -63,6 +67,7 @@ __global__ void __launch_bounds__(attnd::kThreads, 1)
   const uint32_t v_full = smem_u32(bars + 2 * S), v_empty = smem_u32(bars + 3 * S);
   const uint32_t s_full = smem_u32(bars + 4 * S), p_full = smem_u32(bars + 4 * S + 2);
   const uint32_t o_full = smem_u32(bars + 4 * S + 4);
+  const uint32_t qd_full = smem_u32(bars + 4 * S + 6), qd_empty = smem_u32(bars + 4 * S + 8);
   const int warp = warp_id(), lane = lane_id();
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
@@ -75,6 +80,8 @@ __global__ void __launch_bounds__(attnd::kThreads, 1)
       mbar_init(s_full + 8 * b, 1);
       mbar_init(p_full + 8 * b, 128);
       mbar_init(o_full + 8 * b, 1);
+      mbar_init(qd_full + 8 * b, 2);   // a.qrot: warps 2-3 rotate each frame's Q_g
+      mbar_init(qd_empty + 8 * b, 1);  // the frame's last S MMA
     }
     fence_mbar_init();
   }
@@ -97,7 +104,8 @@ __global__ void __launch_bounds__(attnd::kThreads, 1)
     if (h < G)
       v = *reinterpret_cast<const uint4*>(reinterpret_cast<const uint16_t*>(a.Q) +
                                           ((size_t)row * a.Hq + g * G + h) * 128 + ci * 8);
-    sts128(base + kQ + hf * kHalf16 + h * 128 + ((c ^ (h & 7)) << 4), v);
+    // chunk-frame links keep the raw rows: every frame's R(−Δ)·q is built from them
+    sts128(base + (a.qrot ? kQraw : kQ) + hf * kHalf16 + h * 128 + ((c ^ (h & 7)) << 4), v);
     for (int i = u; i < 2 * 2 * kHalf16 / 16; i += kThreads) sts128(base + kP + 16 * i, make_uint4(0u, 0u, 0u, 0u));
     fence_async_smem();  // generic-proxy smem writes -> visible to the tcgen05.mma operand reads
   }
@@ -151,6 +159,9 @@ __global__ void __launch_bounds__(attnd::kThreads, 1)
       constexpr uint32_t idS = idesc_bf16(128, 16, 0, 0);  // K tile (K-major) x Q_g (K-major)
       constexpr uint32_t idO = idesc_bf16(128, 16, 1, 0);  // V tile read MN-major (dims) x P (K-major)
       const uint64_t dK0 = sdesc_sw128(base + kK, 16, 1024), dQ = sdesc_sw128(base + kQ, 16, 1024);
+      const uint64_t dQ1 = sdesc_sw128(base + kQ1, 16, 1024);
+      const int* bdq = a.qrot ? a.bdelta + a.seq_bt_off[seq] : nullptr;
+      int fi = -1, fr_cur = 0, fr_next = bdq ? bdq[min(j0 * 8, last_blk)] : 0;
       const uint64_t dV0 = sdesc_sw128(base + kV, kTile, 1024), dP0 = sdesc_sw128(base + kP, 16, 1024);
       auto issue_pv = [&](int u) {
         const int pb = u & 1, s = u % S;
@@ -167,6 +178,19 @@ __global__ void __launch_bounds__(attnd::kThreads, 1)
       };
       for (int t = 0; t < n; ++t) {
         const int s = t % S, sb = t & 1;
+        uint64_t dq = dQ;
+        bool frame_end = false;
+        if (bdq) {  // chunk-frame link: S = K·(R(−Δ)q)ᵀ with the Q_g buffer of this tile's frame
+          const int fr = fr_next;
+          fr_next = t + 1 < n ? bdq[min((j0 + t + 1) * 8, last_blk)] : fr;
+          if (t == 0 || fr != fr_cur) {
+            ++fi;
+            mbar_wait(qd_full + 8 * (fi & 1), (fi >> 1) & 1);
+          }
+          fr_cur = fr;
+          frame_end = t + 1 == n || fr_next != fr;
+          dq = (fi & 1) ? dQ1 : dQ;
+        }
         mbar_wait(k_full + 8 * s, (t / S) & 1);
         tc_fence_after();
         // Sᵀ(t) overwrites the buffer read by the softmax of t-2, whose P(t-2) the MMA warp waited for below
@@ -174,12 +198,65 @@ __global__ void __launch_bounds__(attnd::kThreads, 1)
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk)  // dims 16kk..16kk+15 of both K-major operands
           umma_bf16_e(tmem + kTmS + 16 * sb, dk + (uint64_t)(((kk >> 2) * kTile + (kk & 3) * 32) >> 4),
-                      dQ + (uint64_t)(((kk >> 2) * kHalf16 + (kk & 3) * 32) >> 4), idS, kk > 0);
+                      dq + (uint64_t)(((kk >> 2) * kHalf16 + (kk & 3) * 32) >> 4), idS, kk > 0);
         umma_commit_e(s_full + 8 * sb);
         umma_commit_e(k_empty + 8 * s);
+        if (frame_end) umma_commit_e(qd_empty + 8 * (fi & 1));  // this frame's Q_g buffer may be rewritten
         if (t >= 1) issue_pv(t - 1);
       }
       issue_pv(n - 1);
+    }
+  } else if (warp < 4) {
+    // ------------------------------------------------------------------ chunk-frame Q_g rotation (warps 2-3)
+    // For every frame Δ along the KV range: R(−Δ)·q of the G head rows (NeoX pairs (j, j+64), fp32 rotation
+    // of the bf16 q rounded to bf16 — the Q-side re-base arithmetic of the prefill kernels) from the raw rows
+    // into the Q_g buffer of the frame's parity; rows G..15 stay zero.  Thread u: (row u>>3, chunk u&7) and
+    // (row 8 + u>>3, chunk u&7).
+    if (a.qrot && n > 0) {
+      const int u = threadIdx.x - 64;
+      const int* bdq = a.bdelta + a.seq_bt_off[seq];
+      int fi = -1, fr_cur = 0;
+      for (int t = 0; t < n; ++t) {
+        const int fr = bdq[min((j0 + t) * 8, last_blk)];
+        if (t > 0 && fr == fr_cur) continue;
+        fr_cur = fr;
+        ++fi;
+        const int ad = fr < 0 ? -fr : fr;
+        const float sg = fr < 0 ? 1.f : -1.f;  // R(−Δ): sin(−Δθ) = −sign(Δ)·sin(|Δ|θ)
+        mbar_wait(qd_empty + 8 * (fi & 1), ((fi >> 1) & 1) ^ 1);  // the S MMAs of frame fi−2 are done
+        const uint32_t qb = base + ((fi & 1) ? kQ1 : kQ);
+#pragma unroll
+        for (int k2 = 0; k2 < 2; ++k2) {
+          const int h = (u >> 3) + 8 * k2, c = u & 7;
+          const uint32_t off = (uint32_t)(h * 128 + ((c ^ (h & 7)) << 4));
+          uint4 xa = lds128(base + kQraw + off), xb = lds128(base + kQraw + kHalf16 + off);
+          if (fr != 0 && h < G) {
+            const float4* cp = reinterpret_cast<const float4*>(a.cos_t + (size_t)ad * 64 + c * 8);
+            const float4* sp = reinterpret_cast<const float4*>(a.sin_t + (size_t)ad * 64 + c * 8);
+            const float4 c0 = __ldg(cp), c1 = __ldg(cp + 1), s0 = __ldg(sp), s1 = __ldg(sp + 1);
+            const float cs[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+            const float sn[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+            uint32_t a4[4] = {xa.x, xa.y, xa.z, xa.w}, b4[4] = {xb.x, xb.y, xb.z, xb.w};
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const float a0 = __uint_as_float(a4[k] << 16), a1 = __uint_as_float(a4[k] & 0xFFFF0000u);
+              const float b0 = __uint_as_float(b4[k] << 16), b1 = __uint_as_float(b4[k] & 0xFFFF0000u);
+              float ra0, rb0, ra1, rb1;
+              rebase_pair(a0, b0, cs[2 * k], sg * sn[2 * k], ra0, rb0);
+              rebase_pair(a1, b1, cs[2 * k + 1], sg * sn[2 * k + 1], ra1, rb1);
+              a4[k] = pack_bf16(ra0, ra1);
+              b4[k] = pack_bf16(rb0, rb1);
+            }
+            xa = make_uint4(a4[0], a4[1], a4[2], a4[3]);
+            xb = make_uint4(b4[0], b4[1], b4[2], b4[3]);
+          }
+          sts128(qb + off, xa);
+          sts128(qb + kHalf16 + off, xb);
+        }
+        fence_async_smem();  // generic-proxy smem writes -> visible to the S MMAs' operand reads
+        __syncwarp();
+        if (lane == 0) mbar_arrive(qd_full + 8 * (fi & 1));
+      }
     }
   } else if (warp >= 4) {
     // ------------------------------------------------------------------ softmax (one thread per key) + epilogue

@@ -140,3 +140,31 @@ def test_decode_kernel_unsplit_large_batch():
             eng.release(h)
     finally:
         eng.close()
+
+
+def test_decode_kernel_over_chunk_frame_links(env):
+    """Decode over kv_share 3 links without materializing them: the cached keys still sit in their chunks'
+    compile frames and the decode kernel rotates the query by −Δ per 128-key frame (the Q-side re-base,
+    reading R24).  Against the oracle's decode and against decode after materialize (re-based copies)."""
+    cfg, eng, ids, oids, Wt, store = env
+    q = sg.make_query(sg.workload_seed(0x52), 2, 24, cfg.vocab)
+    toks = [int(t) for t in sg.tokens(0xDEC0DE, 11, STEPS, cfg.vocab, None)]
+    order = [0, 1, 2, 3, 4]
+    segs = [("cached", ids[c]) for c in order] + [("tokens", q)]
+    ha = eng.link(segs, "legolink:16", keep_linked=True, kv_share=3).linked
+    hb = eng.link(segs, "legolink:16", keep_linked=True, kv_share=3).linked
+    try:
+        assert (eng.linked_sharing(ha)[1] != 0).any()           # frames still pending on the keys
+        eng.materialize(hb)
+        ref = P.link(store, [("cached", oids[c]) for c in order] + [("tokens", q)], "legolink:16")
+        K, V = ref.K, ref.V
+        for t in toks:
+            da = eng.decode([ha], [t], use_graph=False)
+            assert B.last_attention_kernel() == 5                      # the decode kernel, frames and all
+            db = eng.decode([hb], [t], use_graph=False)
+            lg, K, V = P.decode(Wt, K, V, t)
+            assert rel(da.logits[0], lg) < 2e-2
+            assert rel(da.logits[0], db.logits[0]) < 2e-2
+    finally:
+        eng.release(ha)
+        eng.release(hb)
