@@ -19,8 +19,9 @@ eng = B.Engine(w.model, num_blocks=(sum(len(c) for c in w.chunks) + 2 * sum(Ns))
 ids = eng.generate_context_cache(w.chunks)
 reqs = [[("cached", ids[s.chunk]) if s.cached else ("tokens", s.tokens) for s in r] for r in w.requests]
 hs = [o.linked for o in eng.link_batch(reqs, w.alg, keep_linked=True, want_logits=False, kv_share=3)]
-for h in hs:
-    eng.materialize(h)
+if not os.environ.get("DECODE_FRAMES"):  # DECODE_FRAMES=1: decode the chunk-frame links as linked (q rotation)
+    for h in hs:
+        eng.materialize(h)
 toks = [int(t) for t in sg.tokens(0xDEC0DE, 7, nr, w.model.vocab, None)]
 dl = torch.empty((nr, w.model.vocab), dtype=torch.float32, device="cuda:0")
 for _ in range(3):
