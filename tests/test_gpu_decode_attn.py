@@ -102,10 +102,12 @@ def test_decode_kernel_batched_equals_single(env):
             eng.release(x.linked)
 
 
-def test_decode_kernel_unsplit_large_batch():
+@pytest.mark.parametrize("kv_share", [0, 3], ids=["copy", "chunk-frame"])
+def test_decode_kernel_unsplit_large_batch(kv_share):
     """>= 148 (sequence, kv-head) items: the decode kernel runs them unsplit (no combine; the bench's batch-32
     decode takes this path).  20 sequences x 8 kv-heads of TINY_TP8 against the oracle's decode, and against
-    the split schedule (PIC_DEC_SPLIT=1) within bf16 rounding."""
+    the split schedule (PIC_DEC_SPLIT=1) within bf16 rounding.  kv_share 3 is the bench's own case: the
+    batch decodes chunk-frame links directly, each sequence with its own per-frame Δ (reading R24)."""
     cfg = sg.TINY_TP8
     ws = sg.workload_seed(0x55)
     chunks = sg.make_chunks(ws, 6, 128, cfg.vocab, cfg.bos_id)
@@ -118,8 +120,10 @@ def test_decode_kernel_unsplit_large_batch():
         orders = [[(i + j) % 6 for j in range(3 + i % 3)] for i in range(20)]
         qs = [sg.make_query(ws, i, 8 + i, cfg.vocab) for i in range(20)]
         reqs = [[("cached", ids[c]) for c in o] + [("tokens", q)] for o, q in zip(orders, qs)]
-        hs = [o.linked for o in eng.link_batch(reqs, "legolink:16", keep_linked=True)]
-        hs2 = [o.linked for o in eng.link_batch(reqs, "legolink:16", keep_linked=True)]
+        hs = [o.linked for o in eng.link_batch(reqs, "legolink:16", keep_linked=True, kv_share=kv_share)]
+        hs2 = [o.linked for o in eng.link_batch(reqs, "legolink:16", keep_linked=True, kv_share=kv_share)]
+        if kv_share == 3:
+            assert any((eng.linked_sharing(h)[1] != 0).any() for h in hs)    # frames pending on the keys
         refs = [P.link(store, [("cached", oids[c]) for c in o] + [("tokens", q)], "legolink:16")
                 for o, q in zip(orders, qs)]
         KV = [(r.K, r.V) for r in refs]
@@ -168,3 +172,26 @@ def test_decode_kernel_over_chunk_frame_links(env):
     finally:
         eng.release(ha)
         eng.release(hb)
+
+
+def test_decode_over_unaligned_chunk_frames(env):
+    """Chunk-frame links whose chunks do not start on a 128-key tile (the 200-token chunk 6 first): the
+    blocks of a tile may then carry different Δ, which the decode kernel's one-rotation-per-tile schedule
+    cannot take, so the engine falls back to a prefill kernel with per-block rotation (or the decode kernel
+    where every tile is uniform).  Whichever kernel runs, the decode must equal the oracle's."""
+    cfg, eng, ids, oids, Wt, store = env
+    q = sg.make_query(sg.workload_seed(0x52), 3, 9, cfg.vocab)
+    toks = [int(t) for t in sg.tokens(0xDEC0DE, 13, 4, cfg.vocab, None)]
+    for order in ([6, 0, 1, 2], [0, 6, 3]):
+        segs = [("cached", ids[c]) for c in order] + [("tokens", q)]
+        h = eng.link(segs, "legolink:16", keep_linked=True, kv_share=3).linked
+        ref = P.link(store, [("cached", oids[c]) for c in order] + [("tokens", q)], "legolink:16")
+        K, V = ref.K, ref.V
+        try:
+            for t in toks:
+                d = eng.decode([h], [t], use_graph=False)
+                assert B.last_attention_kernel() in (1, 2, 5)
+                lg, K, V = P.decode(Wt, K, V, t)
+                assert rel(d.logits[0], lg) < 2e-2, (order, t)
+        finally:
+            eng.release(h)
